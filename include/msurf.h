@@ -1,0 +1,143 @@
+/* msurf.h — C ABI of libmsurf.so, the B200 (sm_100a) FSM surface-topography
+ * hot path. Plain POD structs, plain pointers and sizes, explicit CUDA stream
+ * (passed as void*), int status + thread-local msurf_last_error().
+ *
+ * The reference (arXiv 2603.28160, package `millsurf`) is pure Python/NumPy
+ * and has no FFI of its own; each entry point below replaces the reference
+ * function it cites (file:line under /root/reference/pkg/src/millsurf/), and
+ * the Python host package paper_2603_28160_b200 binds them with ctypes
+ * (INTEGRATION.md shows the binding a maintainer would add to millsurf).
+ *
+ * Device buffers are caller-owned (the Python host allocates them with
+ * PyTorch); no entry point allocates on the hot path.
+ */
+#ifndef MSURF_H
+#define MSURF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MSURF_ABI_VERSION 1
+
+/* kinematics mode of a sweep launch (uniform across the jobs of one launch) */
+#define MSURF_MODE_REF 0      /* reference composite-matrix order, engine.py:257-296 */
+#define MSURF_MODE_EXT 1      /* rotated tool-frame points, z' time-invariant   */
+#define MSURF_MODE_EXT_TILT 2 /* rotated tool-frame points + lead tilt (z' per step) */
+
+#define MSURF_CTR_LIVE_ROWS 0  /* (step, tooth, pass) rows surviving the 2-D cull */
+#define MSURF_CTR_EVAL 1       /* edge points evaluated (P_eng, chunk granularity) */
+#define MSURF_CTR_DEPOSITS 2   /* points landing in the owned grid (P_in)          */
+#define MSURF_CTR_ATOMICS 3    /* atomicMin issued after run-length/stale-read skip */
+#define MSURF_NUM_CTRS 4
+
+/* One surface sweep (one parameter set; one strip of it under sharding).
+ * Replaces the per-worker body engine.py:215-313 (_run_step_range) for all
+ * steps x teeth x edge points x raster passes of one surface.
+ * Layout: 8-byte fields first, then 4-byte fields, no implicit padding. */
+typedef struct msurf_job {
+  /* grid (surface_grid.py:25-75): node (i,j) at (x_min+i*spacing, y_min+j*spacing) */
+  double spacing, x_min, y_min;
+  int64_t m, n;      /* cell counts; nodes (m+1) x (n+1)                       */
+  int64_t j_lo, j_hi; /* owned feed-direction node columns [j_lo, j_hi]          */
+  uint64_t* keys;    /* device (m+1) x (j_hi-j_lo+1), order-preserving u64 keys  */
+  /* time (engine.py:152-170, 240-241) */
+  double t_start, dt;
+  int64_t steps;
+  double y0, feed_speed, omega;
+  /* per-tooth / per-point device arrays */
+  const double* tooth_base;  /* [teeth] phase + (2pi)(K-1)/Z (kinematics.py:76)      */
+  const double* tooth_rows;  /* REF: [teeth][8] e00 e01 e02 e03 e10 e11 e12 e13      */
+  const double* px;          /* REF: edge x [points]; EXT: tool-frame x [teeth][points] */
+  const double* py;
+  const double* pz;
+  const uint64_t* zkey;      /* [teeth][points] keys of z' (REF, EXT without tilt)    */
+  const double* chunk_box;   /* [teeth][nchunk][6] tool-frame xlo xhi ylo yhi zlo zhi */
+  const double* pass_x0;     /* [passes] spindle x of each raster pass               */
+  /* extended kinematics */
+  double tilt_c, tilt_s, zoff;
+  double vib_amp, vib_omega, vib_phase;
+  /* optional host-libm trig tables (parity mode); NULL = device sincos */
+  const double* trig_table;  /* [steps][teeth][2] = cos, sin of the tooth angle      */
+  const double* vib_table;   /* [steps] sin(vib_omega*t + vib_phase)                  */
+  /* optional trajectory record (REF mode, pass 0): per (step, tooth) the
+   * workpiece x', y', z' of edge point min_index[tooth] (engine.py:266-270) */
+  double* traj;              /* device [steps][teeth][3] or NULL                      */
+  const int32_t* min_index;  /* [teeth] argmin of z' (engine.py:189)                  */
+  unsigned long long* counters; /* device [MSURF_NUM_CTRS], accumulated             */
+  int32_t teeth, points, passes, reserved0;
+} msurf_job;
+
+int msurf_abi_version(void);
+const char* msurf_last_error(void);
+int msurf_sizeof_job(void);
+
+/* Initialise n_surf contiguous surfaces of `count` keys each with the key of
+ * value[s] (device array): HeightField init to the stock height, surface_grid.py:107-108. */
+int msurf_fill_keys(uint64_t* keys, int64_t count, int32_t n_surf, const double* value,
+                    void* stream);
+
+/* The FSM sweep (engine.py:215-313 / 316-357). `jobs` is a DEVICE array of
+ * n_jobs descriptors; `tile_prefix` a DEVICE array of n_jobs+1 exclusive
+ * prefix sums of tiles per job, tiles(job) = passes*teeth*ceil(steps/tile_steps).
+ * tile_steps must be msurf_tile_steps(). Deposits are atomicMin on keys, so
+ * the result is independent of scheduling (engine.py:316-317 determinism). */
+int msurf_tile_steps(void);
+int msurf_sweep(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile_prefix,
+                int64_t n_tiles, int32_t mode, int32_t max_points, void* stream);
+
+/* Decode keys to fp64 heights in place and count machined cells
+ * (HeightField.machined_cell_count, surface_grid.py:128-129). Batched over
+ * n_surf surfaces of `count` nodes each, contiguous; sentinel[n_surf] (the
+ * initial stock height of each surface) and machined[n_surf] are device
+ * arrays, machined is accumulated. */
+int msurf_decode(uint64_t* keys, int64_t count, int32_t n_surf, const double* sentinel,
+                 unsigned long long* machined, void* stream);
+
+/* Areal roughness moments (roughness.py:93-135, leveling='mean').
+ * h: device fp64 heights, row-major with leading dimension ld; surface s
+ * starts at h + s*surf_stride. ROI rows [i_lo, i_lo+rows), cols [j_lo, j_lo+cols).
+ * sentinel[n_surf] device. exclude_uncut=0 counts uncut cells (the host raises
+ * DomainError like roughness.py:86-89); =1 skips them. Reductions are
+ * deterministic (fixed block partition, fixed-order tree): reruns are
+ * bit-identical. work: device scratch of n_surf * MSURF_RED_BLOCKS * 5 doubles.
+ * pass1 -> stats1[s][5] = sum z_um, max z_um, min z_um, n_used, n_uncut
+ * pass2 reads mean = stats1[s][0] / stats1[s][3] (under strip sharding the
+ * caller all-reduces stats1 first, so the mean is global)
+ *       -> out2[s][4] = sum|d|, sum d^2, sum d^3, sum d^4 */
+#define MSURF_RED_BLOCKS 256
+int msurf_areal_pass1(const double* h, int64_t ld, int64_t surf_stride, int32_t n_surf,
+                      int64_t i_lo, int64_t j_lo, int64_t rows, int64_t cols,
+                      const double* sentinel, int32_t exclude_uncut, double* work,
+                      double* stats1, void* stream);
+int msurf_areal_pass2(const double* h, int64_t ld, int64_t surf_stride, int32_t n_surf,
+                      int64_t i_lo, int64_t j_lo, int64_t rows, int64_t cols,
+                      const double* sentinel, int32_t exclude_uncut, const double* stats1,
+                      double* work, double* out2, void* stream);
+
+/* Profile roughness (roughness.py:138-188; Rz = Rp + Rv is the product's
+ * extension). Profile p of surface s: `len` samples starting at
+ * h + s*surf_stride + start[p], spaced `stride` (1 = feed profile, ld =
+ * pick-feed); sentinel[n_surf] device. If stats_in is NULL each block uses
+ * its own mean (single GPU); otherwise mean = stats_in[k][0]/stats_in[k][1]
+ * of the caller's all-reduced first pass (strip-sharded profiles).
+ * out[k = s*n_prof+p][8] = sum z_um, n_used, n_uncut, max z_um, min z_um,
+ * sum|z - mean|, 0, 0 */
+int msurf_profiles(const double* h, int64_t surf_stride, int32_t n_surf,
+                   const int64_t* start, int32_t n_prof, int64_t len, int64_t stride,
+                   const double* sentinel, int32_t exclude_uncut, const double* stats_in,
+                   double* out, void* stream);
+
+/* Microbenchmarks for the roofline denominators (not in MEASURED_PEAKS.json):
+ * which=0: non-FMA DADD/DMUL issue (ops/s), which=1: DFMA (FMA/s),
+ * which=2: 64-bit atomicMin (RED.MIN.64) to random L2-resident addresses
+ * (ops/s). Synchronous; creates and destroys its own scratch. */
+int msurf_microbench(int32_t which, double* result);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MSURF_H */

@@ -1,0 +1,174 @@
+"""ctypes binding of libmsurf.so (include/msurf.h) and device plumbing.
+
+PyTorch is used only for device memory, pinned staging buffers and the
+current CUDA stream. Every compute step runs in libmsurf.so; if the library
+or a CUDA device is missing the product raises NativeUnavailableError —
+there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .errors import MillsurfError, NativeUnavailableError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmsurf.so")
+ABI_VERSION = 1
+NUM_CTRS = 4
+RED_BLOCKS = 256
+
+c_double, c_int64, c_int32, c_void_p = ctypes.c_double, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
+
+
+class MsurfJob(ctypes.Structure):
+    """Mirror of msurf_job (include/msurf.h)."""
+
+    _fields_ = [
+        ("spacing", c_double), ("x_min", c_double), ("y_min", c_double),
+        ("m", c_int64), ("n", c_int64), ("j_lo", c_int64), ("j_hi", c_int64),
+        ("keys", c_void_p),
+        ("t_start", c_double), ("dt", c_double), ("steps", c_int64),
+        ("y0", c_double), ("feed_speed", c_double), ("omega", c_double),
+        ("tooth_base", c_void_p), ("tooth_rows", c_void_p),
+        ("px", c_void_p), ("py", c_void_p), ("pz", c_void_p),
+        ("zkey", c_void_p), ("chunk_box", c_void_p), ("pass_x0", c_void_p),
+        ("tilt_c", c_double), ("tilt_s", c_double), ("zoff", c_double),
+        ("vib_amp", c_double), ("vib_omega", c_double), ("vib_phase", c_double),
+        ("trig_table", c_void_p), ("vib_table", c_void_p),
+        ("traj", c_void_p), ("min_index", c_void_p), ("counters", c_void_p),
+        ("teeth", c_int32), ("points", c_int32), ("passes", c_int32), ("reserved0", c_int32),
+    ]
+
+
+EXPORTS = {
+    "msurf_abi_version": (ctypes.c_int, []),
+    "msurf_last_error": (ctypes.c_char_p, []),
+    "msurf_sizeof_job": (ctypes.c_int, []),
+    "msurf_tile_steps": (ctypes.c_int, []),
+    "msurf_fill_keys": (ctypes.c_int, [c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
+    "msurf_sweep": (ctypes.c_int, [c_void_p, c_int32, c_void_p, c_int64, c_int32, c_int32, c_void_p]),
+    "msurf_decode": (ctypes.c_int, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p]),
+    "msurf_areal_pass1": (ctypes.c_int, [c_void_p, c_int64, c_int64, c_int32, c_int64, c_int64,
+                                         c_int64, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
+                                         c_void_p]),
+    "msurf_areal_pass2": (ctypes.c_int, [c_void_p, c_int64, c_int64, c_int32, c_int64, c_int64,
+                                         c_int64, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
+                                         c_void_p, c_void_p]),
+    "msurf_profiles": (ctypes.c_int, [c_void_p, c_int64, c_int32, c_void_p, c_int32, c_int64,
+                                      c_int64, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
+    "msurf_microbench": (ctypes.c_int, [c_int32, ctypes.POINTER(c_double)]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libmsurf.so and declare every exported symbol (no GPU needed)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailableError(
+                f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in EXPORTS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.msurf_abi_version() != ABI_VERSION:
+            raise NativeUnavailableError("libmsurf.so ABI version mismatch; rebuild")
+        if lib.msurf_sizeof_job() != ctypes.sizeof(MsurfJob):
+            raise NativeUnavailableError("msurf_job layout mismatch between header and binding")
+        _lib = lib
+        return lib
+
+
+def lib():
+    return _lib if _lib is not None else load_library()
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        raise MillsurfError("libmsurf: " + lib().msurf_last_error().decode())
+
+
+def require_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeUnavailableError("no CUDA device: the FSM sweep runs only on the GPU")
+    lib()
+    return torch
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+class Arena:
+    """Packs many small host arrays into one pinned staging buffer and one
+    device buffer, so a sweep's inputs cross PCIe in a single H2D copy."""
+
+    _pinned = {}
+
+    def __init__(self):
+        self._parts = []
+        self.size = 0
+
+    def add(self, arr) -> int:
+        a = np.ascontiguousarray(arr)
+        off = (self.size + 255) & ~255
+        self._parts.append((off, a))
+        self.size = off + a.nbytes
+        return off
+
+    def reserve(self, nbytes: int) -> int:
+        off = (self.size + 255) & ~255
+        self._parts.append((off, None))
+        self.size = off + nbytes
+        return off
+
+    @classmethod
+    def _staging(cls, nbytes: int, device):
+        import torch
+
+        key = device.index if device.index is not None else 0
+        ent = cls._pinned.get(key)
+        if ent is None or ent[0].numel() < nbytes:
+            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
+            ent = (buf, torch.cuda.Event())
+            ent[1].record()
+            cls._pinned[key] = ent
+        return ent
+
+    def upload(self, device, fill_structs=None):
+        """Allocate the device buffer, let ``fill_structs(base_ptr)`` return
+        [(offset, bytes)] (descriptors holding device pointers), then copy
+        everything with one cudaMemcpyAsync on the current stream."""
+        import torch
+
+        dev = torch.empty(max(self.size, 1), dtype=torch.uint8, device=device)
+        base = dev.data_ptr()
+        extra = fill_structs(base) if fill_structs else []
+        stage, done = self._staging(self.size, dev.device)
+        # the pinned buffer is reused across calls: wait for its previous copy only
+        done.synchronize()
+        host = stage.numpy()
+        for off, a in self._parts:
+            if a is not None:
+                host[off:off + a.nbytes] = a.view(np.uint8).reshape(-1)
+        for off, b in extra:
+            host[off:off + len(b)] = np.frombuffer(b, dtype=np.uint8)
+        dev.copy_(stage[: max(self.size, 1)], non_blocking=True)
+        done.record()
+        return dev

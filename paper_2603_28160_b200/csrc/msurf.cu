@@ -1,0 +1,735 @@
+// libmsurf.so — B200 (sm_100a) kernels for the FSM surface-topography hot path
+// of arXiv 2603.28160 (reference package `millsurf`), behind the C ABI in
+// include/msurf.h.
+//
+//  * sweep_kernel<MODE>: engine.py:215-313 for all (pass, tooth, step, edge
+//    point) of one or many surfaces. One CTA = one (surface, pass, tooth, tile
+//    of 256 time steps). Phase 1: one thread per step hoists the fp64 trig
+//    and the composite coefficients and builds a per-(step, 32-point chunk)
+//    2-D bounding-box cull mask (generalises the x-only row cull of
+//    engine.py:272-287), then compacts the live steps in order. Phase 2: one
+//    warp per 32-point chunk, one lane per edge point, walks the live steps in
+//    time order: affine transform in the reference's exact op order, cell
+//    location with the reference's exact IEEE division on near-boundary
+//    points, and a run-length min pre-reduction in registers (consecutive
+//    steps of one point mostly land in the same cell), flushed to HBM as an
+//    atomicMin on order-preserving u64 keys after a stale-read skip.
+//  * decode / areal pass1+pass2 / profiles: deterministic fixed-partition
+//    warp-shuffle + block reductions (roughness.py:76-188).
+//  * microbenchmarks for the FP64 and atomic roofline denominators.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+
+#include "msurf.h"
+#include "msurf_trig.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kTileSteps = 256;  // rows (time steps) per CTA; == kThreads
+constexpr int kWarps = kThreads / 32;
+constexpr double kNearEps = 0x1p-30;  // fast-path locate guard (see cell_fast)
+
+thread_local std::string g_err;
+
+int set_err(const std::string& s) {
+  g_err = s;
+  return 1;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(std::string(what) + ": " + cudaGetErrorString(e));
+  return 0;
+}
+
+// ----------------------------------------------------------- key encoding
+// Order-preserving map fp64 -> u64 (unsigned compare == IEEE compare for
+// non-NaN; -0 is canonicalised to +0 first, IEEE treats them equal).
+__device__ __forceinline__ uint64_t enc_key(double z) {
+  z = __dadd_rn(z, 0.0);
+  const uint64_t b = (uint64_t)__double_as_longlong(z);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dec_key(uint64_t k) {
+  const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+// ---------------------------------------------------------- cell location
+// Reference: idx = floor((w - lo)/dd + 0.5) (engine.py:298-300,
+// surface_grid.py:85-86), true IEEE division. Fast path: tq ~= w*inv + c0
+// with c0 = 0.5 - lo*inv (one FMA; |error| < 1e-11 for |tq| < 2^21). If tq is
+// within 2^-30 of an integer the floor could differ, so those (rare) points
+// take the exact reference sequence. Result: bit-identical cell indices.
+__device__ __forceinline__ int cell_index(double w, double lo, double dd, double inv,
+                                          double c0) {
+  double tq = __fma_rn(w, inv, c0);
+  double fl = floor(tq);
+  const double d = __dsub_rn(tq, fl);
+  if (fabs(__dsub_rn(d, 0.5)) > 0.5 - kNearEps) {
+    tq = __dadd_rn(__ddiv_rn(__dsub_rn(w, lo), dd), 0.5);
+    fl = floor(tq);
+  }
+  // |fl| beyond int range saturates, which the unsigned range checks reject.
+  return __double2int_rz(fl);
+}
+
+__device__ __forceinline__ void flush_min(uint64_t* __restrict__ keys, long long idx,
+                                          uint64_t key, unsigned& n_atom) {
+  if (idx < 0) return;
+  // Stale-read skip: heights only decrease, so a cached (possibly stale,
+  // i.e. higher) value <= key proves the atomic would be a no-op.
+  const uint64_t cur = __ldca(reinterpret_cast<const unsigned long long*>(keys + idx));
+  if (cur > key) {
+    atomicMin(reinterpret_cast<unsigned long long*>(keys + idx), (unsigned long long)key);
+    ++n_atom;
+  }
+}
+
+__device__ __forceinline__ unsigned warp_sum_u(unsigned v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 2)
+    sweep_kernel(const msurf_job* __restrict__ jobs, int n_jobs,
+                 const int64_t* __restrict__ prefix, int mask_words) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* rowv = reinterpret_cast<double*>(smem_raw);                        // [T][8]
+  uint64_t* masks = reinterpret_cast<uint64_t*>(rowv + kTileSteps * 8);      // [T][W]
+  int* live = reinterpret_cast<int*>(masks + kTileSteps * mask_words);       // [T]
+  __shared__ msurf_job J;
+  __shared__ int warp_cnt[kWarps];
+  __shared__ int s_job;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const long long tile = blockIdx.x;
+
+  if (tid == 0) {
+    int lo = 0, hi = n_jobs - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (prefix[mid] <= tile) lo = mid; else hi = mid - 1;
+    }
+    s_job = lo;
+  }
+  __syncthreads();
+  {
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(jobs + s_job);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&J);
+    for (int w = tid; w < (int)(sizeof(msurf_job) / 8); w += kThreads) dst[w] = src[w];
+  }
+  __syncthreads();
+
+  const long long local = tile - prefix[s_job];
+  const long long nst = (J.steps + kTileSteps - 1) / kTileSteps;
+  const int st = (int)(local % nst);
+  const long long rem = local / nst;
+  const int tooth = (int)(rem % J.teeth);
+  const int pass = (int)(rem / J.teeth);
+  const int npts = J.points;
+  const int nchunk = (npts + 31) >> 5;
+  const double dd = J.spacing;
+
+  // ---------------- phase 1: one thread per time step of the tile
+  const double wx_lo = J.x_min - 1.5 * dd;
+  const double wx_hi = J.x_min + (double)J.m * dd + 1.5 * dd;
+  const double wy_lo = J.y_min + (double)J.j_lo * dd - 1.5 * dd;
+  const double wy_hi = J.y_min + (double)J.j_hi * dd + 1.5 * dd;
+  bool any = false;
+  {
+    const long long s = (long long)st * kTileSteps + tid;
+    uint64_t* my_mask = masks + tid * mask_words;
+    for (int w = 0; w < mask_words; ++w) my_mask[w] = 0ull;
+    if (s < J.steps) {
+      // engine.py:240-241, kinematics.py:77 — one rounding per op, no FMA
+      const double t = __dadd_rn(J.t_start, __dmul_rn((double)s, J.dt));
+      const double ty = __dadd_rn(J.y0, __dmul_rn(J.feed_speed, t));
+      double c, sn;
+      if (J.trig_table) {
+        c = J.trig_table[(s * J.teeth + tooth) * 2 + 0];
+        sn = J.trig_table[(s * J.teeth + tooth) * 2 + 1];
+      } else {
+        const double th = __dsub_rn(J.tooth_base[tooth], __dmul_rn(J.omega, t));
+        msurf_sincos(th, &sn, &c);
+      }
+      const double ns = -sn;
+      double xoff = J.pass_x0[pass];
+      if (MODE != MSURF_MODE_REF && J.vib_amp != 0.0) {
+        const double sv = J.vib_table ? J.vib_table[s]
+                                      : msurf_sin(__dadd_rn(__dmul_rn(J.vib_omega, t), J.vib_phase));
+        xoff = __dadd_rn(xoff, __dmul_rn(J.vib_amp, sv));
+      }
+      double* rv = rowv + tid * 8;
+      if (MODE == MSURF_MODE_REF) {
+        // engine.py:257-264 composite coefficients, exact op order
+        const double* e = J.tooth_rows + tooth * 8;
+        rv[0] = __dadd_rn(__dmul_rn(c, e[0]), __dmul_rn(sn, e[4]));
+        rv[1] = __dadd_rn(__dmul_rn(c, e[1]), __dmul_rn(sn, e[5]));
+        rv[2] = __dadd_rn(__dmul_rn(c, e[2]), __dmul_rn(sn, e[6]));
+        rv[3] = __dadd_rn(__dadd_rn(__dmul_rn(c, e[3]), __dmul_rn(sn, e[7])), xoff);
+        rv[4] = __dadd_rn(__dmul_rn(ns, e[0]), __dmul_rn(c, e[4]));
+        rv[5] = __dadd_rn(__dmul_rn(ns, e[1]), __dmul_rn(c, e[5]));
+        rv[6] = __dadd_rn(__dmul_rn(ns, e[2]), __dmul_rn(c, e[6]));
+        rv[7] = __dadd_rn(__dadd_rn(__dmul_rn(ns, e[3]), __dmul_rn(c, e[7])), ty);
+        if (J.traj && pass == 0) {
+          // engine.py:266-270: min-z edge point of this (step, tooth)
+          const int p = J.min_index[tooth];
+          const double xp = J.px[p], yp = J.py[p], zp = J.pz[p];
+          double* tr = J.traj + (s * J.teeth + tooth) * 3;
+          tr[0] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(rv[0], xp), __dmul_rn(rv[1], yp)),
+                                      __dmul_rn(rv[2], zp)), rv[3]);
+          tr[1] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(rv[4], xp), __dmul_rn(rv[5], yp)),
+                                      __dmul_rn(rv[6], zp)), rv[7]);
+          tr[2] = dec_key(J.zkey[(long long)tooth * J.points + p]);
+        }
+      } else {
+        rv[0] = c;
+        rv[1] = sn;
+        rv[2] = xoff;
+        rv[3] = ty;
+      }
+      // 2-D chunk cull; conservative by 1.5 cells >> rounding differences
+      const double* box = J.chunk_box + (long long)tooth * nchunk * 6;
+      for (int q = 0; q < nchunk; ++q) {
+        const double xl = box[q * 6 + 0], xh = box[q * 6 + 1];
+        const double yl = box[q * 6 + 2], yh = box[q * 6 + 3];
+        const double x_lo = fmin(c * xl, c * xh) + fmin(sn * yl, sn * yh) + xoff;
+        const double x_hi = fmax(c * xl, c * xh) + fmax(sn * yl, sn * yh) + xoff;
+        double v_lo = fmin(ns * xl, ns * xh) + fmin(c * yl, c * yh);
+        double v_hi = fmax(ns * xl, ns * xh) + fmax(c * yl, c * yh);
+        if (MODE == MSURF_MODE_EXT_TILT) {
+          const double zl = box[q * 6 + 4], zh = box[q * 6 + 5];
+          const double a1 = J.tilt_c * v_lo, a2 = J.tilt_c * v_hi;
+          const double b1 = J.tilt_s * zl, b2 = J.tilt_s * zh;
+          v_lo = fmin(a1, a2) - fmax(b1, b2);
+          v_hi = fmax(a1, a2) - fmin(b1, b2);
+        }
+        const bool keep = (x_hi >= wx_lo) & (x_lo <= wx_hi) & (v_hi + ty >= wy_lo) &
+                          (v_lo + ty <= wy_hi);
+        if (keep) {
+          my_mask[q >> 6] |= 1ull << (q & 63);
+          any = true;
+        }
+      }
+    }
+  }
+  // ordered compaction of live steps
+  const unsigned bal = __ballot_sync(0xffffffffu, any);
+  if (lane == 0) warp_cnt[warp] = __popc(bal);
+  __syncthreads();
+  int base = 0, n_live = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    if (w < warp) base += warp_cnt[w];
+    n_live += warp_cnt[w];
+  }
+  if (any) live[base + __popc(bal & ((1u << lane) - 1u))] = tid;
+  __syncthreads();
+  if (n_live == 0) return;
+
+  // ---------------- phase 2: warp = 32-point chunk, lane = edge point
+  const double inv = 1.0 / dd;
+  const double cx0 = 0.5 - J.x_min * inv;
+  const double cy0 = 0.5 - J.y_min * inv;
+  const unsigned span_i = (unsigned)J.m;
+  const int j_lo = (int)J.j_lo;
+  const unsigned span_j = (unsigned)(J.j_hi - J.j_lo);
+  const long long ldk = J.j_hi - J.j_lo + 1;
+  uint64_t* __restrict__ keys = J.keys;
+  const int rsplit = kWarps / nchunk > 1 ? kWarps / nchunk : 1;
+  const int units = nchunk * rsplit;
+  unsigned n_eval = 0, n_dep = 0, n_atom = 0;
+
+  for (int u = warp; u < units; u += kWarps) {
+    const int q = u % nchunk;
+    const int part = u / nchunk;
+    const int r0 = (int)((long long)part * n_live / rsplit);
+    const int r1 = (int)((long long)(part + 1) * n_live / rsplit);
+    const int p = q * 32 + lane;
+    const bool valid = p < npts;
+    const int word = q >> 6;
+    const uint64_t bit = 1ull << (q & 63);
+    double ax = 0.0, ay = 0.0, az = 0.0;
+    uint64_t zk = ~0ull;
+    if (valid) {
+      if (MODE == MSURF_MODE_REF) {
+        ax = J.px[p];
+        ay = J.py[p];
+        az = J.pz[p];
+      } else {
+        const long long o = (long long)tooth * npts + p;
+        ax = J.px[o];
+        ay = J.py[o];
+        az = J.pz[o];
+      }
+      if (MODE != MSURF_MODE_EXT_TILT) zk = J.zkey[(long long)tooth * npts + p];
+    }
+    long long last = -1;
+    uint64_t run = ~0ull;
+    for (int li = r0; li < r1; ++li) {
+      const int r = live[li];
+      if (!(masks[r * mask_words + word] & bit)) continue;
+      const double* rv = rowv + r * 8;
+      double xw, yw;
+      uint64_t key = zk;
+      if (MODE == MSURF_MODE_REF) {
+        // engine.py:289-296: xw = ((m00*xp + m01*yp) + m02*zp) + m03
+        xw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(rv[0], ax), __dmul_rn(rv[1], ay)),
+                                 __dmul_rn(rv[2], az)), rv[3]);
+        yw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(rv[4], ax), __dmul_rn(rv[5], ay)),
+                                 __dmul_rn(rv[6], az)), rv[7]);
+      } else {
+        const double c = rv[0], sn = rv[1];
+        const double uu = __dadd_rn(__dmul_rn(c, ax), __dmul_rn(sn, ay));
+        const double vv = __dadd_rn(__dmul_rn(-sn, ax), __dmul_rn(c, ay));
+        xw = __dadd_rn(uu, rv[2]);
+        if (MODE == MSURF_MODE_EXT_TILT) {
+          const double yv = __dsub_rn(__dmul_rn(J.tilt_c, vv), __dmul_rn(J.tilt_s, az));
+          const double zz =
+              __dadd_rn(__dadd_rn(__dmul_rn(J.tilt_s, vv), __dmul_rn(J.tilt_c, az)), J.zoff);
+          yw = __dadd_rn(yv, rv[3]);
+          key = enc_key(zz);
+        } else {
+          yw = __dadd_rn(vv, rv[3]);
+        }
+      }
+      n_eval += valid;
+      const int gi = cell_index(xw, J.x_min, dd, inv, cx0);
+      const int gj = cell_index(yw, J.y_min, dd, inv, cy0);
+      const bool inside = valid & ((unsigned)gi <= span_i) & ((unsigned)(gj - j_lo) <= span_j);
+      if (inside) {
+        ++n_dep;
+        const long long idx = (long long)gi * ldk + (gj - j_lo);
+        if (idx == last) {
+          run = key < run ? key : run;
+        } else {
+          flush_min(keys, last, run, n_atom);
+          last = idx;
+          run = key;
+        }
+      }
+    }
+    flush_min(keys, last, run, n_atom);
+  }
+
+  // counters: one atomic per warp
+  n_eval = warp_sum_u(n_eval);
+  n_dep = warp_sum_u(n_dep);
+  n_atom = warp_sum_u(n_atom);
+  if (lane == 0 && J.counters) {
+    if (warp == 0) atomicAdd(J.counters + MSURF_CTR_LIVE_ROWS, (unsigned long long)n_live);
+    atomicAdd(J.counters + MSURF_CTR_EVAL, (unsigned long long)n_eval);
+    atomicAdd(J.counters + MSURF_CTR_DEPOSITS, (unsigned long long)n_dep);
+    atomicAdd(J.counters + MSURF_CTR_ATOMICS, (unsigned long long)n_atom);
+  }
+}
+
+// --------------------------------------------------------------- fill/decode
+__global__ void fill_kernel(uint64_t* __restrict__ keys, long long count,
+                            const double* __restrict__ value) {
+  const uint64_t key = enc_key(value[blockIdx.y]);
+  uint64_t* base = keys + (long long)blockIdx.y * count;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride)
+    base[i] = key;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    decode_kernel(uint64_t* __restrict__ keys, long long count, const double* __restrict__ sent,
+                  unsigned long long* __restrict__ machined) {
+  uint64_t* base = keys + (long long)blockIdx.y * count;
+  const double sentinel = sent[blockIdx.y];
+  double* out = reinterpret_cast<double*>(base);
+  unsigned cnt = 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    const double h = dec_key(base[i]);
+    out[i] = h;
+    cnt += (h < sentinel);
+  }
+  cnt = warp_sum_u(cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(machined + blockIdx.y, (unsigned long long)cnt);
+}
+
+// ------------------------------------------------------------ reductions
+template <int NV>
+struct Acc {
+  double v[NV];
+};
+
+__device__ __forceinline__ double shfl_d(double v, int o) {
+  return __shfl_xor_sync(0xffffffffu, v, o);
+}
+
+// fixed-order block reduction; kind[k]: 0 sum, 1 max, 2 min
+template <int NV>
+__device__ void block_reduce(double (&v)[NV], const int (&kind)[NV], double* sh /*[kWarps*NV]*/) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const double w = shfl_d(v[k], o);
+      v[k] = kind[k] == 0 ? v[k] + w : (kind[k] == 1 ? fmax(v[k], w) : fmin(v[k], w));
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) sh[warp * NV + k] = v[k];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      v[k] = lane < kWarps ? sh[lane * NV + k] : (kind[k] == 0 ? 0.0 : (kind[k] == 1 ? -INFINITY : INFINITY));
+    }
+#pragma unroll
+    for (int o = 4; o; o >>= 1) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const double w = shfl_d(v[k], o);
+        v[k] = kind[k] == 0 ? v[k] + w : (kind[k] == 1 ? fmax(v[k], w) : fmin(v[k], w));
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    areal_pass1_kernel(const double* __restrict__ h, long long ld, long long sstride,
+                       long long i_lo, long long j_lo, long long rows, long long cols,
+                       const double* __restrict__ sent, int exclude, double* __restrict__ work) {
+  __shared__ double sh[kWarps * 5];
+  const double* hs = h + (long long)blockIdx.y * sstride;
+  const double sentinel = sent[blockIdx.y];
+  double v[5] = {0.0, -INFINITY, INFINITY, 0.0, 0.0};
+  const int kind[5] = {0, 1, 2, 0, 0};
+  for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+    const double* row = hs + (i_lo + r) * ld + j_lo;
+    for (long long c = threadIdx.x; c < cols; c += blockDim.x) {
+      const double hv = row[c];
+      const bool cut = hv < sentinel;
+      if (!cut) v[4] += 1.0;
+      if (cut || !exclude) {
+        const double z = hv * 1000.0;  // roughness.py:105 (MM_TO_UM)
+        v[0] += z;
+        v[1] = fmax(v[1], z);
+        v[2] = fmin(v[2], z);
+        v[3] += 1.0;
+      }
+    }
+  }
+  block_reduce<5>(v, kind, sh);
+  if (threadIdx.x == 0) {
+    double* o = work + ((long long)blockIdx.y * gridDim.x + blockIdx.x) * 5;
+    for (int k = 0; k < 5; ++k) o[k] = v[k];
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    areal_pass2_kernel(const double* __restrict__ h, long long ld, long long sstride,
+                       long long i_lo, long long j_lo, long long rows, long long cols,
+                       const double* __restrict__ sent, int exclude,
+                       const double* __restrict__ stats1, double* __restrict__ work) {
+  __shared__ double sh[kWarps * 4];
+  const double* hs = h + (long long)blockIdx.y * sstride;
+  const double sentinel = sent[blockIdx.y];
+  const double mu = stats1[blockIdx.y * 5 + 0] / stats1[blockIdx.y * 5 + 3];  // z.mean()
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  const int kind[4] = {0, 0, 0, 0};
+  for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+    const double* row = hs + (i_lo + r) * ld + j_lo;
+    for (long long c = threadIdx.x; c < cols; c += blockDim.x) {
+      const double hv = row[c];
+      if (hv < sentinel || !exclude) {
+        const double d = hv * 1000.0 - mu;  // roughness.py:105-106
+        const double d2 = d * d;
+        v[0] += fabs(d);
+        v[1] += d2;
+        v[2] += d2 * d;
+        v[3] += d2 * d2;
+      }
+    }
+  }
+  block_reduce<4>(v, kind, sh);
+  if (threadIdx.x == 0) {
+    double* o = work + ((long long)blockIdx.y * gridDim.x + blockIdx.x) * 4;
+    for (int k = 0; k < 4; ++k) o[k] = v[k];
+  }
+}
+
+// one block per surface: reduce nb partials in fixed order
+template <int NV>
+__global__ void __launch_bounds__(kThreads)
+    finalize_kernel(const double* __restrict__ work, int nb, int k0max, double* __restrict__ out) {
+  __shared__ double sh[kWarps * NV];
+  double v[NV];
+  int kind[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    kind[k] = (NV == 5 && k == 1) ? 1 : ((NV == 5 && k == 2) ? 2 : 0);
+    v[k] = kind[k] == 0 ? 0.0 : (kind[k] == 1 ? -INFINITY : INFINITY);
+  }
+  const double* w = work + (long long)blockIdx.x * nb * NV;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const double x = w[b * NV + k];
+      v[k] = kind[k] == 0 ? v[k] + x : (kind[k] == 1 ? fmax(v[k], x) : fmin(v[k], x));
+    }
+  }
+  block_reduce<NV>(v, kind, sh);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NV; ++k) out[(long long)blockIdx.x * NV + k] = v[k];
+  (void)k0max;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    profiles_kernel(const double* __restrict__ h, long long sstride, const long long* __restrict__ start,
+                    int n_prof, long long len, long long stride, const double* __restrict__ sent,
+                    int exclude, const double* __restrict__ stats_in, double* __restrict__ out) {
+  __shared__ double sh[kWarps * 5];
+  __shared__ double s_mean;
+  const int prof = blockIdx.x;
+  const int surf = blockIdx.y;
+  const double* base = h + (long long)surf * sstride + start[prof];
+  const double sentinel = sent[surf];
+  double v[5] = {0.0, 0.0, 0.0, -INFINITY, INFINITY};  // sum z, n_cut, n_uncut, max, min
+  const int kind[5] = {0, 0, 0, 1, 2};
+  for (long long k = threadIdx.x; k < len; k += blockDim.x) {
+    const double hv = base[k * stride];
+    const bool cut = hv < sentinel;
+    if (!cut) v[2] += 1.0;
+    if (cut || !exclude) {
+      const double z = hv * 1000.0;
+      v[0] += z;
+      v[1] += 1.0;
+      v[3] = fmax(v[3], z);
+      v[4] = fmin(v[4], z);
+    }
+  }
+  block_reduce<5>(v, kind, sh);
+  if (threadIdx.x == 0) {
+    const long long k = (long long)surf * n_prof + prof;
+    s_mean = stats_in ? stats_in[k * 8 + 0] / stats_in[k * 8 + 1] : (v[1] > 0 ? v[0] / v[1] : 0.0);
+  }
+  __syncthreads();
+  const double mu = s_mean;
+  double a[1] = {0.0};
+  const int ka[1] = {0};
+  for (long long k = threadIdx.x; k < len; k += blockDim.x) {
+    const double hv = base[k * stride];
+    if (hv < sentinel || !exclude) a[0] += fabs(hv * 1000.0 - mu);
+  }
+  __syncthreads();
+  block_reduce<1>(a, ka, sh);
+  if (threadIdx.x == 0) {
+    double* o = out + ((long long)surf * n_prof + prof) * 8;
+    o[0] = v[0]; o[1] = v[1]; o[2] = v[2]; o[3] = v[3]; o[4] = v[4]; o[5] = a[0];
+    o[6] = 0.0; o[7] = 0.0;
+  }
+}
+
+// ------------------------------------------------------------ microbench
+__global__ void mb_dp_kernel(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x * 1e-9, x1 = x0 + 1.0, x2 = x0 + 2.0, x3 = x0 + 3.0;
+  double x4 = x0 + 4.0, x5 = x0 + 5.0, x6 = x0 + 6.0, x7 = x0 + 7.0;
+  for (int i = 0; i < iters; ++i) {
+    x0 = __dadd_rn(__dmul_rn(x0, a), b); x1 = __dadd_rn(__dmul_rn(x1, a), b);
+    x2 = __dadd_rn(__dmul_rn(x2, a), b); x3 = __dadd_rn(__dmul_rn(x3, a), b);
+    x4 = __dadd_rn(__dmul_rn(x4, a), b); x5 = __dadd_rn(__dmul_rn(x5, a), b);
+    x6 = __dadd_rn(__dmul_rn(x6, a), b); x7 = __dadd_rn(__dmul_rn(x7, a), b);
+  }
+  const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (s == 12345.678) out[0] = s;
+}
+
+__global__ void mb_fma_kernel(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x * 1e-9, x1 = x0 + 1.0, x2 = x0 + 2.0, x3 = x0 + 3.0;
+  double x4 = x0 + 4.0, x5 = x0 + 5.0, x6 = x0 + 6.0, x7 = x0 + 7.0;
+  for (int i = 0; i < iters; ++i) {
+    x0 = __fma_rn(x0, a, b); x1 = __fma_rn(x1, a, b); x2 = __fma_rn(x2, a, b);
+    x3 = __fma_rn(x3, a, b); x4 = __fma_rn(x4, a, b); x5 = __fma_rn(x5, a, b);
+    x6 = __fma_rn(x6, a, b); x7 = __fma_rn(x7, a, b);
+  }
+  const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (s == 12345.678) out[0] = s;
+}
+
+__global__ void mb_atomic_kernel(unsigned long long* buf, long long mask, int iters) {
+  unsigned long long x = (blockIdx.x * 1315423911ull) ^ (threadIdx.x * 2654435761ull) ^ 0x9e3779b97f4a7c15ull;
+  for (int i = 0; i < iters; ++i) {
+    x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+    atomicMin(buf + (x & mask), x >> 1);
+  }
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+int msurf_abi_version(void) { return MSURF_ABI_VERSION; }
+const char* msurf_last_error(void) { return g_err.c_str(); }
+int msurf_sizeof_job(void) { return (int)sizeof(msurf_job); }
+int msurf_tile_steps(void) { return kTileSteps; }
+
+int msurf_fill_keys(uint64_t* keys, int64_t count, int32_t n_surf, const double* value,
+                    void* stream) {
+  if (count < 0 || n_surf < 1 || (count > 0 && (!keys || !value)))
+    return set_err("msurf_fill_keys: bad arguments");
+  if (count == 0) return 0;
+  long long blocks = (count + kThreads - 1) / kThreads;
+  const long long cap = n_surf > 1 ? 64 : 148 * 8;
+  if (blocks > cap) blocks = cap;
+  fill_kernel<<<dim3((unsigned)blocks, (unsigned)n_surf), kThreads, 0, (cudaStream_t)stream>>>(
+      keys, count, value);
+  return check_launch("fill_kernel");
+}
+
+int msurf_sweep(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile_prefix,
+                int64_t n_tiles, int32_t mode, int32_t max_points, void* stream) {
+  if (n_jobs < 1 || !jobs || !tile_prefix || n_tiles < 0 || max_points < 1)
+    return set_err("msurf_sweep: bad arguments");
+  if (n_tiles == 0) return 0;
+  if (n_tiles > 0x7fffffffLL) return set_err("msurf_sweep: too many tiles");
+  const int nchunk = (max_points + 31) / 32;
+  const int mask_words = (nchunk + 63) / 64;
+  const size_t smem = (size_t)kTileSteps * 8 * sizeof(double) +
+                      (size_t)kTileSteps * mask_words * sizeof(uint64_t) + (size_t)kTileSteps * sizeof(int);
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  switch (mode) {
+    case MSURF_MODE_REF:
+      if (smem > 48 * 1024) e = cudaFuncSetAttribute(sweep_kernel<MSURF_MODE_REF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) sweep_kernel<MSURF_MODE_REF><<<(unsigned)n_tiles, kThreads, smem, st>>>(jobs, n_jobs, tile_prefix, mask_words);
+      break;
+    case MSURF_MODE_EXT:
+      if (smem > 48 * 1024) e = cudaFuncSetAttribute(sweep_kernel<MSURF_MODE_EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) sweep_kernel<MSURF_MODE_EXT><<<(unsigned)n_tiles, kThreads, smem, st>>>(jobs, n_jobs, tile_prefix, mask_words);
+      break;
+    case MSURF_MODE_EXT_TILT:
+      if (smem > 48 * 1024) e = cudaFuncSetAttribute(sweep_kernel<MSURF_MODE_EXT_TILT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) sweep_kernel<MSURF_MODE_EXT_TILT><<<(unsigned)n_tiles, kThreads, smem, st>>>(jobs, n_jobs, tile_prefix, mask_words);
+      break;
+    default:
+      return set_err("msurf_sweep: unknown mode");
+  }
+  if (e != cudaSuccess) return set_err(std::string("msurf_sweep: smem attribute: ") + cudaGetErrorString(e));
+  return check_launch("sweep_kernel");
+}
+
+int msurf_decode(uint64_t* keys, int64_t count, int32_t n_surf, const double* sentinel,
+                 unsigned long long* machined, void* stream) {
+  if (count < 0 || n_surf < 1 || !keys || !machined || !sentinel)
+    return set_err("msurf_decode: bad arguments");
+  if (count == 0) return 0;
+  long long blocks = (count + kThreads - 1) / kThreads;
+  const long long cap = n_surf > 1 ? 64 : 148 * 8;
+  if (blocks > cap) blocks = cap;
+  dim3 grid((unsigned)blocks, (unsigned)n_surf);
+  decode_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(keys, count, sentinel, machined);
+  return check_launch("decode_kernel");
+}
+
+static int red_blocks(int64_t rows) {
+  return (int)(rows < MSURF_RED_BLOCKS ? (rows > 0 ? rows : 1) : MSURF_RED_BLOCKS);
+}
+
+int msurf_areal_pass1(const double* h, int64_t ld, int64_t surf_stride, int32_t n_surf,
+                      int64_t i_lo, int64_t j_lo, int64_t rows, int64_t cols,
+                      const double* sentinel, int32_t exclude_uncut, double* work,
+                      double* out1, void* stream) {
+  if (!h || !work || !out1 || !sentinel || n_surf < 1 || rows < 1 || cols < 1 || i_lo < 0 || j_lo < 0 || ld < cols)
+    return set_err("msurf_areal_pass1: bad arguments");
+  const int nb = red_blocks(rows);
+  cudaStream_t st = (cudaStream_t)stream;
+  areal_pass1_kernel<<<dim3(nb, n_surf), kThreads, 0, st>>>(h, ld, surf_stride, i_lo, j_lo, rows, cols,
+                                                           sentinel, exclude_uncut, work);
+  if (check_launch("areal_pass1_kernel")) return 1;
+  finalize_kernel<5><<<n_surf, kThreads, 0, st>>>(work, nb, 0, out1);
+  return check_launch("finalize_kernel<5>");
+}
+
+int msurf_areal_pass2(const double* h, int64_t ld, int64_t surf_stride, int32_t n_surf,
+                      int64_t i_lo, int64_t j_lo, int64_t rows, int64_t cols,
+                      const double* sentinel, int32_t exclude_uncut, const double* stats1,
+                      double* work, double* out2, void* stream) {
+  if (!h || !work || !out2 || !stats1 || !sentinel || n_surf < 1 || rows < 1 || cols < 1 || i_lo < 0 || j_lo < 0 || ld < cols)
+    return set_err("msurf_areal_pass2: bad arguments");
+  const int nb = red_blocks(rows);
+  cudaStream_t st = (cudaStream_t)stream;
+  areal_pass2_kernel<<<dim3(nb, n_surf), kThreads, 0, st>>>(h, ld, surf_stride, i_lo, j_lo, rows, cols,
+                                                           sentinel, exclude_uncut, stats1, work);
+  if (check_launch("areal_pass2_kernel")) return 1;
+  finalize_kernel<4><<<n_surf, kThreads, 0, st>>>(work, nb, 0, out2);
+  return check_launch("finalize_kernel<4>");
+}
+
+int msurf_profiles(const double* h, int64_t surf_stride, int32_t n_surf, const int64_t* start,
+                   int32_t n_prof, int64_t len, int64_t stride, const double* sentinel,
+                   int32_t exclude_uncut, const double* stats_in, double* out, void* stream) {
+  if (!h || !start || !out || !sentinel || n_surf < 1 || n_prof < 1 || len < 1 || stride < 1)
+    return set_err("msurf_profiles: bad arguments");
+  profiles_kernel<<<dim3(n_prof, n_surf), kThreads, 0, (cudaStream_t)stream>>>(
+      h, surf_stride, reinterpret_cast<const long long*>(start), n_prof, len, stride, sentinel,
+      exclude_uncut, stats_in, out);
+  return check_launch("profiles_kernel");
+}
+
+int msurf_microbench(int32_t which, double* result) {
+  if (!result) return set_err("msurf_microbench: null result");
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float ms = 0.f;
+  if (which == 0 || which == 1) {
+    double* out = nullptr;
+    if (cudaMalloc(&out, 8) != cudaSuccess) return set_err("microbench: cudaMalloc");
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(a);
+      if (which == 0) mb_dp_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+      else mb_fma_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+    }
+    cudaEventElapsedTime(&ms, a, b);
+    cudaFree(out);
+    const double ops = (double)blocks * threads * iters * 8.0 * (which == 0 ? 2.0 : 1.0);
+    *result = ops / (ms * 1e-3);
+  } else if (which == 2) {
+    unsigned long long* buf = nullptr;
+    const long long n = 1ll << 24;  // 128 MiB of keys: L2-sized working set
+    if (cudaMalloc(&buf, n * 8) != cudaSuccess) return set_err("microbench: cudaMalloc");
+    cudaMemset(buf, 0xff, n * 8);
+    const int blocks = sms * 8, threads = 256, iters = 256;
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(a);
+      mb_atomic_kernel<<<blocks, threads>>>(buf, n - 1, iters);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+    }
+    cudaEventElapsedTime(&ms, a, b);
+    cudaFree(buf);
+    *result = (double)blocks * threads * iters / (ms * 1e-3);
+  } else {
+    return set_err("msurf_microbench: unknown kind");
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return check_launch("microbench");
+}
+
+}  // extern "C"

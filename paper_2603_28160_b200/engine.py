@@ -1,0 +1,335 @@
+"""The FSM sweep on the GPU — drop-in for millsurf.engine (engine.py:63-485).
+
+``simulate(config)`` plans on the host (planner.py), ships every per-surface
+array to HBM in one copy, and runs three kernels from libmsurf.so on the
+current stream: key fill (stock height), the sweep, and the key -> fp64
+decode that also counts machined cells. ``simulate_batch`` runs many
+parameter sets in the same three launches (the batched dataset mode).
+The returned HeightField stays in HBM until its NumPy view is requested, so
+``areal_metrics`` on it never leaves the device.
+
+``main_loop_seconds`` is the device time of fill + sweep + decode measured
+with CUDA events (the reference times its main loop plus the min-merge,
+engine.py:329-342).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from . import _native
+from .errors import ConfigError, MillsurfError
+from .extensions import Extensions
+from .grid import GridSpec, HeightField, TrajectoryRecord
+from .planner import MODE_REF, SweepPlan, plan, time_step
+
+DEFAULT_MAX_STEP_ANGLE_RAD = math.radians(0.5)
+
+__all__ = ["SimulationConfig", "SimulationResult", "time_step", "simulate", "simulate_batch",
+           "simulate_reference", "run_benchmark", "BenchmarkReport", "BenchmarkRow", "sweep_plans"]
+
+
+@dataclass(frozen=True)
+class SimulationConfig:
+    """Same fields and defaults as millsurf.engine.SimulationConfig (engine.py:63-73).
+    ``worker_count`` is accepted for compatibility; the GPU result does not
+    depend on it (the reference guarantees the same, engine.py:316-317)."""
+
+    tool: object
+    process: object
+    grid: GridSpec
+    edge_point_count: int | None = None
+    max_step_angle_rad: float = DEFAULT_MAX_STEP_ANGLE_RAD
+    time_step_s: float | None = None
+    span_s: tuple | None = None
+    record_trajectory: bool = False
+    worker_count: int = 1
+
+
+@dataclass
+class SimulationResult:
+    field: HeightField
+    trajectory: TrajectoryRecord | None
+    time_steps: int
+    trajectory_points: int
+    cells_updated: int
+    main_loop_seconds: float
+    counters: dict = field(default_factory=dict)
+
+
+@dataclass
+class _Surface:
+    plan: SweepPlan
+    j_lo: int
+    j_hi: int
+    key_off: int = 0          # element offset into the keys tensor
+    nodes: int = 0
+
+
+def _trig_tables(p: SweepPlan):
+    """Host-libm tables (parity mode): exactly the reference's per-row trig
+    (engine.py:240, 252-255) — np.cos/np.sin of base_K - omega*t."""
+    t = p.t_start + np.arange(p.steps, dtype=np.float64) * p.dt
+    tab = np.empty((p.steps, p.teeth, 2))
+    for k in range(p.teeth):
+        th = p.tooth_base[k] - p.omega * t
+        tab[:, k, 0] = np.cos(th)
+        tab[:, k, 1] = np.sin(th)
+    vib = np.sin(p.vib_omega * t + p.vib_phase) if p.vib_amp != 0.0 else None
+    return tab, vib
+
+
+def sweep_plans(surfaces, trig: str = "device", device=None, return_device=False):
+    """Run the sweep for ``surfaces`` (list of (SweepPlan, j_lo, j_hi)) in one
+    batch. Returns (heights fp64 tensor views, counters, machined, device_ms, traj)."""
+    torch = _native.require_cuda()
+    lib = _native.lib()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    if trig not in ("device", "host"):
+        raise ConfigError(f"trig must be 'device' or 'host', got {trig!r}")
+    surfs = [_Surface(p, lo, hi) for p, lo, hi in surfaces]
+    total = 0
+    for s in surfs:
+        s.key_off = total
+        s.nodes = (s.plan.grid.m + 1) * (s.j_hi - s.j_lo + 1)
+        total += s.nodes
+    keys = torch.empty(max(total, 1), dtype=torch.int64, device=dev)
+    need_traj = [s.plan.record for s in surfs]
+    traj = None
+    if any(need_traj):
+        traj = torch.empty(sum(s.plan.steps * s.plan.teeth * 3 for s, r in zip(surfs, need_traj) if r),
+                           dtype=torch.float64, device=dev)
+
+    ar = _native.Arena()
+    offs = []
+    for s in surfs:
+        p = s.plan
+        o = dict(
+            tooth_base=ar.add(p.tooth_base.astype(np.float64)),
+            tooth_rows=ar.add(p.tooth_rows.astype(np.float64)),
+            px=ar.add(p.px), py=ar.add(p.py), pz=ar.add(p.pz),
+            zkey=ar.add(p.zkey.astype(np.uint64)),
+            chunk_box=ar.add(p.chunk_box.astype(np.float64)),
+            pass_x0=ar.add(p.pass_x0.astype(np.float64)),
+            min_index=ar.add(p.min_index.astype(np.int32)),
+            counters=ar.add(np.zeros(_native.NUM_CTRS, dtype=np.uint64)),
+        )
+        if trig == "host":
+            tab, vib = _trig_tables(p)
+            o["trig_table"] = ar.add(tab)
+            if vib is not None:
+                o["vib_table"] = ar.add(vib)
+        offs.append(o)
+    n = len(surfs)
+    sentinel_off = ar.add(np.array([s.plan.initial_height for s in surfs], dtype=np.float64))
+    machined_off = ar.add(np.zeros(n, dtype=np.uint64))
+    groups = {}
+    for i, s in enumerate(surfs):
+        groups.setdefault(s.plan.mode, []).append(i)
+    tile_steps = lib.msurf_tile_steps()
+    group_meta = []
+    for mode, idx in sorted(groups.items()):
+        tiles = [surfs[i].plan.passes * surfs[i].plan.teeth *
+                 ((surfs[i].plan.steps + tile_steps - 1) // tile_steps) for i in idx]
+        prefix = np.concatenate([[0], np.cumsum(tiles)]).astype(np.int64)
+        job_off = ar.add(np.zeros(len(idx) * ctypes.sizeof(_native.MsurfJob), dtype=np.uint8))
+        pre_off = ar.add(prefix)
+        group_meta.append((mode, idx, job_off, pre_off, int(prefix[-1]),
+                           max(surfs[i].plan.points for i in idx)))
+    keys_ptr = keys.data_ptr()
+    traj_ptr = traj.data_ptr() if traj is not None else 0
+
+    def fill(base):
+        out = []
+        toff = 0
+        tptrs = []
+        for s, r in zip(surfs, need_traj):
+            tptrs.append(traj_ptr + toff * 8 if r else 0)
+            if r:
+                toff += s.plan.steps * s.plan.teeth * 3
+        for mode, idx, job_off, _, _, _ in group_meta:
+            arr = (_native.MsurfJob * len(idx))()
+            for k, i in enumerate(idx):
+                s, o, p = surfs[i], offs[i], surfs[i].plan
+                g = p.grid
+                j = arr[k]
+                j.spacing, j.x_min, j.y_min = g.spacing_mm, g.x_min_mm, g.y_min_mm
+                j.m, j.n, j.j_lo, j.j_hi = g.m, g.n, s.j_lo, s.j_hi
+                j.keys = keys_ptr + s.key_off * 8
+                j.t_start, j.dt, j.steps = p.t_start, p.dt, p.steps
+                j.y0, j.feed_speed, j.omega = p.y0, p.feed_speed, p.omega
+                for name in ("tooth_base", "tooth_rows", "px", "py", "pz", "zkey", "chunk_box",
+                             "pass_x0", "min_index", "counters"):
+                    setattr(j, name, base + o[name])
+                j.tilt_c, j.tilt_s, j.zoff = p.tilt_c, p.tilt_s, p.zoff
+                j.vib_amp, j.vib_omega, j.vib_phase = p.vib_amp, p.vib_omega, p.vib_phase
+                j.trig_table = base + o["trig_table"] if "trig_table" in o else None
+                j.vib_table = base + o["vib_table"] if "vib_table" in o else None
+                j.traj = tptrs[i] or None
+                j.teeth, j.points, j.passes = p.teeth, p.points, p.passes
+            out.append((job_off, bytes(arr)))
+        return out
+
+    stream = torch.cuda.current_stream(dev)
+    sp = _native.stream_ptr(stream)
+    buf = ar.upload(dev, fill)
+    base = buf.data_ptr()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    same = len({s.nodes for s in surfs}) == 1
+    if same:
+        _native.check(lib.msurf_fill_keys(keys_ptr, surfs[0].nodes, n, base + sentinel_off, sp))
+    else:
+        for i, s in enumerate(surfs):
+            _native.check(lib.msurf_fill_keys(keys_ptr + s.key_off * 8, s.nodes, 1,
+                                              base + sentinel_off + 8 * i, sp))
+    for mode, idx, job_off, pre_off, n_tiles, max_pts in group_meta:
+        _native.check(lib.msurf_sweep(base + job_off, len(idx), base + pre_off, n_tiles, mode,
+                                      max_pts, sp))
+    if same:
+        _native.check(lib.msurf_decode(keys_ptr, surfs[0].nodes, n, base + sentinel_off,
+                                       base + machined_off, sp))
+    else:
+        for i, s in enumerate(surfs):
+            _native.check(lib.msurf_decode(keys_ptr + s.key_off * 8, s.nodes, 1,
+                                           base + sentinel_off + 8 * i, base + machined_off + 8 * i, sp))
+    ev1.record(stream)
+    # small D2H: counters + machined counts (synchronises the stream)
+    ctr = []
+    u64 = buf.view(torch.int64)
+    for o in offs:
+        ctr.append(u64[o["counters"] // 8: o["counters"] // 8 + _native.NUM_CTRS])
+    small = torch.stack(ctr).cpu().numpy() if ctr else np.zeros((0, 4), np.int64)
+    machined = u64[machined_off // 8: machined_off // 8 + n].cpu().numpy()
+    device_ms = ev0.elapsed_time(ev1)
+    heights = keys.view(torch.float64)
+    views = [heights[s.key_off: s.key_off + s.nodes] for s in surfs]
+    trajs = []
+    if traj is not None:
+        toff = 0
+        for s, r in zip(surfs, need_traj):
+            if r:
+                k = s.plan.steps * s.plan.teeth * 3
+                trajs.append(traj[toff: toff + k])
+                toff += k
+            else:
+                trajs.append(None)
+    else:
+        trajs = [None] * n
+    return views, small, machined, device_ms, trajs, buf
+
+
+def _counters_dict(row) -> dict:
+    return {"live_rows": int(row[0]), "points_evaluated": int(row[1]),
+            "deposits": int(row[2]), "atomics": int(row[3])}
+
+
+def _build_trajectory(p: SweepPlan, traj_dev) -> TrajectoryRecord:
+    xyz = traj_dev.cpu().numpy().reshape(p.steps * p.teeth, 3)
+    rec = TrajectoryRecord(p.steps * p.teeth)
+    t = p.t_start + np.arange(p.steps, dtype=np.float64) * p.dt   # engine.py:240
+    rec.extend_block(np.repeat(t, p.teeth), np.tile(np.arange(1, p.teeth + 1, dtype=np.int64), p.steps),
+                     xyz[:, 0].copy(), xyz[:, 1].copy(), xyz[:, 2].copy())
+    return rec
+
+
+def simulate(config: SimulationConfig, extensions: Extensions | None = None, *,
+             trig: str = "device") -> SimulationResult:
+    """GPU FSM sweep with the reference's contract (engine.py:316-357).
+
+    ``extensions`` selects the extended kinematics (extensions.py).
+    ``trig='host'`` takes the per-(step, tooth) cos/sin from the host libm
+    (exactly the reference's values) instead of the device's correctly
+    rounded double-double sincos — the parity mode."""
+    p = plan(config, extensions)
+    views, small, machined, ms, trajs, _ = sweep_plans([(p, 0, p.grid.n)], trig=trig)
+    field_ = HeightField(p.grid, p.initial_height, device=views[0])
+    trajectory = _build_trajectory(p, trajs[0]) if p.record else None
+    return SimulationResult(field=field_, trajectory=trajectory, time_steps=p.steps,
+                            trajectory_points=p.trajectory_points, cells_updated=int(machined[0]),
+                            main_loop_seconds=ms * 1e-3, counters=_counters_dict(small[0]))
+
+
+def simulate_batch(configs, extensions=None, *, trig: str = "device"):
+    """Batched mode: many parameter sets swept in the same kernel launches.
+    ``extensions`` is None, one Extensions, or a list aligned with configs."""
+    if isinstance(extensions, (list, tuple)):
+        exts = list(extensions)
+        if len(exts) != len(configs):
+            raise ConfigError("extensions list must align with configs")
+    else:
+        exts = [extensions] * len(configs)
+    plans = [plan(c, e) for c, e in zip(configs, exts)]
+    if not plans:
+        return []
+    views, small, machined, ms, trajs, _ = sweep_plans([(p, 0, p.grid.n) for p in plans], trig=trig)
+    out = []
+    for p, v, row, mc, tr in zip(plans, views, small, machined, trajs):
+        out.append(SimulationResult(
+            field=HeightField(p.grid, p.initial_height, device=v),
+            trajectory=_build_trajectory(p, tr) if p.record else None,
+            time_steps=p.steps, trajectory_points=p.trajectory_points, cells_updated=int(mc),
+            main_loop_seconds=ms * 1e-3 / len(plans), counters=_counters_dict(row)))
+    return out
+
+
+def simulate_reference(config: SimulationConfig, extensions: Extensions | None = None) -> SimulationResult:
+    """The reference's 'naive' kernel is its oracle (engine.py:360-406). On the
+    GPU the same sweep runs in parity mode: trig from the host libm, so every
+    input the reference rounds is bit-identical by construction."""
+    return simulate(config, extensions, trig="host")
+
+
+@dataclass(frozen=True)
+class BenchmarkRow:
+    scale: float
+    trajectory_points: int
+    t_reference_s: float
+    t_optimized_s: float
+    speedup: float
+
+
+@dataclass
+class BenchmarkReport:
+    case_id: str
+    rows: list = field(default_factory=list)
+
+    def to_json_dict(self) -> dict:
+        return {"case_id": self.case_id,
+                "rows": [{"scale": r.scale, "trajectory_points": r.trajectory_points,
+                          "t_reference_s": r.t_reference_s, "t_optimized_s": r.t_optimized_s,
+                          "speedup": r.speedup} for r in self.rows]}
+
+    def to_text(self) -> str:
+        header = f"{'scale':>8} {'trajectory_points':>18} {'t_reference_s':>14} {'t_optimized_s':>14} {'speedup':>9}"
+        lines = [f"case: {self.case_id}", header, "-" * len(header)]
+        for r in self.rows:
+            lines.append(f"{r.scale:>8g} {r.trajectory_points:>18d} {r.t_reference_s:>14.4f} "
+                         f"{r.t_optimized_s:>14.4f} {r.speedup:>9.1f}")
+        return "\n".join(lines)
+
+
+def run_benchmark(config: SimulationConfig, sizes, case_id: str = "benchmark") -> BenchmarkReport:
+    """engine.py:449-485 shape: per size multiplier, parity-mode run vs device-
+    trig run, fields must agree exactly (a mismatch aborts)."""
+    if not sizes:
+        raise ConfigError("benchmark sizes must be non-empty")
+    base_dt = time_step(config)
+    rep = BenchmarkReport(case_id=case_id)
+    for size in sizes:
+        if size <= 0:
+            raise ConfigError(f"benchmark size must be > 0, got {size}")
+        scaled = replace(config, time_step_s=base_dt / size)
+        opt = simulate(scaled)
+        ref = simulate_reference(scaled)
+        if not np.array_equal(opt.field.heights, ref.field.heights):
+            raise MillsurfError(f"kernel mismatch at size {size}: device-trig and host-trig fields differ")
+        rep.rows.append(BenchmarkRow(scale=size, trajectory_points=opt.trajectory_points,
+                                     t_reference_s=ref.main_loop_seconds, t_optimized_s=opt.main_loop_seconds,
+                                     speedup=ref.main_loop_seconds / opt.main_loop_seconds
+                                     if opt.main_loop_seconds > 0 else math.inf))
+    return rep

@@ -1,0 +1,303 @@
+"""Host-side sweep planning: SimulationConfig (+ Extensions) -> device arrays.
+
+Restates the reference planner (engine.py:134-212, ``_plan``) for the
+reference kinematics, and states the extended model (extensions.py) for the
+rest. Everything here is O(teeth x edge points) NumPy on the host, done once
+per surface; the O(steps x teeth x points) work runs on the GPU. Evaluation
+order matches the reference expression by expression, so the device sweep
+reproduces the reference's heights bit-for-bit.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import ConfigError, DomainError
+from .extensions import Extensions
+from .geometry import default_point_count, edge_coordinates, effective_half_length
+from .kinematics import edge_to_tool_rows, tooth_base_angle
+
+MODE_REF, MODE_EXT, MODE_EXT_TILT = 0, 1, 2
+CHUNK = 32  # edge points per warp
+MAX_POINTS = 64 * 64 * 32  # mask words are bounded by the CTA's shared memory
+
+
+def encode_keys(z: np.ndarray) -> np.ndarray:
+    """Order-preserving fp64 -> u64 keys (the device's enc_key): -0 -> +0,
+    negative values bit-inverted, non-negative ones with the sign bit set."""
+    z = np.ascontiguousarray(z, dtype=np.float64) + 0.0
+    b = z.view(np.uint64)
+    neg = (b >> np.uint64(63)).astype(bool)
+    return np.where(neg, ~b, b | np.uint64(1 << 63))
+
+
+def decode_keys(k: np.ndarray) -> np.ndarray:
+    k = np.ascontiguousarray(k, dtype=np.uint64)
+    pos = (k >> np.uint64(63)).astype(bool)
+    b = np.where(pos, k & np.uint64(0x7FFFFFFFFFFFFFFF), ~k)
+    return b.view(np.float64)
+
+
+def time_step(config) -> float:
+    """Resolved dt: explicit, else min(step-angle guard, one-cell feed guard)
+    (engine.py:86-98)."""
+    if config.time_step_s is not None:
+        if config.time_step_s <= 0:
+            raise ConfigError(f"time_step_s must be > 0, got {config.time_step_s}")
+        return config.time_step_s
+    if config.max_step_angle_rad <= 0:
+        raise ConfigError(f"max_step_angle_rad must be > 0, got {config.max_step_angle_rad}")
+    by_angle = config.max_step_angle_rad / config.process.angular_velocity_rad_s
+    by_feed = config.grid.spacing_mm / config.process.feed_speed_mm_s
+    return min(by_angle, by_feed)
+
+
+@dataclass
+class SweepPlan:
+    mode: int
+    grid: object
+    teeth: int
+    points: int
+    steps: int
+    dt: float
+    t_start: float
+    x0: float
+    y0: float
+    z0: float
+    feed_speed: float
+    omega: float
+    initial_height: float
+    half_length: float
+    tooth_base: np.ndarray            # (Z,)
+    tooth_rows: np.ndarray            # (Z, 8) REF, zeros otherwise
+    px: np.ndarray                    # REF (N,), EXT (Z, N)
+    py: np.ndarray
+    pz: np.ndarray
+    zw: np.ndarray                    # (Z, N) z' (time-invariant unless tilt)
+    zkey: np.ndarray                  # (Z, N) u64
+    chunk_box: np.ndarray             # (Z, nchunk, 6)
+    pass_x0: np.ndarray               # (P,)
+    min_index: np.ndarray             # (Z,) int32
+    tilt_c: float = 1.0
+    tilt_s: float = 0.0
+    zoff: float = 0.0
+    vib_amp: float = 0.0
+    vib_omega: float = 0.0
+    vib_phase: float = 0.0
+    record: bool = False
+    extras: dict = field(default_factory=dict)
+
+    @property
+    def passes(self) -> int:
+        return int(self.pass_x0.shape[0])
+
+    @property
+    def trajectory_points(self) -> int:
+        """steps x teeth x points x passes (engine.py:129-131)."""
+        return self.steps * self.teeth * self.points * self.passes
+
+
+def _chunk_boxes(xt: np.ndarray, yt: np.ndarray, zt: np.ndarray) -> np.ndarray:
+    """Per tooth and 32-point chunk, tool-frame [xlo, xhi, ylo, yhi, zlo, zhi]."""
+    z_n, n = xt.shape
+    nchunk = (n + CHUNK - 1) // CHUNK
+    pad = nchunk * CHUNK - n
+    out = np.empty((z_n, nchunk, 6))
+    for a, arr in enumerate((xt, yt, zt)):
+        full = np.concatenate([arr, np.repeat(arr[:, -1:], pad, axis=1)], axis=1) if pad else arr
+        blk = full.reshape(z_n, nchunk, CHUNK)
+        out[:, :, 2 * a] = blk.min(axis=2)
+        out[:, :, 2 * a + 1] = blk.max(axis=2)
+    return out
+
+
+def _span(config, margin: float):
+    """Auto-span (engine.py:153-162) or explicit span (163-167); steps (170)."""
+    grid, proc = config.grid, config.process
+    x0, y0, z0 = proc.initial_position_mm
+    dt = time_step(config)
+    if config.span_s is None:
+        y0 = grid.y_min_mm - margin
+        t_start = 0.0
+        t_end = (grid.y_max_mm + margin - y0) / proc.feed_speed_mm_s
+    else:
+        t_start, t_end = config.span_s
+        if t_start < 0 or t_end <= t_start:
+            raise ConfigError(f"span_s must satisfy 0 <= start < end, got {config.span_s}")
+        if y0 is None:
+            raise ConfigError("initial position y is required when span_s is explicit")
+    if z0 is None:
+        z0 = 0.0
+    steps = int(math.floor((t_end - t_start) / dt)) + 1
+    return dt, t_start, steps, x0, y0, z0
+
+
+def edge_noise(teeth: int, n: int, sigma: float, corr: float, ds: float, seed: int) -> np.ndarray:
+    """Per-flute edge-radius perturbation (Extensions.noise_*): white noise
+    from default_rng(seed) of shape (teeth, n), smoothed along the edge by a
+    Gaussian of std g = corr/(2 ds) samples (truncated at 4g), divided by
+    sqrt(sum k^2) and scaled by sigma."""
+    rng = np.random.default_rng(seed)
+    white = rng.standard_normal((teeth, n))
+    g = corr / (2.0 * ds)
+    if g < 0.5:
+        return sigma * white
+    w = int(math.ceil(4.0 * g))
+    k = np.exp(-0.5 * (np.arange(-w, w + 1, dtype=np.float64) / g) ** 2)
+    norm = math.sqrt(float(np.sum(k * k)))
+    out = np.empty((teeth, n))
+    for t in range(teeth):
+        out[t] = sigma * (np.convolve(white[t], k, mode="same") / norm)
+    return out
+
+
+def plan(config, ext: Extensions | None = None) -> SweepPlan:
+    ext = ext or Extensions()
+    tool, proc, grid = config.tool, config.process, config.grid
+    if proc.depth_of_cut_mm > tool.insert_radius_mm:
+        raise ConfigError(f"depth of cut {proc.depth_of_cut_mm} mm exceeds insert radius "
+                          f"{tool.insert_radius_mm} mm")
+    if getattr(config, "worker_count", 1) < 1:
+        raise ConfigError(f"worker_count must be >= 1, got {config.worker_count}")
+    passes = int(ext.passes)
+    if ext.kinematic:
+        p = _plan_ext(config, ext)
+    else:
+        p = _plan_ref(config)
+    p.pass_x0 = np.array([p.x0 + k * ext.stepover_mm for k in range(passes)], dtype=np.float64)
+    p.record = bool(getattr(config, "record_trajectory", False))
+    if p.record and p.mode != MODE_REF:
+        raise ConfigError("record_trajectory is defined for the reference kinematics only")
+    if p.points > MAX_POINTS:
+        raise ConfigError(f"edge_point_count {p.points} exceeds the device limit {MAX_POINTS}")
+    if max(grid.m, grid.n) >= 1 << 21:
+        raise ConfigError("grid axes must have fewer than 2^21 cells")
+    return p
+
+
+def _plan_ref(config) -> SweepPlan:
+    """engine.py:134-212 restated."""
+    tool, proc, grid = config.tool, config.process, config.grid
+    half = effective_half_length(tool.insert_radius_mm, proc.depth_of_cut_mm,
+                                 proc.feed_per_tooth_mm, tool.radial_rake_rad)
+    n = config.edge_point_count
+    if n is None:
+        n = default_point_count(half, grid.spacing_mm)
+    if n < 2:
+        raise DomainError(f"point_count must be >= 2, got {n}")
+    if half > tool.insert_radius_mm:
+        raise DomainError(f"engaged half-length {half:.6g} mm exceeds the insert radius "
+                          f"{tool.insert_radius_mm} mm (feed per tooth too large for this insert)")
+    xp, yp, zp = edge_coordinates(half, n, tool.insert_radius_mm)
+    margin = tool.cutting_diameter_mm / 2.0 + half                  # engine.py:158
+    dt, t_start, steps, x0, y0, z0 = _span(config, margin)
+    z_n = tool.tooth_count
+    rows = np.zeros((z_n, 8))
+    xt = np.empty((z_n, n))
+    yt = np.empty((z_n, n))
+    zw = np.empty((z_n, n))
+    for k in range(1, z_n + 1):
+        e = edge_to_tool_rows(tool, k)
+        rows[k - 1] = [e[0][0], e[0][1], e[0][2], e[0][3], e[1][0], e[1][1], e[1][2], e[1][3]]
+        tz = e[2][3] + z0                                           # engine.py:181-182
+        zw[k - 1] = ((e[2][0] * xp + e[2][1] * yp) + e[2][2] * zp) + tz
+        xt[k - 1] = ((e[0][0] * xp + e[0][1] * yp) + e[0][2] * zp) + e[0][3]
+        yt[k - 1] = ((e[1][0] * xp + e[1][1] * yp) + e[1][2] * zp) + e[1][3]
+    return SweepPlan(
+        mode=MODE_REF, grid=grid, teeth=z_n, points=n, steps=steps, dt=dt, t_start=t_start,
+        x0=x0, y0=y0, z0=z0, feed_speed=proc.feed_speed_mm_s, omega=proc.angular_velocity_rad_s,
+        initial_height=z0 + proc.depth_of_cut_mm, half_length=half,
+        tooth_base=np.array([tooth_base_angle(proc.phase_rad, k, z_n) for k in range(1, z_n + 1)]),
+        tooth_rows=rows, px=xp, py=yp, pz=zp, zw=zw, zkey=encode_keys(zw),
+        chunk_box=_chunk_boxes(xt, yt, zw), pass_x0=np.array([x0]),
+        min_index=np.argmin(zw, axis=1).astype(np.int32),
+    )
+
+
+def _plan_ext(config, ext: Extensions) -> SweepPlan:
+    """Extended model (extensions.py / DESIGN.md §3)."""
+    tool, proc, grid = config.tool, config.process, config.grid
+    r = tool.insert_radius_mm
+    a_p = proc.depth_of_cut_mm
+    tau = ext.tilt_rad
+    z_n = tool.tooth_count
+    if ext.profile == "insert":
+        half = effective_half_length(r, a_p, proc.feed_per_tooth_mm, tool.radial_rake_rad)
+        n = config.edge_point_count or default_point_count(half, grid.spacing_mm)
+        if n < 2:
+            raise DomainError(f"point_count must be >= 2, got {n}")
+        ex, ey, ez = edge_coordinates(half, n, r)
+        nx = ex / r
+        nz = -(r - ez) / r
+        arc = 2.0 * r * math.asin(min(1.0, half / r))
+        base_margin = tool.cutting_diameter_mm / 2.0 + half
+    else:
+        n = config.edge_point_count
+        if n is None or n < 2:
+            raise ConfigError("the ball profile needs edge_point_count >= 2")
+        kmax = min(math.pi / 2.0, math.acos((r - a_p) / r) + abs(tau))
+        kap = kmax * np.arange(n, dtype=np.float64) / (n - 1)
+        kap[-1] = kmax
+        nx = np.sin(kap)
+        nz = -np.cos(kap)
+        ex = r * nx
+        ey = np.zeros(n)
+        ez = r - r * np.cos(kap)
+        arc = r * kmax
+        half = r * math.sin(kmax)
+        base_margin = half
+    sigma = ext.noise_sigma_mm
+    if sigma != 0.0:
+        delta = edge_noise(z_n, n, sigma, ext.noise_corr_mm, arc / (n - 1), int(ext.noise_seed))
+    beta, rho, lam = ext.helix_angle_rad, ext.runout_offset_mm, ext.runout_phase_rad
+    if beta != 0.0:
+        r_ref = ext.helix_ref_radius_mm
+        if r_ref is None:
+            r_ref = tool.cutting_diameter_mm / 2.0 if ext.profile == "insert" else r
+        tanb_over_r = math.tan(beta) / r_ref
+    radial = None if ext.profile == "insert" else 0.0
+    xt = np.empty((z_n, n))
+    yt = np.empty((z_n, n))
+    zt = np.empty((z_n, n))
+    for k in range(1, z_n + 1):
+        if sigma != 0.0:
+            px = ex + delta[k - 1] * nx
+            pz = ez + delta[k - 1] * nz
+        else:
+            px, pz = ex, ez
+        py = ey
+        e = edge_to_tool_rows(tool, k, radial_offset_mm=radial)
+        qx = ((e[0][0] * px + e[0][1] * py) + e[0][2] * pz) + e[0][3]
+        qy = ((e[1][0] * px + e[1][1] * py) + e[1][2] * pz) + e[1][3]
+        qz = ((e[2][0] * px + e[2][1] * py) + e[2][2] * pz) + e[2][3]
+        if beta != 0.0:
+            psi = pz * tanb_over_r
+            cps, sps = np.cos(psi), np.sin(psi)
+            qx, qy = cps * qx + sps * qy, (-sps) * qx + cps * qy
+        if rho != 0.0:
+            ang = lam + (2.0 * math.pi) * (k - 1) / z_n
+            qx = qx + rho * math.cos(ang)
+            qy = qy + rho * math.sin(ang)
+        xt[k - 1], yt[k - 1], zt[k - 1] = qx, qy, qz
+    tilt = tau != 0.0
+    tc, ts = math.cos(tau), math.sin(tau)
+    z_shift = -float(np.min(tc * zt - abs(ts) * np.sqrt(xt * xt + yt * yt))) if tilt else 0.0
+    amp = ext.vib_amplitude_mm
+    margin = base_margin + (abs(rho) + abs(amp) + 5.0 * abs(sigma) + abs(ts) * float(np.max(np.abs(zt))))
+    dt, t_start, steps, x0, y0, z0 = _span(config, margin)
+    zoff = z0 + z_shift
+    zw = zt + zoff
+    return SweepPlan(
+        mode=MODE_EXT_TILT if tilt else MODE_EXT, grid=grid, teeth=z_n, points=n, steps=steps,
+        dt=dt, t_start=t_start, x0=x0, y0=y0, z0=z0, feed_speed=proc.feed_speed_mm_s,
+        omega=proc.angular_velocity_rad_s, initial_height=z0 + a_p, half_length=half,
+        tooth_base=np.array([tooth_base_angle(proc.phase_rad, k, z_n) for k in range(1, z_n + 1)]),
+        tooth_rows=np.zeros((z_n, 8)), px=xt, py=yt, pz=zt, zw=zw, zkey=encode_keys(zw),
+        chunk_box=_chunk_boxes(xt, yt, zt), pass_x0=np.array([x0]),
+        min_index=np.argmin(zw, axis=1).astype(np.int32),
+        tilt_c=tc, tilt_s=ts, zoff=zoff, vib_amp=amp,
+        vib_omega=2.0 * math.pi * ext.vib_frequency_hz, vib_phase=ext.vib_phase_rad,
+    )

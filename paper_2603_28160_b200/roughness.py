@@ -1,0 +1,317 @@
+"""Areal and profile roughness on the GPU — drop-in for millsurf.roughness.
+
+Areal parameters (roughness.py:26-135): z in µm = h * 1000, deviations from
+the arithmetic mean, Sa = mean|d|, Sq = sqrt(mean d^2), Sp = max d,
+Sv = -min d, Sz = Sp + Sv, Ssk = mean d^3 / Sq^3, Sku = mean d^4 / Sq^4
+(None on a flat region). Two deterministic device passes
+(msurf_areal_pass1: sum/max/min/counts; msurf_areal_pass2: the four central
+moments around the device-computed mean) and one 9-double D2H read.
+
+Profiles (roughness.py:138-188): Ra = mean|z - mean z| (µm); the product
+adds Rz = Rp + Rv over the same profile, and ``profile_roughness`` evaluates
+many profiles (e.g. "every 64th row") in one launch.
+
+``uncut='raise'`` (default) mirrors the reference: any uncut cell in the ROI
+raises DomainError (roughness.py:86-89). ``uncut='exclude'`` is the product's
+documented extension for fine grids where sparse uncut cells remain
+(SURVEY.md §0 fact 7): statistics over machined cells only.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .errors import DomainError
+from .grid import HeightField
+
+MM_TO_UM = 1000.0
+
+
+@dataclass(frozen=True)
+class ArealMetrics:
+    sa_um: float
+    sq_um: float
+    sp_um: float
+    sv_um: float
+    sz_um: float
+    ssk: float | None
+    sku: float | None
+    cell_count: int
+
+    def to_json_dict(self) -> dict:
+        return {"Sa_um": self.sa_um, "Sq_um": self.sq_um, "Sp_um": self.sp_um, "Sv_um": self.sv_um,
+                "Sz_um": self.sz_um, "Ssk": self.ssk, "Sku": self.sku, "cell_count": self.cell_count}
+
+    def to_text(self) -> str:
+        rows = [("Sa", f"{self.sa_um:.6f} um"), ("Sq", f"{self.sq_um:.6f} um"),
+                ("Sp", f"{self.sp_um:.6f} um"), ("Sv", f"{self.sv_um:.6f} um"),
+                ("Sz", f"{self.sz_um:.6f} um"),
+                ("Ssk", "undefined" if self.ssk is None else f"{self.ssk:.6f}"),
+                ("Sku", "undefined" if self.sku is None else f"{self.sku:.6f}"),
+                ("cells", str(self.cell_count))]
+        w = max(len(k) for k, _ in rows)
+        return "\n".join(f"{k:<{w}}  {v}" for k, v in rows)
+
+
+@dataclass(frozen=True)
+class LineProfile:
+    """Feed profiles run along Y (fixed i), pick-feed along X (fixed j)."""
+
+    direction: str
+    index: int
+    positions_mm: np.ndarray
+    heights_mm: np.ndarray
+    spacing_mm: float
+
+
+@dataclass(frozen=True)
+class ProfileRoughness:
+    index: int
+    ra_um: float
+    rz_um: float
+    rp_um: float
+    rv_um: float
+    sample_count: int
+
+
+def _check_roi(spec, roi):
+    if roi is None:
+        roi = (0, 0, spec.m, spec.n)
+    i_lo, j_lo, i_hi, j_hi = (int(v) for v in roi)
+    if not (0 <= i_lo <= i_hi <= spec.m and 0 <= j_lo <= j_hi <= spec.n):
+        raise DomainError(f"roi {roi} outside grid [0, {spec.m}] x [0, {spec.n}] or empty")
+    return i_lo, j_lo, i_hi, j_hi
+
+
+def _metrics_from_moments(st1, st2) -> ArealMetrics:
+    n = st1[3]
+    mean = st1[0] / n
+    sa = float(st2[0] / n)
+    sq = float(np.sqrt(st2[1] / n))
+    sp = float(st1[1] - mean)
+    sv = float(-(st1[2] - mean))
+    if sq == 0.0:
+        ssk = sku = None
+    else:
+        ssk = float((st2[2] / n) / sq ** 3)
+        sku = float((st2[3] / n) / sq ** 4)
+    return ArealMetrics(sa_um=sa, sq_um=sq, sp_um=sp, sv_um=sv, sz_um=sp + sv, ssk=ssk, sku=sku,
+                        cell_count=int(n))
+
+
+class _Scratch:
+    """Per-device scratch for the reductions (work partials + outputs)."""
+
+    _cache = {}
+
+    @classmethod
+    def get(cls, torch, device, n_surf: int):
+        key = (device.index if device.index is not None else torch.cuda.current_device())
+        need = n_surf * _native.RED_BLOCKS * 5 + n_surf * 16
+        t = cls._cache.get(key)
+        if t is None or t.numel() < need:
+            t = torch.empty(need, dtype=torch.float64, device=device)
+            cls._cache[key] = t
+        return t
+
+
+def areal_moments_device(h_dev, ld, n_surf, surf_stride, roi_box, sentinels_dev, exclude,
+                         allreduce=None):
+    """Run both areal passes; returns (stats1 [n_surf,5], moments [n_surf,4])
+    on the host. ``allreduce(tensor, op)`` (strip sharding) combines the
+    partial first-pass stats (kind "stats1": columns sum, max, min, n, n_uncut)
+    and second-pass moments (kind "moments": four sums) across ranks in place."""
+    torch = _native.require_cuda()
+    lib = _native.lib()
+    i_lo, j_lo, rows, cols = roi_box
+    dev = h_dev.device
+    sc = _Scratch.get(torch, dev, n_surf)
+    work = sc.data_ptr()
+    out1 = sc[n_surf * _native.RED_BLOCKS * 5:]
+    st1 = out1[: n_surf * 5]
+    st2 = out1[n_surf * 5: n_surf * 9]
+    sp = _native.stream_ptr()
+    _native.check(lib.msurf_areal_pass1(h_dev.data_ptr(), ld, surf_stride, n_surf, i_lo, j_lo, rows,
+                                        cols, sentinels_dev.data_ptr(), int(exclude), work,
+                                        st1.data_ptr(), sp))
+    if allreduce is not None:
+        allreduce(st1.view(n_surf, 5), "stats1")
+    _native.check(lib.msurf_areal_pass2(h_dev.data_ptr(), ld, surf_stride, n_surf, i_lo, j_lo, rows,
+                                        cols, sentinels_dev.data_ptr(), int(exclude), st1.data_ptr(),
+                                        work, st2.data_ptr(), sp))
+    if allreduce is not None:
+        allreduce(st2.view(n_surf, 4), "moments")
+    both = out1[: n_surf * 9].cpu().numpy()
+    return both[: n_surf * 5].reshape(n_surf, 5), both[n_surf * 5:].reshape(n_surf, 4)
+
+
+def _sentinel_tensor(torch, values, device):
+    return torch.tensor(np.asarray(values, dtype=np.float64), device=device)
+
+
+def areal_metrics(field: HeightField, roi=None, leveling: str = "mean", uncut: str = "raise") -> ArealMetrics:
+    """Areal parameters over the inclusive node range (i_lo, j_lo, i_hi, j_hi)."""
+    if leveling != "mean":
+        if leveling == "plane":
+            raise DomainError("leveling='plane' is not implemented on the device path yet")
+        raise DomainError(f"unknown leveling mode {leveling!r}")
+    if uncut not in ("raise", "exclude"):
+        raise DomainError(f"uncut must be 'raise' or 'exclude', got {uncut!r}")
+    i_lo, j_lo, i_hi, j_hi = _check_roi(field.spec, roi)
+    torch = _native.require_cuda()
+    h = field.device_heights()
+    sent = _sentinel_tensor(torch, [field.initial_height_mm], h.device)
+    st1, st2 = areal_moments_device(h, field.spec.n + 1, 1, 0,
+                                    (i_lo, j_lo, i_hi - i_lo + 1, j_hi - j_lo + 1), sent,
+                                    uncut == "exclude")
+    return _finish_areal(st1[0], st2[0], uncut)
+
+
+def _finish_areal(st1, st2, uncut) -> ArealMetrics:
+    if uncut == "raise" and st1[4] > 0:
+        raise DomainError("roughness over unmachined stock is undefined: roi contains uncut cells")
+    if st1[3] <= 0:
+        raise DomainError("no machined cells in roi")
+    return _metrics_from_moments(st1, st2)
+
+
+def areal_metrics_batch(fields, roi=None, uncut: str = "raise"):
+    """Areal metrics of many same-shape fields that live in one contiguous
+    device buffer (simulate_batch output) in two launches; falls back to one
+    call per field when they do not share a buffer. Returns a list of
+    ArealMetrics or DomainError instances (per-sample status, dataset.py:177-180)."""
+    if not fields:
+        return []
+    torch = _native.require_cuda()
+    spec = fields[0].spec
+    same = all(f.spec == spec for f in fields)
+    devs = [f.device_heights() for f in fields]
+    stride = None
+    if same and len(devs) > 1:
+        p0 = devs[0].data_ptr()
+        st = devs[1].data_ptr() - p0
+        if st > 0 and all(d.data_ptr() == p0 + k * st for k, d in enumerate(devs)) and st % 8 == 0:
+            stride = st // 8
+    if not same or (len(devs) > 1 and stride is None):
+        out = []
+        for f in fields:
+            try:
+                out.append(areal_metrics(f, roi=roi, uncut=uncut))
+            except DomainError as exc:
+                out.append(exc)
+        return out
+    i_lo, j_lo, i_hi, j_hi = _check_roi(spec, roi)
+    sent = _sentinel_tensor(torch, [f.initial_height_mm for f in fields], devs[0].device)
+    st1, st2 = areal_moments_device(devs[0], spec.n + 1, len(fields), stride or 0,
+                                    (i_lo, j_lo, i_hi - i_lo + 1, j_hi - j_lo + 1), sent,
+                                    uncut == "exclude")
+    out = []
+    for a, b in zip(st1, st2):
+        try:
+            out.append(_finish_areal(a, b, uncut))
+        except DomainError as exc:
+            out.append(exc)
+    return out
+
+
+def extract_profile(field: HeightField, direction: str, index=None, roi=None) -> LineProfile:
+    """Feed-direction column (fixed x) or pick-feed row (fixed y) (roughness.py:138-180)."""
+    spec = field.spec
+    i_lo, j_lo, i_hi, j_hi = _check_roi(spec, roi)
+    if direction == "feed":
+        idx = round(spec.m / 2) if index is None else index
+        if not i_lo <= idx <= i_hi:
+            raise DomainError(f"feed profile index {idx} outside roi columns {i_lo}..{i_hi}")
+        start, length, step = idx * (spec.n + 1) + j_lo, j_hi - j_lo + 1, 1
+        positions = spec.y_coords()[j_lo:j_hi + 1]
+    elif direction == "pickfeed":
+        idx = round(spec.n / 2) if index is None else index
+        if not j_lo <= idx <= j_hi:
+            raise DomainError(f"pick-feed profile index {idx} outside roi rows {j_lo}..{j_hi}")
+        start, length, step = i_lo * (spec.n + 1) + idx, i_hi - i_lo + 1, spec.n + 1
+        positions = spec.x_coords()[i_lo:i_hi + 1]
+    else:
+        raise DomainError(f"direction must be 'feed' or 'pickfeed', got {direction!r}")
+    if field.on_device:
+        h = field.device_heights()
+        heights = h[start: start + (length - 1) * step + 1: step].cpu().numpy()
+    else:
+        heights = field.heights[start: start + (length - 1) * step + 1: step].copy()
+    if np.any(heights >= field.initial_height_mm):
+        raise DomainError(f"{direction} profile at index {idx} crosses uncut cells")
+    return LineProfile(direction=direction, index=idx, positions_mm=positions.copy(),
+                       heights_mm=heights, spacing_mm=spec.spacing_mm)
+
+
+def _profiles_device(h_dev, n_surf, surf_stride, starts, length, step, sentinels_dev, exclude,
+                     stats_in=None):
+    """One msurf_profiles launch; returns the [n_surf, n_prof, 8] rows on the host."""
+    torch = _native.require_cuda()
+    lib = _native.lib()
+    dev = h_dev.device
+    n_prof = len(starts)
+    st = torch.tensor(np.asarray(starts, dtype=np.int64), device=dev)
+    out = torch.empty(n_surf * n_prof * 8, dtype=torch.float64, device=dev)
+    _native.check(lib.msurf_profiles(h_dev.data_ptr(), surf_stride, n_surf, st.data_ptr(), n_prof,
+                                     length, step, sentinels_dev.data_ptr(), int(exclude),
+                                     stats_in.data_ptr() if stats_in is not None else None,
+                                     out.data_ptr(), _native.stream_ptr()))
+    return out
+
+
+def _finish_profile(row, idx, uncut) -> ProfileRoughness:
+    s, n, n_unc, zmax, zmin, sabs = row[:6]
+    if uncut == "raise" and n_unc > 0:
+        raise DomainError(f"profile at index {idx} crosses uncut cells")
+    if n < 2:
+        raise DomainError("line roughness needs at least 2 samples")
+    mean = s / n
+    rp, rv = float(zmax - mean), float(-(zmin - mean))
+    return ProfileRoughness(index=int(idx), ra_um=float(sabs / n), rz_um=rp + rv, rp_um=rp, rv_um=rv,
+                            sample_count=int(n))
+
+
+def profile_roughness(field: HeightField, indices=None, direction: str = "feed", every: int | None = None,
+                      roi=None, uncut: str = "raise"):
+    """Ra and Rz of many profiles in one launch. ``every=64`` takes every 64th
+    feed profile (fixed x index i = 0, 64, 128, ...) inside the ROI."""
+    spec = field.spec
+    i_lo, j_lo, i_hi, j_hi = _check_roi(spec, roi)
+    if direction == "feed":
+        if indices is None:
+            indices = list(range(i_lo, i_hi + 1, every)) if every else [round(spec.m / 2)]
+        for idx in indices:
+            if not i_lo <= idx <= i_hi:
+                raise DomainError(f"feed profile index {idx} outside roi columns {i_lo}..{i_hi}")
+        starts = [idx * (spec.n + 1) + j_lo for idx in indices]
+        length, step = j_hi - j_lo + 1, 1
+    elif direction == "pickfeed":
+        if indices is None:
+            indices = list(range(j_lo, j_hi + 1, every)) if every else [round(spec.n / 2)]
+        for idx in indices:
+            if not j_lo <= idx <= j_hi:
+                raise DomainError(f"pick-feed profile index {idx} outside roi rows {j_lo}..{j_hi}")
+        starts = [i_lo * (spec.n + 1) + idx for idx in indices]
+        length, step = i_hi - i_lo + 1, spec.n + 1
+    else:
+        raise DomainError(f"direction must be 'feed' or 'pickfeed', got {direction!r}")
+    torch = _native.require_cuda()
+    h = field.device_heights()
+    sent = _sentinel_tensor(torch, [field.initial_height_mm], h.device)
+    rows = _profiles_device(h, 1, 0, starts, length, step, sent, uncut == "exclude")
+    rows = rows.cpu().numpy().reshape(len(indices), 8)
+    return [_finish_profile(r, idx, uncut) for r, idx in zip(rows, indices)]
+
+
+def line_roughness(profile: LineProfile) -> float:
+    """Ra of a profile in µm (roughness.py:183-188), reduced on the device."""
+    if profile.heights_mm.size < 2:
+        raise DomainError("line roughness needs at least 2 samples")
+    torch = _native.require_cuda()
+    h = torch.from_numpy(np.ascontiguousarray(profile.heights_mm, dtype=np.float64)).cuda()
+    sent = _sentinel_tensor(torch, [np.inf], h.device)
+    row = _profiles_device(h, 1, 0, [0], h.numel(), 1, sent, False).cpu().numpy()
+    return float(row[5] / row[1])

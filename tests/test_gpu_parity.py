@@ -1,0 +1,164 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference goldens
+and the CPU oracles. Heights: bit-exact (tolerance 0). Roughness: 1e-9
+relative (north-star gate 0.1 %). Requires a B200 and the built libmsurf.so."""
+
+import math
+from types import SimpleNamespace as NS
+
+import numpy as np
+import pytest
+
+import golden_io
+import paper_2603_28160_b200 as ms
+from oracle import fsm_ext_oracle as xorc
+from oracle import fsm_oracle as orc
+from test_host_cpu import EXT_CASES, _ext_cfg
+
+pytestmark = pytest.mark.gpu
+CASES = golden_io.case_names()
+REL = 1e-9
+
+
+def _rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+@pytest.mark.parametrize("trig", ["device", "host"])
+@pytest.mark.parametrize("name", CASES)
+def test_heights_bitexact_vs_reference_goldens(name, trig):
+    g = golden_io.load(name)
+    cfg = golden_io.product_config(g["config"])
+    res = ms.simulate(cfg, trig=trig)
+    assert res.time_steps == g["counters"]["time_steps"]
+    assert res.trajectory_points == g["counters"]["trajectory_points"]
+    assert res.cells_updated == g["counters"]["cells_updated"]
+    h = res.field.heights
+    assert golden_io.heights_match(g, h), golden_io.max_abs_diff(g, h, cfg.grid.n + 1)
+    if "traj" in g:
+        tr = g["traj"]
+        rec = res.trajectory
+        assert rec is not None and len(rec) == tr.shape[1]
+        assert np.array_equal(rec.t_s, tr[0]) and np.array_equal(rec.tooth, tr[1].astype(np.int64))
+        assert np.array_equal(rec.z_mm, tr[4])
+        if trig == "host":
+            assert np.array_equal(rec.x_mm, tr[2]) and np.array_equal(rec.y_mm, tr[3])
+        else:
+            assert np.max(np.abs(rec.x_mm - tr[2])) < 1e-12 and np.max(np.abs(rec.y_mm - tr[3])) < 1e-12
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_roughness_vs_reference_goldens(name):
+    g = golden_io.load(name)
+    rough = g["roughness"]
+    res = ms.simulate(golden_io.product_config(g["config"]))
+    if rough.get("areal"):
+        am = ms.areal_metrics(res.field, roi=tuple(rough["roi"]))
+        ref = rough["areal"]
+        got = am.to_json_dict()
+        for k in ("Sa_um", "Sq_um", "Sp_um", "Sv_um", "Sz_um", "Ssk", "Sku"):
+            if ref[k] is None:
+                assert got[k] is None
+            else:
+                assert _rel(got[k], ref[k]) < REL or abs(got[k] - ref[k]) < 1e-12, (k, got[k], ref[k])
+        assert got["cell_count"] == ref["cell_count"]
+    if "Ra" in rough:
+        i_lo, j_lo, i_hi, j_hi = rough["roi"]
+        prof = ms.extract_profile(res.field, "feed", index=rough["profile_index"], roi=tuple(rough["roi"]))
+        assert _rel(ms.line_roughness(prof), rough["Ra"]) < REL
+        pr = ms.profile_roughness(res.field, indices=[rough["profile_index"]], roi=tuple(rough["roi"]))[0]
+        assert _rel(pr.ra_um, rough["Ra"]) < REL
+    if "areal_full_error" in rough:
+        with pytest.raises(ms.DomainError):
+            ms.areal_metrics(res.field)
+    elif "areal_full" in rough:
+        am = ms.areal_metrics(res.field)
+        assert _rel(am.sa_um, rough["areal_full"]["Sa_um"]) < REL
+
+
+@pytest.mark.parametrize("case", sorted(EXT_CASES))
+@pytest.mark.parametrize("trig", ["device", "host"])
+def test_extended_model_bitexact_vs_ext_oracle(case, trig):
+    kw = EXT_CASES[case]
+    cfg = _ext_cfg(kw.get("profile", "insert"))
+    res = ms.simulate(cfg, ms.Extensions(**kw), trig=trig)
+    h_ref, p, ctr, _ = xorc.ext_sweep(cfg, NS(**kw), workers=4)
+    h = res.field.heights
+    assert res.trajectory_points == ctr["trajectory_points"]
+    assert res.cells_updated == ctr["cells_updated"]
+    assert np.array_equal(h, h_ref), float(np.max(np.abs(h - h_ref)))
+    assert res.counters["deposits"] == ctr["deposits"]
+
+
+def test_force_extended_equals_reference_on_goldens():
+    for name in CASES:
+        g = golden_io.load(name)
+        cfg = golden_io.product_config(g["config"], record_trajectory=False)
+        res = ms.simulate(cfg, ms.Extensions(force_extended=True))
+        assert golden_io.heights_match(g, res.field.heights), name
+
+
+def test_batched_equals_individual():
+    names = ["small_0", "small_3", "tiny", "small_1004", "config1_ref"]
+    cfgs = [golden_io.product_config(golden_io.load(n)["config"], record_trajectory=False) for n in names]
+    batch = ms.simulate_batch(cfgs)
+    for n, r in zip(names, batch):
+        assert golden_io.heights_match(golden_io.load(n), r.field.heights), n
+
+
+def test_batched_ext_same_shape_and_metrics():
+    cfg = _ext_cfg("ball")
+    exts = [ms.Extensions(profile="ball", helix_angle_rad=math.radians(20 + 5 * k),
+                          runout_offset_mm=0.001 * k, runout_phase_rad=0.7 * k) for k in range(6)]
+    batch = ms.simulate_batch([cfg] * 6, exts)
+    mets = ms.areal_metrics_batch([b.field for b in batch], uncut="exclude")
+    for e, b, m in zip(exts, batch, mets):
+        kw = {k: getattr(e, k) for k in ("profile", "helix_angle_rad", "runout_offset_mm", "runout_phase_rad")}
+        h_ref, p, _, _ = xorc.ext_sweep(cfg, NS(**kw), workers=2)
+        assert np.array_equal(b.field.device_heights().cpu().numpy(), h_ref)
+        exp = orc.areal_metrics(h_ref.reshape(p.m + 1, p.n + 1), p.initial_height, uncut="exclude")
+        assert _rel(m.sa_um, exp["Sa"]) < REL and _rel(m.sku, exp["Sku"]) < REL
+
+
+def test_profiles_ra_rz_every_k_rows():
+    kw = EXT_CASES["ball_noise"]
+    cfg = _ext_cfg("ball")
+    res = ms.simulate(cfg, ms.Extensions(**kw))
+    h_ref, p, _, _ = xorc.ext_sweep(cfg, NS(**kw), workers=2)
+    a2 = h_ref.reshape(p.m + 1, p.n + 1)
+    prs = ms.profile_roughness(res.field, every=16, uncut="exclude")
+    assert [q.index for q in prs] == list(range(0, p.m + 1, 16))
+    for q in prs:
+        exp = orc.profile_roughness(a2[q.index], p.initial_height, uncut="exclude")
+        assert _rel(q.ra_um, exp["Ra"]) < REL and _rel(q.rz_um, exp["Rz"]) < REL
+
+
+def test_no_engagement_and_edge_cases():
+    g = golden_io.load("tiny")
+    d = g["config"]
+    proc = dict(d["process"])
+    proc["initial_position_mm"] = [100.0, None, 0.0]
+    d2 = dict(d, process=proc)
+    res = ms.simulate(golden_io.product_config(d2))
+    assert res.cells_updated == 0
+    assert np.all(res.field.heights == res.field.initial_height_mm)
+    with pytest.raises(ms.DomainError):
+        ms.areal_metrics(res.field)
+    # 1-cell grid, odd point counts, large N (> 2048 -> several mask words)
+    for n_pts, spacing in ((2, 0.3), (33, 0.05), (2500, 0.004)):
+        cfg = golden_io.product_config(d, edge_point_count=n_pts, record_trajectory=False,
+                                       grid=ms.GridSpec(spacing, -0.2, 0.0, 1 if spacing == 0.3 else 40, 1 if spacing == 0.3 else 30))
+        res = ms.simulate(cfg)
+        h_ref, _, ctr, _ = orc.sweep(cfg, workers=2)
+        assert np.array_equal(res.field.heights, h_ref)
+        assert res.counters["deposits"] == ctr["deposits"]
+
+
+def test_heightfield_device_roundtrip_and_merge():
+    g = golden_io.load("small_3")
+    cfg = golden_io.product_config(g["config"], record_trajectory=False)
+    a = ms.simulate(cfg).field
+    b = ms.simulate(cfg).field
+    a.merge_min(b)
+    assert golden_io.heights_match(g, a.heights)
+    c = a.copy()
+    assert np.array_equal(c.heights, a.heights)

@@ -1,0 +1,212 @@
+"""CPU-only tests: C-ABI library loads and exports every declared symbol,
+the host planner reproduces the reference plan bit-exactly (vs the oracle,
+itself pinned to the reference goldens), the extended planner equals the
+extended oracle, key encoding is order-preserving, samplers are bit-exact,
+and configuration errors raise the reference's exception types."""
+
+import ctypes
+import math
+import os
+import re
+from types import SimpleNamespace as NS
+
+import numpy as np
+import pytest
+
+import golden_io
+import paper_2603_28160_b200 as ms
+from paper_2603_28160_b200 import _native, planner
+from oracle import fsm_ext_oracle as xorc
+from oracle import fsm_oracle as orc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CASES = golden_io.case_names()
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _native.load_library()
+    header = open(os.path.join(ROOT, "include", "msurf.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(msurf_\w+)\s*\(", header, re.M))
+    assert declared, "no declarations parsed"
+    assert declared == set(_native.EXPORTS), declared ^ set(_native.EXPORTS)
+    for name in declared:
+        assert getattr(lib, name) is not None
+    assert lib.msurf_abi_version() == _native.ABI_VERSION
+    assert lib.msurf_sizeof_job() == ctypes.sizeof(_native.MsurfJob)
+    assert lib.msurf_tile_steps() == 256
+
+
+def test_error_path_without_gpu_reports_message():
+    lib = _native.load_library()
+    assert lib.msurf_sweep(None, 0, None, 0, 0, 1, None) != 0
+    assert b"bad arguments" in lib.msurf_last_error()
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_ref_plan_matches_oracle_plan(name):
+    g = golden_io.load(name)
+    cfg = golden_io.product_config(g["config"])
+    p = planner.plan(cfg)
+    o = orc.plan(golden_io.namespace_config(g["config"]))
+    assert p.mode == planner.MODE_REF
+    assert (p.steps, p.points, p.teeth) == (o.steps, o.points, o.teeth)
+    assert p.dt == o.dt and p.t_start == o.t_start and p.y0 == o.y0
+    assert p.initial_height == o.initial_height == g["counters"]["initial_height"]
+    assert p.trajectory_points == g["counters"]["trajectory_points"]
+    assert np.array_equal(p.px, o.xp) and np.array_equal(p.pz, o.zp)
+    for k in range(p.teeth):
+        assert np.array_equal(p.zw[k], o.zw[k])
+        assert p.min_index[k] == o.min_index[k]
+        e = o.rows[k]
+        assert list(p.tooth_rows[k]) == [e[0][0], e[0][1], e[0][2], e[0][3], e[1][0], e[1][1], e[1][2], e[1][3]]
+        assert p.tooth_base[k] == orc.tooth_base(cfg.process.phase_rad, k + 1, p.teeth)
+    assert np.array_equal(planner.decode_keys(p.zkey), p.zw + 0.0)
+    # chunk boxes enclose the tool-frame points
+    nchunk = (p.points + 31) // 32
+    assert p.chunk_box.shape == (p.teeth, nchunk, 6)
+
+
+EXT_CASES = {
+    "helix_insert": dict(helix_angle_rad=math.radians(30)),
+    "ball_tilt": dict(profile="ball", tilt_rad=math.radians(15), helix_angle_rad=math.radians(30),
+                      runout_offset_mm=0.005, runout_phase_rad=math.radians(40), passes=3, stepover_mm=0.3),
+    "vib_runout": dict(runout_offset_mm=0.003, vib_amplitude_mm=0.002, vib_frequency_hz=300.0),
+    "ball_noise": dict(profile="ball", tilt_rad=math.radians(10), runout_offset_mm=0.004,
+                       noise_sigma_mm=0.001, noise_corr_mm=0.02, noise_seed=7),
+}
+
+
+def _ext_cfg(profile="insert"):
+    if profile == "ball":
+        tool = ms.ToolDefinition(cutting_diameter_mm=6.0, insert_radius_mm=3.0, tooth_count=2)
+        proc = ms.derive_kinematics(tooth_count=2, cutting_diameter_mm=6.0, depth_of_cut_mm=0.2,
+                                    spindle_speed_rpm=6000.0, feed_per_tooth_mm=0.08,
+                                    initial_position_mm=(-0.3, None, 0.0))
+        grid = ms.GridSpec.from_nodes(0.01, -0.5, 0.0, 101, 81)
+        return ms.SimulationConfig(tool=tool, process=proc, grid=grid, edge_point_count=77,
+                                   time_step_s=(2 * math.pi / 720) / proc.angular_velocity_rad_s)
+    tool = ms.ToolDefinition(cutting_diameter_mm=10.0, insert_radius_mm=5.0, tooth_count=4)
+    proc = ms.derive_kinematics(tooth_count=4, cutting_diameter_mm=10.0, depth_of_cut_mm=1.0,
+                                spindle_speed_rpm=3000.0, feed_per_tooth_mm=0.05,
+                                initial_position_mm=(0.0, -2.0, 0.0))
+    grid = ms.GridSpec.from_nodes(0.02, -0.99, 0.0, 100, 100)
+    om = proc.angular_velocity_rad_s
+    return ms.SimulationConfig(tool=tool, process=proc, grid=grid, edge_point_count=61,
+                               time_step_s=(2 * math.pi / 720) / om, span_s=(0.0, 4 * 2 * math.pi / om))
+
+
+@pytest.mark.parametrize("case", sorted(EXT_CASES))
+def test_ext_plan_matches_ext_oracle(case):
+    kw = EXT_CASES[case]
+    cfg = _ext_cfg(kw.get("profile", "insert"))
+    ext = ms.Extensions(**kw)
+    p = planner.plan(cfg, ext)
+    o = xorc.ext_plan(cfg, NS(**kw))
+    assert p.mode == (planner.MODE_EXT_TILT if kw.get("tilt_rad") else planner.MODE_EXT)
+    assert (p.steps, p.points, p.teeth) == (o.steps, o.points, o.teeth)
+    assert p.y0 == o.y0 and p.dt == o.dt
+    assert np.array_equal(p.px, o.xt) and np.array_equal(p.py, o.yt) and np.array_equal(p.pz, o.zt)
+    assert np.array_equal(p.zw, o.zw) and p.zoff == o.zoff
+    assert list(p.pass_x0) == list(o.pass_x0)
+    assert (p.tilt_c, p.tilt_s, p.vib_amp, p.vib_omega, p.vib_phase) == \
+        (o.tilt_c, o.tilt_s, o.vib_amp, o.vib_omega, o.vib_phase)
+    assert list(p.tooth_base) == list(o.base)
+
+
+def test_ext_zero_formulation_is_reference_on_goldens():
+    # the extended formulation with every extension at zero reproduces the
+    # reference bit-exactly on the reference's own golden cases
+    for name in CASES:
+        g = golden_io.load(name)
+        cfg = golden_io.namespace_config(g["config"])
+        h, _, _, _ = xorc.ext_sweep(cfg, NS(force_extended=True), workers=4)
+        assert golden_io.heights_match(g, h), name
+
+
+def test_key_encoding_is_order_preserving():
+    rng = np.random.default_rng(3)
+    z = np.concatenate([rng.normal(0, 1, 5000), rng.normal(0, 1e-300, 100), [0.0, -0.0, 1e308, -1e308,
+                                                                             5e-324, -5e-324]])
+    k = planner.encode_keys(z)
+    order_z = np.argsort(z, kind="stable")
+    assert np.all(np.diff(k[order_z].astype(np.float64)) >= 0) or np.all(k[order_z][1:] >= k[order_z][:-1])
+    assert np.array_equal(planner.decode_keys(k), z + 0.0)
+    assert planner.encode_keys(np.array([-0.0]))[0] == planner.encode_keys(np.array([0.0]))[0]
+
+
+def test_lhs_bit_exact_with_reference_goldens():
+    z = np.load(os.path.join(golden_io.GOLDEN, "lhs.npz"))
+    names = ["cutting_speed_m_min", "feed_per_tooth_mm", "depth_of_cut_mm", "grid_spacing_mm",
+             "radial_rake_deg", "phase_deg"]
+    ranges = [ms.ParameterRange(n, *b) for n, b in zip(names, z["bounds"])]
+    for key in z.files:
+        if key.startswith("lhs_"):
+            _, count, seed = key.split("_")
+            assert np.array_equal(ms.lhs_sample(ranges, int(count), int(seed)), z[key])
+
+
+def test_uniform_sampler_shape_and_bounds():
+    ranges = [ms.ParameterRange("feed_per_tooth_mm", 0.02, 0.2), ms.ParameterRange("spindle_speed_rpm", 2000, 12000)]
+    s = ms.uniform_sample(ranges, 256, 0)
+    assert s.shape == (256, 2)
+    assert s[:, 0].min() >= 0.02 and s[:, 0].max() <= 0.2
+    assert np.array_equal(s, ms.uniform_sample(ranges, 256, 0))
+
+
+def test_reference_error_types():
+    with pytest.raises(ms.ConfigError):
+        ms.ParameterRange("helix", 0, 1)
+    with pytest.raises(ms.DomainError):
+        ms.ToolDefinition(cutting_diameter_mm=-1, insert_radius_mm=1, tooth_count=1)
+    with pytest.raises(ms.ConfigError):
+        ms.derive_kinematics(tooth_count=2, cutting_diameter_mm=10, depth_of_cut_mm=1)
+    g = golden_io.load("tiny")
+    cfg = golden_io.product_config(g["config"], time_step_s=-1.0)
+    with pytest.raises(ms.ConfigError):
+        planner.plan(cfg)
+    cfg = golden_io.product_config(g["config"], span_s=(0.0, 0.01))
+    with pytest.raises(ms.ConfigError):  # explicit span needs y0 (engine.py:166-167)
+        planner.plan(cfg)
+    cfg = golden_io.product_config(g["config"], worker_count=0)
+    with pytest.raises(ms.ConfigError):
+        planner.plan(cfg)
+    assert issubclass(ms.DomainError, ValueError) and issubclass(ms.ConfigError, ms.MillsurfError)
+
+
+def test_time_step_kats():
+    # test_engine.py:31-42
+    g = golden_io.load("tiny")
+    cfg = golden_io.product_config(g["config"], time_step_s=None)
+    dt = ms.time_step(cfg)
+    assert dt == pytest.approx(1.5400e-5, rel=1e-4)
+    assert dt == math.radians(0.5) / cfg.process.angular_velocity_rad_s
+
+
+def test_locate_kats():
+    spec = ms.GridSpec(0.01, 0.0, 0.0, 10, 10)
+    assert ms.locate(0.012, 0.0, spec) == (1, 0)
+    assert ms.locate(-0.006, 0.0, spec) is None
+    assert ms.locate(0.005, 0.0, spec) == (1, 0)
+
+
+def test_host_heightfield_semantics():
+    spec = ms.GridSpec(0.1, 0.0, 0.0, 3, 2)
+    f = ms.HeightField(spec, 0.5)
+    assert ms.update_min(f, (1, 1), 0.1) and not ms.update_min(f, (1, 1), 0.1)
+    assert f.machined_cell_count() == 1
+    g = ms.HeightField(spec, 0.5)
+    ms.update_min(g, (0, 0), 0.2)
+    f.merge_min(g)
+    assert f.machined_cell_count() == 2
+    with pytest.raises(ms.DomainError):
+        ms.update_min(f, (4, 0), 0.0)
+
+
+def test_device_required_no_cpu_fallback(monkeypatch):
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    g = golden_io.load("tiny")
+    with pytest.raises(ms.NativeUnavailableError):
+        ms.simulate(golden_io.product_config(g["config"]))

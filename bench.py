@@ -1,0 +1,398 @@
+"""Benchmark of the B200 FSM hot path (BASELINE.json metric: edge-point
+updates/s and surfaces/s at 1/2/4/8 B200, % of roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+A "step" is one pass of the hot path over one surface: Z-map init, the
+sweep of every (pass, step, tooth, edge point), key decode, areal roughness
+(two passes) and Ra/Rz of every 64th feed profile. Default workload is
+BASELINE configs[1] (config 2: ball-end raster). N>1 (torchrun, one rank
+per GPU, NCCL) shards the surface into feed-direction strips: the total
+work is fixed ("scaling": "strong") and the only collective is the
+all-reduce of the partial roughness moments.
+
+``value`` is device-timed (CUDA events, inputs resident in HBM, L2 flushed
+between steps, max over ranks); ``e2e`` goes through the public API
+(simulate + areal_metrics + profile_roughness + the height map read back)
+with host planning and host<->device copies inside the timed region.
+``--impl reference`` times the reference algorithm's CPU restatement
+(oracle/, all host threads) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "edge-point updates/s"
+UNIT = "updates/s"
+# algorithmic FP64 operations per evaluated edge point:
+# affine/rotation + feed/offset adds + cell location (2 x [sub, div, add, floor])
+FLOPS_PER_POINT = {0: 20, 1: 16, 2: 23}
+FLOPS_PER_ROW = 2 * 60 + 32  # 2*C_trig + 32, C_trig ~ 60 ops (double-double sincos)
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def workload(cfg_id: int):
+    from paper_2603_28160_b200 import configs
+
+    if cfg_id not in configs.FACTORIES:
+        raise SystemExit(f"--config {cfg_id}: choose one of {sorted(configs.FACTORIES)} (3 is the batch bench)")
+    cfg, ext, meta = configs.FACTORIES[cfg_id]()
+    return cfg, ext, meta
+
+
+def describe(cfg, ext, meta, plan, world):
+    g = cfg.grid
+    return {
+        "workload": f"{meta['name']} (BASELINE configs[{int(meta['name'][-1]) - 1}])",
+        "tool": f"{'ball' if ext and ext.profile == 'ball' else 'flat(insert D=2R)'} R={cfg.tool.insert_radius_mm} "
+                f"Z={cfg.tool.tooth_count}",
+        "grid_nodes": [g.m + 1, g.n + 1], "spacing_mm": g.spacing_mm,
+        "edge_points": plan.points, "time_steps_per_pass": plan.steps, "passes": plan.passes,
+        "steps_per_rev": round(2 * math.pi / (plan.omega * plan.dt)),
+        "edge_point_updates_per_surface": plan.trajectory_points,
+        "outputs": "heights + Sa/Sq/Sp/Sv/Sz/Ssk/Sku + Ra/Rz every 64th feed profile (uncut cells excluded)",
+        "parallelism": f"feed strips x{world}" if world > 1 else "single GPU",
+        "l2": "flushed between timed steps (256 MiB write)",
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+def profiled_traffic(cfg_name):
+    """dram bytes per sweep launch from the committed ncu capture (profiles/)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get(cfg_name)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------- CPU legs
+def cpu_sample(cfg, ext, plan, target_s: float = 12.0, threads: int | None = None):
+    """Bounded sample of the same workload on the host cores with the CPU
+    restatement of the reference algorithm (oracle/fsm_ext_oracle.py): step
+    windows spread evenly over the first pass, sized for ~target_s of work."""
+    from types import SimpleNamespace as NS
+
+    from oracle import fsm_ext_oracle as xorc
+
+    threads = threads or os.cpu_count() or 1
+    ext_ns = ext  # duck-typed: the oracle reads extension fields by name
+    steps = plan.steps
+    n_win = 16
+
+    def run(win_len):
+        wins = [(int(round((k + 0.5) * steps / n_win - win_len / 2)),
+                 int(round((k + 0.5) * steps / n_win + win_len / 2))) for k in range(n_win)]
+        t0 = time.perf_counter()
+        _, _, ctr, _ = xorc.ext_sweep(cfg, ext_ns, workers=threads, windows=wins, pass_limit=1)
+        return ctr["trajectory_points"], time.perf_counter() - t0
+
+    win = max(8, steps // 2000)
+    pts, dt = run(win)
+    if dt < target_s / 4:
+        win = min(steps // n_win, int(win * max(1.0, target_s / max(dt, 1e-3) * 0.8)))
+        pts, dt = run(win)
+    return {"value": pts / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"first pass, {n_win} step windows x {win} steps spread over {steps} steps "
+                      f"({pts} edge-point updates in {dt:.2f} s, oracle/fsm_ext_oracle.py, "
+                      f"{threads} threads)"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cfg, ext, meta = workload(args.config)
+    from paper_2603_28160_b200.planner import plan as make_plan
+
+    p = make_plan(cfg, ext)
+    vals = []
+    sample = None
+    for i in range(args.warmup + args.steps):
+        cb = cpu_sample(cfg, ext, p, target_s=args.cpu_seconds)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+            sample = cb
+    v = statistics.median(vals)
+    sample["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * p.trajectory_points / v, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": describe(cfg, ext, meta, p, 1),
+            "surfaces_per_s": v / p.trajectory_points,
+            "cpu_baseline": sample,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU leg
+def run_ours(args, rank, world):
+    import numpy as np
+    import torch
+
+    import paper_2603_28160_b200 as ms
+    from paper_2603_28160_b200 import _native, sharded
+    from paper_2603_28160_b200.engine import SweepBatch
+    from paper_2603_28160_b200.planner import plan as make_plan
+
+    dist = torch.distributed
+    local = _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    cfg, ext, meta = workload(args.config)
+    p = make_plan(cfg, ext)
+    uncut = meta["uncut"]
+    every = meta.get("profiles_every", 64)
+    j_lo, j_hi = sharded.strip_bounds(p.grid.n + 1, world)[rank]
+    batch = SweepBatch([(p, j_lo, j_hi)])
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step(events):
+        batch.launch(events=events)
+        res = sharded.StripResult(plan=p, j_lo=j_lo, j_hi=j_hi, heights=batch.heights()[0], counters={},
+                                  cells_updated=0, main_loop_seconds=0.0, batch=batch)
+        am = sharded.areal_metrics_strip(res, uncut=uncut, group=group)
+        prs = sharded.profile_roughness_strip(res, every=every, uncut=uncut, group=group)
+        return am, prs
+
+    # warm-up
+    for _ in range(args.warmup):
+        step(None)
+    torch.cuda.synchronize()
+    ctr, machined = batch.counters()
+
+    # timed region: K steps, each bracketed by CUDA events; L2 flushed between
+    clocks = ClockSampler(local)
+    clocks.start()
+    step_ms, sweep_ms = [], []
+    launches = 0
+    barrier()
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        flush.fill_(1)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e_end = torch.cuda.Event(enable_timing=True)
+        am, prs = step(ev)
+        e_end.record()
+        torch.cuda.synchronize()
+        step_ms.append(ev[0].elapsed_time(e_end))
+        sweep_ms.append(ev[1].elapsed_time(ev[2]))
+        launches += batch.launches_per_run + 2 + 2 + 2  # areal 2x(pass+finalize), profiles 2
+    barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ctr, machined = batch.counters()
+
+    tot = torch.tensor([sum(step_ms), sum(sweep_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms_per_step = float(tot[0]) / args.steps
+    sweep_ms_avg = float(tot[1]) / args.steps
+    p_total = p.trajectory_points
+    value = p_total / (ms_per_step * 1e-3)
+
+    # ---- roofline of the dominant kernel (the sweep), this rank's launch
+    mode = p.mode
+    evald = int(ctr[0][1])
+    live = int(ctr[0][0])
+    flops = FLOPS_PER_POINT[mode] * evald + FLOPS_PER_ROW * live
+    lib = _native.lib()
+    import ctypes
+
+    r = ctypes.c_double(0.0)
+    _native.check(lib.msurf_microbench(0, ctypes.byref(r)))
+    fp64_peak = r.value
+    _native.check(lib.msurf_microbench(2, ctypes.byref(r)))
+    atom_peak = r.value
+    achieved = flops / (sweep_ms_avg * 1e-3)
+    roofline = {
+        "bound": "fp64", "achieved": achieved / 1e12, "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
+        "frac": achieved / fp64_peak,
+        "traffic": profiled_traffic(meta["name"]),
+        "kernel": "sweep_kernel<MODE>", "sweep_ms": sweep_ms_avg,
+        "peak_source": "measured in this run: msurf_microbench(0), non-FMA DADD/DMUL issue rate "
+                       "(MEASURED_PEAKS.json has no FP64 entry)",
+        "flops_per_launch": flops,
+        "flops_model": f"{FLOPS_PER_POINT[mode]} x points_evaluated + {FLOPS_PER_ROW} x live rows",
+        "points_evaluated": evald, "live_rows": live, "deposits": int(ctr[0][2]),
+        "atomics": int(ctr[0][3]),
+        "atomic_rate_per_s": int(ctr[0][3]) / (sweep_ms_avg * 1e-3),
+        "atomic_peak_per_s": atom_peak,
+        "hbm": {"bytes_per_step": 24 * (p.grid.m + 1) * (j_hi - j_lo + 1) + 8 * int(ctr[0][3]),
+                "peak_gbs": measured_peaks().get("hbm_gbs")},
+    }
+
+    # ---- e2e through the public API with host buffers
+    e2e_ms = []
+    h2d = d2h = 0
+    for i in range(args.warmup + args.steps):
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if world == 1:
+            res = ms.simulate(cfg, ext)
+            am = ms.areal_metrics(res.field, uncut=uncut)
+            prs = ms.profile_roughness(res.field, every=every, uncut=uncut)
+            hh = res.field.heights
+            nbytes = hh.nbytes
+        else:
+            sres = sharded.simulate_strip(cfg, ext, rank, world)
+            am = sharded.areal_metrics_strip(sres, uncut=uncut, group=group)
+            prs = sharded.profile_roughness_strip(sres, every=every, uncut=uncut, group=group)
+            hh = sres.heights.cpu().numpy()
+            nbytes = hh.nbytes
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            e2e_ms.append(dt * 1e3)
+        h2d = batch.h2d_bytes
+        d2h = nbytes + 8 * (9 + 8 * len(prs) + 5)
+    et = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_step = float(et[0]) / args.steps
+    e2e = {"value": p_total / (e2e_step * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_step,
+           "api": "simulate + areal_metrics + profile_roughness + HeightField.heights"
+           if world == 1 else "sharded.simulate_strip + areal/profile all-reduce + strip read-back"}
+
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_sample(cfg, ext, p, target_s=args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": describe(cfg, ext, meta, p, world),
+            "surfaces_per_s": 1e3 / ms_per_step,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk,
+            "metrics": {"Sa_um": am.sa_um, "Sq_um": am.sq_um, "Sz_um": am.sz_um, "Ssk": am.ssk,
+                        "Sku": am.sku, "cells": am.cell_count,
+                        "Ra_um_mean": float(np.mean([q.ra_um for q in prs])),
+                        "Rz_um_mean": float(np.mean([q.rz_um for q in prs])), "profiles": len(prs)},
+            "machined_cells_rank0": int(machined[0]),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(_env_int("LOCAL_RANK", 0))
+        dist.init_process_group("nccl")
+    try:
+        run_ours(args, rank, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

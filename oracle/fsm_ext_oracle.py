@@ -304,10 +304,11 @@ def _ext_range(p: ExtPlan, x0p, lo_step, hi_step, heights, counters):
     counters["deposits"] = counters.get("deposits", 0) + deposits
 
 
-def ext_sweep(cfg, ext=None, workers=1, step_limit=None):
+def ext_sweep(cfg, ext=None, workers=1, step_limit=None, windows=None, pass_limit=None):
     """Extended sweep over all passes. Returns (heights, plan, counters, wall).
-    ``step_limit`` truncates every pass to its first steps (bounded CPU-baseline
-    samples only)."""
+    Bounded CPU-baseline samples only: ``step_limit`` truncates every pass to
+    its first steps; ``windows`` = [(lo, hi), ...] sweeps only those step
+    ranges; ``pass_limit`` only the first passes (extended path only)."""
     passes = int(_get(ext, "passes", 1))
     if not kinematic_extensions_active(ext):
         base = ref.plan(cfg)
@@ -332,10 +333,20 @@ def ext_sweep(cfg, ext=None, workers=1, step_limit=None):
 
     p = ext_plan(cfg, ext)
     steps = p.steps if step_limit is None else min(p.steps, step_limit)
-    w = max(1, min(workers, steps))
-    bounds = [round(i * steps / w) for i in range(w + 1)]
-    tasks = [(x0p, bounds[i], bounds[i + 1]) for x0p in p.pass_x0 for i in range(w)
-             if bounds[i] < bounds[i + 1]]
+    pass_x0 = p.pass_x0 if pass_limit is None else p.pass_x0[:pass_limit]
+    if windows is None:
+        windows = [(0, steps)]
+    w = max(1, workers)
+    tasks = []
+    for x0p in pass_x0:
+        for lo, hi in windows:
+            lo, hi = max(0, lo), min(hi, steps)
+            if hi <= lo:
+                continue
+            k = max(1, min(w, hi - lo))
+            b = [lo + round(i * (hi - lo) / k) for i in range(k + 1)]
+            tasks += [(x0p, b[i], b[i + 1]) for i in range(k) if b[i] < b[i + 1]]
+    sampled = sum(hi - lo for _, lo, hi in tasks) // max(1, len(pass_x0))
     nf = min(w, len(tasks))
     fields = [np.full((p.m + 1) * (p.n + 1), p.initial_height) for _ in range(nf)]
     ctrs = [dict() for _ in range(nf)]
@@ -355,7 +366,7 @@ def ext_sweep(cfg, ext=None, workers=1, step_limit=None):
     for other in fields[1:]:
         np.minimum(h, other, out=h)
     wall = time.perf_counter() - t0
-    counters = {"time_steps": steps, "trajectory_points": steps * p.teeth * p.points * len(p.pass_x0),
+    counters = {"time_steps": steps, "trajectory_points": sampled * p.teeth * p.points * len(pass_x0),
                 "cells_updated": int(np.count_nonzero(h < p.initial_height)),
                 "deposits": sum(c.get("deposits", 0) for c in ctrs)}
     return h, p, counters, wall

@@ -17,7 +17,7 @@ import numpy as np
 from .errors import MillsurfError, NativeUnavailableError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmsurf.so")
+LIB_PATH = os.environ.get("MSURF_LIB") or os.path.join(_HERE, "libmsurf.so")
 ABI_VERSION = 1
 NUM_CTRS = 4
 RED_BLOCKS = 256

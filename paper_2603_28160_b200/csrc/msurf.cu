@@ -61,34 +61,27 @@ __device__ __forceinline__ double dec_key(uint64_t k) {
 }
 
 // ---------------------------------------------------------- cell location
-// Reference: idx = floor((w - lo)/dd + 0.5) (engine.py:298-300,
-// surface_grid.py:85-86), true IEEE division. Fast path: tq ~= w*inv + c0
-// with c0 = 0.5 - lo*inv (one FMA; |error| < 1e-11 for |tq| < 2^21). If tq is
-// within 2^-30 of an integer the floor could differ, so those (rare) points
-// take the exact reference sequence. Result: bit-identical cell indices.
-__device__ __forceinline__ int cell_index(double w, double lo, double dd, double inv,
-                                          double c0) {
-  double tq = __fma_rn(w, inv, c0);
-  double fl = floor(tq);
-  const double d = __dsub_rn(tq, fl);
-  if (fabs(__dsub_rn(d, 0.5)) > 0.5 - kNearEps) {
-    tq = __dadd_rn(__ddiv_rn(__dsub_rn(w, lo), dd), 0.5);
-    fl = floor(tq);
-  }
-  // |fl| beyond int range saturates, which the unsigned range checks reject.
-  return __double2int_rz(fl);
+// Reference: idx = floor((w - lo)/dd + 0.5) with a true IEEE division
+// (engine.py:298-300, surface_grid.py:85-86).
+// Fast path: tq = fma(w, 1/dd, 0.5 - lo/dd) is within 1e-11 of the exact
+// quotient+0.5 for |tq| < 2^21. Adding 1.5*2^22 rounds tq to a multiple of
+// 2^-30 and leaves floor(tq) in mantissa bits [30, 52) and the fraction in
+// bits [0, 30): two DP ops plus integer ops instead of FRND/F2I. When the
+// fraction is within 2^-29 of an integer (or |tq| is out of range) the floor
+// could differ from the reference's, so those rare points take the exact
+// reference sequence. Result: bit-identical cell indices.
+__device__ __noinline__ int cell_index_exact(double w, double lo, double dd) {
+  const double tq = __dadd_rn(__ddiv_rn(__dsub_rn(w, lo), dd), 0.5);
+  return __double2int_rz(floor(tq));  // saturates far outside; range checks reject
 }
 
-__device__ __forceinline__ void flush_min(uint64_t* __restrict__ keys, long long idx,
-                                          uint64_t key, unsigned& n_atom) {
-  if (idx < 0) return;
-  // Stale-read skip: heights only decrease, so a cached (possibly stale,
-  // i.e. higher) value <= key proves the atomic would be a no-op.
-  const uint64_t cur = __ldca(reinterpret_cast<const unsigned long long*>(keys + idx));
-  if (cur > key) {
-    atomicMin(reinterpret_cast<unsigned long long*>(keys + idx), (unsigned long long)key);
-    ++n_atom;
-  }
+__device__ __forceinline__ int cell_index(double w, double lo, double dd, double inv, double c0) {
+  const double tq = __fma_rn(w, inv, c0);
+  const long long b = __double_as_longlong(__dadd_rn(tq, 0x1.8p22));
+  const unsigned f = (unsigned)b & 0x3fffffffu;
+  const bool ok = ((int)(b >> 52) == 1045) & ((f - 2u) <= 0x3fffffffu - 4u);
+  if (__builtin_expect(ok, 1)) return (int)((b & 0x000fffffffffffffLL) >> 30) - (1 << 21);
+  return cell_index_exact(w, lo, dd);
 }
 
 __device__ __forceinline__ unsigned warp_sum_u(unsigned v) {
@@ -98,7 +91,7 @@ __device__ __forceinline__ unsigned warp_sum_u(unsigned v) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 4)
     sweep_kernel(const msurf_job* __restrict__ jobs, int n_jobs,
                  const int64_t* __restrict__ prefix, int mask_words) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -246,6 +239,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   const unsigned span_j = (unsigned)(J.j_hi - J.j_lo);
   const long long ldk = J.j_hi - J.j_lo + 1;
   uint64_t* __restrict__ keys = J.keys;
+  const double x_min = J.x_min, y_min = J.y_min;
+  const double tilt_c = J.tilt_c, tilt_s = J.tilt_s, zoff = J.zoff;
   const int rsplit = kWarps / nchunk > 1 ? kWarps / nchunk : 1;
   const int units = nchunk * rsplit;
   unsigned n_eval = 0, n_dep = 0, n_atom = 0;
@@ -259,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const bool valid = p < npts;
     const int word = q >> 6;
     const uint64_t bit = 1ull << (q & 63);
-    double ax = 0.0, ay = 0.0, az = 0.0;
+    double ax = 0.0, ay = 0.0, az = 0.0, tsz = 0.0, tcz = 0.0;
     uint64_t zk = ~0ull;
     if (valid) {
       if (MODE == MSURF_MODE_REF) {
@@ -273,53 +268,85 @@ __global__ void __launch_bounds__(kThreads, 2)
         az = J.pz[o];
       }
       if (MODE != MSURF_MODE_EXT_TILT) zk = J.zkey[(long long)tooth * npts + p];
+      if (MODE == MSURF_MODE_EXT_TILT) {
+        tsz = __dmul_rn(tilt_s, az);  // time-invariant halves of the tilt products
+        tcz = __dmul_rn(tilt_c, az);
+      }
     }
+    // run-length min pre-reduction: (last, run) is the open run of this lane;
+    // pend is the (possibly stale) stored key of `last`, prefetched when the
+    // run opened so its latency hides behind the following rows.
     long long last = -1;
-    uint64_t run = ~0ull;
-    for (int li = r0; li < r1; ++li) {
-      const int r = live[li];
-      if (!(masks[r * mask_words + word] & bit)) continue;
-      const double* rv = rowv + r * 8;
-      double xw, yw;
-      uint64_t key = zk;
-      if (MODE == MSURF_MODE_REF) {
-        // engine.py:289-296: xw = ((m00*xp + m01*yp) + m02*zp) + m03
-        xw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(rv[0], ax), __dmul_rn(rv[1], ay)),
-                                 __dmul_rn(rv[2], az)), rv[3]);
-        yw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(rv[4], ax), __dmul_rn(rv[5], ay)),
-                                 __dmul_rn(rv[6], az)), rv[7]);
-      } else {
-        const double c = rv[0], sn = rv[1];
-        const double uu = __dadd_rn(__dmul_rn(c, ax), __dmul_rn(sn, ay));
-        const double vv = __dadd_rn(__dmul_rn(-sn, ax), __dmul_rn(c, ay));
-        xw = __dadd_rn(uu, rv[2]);
-        if (MODE == MSURF_MODE_EXT_TILT) {
-          const double yv = __dsub_rn(__dmul_rn(J.tilt_c, vv), __dmul_rn(J.tilt_s, az));
-          const double zz =
-              __dadd_rn(__dadd_rn(__dmul_rn(J.tilt_s, vv), __dmul_rn(J.tilt_c, az)), J.zoff);
-          yw = __dadd_rn(yv, rv[3]);
-          key = enc_key(zz);
-        } else {
-          yw = __dadd_rn(vv, rv[3]);
-        }
+    uint64_t run = ~0ull, pend = 0ull;
+    const uint64_t* mword = masks + word;
+    // 32 live rows at a time: one ballot finds the rows whose cull mask keeps
+    // this chunk, so skipped (row, chunk) pairs cost ~1/32 of an iteration
+    for (int l0 = r0; l0 < r1; l0 += 32) {
+      const int li = l0 + lane;
+      int rr = 0;
+      bool on = false;
+      if (li < r1) {
+        rr = live[li];
+        on = (mword[rr * mask_words] & bit) != 0ull;
       }
-      n_eval += valid;
-      const int gi = cell_index(xw, J.x_min, dd, inv, cx0);
-      const int gj = cell_index(yw, J.y_min, dd, inv, cy0);
-      const bool inside = valid & ((unsigned)gi <= span_i) & ((unsigned)(gj - j_lo) <= span_j);
-      if (inside) {
-        ++n_dep;
-        const long long idx = (long long)gi * ldk + (gj - j_lo);
-        if (idx == last) {
-          run = key < run ? key : run;
+      unsigned bal = __ballot_sync(0xffffffffu, on);
+      while (bal) {
+        const int k = __ffs(bal) - 1;
+        bal &= bal - 1u;
+        const int r = __shfl_sync(0xffffffffu, rr, k);
+        const double* rv = rowv + r * 8;
+        double xw, yw;
+        uint64_t key = zk;
+        if (MODE == MSURF_MODE_REF) {
+          // engine.py:289-296: xw = ((m00*xp + m01*yp) + m02*zp) + m03
+          const double2 r01 = *reinterpret_cast<const double2*>(rv + 0);
+          const double2 r23 = *reinterpret_cast<const double2*>(rv + 2);
+          const double2 r45 = *reinterpret_cast<const double2*>(rv + 4);
+          const double2 r67 = *reinterpret_cast<const double2*>(rv + 6);
+          xw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r01.x, ax), __dmul_rn(r01.y, ay)),
+                                   __dmul_rn(r23.x, az)), r23.y);
+          yw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r45.x, ax), __dmul_rn(r45.y, ay)),
+                                   __dmul_rn(r67.x, az)), r67.y);
         } else {
-          flush_min(keys, last, run, n_atom);
-          last = idx;
-          run = key;
+          const double2 cs = *reinterpret_cast<const double2*>(rv + 0);
+          const double2 of = *reinterpret_cast<const double2*>(rv + 2);
+          const double uu = __dadd_rn(__dmul_rn(cs.x, ax), __dmul_rn(cs.y, ay));
+          const double vv = __dadd_rn(__dmul_rn(-cs.y, ax), __dmul_rn(cs.x, ay));
+          xw = __dadd_rn(uu, of.x);
+          if (MODE == MSURF_MODE_EXT_TILT) {
+            const double yv = __dsub_rn(__dmul_rn(tilt_c, vv), tsz);
+            const double zz = __dadd_rn(__dadd_rn(__dmul_rn(tilt_s, vv), tcz), zoff);
+            yw = __dadd_rn(yv, of.y);
+            key = enc_key(zz);
+          } else {
+            yw = __dadd_rn(vv, of.y);
+          }
+        }
+        n_eval += valid;
+        const int gi = cell_index(xw, x_min, dd, inv, cx0);
+        const int gj = cell_index(yw, y_min, dd, inv, cy0);
+        const bool inside = valid & ((unsigned)gi <= span_i) & ((unsigned)(gj - j_lo) <= span_j);
+        if (inside) {
+          ++n_dep;
+          const long long idx = (long long)gi * ldk + (gj - j_lo);
+          if (idx == last) {
+            run = key < run ? key : run;
+          } else {
+            if (last >= 0 && run < pend) {
+              atomicMin(reinterpret_cast<unsigned long long*>(keys + last), (unsigned long long)run);
+              ++n_atom;
+            }
+            last = idx;
+            run = key;
+            pend = __ldca(reinterpret_cast<const unsigned long long*>(keys + idx));
+          }
         }
       }
     }
-    flush_min(keys, last, run, n_atom);
+    if (last >= 0 && run < pend) {
+      atomicMin(reinterpret_cast<unsigned long long*>(keys + last), (unsigned long long)run);
+      ++n_atom;
+    }
   }
 
   // counters: one atomic per warp

@@ -83,144 +83,183 @@ def _trig_tables(p: SweepPlan):
     return tab, vib
 
 
-def sweep_plans(surfaces, trig: str = "device", device=None, return_device=False):
-    """Run the sweep for ``surfaces`` (list of (SweepPlan, j_lo, j_hi)) in one
-    batch. Returns (heights fp64 tensor views, counters, machined, device_ms, traj)."""
-    torch = _native.require_cuda()
-    lib = _native.lib()
-    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-    if trig not in ("device", "host"):
-        raise ConfigError(f"trig must be 'device' or 'host', got {trig!r}")
-    surfs = [_Surface(p, lo, hi) for p, lo, hi in surfaces]
-    total = 0
-    for s in surfs:
-        s.key_off = total
-        s.nodes = (s.plan.grid.m + 1) * (s.j_hi - s.j_lo + 1)
-        total += s.nodes
-    keys = torch.empty(max(total, 1), dtype=torch.int64, device=dev)
-    need_traj = [s.plan.record for s in surfs]
-    traj = None
-    if any(need_traj):
-        traj = torch.empty(sum(s.plan.steps * s.plan.teeth * 3 for s, r in zip(surfs, need_traj) if r),
-                           dtype=torch.float64, device=dev)
+class SweepBatch:
+    """A set of surfaces (plans, each with its owned column range [j_lo, j_hi])
+    uploaded to HBM once and swept by ``launch()`` as many times as needed
+    (the benchmark times repeated launches with inputs resident).
 
-    ar = _native.Arena()
-    offs = []
-    for s in surfs:
-        p = s.plan
-        o = dict(
-            tooth_base=ar.add(p.tooth_base.astype(np.float64)),
-            tooth_rows=ar.add(p.tooth_rows.astype(np.float64)),
-            px=ar.add(p.px), py=ar.add(p.py), pz=ar.add(p.pz),
-            zkey=ar.add(p.zkey.astype(np.uint64)),
-            chunk_box=ar.add(p.chunk_box.astype(np.float64)),
-            pass_x0=ar.add(p.pass_x0.astype(np.float64)),
-            min_index=ar.add(p.min_index.astype(np.int32)),
-            counters=ar.add(np.zeros(_native.NUM_CTRS, dtype=np.uint64)),
-        )
-        if trig == "host":
-            tab, vib = _trig_tables(p)
-            o["trig_table"] = ar.add(tab)
-            if vib is not None:
-                o["vib_table"] = ar.add(vib)
-        offs.append(o)
-    n = len(surfs)
-    sentinel_off = ar.add(np.array([s.plan.initial_height for s in surfs], dtype=np.float64))
-    machined_off = ar.add(np.zeros(n, dtype=np.uint64))
-    groups = {}
-    for i, s in enumerate(surfs):
-        groups.setdefault(s.plan.mode, []).append(i)
-    tile_steps = lib.msurf_tile_steps()
-    group_meta = []
-    for mode, idx in sorted(groups.items()):
-        tiles = [surfs[i].plan.passes * surfs[i].plan.teeth *
-                 ((surfs[i].plan.steps + tile_steps - 1) // tile_steps) for i in idx]
-        prefix = np.concatenate([[0], np.cumsum(tiles)]).astype(np.int64)
-        job_off = ar.add(np.zeros(len(idx) * ctypes.sizeof(_native.MsurfJob), dtype=np.uint8))
-        pre_off = ar.add(prefix)
-        group_meta.append((mode, idx, job_off, pre_off, int(prefix[-1]),
-                           max(surfs[i].plan.points for i in idx)))
-    keys_ptr = keys.data_ptr()
-    traj_ptr = traj.data_ptr() if traj is not None else 0
+    Device layout: one uint8 arena holding every per-surface array, the job
+    descriptors (msurf_job) and tile prefix sums, written by ONE H2D copy;
+    one int64 tensor holding all surfaces' Z-maps back to back (u64 keys
+    during the sweep, fp64 heights after the decode, in place)."""
 
-    def fill(base):
-        out = []
+    def __init__(self, surfaces, trig: str = "device", device=None):
+        torch = _native.require_cuda()
+        self.torch = torch
+        self.lib = _native.lib()
+        self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        if trig not in ("device", "host"):
+            raise ConfigError(f"trig must be 'device' or 'host', got {trig!r}")
+        surfs = [_Surface(p, lo, hi) for p, lo, hi in surfaces]
+        if not surfs:
+            raise ConfigError("empty batch")
+        total = 0
+        for s in surfs:
+            s.key_off = total
+            s.nodes = (s.plan.grid.m + 1) * (s.j_hi - s.j_lo + 1)
+            total += s.nodes
+        self.surfs = surfs
+        self.keys = torch.empty(max(total, 1), dtype=torch.int64, device=self.dev)
+        self.need_traj = [s.plan.record for s in surfs]
+        traj_len = sum(s.plan.steps * s.plan.teeth * 3 for s, r in zip(surfs, self.need_traj) if r)
+        self.traj = torch.empty(traj_len, dtype=torch.float64, device=self.dev) if traj_len else None
+
+        ar = _native.Arena()
+        offs = []
+        for s in surfs:
+            p = s.plan
+            o = dict(
+                tooth_base=ar.add(p.tooth_base.astype(np.float64)),
+                tooth_rows=ar.add(p.tooth_rows.astype(np.float64)),
+                px=ar.add(p.px), py=ar.add(p.py), pz=ar.add(p.pz),
+                zkey=ar.add(p.zkey.astype(np.uint64)),
+                chunk_box=ar.add(p.chunk_box.astype(np.float64)),
+                pass_x0=ar.add(p.pass_x0.astype(np.float64)),
+                min_index=ar.add(p.min_index.astype(np.int32)),
+            )
+            if trig == "host":
+                tab, vib = _trig_tables(p)
+                o["trig_table"] = ar.add(tab)
+                if vib is not None:
+                    o["vib_table"] = ar.add(vib)
+            offs.append(o)
+        n = len(surfs)
+        self.n = n
+        self.sentinel_off = ar.add(np.array([s.plan.initial_height for s in surfs], dtype=np.float64))
+        # counters [n][4] then machined [n], contiguous: zeroed by one memset per launch
+        self.ctr_off = ar.add(np.zeros(n * (_native.NUM_CTRS + 1), dtype=np.uint64))
+        self.machined_off = self.ctr_off + n * _native.NUM_CTRS * 8
+        groups = {}
+        for i, s in enumerate(surfs):
+            groups.setdefault(s.plan.mode, []).append(i)
+        tile_steps = self.lib.msurf_tile_steps()
+        self.group_meta = []
+        for mode, idx in sorted(groups.items()):
+            tiles = [surfs[i].plan.passes * surfs[i].plan.teeth *
+                     ((surfs[i].plan.steps + tile_steps - 1) // tile_steps) for i in idx]
+            prefix = np.concatenate([[0], np.cumsum(tiles)]).astype(np.int64)
+            job_off = ar.add(np.zeros(len(idx) * ctypes.sizeof(_native.MsurfJob), dtype=np.uint8))
+            pre_off = ar.add(prefix)
+            self.group_meta.append((mode, idx, job_off, pre_off, int(prefix[-1]),
+                                    max(surfs[i].plan.points for i in idx)))
+        keys_ptr = self.keys.data_ptr()
+        traj_ptr = self.traj.data_ptr() if self.traj is not None else 0
+        self.traj_off = []
         toff = 0
-        tptrs = []
-        for s, r in zip(surfs, need_traj):
-            tptrs.append(traj_ptr + toff * 8 if r else 0)
+        for s, r in zip(surfs, self.need_traj):
+            self.traj_off.append(toff if r else None)
             if r:
                 toff += s.plan.steps * s.plan.teeth * 3
-        for mode, idx, job_off, _, _, _ in group_meta:
-            arr = (_native.MsurfJob * len(idx))()
-            for k, i in enumerate(idx):
-                s, o, p = surfs[i], offs[i], surfs[i].plan
-                g = p.grid
-                j = arr[k]
-                j.spacing, j.x_min, j.y_min = g.spacing_mm, g.x_min_mm, g.y_min_mm
-                j.m, j.n, j.j_lo, j.j_hi = g.m, g.n, s.j_lo, s.j_hi
-                j.keys = keys_ptr + s.key_off * 8
-                j.t_start, j.dt, j.steps = p.t_start, p.dt, p.steps
-                j.y0, j.feed_speed, j.omega = p.y0, p.feed_speed, p.omega
-                for name in ("tooth_base", "tooth_rows", "px", "py", "pz", "zkey", "chunk_box",
-                             "pass_x0", "min_index", "counters"):
-                    setattr(j, name, base + o[name])
-                j.tilt_c, j.tilt_s, j.zoff = p.tilt_c, p.tilt_s, p.zoff
-                j.vib_amp, j.vib_omega, j.vib_phase = p.vib_amp, p.vib_omega, p.vib_phase
-                j.trig_table = base + o["trig_table"] if "trig_table" in o else None
-                j.vib_table = base + o["vib_table"] if "vib_table" in o else None
-                j.traj = tptrs[i] or None
-                j.teeth, j.points, j.passes = p.teeth, p.points, p.passes
-            out.append((job_off, bytes(arr)))
+
+        def fill(base):
+            out = []
+            for mode, idx, job_off, _, _, _ in self.group_meta:
+                arr = (_native.MsurfJob * len(idx))()
+                for k, i in enumerate(idx):
+                    s, o, p = surfs[i], offs[i], surfs[i].plan
+                    g = p.grid
+                    j = arr[k]
+                    j.spacing, j.x_min, j.y_min = g.spacing_mm, g.x_min_mm, g.y_min_mm
+                    j.m, j.n, j.j_lo, j.j_hi = g.m, g.n, s.j_lo, s.j_hi
+                    j.keys = keys_ptr + s.key_off * 8
+                    j.t_start, j.dt, j.steps = p.t_start, p.dt, p.steps
+                    j.y0, j.feed_speed, j.omega = p.y0, p.feed_speed, p.omega
+                    for name in ("tooth_base", "tooth_rows", "px", "py", "pz", "zkey", "chunk_box",
+                                 "pass_x0", "min_index"):
+                        setattr(j, name, base + o[name])
+                    j.counters = base + self.ctr_off + i * _native.NUM_CTRS * 8
+                    j.tilt_c, j.tilt_s, j.zoff = p.tilt_c, p.tilt_s, p.zoff
+                    j.vib_amp, j.vib_omega, j.vib_phase = p.vib_amp, p.vib_omega, p.vib_phase
+                    j.trig_table = base + o["trig_table"] if "trig_table" in o else None
+                    j.vib_table = base + o["vib_table"] if "vib_table" in o else None
+                    j.traj = traj_ptr + self.traj_off[i] * 8 if self.need_traj[i] else None
+                    j.teeth, j.points, j.passes = p.teeth, p.points, p.passes
+                out.append((job_off, bytes(arr)))
+            return out
+
+        self.h2d_bytes = ar.size
+        self.buf = ar.upload(self.dev, fill)
+        self.base = self.buf.data_ptr()
+        self.same_shape = len({s.nodes for s in surfs}) == 1
+        self.launches_per_run = 2 * (1 if self.same_shape else n) + len(self.group_meta)
+
+    # ------------------------------------------------------------------
+    def launch(self, stream=None, events=None):
+        """Enqueue fill -> sweep(s) -> decode on ``stream`` (async).
+        ``events`` = (start, after_fill, after_sweep, end) CUDA events, optional."""
+        torch, lib = self.torch, self.lib
+        st = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        sp = int(st.cuda_stream)
+        base, keys_ptr = self.base, self.keys.data_ptr()
+        if events:
+            events[0].record(st)
+        with torch.cuda.stream(st):
+            self.buf[self.ctr_off: self.ctr_off + self.n * (_native.NUM_CTRS + 1) * 8].zero_()
+        if self.same_shape:
+            _native.check(lib.msurf_fill_keys(keys_ptr, self.surfs[0].nodes, self.n,
+                                              base + self.sentinel_off, sp))
+        else:
+            for i, s in enumerate(self.surfs):
+                _native.check(lib.msurf_fill_keys(keys_ptr + s.key_off * 8, s.nodes, 1,
+                                                  base + self.sentinel_off + 8 * i, sp))
+        if events:
+            events[1].record(st)
+        for mode, idx, job_off, pre_off, n_tiles, max_pts in self.group_meta:
+            _native.check(lib.msurf_sweep(base + job_off, len(idx), base + pre_off, n_tiles, mode,
+                                          max_pts, sp))
+        if events:
+            events[2].record(st)
+        if self.same_shape:
+            _native.check(lib.msurf_decode(keys_ptr, self.surfs[0].nodes, self.n, base + self.sentinel_off,
+                                           base + self.machined_off, sp))
+        else:
+            for i, s in enumerate(self.surfs):
+                _native.check(lib.msurf_decode(keys_ptr + s.key_off * 8, s.nodes, 1,
+                                               base + self.sentinel_off + 8 * i,
+                                               base + self.machined_off + 8 * i, sp))
+        if events:
+            events[3].record(st)
+
+    def heights(self):
+        """fp64 views (valid after a launch) — one per surface."""
+        h = self.keys.view(self.torch.float64)
+        return [h[s.key_off: s.key_off + s.nodes] for s in self.surfs]
+
+    def sentinels_device(self):
+        return self.buf[self.sentinel_off: self.sentinel_off + 8 * self.n].view(self.torch.float64)
+
+    def counters(self):
+        """(counters [n,4], machined [n]) on the host (synchronises)."""
+        u64 = self.buf[self.ctr_off: self.ctr_off + self.n * (_native.NUM_CTRS + 1) * 8].view(self.torch.int64)
+        a = u64.cpu().numpy()
+        return a[: self.n * _native.NUM_CTRS].reshape(self.n, _native.NUM_CTRS), a[self.n * _native.NUM_CTRS:]
+
+    def trajectories(self):
+        out = []
+        for s, r, o in zip(self.surfs, self.need_traj, self.traj_off):
+            out.append(self.traj[o: o + s.plan.steps * s.plan.teeth * 3] if r else None)
         return out
 
-    stream = torch.cuda.current_stream(dev)
-    sp = _native.stream_ptr(stream)
-    buf = ar.upload(dev, fill)
-    base = buf.data_ptr()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    same = len({s.nodes for s in surfs}) == 1
-    if same:
-        _native.check(lib.msurf_fill_keys(keys_ptr, surfs[0].nodes, n, base + sentinel_off, sp))
-    else:
-        for i, s in enumerate(surfs):
-            _native.check(lib.msurf_fill_keys(keys_ptr + s.key_off * 8, s.nodes, 1,
-                                              base + sentinel_off + 8 * i, sp))
-    for mode, idx, job_off, pre_off, n_tiles, max_pts in group_meta:
-        _native.check(lib.msurf_sweep(base + job_off, len(idx), base + pre_off, n_tiles, mode,
-                                      max_pts, sp))
-    if same:
-        _native.check(lib.msurf_decode(keys_ptr, surfs[0].nodes, n, base + sentinel_off,
-                                       base + machined_off, sp))
-    else:
-        for i, s in enumerate(surfs):
-            _native.check(lib.msurf_decode(keys_ptr + s.key_off * 8, s.nodes, 1,
-                                           base + sentinel_off + 8 * i, base + machined_off + 8 * i, sp))
-    ev1.record(stream)
-    # small D2H: counters + machined counts (synchronises the stream)
-    ctr = []
-    u64 = buf.view(torch.int64)
-    for o in offs:
-        ctr.append(u64[o["counters"] // 8: o["counters"] // 8 + _native.NUM_CTRS])
-    small = torch.stack(ctr).cpu().numpy() if ctr else np.zeros((0, 4), np.int64)
-    machined = u64[machined_off // 8: machined_off // 8 + n].cpu().numpy()
-    device_ms = ev0.elapsed_time(ev1)
-    heights = keys.view(torch.float64)
-    views = [heights[s.key_off: s.key_off + s.nodes] for s in surfs]
-    trajs = []
-    if traj is not None:
-        toff = 0
-        for s, r in zip(surfs, need_traj):
-            if r:
-                k = s.plan.steps * s.plan.teeth * 3
-                trajs.append(traj[toff: toff + k])
-                toff += k
-            else:
-                trajs.append(None)
-    else:
-        trajs = [None] * n
-    return views, small, machined, device_ms, trajs, buf
+
+def sweep_plans(surfaces, trig: str = "device", device=None):
+    """One-shot: upload, launch, collect. Returns (heights views, counters,
+    machined, device_ms, trajectories, batch)."""
+    torch = _native.require_cuda()
+    b = SweepBatch(surfaces, trig=trig, device=device)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    b.launch(events=ev)
+    small, machined = b.counters()
+    return b.heights(), small, machined, ev[0].elapsed_time(ev[3]), b.trajectories(), b
 
 
 def _counters_dict(row) -> dict:

@@ -1,0 +1,187 @@
+"""Multi-GPU: feed-direction strips for one large surface, parameter-set
+shards for batches. One process per GPU (torchrun), torch.distributed over
+NCCL for the only exchange the path has: the partial roughness moments.
+
+Strip sharding: rank r owns node columns [j_lo, j_hi] of
+the Z-map (all rows i) and holds only that (m+1) x (j_hi-j_lo+1) slab. The
+sweep kernel's 2-D cull window is the strip, so each GPU evaluates only the
+(step, tooth, 32-point chunk) work whose footprint meets its strip; heights
+never cross GPUs. Roughness then needs two tiny all-reduces per output:
+  areal:    stats1 = [sum z, max z, min z, n, n_uncut]  -> global mean
+            moments = [sum|d|, sum d^2, sum d^3, sum d^4] around that mean
+  profiles: [sum z, n, n_uncut, max z, min z] then [sum |z - mean|]
+Batched runs shard by parameter set with no communication at all.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .errors import ConfigError, DomainError
+from .extensions import Extensions
+from .grid import GridSpec
+from .planner import plan as make_plan
+from .roughness import (ArealMetrics, ProfileRoughness, _finish_areal, _finish_profile,
+                        _metrics_from_moments)
+
+# column layouts of the reduced records (see include/msurf.h)
+STATS1_SUM, STATS1_MAX, STATS1_MIN = (0, 3, 4), (1,), (2,)
+PROF_SUM, PROF_MAX, PROF_MIN = (0, 1, 2), (3,), (4,)
+
+
+def strip_bounds(nodes: int, world: int):
+    """Contiguous, near-equal split of `nodes` feed-direction node columns."""
+    if world < 1 or nodes < world:
+        raise ConfigError(f"cannot split {nodes} columns over {world} ranks")
+    cuts = [round(r * nodes / world) for r in range(world + 1)]
+    return [(cuts[r], cuts[r + 1] - 1) for r in range(world)]
+
+
+def batch_slice(count: int, rank: int, world: int) -> slice:
+    """Parameter-set shard of a batch: contiguous block for rank."""
+    lo = (count * rank) // world
+    hi = (count * (rank + 1)) // world
+    return slice(lo, hi)
+
+
+def combine(t, sums, maxs, mins, group=None):
+    """In-place all-reduce of a [k, c] record tensor whose columns are SUM,
+    MAX or MIN quantities: two collectives (SUM on the sum columns, MAX on
+    [max columns, -min columns])."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return t
+    s = t[:, list(sums)].contiguous()
+    dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
+    mm = torch.cat([t[:, list(maxs)], -t[:, list(mins)]], dim=1).contiguous()
+    dist.all_reduce(mm, op=dist.ReduceOp.MAX, group=group)
+    t[:, list(sums)] = s
+    t[:, list(maxs)] = mm[:, : len(maxs)]
+    t[:, list(mins)] = -mm[:, len(maxs):]
+    return t
+
+
+def make_allreduce(group=None):
+    """Callable(tensor, kind) for roughness.areal_moments_device."""
+
+    def ar(t, kind):
+        if kind == "stats1":
+            combine(t, STATS1_SUM, STATS1_MAX, STATS1_MIN, group)
+        elif kind == "moments":
+            combine(t, tuple(range(t.shape[1])), (), (), group)
+        elif kind == "profiles1":
+            combine(t, PROF_SUM, PROF_MAX, PROF_MIN, group)
+        elif kind == "profiles2":
+            combine(t, tuple(range(t.shape[1])), (), (), group)
+        else:
+            raise ValueError(kind)
+        return t
+
+    return ar
+
+
+@dataclass
+class StripResult:
+    plan: object
+    j_lo: int
+    j_hi: int
+    heights: object           # device fp64 (m+1) * (j_hi-j_lo+1), row-major
+    counters: dict
+    cells_updated: int
+    main_loop_seconds: float
+    batch: object
+
+
+def simulate_strip(config, ext: Extensions | None, rank: int, world: int, trig: str = "device") -> StripResult:
+    """Sweep this rank's feed-direction strip of one surface."""
+    from .engine import SweepBatch
+
+    torch = _native.require_cuda()
+    p = make_plan(config, ext)
+    if p.record:
+        raise ConfigError("record_trajectory is not supported under strip sharding")
+    j_lo, j_hi = strip_bounds(p.grid.n + 1, world)[rank]
+    b = SweepBatch([(p, j_lo, j_hi)], trig=trig)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    b.launch(events=ev)
+    ctr, machined = b.counters()
+    return StripResult(plan=p, j_lo=j_lo, j_hi=j_hi, heights=b.heights()[0],
+                       counters={"live_rows": int(ctr[0][0]), "points_evaluated": int(ctr[0][1]),
+                                 "deposits": int(ctr[0][2]), "atomics": int(ctr[0][3])},
+                       cells_updated=int(machined[0]), main_loop_seconds=ev[0].elapsed_time(ev[3]) * 1e-3,
+                       batch=b)
+
+
+def strip_roi(grid: GridSpec, roi, j_lo: int, j_hi: int):
+    """Intersect a global inclusive ROI with a strip -> local (i_lo, jl_lo, rows, cols) or None."""
+    if roi is None:
+        roi = (0, 0, grid.m, grid.n)
+    i_lo, a, i_hi, b = roi
+    if not (0 <= i_lo <= i_hi <= grid.m and 0 <= a <= b <= grid.n):
+        raise DomainError(f"roi {roi} outside grid [0, {grid.m}] x [0, {grid.n}] or empty")
+    lo, hi = max(a, j_lo), min(b, j_hi)
+    if lo > hi:
+        return None
+    return (i_lo, lo - j_lo, i_hi - i_lo + 1, hi - lo + 1)
+
+
+def areal_metrics_strip(res: StripResult, roi=None, uncut: str = "raise", group=None) -> ArealMetrics:
+    """Global areal metrics of a strip-sharded surface (two all-reduces)."""
+    import torch
+
+    lib = _native.lib()
+    grid = res.plan.grid
+    box = strip_roi(grid, roi, res.j_lo, res.j_hi)
+    ld = res.j_hi - res.j_lo + 1
+    dev = res.heights.device
+    sent = torch.tensor([res.plan.initial_height], dtype=torch.float64, device=dev)
+    work = torch.empty(_native.RED_BLOCKS * 5, dtype=torch.float64, device=dev)
+    st1 = torch.zeros((1, 5), dtype=torch.float64, device=dev)
+    st1[0, 1], st1[0, 2] = -np.inf, np.inf
+    st2 = torch.zeros((1, 4), dtype=torch.float64, device=dev)
+    sp = _native.stream_ptr()
+    ex = int(uncut == "exclude")
+    if box is not None:
+        i_lo, jl, rows, cols = box
+        _native.check(lib.msurf_areal_pass1(res.heights.data_ptr(), ld, 0, 1, i_lo, jl, rows, cols,
+                                            sent.data_ptr(), ex, work.data_ptr(), st1.data_ptr(), sp))
+    combine(st1, STATS1_SUM, STATS1_MAX, STATS1_MIN, group)
+    if box is not None and float(st1[0, 3]) > 0:
+        i_lo, jl, rows, cols = box
+        _native.check(lib.msurf_areal_pass2(res.heights.data_ptr(), ld, 0, 1, i_lo, jl, rows, cols,
+                                            sent.data_ptr(), ex, st1.data_ptr(), work.data_ptr(),
+                                            st2.data_ptr(), sp))
+    combine(st2, (0, 1, 2, 3), (), (), group)
+    return _finish_areal(st1[0].cpu().numpy(), st2[0].cpu().numpy(), uncut)
+
+
+def profile_roughness_strip(res: StripResult, every: int = 64, uncut: str = "raise", group=None):
+    """Ra/Rz of every `every`-th feed profile (fixed i, all j) across strips."""
+    import torch
+
+    lib = _native.lib()
+    grid = res.plan.grid
+    ld = res.j_hi - res.j_lo + 1
+    idx = list(range(0, grid.m + 1, every))
+    dev = res.heights.device
+    starts = torch.tensor([i * ld for i in idx], dtype=torch.int64, device=dev)
+    sent = torch.tensor([res.plan.initial_height], dtype=torch.float64, device=dev)
+    out = torch.empty(len(idx) * 8, dtype=torch.float64, device=dev)
+    sp = _native.stream_ptr()
+    ex = int(uncut == "exclude")
+    _native.check(lib.msurf_profiles(res.heights.data_ptr(), 0, 1, starts.data_ptr(), len(idx), ld, 1,
+                                     sent.data_ptr(), ex, None, out.data_ptr(), sp))
+    first = out.view(-1, 8).clone()
+    combine(first, PROF_SUM, PROF_MAX, PROF_MIN, group)
+    _native.check(lib.msurf_profiles(res.heights.data_ptr(), 0, 1, starts.data_ptr(), len(idx), ld, 1,
+                                     sent.data_ptr(), ex, first.data_ptr(), out.data_ptr(), sp))
+    sabs = out.view(-1, 8)[:, 5:6].contiguous()
+    combine(sabs, (0,), (), (), group)
+    first[:, 5:6] = sabs
+    rows = first.cpu().numpy()
+    return [_finish_profile(r, i, uncut) for r, i in zip(rows, idx)]

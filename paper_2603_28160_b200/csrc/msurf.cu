@@ -32,7 +32,6 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kTileSteps = 256;  // rows (time steps) per CTA; == kThreads
 constexpr int kWarps = kThreads / 32;
-constexpr double kNearEps = 0x1p-30;  // fast-path locate guard (see cell_fast)
 
 thread_local std::string g_err;
 
@@ -63,25 +62,48 @@ __device__ __forceinline__ double dec_key(uint64_t k) {
 // ---------------------------------------------------------- cell location
 // Reference: idx = floor((w - lo)/dd + 0.5) with a true IEEE division
 // (engine.py:298-300, surface_grid.py:85-86).
-// Fast path: tq = fma(w, 1/dd, 0.5 - lo/dd) is within 1e-11 of the exact
-// quotient+0.5 for |tq| < 2^21. Adding 1.5*2^22 rounds tq to a multiple of
-// 2^-30 and leaves floor(tq) in mantissa bits [30, 52) and the fraction in
-// bits [0, 30): two DP ops plus integer ops instead of FRND/F2I. When the
-// fraction is within 2^-29 of an integer (or |tq| is out of range) the floor
-// could differ from the reference's, so those rare points take the exact
-// reference sequence. Result: bit-identical cell indices.
+// Fast path: tq = fma(w, 1/dd, 0.5 - lo/dd) differs from the reference's
+// RN(RN((w-lo)/dd) + 0.5) by < 2^-30 while |w/dd|, |lo/dd|, |tq| < 2^18
+// (host-checked grid bound). Adding 1.5*2^20 rounds tq to a multiple of
+// 2^-32: for |tq| < 2^19 the high word then holds exponent 1043 and
+// floor(tq) + 2^19 in its 20 mantissa bits, and the low word is the fraction
+// in units of 2^-32. So floor = hi - (1043 << 20 | 2^19) (any other exponent
+// means |tq| >= 2^19, i.e. far outside every supported grid, and lands out
+// of range by construction), and "within 2^-29 of an integer" is
+// (lo + 8) < 16 unsigned. Only those rare near-boundary points take the exact
+// reference sequence: bit-identical indices at two DP ops per axis.
+constexpr int kMagicHi = (1043 << 20) | (1 << 19);
+
 __device__ __noinline__ int cell_index_exact(double w, double lo, double dd) {
   const double tq = __dadd_rn(__ddiv_rn(__dsub_rn(w, lo), dd), 0.5);
   return __double2int_rz(floor(tq));  // saturates far outside; range checks reject
 }
 
-__device__ __forceinline__ int cell_index(double w, double lo, double dd, double inv, double c0) {
-  const double tq = __fma_rn(w, inv, c0);
-  const long long b = __double_as_longlong(__dadd_rn(tq, 0x1.8p22));
-  const unsigned f = (unsigned)b & 0x3fffffffu;
-  const bool ok = ((int)(b >> 52) == 1045) & ((f - 2u) <= 0x3fffffffu - 4u);
-  if (__builtin_expect(ok, 1)) return (int)((b & 0x000fffffffffffffLL) >> 30) - (1 << 21);
-  return cell_index_exact(w, lo, dd);
+struct CellFast {
+  int idx;       // floor(tq) if not near
+  bool near;     // fraction within 2^-29 of an integer: use the exact path
+};
+
+__device__ __forceinline__ CellFast cell_fast(double w, double inv, double c0) {
+  const double m = __dadd_rn(__fma_rn(w, inv, c0), 0x1.8p20);
+  const int hi = __double2hiint(m);
+  const unsigned lo = (unsigned)__double2loint(m);
+  CellFast r;
+  r.idx = hi - kMagicHi;
+  r.near = (lo + 8u) < 16u;
+  return r;
+}
+
+// Fire-and-forget global atomic min (RED.E.MIN.64): the explicit .global
+// form avoids the generic-address shared-memory fallback atomicMin compiles to.
+__device__ __forceinline__ void red_min_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_stale_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.cta.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
 }
 
 __device__ __forceinline__ unsigned warp_sum_u(unsigned v) {
@@ -100,6 +122,7 @@ __global__ void __launch_bounds__(kThreads, 4)
   int* live = reinterpret_cast<int*>(masks + kTileSteps * mask_words);       // [T]
   __shared__ msurf_job J;
   __shared__ int warp_cnt[kWarps];
+  __shared__ unsigned warp_eval[kWarps];
   __shared__ int s_job;
 
   const int tid = threadIdx.x;
@@ -134,12 +157,13 @@ __global__ void __launch_bounds__(kThreads, 4)
   const double dd = J.spacing;
 
   // ---------------- phase 1: one thread per time step of the tile
-  const double wx_lo = J.x_min - 1.5 * dd;
-  const double wx_hi = J.x_min + (double)J.m * dd + 1.5 * dd;
-  const double wy_lo = J.y_min + (double)J.j_lo * dd - 1.5 * dd;
-  const double wy_hi = J.y_min + (double)J.j_hi * dd + 1.5 * dd;
   bool any = false;
+  unsigned my_eval = 0;
   {
+    const double wx_lo = J.x_min - 1.5 * dd;
+    const double wx_hi = J.x_min + (double)J.m * dd + 1.5 * dd;
+    const double wy_lo = J.y_min + (double)J.j_lo * dd - 1.5 * dd;
+    const double wy_hi = J.y_min + (double)J.j_hi * dd + 1.5 * dd;
     const long long s = (long long)st * kTileSteps + tid;
     uint64_t* my_mask = masks + tid * mask_words;
     for (int w = 0; w < mask_words; ++w) my_mask[w] = 0ull;
@@ -193,6 +217,7 @@ __global__ void __launch_bounds__(kThreads, 4)
       }
       // 2-D chunk cull; conservative by 1.5 cells >> rounding differences
       const double* box = J.chunk_box + (long long)tooth * nchunk * 6;
+      unsigned kept = 0;
       for (int q = 0; q < nchunk; ++q) {
         const double xl = box[q * 6 + 0], xh = box[q * 6 + 1];
         const double yl = box[q * 6 + 2], yh = box[q * 6 + 3];
@@ -211,20 +236,28 @@ __global__ void __launch_bounds__(kThreads, 4)
                           (v_lo + ty <= wy_hi);
         if (keep) {
           my_mask[q >> 6] |= 1ull << (q & 63);
-          any = true;
+          kept += (q == nchunk - 1) ? (unsigned)(npts - 32 * q) : 32u;
         }
       }
+      any = kept != 0;
+      my_eval = kept;
     }
   }
-  // ordered compaction of live steps
+  // ordered compaction of live steps (keeps time order for the run-length merge)
   const unsigned bal = __ballot_sync(0xffffffffu, any);
-  if (lane == 0) warp_cnt[warp] = __popc(bal);
+  my_eval = warp_sum_u(my_eval);
+  if (lane == 0) {
+    warp_cnt[warp] = __popc(bal);
+    warp_eval[warp] = my_eval;
+  }
   __syncthreads();
   int base = 0, n_live = 0;
+  unsigned n_eval_cta = 0;
 #pragma unroll
   for (int w = 0; w < kWarps; ++w) {
     if (w < warp) base += warp_cnt[w];
     n_live += warp_cnt[w];
+    n_eval_cta += warp_eval[w];
   }
   if (any) live[base + __popc(bal & ((1u << lane) - 1u))] = tid;
   __syncthreads();
@@ -237,13 +270,12 @@ __global__ void __launch_bounds__(kThreads, 4)
   const unsigned span_i = (unsigned)J.m;
   const int j_lo = (int)J.j_lo;
   const unsigned span_j = (unsigned)(J.j_hi - J.j_lo);
-  const long long ldk = J.j_hi - J.j_lo + 1;
-  uint64_t* __restrict__ keys = J.keys;
-  const double x_min = J.x_min, y_min = J.y_min;
+  const int ldk = (int)(J.j_hi - J.j_lo + 1);
+  unsigned long long* __restrict__ keys = reinterpret_cast<unsigned long long*>(J.keys);
   const double tilt_c = J.tilt_c, tilt_s = J.tilt_s, zoff = J.zoff;
   const int rsplit = kWarps / nchunk > 1 ? kWarps / nchunk : 1;
   const int units = nchunk * rsplit;
-  unsigned n_eval = 0, n_dep = 0, n_atom = 0;
+  unsigned n_dep = 0, n_atom = 0;
 
   for (int u = warp; u < units; u += kWarps) {
     const int q = u % nchunk;
@@ -252,35 +284,28 @@ __global__ void __launch_bounds__(kThreads, 4)
     const int r1 = (int)((long long)(part + 1) * n_live / rsplit);
     const int p = q * 32 + lane;
     const bool valid = p < npts;
-    const int word = q >> 6;
     const uint64_t bit = 1ull << (q & 63);
+    const uint64_t* mword = masks + (q >> 6);
     double ax = 0.0, ay = 0.0, az = 0.0, tsz = 0.0, tcz = 0.0;
     uint64_t zk = ~0ull;
     if (valid) {
-      if (MODE == MSURF_MODE_REF) {
-        ax = J.px[p];
-        ay = J.py[p];
-        az = J.pz[p];
-      } else {
-        const long long o = (long long)tooth * npts + p;
-        ax = J.px[o];
-        ay = J.py[o];
-        az = J.pz[o];
-      }
+      const long long o = MODE == MSURF_MODE_REF ? (long long)p : (long long)tooth * npts + p;
+      ax = J.px[o];
+      ay = J.py[o];
+      az = J.pz[o];
       if (MODE != MSURF_MODE_EXT_TILT) zk = J.zkey[(long long)tooth * npts + p];
       if (MODE == MSURF_MODE_EXT_TILT) {
         tsz = __dmul_rn(tilt_s, az);  // time-invariant halves of the tilt products
         tcz = __dmul_rn(tilt_c, az);
       }
     }
-    // run-length min pre-reduction: (last, run) is the open run of this lane;
-    // pend is the (possibly stale) stored key of `last`, prefetched when the
-    // run opened so its latency hides behind the following rows.
-    long long last = -1;
+    // run-length min pre-reduction in registers: (last, run) is this lane's
+    // open run of consecutive live steps landing in one cell; pend is that
+    // cell's stored key, prefetched when the run opened (stale reads only
+    // over-estimate: heights never rise), so the atomicMin is issued only
+    // when it can lower the cell and the load latency hides behind the run.
+    int last = -1;
     uint64_t run = ~0ull, pend = 0ull;
-    const uint64_t* mword = masks + word;
-    // 32 live rows at a time: one ballot finds the rows whose cull mask keeps
-    // this chunk, so skipped (row, chunk) pairs cost ~1/32 of an iteration
     for (int l0 = r0; l0 < r1; l0 += 32) {
       const int li = l0 + lane;
       int rr = 0;
@@ -289,10 +314,10 @@ __global__ void __launch_bounds__(kThreads, 4)
         rr = live[li];
         on = (mword[rr * mask_words] & bit) != 0ull;
       }
-      unsigned bal = __ballot_sync(0xffffffffu, on);
-      while (bal) {
-        const int k = __ffs(bal) - 1;
-        bal &= bal - 1u;
+      unsigned bal2 = __ballot_sync(0xffffffffu, on);
+      while (bal2) {
+        const int k = __ffs(bal2) - 1;
+        bal2 &= bal2 - 1u;
         const int r = __shfl_sync(0xffffffffu, rr, k);
         const double* rv = rowv + r * 8;
         double xw, yw;
@@ -322,40 +347,44 @@ __global__ void __launch_bounds__(kThreads, 4)
             yw = __dadd_rn(vv, of.y);
           }
         }
-        n_eval += valid;
-        const int gi = cell_index(xw, x_min, dd, inv, cx0);
-        const int gj = cell_index(yw, y_min, dd, inv, cy0);
-        const bool inside = valid & ((unsigned)gi <= span_i) & ((unsigned)(gj - j_lo) <= span_j);
+        CellFast ci = cell_fast(xw, inv, cx0);
+        CellFast cj = cell_fast(yw, inv, cy0);
+        if (__builtin_expect(ci.near | cj.near, 0)) {
+          ci.idx = cell_index_exact(xw, J.x_min, dd);
+          cj.idx = cell_index_exact(yw, J.y_min, dd);
+        }
+        const bool inside = valid & ((unsigned)ci.idx <= span_i) & ((unsigned)(cj.idx - j_lo) <= span_j);
         if (inside) {
           ++n_dep;
-          const long long idx = (long long)gi * ldk + (gj - j_lo);
+          const int idx = ci.idx * ldk + (cj.idx - j_lo);
           if (idx == last) {
-            run = key < run ? key : run;
+            if (MODE == MSURF_MODE_EXT_TILT) run = key < run ? key : run;
           } else {
-            if (last >= 0 && run < pend) {
-              atomicMin(reinterpret_cast<unsigned long long*>(keys + last), (unsigned long long)run);
+            if (run < pend) {  // also false for the initial (-1, ~0, 0) state
+              red_min_u64(keys + last, (unsigned long long)run);
               ++n_atom;
             }
             last = idx;
             run = key;
-            pend = __ldca(reinterpret_cast<const unsigned long long*>(keys + idx));
+            pend = ld_stale_u64(keys + idx);
           }
         }
       }
     }
-    if (last >= 0 && run < pend) {
-      atomicMin(reinterpret_cast<unsigned long long*>(keys + last), (unsigned long long)run);
+    if (run < pend) {
+      red_min_u64(keys + last, (unsigned long long)run);
       ++n_atom;
     }
   }
 
   // counters: one atomic per warp
-  n_eval = warp_sum_u(n_eval);
   n_dep = warp_sum_u(n_dep);
   n_atom = warp_sum_u(n_atom);
   if (lane == 0 && J.counters) {
-    if (warp == 0) atomicAdd(J.counters + MSURF_CTR_LIVE_ROWS, (unsigned long long)n_live);
-    atomicAdd(J.counters + MSURF_CTR_EVAL, (unsigned long long)n_eval);
+    if (warp == 0) {
+      atomicAdd(J.counters + MSURF_CTR_LIVE_ROWS, (unsigned long long)n_live);
+      atomicAdd(J.counters + MSURF_CTR_EVAL, (unsigned long long)n_eval_cta);
+    }
     atomicAdd(J.counters + MSURF_CTR_DEPOSITS, (unsigned long long)n_dep);
     atomicAdd(J.counters + MSURF_CTR_ATOMICS, (unsigned long long)n_atom);
   }

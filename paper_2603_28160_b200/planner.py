@@ -173,8 +173,14 @@ def plan(config, ext: Extensions | None = None) -> SweepPlan:
         raise ConfigError("record_trajectory is defined for the reference kinematics only")
     if p.points > MAX_POINTS:
         raise ConfigError(f"edge_point_count {p.points} exceeds the device limit {MAX_POINTS}")
-    if max(grid.m, grid.n) >= 1 << 21:
-        raise ConfigError("grid axes must have fewer than 2^21 cells")
+    # bounds of the device's fast exact cell location (msurf.cu cell_fast):
+    # node indices < 2^19 and grid origin within 2^20 cells of the frame origin
+    if max(grid.m, grid.n) >= (1 << 19) - 2:
+        raise ConfigError("grid axes must have fewer than 2^19 - 2 cells")
+    if max(abs(grid.x_min_mm), abs(grid.y_min_mm)) / grid.spacing_mm >= float(1 << 20):
+        raise ConfigError("grid origin too far from the workpiece frame origin (> 2^20 cells)")
+    if (grid.m + 1) * (grid.n + 1) >= 1 << 31:
+        raise ConfigError("grid has too many nodes for one device surface (>= 2^31)")
     return p
 
 

@@ -214,6 +214,7 @@ def run_ours(args, rank, world):
     import paper_2603_28160_b200 as ms
     from paper_2603_28160_b200 import _native, sharded
     from paper_2603_28160_b200.engine import SweepBatch
+    from paper_2603_28160_b200.pipeline import SurfacePipeline
     from paper_2603_28160_b200.planner import plan as make_plan
 
     dist = torch.distributed
@@ -227,6 +228,7 @@ def run_ours(args, rank, world):
     every = meta.get("profiles_every", 64)
     j_lo, j_hi = sharded.strip_bounds(p.grid.n + 1, world)[rank]
     batch = SweepBatch([(p, j_lo, j_hi)])
+    pipe = SurfacePipeline(batch, every=every, uncut=uncut) if world == 1 else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def barrier():
@@ -234,6 +236,10 @@ def run_ours(args, rank, world):
             dist.barrier()
 
     def step(events):
+        if pipe is not None:
+            # single GPU: sync-free launch sequence, results read after the timed region
+            pipe.enqueue(events=events)
+            return None
         batch.launch(events=events)
         res = sharded.StripResult(plan=p, j_lo=j_lo, j_hi=j_hi, heights=batch.heights()[0], counters={},
                                   cells_updated=0, main_loop_seconds=0.0, batch=batch)
@@ -258,16 +264,20 @@ def run_ours(args, rank, world):
         flush.fill_(1)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         e_end = torch.cuda.Event(enable_timing=True)
-        am, prs = step(ev)
+        out = step(ev)
         e_end.record()
         torch.cuda.synchronize()
         step_ms.append(ev[0].elapsed_time(e_end))
         sweep_ms.append(ev[1].elapsed_time(ev[2]))
-        launches += batch.launches_per_run + 2 + 2 + 2  # areal 2x(pass+finalize), profiles 2
+        launches += pipe.launches_per_run if pipe is not None else batch.launches_per_run + 6
     barrier()
     torch.cuda.synchronize()
     clk = clocks.stop()
     ctr, machined = batch.counters()
+    if pipe is not None:
+        am, prs = pipe.collect()[0]
+    else:
+        am, prs = out
 
     tot = torch.tensor([sum(step_ms), sum(sweep_ms)], dtype=torch.float64, device=dev)
     if world > 1:

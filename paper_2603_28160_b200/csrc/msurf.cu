@@ -29,6 +29,17 @@
 
 namespace {
 
+#ifndef MSURF_STALE_MODE
+#define MSURF_STALE_MODE 2  // 0: prefetched stale-read skip before each RED; 2: plain RED per run
+#endif
+
+#ifndef MSURF_MIN_BLOCKS
+#define MSURF_MIN_BLOCKS 4  // CTAs per SM the register budget is sized for (64 regs)
+#endif
+#ifndef MSURF_UNROLL2
+#define MSURF_UNROLL2 0
+#endif
+
 constexpr int kThreads = 256;
 constexpr int kTileSteps = 256;  // rows (time steps) per CTA; == kThreads
 constexpr int kWarps = kThreads / 32;
@@ -100,7 +111,7 @@ __device__ __forceinline__ void red_min_u64(unsigned long long* p, unsigned long
   asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__device__ __forceinline__ unsigned long long ld_stale_u64(const unsigned long long* p) {
+__device__ __forceinline__ __attribute__((unused)) unsigned long long ld_stale_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.cta.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
@@ -112,8 +123,100 @@ __device__ __forceinline__ unsigned warp_sum_u(unsigned v) {
   return v;
 }
 
+struct Hit {
+  int idx;        // flat node index in the owned strip, -1 if outside
+  uint64_t key;   // order-preserving key of z'
+};
+
+// Workpiece position of one edge point at one live step, and its cell
+// (engine.py:289-300): the reference's exact op order, explicit _rn ops.
+__device__ __forceinline__ double2 lds_f64x2(unsigned saddr) {
+  double2 v;
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(saddr));
+  return v;
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 4)
+__device__ __forceinline__ Hit eval_row(unsigned rv, double ax, double ay, double az,
+                                        double tsz, double tcz, uint64_t zk, double tilt_c,
+                                        double tilt_s, double zoff, double inv, double cx0, double cy0,
+                                        double x_min, double y_min, double dd, unsigned span_i, int j_lo,
+                                        unsigned span_j, int ldk, bool valid) {
+  double xw, yw;
+  uint64_t key = zk;
+  if (MODE == MSURF_MODE_REF) {
+    // engine.py:289-296: xw = ((m00*xp + m01*yp) + m02*zp) + m03
+    const double2 r01 = lds_f64x2(rv + 0);
+    const double2 r23 = lds_f64x2(rv + 16);
+    const double2 r45 = lds_f64x2(rv + 32);
+    const double2 r67 = lds_f64x2(rv + 48);
+    xw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r01.x, ax), __dmul_rn(r01.y, ay)),
+                             __dmul_rn(r23.x, az)), r23.y);
+    yw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r45.x, ax), __dmul_rn(r45.y, ay)),
+                             __dmul_rn(r67.x, az)), r67.y);
+  } else {
+    const double2 cs = lds_f64x2(rv + 0);
+    const double2 of = lds_f64x2(rv + 16);
+    const double uu = __dadd_rn(__dmul_rn(cs.x, ax), __dmul_rn(cs.y, ay));
+    const double vv = __dadd_rn(__dmul_rn(-cs.y, ax), __dmul_rn(cs.x, ay));
+    xw = __dadd_rn(uu, of.x);
+    if (MODE == MSURF_MODE_EXT_TILT) {
+      const double yv = __dsub_rn(__dmul_rn(tilt_c, vv), tsz);
+      const double zz = __dadd_rn(__dadd_rn(__dmul_rn(tilt_s, vv), tcz), zoff);
+      yw = __dadd_rn(yv, of.y);
+      key = enc_key(zz);
+    } else {
+      yw = __dadd_rn(vv, of.y);
+    }
+  }
+  CellFast ci = cell_fast(xw, inv, cx0);
+  CellFast cj = cell_fast(yw, inv, cy0);
+  // padding lanes (valid == false) sit exactly at the tool centre, which is
+  // often a cell boundary: keep them off the exact (division) path
+  if (__builtin_expect((ci.near | cj.near) & valid, 0)) {
+    ci.idx = cell_index_exact(xw, x_min, dd);
+    cj.idx = cell_index_exact(yw, y_min, dd);
+  }
+  const bool inside = valid & ((unsigned)ci.idx <= span_i) & ((unsigned)(cj.idx - j_lo) <= span_j);
+  Hit h;
+  h.idx = inside ? ci.idx * ldk + (cj.idx - j_lo) : -1;
+  h.key = key;
+  return h;
+}
+
+// Run-length min pre-reduction in registers: (last, run) is this lane's open
+// run of consecutive live steps landing in one cell; a run is flushed to HBM
+// with one fire-and-forget RED.MIN when the lane moves to another cell.
+// MSURF_STALE_MODE 0 adds a prefetched stale-read skip of flushes that
+// cannot lower the cell (heights never rise); measured slower on B200 than
+// letting the L2 atomic units absorb the REDs.
+template <int MODE>
+__device__ __forceinline__ void deposit(const Hit& h, unsigned long long* __restrict__ keys, int& last,
+                                        uint64_t& run, uint64_t& pend, unsigned& n_dep, unsigned& n_atom) {
+  if (h.idx < 0) return;
+  ++n_dep;
+  if (h.idx == last) {
+    if (MODE == MSURF_MODE_EXT_TILT) run = h.key < run ? h.key : run;
+    return;
+  }
+#if MSURF_STALE_MODE == 0
+  if (run < pend) {  // also false for the initial (-1, ~0, 0) state
+    red_min_u64(keys + last, (unsigned long long)run);
+    ++n_atom;
+  }
+  pend = ld_stale_u64(keys + h.idx);
+#else
+  if (last >= 0) {
+    red_min_u64(keys + last, (unsigned long long)run);
+    ++n_atom;
+  }
+#endif
+  last = h.idx;
+  run = h.key;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
     sweep_kernel(const msurf_job* __restrict__ jobs, int n_jobs,
                  const int64_t* __restrict__ prefix, int mask_words) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -273,6 +376,7 @@ __global__ void __launch_bounds__(kThreads, 4)
   const int ldk = (int)(J.j_hi - J.j_lo + 1);
   unsigned long long* __restrict__ keys = reinterpret_cast<unsigned long long*>(J.keys);
   const double tilt_c = J.tilt_c, tilt_s = J.tilt_s, zoff = J.zoff;
+  const unsigned rowv_s = (unsigned)__cvta_generic_to_shared(rowv);
   const int rsplit = kWarps / nchunk > 1 ? kWarps / nchunk : 1;
   const int units = nchunk * rsplit;
   unsigned n_dep = 0, n_atom = 0;
@@ -315,63 +419,34 @@ __global__ void __launch_bounds__(kThreads, 4)
         on = (mword[rr * mask_words] & bit) != 0ull;
       }
       unsigned bal2 = __ballot_sync(0xffffffffu, on);
+      // two rows per iteration: their transforms are independent (ILP), the
+      // run-length merge then consumes them in time order
       while (bal2) {
-        const int k = __ffs(bal2) - 1;
+        const int k1 = __ffs(bal2) - 1;
         bal2 &= bal2 - 1u;
-        const int r = __shfl_sync(0xffffffffu, rr, k);
-        const double* rv = rowv + r * 8;
-        double xw, yw;
-        uint64_t key = zk;
-        if (MODE == MSURF_MODE_REF) {
-          // engine.py:289-296: xw = ((m00*xp + m01*yp) + m02*zp) + m03
-          const double2 r01 = *reinterpret_cast<const double2*>(rv + 0);
-          const double2 r23 = *reinterpret_cast<const double2*>(rv + 2);
-          const double2 r45 = *reinterpret_cast<const double2*>(rv + 4);
-          const double2 r67 = *reinterpret_cast<const double2*>(rv + 6);
-          xw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r01.x, ax), __dmul_rn(r01.y, ay)),
-                                   __dmul_rn(r23.x, az)), r23.y);
-          yw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r45.x, ax), __dmul_rn(r45.y, ay)),
-                                   __dmul_rn(r67.x, az)), r67.y);
+        const int ra = __shfl_sync(0xffffffffu, rr, k1);
+        const Hit ha = eval_row<MODE>(rowv_s + ra * 64, ax, ay, az, tsz, tcz, zk, tilt_c, tilt_s, zoff,
+                                      inv, cx0, cy0, J.x_min, J.y_min, dd, span_i, j_lo, span_j, ldk,
+                                      valid);
+        if (MSURF_UNROLL2 && bal2) {
+          const int k2 = __ffs(bal2) - 1;
+          bal2 &= bal2 - 1u;
+          const int rb = __shfl_sync(0xffffffffu, rr, k2);
+          const Hit hb = eval_row<MODE>(rowv_s + rb * 64, ax, ay, az, tsz, tcz, zk, tilt_c, tilt_s, zoff,
+                                        inv, cx0, cy0, J.x_min, J.y_min, dd, span_i, j_lo, span_j, ldk,
+                                        valid);
+          deposit<MODE>(ha, keys, last, run, pend, n_dep, n_atom);
+          deposit<MODE>(hb, keys, last, run, pend, n_dep, n_atom);
         } else {
-          const double2 cs = *reinterpret_cast<const double2*>(rv + 0);
-          const double2 of = *reinterpret_cast<const double2*>(rv + 2);
-          const double uu = __dadd_rn(__dmul_rn(cs.x, ax), __dmul_rn(cs.y, ay));
-          const double vv = __dadd_rn(__dmul_rn(-cs.y, ax), __dmul_rn(cs.x, ay));
-          xw = __dadd_rn(uu, of.x);
-          if (MODE == MSURF_MODE_EXT_TILT) {
-            const double yv = __dsub_rn(__dmul_rn(tilt_c, vv), tsz);
-            const double zz = __dadd_rn(__dadd_rn(__dmul_rn(tilt_s, vv), tcz), zoff);
-            yw = __dadd_rn(yv, of.y);
-            key = enc_key(zz);
-          } else {
-            yw = __dadd_rn(vv, of.y);
-          }
-        }
-        CellFast ci = cell_fast(xw, inv, cx0);
-        CellFast cj = cell_fast(yw, inv, cy0);
-        if (__builtin_expect(ci.near | cj.near, 0)) {
-          ci.idx = cell_index_exact(xw, J.x_min, dd);
-          cj.idx = cell_index_exact(yw, J.y_min, dd);
-        }
-        const bool inside = valid & ((unsigned)ci.idx <= span_i) & ((unsigned)(cj.idx - j_lo) <= span_j);
-        if (inside) {
-          ++n_dep;
-          const int idx = ci.idx * ldk + (cj.idx - j_lo);
-          if (idx == last) {
-            if (MODE == MSURF_MODE_EXT_TILT) run = key < run ? key : run;
-          } else {
-            if (run < pend) {  // also false for the initial (-1, ~0, 0) state
-              red_min_u64(keys + last, (unsigned long long)run);
-              ++n_atom;
-            }
-            last = idx;
-            run = key;
-            pend = ld_stale_u64(keys + idx);
-          }
+          deposit<MODE>(ha, keys, last, run, pend, n_dep, n_atom);
         }
       }
     }
+#if MSURF_STALE_MODE == 0
     if (run < pend) {
+#else
+    if (last >= 0) {
+#endif
       red_min_u64(keys + last, (unsigned long long)run);
       ++n_atom;
     }

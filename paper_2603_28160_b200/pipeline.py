@@ -1,0 +1,102 @@
+"""Resident-input surface pipeline: the whole hot path of one batch of
+surfaces as a sync-free launch sequence (optionally captured in a CUDA graph).
+
+    fill -> sweep -> decode -> areal pass1 -> areal pass2 -> profiles
+
+Everything is preallocated, no host synchronisation sits between launches,
+and ``collect()`` reads all results back with one D2H copy. This is what the
+benchmark times as a "step"; ``simulate`` + ``areal_metrics`` is the same
+work through the drop-in API (with host planning and copies per call).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native
+from .engine import SweepBatch
+from .errors import ConfigError
+from .roughness import _finish_areal, _finish_profile
+
+
+class SurfacePipeline:
+    def __init__(self, batch: SweepBatch, every: int | None = 64, uncut: str = "exclude"):
+        torch = _native.require_cuda()
+        self.torch = torch
+        self.lib = _native.lib()
+        self.batch = batch
+        s0 = batch.surfs[0]
+        if not batch.same_shape or any(s.j_lo != 0 or s.j_hi != s.plan.grid.n for s in batch.surfs):
+            raise ConfigError("SurfacePipeline needs whole, same-shape surfaces (use sharded.* for strips)")
+        self.grid = s0.plan.grid
+        self.n = batch.n
+        self.uncut = uncut
+        self.exclude = int(uncut == "exclude")
+        g = self.grid
+        self.ld = g.n + 1
+        self.nodes = (g.m + 1) * (g.n + 1)
+        self.rows_idx = list(range(0, g.m + 1, every)) if every else []
+        dev = batch.dev
+        n = self.n
+        self.work = torch.empty(n * _native.RED_BLOCKS * 5, dtype=torch.float64, device=dev)
+        self.out = torch.empty(n * 9 + max(1, n * len(self.rows_idx) * 8), dtype=torch.float64, device=dev)
+        self.starts = torch.tensor([i * self.ld for i in self.rows_idx] or [0], dtype=torch.int64, device=dev)
+        self.graph = None
+        self.launches_per_run = batch.launches_per_run + 4 + (1 if self.rows_idx else 0)
+
+    def enqueue(self, events=None):
+        """Launch the full step on the current stream; no host sync."""
+        lib, b = self.lib, self.batch
+        sp = _native.stream_ptr()
+        b.launch(events=events)
+        h = b.keys.data_ptr()
+        sent = b.base + b.sentinel_off
+        o = self.out.data_ptr()
+        n = self.n
+        g = self.grid
+        _native.check(lib.msurf_areal_pass1(h, self.ld, self.nodes, n, 0, 0, g.m + 1, g.n + 1, sent,
+                                            self.exclude, self.work.data_ptr(), o, sp))
+        _native.check(lib.msurf_areal_pass2(h, self.ld, self.nodes, n, 0, 0, g.m + 1, g.n + 1, sent,
+                                            self.exclude, o, self.work.data_ptr(), o + n * 5 * 8, sp))
+        if self.rows_idx:
+            _native.check(lib.msurf_profiles(h, self.nodes, n, self.starts.data_ptr(), len(self.rows_idx),
+                                             g.n + 1, 1, sent, self.exclude, None, o + n * 9 * 8, sp))
+
+    def capture(self):
+        """Capture enqueue() into a CUDA graph (replayed by run())."""
+        torch = self.torch
+        self.enqueue()  # warm the lazy module/kernel loading outside capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.enqueue()
+        self.graph = g
+        return g
+
+    def run(self):
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.enqueue()
+
+    def collect(self):
+        """One D2H: per surface (ArealMetrics | DomainError, [ProfileRoughness])."""
+        a = self.out.cpu().numpy()
+        n = self.n
+        st1 = a[: n * 5].reshape(n, 5)
+        st2 = a[n * 5: n * 9].reshape(n, 4)
+        prof = a[n * 9: n * 9 + n * len(self.rows_idx) * 8].reshape(n, len(self.rows_idx), 8)
+        res = []
+        for s in range(n):
+            try:
+                am = _finish_areal(st1[s], st2[s], self.uncut)
+            except Exception as exc:  # DomainError per sample
+                am = exc
+            prs = []
+            for r, i in zip(prof[s], self.rows_idx):
+                try:
+                    prs.append(_finish_profile(r, i, self.uncut))
+                except Exception as exc:
+                    prs.append(exc)
+            res.append((am, prs))
+        return res

@@ -151,7 +151,7 @@ def areal_metrics_strip(res: StripResult, roi=None, uncut: str = "raise", group=
         _native.check(lib.msurf_areal_pass1(res.heights.data_ptr(), ld, 0, 1, i_lo, jl, rows, cols,
                                             sent.data_ptr(), ex, work.data_ptr(), st1.data_ptr(), sp))
     combine(st1, STATS1_SUM, STATS1_MAX, STATS1_MIN, group)
-    if box is not None and float(st1[0, 3]) > 0:
+    if box is not None:  # an all-excluded ROI yields n = 0 and is rejected on the host
         i_lo, jl, rows, cols = box
         _native.check(lib.msurf_areal_pass2(res.heights.data_ptr(), ld, 0, 1, i_lo, jl, rows, cols,
                                             sent.data_ptr(), ex, st1.data_ptr(), work.data_ptr(),

@@ -291,7 +291,12 @@ def run_ours(args, rank, world):
     mode = p.mode
     evald = int(ctr[0][1])
     live = int(ctr[0][0])
+    engaged = int(ctr[0][4])
     flops = FLOPS_PER_POINT[mode] * evald + FLOPS_PER_ROW * live
+    # SURVEY §8(d) definition: P_eng = points of rows whose whole-tooth 2-D box
+    # meets the window (row-level cull); the kernel's chunk-level cull skips
+    # part of that work, so this fraction also credits the finer cull
+    flops_survey = FLOPS_PER_POINT[mode] * engaged * p.points + FLOPS_PER_ROW * engaged
     lib = _native.lib()
     import ctypes
 
@@ -310,6 +315,9 @@ def run_ours(args, rank, world):
                        "(MEASURED_PEAKS.json has no FP64 entry)",
         "flops_per_launch": flops,
         "flops_model": f"{FLOPS_PER_POINT[mode]} x points_evaluated + {FLOPS_PER_ROW} x live rows",
+        "survey_def": {"P_eng": engaged * p.points, "engaged_rows": engaged,
+                       "achieved": flops_survey / (sweep_ms_avg * 1e-3) / 1e12,
+                       "frac": flops_survey / (sweep_ms_avg * 1e-3) / fp64_peak},
         "points_evaluated": evald, "live_rows": live, "deposits": int(ctr[0][2]),
         "atomics": int(ctr[0][3]),
         "atomic_rate_per_s": int(ctr[0][3]) / (sweep_ms_avg * 1e-3),

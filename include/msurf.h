@@ -27,11 +27,12 @@ extern "C" {
 #define MSURF_MODE_EXT 1      /* rotated tool-frame points, z' time-invariant   */
 #define MSURF_MODE_EXT_TILT 2 /* rotated tool-frame points + lead tilt (z' per step) */
 
-#define MSURF_CTR_LIVE_ROWS 0  /* (step, tooth, pass) rows surviving the 2-D cull */
-#define MSURF_CTR_EVAL 1       /* edge points evaluated (P_eng, chunk granularity) */
-#define MSURF_CTR_DEPOSITS 2   /* points landing in the owned grid (P_in)          */
-#define MSURF_CTR_ATOMICS 3    /* atomicMin issued after run-length/stale-read skip */
-#define MSURF_NUM_CTRS 4
+#define MSURF_CTR_LIVE_ROWS 0  /* (step, tooth, pass) rows with >= 1 chunk surviving the 2-D cull */
+#define MSURF_CTR_EVAL 1       /* edge points evaluated (points of surviving 32-point chunks)    */
+#define MSURF_CTR_DEPOSITS 2   /* evaluated points landing in the owned grid (P_in)              */
+#define MSURF_CTR_ATOMICS 3    /* RED.MIN issued after the time-neighbour pre-reduction          */
+#define MSURF_CTR_ENGAGED_ROWS 4 /* rows whose whole-tooth 2-D box meets the window (SURVEY P_eng/N) */
+#define MSURF_NUM_CTRS 5
 
 /* One surface sweep (one parameter set; one strip of it under sharding).
  * Replaces the per-worker body engine.py:215-313 (_run_step_range) for all
@@ -50,10 +51,11 @@ typedef struct msurf_job {
   /* per-tooth / per-point device arrays */
   const double* tooth_base;  /* [teeth] phase + (2pi)(K-1)/Z (kinematics.py:76)      */
   const double* tooth_rows;  /* REF: [teeth][8] e00 e01 e02 e03 e10 e11 e12 e13      */
-  const double* px;          /* REF: edge x [points]; EXT: tool-frame x [teeth][points] */
-  const double* py;
-  const double* pz;
-  const uint64_t* zkey;      /* [teeth][points] keys of z' (REF, EXT without tilt)    */
+  const double* pts;         /* [teeth][points][4] per-point record (16-B aligned):
+                              * REF      (xp, yp, zp, key of z')  edge frame
+                              * EXT      (xt, yt, key of z', 0)   tool frame
+                              * EXT_TILT (xt, yt, sin(tau)*zt, cos(tau)*zt)        */
+  const double* tooth_box;   /* [teeth][6] whole-tooth tool-frame box (P_eng counter)  */
   const double* chunk_box;   /* [teeth][nchunk][6] tool-frame xlo xhi ylo yhi zlo zhi */
   const double* pass_x0;     /* [passes] spindle x of each raster pass               */
   /* extended kinematics */

@@ -19,7 +19,7 @@ from .errors import MillsurfError, NativeUnavailableError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MSURF_LIB") or os.path.join(_HERE, "libmsurf.so")
 ABI_VERSION = 1
-NUM_CTRS = 4
+NUM_CTRS = 5
 RED_BLOCKS = 256
 
 c_double, c_int64, c_int32, c_void_p = ctypes.c_double, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
@@ -35,8 +35,7 @@ class MsurfJob(ctypes.Structure):
         ("t_start", c_double), ("dt", c_double), ("steps", c_int64),
         ("y0", c_double), ("feed_speed", c_double), ("omega", c_double),
         ("tooth_base", c_void_p), ("tooth_rows", c_void_p),
-        ("px", c_void_p), ("py", c_void_p), ("pz", c_void_p),
-        ("zkey", c_void_p), ("chunk_box", c_void_p), ("pass_x0", c_void_p),
+        ("pts", c_void_p), ("tooth_box", c_void_p), ("chunk_box", c_void_p), ("pass_x0", c_void_p),
         ("tilt_c", c_double), ("tilt_s", c_double), ("zoff", c_double),
         ("vib_amp", c_double), ("vib_omega", c_double), ("vib_phase", c_double),
         ("trig_table", c_void_p), ("vib_table", c_void_p),

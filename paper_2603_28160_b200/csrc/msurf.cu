@@ -29,15 +29,8 @@
 
 namespace {
 
-#ifndef MSURF_STALE_MODE
-#define MSURF_STALE_MODE 2  // 0: prefetched stale-read skip before each RED; 2: plain RED per run
-#endif
-
 #ifndef MSURF_MIN_BLOCKS
-#define MSURF_MIN_BLOCKS 4  // CTAs per SM the register budget is sized for (64 regs)
-#endif
-#ifndef MSURF_UNROLL2
-#define MSURF_UNROLL2 0
+#define MSURF_MIN_BLOCKS 4  // CTAs per SM the register budget is sized for
 #endif
 
 constexpr int kThreads = 256;
@@ -111,11 +104,6 @@ __device__ __forceinline__ void red_min_u64(unsigned long long* p, unsigned long
   asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__device__ __forceinline__ __attribute__((unused)) unsigned long long ld_stale_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.cta.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
-  return v;
-}
 
 __device__ __forceinline__ unsigned warp_sum_u(unsigned v) {
 #pragma unroll
@@ -123,109 +111,19 @@ __device__ __forceinline__ unsigned warp_sum_u(unsigned v) {
   return v;
 }
 
-struct Hit {
-  int idx;        // flat node index in the owned strip, -1 if outside
-  uint64_t key;   // order-preserving key of z'
-};
-
-// Workpiece position of one edge point at one live step, and its cell
-// (engine.py:289-300): the reference's exact op order, explicit _rn ops.
-__device__ __forceinline__ double2 lds_f64x2(unsigned saddr) {
-  double2 v;
-  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(saddr));
-  return v;
-}
-
-template <int MODE>
-__device__ __forceinline__ Hit eval_row(unsigned rv, double ax, double ay, double az,
-                                        double tsz, double tcz, uint64_t zk, double tilt_c,
-                                        double tilt_s, double zoff, double inv, double cx0, double cy0,
-                                        double x_min, double y_min, double dd, unsigned span_i, int j_lo,
-                                        unsigned span_j, int ldk, bool valid) {
-  double xw, yw;
-  uint64_t key = zk;
-  if (MODE == MSURF_MODE_REF) {
-    // engine.py:289-296: xw = ((m00*xp + m01*yp) + m02*zp) + m03
-    const double2 r01 = lds_f64x2(rv + 0);
-    const double2 r23 = lds_f64x2(rv + 16);
-    const double2 r45 = lds_f64x2(rv + 32);
-    const double2 r67 = lds_f64x2(rv + 48);
-    xw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r01.x, ax), __dmul_rn(r01.y, ay)),
-                             __dmul_rn(r23.x, az)), r23.y);
-    yw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r45.x, ax), __dmul_rn(r45.y, ay)),
-                             __dmul_rn(r67.x, az)), r67.y);
-  } else {
-    const double2 cs = lds_f64x2(rv + 0);
-    const double2 of = lds_f64x2(rv + 16);
-    const double uu = __dadd_rn(__dmul_rn(cs.x, ax), __dmul_rn(cs.y, ay));
-    const double vv = __dadd_rn(__dmul_rn(-cs.y, ax), __dmul_rn(cs.x, ay));
-    xw = __dadd_rn(uu, of.x);
-    if (MODE == MSURF_MODE_EXT_TILT) {
-      const double yv = __dsub_rn(__dmul_rn(tilt_c, vv), tsz);
-      const double zz = __dadd_rn(__dadd_rn(__dmul_rn(tilt_s, vv), tcz), zoff);
-      yw = __dadd_rn(yv, of.y);
-      key = enc_key(zz);
-    } else {
-      yw = __dadd_rn(vv, of.y);
-    }
-  }
-  CellFast ci = cell_fast(xw, inv, cx0);
-  CellFast cj = cell_fast(yw, inv, cy0);
-  // padding lanes (valid == false) sit exactly at the tool centre, which is
-  // often a cell boundary: keep them off the exact (division) path
-  if (__builtin_expect((ci.near | cj.near) & valid, 0)) {
-    ci.idx = cell_index_exact(xw, x_min, dd);
-    cj.idx = cell_index_exact(yw, y_min, dd);
-  }
-  const bool inside = valid & ((unsigned)ci.idx <= span_i) & ((unsigned)(cj.idx - j_lo) <= span_j);
-  Hit h;
-  h.idx = inside ? ci.idx * ldk + (cj.idx - j_lo) : -1;
-  h.key = key;
-  return h;
-}
-
-// Run-length min pre-reduction in registers: (last, run) is this lane's open
-// run of consecutive live steps landing in one cell; a run is flushed to HBM
-// with one fire-and-forget RED.MIN when the lane moves to another cell.
-// MSURF_STALE_MODE 0 adds a prefetched stale-read skip of flushes that
-// cannot lower the cell (heights never rise); measured slower on B200 than
-// letting the L2 atomic units absorb the REDs.
-template <int MODE>
-__device__ __forceinline__ void deposit(const Hit& h, unsigned long long* __restrict__ keys, int& last,
-                                        uint64_t& run, uint64_t& pend, unsigned& n_dep, unsigned& n_atom) {
-  if (h.idx < 0) return;
-  ++n_dep;
-  if (h.idx == last) {
-    if (MODE == MSURF_MODE_EXT_TILT) run = h.key < run ? h.key : run;
-    return;
-  }
-#if MSURF_STALE_MODE == 0
-  if (run < pend) {  // also false for the initial (-1, ~0, 0) state
-    red_min_u64(keys + last, (unsigned long long)run);
-    ++n_atom;
-  }
-  pend = ld_stale_u64(keys + h.idx);
-#else
-  if (last >= 0) {
-    red_min_u64(keys + last, (unsigned long long)run);
-    ++n_atom;
-  }
-#endif
-  last = h.idx;
-  run = h.key;
-}
-
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
     sweep_kernel(const msurf_job* __restrict__ jobs, int n_jobs,
                  const int64_t* __restrict__ prefix, int mask_words) {
+  constexpr int RW = MODE == MSURF_MODE_REF ? 8 : 4;  // doubles of row data per live step
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* rowv = reinterpret_cast<double*>(smem_raw);                        // [T][8]
-  uint64_t* masks = reinterpret_cast<uint64_t*>(rowv + kTileSteps * 8);      // [T][W]
-  int* live = reinterpret_cast<int*>(masks + kTileSteps * mask_words);       // [T]
+  double* rowv = reinterpret_cast<double*>(smem_raw);                        // [T][8] by live slot
+  uint64_t* masks = reinterpret_cast<uint64_t*>(rowv + kTileSteps * 8);      // [T][W] by thread
+  int* live = reinterpret_cast<int*>(masks + kTileSteps * mask_words);       // [T] slot -> thread
   __shared__ msurf_job J;
   __shared__ int warp_cnt[kWarps];
   __shared__ unsigned warp_eval[kWarps];
+  __shared__ unsigned warp_eng[kWarps];
   __shared__ int s_job;
 
   const int tid = threadIdx.x;
@@ -258,10 +156,12 @@ __global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
   const int npts = J.points;
   const int nchunk = (npts + 31) >> 5;
   const double dd = J.spacing;
+  const double4* __restrict__ pts = reinterpret_cast<const double4*>(J.pts) + (long long)tooth * npts;
 
   // ---------------- phase 1: one thread per time step of the tile
-  bool any = false;
+  bool any = false, engaged = false;
   unsigned my_eval = 0;
+  double rd[RW];
   {
     const double wx_lo = J.x_min - 1.5 * dd;
     const double wx_hi = J.x_min + (double)J.m * dd + 1.5 * dd;
@@ -289,84 +189,103 @@ __global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
                                       : msurf_sin(__dadd_rn(__dmul_rn(J.vib_omega, t), J.vib_phase));
         xoff = __dadd_rn(xoff, __dmul_rn(J.vib_amp, sv));
       }
-      double* rv = rowv + tid * 8;
       if (MODE == MSURF_MODE_REF) {
         // engine.py:257-264 composite coefficients, exact op order
         const double* e = J.tooth_rows + tooth * 8;
-        rv[0] = __dadd_rn(__dmul_rn(c, e[0]), __dmul_rn(sn, e[4]));
-        rv[1] = __dadd_rn(__dmul_rn(c, e[1]), __dmul_rn(sn, e[5]));
-        rv[2] = __dadd_rn(__dmul_rn(c, e[2]), __dmul_rn(sn, e[6]));
-        rv[3] = __dadd_rn(__dadd_rn(__dmul_rn(c, e[3]), __dmul_rn(sn, e[7])), xoff);
-        rv[4] = __dadd_rn(__dmul_rn(ns, e[0]), __dmul_rn(c, e[4]));
-        rv[5] = __dadd_rn(__dmul_rn(ns, e[1]), __dmul_rn(c, e[5]));
-        rv[6] = __dadd_rn(__dmul_rn(ns, e[2]), __dmul_rn(c, e[6]));
-        rv[7] = __dadd_rn(__dadd_rn(__dmul_rn(ns, e[3]), __dmul_rn(c, e[7])), ty);
+        rd[0] = __dadd_rn(__dmul_rn(c, e[0]), __dmul_rn(sn, e[4]));
+        rd[1] = __dadd_rn(__dmul_rn(c, e[1]), __dmul_rn(sn, e[5]));
+        rd[2] = __dadd_rn(__dmul_rn(c, e[2]), __dmul_rn(sn, e[6]));
+        rd[3] = __dadd_rn(__dadd_rn(__dmul_rn(c, e[3]), __dmul_rn(sn, e[7])), xoff);
+        rd[4] = __dadd_rn(__dmul_rn(ns, e[0]), __dmul_rn(c, e[4]));
+        rd[5] = __dadd_rn(__dmul_rn(ns, e[1]), __dmul_rn(c, e[5]));
+        rd[6] = __dadd_rn(__dmul_rn(ns, e[2]), __dmul_rn(c, e[6]));
+        rd[7] = __dadd_rn(__dadd_rn(__dmul_rn(ns, e[3]), __dmul_rn(c, e[7])), ty);
         if (J.traj && pass == 0) {
           // engine.py:266-270: min-z edge point of this (step, tooth)
-          const int p = J.min_index[tooth];
-          const double xp = J.px[p], yp = J.py[p], zp = J.pz[p];
+          const double4 pt = pts[J.min_index[tooth]];
           double* tr = J.traj + (s * J.teeth + tooth) * 3;
-          tr[0] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(rv[0], xp), __dmul_rn(rv[1], yp)),
-                                      __dmul_rn(rv[2], zp)), rv[3]);
-          tr[1] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(rv[4], xp), __dmul_rn(rv[5], yp)),
-                                      __dmul_rn(rv[6], zp)), rv[7]);
-          tr[2] = dec_key(J.zkey[(long long)tooth * J.points + p]);
+          tr[0] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(rd[0], pt.x), __dmul_rn(rd[1], pt.y)),
+                                      __dmul_rn(rd[2], pt.z)), rd[3]);
+          tr[1] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(rd[4], pt.x), __dmul_rn(rd[5], pt.y)),
+                                      __dmul_rn(rd[6], pt.z)), rd[7]);
+          tr[2] = dec_key((uint64_t)__double_as_longlong(pt.w));
         }
       } else {
-        rv[0] = c;
-        rv[1] = sn;
-        rv[2] = xoff;
-        rv[3] = ty;
+        rd[0] = c;
+        rd[1] = sn;
+        rd[2] = xoff;
+        rd[3] = ty;
       }
-      // 2-D chunk cull; conservative by 1.5 cells >> rounding differences
-      const double* box = J.chunk_box + (long long)tooth * nchunk * 6;
-      unsigned kept = 0;
-      for (int q = 0; q < nchunk; ++q) {
-        const double xl = box[q * 6 + 0], xh = box[q * 6 + 1];
-        const double yl = box[q * 6 + 2], yh = box[q * 6 + 3];
+      // 2-D box test of one tool-frame box at this step (conservative by 1.5
+      // cells >> rounding differences between this bound and the kernel)
+      auto box_hits = [&](const double* b) -> bool {
+        const double xl = b[0], xh = b[1], yl = b[2], yh = b[3];
         const double x_lo = fmin(c * xl, c * xh) + fmin(sn * yl, sn * yh) + xoff;
         const double x_hi = fmax(c * xl, c * xh) + fmax(sn * yl, sn * yh) + xoff;
         double v_lo = fmin(ns * xl, ns * xh) + fmin(c * yl, c * yh);
         double v_hi = fmax(ns * xl, ns * xh) + fmax(c * yl, c * yh);
         if (MODE == MSURF_MODE_EXT_TILT) {
-          const double zl = box[q * 6 + 4], zh = box[q * 6 + 5];
           const double a1 = J.tilt_c * v_lo, a2 = J.tilt_c * v_hi;
-          const double b1 = J.tilt_s * zl, b2 = J.tilt_s * zh;
+          const double b1 = J.tilt_s * b[4], b2 = J.tilt_s * b[5];
           v_lo = fmin(a1, a2) - fmax(b1, b2);
           v_hi = fmax(a1, a2) - fmin(b1, b2);
         }
-        const bool keep = (x_hi >= wx_lo) & (x_lo <= wx_hi) & (v_hi + ty >= wy_lo) &
-                          (v_lo + ty <= wy_hi);
-        if (keep) {
-          my_mask[q >> 6] |= 1ull << (q & 63);
-          kept += (q == nchunk - 1) ? (unsigned)(npts - 32 * q) : 32u;
+        return (x_hi >= wx_lo) & (x_lo <= wx_hi) & (v_hi + ty >= wy_lo) & (v_lo + ty <= wy_hi);
+      };
+      engaged = box_hits(J.tooth_box + tooth * 6);
+      if (engaged) {
+        const double* box = J.chunk_box + (long long)tooth * nchunk * 6;
+        unsigned kept = 0;
+        for (int q = 0; q < nchunk; ++q) {
+          if (box_hits(box + q * 6)) {
+            my_mask[q >> 6] |= 1ull << (q & 63);
+            kept += (q == nchunk - 1) ? (unsigned)(npts - 32 * q) : 32u;
+          }
         }
+        any = kept != 0;
+        my_eval = kept;
       }
-      any = kept != 0;
-      my_eval = kept;
     }
   }
-  // ordered compaction of live steps (keeps time order for the run-length merge)
+  // ordered compaction of live steps (keeps time order for the neighbour merge)
   const unsigned bal = __ballot_sync(0xffffffffu, any);
+  const unsigned eng = __popc(__ballot_sync(0xffffffffu, engaged));
   my_eval = warp_sum_u(my_eval);
   if (lane == 0) {
     warp_cnt[warp] = __popc(bal);
     warp_eval[warp] = my_eval;
+    warp_eng[warp] = eng;
   }
   __syncthreads();
   int base = 0, n_live = 0;
-  unsigned n_eval_cta = 0;
+  unsigned n_eval_cta = 0, n_eng_cta = 0;
 #pragma unroll
   for (int w = 0; w < kWarps; ++w) {
     if (w < warp) base += warp_cnt[w];
     n_live += warp_cnt[w];
     n_eval_cta += warp_eval[w];
+    n_eng_cta += warp_eng[w];
   }
-  if (any) live[base + __popc(bal & ((1u << lane) - 1u))] = tid;
+  if (any) {
+    const int slot = base + __popc(bal & ((1u << lane) - 1u));
+    live[slot] = tid;
+#pragma unroll
+    for (int k = 0; k < RW; ++k) rowv[slot * 8 + k] = rd[k];
+  }
   __syncthreads();
-  if (n_live == 0) return;
+  if (n_live == 0) {
+    if (tid == 0 && J.counters && n_eng_cta)
+      atomicAdd(J.counters + MSURF_CTR_ENGAGED_ROWS, (unsigned long long)n_eng_cta);
+    return;
+  }
 
-  // ---------------- phase 2: warp = 32-point chunk, lane = edge point
+  // ---------------- phase 2: lane = live step, warp walks the 32 points of a chunk
+  // unit = (group of 32 consecutive live steps, 32-point chunk). Each lane
+  // keeps its step's transform in registers; the chunk's point records are
+  // warp-broadcast loads (L1-resident). Consecutive live steps of one point
+  // sit in neighbouring lanes: a lane whose cell equals its predecessor's and
+  // whose key is not lower skips its deposit (the predecessor's run covers it),
+  // so each run of a point through a cell costs one RED.MIN.
   const double inv = 1.0 / dd;
   const double cx0 = 0.5 - J.x_min * inv;
   const double cy0 = 0.5 - J.y_min * inv;
@@ -376,79 +295,77 @@ __global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
   const int ldk = (int)(J.j_hi - J.j_lo + 1);
   unsigned long long* __restrict__ keys = reinterpret_cast<unsigned long long*>(J.keys);
   const double tilt_c = J.tilt_c, tilt_s = J.tilt_s, zoff = J.zoff;
-  const unsigned rowv_s = (unsigned)__cvta_generic_to_shared(rowv);
-  const int rsplit = kWarps / nchunk > 1 ? kWarps / nchunk : 1;
-  const int units = nchunk * rsplit;
+  const int groups = (n_live + 31) >> 5;
+  const int units = groups * nchunk;
   unsigned n_dep = 0, n_atom = 0;
 
   for (int u = warp; u < units; u += kWarps) {
-    const int q = u % nchunk;
-    const int part = u / nchunk;
-    const int r0 = (int)((long long)part * n_live / rsplit);
-    const int r1 = (int)((long long)(part + 1) * n_live / rsplit);
-    const int p = q * 32 + lane;
-    const bool valid = p < npts;
-    const uint64_t bit = 1ull << (q & 63);
-    const uint64_t* mword = masks + (q >> 6);
-    double ax = 0.0, ay = 0.0, az = 0.0, tsz = 0.0, tcz = 0.0;
-    uint64_t zk = ~0ull;
-    if (valid) {
-      const long long o = MODE == MSURF_MODE_REF ? (long long)p : (long long)tooth * npts + p;
-      ax = J.px[o];
-      ay = J.py[o];
-      az = J.pz[o];
-      if (MODE != MSURF_MODE_EXT_TILT) zk = J.zkey[(long long)tooth * npts + p];
-      if (MODE == MSURF_MODE_EXT_TILT) {
-        tsz = __dmul_rn(tilt_s, az);  // time-invariant halves of the tilt products
-        tcz = __dmul_rn(tilt_c, az);
-      }
+    const int g = u / nchunk;
+    const int q = u - g * nchunk;
+    const int slot = g * 32 + lane;
+    bool on = false;
+    double r[RW];
+    if (slot < n_live) {
+      const int rt = live[slot];
+      on = (masks[rt * mask_words + (q >> 6)] >> (q & 63)) & 1ull;
+#pragma unroll
+      for (int k = 0; k < RW; ++k) r[k] = rowv[slot * 8 + k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < RW; ++k) r[k] = 0.0;
     }
-    // run-length min pre-reduction in registers: (last, run) is this lane's
-    // open run of consecutive live steps landing in one cell; pend is that
-    // cell's stored key, prefetched when the run opened (stale reads only
-    // over-estimate: heights never rise), so the atomicMin is issued only
-    // when it can lower the cell and the load latency hides behind the run.
-    int last = -1;
-    uint64_t run = ~0ull, pend = 0ull;
-    for (int l0 = r0; l0 < r1; l0 += 32) {
-      const int li = l0 + lane;
-      int rr = 0;
-      bool on = false;
-      if (li < r1) {
-        rr = live[li];
-        on = (mword[rr * mask_words] & bit) != 0ull;
-      }
-      unsigned bal2 = __ballot_sync(0xffffffffu, on);
-      // two rows per iteration: their transforms are independent (ILP), the
-      // run-length merge then consumes them in time order
-      while (bal2) {
-        const int k1 = __ffs(bal2) - 1;
-        bal2 &= bal2 - 1u;
-        const int ra = __shfl_sync(0xffffffffu, rr, k1);
-        const Hit ha = eval_row<MODE>(rowv_s + ra * 64, ax, ay, az, tsz, tcz, zk, tilt_c, tilt_s, zoff,
-                                      inv, cx0, cy0, J.x_min, J.y_min, dd, span_i, j_lo, span_j, ldk,
-                                      valid);
-        if (MSURF_UNROLL2 && bal2) {
-          const int k2 = __ffs(bal2) - 1;
-          bal2 &= bal2 - 1u;
-          const int rb = __shfl_sync(0xffffffffu, rr, k2);
-          const Hit hb = eval_row<MODE>(rowv_s + rb * 64, ax, ay, az, tsz, tcz, zk, tilt_c, tilt_s, zoff,
-                                        inv, cx0, cy0, J.x_min, J.y_min, dd, span_i, j_lo, span_j, ldk,
-                                        valid);
-          deposit<MODE>(ha, keys, last, run, pend, n_dep, n_atom);
-          deposit<MODE>(hb, keys, last, run, pend, n_dep, n_atom);
+    if (!__any_sync(0xffffffffu, on)) continue;
+    const int p_end = min(32, npts - q * 32);
+    const double4* __restrict__ pc = pts + q * 32;
+#pragma unroll 2
+    for (int k = 0; k < p_end; ++k) {
+      const double4 pt = pc[k];  // same address in every lane: one broadcast load
+      double xw, yw;
+      uint64_t key;
+      if (MODE == MSURF_MODE_REF) {
+        // engine.py:289-296: xw = ((m00*xp + m01*yp) + m02*zp) + m03
+        xw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r[0], pt.x), __dmul_rn(r[1], pt.y)),
+                                 __dmul_rn(r[2], pt.z)), r[3]);
+        yw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r[4], pt.x), __dmul_rn(r[5], pt.y)),
+                                 __dmul_rn(r[6], pt.z)), r[7]);
+        key = (uint64_t)__double_as_longlong(pt.w);
+      } else {
+        const double uu = __dadd_rn(__dmul_rn(r[0], pt.x), __dmul_rn(r[1], pt.y));
+        const double vv = __dadd_rn(__dmul_rn(-r[1], pt.x), __dmul_rn(r[0], pt.y));
+        xw = __dadd_rn(uu, r[2]);
+        if (MODE == MSURF_MODE_EXT_TILT) {
+          // y' = cos(tau) v - sin(tau) z ; z' = (sin(tau) v + cos(tau) z) + zoff
+          const double yv = __dsub_rn(__dmul_rn(tilt_c, vv), pt.z);
+          const double zz = __dadd_rn(__dadd_rn(__dmul_rn(tilt_s, vv), pt.w), zoff);
+          yw = __dadd_rn(yv, r[3]);
+          key = enc_key(zz);
         } else {
-          deposit<MODE>(ha, keys, last, run, pend, n_dep, n_atom);
+          yw = __dadd_rn(vv, r[3]);
+          key = (uint64_t)__double_as_longlong(pt.z);
         }
       }
-    }
-#if MSURF_STALE_MODE == 0
-    if (run < pend) {
-#else
-    if (last >= 0) {
-#endif
-      red_min_u64(keys + last, (unsigned long long)run);
-      ++n_atom;
+      CellFast ci = cell_fast(xw, inv, cx0);
+      CellFast cj = cell_fast(yw, inv, cy0);
+      if (__builtin_expect((ci.near | cj.near) & on, 0)) {
+        ci.idx = cell_index_exact(xw, J.x_min, dd);
+        cj.idx = cell_index_exact(yw, J.y_min, dd);
+      }
+      const bool inside = on & ((unsigned)ci.idx <= span_i) & ((unsigned)(cj.idx - j_lo) <= span_j);
+      const int idx = inside ? ci.idx * ldk + (cj.idx - j_lo) : -1;
+      // time-neighbour pre-reduction
+      const int idx_prev = __shfl_up_sync(0xffffffffu, idx, 1);
+      bool skip = (lane > 0) & (idx == idx_prev);
+      if (MODE == MSURF_MODE_EXT_TILT) {
+        const uint64_t key_prev = __shfl_up_sync(0xffffffffu, key, 1);
+        skip &= key >= key_prev;
+      }
+      if (inside) {
+        ++n_dep;
+        if (!skip) {
+          red_min_u64(keys + idx, (unsigned long long)key);
+          ++n_atom;
+        }
+      }
     }
   }
 
@@ -459,6 +376,7 @@ __global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
     if (warp == 0) {
       atomicAdd(J.counters + MSURF_CTR_LIVE_ROWS, (unsigned long long)n_live);
       atomicAdd(J.counters + MSURF_CTR_EVAL, (unsigned long long)n_eval_cta);
+      atomicAdd(J.counters + MSURF_CTR_ENGAGED_ROWS, (unsigned long long)n_eng_cta);
     }
     atomicAdd(J.counters + MSURF_CTR_DEPOSITS, (unsigned long long)n_dep);
     atomicAdd(J.counters + MSURF_CTR_ATOMICS, (unsigned long long)n_atom);

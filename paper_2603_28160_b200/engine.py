@@ -121,8 +121,8 @@ class SweepBatch:
             o = dict(
                 tooth_base=ar.add(p.tooth_base.astype(np.float64)),
                 tooth_rows=ar.add(p.tooth_rows.astype(np.float64)),
-                px=ar.add(p.px), py=ar.add(p.py), pz=ar.add(p.pz),
-                zkey=ar.add(p.zkey.astype(np.uint64)),
+                pts=ar.add(p.pts.astype(np.float64)),
+                tooth_box=ar.add(p.tooth_box.astype(np.float64)),
                 chunk_box=ar.add(p.chunk_box.astype(np.float64)),
                 pass_x0=ar.add(p.pass_x0.astype(np.float64)),
                 min_index=ar.add(p.min_index.astype(np.int32)),
@@ -174,7 +174,7 @@ class SweepBatch:
                     j.keys = keys_ptr + s.key_off * 8
                     j.t_start, j.dt, j.steps = p.t_start, p.dt, p.steps
                     j.y0, j.feed_speed, j.omega = p.y0, p.feed_speed, p.omega
-                    for name in ("tooth_base", "tooth_rows", "px", "py", "pz", "zkey", "chunk_box",
+                    for name in ("tooth_base", "tooth_rows", "pts", "tooth_box", "chunk_box",
                                  "pass_x0", "min_index"):
                         setattr(j, name, base + o[name])
                     j.counters = base + self.ctr_off + i * _native.NUM_CTRS * 8
@@ -264,7 +264,7 @@ def sweep_plans(surfaces, trig: str = "device", device=None):
 
 def _counters_dict(row) -> dict:
     return {"live_rows": int(row[0]), "points_evaluated": int(row[1]),
-            "deposits": int(row[2]), "atomics": int(row[3])}
+            "deposits": int(row[2]), "atomics": int(row[3]), "engaged_rows": int(row[4])}
 
 
 def _build_trajectory(p: SweepPlan, traj_dev) -> TrajectoryRecord:

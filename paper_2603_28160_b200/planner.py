@@ -88,6 +88,8 @@ class SweepPlan:
     vib_omega: float = 0.0
     vib_phase: float = 0.0
     record: bool = False
+    pts: np.ndarray | None = None        # (Z, N, 4) device point records (msurf_job.pts)
+    tooth_box: np.ndarray | None = None  # (Z, 6) whole-tooth tool-frame boxes
     extras: dict = field(default_factory=dict)
 
     @property
@@ -171,6 +173,7 @@ def plan(config, ext: Extensions | None = None) -> SweepPlan:
     p.record = bool(getattr(config, "record_trajectory", False))
     if p.record and p.mode != MODE_REF:
         raise ConfigError("record_trajectory is defined for the reference kinematics only")
+    _pack(p)
     if p.points > MAX_POINTS:
         raise ConfigError(f"edge_point_count {p.points} exceeds the device limit {MAX_POINTS}")
     # bounds of the device's fast exact cell location (msurf.cu cell_fast):
@@ -182,6 +185,31 @@ def plan(config, ext: Extensions | None = None) -> SweepPlan:
     if (grid.m + 1) * (grid.n + 1) >= 1 << 31:
         raise ConfigError("grid has too many nodes for one device surface (>= 2^31)")
     return p
+
+
+def _pack(p: SweepPlan) -> None:
+    """Per-(tooth, point) 32-byte records the device reads with one broadcast
+    load per point (include/msurf.h msurf_job.pts), plus whole-tooth boxes."""
+    z_n, n = p.teeth, p.points
+    rec = np.zeros((z_n, n, 4))
+    kf = p.zkey.view(np.float64)
+    if p.mode == MODE_REF:
+        rec[:, :, 0] = p.px[None, :]
+        rec[:, :, 1] = p.py[None, :]
+        rec[:, :, 2] = p.pz[None, :]
+        rec[:, :, 3] = kf
+    elif p.mode == MODE_EXT:
+        rec[:, :, 0], rec[:, :, 1], rec[:, :, 2] = p.px, p.py, kf
+    else:
+        # time-invariant halves of the tilt products (the device adds the
+        # time-varying ones): sin(tau)*zt and cos(tau)*zt, one rounding each
+        rec[:, :, 0], rec[:, :, 1] = p.px, p.py
+        rec[:, :, 2] = p.tilt_s * p.pz
+        rec[:, :, 3] = p.tilt_c * p.pz
+    p.pts = rec
+    b = p.chunk_box
+    p.tooth_box = np.stack([b[:, :, 0].min(1), b[:, :, 1].max(1), b[:, :, 2].min(1), b[:, :, 3].max(1),
+                            b[:, :, 4].min(1), b[:, :, 5].max(1)], axis=1)
 
 
 def _plan_ref(config) -> SweepPlan:

@@ -112,7 +112,8 @@ def simulate_strip(config, ext: Extensions | None, rank: int, world: int, trig: 
     ctr, machined = b.counters()
     return StripResult(plan=p, j_lo=j_lo, j_hi=j_hi, heights=b.heights()[0],
                        counters={"live_rows": int(ctr[0][0]), "points_evaluated": int(ctr[0][1]),
-                                 "deposits": int(ctr[0][2]), "atomics": int(ctr[0][3])},
+                                 "deposits": int(ctr[0][2]), "atomics": int(ctr[0][3]),
+                                 "engaged_rows": int(ctr[0][4])},
                        cells_updated=int(machined[0]), main_loop_seconds=ev[0].elapsed_time(ev[3]) * 1e-3,
                        batch=b)
 

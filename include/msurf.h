@@ -109,7 +109,7 @@ int msurf_decode(uint64_t* keys, int64_t count, int32_t n_surf, const double* se
  * pass2 reads mean = stats1[s][0] / stats1[s][3] (under strip sharding the
  * caller all-reduces stats1 first, so the mean is global)
  *       -> out2[s][4] = sum|d|, sum d^2, sum d^3, sum d^4 */
-#define MSURF_RED_BLOCKS 256
+#define MSURF_RED_BLOCKS 1024
 int msurf_areal_pass1(const double* h, int64_t ld, int64_t surf_stride, int32_t n_surf,
                       int64_t i_lo, int64_t j_lo, int64_t rows, int64_t cols,
                       const double* sentinel, int32_t exclude_uncut, double* work,

@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
   __shared__ unsigned warp_eval[kWarps];
   __shared__ unsigned warp_eng[kWarps];
   __shared__ int s_job;
+  __shared__ double4 ptstage[kWarps][32];  // per-warp copy of the current chunk's point records
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -316,10 +317,17 @@ __global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
     }
     if (!__any_sync(0xffffffffu, on)) continue;
     const int p_end = min(32, npts - q * 32);
-    const double4* __restrict__ pc = pts + q * 32;
+    // stage the chunk's 32 point records (1 KB, coalesced) for broadcast reads
+    __syncwarp();
+    if (lane < p_end) {
+      const double2* src = reinterpret_cast<const double2*>(pts + q * 32 + lane);
+      const double2 a = __ldg(src), b = __ldg(src + 1);
+      ptstage[warp][lane] = make_double4(a.x, a.y, b.x, b.y);
+    }
+    __syncwarp();
 #pragma unroll 2
     for (int k = 0; k < p_end; ++k) {
-      const double4 pt = pc[k];  // same address in every lane: one broadcast load
+      const double4 pt = ptstage[warp][k];  // same address in every lane: broadcast
       double xw, yw;
       uint64_t key;
       if (MODE == MSURF_MODE_REF) {
@@ -384,13 +392,21 @@ __global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
 }
 
 // --------------------------------------------------------------- fill/decode
-__global__ void fill_kernel(uint64_t* __restrict__ keys, long long count,
-                            const double* __restrict__ value) {
+// HBM streams: 16-byte vector accesses when the surface size is even (every
+// BASELINE grid), grid-stride over a capped grid, one y-block row per surface.
+__global__ void __launch_bounds__(kThreads)
+    fill_kernel(uint64_t* __restrict__ keys, long long count, const double* __restrict__ value) {
   const uint64_t key = enc_key(value[blockIdx.y]);
   uint64_t* base = keys + (long long)blockIdx.y * count;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride)
-    base[i] = key;
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((count & 1) == 0 && (reinterpret_cast<uintptr_t>(base) & 15) == 0) {
+    ulonglong2* b2 = reinterpret_cast<ulonglong2*>(base);
+    const ulonglong2 kk = make_ulonglong2(key, key);
+    for (long long i = t0; i < count / 2; i += stride) b2[i] = kk;
+  } else {
+    for (long long i = t0; i < count; i += stride) base[i] = key;
+  }
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -398,13 +414,25 @@ __global__ void __launch_bounds__(kThreads)
                   unsigned long long* __restrict__ machined) {
   uint64_t* base = keys + (long long)blockIdx.y * count;
   const double sentinel = sent[blockIdx.y];
-  double* out = reinterpret_cast<double*>(base);
   unsigned cnt = 0;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
-    const double h = dec_key(base[i]);
-    out[i] = h;
-    cnt += (h < sentinel);
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((count & 1) == 0 && (reinterpret_cast<uintptr_t>(base) & 15) == 0) {
+    ulonglong2* b2 = reinterpret_cast<ulonglong2*>(base);
+    double2* o2 = reinterpret_cast<double2*>(base);
+    for (long long i = t0; i < count / 2; i += stride) {
+      const ulonglong2 k = b2[i];
+      const double2 hv = make_double2(dec_key(k.x), dec_key(k.y));
+      o2[i] = hv;
+      cnt += (hv.x < sentinel) + (hv.y < sentinel);
+    }
+  } else {
+    double* out = reinterpret_cast<double*>(base);
+    for (long long i = t0; i < count; i += stride) {
+      const double hv = dec_key(base[i]);
+      out[i] = hv;
+      cnt += (hv < sentinel);
+    }
   }
   cnt = warp_sum_u(cnt);
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(machined + blockIdx.y, (unsigned long long)cnt);
@@ -461,8 +489,10 @@ __global__ void __launch_bounds__(kThreads)
   const double sentinel = sent[blockIdx.y];
   double v[5] = {0.0, -INFINITY, INFINITY, 0.0, 0.0};
   const int kind[5] = {0, 1, 2, 0, 0};
-  for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+  const long long r0 = rows * blockIdx.x / gridDim.x, r1 = rows * (blockIdx.x + 1) / gridDim.x;
+  for (long long r = r0; r < r1; ++r) {
     const double* row = hs + (i_lo + r) * ld + j_lo;
+#pragma unroll 4
     for (long long c = threadIdx.x; c < cols; c += blockDim.x) {
       const double hv = row[c];
       const bool cut = hv < sentinel;
@@ -494,8 +524,10 @@ __global__ void __launch_bounds__(kThreads)
   const double mu = stats1[blockIdx.y * 5 + 0] / stats1[blockIdx.y * 5 + 3];  // z.mean()
   double v[4] = {0.0, 0.0, 0.0, 0.0};
   const int kind[4] = {0, 0, 0, 0};
-  for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+  const long long r0 = rows * blockIdx.x / gridDim.x, r1 = rows * (blockIdx.x + 1) / gridDim.x;
+  for (long long r = r0; r < r1; ++r) {
     const double* row = hs + (i_lo + r) * ld + j_lo;
+#pragma unroll 4
     for (long long c = threadIdx.x; c < cols; c += blockDim.x) {
       const double hv = row[c];
       if (hv < sentinel || !exclude) {
@@ -636,9 +668,10 @@ int msurf_fill_keys(uint64_t* keys, int64_t count, int32_t n_surf, const double*
   if (count < 0 || n_surf < 1 || (count > 0 && (!keys || !value)))
     return set_err("msurf_fill_keys: bad arguments");
   if (count == 0) return 0;
-  long long blocks = (count + kThreads - 1) / kThreads;
-  const long long cap = n_surf > 1 ? 64 : 148 * 8;
+  long long blocks = (count / 2 + kThreads - 1) / kThreads;
+  const long long cap = n_surf > 1 ? 64 : 148 * 16;
   if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
   fill_kernel<<<dim3((unsigned)blocks, (unsigned)n_surf), kThreads, 0, (cudaStream_t)stream>>>(
       keys, count, value);
   return check_launch("fill_kernel");
@@ -681,16 +714,23 @@ int msurf_decode(uint64_t* keys, int64_t count, int32_t n_surf, const double* se
   if (count < 0 || n_surf < 1 || !keys || !machined || !sentinel)
     return set_err("msurf_decode: bad arguments");
   if (count == 0) return 0;
-  long long blocks = (count + kThreads - 1) / kThreads;
-  const long long cap = n_surf > 1 ? 64 : 148 * 8;
+  long long blocks = (count / 2 + kThreads - 1) / kThreads;
+  const long long cap = n_surf > 1 ? 64 : 148 * 16;
   if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
   dim3 grid((unsigned)blocks, (unsigned)n_surf);
   decode_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(keys, count, sentinel, machined);
   return check_launch("decode_kernel");
 }
 
-static int red_blocks(int64_t rows) {
-  return (int)(rows < MSURF_RED_BLOCKS ? (rows > 0 ? rows : 1) : MSURF_RED_BLOCKS);
+// blocks per surface: ~4096 elements per block, at most one per row, at most
+// MSURF_RED_BLOCKS; a pure function of the ROI shape, so reductions are
+// bit-reproducible run to run
+static int red_blocks(int64_t rows, int64_t cols) {
+  long long nb = rows * cols / 4096;
+  if (nb > rows) nb = rows;
+  if (nb > MSURF_RED_BLOCKS) nb = MSURF_RED_BLOCKS;
+  return (int)(nb < 1 ? 1 : nb);
 }
 
 int msurf_areal_pass1(const double* h, int64_t ld, int64_t surf_stride, int32_t n_surf,
@@ -699,7 +739,7 @@ int msurf_areal_pass1(const double* h, int64_t ld, int64_t surf_stride, int32_t 
                       double* out1, void* stream) {
   if (!h || !work || !out1 || !sentinel || n_surf < 1 || rows < 1 || cols < 1 || i_lo < 0 || j_lo < 0 || ld < cols)
     return set_err("msurf_areal_pass1: bad arguments");
-  const int nb = red_blocks(rows);
+  const int nb = red_blocks(rows, cols);
   cudaStream_t st = (cudaStream_t)stream;
   areal_pass1_kernel<<<dim3(nb, n_surf), kThreads, 0, st>>>(h, ld, surf_stride, i_lo, j_lo, rows, cols,
                                                            sentinel, exclude_uncut, work);
@@ -714,7 +754,7 @@ int msurf_areal_pass2(const double* h, int64_t ld, int64_t surf_stride, int32_t 
                       double* work, double* out2, void* stream) {
   if (!h || !work || !out2 || !stats1 || !sentinel || n_surf < 1 || rows < 1 || cols < 1 || i_lo < 0 || j_lo < 0 || ld < cols)
     return set_err("msurf_areal_pass2: bad arguments");
-  const int nb = red_blocks(rows);
+  const int nb = red_blocks(rows, cols);
   cudaStream_t st = (cudaStream_t)stream;
   areal_pass2_kernel<<<dim3(nb, n_surf), kThreads, 0, st>>>(h, ld, surf_stride, i_lo, j_lo, rows, cols,
                                                            sentinel, exclude_uncut, stats1, work);

@@ -56,7 +56,8 @@ typedef struct msurf_job {
                               * EXT      (xt, yt, key of z', 0)   tool frame
                               * EXT_TILT (xt, yt, sin(tau)*zt, cos(tau)*zt)        */
   const double* tooth_box;   /* [teeth][6] whole-tooth tool-frame box (P_eng counter)  */
-  const double* chunk_box;   /* [teeth][nchunk][6] tool-frame xlo xhi ylo yhi zlo zhi */
+  const double* chunk_circ;  /* [teeth][nchunk][6] cull record per 32-point chunk:
+                              * (xc, yc, rx, ry, yz, 0) — see planner._chunk_circles */
   const double* pass_x0;     /* [passes] spindle x of each raster pass               */
   /* extended kinematics */
   double tilt_c, tilt_s, zoff;

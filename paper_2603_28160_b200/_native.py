@@ -35,7 +35,7 @@ class MsurfJob(ctypes.Structure):
         ("t_start", c_double), ("dt", c_double), ("steps", c_int64),
         ("y0", c_double), ("feed_speed", c_double), ("omega", c_double),
         ("tooth_base", c_void_p), ("tooth_rows", c_void_p),
-        ("pts", c_void_p), ("tooth_box", c_void_p), ("chunk_box", c_void_p), ("pass_x0", c_void_p),
+        ("pts", c_void_p), ("tooth_box", c_void_p), ("chunk_circ", c_void_p), ("pass_x0", c_void_p),
         ("tilt_c", c_double), ("tilt_s", c_double), ("zoff", c_double),
         ("vib_amp", c_double), ("vib_omega", c_double), ("vib_phase", c_double),
         ("trig_table", c_void_p), ("vib_table", c_void_p),

@@ -235,10 +235,21 @@ __global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
       };
       engaged = box_hits(J.tooth_box + tooth * 6);
       if (engaged) {
-        const double* box = J.chunk_box + (long long)tooth * nchunk * 6;
+        // per-chunk bounding circles: x = c*xc + s*yc + xoff +- rx,
+        // y = cos(tau)*(c*yc - s*xc) + yz + ty +- ry, against the window
+        // (centre, half-width) widened by 1.5 cells
+        const double wxc = 0.5 * (wx_lo + wx_hi), wxh = 0.5 * (wx_hi - wx_lo);
+        const double wyc = 0.5 * (wy_lo + wy_hi), wyh = 0.5 * (wy_hi - wy_lo);
+        const double ox = xoff - wxc, oy = ty - wyc;
+        const double tcv = MODE == MSURF_MODE_EXT_TILT ? J.tilt_c : 1.0;
+        const double2* circ = reinterpret_cast<const double2*>(J.chunk_circ) + (long long)tooth * nchunk * 3;
         unsigned kept = 0;
         for (int q = 0; q < nchunk; ++q) {
-          if (box_hits(box + q * 6)) {
+          const double2 a = circ[q * 3 + 0], b = circ[q * 3 + 1], z = circ[q * 3 + 2];
+          const double uc = c * a.x + sn * a.y;
+          const double vc = c * a.y - sn * a.x;
+          const bool hit = (fabs(uc + ox) <= wxh + b.x) & (fabs(tcv * vc + z.x + oy) <= wyh + b.y);
+          if (hit) {
             my_mask[q >> 6] |= 1ull << (q & 63);
             kept += (q == nchunk - 1) ? (unsigned)(npts - 32 * q) : 32u;
           }

@@ -123,7 +123,7 @@ class SweepBatch:
                 tooth_rows=ar.add(p.tooth_rows.astype(np.float64)),
                 pts=ar.add(p.pts.astype(np.float64)),
                 tooth_box=ar.add(p.tooth_box.astype(np.float64)),
-                chunk_box=ar.add(p.chunk_box.astype(np.float64)),
+                chunk_circ=ar.add(p.chunk_circ.astype(np.float64)),
                 pass_x0=ar.add(p.pass_x0.astype(np.float64)),
                 min_index=ar.add(p.min_index.astype(np.int32)),
             )
@@ -174,7 +174,7 @@ class SweepBatch:
                     j.keys = keys_ptr + s.key_off * 8
                     j.t_start, j.dt, j.steps = p.t_start, p.dt, p.steps
                     j.y0, j.feed_speed, j.omega = p.y0, p.feed_speed, p.omega
-                    for name in ("tooth_base", "tooth_rows", "pts", "tooth_box", "chunk_box",
+                    for name in ("tooth_base", "tooth_rows", "pts", "tooth_box", "chunk_circ",
                                  "pass_x0", "min_index"):
                         setattr(j, name, base + o[name])
                     j.counters = base + self.ctr_off + i * _native.NUM_CTRS * 8

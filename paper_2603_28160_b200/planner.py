@@ -78,7 +78,7 @@ class SweepPlan:
     pz: np.ndarray
     zw: np.ndarray                    # (Z, N) z' (time-invariant unless tilt)
     zkey: np.ndarray                  # (Z, N) u64
-    chunk_box: np.ndarray             # (Z, nchunk, 6)
+    chunk_box: np.ndarray             # (Z, nchunk, 6) tool-frame boxes
     pass_x0: np.ndarray               # (P,)
     min_index: np.ndarray             # (Z,) int32
     tilt_c: float = 1.0
@@ -89,6 +89,7 @@ class SweepPlan:
     vib_phase: float = 0.0
     record: bool = False
     pts: np.ndarray | None = None        # (Z, N, 4) device point records (msurf_job.pts)
+    chunk_circ: np.ndarray | None = None # (Z, nchunk, 6) device cull records
     tooth_box: np.ndarray | None = None  # (Z, 6) whole-tooth tool-frame boxes
     extras: dict = field(default_factory=dict)
 
@@ -100,6 +101,34 @@ class SweepPlan:
     def trajectory_points(self) -> int:
         """steps x teeth x points x passes (engine.py:129-131)."""
         return self.steps * self.teeth * self.points * self.passes
+
+
+def _chunk_circles(xt, yt, zt, tilt_c: float, tilt_s: float) -> np.ndarray:
+    """Per tooth and 32-point chunk the device's cull record
+    (xc, yc, rx, ry, yz, 0): tool-frame centre, the radius bounding the
+    chunk's workpiece x-extent at any rotation, the radius of its y-extent
+    after the lead tilt, and the tilt's z offset -sin(tau)*zc. A rotation by
+    theta maps the chunk into x = c*xc + s*yc +- rx (+ x offset) and
+    y = cos(tau)*(c*yc - s*xc) + yz +- ry (+ feed), which the kernel tests
+    against the owned window widened by 1.5 cells (conservative)."""
+    z_n, n = xt.shape
+    nchunk = (n + CHUNK - 1) // CHUNK
+    pad = nchunk * CHUNK - n
+    def blk(a):
+        full = np.concatenate([a, np.repeat(a[:, -1:], pad, axis=1)], axis=1) if pad else a
+        return full.reshape(z_n, nchunk, CHUNK)
+    bx, by, bz = blk(xt), blk(yt), blk(zt)
+    xc = 0.5 * (bx.min(2) + bx.max(2))
+    yc = 0.5 * (by.min(2) + by.max(2))
+    zc = 0.5 * (bz.min(2) + bz.max(2))
+    zr = 0.5 * (bz.max(2) - bz.min(2))
+    rho = np.sqrt(((bx - xc[:, :, None]) ** 2 + (by - yc[:, :, None]) ** 2).max(2))
+    rho = rho * (1.0 + 1e-12) + 1e-12
+    out = np.zeros((z_n, nchunk, 6))
+    out[:, :, 0], out[:, :, 1], out[:, :, 2] = xc, yc, rho
+    out[:, :, 3] = tilt_c * rho + abs(tilt_s) * (zr * (1.0 + 1e-12) + 1e-12)
+    out[:, :, 4] = -tilt_s * zc
+    return out
 
 
 def _chunk_boxes(xt: np.ndarray, yt: np.ndarray, zt: np.ndarray) -> np.ndarray:
@@ -207,6 +236,14 @@ def _pack(p: SweepPlan) -> None:
         rec[:, :, 2] = p.tilt_s * p.pz
         rec[:, :, 3] = p.tilt_c * p.pz
     p.pts = rec
+    if p.mode == MODE_REF:
+        xt = (p.tooth_rows[:, 0:1] * p.px[None, :] + p.tooth_rows[:, 1:2] * p.py[None, :]) \
+            + p.tooth_rows[:, 2:3] * p.pz[None, :] + p.tooth_rows[:, 3:4]
+        yt = (p.tooth_rows[:, 4:5] * p.px[None, :] + p.tooth_rows[:, 5:6] * p.py[None, :]) \
+            + p.tooth_rows[:, 6:7] * p.pz[None, :] + p.tooth_rows[:, 7:8]
+        p.chunk_circ = _chunk_circles(xt, yt, p.zw, 1.0, 0.0)
+    else:
+        p.chunk_circ = _chunk_circles(p.px, p.py, p.pz, p.tilt_c, p.tilt_s)
     b = p.chunk_box
     p.tooth_box = np.stack([b[:, :, 0].min(1), b[:, :, 1].max(1), b[:, :, 2].min(1), b[:, :, 3].max(1),
                             b[:, :, 4].min(1), b[:, :, 5].max(1)], axis=1)

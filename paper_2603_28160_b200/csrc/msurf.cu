@@ -29,6 +29,9 @@
 
 namespace {
 
+#ifndef MSURF_TWO_SIDED
+#define MSURF_TWO_SIDED 1  // tilt mode: deposit only local minima of each cell run
+#endif
 #ifndef MSURF_MIN_BLOCKS
 #define MSURF_MIN_BLOCKS 4  // CTAs per SM the register budget is sized for
 #endif
@@ -53,10 +56,14 @@ int check_launch(const char* what) {
 // ----------------------------------------------------------- key encoding
 // Order-preserving map fp64 -> u64 (unsigned compare == IEEE compare for
 // non-NaN; -0 is canonicalised to +0 first, IEEE treats them equal).
+__device__ __forceinline__ uint64_t enc_key_raw(double z) {
+  // key = bits ^ (sign ? ~0 : 2^63) on the two 32-bit halves: 3 integer ops
+  const unsigned hi = (unsigned)__double2hiint(z), lo = (unsigned)__double2loint(z);
+  const unsigned sgn = (unsigned)((int)hi >> 31);
+  return ((uint64_t)(hi ^ (sgn | 0x80000000u)) << 32) | (uint64_t)(lo ^ sgn);
+}
 __device__ __forceinline__ uint64_t enc_key(double z) {
-  z = __dadd_rn(z, 0.0);
-  const uint64_t b = (uint64_t)__double_as_longlong(z);
-  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+  return enc_key_raw(__dadd_rn(z, 0.0));  // -0 -> +0 first (IEEE treats them equal)
 }
 __device__ __forceinline__ double dec_key(uint64_t k) {
   const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
@@ -104,6 +111,14 @@ __device__ __forceinline__ void red_min_u64(unsigned long long* p, unsigned long
   asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+
+// predicated form: no branch around the RED
+__device__ __forceinline__ void red_min_u64_if(unsigned long long* p, unsigned long long v, bool pred) {
+  asm volatile(
+      "{ .reg .pred q; setp.ne.u32 q, %2, 0; @q red.relaxed.gpu.global.min.u64 [%0], %1; }" ::"l"(p),
+      "l"(v), "r"((unsigned)pred)
+      : "memory");
+}
 
 __device__ __forceinline__ unsigned warp_sum_u(unsigned v) {
 #pragma unroll
@@ -357,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
           const double yv = __dsub_rn(__dmul_rn(tilt_c, vv), pt.z);
           const double zz = __dadd_rn(__dadd_rn(__dmul_rn(tilt_s, vv), pt.w), zoff);
           yw = __dadd_rn(yv, r[3]);
-          key = enc_key(zz);
+          key = enc_key_raw(zz);  // zz = (..) + zoff with zoff != -0 (host-canonical): never -0
         } else {
           yw = __dadd_rn(vv, r[3]);
           key = (uint64_t)__double_as_longlong(pt.z);
@@ -371,20 +386,24 @@ __global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
       }
       const bool inside = on & ((unsigned)ci.idx <= span_i) & ((unsigned)(cj.idx - j_lo) <= span_j);
       const int idx = inside ? ci.idx * ldk + (cj.idx - j_lo) : -1;
-      // time-neighbour pre-reduction
+      // time-neighbour pre-reduction: within a run of lanes (consecutive
+      // live steps) whose point sits in one cell, only the run's minimum
+      // deposits. Constant z' (REF/EXT): the run's first lane. Tilt: lanes
+      // that are a local minimum (< predecessor, <= successor).
       const int idx_prev = __shfl_up_sync(0xffffffffu, idx, 1);
-      bool skip = (lane > 0) & (idx == idx_prev);
+      bool dep = inside & ((lane == 0) | (idx != idx_prev));
       if (MODE == MSURF_MODE_EXT_TILT) {
         const uint64_t key_prev = __shfl_up_sync(0xffffffffu, key, 1);
-        skip &= key >= key_prev;
+        dep = inside & ((lane == 0) | (idx != idx_prev) | (key < key_prev));
+#if MSURF_TWO_SIDED
+        const int idx_next = __shfl_down_sync(0xffffffffu, idx, 1);
+        const uint64_t key_next = __shfl_down_sync(0xffffffffu, key, 1);
+        dep &= (lane == 31) | (idx != idx_next) | (key <= key_next);
+#endif
       }
-      if (inside) {
-        ++n_dep;
-        if (!skip) {
-          red_min_u64(keys + idx, (unsigned long long)key);
-          ++n_atom;
-        }
-      }
+      n_dep += inside;
+      n_atom += dep;
+      red_min_u64_if(keys + idx, (unsigned long long)key, dep);
     }
   }
 

@@ -359,7 +359,7 @@ def _plan_ext(config, ext: Extensions) -> SweepPlan:
     amp = ext.vib_amplitude_mm
     margin = base_margin + (abs(rho) + abs(amp) + 5.0 * abs(sigma) + abs(ts) * float(np.max(np.abs(zt))))
     dt, t_start, steps, x0, y0, z0 = _span(config, margin)
-    zoff = z0 + z_shift
+    zoff = (z0 + z_shift) + 0.0  # canonical: never -0 (the device relies on it)
     zw = zt + zoff
     return SweepPlan(
         mode=MODE_EXT_TILT if tilt else MODE_EXT, grid=grid, teeth=z_n, points=n, steps=steps,

@@ -229,6 +229,8 @@ def run_ours(args, rank, world):
     j_lo, j_hi = sharded.strip_bounds(p.grid.n + 1, world)[rank]
     batch = SweepBatch([(p, j_lo, j_hi)])
     pipe = SurfacePipeline(batch, every=every, uncut=uncut) if world == 1 else None
+    if pipe is not None and not args.no_graph:
+        pipe.capture()  # three CUDA graphs: fill | sweep | decode + reductions
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def barrier():
@@ -238,7 +240,7 @@ def run_ours(args, rank, world):
     def step(events):
         if pipe is not None:
             # single GPU: sync-free launch sequence, results read after the timed region
-            pipe.enqueue(events=events)
+            pipe.run(events=events)
             return None
         batch.launch(events=events)
         res = sharded.StripResult(plan=p, j_lo=j_lo, j_hi=j_hi, heights=batch.heights()[0], counters={},
@@ -391,6 +393,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the step without CUDA graphs")
     args = ap.parse_args()
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)

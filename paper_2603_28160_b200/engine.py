@@ -194,17 +194,10 @@ class SweepBatch:
         self.launches_per_run = 2 * (1 if self.same_shape else n) + len(self.group_meta)
 
     # ------------------------------------------------------------------
-    def launch(self, stream=None, events=None):
-        """Enqueue fill -> sweep(s) -> decode on ``stream`` (async).
-        ``events`` = (start, after_fill, after_sweep, end) CUDA events, optional."""
-        torch, lib = self.torch, self.lib
-        st = stream if stream is not None else torch.cuda.current_stream(self.dev)
-        sp = int(st.cuda_stream)
-        base, keys_ptr = self.base, self.keys.data_ptr()
-        if events:
-            events[0].record(st)
-        with torch.cuda.stream(st):
-            self.buf[self.ctr_off: self.ctr_off + self.n * (_native.NUM_CTRS + 1) * 8].zero_()
+    def launch_fill(self, sp: int) -> None:
+        """Zero the counters and initialise every Z-map to its stock height."""
+        lib, base, keys_ptr = self.lib, self.base, self.keys.data_ptr()
+        self.buf[self.ctr_off: self.ctr_off + self.n * (_native.NUM_CTRS + 1) * 8].zero_()
         if self.same_shape:
             _native.check(lib.msurf_fill_keys(keys_ptr, self.surfs[0].nodes, self.n,
                                               base + self.sentinel_off, sp))
@@ -212,13 +205,17 @@ class SweepBatch:
             for i, s in enumerate(self.surfs):
                 _native.check(lib.msurf_fill_keys(keys_ptr + s.key_off * 8, s.nodes, 1,
                                                   base + self.sentinel_off + 8 * i, sp))
-        if events:
-            events[1].record(st)
+
+    def launch_sweep(self, sp: int) -> None:
+        """One msurf_sweep launch per kinematics mode present in the batch."""
+        lib, base = self.lib, self.base
         for mode, idx, job_off, pre_off, n_tiles, max_pts in self.group_meta:
             _native.check(lib.msurf_sweep(base + job_off, len(idx), base + pre_off, n_tiles, mode,
                                           max_pts, sp))
-        if events:
-            events[2].record(st)
+
+    def launch_decode(self, sp: int) -> None:
+        """Keys -> fp64 heights in place, machined-cell counts."""
+        lib, base, keys_ptr = self.lib, self.base, self.keys.data_ptr()
         if self.same_shape:
             _native.check(lib.msurf_decode(keys_ptr, self.surfs[0].nodes, self.n, base + self.sentinel_off,
                                            base + self.machined_off, sp))
@@ -227,8 +224,25 @@ class SweepBatch:
                 _native.check(lib.msurf_decode(keys_ptr + s.key_off * 8, s.nodes, 1,
                                                base + self.sentinel_off + 8 * i,
                                                base + self.machined_off + 8 * i, sp))
-        if events:
-            events[3].record(st)
+
+    def launch(self, stream=None, events=None):
+        """Enqueue fill -> sweep(s) -> decode on ``stream`` (async).
+        ``events`` = (start, after_fill, after_sweep, end) CUDA events, optional."""
+        torch = self.torch
+        st = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        sp = int(st.cuda_stream)
+        with torch.cuda.stream(st):
+            if events:
+                events[0].record(st)
+            self.launch_fill(sp)
+            if events:
+                events[1].record(st)
+            self.launch_sweep(sp)
+            if events:
+                events[2].record(st)
+            self.launch_decode(sp)
+            if events:
+                events[3].record(st)
 
     def heights(self):
         """fp64 views (valid after a launch) — one per surface."""

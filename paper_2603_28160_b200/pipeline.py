@@ -44,11 +44,8 @@ class SurfacePipeline:
         self.graph = None
         self.launches_per_run = batch.launches_per_run + 4 + (1 if self.rows_idx else 0)
 
-    def enqueue(self, events=None):
-        """Launch the full step on the current stream; no host sync."""
+    def _reduce(self, sp: int) -> None:
         lib, b = self.lib, self.batch
-        sp = _native.stream_ptr()
-        b.launch(events=events)
         h = b.keys.data_ptr()
         sent = b.base + b.sentinel_off
         o = self.out.data_ptr()
@@ -62,22 +59,48 @@ class SurfacePipeline:
             _native.check(lib.msurf_profiles(h, self.nodes, n, self.starts.data_ptr(), len(self.rows_idx),
                                              g.n + 1, 1, sent, self.exclude, None, o + n * 9 * 8, sp))
 
-    def capture(self):
-        """Capture enqueue() into a CUDA graph (replayed by run())."""
-        torch = self.torch
-        self.enqueue()  # warm the lazy module/kernel loading outside capture
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self.enqueue()
-        self.graph = g
-        return g
+    def stages(self):
+        """The step as three launch groups: (fill), (sweep), (decode + reductions)."""
+        b = self.batch
+        return [b.launch_fill, b.launch_sweep, lambda sp: (b.launch_decode(sp), self._reduce(sp))]
 
-    def run(self):
-        if self.graph is not None:
-            self.graph.replay()
-        else:
-            self.enqueue()
+    def enqueue(self, events=None):
+        """Launch the full step on the current stream; no host sync.
+        ``events`` (4): before fill, after fill, after sweep, at the end."""
+        st = self.torch.cuda.current_stream()
+        sp = int(st.cuda_stream)
+        for k, stage in enumerate(self.stages()):
+            if events:
+                events[k].record(st)
+            stage(sp)
+        if events:
+            events[3].record(st)
+
+    def capture(self):
+        """Capture each stage into its own CUDA graph; run() replays them with
+        optional events between stages (so the sweep is still timed alone)."""
+        torch = self.torch
+        self.enqueue()  # lazy module loading and allocator warm-up outside capture
+        torch.cuda.synchronize()
+        graphs = []
+        for stage in self.stages():
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                stage(int(torch.cuda.current_stream().cuda_stream))
+            graphs.append(g)
+        self.graph = graphs
+        return graphs
+
+    def run(self, events=None):
+        if self.graph is None:
+            return self.enqueue(events)
+        st = self.torch.cuda.current_stream()
+        for k, g in enumerate(self.graph):
+            if events:
+                events[k].record(st)
+            g.replay()
+        if events:
+            events[3].record(st)
 
     def collect(self):
         """One D2H: per surface (ArealMetrics | DomainError, [ProfileRoughness])."""

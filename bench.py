@@ -142,46 +142,55 @@ def profiled_traffic(cfg_name):
     """dram bytes per sweep launch from the committed ncu capture (profiles/)."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            return json.load(fh).get(cfg_name)
+            ent = json.load(fh).get(cfg_name)
+        return None if ent is None else ent["dram_bytes_per_sweep_launch"]
     except (OSError, ValueError):
         return None
 
 
 # ---------------------------------------------------------------- CPU legs
 def cpu_sample(cfg, ext, plan, target_s: float = 12.0, threads: int | None = None):
-    """Bounded sample of the same workload on the host cores with the CPU
-    restatement of the reference algorithm (oracle/fsm_ext_oracle.py): step
-    windows spread evenly over the first pass, sized for ~target_s of work."""
-    from types import SimpleNamespace as NS
-
+    """The same workload on the host cores with the CPU restatement of the
+    reference algorithm (oracle/fsm_ext_oracle.py, all threads). If the whole
+    surface fits in ~target_s it is run in full; otherwise a bounded sample:
+    16 step windows spread over the first pass, sized for ~target_s."""
     from oracle import fsm_ext_oracle as xorc
 
     threads = threads or os.cpu_count() or 1
-    ext_ns = ext  # duck-typed: the oracle reads extension fields by name
     steps = plan.steps
     n_win = 16
 
-    def run(win_len):
+    def run(win_len, passes=1):
         wins = [(int(round((k + 0.5) * steps / n_win - win_len / 2)),
                  int(round((k + 0.5) * steps / n_win + win_len / 2))) for k in range(n_win)]
         t0 = time.perf_counter()
-        _, _, ctr, _ = xorc.ext_sweep(cfg, ext_ns, workers=threads, windows=wins, pass_limit=1)
+        _, _, ctr, _ = xorc.ext_sweep(cfg, ext, workers=threads, windows=wins, pass_limit=passes)
         return ctr["trajectory_points"], time.perf_counter() - t0
 
-    win = max(8, steps // 2000)
+    win = max(8, steps // 400)
     pts, dt = run(win)
-    if dt < target_s / 4:
-        win = min(steps // n_win, int(win * max(1.0, target_s / max(dt, 1e-3) * 0.8)))
-        pts, dt = run(win)
+    rate = pts / dt
+    if plan.trajectory_points / rate <= target_s:
+        t0 = time.perf_counter()
+        _, _, ctr, _ = xorc.ext_sweep(cfg, ext, workers=threads)
+        dt = time.perf_counter() - t0
+        pts = ctr["trajectory_points"]
+        what = f"the full workload ({pts} edge-point updates in {dt:.2f} s"
+    else:
+        while dt < 0.5 * target_s and win < steps // n_win:
+            win = min(steps // n_win, int(win * max(2.0, 0.7 * target_s / max(dt, 1e-3))))
+            pts, dt = run(win)
+        what = (f"first pass, {n_win} step windows x {win} steps spread over {steps} steps "
+                f"({pts} edge-point updates in {dt:.2f} s")
     return {"value": pts / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"first pass, {n_win} step windows x {win} steps spread over {steps} steps "
-                      f"({pts} edge-point updates in {dt:.2f} s, oracle/fsm_ext_oracle.py, "
-                      f"{threads} threads)"}
+            "sample": what + f", oracle/fsm_ext_oracle.py, {threads} threads)"}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
+    if args.config == 3:
+        return run_reference_batch(args)
     cfg, ext, meta = workload(args.config)
     from paper_2603_28160_b200.planner import plan as make_plan
 
@@ -202,6 +211,30 @@ def run_reference(args, rank, world):
             "config": describe(cfg, ext, meta, p, 1),
             "surfaces_per_s": v / p.trajectory_points,
             "cpu_baseline": sample,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_reference_batch(args):
+    """Reference arm for the batched workload: the CPU restatement on 4 of
+    the 256 parameter sets (bounded windows), mean update rate."""
+    import numpy as np
+
+    base, ext, meta, ranges, mine, plans, total_points = config3_workload(0, 1)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        per = args.cpu_seconds / 4
+        rates = [cpu_sample(c, e, p, target_s=per)["value"] for (c, e), p in list(zip(mine, plans))[:4]]
+        if i >= args.warmup:
+            vals.append(float(np.mean(rates)))
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_points / v,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "config3 (BASELINE configs[2]): 256 parameter sets"},
+            "surfaces_per_s": meta["count"] * v / total_points,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                             "sample": "4 of 256 parameter sets, 16 step windows each (oracle/fsm_ext_oracle.py)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -323,7 +356,8 @@ def run_ours(args, rank, world):
         "points_evaluated": evald, "live_rows": live, "deposits": int(ctr[0][2]),
         "atomics": int(ctr[0][3]),
         "atomic_rate_per_s": int(ctr[0][3]) / (sweep_ms_avg * 1e-3),
-        "atomic_peak_per_s": atom_peak,
+        "atomic_random_rate_per_s": atom_peak,
+        "atomic_note": "msurf_microbench(2): random-address RED.MIN rate; the sweep's REDs have locality",
         "hbm": {"bytes_per_step": 24 * (p.grid.m + 1) * (j_hi - j_lo + 1) + 8 * int(ctr[0][3]),
                 "peak_gbs": measured_peaks().get("hbm_gbs")},
     }
@@ -384,6 +418,144 @@ def run_ours(args, rank, world):
         print(json.dumps(line), flush=True)
 
 
+def config3_workload(rank, world):
+    """BASELINE configs[2]: 256 parameter sets from default_rng(0), uniform
+    (dataset.uniform_sample), sharded by parameter set across ranks."""
+    from paper_2603_28160_b200 import configs, sharded
+    from paper_2603_28160_b200.dataset import ParameterRange, apply_sample, uniform_sample
+    from paper_2603_28160_b200.planner import plan as make_plan
+
+    base, ext, meta = configs.config3_base()
+    ranges = [ParameterRange(n, lo, hi) for n, lo, hi in meta["ranges"]]
+    samples = uniform_sample(ranges, meta["count"], meta["seed"])
+    names = [r.name for r in ranges]
+    all_cfgs = [apply_sample(base, ext, names, samples[i], meta["steps_per_rev"]) for i in range(meta["count"])]
+    sl = sharded.batch_slice(meta["count"], rank, world)
+    mine = all_cfgs[sl]
+    plans = [make_plan(c, e) for c, e in mine]
+    total_points = sum(make_plan(c, e).trajectory_points for c, e in all_cfgs) if world > 1 else \
+        sum(p.trajectory_points for p in plans)
+    return base, ext, meta, ranges, mine, plans, total_points
+
+
+def run_batch(args, rank, world):
+    """Batched dataset mode: every parameter set of this rank in ONE sweep
+    launch (+ fill/decode/reductions), value = all ranks' edge-point updates
+    / max-rank step time; surfaces/s alongside."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    import paper_2603_28160_b200 as ms
+    from paper_2603_28160_b200 import _native
+    from paper_2603_28160_b200.engine import SweepBatch
+    from paper_2603_28160_b200.pipeline import SurfacePipeline
+
+    dist = torch.distributed
+    local = _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    base, ext, meta, ranges, mine, plans, total_points = config3_workload(rank, world)
+    batch = SweepBatch([(p, 0, p.grid.n) for p in plans])
+    pipe = SurfacePipeline(batch, every=None, uncut=meta["uncut"])
+    if not args.no_graph:
+        pipe.capture()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        pipe.run()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    step_ms, sweep_ms = [], []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        flush.fill_(1)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        pipe.run(events=ev)
+        torch.cuda.synchronize()
+        step_ms.append(ev[0].elapsed_time(ev[3]))
+        sweep_ms.append(ev[1].elapsed_time(ev[2]))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ctr, machined = batch.counters()
+    res = pipe.collect()
+    tot = torch.tensor([sum(step_ms), sum(sweep_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms_step = float(tot[0]) / args.steps
+    sweep_avg = float(tot[1]) / args.steps
+    value = total_points / (ms_step * 1e-3)
+    evald, live, engaged = int(ctr[:, 1].sum()), int(ctr[:, 0].sum()), int(ctr[:, 4].sum())
+    npts = plans[0].points
+    mode = plans[0].mode
+    flops = FLOPS_PER_POINT[mode] * evald + FLOPS_PER_ROW * live
+    flops_survey = FLOPS_PER_POINT[mode] * engaged * npts + FLOPS_PER_ROW * engaged
+    lib = _native.lib()
+    r = ctypes.c_double(0.0)
+    _native.check(lib.msurf_microbench(0, ctypes.byref(r)))
+    fp64_peak = r.value
+    achieved = flops / (sweep_avg * 1e-3)
+    roofline = {"bound": "fp64", "achieved": achieved / 1e12, "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
+                "frac": achieved / fp64_peak, "traffic": profiled_traffic(meta["name"]),
+                "kernel": "sweep_kernel<MODE>", "sweep_ms": sweep_avg,
+                "peak_source": "measured in this run: msurf_microbench(0), non-FMA DADD/DMUL issue rate",
+                "flops_per_launch": flops, "survey_def": {"frac": flops_survey / (sweep_avg * 1e-3) / fp64_peak},
+                "points_evaluated": evald, "live_rows": live, "deposits": int(ctr[:, 2].sum()),
+                "atomics": int(ctr[:, 3].sum())}
+    # e2e: public batched API with host planning, one H2D, metrics + every height map read back
+    e2e_ms = []
+    d2h = 0
+    names = [rg.name for rg in ranges]
+    for i in range(args.warmup + args.steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = ms.simulate_batch([c for c, _ in mine], [e for _, e in mine])
+        mets = ms.areal_metrics_batch([o.field for o in out], uncut=meta["uncut"])
+        d2h = 0
+        for o in out:
+            d2h += o.field.heights.nbytes
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    et = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_step = float(et[0]) / args.steps
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        per = args.cpu_seconds / 4
+        rates = [cpu_sample(c, e, p, target_s=per)["value"] for (c, e), p in list(zip(mine, plans))[:4]]
+        cpu = {"value": float(np.mean(rates)), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+               "sample": "4 of the 256 parameter sets, 16 step windows each, oracle/fsm_ext_oracle.py, "
+                         "mean edge-point-update rate"}
+    if rank == 0:
+        ok = [m for m, _ in res if not isinstance(m, Exception)]
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "config3 (BASELINE configs[2]): 256 parameter sets, batched",
+                           "sets": meta["count"], "sets_this_rank": len(plans), "grid_nodes": [512, 512],
+                           "spacing_mm": 0.004, "edge_points": npts, "steps_per_rev": meta["steps_per_rev"],
+                           "edge_point_updates_per_batch": total_points,
+                           "parallelism": f"parameter-set shards x{world}" if world > 1 else "single GPU",
+                           "l2": "flushed between timed steps (256 MiB write)"},
+                "surfaces_per_s": meta["count"] / (ms_step * 1e-3),
+                "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": {"value": total_points / (e2e_step * 1e-3), "unit": UNIT,
+                        "h2d_bytes_per_step": int(batch.h2d_bytes), "d2h_bytes_per_step": int(d2h),
+                        "ms_per_step": e2e_step, "api": "simulate_batch + areal_metrics_batch + heights"},
+                "gpu_launches": pipe.launches_per_run * args.steps, "clocks": clk,
+                "metrics": {"surfaces_ok": len(ok), "Sa_um_mean": float(np.mean([m.sa_um for m in ok])) if ok else None}}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -407,7 +579,10 @@ def main():
         torch.cuda.set_device(_env_int("LOCAL_RANK", 0))
         dist.init_process_group("nccl")
     try:
-        run_ours(args, rank, world)
+        if args.config == 3:
+            run_batch(args, rank, world)
+        else:
+            run_ours(args, rank, world)
     finally:
         if world > 1:
             import torch.distributed as dist

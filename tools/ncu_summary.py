@@ -14,8 +14,9 @@ def ncu(rep, *args):
 def main():
     rep = sys.argv[1]
     rows = ncu(rep, "--page", "raw")
-    hdr, vals = rows[0], rows[2]
+    hdr, units, vals = rows[0], rows[1], rows[2]
     d = dict(zip(hdr, vals))
+    u = dict(zip(hdr, units))
     keys = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
             "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
             "launch__occupancy_limit_registers", "smsp__inst_executed.sum",
@@ -27,7 +28,7 @@ def main():
             "lts__t_requests_srcunit_l1_op_atom.sum", "smsp__thread_inst_executed_per_inst_executed.ratio"]
     for k in keys:
         if k in d:
-            print(f"{k:70s} {d[k]}")
+            print(f"{k:70s} {d[k]} {u.get(k, '')}")
     st = sorted(((k, float(v)) for k, v in d.items()
                  if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")
                  and v not in ("", "n/a")), key=lambda kv: -kv[1])

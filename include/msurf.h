@@ -43,10 +43,14 @@ typedef struct msurf_job {
   double spacing, x_min, y_min;
   int64_t m, n;      /* cell counts; nodes (m+1) x (n+1)                       */
   int64_t j_lo, j_hi; /* owned feed-direction node columns [j_lo, j_hi]          */
-  uint64_t* keys;    /* device (m+1) x (j_hi-j_lo+1), order-preserving u64 keys  */
+  int64_t ld;        /* keys row pitch in nodes (>= j_hi - j_lo + 1)            */
+  uint64_t* keys;    /* device: node (i, j) at keys[i * ld + (j - j_lo)],        *
+                      * order-preserving u64 keys of the heights                 */
   /* time (engine.py:152-170, 240-241) */
   double t_start, dt;
-  int64_t steps;
+  int64_t steps;     /* time steps of one pass (engine.py:170)                   */
+  int64_t step_lo, step_hi; /* this job sweeps steps [step_lo, step_hi) of every pass:
+                      * the window whose footprint can reach the owned columns */
   double y0, feed_speed, omega;
   /* per-tooth / per-point device arrays */
   const double* tooth_base;  /* [teeth] phase + (2pi)(K-1)/Z (kinematics.py:76)      */
@@ -84,7 +88,8 @@ int msurf_fill_keys(uint64_t* keys, int64_t count, int32_t n_surf, const double*
 
 /* The FSM sweep (engine.py:215-313 / 316-357). `jobs` is a DEVICE array of
  * n_jobs descriptors; `tile_prefix` a DEVICE array of n_jobs+1 exclusive
- * prefix sums of tiles per job, tiles(job) = passes*teeth*ceil(steps/tile_steps).
+ * prefix sums of tiles per job,
+ * tiles(job) = passes*teeth*ceil((step_hi-step_lo)/tile_steps).
  * tile_steps must be msurf_tile_steps(). Deposits are atomicMin on keys, so
  * the result is independent of scheduling (engine.py:316-317 determinism). */
 int msurf_tile_steps(void);

@@ -30,9 +30,10 @@ class MsurfJob(ctypes.Structure):
 
     _fields_ = [
         ("spacing", c_double), ("x_min", c_double), ("y_min", c_double),
-        ("m", c_int64), ("n", c_int64), ("j_lo", c_int64), ("j_hi", c_int64),
+        ("m", c_int64), ("n", c_int64), ("j_lo", c_int64), ("j_hi", c_int64), ("ld", c_int64),
         ("keys", c_void_p),
         ("t_start", c_double), ("dt", c_double), ("steps", c_int64),
+        ("step_lo", c_int64), ("step_hi", c_int64),
         ("y0", c_double), ("feed_speed", c_double), ("omega", c_double),
         ("tooth_base", c_void_p), ("tooth_rows", c_void_p),
         ("pts", c_void_p), ("tooth_box", c_void_p), ("chunk_circ", c_void_p), ("pass_x0", c_void_p),

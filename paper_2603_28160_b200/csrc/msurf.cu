@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
   __syncthreads();
 
   const long long local = tile - prefix[s_job];
-  const long long nst = (J.steps + kTileSteps - 1) / kTileSteps;
+  const long long nst = (J.step_hi - J.step_lo + kTileSteps - 1) / kTileSteps;
   const int st = (int)(local % nst);
   const long long rem = local / nst;
   const int tooth = (int)(rem % J.teeth);
@@ -183,10 +183,10 @@ __global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
     const double wx_hi = J.x_min + (double)J.m * dd + 1.5 * dd;
     const double wy_lo = J.y_min + (double)J.j_lo * dd - 1.5 * dd;
     const double wy_hi = J.y_min + (double)J.j_hi * dd + 1.5 * dd;
-    const long long s = (long long)st * kTileSteps + tid;
+    const long long s = J.step_lo + (long long)st * kTileSteps + tid;
     uint64_t* my_mask = masks + tid * mask_words;
     for (int w = 0; w < mask_words; ++w) my_mask[w] = 0ull;
-    if (s < J.steps) {
+    if (s < J.step_hi) {
       // engine.py:240-241, kinematics.py:77 — one rounding per op, no FMA
       const double t = __dadd_rn(J.t_start, __dmul_rn((double)s, J.dt));
       const double ty = __dadd_rn(J.y0, __dmul_rn(J.feed_speed, t));
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
   const unsigned span_i = (unsigned)J.m;
   const int j_lo = (int)J.j_lo;
   const unsigned span_j = (unsigned)(J.j_hi - J.j_lo);
-  const int ldk = (int)(J.j_hi - J.j_lo + 1);
+  const int ldk = (int)J.ld;
   unsigned long long* __restrict__ keys = reinterpret_cast<unsigned long long*>(J.keys);
   const double tilt_c = J.tilt_c, tilt_s = J.tilt_s, zoff = J.zoff;
   const int groups = (n_live + 31) >> 5;

@@ -25,9 +25,12 @@ from . import _native
 from .errors import ConfigError, MillsurfError
 from .extensions import Extensions
 from .grid import GridSpec, HeightField, TrajectoryRecord
-from .planner import MODE_REF, SweepPlan, plan, time_step
+from .planner import MODE_REF, SweepPlan, plan, step_window, time_step
 
 DEFAULT_MAX_STEP_ANGLE_RAD = math.radians(0.5)
+# Z-map bytes one sweep job may cover: keeps its RED.MIN traffic in the
+# 126 MB L2 (surfaces above this are cut into feed-direction sub-strips)
+L2_TILE_BYTES = 48 << 20
 
 __all__ = ["SimulationConfig", "SimulationResult", "time_step", "simulate", "simulate_batch",
            "simulate_reference", "run_benchmark", "BenchmarkReport", "BenchmarkRow", "sweep_plans"]
@@ -93,7 +96,7 @@ class SweepBatch:
     one int64 tensor holding all surfaces' Z-maps back to back (u64 keys
     during the sweep, fp64 heights after the decode, in place)."""
 
-    def __init__(self, surfaces, trig: str = "device", device=None):
+    def __init__(self, surfaces, trig: str = "device", device=None, l2_tile_bytes: int = L2_TILE_BYTES):
         torch = _native.require_cuda()
         self.torch = torch
         self.lib = _native.lib()
@@ -136,22 +139,41 @@ class SweepBatch:
         n = len(surfs)
         self.n = n
         self.sentinel_off = ar.add(np.array([s.plan.initial_height for s in surfs], dtype=np.float64))
-        # counters [n][4] then machined [n], contiguous: zeroed by one memset per launch
+        # counters [n][NUM_CTRS] then machined [n], contiguous: zeroed by one memset per launch
         self.ctr_off = ar.add(np.zeros(n * (_native.NUM_CTRS + 1), dtype=np.uint64))
         self.machined_off = self.ctr_off + n * _native.NUM_CTRS * 8
-        groups = {}
-        for i, s in enumerate(surfs):
-            groups.setdefault(s.plan.mode, []).append(i)
+        # Jobs: each surface is cut into feed-direction sub-strips whose Z-map
+        # slab fits in L2 (the RED.MIN traffic then stays on chip), each with
+        # the time window whose footprint can reach it; sub-strips of one
+        # surface are consecutive in the tile order so resident CTAs share one.
         tile_steps = self.lib.msurf_tile_steps()
+        jobs = []  # (surface index, j_lo, j_hi, step_lo, step_hi)
+        for i, s in enumerate(surfs):
+            w = s.j_hi - s.j_lo + 1
+            rows = s.plan.grid.m + 1
+            k = max(1, min(w, -(-rows * w * 8 // l2_tile_bytes)))
+            if s.plan.record:
+                k = 1  # the trajectory record needs every step in one job
+            for q in range(k):
+                lo = s.j_lo + (w * q) // k
+                hi = s.j_lo + (w * (q + 1)) // k - 1
+                whole = k == 1 and s.j_lo == 0 and s.j_hi == s.plan.grid.n
+                s_lo, s_hi = (0, s.plan.steps) if (whole or s.plan.record) else step_window(s.plan, lo, hi)
+                if s_hi > s_lo:
+                    jobs.append((i, lo, hi, s_lo, s_hi))
+        self.jobs = jobs
+        groups = {}
+        for jn, jb in enumerate(jobs):
+            groups.setdefault(surfs[jb[0]].plan.mode, []).append(jn)
         self.group_meta = []
-        for mode, idx in sorted(groups.items()):
-            tiles = [surfs[i].plan.passes * surfs[i].plan.teeth *
-                     ((surfs[i].plan.steps + tile_steps - 1) // tile_steps) for i in idx]
+        for mode, jidx in sorted(groups.items()):
+            tiles = [surfs[jobs[j][0]].plan.passes * surfs[jobs[j][0]].plan.teeth *
+                     ((jobs[j][4] - jobs[j][3] + tile_steps - 1) // tile_steps) for j in jidx]
             prefix = np.concatenate([[0], np.cumsum(tiles)]).astype(np.int64)
-            job_off = ar.add(np.zeros(len(idx) * ctypes.sizeof(_native.MsurfJob), dtype=np.uint8))
+            job_off = ar.add(np.zeros(len(jidx) * ctypes.sizeof(_native.MsurfJob), dtype=np.uint8))
             pre_off = ar.add(prefix)
-            self.group_meta.append((mode, idx, job_off, pre_off, int(prefix[-1]),
-                                    max(surfs[i].plan.points for i in idx)))
+            self.group_meta.append((mode, jidx, job_off, pre_off, int(prefix[-1]),
+                                    max(surfs[jobs[j][0]].plan.points for j in jidx)))
         keys_ptr = self.keys.data_ptr()
         traj_ptr = self.traj.data_ptr() if self.traj is not None else 0
         self.traj_off = []
@@ -163,16 +185,19 @@ class SweepBatch:
 
         def fill(base):
             out = []
-            for mode, idx, job_off, _, _, _ in self.group_meta:
-                arr = (_native.MsurfJob * len(idx))()
-                for k, i in enumerate(idx):
+            for mode, jidx, job_off, _, _, _ in self.group_meta:
+                arr = (_native.MsurfJob * len(jidx))()
+                for k, jn in enumerate(jidx):
+                    i, lo, hi, s_lo, s_hi = jobs[jn]
                     s, o, p = surfs[i], offs[i], surfs[i].plan
                     g = p.grid
                     j = arr[k]
                     j.spacing, j.x_min, j.y_min = g.spacing_mm, g.x_min_mm, g.y_min_mm
-                    j.m, j.n, j.j_lo, j.j_hi = g.m, g.n, s.j_lo, s.j_hi
-                    j.keys = keys_ptr + s.key_off * 8
+                    j.m, j.n, j.j_lo, j.j_hi = g.m, g.n, lo, hi
+                    j.ld = s.j_hi - s.j_lo + 1
+                    j.keys = keys_ptr + (s.key_off + (lo - s.j_lo)) * 8
                     j.t_start, j.dt, j.steps = p.t_start, p.dt, p.steps
+                    j.step_lo, j.step_hi = s_lo, s_hi
                     j.y0, j.feed_speed, j.omega = p.y0, p.feed_speed, p.omega
                     for name in ("tooth_base", "tooth_rows", "pts", "tooth_box", "chunk_circ",
                                  "pass_x0", "min_index"):
@@ -182,7 +207,9 @@ class SweepBatch:
                     j.vib_amp, j.vib_omega, j.vib_phase = p.vib_amp, p.vib_omega, p.vib_phase
                     j.trig_table = base + o["trig_table"] if "trig_table" in o else None
                     j.vib_table = base + o["vib_table"] if "vib_table" in o else None
-                    j.traj = traj_ptr + self.traj_off[i] * 8 if self.need_traj[i] else None
+                    # trajectory rows are written by the job that owns column j_lo of
+                    # the surface and covers every step (REF mode records need no cull)
+                    j.traj = (traj_ptr + self.traj_off[i] * 8) if (self.need_traj[i] and lo == s.j_lo) else None
                     j.teeth, j.points, j.passes = p.teeth, p.points, p.passes
                 out.append((job_off, bytes(arr)))
             return out

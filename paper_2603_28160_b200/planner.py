@@ -249,6 +249,29 @@ def _pack(p: SweepPlan) -> None:
                             b[:, :, 4].min(1), b[:, :, 5].max(1)], axis=1)
 
 
+def reach_y(p: SweepPlan) -> float:
+    """Upper bound of |y_w - ty| over every edge point and rotation (feed-
+    direction reach of the footprint), from the device cull records."""
+    c = p.chunk_circ
+    rad = np.sqrt(c[:, :, 0] ** 2 + c[:, :, 1] ** 2)
+    return float(np.max(abs(p.tilt_c) * rad + c[:, :, 3] + np.abs(c[:, :, 4]))) + 2.0 * p.grid.spacing_mm
+
+
+def step_window(p: SweepPlan, j_lo: int, j_hi: int):
+    """Steps [s_lo, s_hi) whose footprint can reach node columns [j_lo, j_hi]
+    (each strip sweeps only the time steps that meet it).
+    Conservative: the kernel's exact 2-D chunk cull still applies inside."""
+    g = p.grid
+    reach = reach_y(p) + 1.5 * g.spacing_mm
+    y_lo = g.y_min_mm + j_lo * g.spacing_mm - reach
+    y_hi = g.y_min_mm + j_hi * g.spacing_mm + reach
+    t_lo = (y_lo - p.y0) / p.feed_speed
+    t_hi = (y_hi - p.y0) / p.feed_speed
+    s_lo = math.floor((t_lo - p.t_start) / p.dt) - 2
+    s_hi = math.ceil((t_hi - p.t_start) / p.dt) + 3
+    return max(0, min(p.steps, s_lo)), max(0, min(p.steps, s_hi))
+
+
 def _plan_ref(config) -> SweepPlan:
     """engine.py:134-212 restated."""
     tool, proc, grid = config.tool, config.process, config.grid

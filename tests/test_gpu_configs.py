@@ -33,12 +33,21 @@ def _rel(a, b):
 
 
 def _check_vs_oracle(cfg, ext, every=64):
-    res = ms.simulate(cfg, ext)
+    """Heights: bit-exact with host-libm trig (the oracle's cos/sin). With the
+    device's correctly rounded sincos, glibc's 1-ulp misroundings (~0.1 % of
+    rows) can move a height by an ulp where z' depends on the angle (tilt), so
+    that mode is held to 1e-12 mm (north-star gate 1e-6 mm)."""
     h_ref, p, ctr, _ = xorc.ext_sweep(cfg, ext, workers=WORKERS)
+    exact = ms.simulate(cfg, ext, trig="host")
+    assert np.array_equal(exact.field.heights, h_ref), int(np.count_nonzero(exact.field.heights != h_ref))
+    res = ms.simulate(cfg, ext)
     assert res.trajectory_points == ctr["trajectory_points"]
     assert res.cells_updated == ctr["cells_updated"]
     h = res.field.device_heights().cpu().numpy()
-    assert np.array_equal(h, h_ref), int(np.count_nonzero(h != h_ref))
+    diff = np.abs(h - h_ref)
+    assert float(diff.max()) <= 1e-12, (float(diff.max()), int(np.count_nonzero(diff)))
+    if ext is None or ext.tilt_rad == 0.0:
+        assert np.array_equal(h, h_ref), int(np.count_nonzero(diff))
     a2 = h_ref.reshape(p.m + 1, p.n + 1)
     got = ms.areal_metrics(res.field, uncut="exclude")
     exp = orc.areal_metrics(a2, p.initial_height, uncut="exclude")
@@ -71,7 +80,7 @@ def test_config3_batch_vs_oracle():
     mets = ms.areal_metrics_batch([o.field for o in out], uncut="exclude")
     for (c, e), o, m in zip(pairs, out, mets):
         h_ref, p, ctr, _ = xorc.ext_sweep(c, e, workers=WORKERS)
-        assert np.array_equal(o.field.device_heights().cpu().numpy(), h_ref)
+        assert np.array_equal(o.field.device_heights().cpu().numpy(), h_ref)  # no tilt: exact
         exp = orc.areal_metrics(h_ref.reshape(p.m + 1, p.n + 1), p.initial_height, uncut="exclude")
         assert _rel(m.sa_um, exp["Sa"]) < REL and _rel(m.sq_um, exp["Sq"]) < REL
 

@@ -33,12 +33,18 @@ namespace {
 #define MSURF_TWO_SIDED 1  // tilt mode: deposit only local minima of each cell run
 #endif
 #ifndef MSURF_MIN_BLOCKS
-#define MSURF_MIN_BLOCKS 4  // CTAs per SM the register budget is sized for
+#define MSURF_MIN_BLOCKS 6  // CTAs per SM the register budget is sized for (80 regs at 128 threads)
 #endif
 
-constexpr int kThreads = 256;
-constexpr int kTileSteps = 256;  // rows (time steps) per CTA; == kThreads
+#ifndef MSURF_TILE
+#define MSURF_TILE 128
+#endif
+
+constexpr int kThreads = 256;      // reduction / stream kernels
 constexpr int kWarps = kThreads / 32;
+constexpr int kTileSteps = MSURF_TILE;  // sweep: time steps per CTA == threads per CTA
+constexpr int kSweepThreads = kTileSteps;
+constexpr int kSweepWarps = kSweepThreads / 32;
 
 thread_local std::string g_err;
 
@@ -127,7 +133,7 @@ __device__ __forceinline__ unsigned warp_sum_u(unsigned v) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
+__global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
     sweep_kernel(const msurf_job* __restrict__ jobs, int n_jobs,
                  const int64_t* __restrict__ prefix, int mask_words) {
   constexpr int RW = MODE == MSURF_MODE_REF ? 8 : 4;  // doubles of row data per live step
@@ -136,11 +142,11 @@ __global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
   uint64_t* masks = reinterpret_cast<uint64_t*>(rowv + kTileSteps * 8);      // [T][W] by thread
   int* live = reinterpret_cast<int*>(masks + kTileSteps * mask_words);       // [T] slot -> thread
   __shared__ msurf_job J;
-  __shared__ int warp_cnt[kWarps];
-  __shared__ unsigned warp_eval[kWarps];
-  __shared__ unsigned warp_eng[kWarps];
+  __shared__ int warp_cnt[kSweepWarps];
+  __shared__ unsigned warp_eval[kSweepWarps];
+  __shared__ unsigned warp_eng[kSweepWarps];
   __shared__ int s_job;
-  __shared__ double4 ptstage[kWarps][32];  // per-warp copy of the current chunk's point records
+  __shared__ double4 ptstage[kSweepWarps][32];  // per-warp copy of the current chunk's point records
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -159,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
   {
     const unsigned long long* src = reinterpret_cast<const unsigned long long*>(jobs + s_job);
     unsigned long long* dst = reinterpret_cast<unsigned long long*>(&J);
-    for (int w = tid; w < (int)(sizeof(msurf_job) / 8); w += kThreads) dst[w] = src[w];
+    for (int w = tid; w < (int)(sizeof(msurf_job) / 8); w += kSweepThreads) dst[w] = src[w];
   }
   __syncthreads();
 
@@ -287,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
   int base = 0, n_live = 0;
   unsigned n_eval_cta = 0, n_eng_cta = 0;
 #pragma unroll
-  for (int w = 0; w < kWarps; ++w) {
+  for (int w = 0; w < kSweepWarps; ++w) {
     if (w < warp) base += warp_cnt[w];
     n_live += warp_cnt[w];
     n_eval_cta += warp_eval[w];
@@ -326,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, MSURF_MIN_BLOCKS)
   const int units = groups * nchunk;
   unsigned n_dep = 0, n_atom = 0;
 
-  for (int u = warp; u < units; u += kWarps) {
+  for (int u = warp; u < units; u += kSweepWarps) {
     const int g = u / nchunk;
     const int q = u - g * nchunk;
     const int slot = g * 32 + lane;
@@ -722,15 +728,15 @@ int msurf_sweep(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile_prefi
   switch (mode) {
     case MSURF_MODE_REF:
       if (smem > 48 * 1024) e = cudaFuncSetAttribute(sweep_kernel<MSURF_MODE_REF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e == cudaSuccess) sweep_kernel<MSURF_MODE_REF><<<(unsigned)n_tiles, kThreads, smem, st>>>(jobs, n_jobs, tile_prefix, mask_words);
+      if (e == cudaSuccess) sweep_kernel<MSURF_MODE_REF><<<(unsigned)n_tiles, kSweepThreads, smem, st>>>(jobs, n_jobs, tile_prefix, mask_words);
       break;
     case MSURF_MODE_EXT:
       if (smem > 48 * 1024) e = cudaFuncSetAttribute(sweep_kernel<MSURF_MODE_EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e == cudaSuccess) sweep_kernel<MSURF_MODE_EXT><<<(unsigned)n_tiles, kThreads, smem, st>>>(jobs, n_jobs, tile_prefix, mask_words);
+      if (e == cudaSuccess) sweep_kernel<MSURF_MODE_EXT><<<(unsigned)n_tiles, kSweepThreads, smem, st>>>(jobs, n_jobs, tile_prefix, mask_words);
       break;
     case MSURF_MODE_EXT_TILT:
       if (smem > 48 * 1024) e = cudaFuncSetAttribute(sweep_kernel<MSURF_MODE_EXT_TILT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e == cudaSuccess) sweep_kernel<MSURF_MODE_EXT_TILT><<<(unsigned)n_tiles, kThreads, smem, st>>>(jobs, n_jobs, tile_prefix, mask_words);
+      if (e == cudaSuccess) sweep_kernel<MSURF_MODE_EXT_TILT><<<(unsigned)n_tiles, kSweepThreads, smem, st>>>(jobs, n_jobs, tile_prefix, mask_words);
       break;
     default:
       return set_err("msurf_sweep: unknown mode");

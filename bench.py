@@ -49,6 +49,14 @@ def _env_int(k, d):
         return d
 
 
+def _local_device() -> int:
+    import torch
+
+    local = _env_int("LOCAL_RANK", 0)
+    n = torch.cuda.device_count()
+    return local % n if n else local
+
+
 def workload(cfg_id: int):
     from paper_2603_28160_b200 import configs
 
@@ -251,7 +259,7 @@ def run_ours(args, rank, world):
     from paper_2603_28160_b200.planner import plan as make_plan
 
     dist = torch.distributed
-    local = _env_int("LOCAL_RANK", 0)
+    local = _local_device()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
@@ -261,9 +269,12 @@ def run_ours(args, rank, world):
     every = meta.get("profiles_every", 64)
     j_lo, j_hi = sharded.strip_bounds(p.grid.n + 1, world)[rank]
     batch = SweepBatch([(p, j_lo, j_hi)])
-    pipe = SurfacePipeline(batch, every=every, uncut=uncut) if world == 1 else None
-    if pipe is not None and not args.no_graph:
-        pipe.capture()  # three CUDA graphs: fill | sweep | decode + reductions
+    if world == 1:
+        pipe = SurfacePipeline(batch, every=every, uncut=uncut)
+        if not args.no_graph:
+            pipe.capture()  # three CUDA graphs: fill | sweep | decode + reductions
+    else:
+        pipe = sharded.StripPipeline(batch, every=every, uncut=uncut, group=group)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def barrier():
@@ -271,16 +282,10 @@ def run_ours(args, rank, world):
             dist.barrier()
 
     def step(events):
-        if pipe is not None:
-            # single GPU: sync-free launch sequence, results read after the timed region
-            pipe.run(events=events)
-            return None
-        batch.launch(events=events)
-        res = sharded.StripResult(plan=p, j_lo=j_lo, j_hi=j_hi, heights=batch.heights()[0], counters={},
-                                  cells_updated=0, main_loop_seconds=0.0, batch=batch)
-        am = sharded.areal_metrics_strip(res, uncut=uncut, group=group)
-        prs = sharded.profile_roughness_strip(res, every=every, uncut=uncut, group=group)
-        return am, prs
+        # sync-free launch sequence (N>1: plus three tiny all-reduces); the
+        # results are read back after the timed region
+        pipe.run(events=events)
+        return None
 
     # warm-up
     for _ in range(args.warmup):
@@ -304,15 +309,12 @@ def run_ours(args, rank, world):
         torch.cuda.synchronize()
         step_ms.append(ev[0].elapsed_time(e_end))
         sweep_ms.append(ev[1].elapsed_time(ev[2]))
-        launches += pipe.launches_per_run if pipe is not None else batch.launches_per_run + 6
+        launches += pipe.launches_per_run
     barrier()
     torch.cuda.synchronize()
     clk = clocks.stop()
     ctr, machined = batch.counters()
-    if pipe is not None:
-        am, prs = pipe.collect()[0]
-    else:
-        am, prs = out
+    am, prs = pipe.collect()[0] if world == 1 else pipe.collect()
 
     tot = torch.tensor([sum(step_ms), sum(sweep_ms)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -453,7 +455,7 @@ def run_batch(args, rank, world):
     from paper_2603_28160_b200.pipeline import SurfacePipeline
 
     dist = torch.distributed
-    local = _env_int("LOCAL_RANK", 0)
+    local = _local_device()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     base, ext, meta, ranges, mine, plans, total_points = config3_workload(rank, world)
@@ -576,8 +578,10 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(_env_int("LOCAL_RANK", 0))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(_local_device())
+        # MSURF_DIST_BACKEND=gloo lets the N>1 path be exercised with several
+        # ranks on one GPU (functional check only; NCCL needs one GPU per rank)
+        dist.init_process_group(os.environ.get("MSURF_DIST_BACKEND", "nccl"))
     try:
         if args.config == 3:
             run_batch(args, rank, world)

@@ -186,3 +186,107 @@ def profile_roughness_strip(res: StripResult, every: int = 64, uncut: str = "rai
     first[:, 5:6] = sabs
     rows = first.cpu().numpy()
     return [_finish_profile(r, i, uncut) for r, i in zip(rows, idx)]
+
+
+class StripPipeline:
+    """Sync-free multi-GPU step for one strip-sharded surface: sweep of this
+    rank's strip, then the roughness reductions with THREE small NCCL
+    all-reduces per step (round 1: areal + profile sums, and their max/min;
+    round 2: areal central moments + profile |d| sums). Results are read back
+    by collect() after the timed region."""
+
+    def __init__(self, batch, every: int = 64, uncut: str = "exclude", group=None):
+        import torch
+
+        self.torch = torch
+        self.lib = _native.lib()
+        self.batch = batch
+        s = batch.surfs[0]
+        self.plan, self.j_lo, self.j_hi = s.plan, s.j_lo, s.j_hi
+        g = self.plan.grid
+        self.ld = self.j_hi - self.j_lo + 1
+        self.rows = g.m + 1
+        self.uncut, self.exclude, self.group = uncut, int(uncut == "exclude"), group
+        self.prof_idx = list(range(0, g.m + 1, every)) if every else []
+        P = len(self.prof_idx)
+        dev = batch.dev
+        f64 = torch.float64
+        self.work = torch.empty(_native.RED_BLOCKS * 5, dtype=f64, device=dev)
+        self.st1 = torch.empty((1, 5), dtype=f64, device=dev)
+        self.st2 = torch.empty((1, 4), dtype=f64, device=dev)
+        self.prof = torch.empty((max(P, 1), 8), dtype=f64, device=dev)
+        self.first = torch.empty((max(P, 1), 8), dtype=f64, device=dev)
+        self.starts = torch.tensor([i * self.ld for i in self.prof_idx] or [0], dtype=torch.int64, device=dev)
+        self.P = P
+        self.launches_per_run = batch.launches_per_run + 4 + (2 if P else 0)
+
+    def _allreduce(self, t, op):
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.all_reduce(t, op=op, group=self.group)
+
+    def run(self, events=None):
+        import torch.distributed as dist
+
+        torch, lib, b = self.torch, self.lib, self.batch
+        st = torch.cuda.current_stream()
+        sp = int(st.cuda_stream)
+        if events:
+            events[0].record(st)
+        b.launch_fill(sp)
+        if events:
+            events[1].record(st)
+        b.launch_sweep(sp)
+        if events:
+            events[2].record(st)
+        b.launch_decode(sp)
+        h = b.keys.data_ptr()
+        sent = b.base + b.sentinel_off
+        P = self.P
+        _native.check(lib.msurf_areal_pass1(h, self.ld, 0, 1, 0, 0, self.rows, self.ld, sent, self.exclude,
+                                            self.work.data_ptr(), self.st1.data_ptr(), sp))
+        if P:
+            _native.check(lib.msurf_profiles(h, 0, 1, self.starts.data_ptr(), P, self.ld, 1, sent,
+                                             self.exclude, None, self.prof.data_ptr(), sp))
+        # round 1: sums [sum z, n, n_uncut] and extrema [max z, -min z] of areal + profiles
+        sums = torch.cat([self.st1[:, [0, 3, 4]], self.prof[:P, 0:3]], dim=0)
+        ext = torch.cat([torch.stack([self.st1[:, 1], -self.st1[:, 2]], dim=1),
+                         torch.stack([self.prof[:P, 3], -self.prof[:P, 4]], dim=1)], dim=0)
+        self._allreduce(sums, dist.ReduceOp.SUM)
+        self._allreduce(ext, dist.ReduceOp.MAX)
+        self.st1[:, [0, 3, 4]] = sums[0:1]
+        self.st1[:, 1], self.st1[:, 2] = ext[0:1, 0], -ext[0:1, 1]
+        if P:
+            self.first[:P, 0:3] = sums[1:]
+            self.first[:P, 3], self.first[:P, 4] = ext[1:, 0], -ext[1:, 1]
+        # round 2: central moments around the global means
+        _native.check(lib.msurf_areal_pass2(h, self.ld, 0, 1, 0, 0, self.rows, self.ld, sent, self.exclude,
+                                            self.st1.data_ptr(), self.work.data_ptr(), self.st2.data_ptr(), sp))
+        if P:
+            _native.check(lib.msurf_profiles(h, 0, 1, self.starts.data_ptr(), P, self.ld, 1, sent,
+                                             self.exclude, self.first.data_ptr(), self.prof.data_ptr(), sp))
+        mom = torch.cat([self.st2.reshape(-1), self.prof[:P, 5]])
+        self._allreduce(mom, dist.ReduceOp.SUM)
+        self.st2.copy_(mom[:4].view(1, 4))
+        if P:
+            self.first[:P, 5] = mom[4:]
+        if events:
+            events[3].record(st)
+
+    def collect(self):
+        st1 = self.st1[0].cpu().numpy()
+        st2 = self.st2[0].cpu().numpy()
+        try:
+            am = _finish_areal(st1, st2, self.uncut)
+        except DomainError as exc:
+            am = exc
+        prs = []
+        if self.P:
+            rows = self.first[: self.P].cpu().numpy()
+            for r, i in zip(rows, self.prof_idx):
+                try:
+                    prs.append(_finish_profile(r, i, self.uncut))
+                except DomainError as exc:
+                    prs.append(exc)
+        return am, prs

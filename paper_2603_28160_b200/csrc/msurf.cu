@@ -29,6 +29,9 @@
 
 namespace {
 
+#ifndef MSURF_FLOAT_DEDUPE
+#define MSURF_FLOAT_DEDUPE 1  // tilt mode: neighbour comparisons on float32 z' (exactness argued inline)
+#endif
 #ifndef MSURF_TWO_SIDED
 #define MSURF_TWO_SIDED 1  // tilt mode: deposit only local minima of each cell run
 #endif
@@ -360,7 +363,7 @@ __global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
 #pragma unroll 2
     for (int k = 0; k < p_end; ++k) {
       const double4 pt = ptstage[warp][k];  // same address in every lane: broadcast
-      double xw, yw;
+      double xw, yw, zkey_src = 0.0;
       uint64_t key;
       if (MODE == MSURF_MODE_REF) {
         // engine.py:289-296: xw = ((m00*xp + m01*yp) + m02*zp) + m03
@@ -379,6 +382,7 @@ __global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
           const double zz = __dadd_rn(__dadd_rn(__dmul_rn(tilt_s, vv), pt.w), zoff);
           yw = __dadd_rn(yv, r[3]);
           key = enc_key_raw(zz);  // zz = (..) + zoff with zoff != -0 (host-canonical): never -0
+          zkey_src = zz;
         } else {
           yw = __dadd_rn(vv, r[3]);
           key = (uint64_t)__double_as_longlong(pt.z);
@@ -399,12 +403,28 @@ __global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
       const int idx_prev = __shfl_up_sync(0xffffffffu, idx, 1);
       bool dep = inside & ((lane == 0) | (idx != idx_prev));
       if (MODE == MSURF_MODE_EXT_TILT) {
+#if MSURF_FLOAT_DEDUPE
+        // compare float32 roundings of z': rounding is monotone, so
+        // zf > zf_neighbour proves z' > z'_neighbour; a lane is skipped only
+        // when a same-cell neighbour is provably lower, and every chain of
+        // skips ends at a deposited lane whose z' is lower still (ties in
+        // float keep both deposits) -> 32-bit shuffles instead of 64-bit
+        const float zf = __double2float_rn(zkey_src);
+        const float zf_prev = __shfl_up_sync(0xffffffffu, zf, 1);
+        dep = inside & !((lane > 0) & (idx == idx_prev) & (zf > zf_prev));
+#if MSURF_TWO_SIDED
+        const int idx_next = __shfl_down_sync(0xffffffffu, idx, 1);
+        const float zf_next = __shfl_down_sync(0xffffffffu, zf, 1);
+        dep &= !((lane < 31) & (idx == idx_next) & (zf > zf_next));
+#endif
+#else
         const uint64_t key_prev = __shfl_up_sync(0xffffffffu, key, 1);
         dep = inside & ((lane == 0) | (idx != idx_prev) | (key < key_prev));
 #if MSURF_TWO_SIDED
         const int idx_next = __shfl_down_sync(0xffffffffu, idx, 1);
         const uint64_t key_next = __shfl_down_sync(0xffffffffu, key, 1);
         dep &= (lane == 31) | (idx != idx_next) | (key <= key_next);
+#endif
 #endif
       }
       n_dep += inside;

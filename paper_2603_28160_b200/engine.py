@@ -53,15 +53,59 @@ class SimulationConfig:
     worker_count: int = 1
 
 
-@dataclass
+class _Launch:
+    """Device-side state of one asynchronous sweep launch: the batch (keeps
+    every buffer alive), its events, and the small D2H read of the counters
+    performed once, on first demand."""
+
+    def __init__(self, batch, events):
+        self.batch, self.events = batch, events
+        self._small = None
+
+    def counters(self):
+        if self._small is None:
+            self._small = self.batch.counters()
+        return self._small
+
+    def device_seconds(self):
+        self.events[3].synchronize()
+        return self.events[0].elapsed_time(self.events[3]) * 1e-3
+
+
 class SimulationResult:
-    field: HeightField
-    trajectory: TrajectoryRecord | None
-    time_steps: int
-    trajectory_points: int
-    cells_updated: int
-    main_loop_seconds: float
-    counters: dict = field(default_factory=dict)
+    """Same fields as millsurf.engine.SimulationResult (engine.py:76-83).
+    ``simulate`` returns before the GPU finishes: ``cells_updated``,
+    ``main_loop_seconds`` and ``counters`` synchronise on first access, the
+    height field stays in HBM until ``field.heights`` is read."""
+
+    def __init__(self, field, trajectory, time_steps, trajectory_points, cells_updated=None,
+                 main_loop_seconds=None, counters=None, launch=None, index=0, share=1.0):
+        self.field, self.trajectory = field, trajectory
+        self.time_steps, self.trajectory_points = time_steps, trajectory_points
+        self._cells, self._secs, self._ctrs = cells_updated, main_loop_seconds, counters
+        self._launch, self._index, self._share = launch, index, share
+
+    @property
+    def cells_updated(self) -> int:
+        if self._cells is None:
+            self._cells = int(self._launch.counters()[1][self._index])
+        return self._cells
+
+    @property
+    def main_loop_seconds(self) -> float:
+        if self._secs is None:
+            self._secs = self._launch.device_seconds() * self._share
+        return self._secs
+
+    @property
+    def counters(self) -> dict:
+        if self._ctrs is None:
+            self._ctrs = _counters_dict(self._launch.counters()[0][self._index])
+        return self._ctrs
+
+    def __repr__(self) -> str:
+        return (f"SimulationResult(time_steps={self.time_steps}, trajectory_points={self.trajectory_points}, "
+                f"cells_updated={self.cells_updated})")
 
 
 @dataclass
@@ -326,12 +370,27 @@ def simulate(config: SimulationConfig, extensions: Extensions | None = None, *,
     (exactly the reference's values) instead of the device's correctly
     rounded double-double sincos — the parity mode."""
     p = plan(config, extensions)
-    views, small, machined, ms, trajs, _ = sweep_plans([(p, 0, p.grid.n)], trig=trig)
-    field_ = HeightField(p.grid, p.initial_height, device=views[0])
-    trajectory = _build_trajectory(p, trajs[0]) if p.record else None
-    return SimulationResult(field=field_, trajectory=trajectory, time_steps=p.steps,
-                            trajectory_points=p.trajectory_points, cells_updated=int(machined[0]),
-                            main_loop_seconds=ms * 1e-3, counters=_counters_dict(small[0]))
+    return _launch_results([p], trig)[0]
+
+
+def _launch_results(plans, trig):
+    """Upload, launch asynchronously, wrap the fields (no host sync unless a
+    trajectory record is requested)."""
+    torch = _native.require_cuda()
+    b = SweepBatch([(p, 0, p.grid.n) for p in plans], trig=trig)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    b.launch(events=ev)
+    lk = _Launch(b, ev)
+    views, trajs = b.heights(), b.trajectories()
+    sents = b.sentinels_device()
+    out = []
+    for i, (p, v, tr) in enumerate(zip(plans, views, trajs)):
+        f = HeightField(p.grid, p.initial_height, device=v)
+        f._dev_sentinel = sents[i:i + 1]
+        out.append(SimulationResult(field=f, trajectory=_build_trajectory(p, tr) if p.record else None,
+                                    time_steps=p.steps, trajectory_points=p.trajectory_points,
+                                    launch=lk, index=i, share=1.0 / len(plans)))
+    return out
 
 
 def simulate_batch(configs, extensions=None, *, trig: str = "device"):
@@ -346,15 +405,7 @@ def simulate_batch(configs, extensions=None, *, trig: str = "device"):
     plans = [plan(c, e) for c, e in zip(configs, exts)]
     if not plans:
         return []
-    views, small, machined, ms, trajs, _ = sweep_plans([(p, 0, p.grid.n) for p in plans], trig=trig)
-    out = []
-    for p, v, row, mc, tr in zip(plans, views, small, machined, trajs):
-        out.append(SimulationResult(
-            field=HeightField(p.grid, p.initial_height, device=v),
-            trajectory=_build_trajectory(p, tr) if p.record else None,
-            time_steps=p.steps, trajectory_points=p.trajectory_points, cells_updated=int(mc),
-            main_loop_seconds=ms * 1e-3 / len(plans), counters=_counters_dict(row)))
-    return out
+    return _launch_results(plans, trig)
 
 
 def simulate_reference(config: SimulationConfig, extensions: Extensions | None = None) -> SimulationResult:

@@ -152,6 +152,15 @@ def _sentinel_tensor(torch, values, device):
     return torch.tensor(np.asarray(values, dtype=np.float64), device=device)
 
 
+def _field_sentinel(torch, field, device):
+    """Device stock height of a field: the sweep's own copy when available
+    (no H2D copy / host sync), else a fresh 1-element tensor."""
+    s = getattr(field, "_dev_sentinel", None)
+    if s is not None and s.device == device:
+        return s
+    return _sentinel_tensor(torch, [field.initial_height_mm], device)
+
+
 def areal_metrics(field: HeightField, roi=None, leveling: str = "mean", uncut: str = "raise") -> ArealMetrics:
     """Areal parameters over the inclusive node range (i_lo, j_lo, i_hi, j_hi)."""
     if leveling != "mean":
@@ -163,7 +172,7 @@ def areal_metrics(field: HeightField, roi=None, leveling: str = "mean", uncut: s
     i_lo, j_lo, i_hi, j_hi = _check_roi(field.spec, roi)
     torch = _native.require_cuda()
     h = field.device_heights()
-    sent = _sentinel_tensor(torch, [field.initial_height_mm], h.device)
+    sent = _field_sentinel(torch, field, h.device)
     st1, st2 = areal_moments_device(h, field.spec.n + 1, 1, 0,
                                     (i_lo, j_lo, i_hi - i_lo + 1, j_hi - j_lo + 1), sent,
                                     uncut == "exclude")
@@ -204,7 +213,12 @@ def areal_metrics_batch(fields, roi=None, uncut: str = "raise"):
                 out.append(exc)
         return out
     i_lo, j_lo, i_hi, j_hi = _check_roi(spec, roi)
-    sent = _sentinel_tensor(torch, [f.initial_height_mm for f in fields], devs[0].device)
+    ss = [getattr(f, "_dev_sentinel", None) for f in fields]
+    if all(x is not None for x in ss) and all(x.data_ptr() == ss[0].data_ptr() + 8 * k for k, x in enumerate(ss)):
+        # the batch's own contiguous device sentinels (simulate_batch): no H2D copy
+        sent = ss[0].as_strided((len(fields),), (1,))
+    else:
+        sent = _sentinel_tensor(torch, [f.initial_height_mm for f in fields], devs[0].device)
     st1, st2 = areal_moments_device(devs[0], spec.n + 1, len(fields), stride or 0,
                                     (i_lo, j_lo, i_hi - i_lo + 1, j_hi - j_lo + 1), sent,
                                     uncut == "exclude")
@@ -300,7 +314,7 @@ def profile_roughness(field: HeightField, indices=None, direction: str = "feed",
         raise DomainError(f"direction must be 'feed' or 'pickfeed', got {direction!r}")
     torch = _native.require_cuda()
     h = field.device_heights()
-    sent = _sentinel_tensor(torch, [field.initial_height_mm], h.device)
+    sent = _field_sentinel(torch, field, h.device)
     rows = _profiles_device(h, 1, 0, starts, length, step, sent, uncut == "exclude")
     rows = rows.cpu().numpy().reshape(len(indices), 8)
     return [_finish_profile(r, idx, uncut) for r, idx in zip(rows, indices)]

@@ -135,6 +135,28 @@ __device__ __forceinline__ unsigned warp_sum_u(unsigned v) {
   return v;
 }
 
+// 2-D box test of one tool-frame box [xl xh yl yh zl zh] rotated by (c, s),
+// offset by (xoff, ty), after the lead tilt, against a window. Conservative
+// by construction of the window (1.5 cells >> rounding differences).
+template <int MODE>
+__device__ __forceinline__ bool tool_box_hits(const double* b, double c, double sn, double xoff, double ty,
+                                              double wx_lo, double wx_hi, double wy_lo, double wy_hi,
+                                              double tilt_c, double tilt_s) {
+  const double ns = -sn;
+  const double xl = b[0], xh = b[1], yl = b[2], yh = b[3];
+  const double x_lo = fmin(c * xl, c * xh) + fmin(sn * yl, sn * yh) + xoff;
+  const double x_hi = fmax(c * xl, c * xh) + fmax(sn * yl, sn * yh) + xoff;
+  double v_lo = fmin(ns * xl, ns * xh) + fmin(c * yl, c * yh);
+  double v_hi = fmax(ns * xl, ns * xh) + fmax(c * yl, c * yh);
+  if (MODE == MSURF_MODE_EXT_TILT) {
+    const double a1 = tilt_c * v_lo, a2 = tilt_c * v_hi;
+    const double b1 = tilt_s * b[4], b2 = tilt_s * b[5];
+    v_lo = fmin(a1, a2) - fmax(b1, b2);
+    v_hi = fmax(a1, a2) - fmin(b1, b2);
+  }
+  return (x_hi >= wx_lo) & (x_lo <= wx_hi) & (v_hi + ty >= wy_lo) & (v_lo + ty <= wy_hi);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
     sweep_kernel(const msurf_job* __restrict__ jobs, int n_jobs,
@@ -199,87 +221,95 @@ __global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
       // engine.py:240-241, kinematics.py:77 — one rounding per op, no FMA
       const double t = __dadd_rn(J.t_start, __dmul_rn((double)s, J.dt));
       const double ty = __dadd_rn(J.y0, __dmul_rn(J.feed_speed, t));
-      double c, sn;
-      if (J.trig_table) {
-        c = J.trig_table[(s * J.teeth + tooth) * 2 + 0];
-        sn = J.trig_table[(s * J.teeth + tooth) * 2 + 1];
-      } else {
-        const double th = __dsub_rn(J.tooth_base[tooth], __dmul_rn(J.omega, t));
-        msurf_sincos(th, &sn, &c);
+      const double th = __dsub_rn(J.tooth_base[tooth], __dmul_rn(J.omega, t));
+      const double x0p = J.pass_x0[pass];
+      // Cheap conservative pre-cull of the whole tooth with a float sincos
+      // (double Cody-Waite reduction, |error| < 1e-6 in c, s -> < 1e-4 mm of
+      // position for a 100 mm tool, covered by the extra margin; vibration
+      // covered by its amplitude): most rows of a windowed strip, and the
+      // rows far from the grid, never pay for the double-double sincos.
+      bool maybe = true;
+      if (!J.trig_table && !(J.traj && pass == 0)) {
+        const double kd = rint(th * MSURF_TWO_OVER_PI);
+        const double r = __fma_rn(-kd, MSURF_PIO2_2, __fma_rn(-kd, MSURF_PIO2_1, th));
+        float sf, cf;
+        __sincosf((float)r, &sf, &cf);
+        const int quad = ((int)(long long)kd) & 3;
+        double ca = cf, sa = sf;
+        if (quad == 1) { ca = -sf; sa = cf; }
+        else if (quad == 2) { ca = -cf; sa = -sf; }
+        else if (quad == 3) { ca = sf; sa = -cf; }
+        const double mg = 1e-4 + fabs(J.vib_amp);
+        maybe = tool_box_hits<MODE>(J.tooth_box + tooth * 6, ca, sa, x0p, ty, wx_lo - mg, wx_hi + mg,
+                                    wy_lo - mg, wy_hi + mg, J.tilt_c, J.tilt_s);
       }
-      const double ns = -sn;
-      double xoff = J.pass_x0[pass];
-      if (MODE != MSURF_MODE_REF && J.vib_amp != 0.0) {
-        const double sv = J.vib_table ? J.vib_table[s]
-                                      : msurf_sin(__dadd_rn(__dmul_rn(J.vib_omega, t), J.vib_phase));
-        xoff = __dadd_rn(xoff, __dmul_rn(J.vib_amp, sv));
-      }
-      if (MODE == MSURF_MODE_REF) {
-        // engine.py:257-264 composite coefficients, exact op order
-        const double* e = J.tooth_rows + tooth * 8;
-        rd[0] = __dadd_rn(__dmul_rn(c, e[0]), __dmul_rn(sn, e[4]));
-        rd[1] = __dadd_rn(__dmul_rn(c, e[1]), __dmul_rn(sn, e[5]));
-        rd[2] = __dadd_rn(__dmul_rn(c, e[2]), __dmul_rn(sn, e[6]));
-        rd[3] = __dadd_rn(__dadd_rn(__dmul_rn(c, e[3]), __dmul_rn(sn, e[7])), xoff);
-        rd[4] = __dadd_rn(__dmul_rn(ns, e[0]), __dmul_rn(c, e[4]));
-        rd[5] = __dadd_rn(__dmul_rn(ns, e[1]), __dmul_rn(c, e[5]));
-        rd[6] = __dadd_rn(__dmul_rn(ns, e[2]), __dmul_rn(c, e[6]));
-        rd[7] = __dadd_rn(__dadd_rn(__dmul_rn(ns, e[3]), __dmul_rn(c, e[7])), ty);
-        if (J.traj && pass == 0) {
-          // engine.py:266-270: min-z edge point of this (step, tooth)
-          const double4 pt = pts[J.min_index[tooth]];
-          double* tr = J.traj + (s * J.teeth + tooth) * 3;
-          tr[0] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(rd[0], pt.x), __dmul_rn(rd[1], pt.y)),
-                                      __dmul_rn(rd[2], pt.z)), rd[3]);
-          tr[1] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(rd[4], pt.x), __dmul_rn(rd[5], pt.y)),
-                                      __dmul_rn(rd[6], pt.z)), rd[7]);
-          tr[2] = dec_key((uint64_t)__double_as_longlong(pt.w));
+      if (maybe) {
+        double c, sn;
+        if (J.trig_table) {
+          c = J.trig_table[(s * J.teeth + tooth) * 2 + 0];
+          sn = J.trig_table[(s * J.teeth + tooth) * 2 + 1];
+        } else {
+          msurf_sincos(th, &sn, &c);
         }
-      } else {
-        rd[0] = c;
-        rd[1] = sn;
-        rd[2] = xoff;
-        rd[3] = ty;
-      }
-      // 2-D box test of one tool-frame box at this step (conservative by 1.5
-      // cells >> rounding differences between this bound and the kernel)
-      auto box_hits = [&](const double* b) -> bool {
-        const double xl = b[0], xh = b[1], yl = b[2], yh = b[3];
-        const double x_lo = fmin(c * xl, c * xh) + fmin(sn * yl, sn * yh) + xoff;
-        const double x_hi = fmax(c * xl, c * xh) + fmax(sn * yl, sn * yh) + xoff;
-        double v_lo = fmin(ns * xl, ns * xh) + fmin(c * yl, c * yh);
-        double v_hi = fmax(ns * xl, ns * xh) + fmax(c * yl, c * yh);
-        if (MODE == MSURF_MODE_EXT_TILT) {
-          const double a1 = J.tilt_c * v_lo, a2 = J.tilt_c * v_hi;
-          const double b1 = J.tilt_s * b[4], b2 = J.tilt_s * b[5];
-          v_lo = fmin(a1, a2) - fmax(b1, b2);
-          v_hi = fmax(a1, a2) - fmin(b1, b2);
+        const double ns = -sn;
+        double xoff = x0p;
+        if (MODE != MSURF_MODE_REF && J.vib_amp != 0.0) {
+          const double sv = J.vib_table ? J.vib_table[s]
+                                        : msurf_sin(__dadd_rn(__dmul_rn(J.vib_omega, t), J.vib_phase));
+          xoff = __dadd_rn(xoff, __dmul_rn(J.vib_amp, sv));
         }
-        return (x_hi >= wx_lo) & (x_lo <= wx_hi) & (v_hi + ty >= wy_lo) & (v_lo + ty <= wy_hi);
-      };
-      engaged = box_hits(J.tooth_box + tooth * 6);
-      if (engaged) {
-        // per-chunk bounding circles: x = c*xc + s*yc + xoff +- rx,
-        // y = cos(tau)*(c*yc - s*xc) + yz + ty +- ry, against the window
-        // (centre, half-width) widened by 1.5 cells
-        const double wxc = 0.5 * (wx_lo + wx_hi), wxh = 0.5 * (wx_hi - wx_lo);
-        const double wyc = 0.5 * (wy_lo + wy_hi), wyh = 0.5 * (wy_hi - wy_lo);
-        const double ox = xoff - wxc, oy = ty - wyc;
-        const double tcv = MODE == MSURF_MODE_EXT_TILT ? J.tilt_c : 1.0;
-        const double2* circ = reinterpret_cast<const double2*>(J.chunk_circ) + (long long)tooth * nchunk * 3;
-        unsigned kept = 0;
-        for (int q = 0; q < nchunk; ++q) {
-          const double2 a = circ[q * 3 + 0], b = circ[q * 3 + 1], z = circ[q * 3 + 2];
-          const double uc = c * a.x + sn * a.y;
-          const double vc = c * a.y - sn * a.x;
-          const bool hit = (fabs(uc + ox) <= wxh + b.x) & (fabs(tcv * vc + z.x + oy) <= wyh + b.y);
-          if (hit) {
-            my_mask[q >> 6] |= 1ull << (q & 63);
-            kept += (q == nchunk - 1) ? (unsigned)(npts - 32 * q) : 32u;
+        if (MODE == MSURF_MODE_REF) {
+          // engine.py:257-264 composite coefficients, exact op order
+          const double* e = J.tooth_rows + tooth * 8;
+          rd[0] = __dadd_rn(__dmul_rn(c, e[0]), __dmul_rn(sn, e[4]));
+          rd[1] = __dadd_rn(__dmul_rn(c, e[1]), __dmul_rn(sn, e[5]));
+          rd[2] = __dadd_rn(__dmul_rn(c, e[2]), __dmul_rn(sn, e[6]));
+          rd[3] = __dadd_rn(__dadd_rn(__dmul_rn(c, e[3]), __dmul_rn(sn, e[7])), xoff);
+          rd[4] = __dadd_rn(__dmul_rn(ns, e[0]), __dmul_rn(c, e[4]));
+          rd[5] = __dadd_rn(__dmul_rn(ns, e[1]), __dmul_rn(c, e[5]));
+          rd[6] = __dadd_rn(__dmul_rn(ns, e[2]), __dmul_rn(c, e[6]));
+          rd[7] = __dadd_rn(__dadd_rn(__dmul_rn(ns, e[3]), __dmul_rn(c, e[7])), ty);
+          if (J.traj && pass == 0) {
+            // engine.py:266-270: min-z edge point of this (step, tooth)
+            const double4 pt = pts[J.min_index[tooth]];
+            double* tr = J.traj + (s * J.teeth + tooth) * 3;
+            tr[0] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(rd[0], pt.x), __dmul_rn(rd[1], pt.y)),
+                                        __dmul_rn(rd[2], pt.z)), rd[3]);
+            tr[1] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(rd[4], pt.x), __dmul_rn(rd[5], pt.y)),
+                                        __dmul_rn(rd[6], pt.z)), rd[7]);
+            tr[2] = dec_key((uint64_t)__double_as_longlong(pt.w));
           }
+        } else {
+          rd[0] = c;
+          rd[1] = sn;
+          rd[2] = xoff;
+          rd[3] = ty;
         }
-        any = kept != 0;
-        my_eval = kept;
+        engaged = tool_box_hits<MODE>(J.tooth_box + tooth * 6, c, sn, xoff, ty, wx_lo, wx_hi, wy_lo, wy_hi,
+                                      J.tilt_c, J.tilt_s);
+        if (engaged) {
+          // per-chunk bounding circles: x = c*xc + s*yc + xoff +- rx,
+          // y = cos(tau)*(c*yc - s*xc) + yz + ty +- ry, against the window
+          // (centre, half-width) widened by 1.5 cells
+          const double wxc = 0.5 * (wx_lo + wx_hi), wxh = 0.5 * (wx_hi - wx_lo);
+          const double wyc = 0.5 * (wy_lo + wy_hi), wyh = 0.5 * (wy_hi - wy_lo);
+          const double ox = xoff - wxc, oy = ty - wyc;
+          const double tcv = MODE == MSURF_MODE_EXT_TILT ? J.tilt_c : 1.0;
+          const double2* circ = reinterpret_cast<const double2*>(J.chunk_circ) + (long long)tooth * nchunk * 3;
+          unsigned kept = 0;
+          for (int q = 0; q < nchunk; ++q) {
+            const double2 a = circ[q * 3 + 0], b = circ[q * 3 + 1], z = circ[q * 3 + 2];
+            const double uc = c * a.x + sn * a.y;
+            const double vc = c * a.y - sn * a.x;
+            const bool hit = (fabs(uc + ox) <= wxh + b.x) & (fabs(tcv * vc + z.x + oy) <= wyh + b.y);
+            if (hit) {
+              my_mask[q >> 6] |= 1ull << (q & 63);
+              kept += (q == nchunk - 1) ? (unsigned)(npts - 32 * q) : 32u;
+            }
+          }
+          any = kept != 0;
+          my_eval = kept;
+        }
       }
     }
   }

@@ -30,7 +30,7 @@ from .planner import MODE_REF, SweepPlan, plan, step_window, time_step
 DEFAULT_MAX_STEP_ANGLE_RAD = math.radians(0.5)
 # Z-map bytes one sweep job may cover: keeps its RED.MIN traffic in the
 # 126 MB L2 (surfaces above this are cut into feed-direction sub-strips)
-L2_TILE_BYTES = 48 << 20
+L2_TILE_BYTES = int(float(__import__("os").environ.get("MSURF_L2_TILE_MB", "48")) * (1 << 20))
 
 __all__ = ["SimulationConfig", "SimulationResult", "time_step", "simulate", "simulate_batch",
            "simulate_reference", "run_benchmark", "BenchmarkReport", "BenchmarkRow", "sweep_plans"]

@@ -434,9 +434,11 @@ def config3_workload(rank, world):
     all_cfgs = [apply_sample(base, ext, names, samples[i], meta["steps_per_rev"]) for i in range(meta["count"])]
     sl = sharded.batch_slice(meta["count"], rank, world)
     mine = all_cfgs[sl]
-    plans = [make_plan(c, e) for c, e in mine]
-    total_points = sum(make_plan(c, e).trajectory_points for c, e in all_cfgs) if world > 1 else \
-        sum(p.trajectory_points for p in plans)
+    from paper_2603_28160_b200.planner import plan_many
+
+    plans = plan_many([c for c, _ in mine], [e for _, e in mine])
+    total_points = sum(p.trajectory_points for p in plan_many([c for c, _ in all_cfgs], [e for _, e in all_cfgs])) \
+        if world > 1 else sum(p.trajectory_points for p in plans)
     return base, ext, meta, ranges, mine, plans, total_points
 
 

@@ -25,7 +25,7 @@ from . import _native
 from .errors import ConfigError, MillsurfError
 from .extensions import Extensions
 from .grid import GridSpec, HeightField, TrajectoryRecord
-from .planner import MODE_REF, SweepPlan, plan, step_window, time_step
+from .planner import MODE_REF, SweepPlan, plan, plan_many, step_window, time_step
 
 DEFAULT_MAX_STEP_ANGLE_RAD = math.radians(0.5)
 # Z-map bytes one sweep job may cover: keeps its RED.MIN traffic in the
@@ -402,10 +402,9 @@ def simulate_batch(configs, extensions=None, *, trig: str = "device"):
             raise ConfigError("extensions list must align with configs")
     else:
         exts = [extensions] * len(configs)
-    plans = [plan(c, e) for c, e in zip(configs, exts)]
-    if not plans:
+    if not configs:
         return []
-    return _launch_results(plans, trig)
+    return _launch_results(plan_many(configs, exts), trig)
 
 
 def simulate_reference(config: SimulationConfig, extensions: Extensions | None = None) -> SimulationResult:

@@ -203,22 +203,13 @@ def plan(config, ext: Extensions | None = None) -> SweepPlan:
     if p.record and p.mode != MODE_REF:
         raise ConfigError("record_trajectory is defined for the reference kinematics only")
     _pack(p)
-    if p.points > MAX_POINTS:
-        raise ConfigError(f"edge_point_count {p.points} exceeds the device limit {MAX_POINTS}")
-    # bounds of the device's fast exact cell location (msurf.cu cell_fast):
-    # node indices < 2^19 and grid origin within 2^20 cells of the frame origin
-    if max(grid.m, grid.n) >= (1 << 19) - 2:
-        raise ConfigError("grid axes must have fewer than 2^19 - 2 cells")
-    if max(abs(grid.x_min_mm), abs(grid.y_min_mm)) / grid.spacing_mm >= float(1 << 20):
-        raise ConfigError("grid origin too far from the workpiece frame origin (> 2^20 cells)")
-    if (grid.m + 1) * (grid.n + 1) >= 1 << 31:
-        raise ConfigError("grid has too many nodes for one device surface (>= 2^31)")
+    _check_device_limits(p, grid)
     return p
 
 
-def _pack(p: SweepPlan) -> None:
+def _pack_records(p: SweepPlan) -> None:
     """Per-(tooth, point) 32-byte records the device reads with one broadcast
-    load per point (include/msurf.h msurf_job.pts), plus whole-tooth boxes."""
+    load per point (include/msurf.h msurf_job.pts)."""
     z_n, n = p.teeth, p.points
     rec = np.zeros((z_n, n, 4))
     kf = p.zkey.view(np.float64)
@@ -236,6 +227,11 @@ def _pack(p: SweepPlan) -> None:
         rec[:, :, 2] = p.tilt_s * p.pz
         rec[:, :, 3] = p.tilt_c * p.pz
     p.pts = rec
+
+
+def _pack(p: SweepPlan) -> None:
+    """Device records, bounding circles and whole-tooth boxes."""
+    _pack_records(p)
     if p.mode == MODE_REF:
         xt = (p.tooth_rows[:, 0:1] * p.px[None, :] + p.tooth_rows[:, 1:2] * p.py[None, :]) \
             + p.tooth_rows[:, 2:3] * p.pz[None, :] + p.tooth_rows[:, 3:4]
@@ -247,6 +243,19 @@ def _pack(p: SweepPlan) -> None:
     b = p.chunk_box
     p.tooth_box = np.stack([b[:, :, 0].min(1), b[:, :, 1].max(1), b[:, :, 2].min(1), b[:, :, 3].max(1),
                             b[:, :, 4].min(1), b[:, :, 5].max(1)], axis=1)
+
+
+def _check_device_limits(p: SweepPlan, grid) -> None:
+    if p.points > MAX_POINTS:
+        raise ConfigError(f"edge_point_count {p.points} exceeds the device limit {MAX_POINTS}")
+    # bounds of the device's fast exact cell location (msurf.cu cell_fast):
+    # node indices < 2^19 and grid origin within 2^20 cells of the frame origin
+    if max(grid.m, grid.n) >= (1 << 19) - 2:
+        raise ConfigError("grid axes must have fewer than 2^19 - 2 cells")
+    if max(abs(grid.x_min_mm), abs(grid.y_min_mm)) / grid.spacing_mm >= float(1 << 20):
+        raise ConfigError("grid origin too far from the workpiece frame origin (> 2^20 cells)")
+    if (grid.m + 1) * (grid.n + 1) >= 1 << 31:
+        raise ConfigError("grid has too many nodes for one device surface (>= 2^31)")
 
 
 def reach_y(p: SweepPlan) -> float:
@@ -394,4 +403,179 @@ def _plan_ext(config, ext: Extensions) -> SweepPlan:
         min_index=np.argmin(zw, axis=1).astype(np.int32),
         tilt_c=tc, tilt_s=ts, zoff=zoff, vib_amp=amp,
         vib_omega=2.0 * math.pi * ext.vib_frequency_hz, vib_phase=ext.vib_phase_rad,
+        extras={"base_margin": base_margin},
     )
+
+
+# ------------------------------------------------------------------ batches
+def _ext_group_key(config, ext: Extensions):
+    """Everything the extended model's per-point geometry depends on, except
+    the per-sample helix angle and tool-axis runout (vectorised below)."""
+    tool, proc, grid = config.tool, config.process, config.grid
+    half = None
+    if ext.profile == "insert":
+        half = effective_half_length(tool.insert_radius_mm, proc.depth_of_cut_mm, proc.feed_per_tooth_mm,
+                                     tool.radial_rake_rad)
+    return (ext.profile, tool.cutting_diameter_mm, tool.insert_radius_mm, tool.tooth_count,
+            tool.radial_rake_rad, tool.axial_rake_rad, tool.runouts_mm, proc.depth_of_cut_mm, half,
+            config.edge_point_count, grid.spacing_mm, ext.tilt_rad, ext.noise_sigma_mm, ext.noise_corr_mm,
+            ext.noise_seed, ext.helix_ref_radius_mm, bool(ext.helix_angle_rad != 0.0),
+            bool(ext.runout_offset_mm != 0.0))
+
+
+def plan_many(configs, exts):
+    """plan() for many parameter sets. Extended-model sets that share their
+    edge geometry are planned together with (sets, teeth, points) arrays —
+    the same element-wise operations as plan(), so every array is bitwise
+    identical to the per-set plan (tests/test_host_cpu.py) — which keeps host
+    planning of a 256-set batch in the low milliseconds."""
+    exts = [e or Extensions() for e in exts]
+    out = [None] * len(configs)
+    groups = {}
+    for i, (c, e) in enumerate(zip(configs, exts)):
+        if e.kinematic and getattr(c, "edge_point_count", None) and not getattr(c, "record_trajectory", False):
+            try:
+                groups.setdefault(_ext_group_key(c, e), []).append(i)
+                continue
+            except (ConfigError, DomainError):
+                pass
+        out[i] = plan(c, e)
+    for idx in groups.values():
+        if len(idx) < 4:
+            for i in idx:
+                out[i] = plan(configs[i], exts[i])
+            continue
+        for i, p in zip(idx, _plan_ext_group([configs[i] for i in idx], [exts[i] for i in idx])):
+            out[i] = p
+    return out
+
+
+def _plan_ext_group(configs, exts):
+    c0, e0 = configs[0], exts[0]
+    # sample-independent part: one per-set plan() restated without helix/runout
+    base = _plan_ext(c0, replace_ext(e0, helix_angle_rad=0.0, runout_offset_mm=0.0))
+    tool = c0.tool
+    z_n, n = base.teeth, base.points
+    r = tool.insert_radius_mm
+    B = len(configs)
+    # rebuild the per-tooth tool-frame points before helix/runout (same ops as _plan_ext)
+    if e0.profile == "insert":
+        half = base.half_length
+        ex, ey, ez = edge_coordinates(half, n, r)
+        nx = ex / r
+        nz = -(r - ez) / r
+        arc = 2.0 * r * math.asin(min(1.0, half / r))
+    else:
+        kmax = min(math.pi / 2.0, math.acos((r - c0.process.depth_of_cut_mm) / r) + abs(e0.tilt_rad))
+        kap = kmax * np.arange(n, dtype=np.float64) / (n - 1)
+        kap[-1] = kmax
+        nx = np.sin(kap)
+        nz = -np.cos(kap)
+        ex = r * nx
+        ey = np.zeros(n)
+        ez = r - r * np.cos(kap)
+        arc = r * kmax
+    sigma = e0.noise_sigma_mm
+    if sigma != 0.0:
+        delta = edge_noise(z_n, n, sigma, e0.noise_corr_mm, arc / (n - 1), int(e0.noise_seed))
+    radial = None if e0.profile == "insert" else 0.0
+    qx0 = np.empty((z_n, n))
+    qy0 = np.empty((z_n, n))
+    qz0 = np.empty((z_n, n))
+    pzs = np.empty((z_n, n))
+    for k in range(1, z_n + 1):
+        if sigma != 0.0:
+            px = ex + delta[k - 1] * nx
+            pz = ez + delta[k - 1] * nz
+        else:
+            px, pz = ex, ez
+        e = edge_to_tool_rows(tool, k, radial_offset_mm=radial)
+        qx0[k - 1] = ((e[0][0] * px + e[0][1] * ey) + e[0][2] * pz) + e[0][3]
+        qy0[k - 1] = ((e[1][0] * px + e[1][1] * ey) + e[1][2] * pz) + e[1][3]
+        qz0[k - 1] = ((e[2][0] * px + e[2][1] * ey) + e[2][2] * pz) + e[2][3]
+        pzs[k - 1] = pz
+    qx = np.broadcast_to(qx0, (B, z_n, n))
+    qy = np.broadcast_to(qy0, (B, z_n, n))
+    if e0.helix_angle_rad != 0.0:
+        r_ref = e0.helix_ref_radius_mm
+        if r_ref is None:
+            r_ref = tool.cutting_diameter_mm / 2.0 if e0.profile == "insert" else r
+        tbr = np.array([math.tan(e.helix_angle_rad) / r_ref for e in exts])
+        psi = pzs[None, :, :] * tbr[:, None, None]
+        cps, sps = np.cos(psi), np.sin(psi)
+        qx, qy = cps * qx + sps * qy, (-sps) * qx + cps * qy
+    if e0.runout_offset_mm != 0.0:
+        offx = np.empty((B, z_n))
+        offy = np.empty((B, z_n))
+        for b, e in enumerate(exts):
+            for k in range(1, z_n + 1):
+                ang = e.runout_phase_rad + (2.0 * math.pi) * (k - 1) / z_n
+                offx[b, k - 1] = e.runout_offset_mm * math.cos(ang)
+                offy[b, k - 1] = e.runout_offset_mm * math.sin(ang)
+        qx = qx + offx[:, :, None]
+        qy = qy + offy[:, :, None]
+    xt = np.ascontiguousarray(qx)
+    yt = np.ascontiguousarray(qy)
+    zt = qz0
+    tau = e0.tilt_rad
+    tilt = tau != 0.0
+    tc, ts = math.cos(tau), math.sin(tau)
+    zmax = float(np.max(np.abs(zt)))
+    if tilt:
+        zsh = -np.min((tc * zt[None] - abs(ts) * np.sqrt(xt * xt + yt * yt)).reshape(B, -1), axis=1)
+    plans = []
+    boxes = _chunk_boxes(xt.reshape(B * z_n, n), yt.reshape(B * z_n, n),
+                         np.broadcast_to(zt, (B, z_n, n)).reshape(B * z_n, n)).reshape(B, z_n, -1, 6)
+    circs = _chunk_circles(xt.reshape(B * z_n, n), yt.reshape(B * z_n, n),
+                           np.broadcast_to(zt, (B, z_n, n)).reshape(B * z_n, n), tc, ts).reshape(B, z_n, -1, 6)
+    base_margin = base.extras.get("base_margin")
+    tooth_box = np.stack([boxes[..., 0].min(2), boxes[..., 1].max(2), boxes[..., 2].min(2),
+                          boxes[..., 3].max(2), boxes[..., 4].min(2), boxes[..., 5].max(2)], axis=2)
+    spans = []
+    zoffs = np.empty(B)
+    for b, (cfg, e) in enumerate(zip(configs, exts)):
+        z_shift = float(zsh[b]) if tilt else 0.0
+        margin = base_margin + (abs(e.runout_offset_mm) + abs(e.vib_amplitude_mm) + 5.0 * abs(sigma)
+                                + abs(ts) * zmax)
+        sp = _span(cfg, margin)
+        spans.append(sp)
+        zoffs[b] = (sp[5] + z_shift) + 0.0
+    zw_all = zt[None, :, :] + zoffs[:, None, None]
+    keys_all = encode_keys(zw_all)
+    minidx = np.argmin(zw_all, axis=2).astype(np.int32)
+    rec = np.zeros((B, z_n, n, 4))
+    rec[..., 0], rec[..., 1] = xt, yt
+    if tilt:
+        rec[..., 2] = ts * zt[None]
+        rec[..., 3] = tc * zt[None]
+    else:
+        rec[..., 2] = keys_all.view(np.float64)
+    mode = MODE_EXT_TILT if tilt else MODE_EXT
+    plans = []
+    for b, (cfg, e) in enumerate(zip(configs, exts)):
+        proc, grid = cfg.process, cfg.grid
+        dt, t_start, steps, x0, y0, z0 = spans[b]
+        p = SweepPlan(
+            mode=mode, grid=grid, teeth=z_n, points=n, steps=steps,
+            dt=dt, t_start=t_start, x0=x0, y0=y0, z0=z0, feed_speed=proc.feed_speed_mm_s,
+            omega=proc.angular_velocity_rad_s, initial_height=z0 + proc.depth_of_cut_mm,
+            half_length=base.half_length,
+            tooth_base=np.array([tooth_base_angle(proc.phase_rad, k, z_n) for k in range(1, z_n + 1)]),
+            tooth_rows=np.zeros((z_n, 8)), px=xt[b], py=yt[b], pz=zt, zw=zw_all[b], zkey=keys_all[b],
+            chunk_box=boxes[b], pass_x0=np.array([x0 + k * e.stepover_mm for k in range(int(e.passes))],
+                                                 dtype=np.float64),
+            min_index=minidx[b], tilt_c=tc, tilt_s=ts, zoff=float(zoffs[b]), vib_amp=e.vib_amplitude_mm,
+            vib_omega=2.0 * math.pi * e.vib_frequency_hz, vib_phase=e.vib_phase_rad)
+        p.chunk_circ = circs[b]
+        p.pts = rec[b]
+        p.tooth_box = tooth_box[b]
+        p.record = False
+        _check_device_limits(p, grid)
+        plans.append(p)
+    return plans
+
+
+def replace_ext(ext: Extensions, **kw) -> Extensions:
+    from dataclasses import replace as _r
+
+    return _r(ext, **kw)

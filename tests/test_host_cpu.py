@@ -210,3 +210,30 @@ def test_device_required_no_cpu_fallback(monkeypatch):
     g = golden_io.load("tiny")
     with pytest.raises(ms.NativeUnavailableError):
         ms.simulate(golden_io.product_config(g["config"]))
+
+
+def test_plan_many_bitwise_equals_per_set_plan():
+    """The vectorised batch planner (simulate_batch) reproduces plan() per set."""
+    from paper_2603_28160_b200 import configs
+    from paper_2603_28160_b200.dataset import ParameterRange, apply_sample, uniform_sample
+
+    base, ext, meta = configs.config3_base()
+    ranges = [ParameterRange(n, lo, hi) for n, lo, hi in meta["ranges"]]
+    samples = uniform_sample(ranges, 24, 3)
+    names = [r.name for r in ranges]
+    pairs = [apply_sample(base, ext, names, samples[i], 3600) for i in range(24)]
+    # plus a tilt/noise group and a reference-kinematics set
+    cfg_b = _ext_cfg("ball")
+    for k in range(5):
+        pairs.append((cfg_b, ms.Extensions(profile="ball", tilt_rad=0.2, helix_angle_rad=0.3 + 0.05 * k,
+                                           runout_offset_mm=0.001 * k, noise_sigma_mm=0.001, noise_corr_mm=0.02)))
+    pairs.append((golden_io.product_config(golden_io.load("small_3")["config"]), None))
+    many = planner.plan_many([c for c, _ in pairs], [e for _, e in pairs])
+    for (c, e), a in zip(pairs, many):
+        b = planner.plan(c, e)
+        for f in ("px", "py", "pz", "zw", "zkey", "chunk_box", "chunk_circ", "pts", "tooth_box", "pass_x0",
+                  "tooth_base", "min_index"):
+            assert np.array_equal(getattr(a, f), getattr(b, f)), f
+        for f in ("steps", "dt", "t_start", "y0", "x0", "zoff", "initial_height", "mode", "tilt_c", "tilt_s",
+                  "vib_amp", "vib_omega", "vib_phase", "feed_speed", "omega", "points", "teeth"):
+            assert getattr(a, f) == getattr(b, f), f

@@ -110,7 +110,8 @@ int msurf_decode(uint64_t* keys, int64_t count, int32_t n_surf, const double* se
  * sentinel[n_surf] device. exclude_uncut=0 counts uncut cells (the host raises
  * DomainError like roughness.py:86-89); =1 skips them. Reductions are
  * deterministic (fixed block partition, fixed-order tree): reruns are
- * bit-identical. work: device scratch of n_surf * MSURF_RED_BLOCKS * 5 doubles.
+ * bit-identical. work: device scratch of n_surf * MSURF_RED_BLOCKS * 5 doubles
+ * (the plane-leveling passes below need * 10).
  * pass1 -> stats1[s][5] = sum z_um, max z_um, min z_um, n_used, n_uncut
  * pass2 reads mean = stats1[s][0] / stats1[s][3] (under strip sharding the
  * caller all-reduces stats1 first, so the mean is global)
@@ -124,6 +125,21 @@ int msurf_areal_pass2(const double* h, int64_t ld, int64_t surf_stride, int32_t 
                       int64_t i_lo, int64_t j_lo, int64_t rows, int64_t cols,
                       const double* sentinel, int32_t exclude_uncut, const double* stats1,
                       double* work, double* out2, void* stream);
+
+/* Plane leveling (roughness.py:108-113, leveling='plane'): pass 1 writes the
+ * normal-equation sums per surface, out[s][10] = n, Si, Sj, Sii, Sjj, Sij, Sz,
+ * Siz, Sjz, n_uncut (i, j = offsets inside the ROI, z in um); the host solves
+ * the 3x3 system for z ~ a*i + b*j + c; pass 2 with coef[s][3] = (a, b, c)
+ * writes out[s][6] = S|d|, Sd^2, Sd^3, Sd^4, max d, min d of d = z - plane.
+ * work: n_surf * MSURF_RED_BLOCKS * 10 doubles. */
+int msurf_areal_plane_pass1(const double* h, int64_t ld, int64_t surf_stride, int32_t n_surf,
+                            int64_t i_lo, int64_t j_lo, int64_t rows, int64_t cols,
+                            const double* sentinel, int32_t exclude_uncut, double* work, double* out,
+                            void* stream);
+int msurf_areal_plane_pass2(const double* h, int64_t ld, int64_t surf_stride, int32_t n_surf,
+                            int64_t i_lo, int64_t j_lo, int64_t rows, int64_t cols,
+                            const double* sentinel, int32_t exclude_uncut, const double* coef,
+                            double* work, double* out, void* stream);
 
 /* Profile roughness (roughness.py:138-188; Rz = Rp + Rv is the product's
  * extension). Profile p of surface s: `len` samples starting at

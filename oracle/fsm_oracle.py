@@ -302,7 +302,7 @@ def locate(x, y, spacing, x_min, y_min, m, n):
 MM_TO_UM = 1000.0
 
 
-def areal_metrics(heights2d, initial_height, roi=None, uncut="raise"):
+def areal_metrics(heights2d, initial_height, roi=None, uncut="raise", leveling="mean"):
     """roughness.py:76-135 with leveling='mean'. ``uncut='exclude'`` is the
     product's documented extension (statistics over machined cells only).
     Returns dict with Sa Sq Sp Sv Sz Ssk Sku cell_count (µm)."""
@@ -322,7 +322,18 @@ def areal_metrics(heights2d, initial_height, roi=None, uncut="raise"):
         z = block[cut] * MM_TO_UM
         if z.size == 0:
             raise OracleDomainError("no machined cells in roi")
-    d = z - z.mean()
+    if leveling == "plane":
+        # roughness.py:108-113: least-squares plane over node offsets (i, j)
+        if uncut != "raise":
+            xi, yj = np.nonzero(cut)
+        else:
+            xi, yj = np.meshgrid(np.arange(block.shape[0]), np.arange(block.shape[1]), indexing="ij")
+            xi, yj = xi.ravel(), yj.ravel()
+        a = np.column_stack([xi, yj, np.ones(z.size)])
+        coef, *_ = np.linalg.lstsq(a, z.ravel(), rcond=None)
+        d = z.ravel() - a @ coef
+    else:
+        d = z - z.mean()
     sa = float(np.mean(np.abs(d)))
     sq = float(np.sqrt(np.mean(d * d)))
     sp = float(np.max(d))

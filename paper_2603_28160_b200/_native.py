@@ -59,6 +59,12 @@ EXPORTS = {
     "msurf_areal_pass2": (ctypes.c_int, [c_void_p, c_int64, c_int64, c_int32, c_int64, c_int64,
                                          c_int64, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
                                          c_void_p, c_void_p]),
+    "msurf_areal_plane_pass1": (ctypes.c_int, [c_void_p, c_int64, c_int64, c_int32, c_int64, c_int64,
+                                               c_int64, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
+                                               c_void_p]),
+    "msurf_areal_plane_pass2": (ctypes.c_int, [c_void_p, c_int64, c_int64, c_int32, c_int64, c_int64,
+                                               c_int64, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
+                                               c_void_p, c_void_p]),
     "msurf_profiles": (ctypes.c_int, [c_void_p, c_int64, c_int32, c_void_p, c_int32, c_int64,
                                       c_int64, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     "msurf_microbench": (ctypes.c_int, [c_int32, ctypes.POINTER(c_double)]),

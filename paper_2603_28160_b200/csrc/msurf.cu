@@ -633,16 +633,17 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// one block per surface: reduce nb partials in fixed order
+// one block per surface: reduce nb partials in fixed order; kinds holds 2 bits
+// per value (0 sum, 1 max, 2 min)
 template <int NV>
 __global__ void __launch_bounds__(kThreads)
-    finalize_kernel(const double* __restrict__ work, int nb, int k0max, double* __restrict__ out) {
+    finalize_kernel(const double* __restrict__ work, int nb, unsigned kinds, double* __restrict__ out) {
   __shared__ double sh[kWarps * NV];
   double v[NV];
   int kind[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    kind[k] = (NV == 5 && k == 1) ? 1 : ((NV == 5 && k == 2) ? 2 : 0);
+    kind[k] = (int)((kinds >> (2 * k)) & 3u);
     v[k] = kind[k] == 0 ? 0.0 : (kind[k] == 1 ? -INFINITY : INFINITY);
   }
   const double* w = work + (long long)blockIdx.x * nb * NV;
@@ -656,7 +657,73 @@ __global__ void __launch_bounds__(kThreads)
   block_reduce<NV>(v, kind, sh);
   if (threadIdx.x == 0)
     for (int k = 0; k < NV; ++k) out[(long long)blockIdx.x * NV + k] = v[k];
-  (void)k0max;
+}
+
+// least-squares plane leveling (roughness.py:108-113, leveling='plane'):
+// pass 1 = the normal-equation sums over the used cells, with i, j the row and
+// column offsets inside the ROI and z in um:
+// [n, Si, Sj, Sii, Sjj, Sij, Sz, Siz, Sjz, n_uncut]
+__global__ void __launch_bounds__(kThreads)
+    plane_pass1_kernel(const double* __restrict__ h, long long ld, long long sstride, long long i_lo,
+                       long long j_lo, long long rows, long long cols, const double* __restrict__ sent,
+                       int exclude, double* __restrict__ work) {
+  __shared__ double sh[kWarps * 10];
+  const double* hs = h + (long long)blockIdx.y * sstride;
+  const double sentinel = sent[blockIdx.y];
+  double v[10] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const int kind[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const long long r0 = rows * blockIdx.x / gridDim.x, r1 = rows * (blockIdx.x + 1) / gridDim.x;
+  for (long long r = r0; r < r1; ++r) {
+    const double* row = hs + (i_lo + r) * ld + j_lo;
+    const double fi = (double)r;
+    for (long long c = threadIdx.x; c < cols; c += blockDim.x) {
+      const double hv = row[c];
+      const bool cut = hv < sentinel;
+      if (!cut) v[9] += 1.0;
+      if (cut || !exclude) {
+        const double z = hv * 1000.0, fj = (double)c;
+        v[0] += 1.0; v[1] += fi; v[2] += fj; v[3] += fi * fi; v[4] += fj * fj; v[5] += fi * fj;
+        v[6] += z; v[7] += fi * z; v[8] += fj * z;
+      }
+    }
+  }
+  block_reduce<10>(v, kind, sh);
+  if (threadIdx.x == 0) {
+    double* o = work + ((long long)blockIdx.y * gridDim.x + blockIdx.x) * 10;
+    for (int k = 0; k < 10; ++k) o[k] = v[k];
+  }
+}
+
+// pass 2: d = z - ((a*i + b*j) + c) -> [S|d|, Sd^2, Sd^3, Sd^4, max d, min d]
+__global__ void __launch_bounds__(kThreads)
+    plane_pass2_kernel(const double* __restrict__ h, long long ld, long long sstride, long long i_lo,
+                       long long j_lo, long long rows, long long cols, const double* __restrict__ sent,
+                       int exclude, const double* __restrict__ coef, double* __restrict__ work) {
+  __shared__ double sh[kWarps * 6];
+  const double* hs = h + (long long)blockIdx.y * sstride;
+  const double sentinel = sent[blockIdx.y];
+  const double a = coef[blockIdx.y * 3 + 0], b = coef[blockIdx.y * 3 + 1], c0 = coef[blockIdx.y * 3 + 2];
+  double v[6] = {0.0, 0.0, 0.0, 0.0, -INFINITY, INFINITY};
+  const int kind[6] = {0, 0, 0, 0, 1, 2};
+  const long long r0 = rows * blockIdx.x / gridDim.x, r1 = rows * (blockIdx.x + 1) / gridDim.x;
+  for (long long r = r0; r < r1; ++r) {
+    const double* row = hs + (i_lo + r) * ld + j_lo;
+    const double ai = a * (double)r;
+    for (long long c = threadIdx.x; c < cols; c += blockDim.x) {
+      const double hv = row[c];
+      if (hv < sentinel || !exclude) {
+        const double d = hv * 1000.0 - ((ai + b * (double)c) + c0);
+        const double d2 = d * d;
+        v[0] += fabs(d); v[1] += d2; v[2] += d2 * d; v[3] += d2 * d2;
+        v[4] = fmax(v[4], d); v[5] = fmin(v[5], d);
+      }
+    }
+  }
+  block_reduce<6>(v, kind, sh);
+  if (threadIdx.x == 0) {
+    double* o = work + ((long long)blockIdx.y * gridDim.x + blockIdx.x) * 6;
+    for (int k = 0; k < 6; ++k) o[k] = v[k];
+  }
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -830,7 +897,7 @@ int msurf_areal_pass1(const double* h, int64_t ld, int64_t surf_stride, int32_t 
   areal_pass1_kernel<<<dim3(nb, n_surf), kThreads, 0, st>>>(h, ld, surf_stride, i_lo, j_lo, rows, cols,
                                                            sentinel, exclude_uncut, work);
   if (check_launch("areal_pass1_kernel")) return 1;
-  finalize_kernel<5><<<n_surf, kThreads, 0, st>>>(work, nb, 0, out1);
+  finalize_kernel<5><<<n_surf, kThreads, 0, st>>>(work, nb, (1u << 2) | (2u << 4), out1);
   return check_launch("finalize_kernel<5>");
 }
 
@@ -845,8 +912,40 @@ int msurf_areal_pass2(const double* h, int64_t ld, int64_t surf_stride, int32_t 
   areal_pass2_kernel<<<dim3(nb, n_surf), kThreads, 0, st>>>(h, ld, surf_stride, i_lo, j_lo, rows, cols,
                                                            sentinel, exclude_uncut, stats1, work);
   if (check_launch("areal_pass2_kernel")) return 1;
-  finalize_kernel<4><<<n_surf, kThreads, 0, st>>>(work, nb, 0, out2);
+  finalize_kernel<4><<<n_surf, kThreads, 0, st>>>(work, nb, 0u, out2);
   return check_launch("finalize_kernel<4>");
+}
+
+int msurf_areal_plane_pass1(const double* h, int64_t ld, int64_t surf_stride, int32_t n_surf,
+                            int64_t i_lo, int64_t j_lo, int64_t rows, int64_t cols,
+                            const double* sentinel, int32_t exclude_uncut, double* work, double* out,
+                            void* stream) {
+  if (!h || !work || !out || !sentinel || n_surf < 1 || rows < 1 || cols < 1 || i_lo < 0 || j_lo < 0 ||
+      ld < cols)
+    return set_err("msurf_areal_plane_pass1: bad arguments");
+  const int nb = red_blocks(rows, cols);
+  cudaStream_t st = (cudaStream_t)stream;
+  plane_pass1_kernel<<<dim3(nb, n_surf), kThreads, 0, st>>>(h, ld, surf_stride, i_lo, j_lo, rows, cols,
+                                                           sentinel, exclude_uncut, work);
+  if (check_launch("plane_pass1_kernel")) return 1;
+  finalize_kernel<10><<<n_surf, kThreads, 0, st>>>(work, nb, 0u, out);
+  return check_launch("finalize_kernel<10>");
+}
+
+int msurf_areal_plane_pass2(const double* h, int64_t ld, int64_t surf_stride, int32_t n_surf,
+                            int64_t i_lo, int64_t j_lo, int64_t rows, int64_t cols,
+                            const double* sentinel, int32_t exclude_uncut, const double* coef,
+                            double* work, double* out, void* stream) {
+  if (!h || !work || !out || !sentinel || !coef || n_surf < 1 || rows < 1 || cols < 1 || i_lo < 0 ||
+      j_lo < 0 || ld < cols)
+    return set_err("msurf_areal_plane_pass2: bad arguments");
+  const int nb = red_blocks(rows, cols);
+  cudaStream_t st = (cudaStream_t)stream;
+  plane_pass2_kernel<<<dim3(nb, n_surf), kThreads, 0, st>>>(h, ld, surf_stride, i_lo, j_lo, rows, cols,
+                                                           sentinel, exclude_uncut, coef, work);
+  if (check_launch("plane_pass2_kernel")) return 1;
+  finalize_kernel<6><<<n_surf, kThreads, 0, st>>>(work, nb, (1u << 8) | (2u << 10), out);
+  return check_launch("finalize_kernel<6>");
 }
 
 int msurf_profiles(const double* h, int64_t surf_stride, int32_t n_surf, const int64_t* start,

@@ -110,7 +110,7 @@ class _Scratch:
     @classmethod
     def get(cls, torch, device, n_surf: int):
         key = (device.index if device.index is not None else torch.cuda.current_device())
-        need = n_surf * _native.RED_BLOCKS * 5 + n_surf * 16
+        need = n_surf * _native.RED_BLOCKS * 10 + n_surf * 16
         t = cls._cache.get(key)
         if t is None or t.numel() < need:
             t = torch.empty(need, dtype=torch.float64, device=device)
@@ -130,7 +130,7 @@ def areal_moments_device(h_dev, ld, n_surf, surf_stride, roi_box, sentinels_dev,
     dev = h_dev.device
     sc = _Scratch.get(torch, dev, n_surf)
     work = sc.data_ptr()
-    out1 = sc[n_surf * _native.RED_BLOCKS * 5:]
+    out1 = sc[n_surf * _native.RED_BLOCKS * 10:]
     st1 = out1[: n_surf * 5]
     st2 = out1[n_surf * 5: n_surf * 9]
     sp = _native.stream_ptr()
@@ -162,11 +162,13 @@ def _field_sentinel(torch, field, device):
 
 
 def areal_metrics(field: HeightField, roi=None, leveling: str = "mean", uncut: str = "raise") -> ArealMetrics:
-    """Areal parameters over the inclusive node range (i_lo, j_lo, i_hi, j_hi)."""
-    if leveling != "mean":
-        if leveling == "plane":
-            raise DomainError("leveling='plane' is not implemented on the device path yet")
+    """Areal parameters over the inclusive node range (i_lo, j_lo, i_hi, j_hi).
+    ``leveling='plane'`` removes the least-squares plane z ~ a*i + b*j + c
+    (roughness.py:108-113) before the statistics."""
+    if leveling not in ("mean", "plane"):
         raise DomainError(f"unknown leveling mode {leveling!r}")
+    if leveling == "plane":
+        return _areal_plane(field, roi, uncut)
     if uncut not in ("raise", "exclude"):
         raise DomainError(f"uncut must be 'raise' or 'exclude', got {uncut!r}")
     i_lo, j_lo, i_hi, j_hi = _check_roi(field.spec, roi)
@@ -177,6 +179,50 @@ def areal_metrics(field: HeightField, roi=None, leveling: str = "mean", uncut: s
                                     (i_lo, j_lo, i_hi - i_lo + 1, j_hi - j_lo + 1), sent,
                                     uncut == "exclude")
     return _finish_areal(st1[0], st2[0], uncut)
+
+
+def _areal_plane(field: HeightField, roi, uncut: str) -> ArealMetrics:
+    """Plane leveling on the device: normal-equation sums (pass 1), a 3x3
+    solve on the host, deviation moments from the plane (pass 2)."""
+    if uncut not in ("raise", "exclude"):
+        raise DomainError(f"uncut must be 'raise' or 'exclude', got {uncut!r}")
+    i_lo, j_lo, i_hi, j_hi = _check_roi(field.spec, roi)
+    torch = _native.require_cuda()
+    lib = _native.lib()
+    h = field.device_heights()
+    sent = _field_sentinel(torch, field, h.device)
+    sc = _Scratch.get(torch, h.device, 1)
+    work = sc.data_ptr()
+    out = sc[_native.RED_BLOCKS * 10:]
+    rows, cols = i_hi - i_lo + 1, j_hi - j_lo + 1
+    ld = field.spec.n + 1
+    ex = int(uncut == "exclude")
+    sp = _native.stream_ptr()
+    _native.check(lib.msurf_areal_plane_pass1(h.data_ptr(), ld, 0, 1, i_lo, j_lo, rows, cols, sent.data_ptr(),
+                                              ex, work, out.data_ptr(), sp))
+    s1 = out[:10].cpu().numpy()
+    if uncut == "raise" and s1[9] > 0:
+        raise DomainError("roughness over unmachined stock is undefined: roi contains uncut cells")
+    n = s1[0]
+    if n <= 0:
+        raise DomainError("no machined cells in roi")
+    ata = np.array([[s1[3], s1[5], s1[1]], [s1[5], s1[4], s1[2]], [s1[1], s1[2], n]])
+    atz = np.array([s1[7], s1[8], s1[6]])
+    coef = np.linalg.lstsq(ata, atz, rcond=None)[0]
+    cdev = torch.tensor(coef, dtype=torch.float64, device=h.device)
+    _native.check(lib.msurf_areal_plane_pass2(h.data_ptr(), ld, 0, 1, i_lo, j_lo, rows, cols, sent.data_ptr(),
+                                              ex, cdev.data_ptr(), work, out.data_ptr(), sp))
+    s2 = out[:6].cpu().numpy()
+    sa = float(s2[0] / n)
+    sq = float(np.sqrt(s2[1] / n))
+    spk, svl = float(s2[4]), float(-s2[5])
+    if sq == 0.0:
+        ssk = sku = None
+    else:
+        ssk = float((s2[2] / n) / sq ** 3)
+        sku = float((s2[3] / n) / sq ** 4)
+    return ArealMetrics(sa_um=sa, sq_um=sq, sp_um=spk, sv_um=svl, sz_um=spk + svl, ssk=ssk, sku=sku,
+                        cell_count=int(n))
 
 
 def _finish_areal(st1, st2, uncut) -> ArealMetrics:

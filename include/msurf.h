@@ -112,9 +112,10 @@ int msurf_decode(uint64_t* keys, int64_t count, int32_t n_surf, const double* se
  * deterministic (fixed block partition, fixed-order tree): reruns are
  * bit-identical. work: device scratch of n_surf * MSURF_RED_BLOCKS * 5 doubles
  * (the plane-leveling passes below need * 10).
- * pass1 -> stats1[s][5] = sum z_um, max z_um, min z_um, n_used, n_uncut
- * pass2 reads mean = stats1[s][0] / stats1[s][3] (under strip sharding the
- * caller all-reduces stats1 first, so the mean is global)
+ * pass1 -> stats1[s][6] = sum z_um, max z_um, min z_um, n_used, n_uncut, mean
+ *          (sum in double-double, mean = sum / n rounded once)
+ * pass2 reads the mean stats1[s][5] (under strip sharding the caller
+ * all-reduces stats1 and recomputes the mean first, so it is global)
  *       -> out2[s][4] = sum|d|, sum d^2, sum d^3, sum d^4 */
 #define MSURF_RED_BLOCKS 1024
 int msurf_areal_pass1(const double* h, int64_t ld, int64_t surf_stride, int32_t n_surf,
@@ -148,7 +149,7 @@ int msurf_areal_plane_pass2(const double* h, int64_t ld, int64_t surf_stride, in
  * its own mean (single GPU); otherwise mean = stats_in[k][0]/stats_in[k][1]
  * of the caller's all-reduced first pass (strip-sharded profiles).
  * out[k = s*n_prof+p][8] = sum z_um, n_used, n_uncut, max z_um, min z_um,
- * sum|z - mean|, 0, 0 */
+ * sum|z - mean|, mean, 0 */
 int msurf_profiles(const double* h, int64_t surf_stride, int32_t n_surf,
                    const int64_t* start, int32_t n_prof, int64_t len, int64_t stride,
                    const double* sentinel, int32_t exclude_uncut, const double* stats_in,

@@ -566,15 +566,51 @@ __device__ void block_reduce(double (&v)[NV], const int (&kind)[NV], double* sh 
   }
 }
 
+// double-double warp+block reduction of (hi, lo) in a fixed order: the mean
+// of the areal pass is then the correctly rounded sum / n, so a constant
+// region has d == 0 exactly (roughness.py:106 on NumPy gives the same)
+__device__ void block_reduce_dd(double& hi, double& lo, double* sh /*[2*kWarps]*/) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const msurf_dd x = {hi, lo};
+    const msurf_dd y = {shfl_d(hi, o), shfl_d(lo, o)};
+    const msurf_dd r = ms_dd_add(x, y);
+    hi = r.hi;
+    lo = r.lo;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) {
+    sh[2 * warp] = hi;
+    sh[2 * warp + 1] = lo;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    hi = lane < kWarps ? sh[2 * lane] : 0.0;
+    lo = lane < kWarps ? sh[2 * lane + 1] : 0.0;
+#pragma unroll
+    for (int o = 4; o; o >>= 1) {
+      const msurf_dd x = {hi, lo};
+      const msurf_dd y = {shfl_d(hi, o), shfl_d(lo, o)};
+      const msurf_dd r = ms_dd_add(x, y);
+      hi = r.hi;
+      lo = r.lo;
+    }
+  }
+}
+
+// pass 1 partials per block: [sum_hi, max z, min z, n, n_uncut, sum_lo]
 __global__ void __launch_bounds__(kThreads)
     areal_pass1_kernel(const double* __restrict__ h, long long ld, long long sstride,
                        long long i_lo, long long j_lo, long long rows, long long cols,
                        const double* __restrict__ sent, int exclude, double* __restrict__ work) {
-  __shared__ double sh[kWarps * 5];
+  __shared__ double sh[kWarps * 4];
+  __shared__ double shd[kWarps * 2];
   const double* hs = h + (long long)blockIdx.y * sstride;
   const double sentinel = sent[blockIdx.y];
-  double v[5] = {0.0, -INFINITY, INFINITY, 0.0, 0.0};
-  const int kind[5] = {0, 1, 2, 0, 0};
+  double v[4] = {-INFINITY, INFINITY, 0.0, 0.0};  // max, min, n, n_uncut
+  const int kind[4] = {1, 2, 0, 0};
+  double shi = 0.0, slo = 0.0;
   const long long r0 = rows * blockIdx.x / gridDim.x, r1 = rows * (blockIdx.x + 1) / gridDim.x;
   for (long long r = r0; r < r1; ++r) {
     const double* row = hs + (i_lo + r) * ld + j_lo;
@@ -582,20 +618,65 @@ __global__ void __launch_bounds__(kThreads)
     for (long long c = threadIdx.x; c < cols; c += blockDim.x) {
       const double hv = row[c];
       const bool cut = hv < sentinel;
-      if (!cut) v[4] += 1.0;
+      if (!cut) v[3] += 1.0;
       if (cut || !exclude) {
-        const double z = hv * 1000.0;  // roughness.py:105 (MM_TO_UM)
-        v[0] += z;
-        v[1] = fmax(v[1], z);
-        v[2] = fmin(v[2], z);
-        v[3] += 1.0;
+        const double z = __dmul_rn(hv, 1000.0);  // roughness.py:105 (MM_TO_UM)
+        const msurf_dd t = ms_two_sum(shi, z);
+        shi = t.hi;
+        slo = __dadd_rn(slo, t.lo);
+        v[0] = fmax(v[0], z);
+        v[1] = fmin(v[1], z);
+        v[2] += 1.0;
       }
     }
   }
-  block_reduce<5>(v, kind, sh);
+  {
+    const msurf_dd t = ms_fast_two_sum(shi, slo);
+    shi = t.hi;
+    slo = t.lo;
+  }
+  block_reduce<4>(v, kind, sh);
+  block_reduce_dd(shi, slo, shd);
   if (threadIdx.x == 0) {
-    double* o = work + ((long long)blockIdx.y * gridDim.x + blockIdx.x) * 5;
-    for (int k = 0; k < 5; ++k) o[k] = v[k];
+    double* o = work + ((long long)blockIdx.y * gridDim.x + blockIdx.x) * 6;
+    o[0] = shi; o[1] = v[0]; o[2] = v[1]; o[3] = v[2]; o[4] = v[3]; o[5] = slo;
+  }
+}
+
+// one block per surface: stats1[s][6] = sum z, max z, min z, n, n_uncut, mean
+// (mean = correctly rounded double-double sum / n)
+__global__ void __launch_bounds__(kThreads)
+    finalize_stats1_kernel(const double* __restrict__ work, int nb, double* __restrict__ out) {
+  __shared__ double sh[kWarps * 4];
+  __shared__ double shd[kWarps * 2];
+  double v[4] = {-INFINITY, INFINITY, 0.0, 0.0};
+  const int kind[4] = {1, 2, 0, 0};
+  double shi = 0.0, slo = 0.0;
+  const double* w = work + (long long)blockIdx.x * nb * 6;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    const msurf_dd x = {shi, slo};
+    const msurf_dd y = {w[b * 6 + 0], w[b * 6 + 5]};
+    const msurf_dd r = ms_dd_add(x, y);
+    shi = r.hi;
+    slo = r.lo;
+    v[0] = fmax(v[0], w[b * 6 + 1]);
+    v[1] = fmin(v[1], w[b * 6 + 2]);
+    v[2] += w[b * 6 + 3];
+    v[3] += w[b * 6 + 4];
+  }
+  block_reduce<4>(v, kind, sh);
+  block_reduce_dd(shi, slo, shd);
+  if (threadIdx.x == 0) {
+    double* o = out + (long long)blockIdx.x * 6;
+    const double n = v[2];
+    double mean = 0.0;
+    if (n > 0.0) {
+      // (shi + slo) / n rounded once: q = shi/n, remainder via FMA
+      const double q = __ddiv_rn(shi, n);
+      const double rem = __dadd_rn(__fma_rn(-q, n, shi), slo);
+      mean = __dadd_rn(q, __ddiv_rn(rem, n));
+    }
+    o[0] = __dadd_rn(shi, slo); o[1] = v[0]; o[2] = v[1]; o[3] = n; o[4] = v[3]; o[5] = mean;
   }
 }
 
@@ -607,7 +688,7 @@ __global__ void __launch_bounds__(kThreads)
   __shared__ double sh[kWarps * 4];
   const double* hs = h + (long long)blockIdx.y * sstride;
   const double sentinel = sent[blockIdx.y];
-  const double mu = stats1[blockIdx.y * 5 + 0] / stats1[blockIdx.y * 5 + 3];  // z.mean()
+  const double mu = stats1[blockIdx.y * 6 + 5];  // z.mean() (roughness.py:106)
   double v[4] = {0.0, 0.0, 0.0, 0.0};
   const int kind[4] = {0, 0, 0, 0};
   const long long r0 = rows * blockIdx.x / gridDim.x, r1 = rows * (blockIdx.x + 1) / gridDim.x;
@@ -617,7 +698,7 @@ __global__ void __launch_bounds__(kThreads)
     for (long long c = threadIdx.x; c < cols; c += blockDim.x) {
       const double hv = row[c];
       if (hv < sentinel || !exclude) {
-        const double d = hv * 1000.0 - mu;  // roughness.py:105-106
+        const double d = __dsub_rn(__dmul_rn(hv, 1000.0), mu);  // roughness.py:105-106, no FMA
         const double d2 = d * d;
         v[0] += fabs(d);
         v[1] += d2;
@@ -726,34 +807,55 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// one block per (surface, profile): pass A = sum (double-double), counts,
+// extrema; mean = correctly rounded sum / n (or the all-reduced first pass of
+// a strip-sharded profile, stats_in); pass B = sum |z - mean|.
+// out[k][8] = sum z, n_used, n_uncut, max z, min z, sum|z-mean|, mean, 0
 __global__ void __launch_bounds__(kThreads)
     profiles_kernel(const double* __restrict__ h, long long sstride, const long long* __restrict__ start,
                     int n_prof, long long len, long long stride, const double* __restrict__ sent,
                     int exclude, const double* __restrict__ stats_in, double* __restrict__ out) {
-  __shared__ double sh[kWarps * 5];
+  __shared__ double sh[kWarps * 4];
+  __shared__ double shd[kWarps * 2];
   __shared__ double s_mean;
   const int prof = blockIdx.x;
   const int surf = blockIdx.y;
   const double* base = h + (long long)surf * sstride + start[prof];
   const double sentinel = sent[surf];
-  double v[5] = {0.0, 0.0, 0.0, -INFINITY, INFINITY};  // sum z, n_cut, n_uncut, max, min
-  const int kind[5] = {0, 0, 0, 1, 2};
+  double v[4] = {0.0, 0.0, -INFINITY, INFINITY};  // n_cut, n_uncut, max, min
+  const int kind[4] = {0, 0, 1, 2};
+  double shi = 0.0, slo = 0.0;
   for (long long k = threadIdx.x; k < len; k += blockDim.x) {
     const double hv = base[k * stride];
     const bool cut = hv < sentinel;
-    if (!cut) v[2] += 1.0;
+    if (!cut) v[1] += 1.0;
     if (cut || !exclude) {
-      const double z = hv * 1000.0;
-      v[0] += z;
-      v[1] += 1.0;
-      v[3] = fmax(v[3], z);
-      v[4] = fmin(v[4], z);
+      const double z = __dmul_rn(hv, 1000.0);
+      const msurf_dd t = ms_two_sum(shi, z);
+      shi = t.hi;
+      slo = __dadd_rn(slo, t.lo);
+      v[0] += 1.0;
+      v[2] = fmax(v[2], z);
+      v[3] = fmin(v[3], z);
     }
   }
-  block_reduce<5>(v, kind, sh);
+  {
+    const msurf_dd t = ms_fast_two_sum(shi, slo);
+    shi = t.hi;
+    slo = t.lo;
+  }
+  block_reduce<4>(v, kind, sh);
+  block_reduce_dd(shi, slo, shd);
   if (threadIdx.x == 0) {
     const long long k = (long long)surf * n_prof + prof;
-    s_mean = stats_in ? stats_in[k * 8 + 0] / stats_in[k * 8 + 1] : (v[1] > 0 ? v[0] / v[1] : 0.0);
+    double mean = 0.0;
+    if (stats_in) {
+      mean = stats_in[k * 8 + 0] / stats_in[k * 8 + 1];
+    } else if (v[0] > 0.0) {
+      const double q = __ddiv_rn(shi, v[0]);
+      mean = __dadd_rn(q, __ddiv_rn(__dadd_rn(__fma_rn(-q, v[0], shi), slo), v[0]));
+    }
+    s_mean = mean;
   }
   __syncthreads();
   const double mu = s_mean;
@@ -761,14 +863,14 @@ __global__ void __launch_bounds__(kThreads)
   const int ka[1] = {0};
   for (long long k = threadIdx.x; k < len; k += blockDim.x) {
     const double hv = base[k * stride];
-    if (hv < sentinel || !exclude) a[0] += fabs(hv * 1000.0 - mu);
+    if (hv < sentinel || !exclude) a[0] += fabs(__dsub_rn(__dmul_rn(hv, 1000.0), mu));
   }
   __syncthreads();
   block_reduce<1>(a, ka, sh);
   if (threadIdx.x == 0) {
     double* o = out + ((long long)surf * n_prof + prof) * 8;
-    o[0] = v[0]; o[1] = v[1]; o[2] = v[2]; o[3] = v[3]; o[4] = v[4]; o[5] = a[0];
-    o[6] = 0.0; o[7] = 0.0;
+    o[0] = __dadd_rn(shi, slo); o[1] = v[0]; o[2] = v[1]; o[3] = v[2]; o[4] = v[3]; o[5] = a[0];
+    o[6] = mu; o[7] = 0.0;
   }
 }
 
@@ -897,8 +999,8 @@ int msurf_areal_pass1(const double* h, int64_t ld, int64_t surf_stride, int32_t 
   areal_pass1_kernel<<<dim3(nb, n_surf), kThreads, 0, st>>>(h, ld, surf_stride, i_lo, j_lo, rows, cols,
                                                            sentinel, exclude_uncut, work);
   if (check_launch("areal_pass1_kernel")) return 1;
-  finalize_kernel<5><<<n_surf, kThreads, 0, st>>>(work, nb, (1u << 2) | (2u << 4), out1);
-  return check_launch("finalize_kernel<5>");
+  finalize_stats1_kernel<<<n_surf, kThreads, 0, st>>>(work, nb, out1);
+  return check_launch("finalize_stats1_kernel");
 }
 
 int msurf_areal_pass2(const double* h, int64_t ld, int64_t surf_stride, int32_t n_surf,

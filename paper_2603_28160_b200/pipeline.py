@@ -39,7 +39,7 @@ class SurfacePipeline:
         dev = batch.dev
         n = self.n
         self.work = torch.empty(n * _native.RED_BLOCKS * 5, dtype=torch.float64, device=dev)
-        self.out = torch.empty(n * 9 + max(1, n * len(self.rows_idx) * 8), dtype=torch.float64, device=dev)
+        self.out = torch.empty(n * 10 + max(1, n * len(self.rows_idx) * 8), dtype=torch.float64, device=dev)
         self.starts = torch.tensor([i * self.ld for i in self.rows_idx] or [0], dtype=torch.int64, device=dev)
         self.graph = None
         self.launches_per_run = batch.launches_per_run + 4 + (1 if self.rows_idx else 0)
@@ -54,10 +54,10 @@ class SurfacePipeline:
         _native.check(lib.msurf_areal_pass1(h, self.ld, self.nodes, n, 0, 0, g.m + 1, g.n + 1, sent,
                                             self.exclude, self.work.data_ptr(), o, sp))
         _native.check(lib.msurf_areal_pass2(h, self.ld, self.nodes, n, 0, 0, g.m + 1, g.n + 1, sent,
-                                            self.exclude, o, self.work.data_ptr(), o + n * 5 * 8, sp))
+                                            self.exclude, o, self.work.data_ptr(), o + n * 6 * 8, sp))
         if self.rows_idx:
             _native.check(lib.msurf_profiles(h, self.nodes, n, self.starts.data_ptr(), len(self.rows_idx),
-                                             g.n + 1, 1, sent, self.exclude, None, o + n * 9 * 8, sp))
+                                             g.n + 1, 1, sent, self.exclude, None, o + n * 10 * 8, sp))
 
     def stages(self):
         """The step as three launch groups: (fill), (sweep), (decode + reductions)."""
@@ -106,9 +106,9 @@ class SurfacePipeline:
         """One D2H: per surface (ArealMetrics | DomainError, [ProfileRoughness])."""
         a = self.out.cpu().numpy()
         n = self.n
-        st1 = a[: n * 5].reshape(n, 5)
-        st2 = a[n * 5: n * 9].reshape(n, 4)
-        prof = a[n * 9: n * 9 + n * len(self.rows_idx) * 8].reshape(n, len(self.rows_idx), 8)
+        st1 = a[: n * 6].reshape(n, 6)
+        st2 = a[n * 6: n * 10].reshape(n, 4)
+        prof = a[n * 10: n * 10 + n * len(self.rows_idx) * 8].reshape(n, len(self.rows_idx), 8)
         res = []
         for s in range(n):
             try:

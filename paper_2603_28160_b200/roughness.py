@@ -88,7 +88,7 @@ def _check_roi(spec, roi):
 
 def _metrics_from_moments(st1, st2) -> ArealMetrics:
     n = st1[3]
-    mean = st1[0] / n
+    mean = st1[5]  # device: double-double sum / n, rounded once
     sa = float(st2[0] / n)
     sq = float(np.sqrt(st2[1] / n))
     sp = float(st1[1] - mean)
@@ -122,8 +122,9 @@ def areal_moments_device(h_dev, ld, n_surf, surf_stride, roi_box, sentinels_dev,
                          allreduce=None):
     """Run both areal passes; returns (stats1 [n_surf,5], moments [n_surf,4])
     on the host. ``allreduce(tensor, op)`` (strip sharding) combines the
-    partial first-pass stats (kind "stats1": columns sum, max, min, n, n_uncut)
-    and second-pass moments (kind "moments": four sums) across ranks in place."""
+    partial first-pass stats (kind "stats1": columns sum, max, min, n, n_uncut,
+    mean — the callee recomputes the mean) and second-pass moments (kind
+    "moments": four sums) across ranks in place."""
     torch = _native.require_cuda()
     lib = _native.lib()
     i_lo, j_lo, rows, cols = roi_box
@@ -131,21 +132,21 @@ def areal_moments_device(h_dev, ld, n_surf, surf_stride, roi_box, sentinels_dev,
     sc = _Scratch.get(torch, dev, n_surf)
     work = sc.data_ptr()
     out1 = sc[n_surf * _native.RED_BLOCKS * 10:]
-    st1 = out1[: n_surf * 5]
-    st2 = out1[n_surf * 5: n_surf * 9]
+    st1 = out1[: n_surf * 6]
+    st2 = out1[n_surf * 6: n_surf * 10]
     sp = _native.stream_ptr()
     _native.check(lib.msurf_areal_pass1(h_dev.data_ptr(), ld, surf_stride, n_surf, i_lo, j_lo, rows,
                                         cols, sentinels_dev.data_ptr(), int(exclude), work,
                                         st1.data_ptr(), sp))
     if allreduce is not None:
-        allreduce(st1.view(n_surf, 5), "stats1")
+        allreduce(st1.view(n_surf, 6), "stats1")
     _native.check(lib.msurf_areal_pass2(h_dev.data_ptr(), ld, surf_stride, n_surf, i_lo, j_lo, rows,
                                         cols, sentinels_dev.data_ptr(), int(exclude), st1.data_ptr(),
                                         work, st2.data_ptr(), sp))
     if allreduce is not None:
         allreduce(st2.view(n_surf, 4), "moments")
-    both = out1[: n_surf * 9].cpu().numpy()
-    return both[: n_surf * 5].reshape(n_surf, 5), both[n_surf * 5:].reshape(n_surf, 4)
+    both = out1[: n_surf * 10].cpu().numpy()
+    return both[: n_surf * 6].reshape(n_surf, 6), both[n_surf * 6:].reshape(n_surf, 4)
 
 
 def _sentinel_tensor(torch, values, device):
@@ -323,12 +324,11 @@ def _profiles_device(h_dev, n_surf, surf_stride, starts, length, step, sentinels
 
 
 def _finish_profile(row, idx, uncut) -> ProfileRoughness:
-    s, n, n_unc, zmax, zmin, sabs = row[:6]
+    s, n, n_unc, zmax, zmin, sabs, mean = row[:7]
     if uncut == "raise" and n_unc > 0:
         raise DomainError(f"profile at index {idx} crosses uncut cells")
     if n < 2:
         raise DomainError("line roughness needs at least 2 samples")
-    mean = s / n
     rp, rv = float(zmax - mean), float(-(zmin - mean))
     return ProfileRoughness(index=int(idx), ra_um=float(sabs / n), rz_um=rp + rv, rp_um=rp, rv_um=rv,
                             sample_count=int(n))

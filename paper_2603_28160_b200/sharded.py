@@ -142,7 +142,7 @@ def areal_metrics_strip(res: StripResult, roi=None, uncut: str = "raise", group=
     dev = res.heights.device
     sent = torch.tensor([res.plan.initial_height], dtype=torch.float64, device=dev)
     work = torch.empty(_native.RED_BLOCKS * 5, dtype=torch.float64, device=dev)
-    st1 = torch.zeros((1, 5), dtype=torch.float64, device=dev)
+    st1 = torch.zeros((1, 6), dtype=torch.float64, device=dev)
     st1[0, 1], st1[0, 2] = -np.inf, np.inf
     st2 = torch.zeros((1, 4), dtype=torch.float64, device=dev)
     sp = _native.stream_ptr()
@@ -152,6 +152,7 @@ def areal_metrics_strip(res: StripResult, roi=None, uncut: str = "raise", group=
         _native.check(lib.msurf_areal_pass1(res.heights.data_ptr(), ld, 0, 1, i_lo, jl, rows, cols,
                                             sent.data_ptr(), ex, work.data_ptr(), st1.data_ptr(), sp))
     combine(st1, STATS1_SUM, STATS1_MAX, STATS1_MIN, group)
+    st1[:, 5] = st1[:, 0] / st1[:, 3]  # global mean
     if box is not None:  # an all-excluded ROI yields n = 0 and is rejected on the host
         i_lo, jl, rows, cols = box
         _native.check(lib.msurf_areal_pass2(res.heights.data_ptr(), ld, 0, 1, i_lo, jl, rows, cols,
@@ -179,6 +180,7 @@ def profile_roughness_strip(res: StripResult, every: int = 64, uncut: str = "rai
                                      sent.data_ptr(), ex, None, out.data_ptr(), sp))
     first = out.view(-1, 8).clone()
     combine(first, PROF_SUM, PROF_MAX, PROF_MIN, group)
+    first[:, 6] = first[:, 0] / first[:, 1]
     _native.check(lib.msurf_profiles(res.heights.data_ptr(), 0, 1, starts.data_ptr(), len(idx), ld, 1,
                                      sent.data_ptr(), ex, first.data_ptr(), out.data_ptr(), sp))
     sabs = out.view(-1, 8)[:, 5:6].contiguous()
@@ -212,7 +214,7 @@ class StripPipeline:
         dev = batch.dev
         f64 = torch.float64
         self.work = torch.empty(_native.RED_BLOCKS * 5, dtype=f64, device=dev)
-        self.st1 = torch.empty((1, 5), dtype=f64, device=dev)
+        self.st1 = torch.empty((1, 6), dtype=f64, device=dev)
         self.st2 = torch.empty((1, 4), dtype=f64, device=dev)
         self.prof = torch.empty((max(P, 1), 8), dtype=f64, device=dev)
         self.first = torch.empty((max(P, 1), 8), dtype=f64, device=dev)
@@ -257,9 +259,11 @@ class StripPipeline:
         self._allreduce(ext, dist.ReduceOp.MAX)
         self.st1[:, [0, 3, 4]] = sums[0:1]
         self.st1[:, 1], self.st1[:, 2] = ext[0:1, 0], -ext[0:1, 1]
+        self.st1[:, 5] = self.st1[:, 0] / self.st1[:, 3]  # global mean
         if P:
             self.first[:P, 0:3] = sums[1:]
             self.first[:P, 3], self.first[:P, 4] = ext[1:, 0], -ext[1:, 1]
+            self.first[:P, 6] = self.first[:P, 0] / self.first[:P, 1]
         # round 2: central moments around the global means
         _native.check(lib.msurf_areal_pass2(h, self.ld, 0, 1, 0, 0, self.rows, self.ld, sent, self.exclude,
                                             self.st1.data_ptr(), self.work.data_ptr(), self.st2.data_ptr(), sp))

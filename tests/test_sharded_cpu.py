@@ -38,8 +38,8 @@ def _stats1(block, sent, exclude):
     cut = block < sent
     z = (block[cut] if exclude else block.ravel()) * 1000.0
     if z.size == 0:
-        return np.array([0.0, -np.inf, np.inf, 0.0, float((~cut).sum())])
-    return np.array([z.sum(), z.max(), z.min(), float(z.size), float((~cut).sum())])
+        return np.array([0.0, -np.inf, np.inf, 0.0, float((~cut).sum()), 0.0])
+    return np.array([z.sum(), z.max(), z.min(), float(z.size), float((~cut).sum()), 0.0])
 
 
 def _moments(block, sent, exclude, mean):
@@ -57,9 +57,10 @@ def _worker(rank, world, port, out):
     strip = h[:, j_lo:j_hi + 1]
     res = {}
     for exclude in (True, False):
-        st1 = torch.tensor(_stats1(strip, sent, exclude)).view(1, 5)
+        st1 = torch.tensor(_stats1(strip, sent, exclude)).view(1, 6)
         sharded.combine(st1, sharded.STATS1_SUM, sharded.STATS1_MAX, sharded.STATS1_MIN)
-        mean = float(st1[0, 0] / st1[0, 3])
+        st1[0, 5] = st1[0, 0] / st1[0, 3]
+        mean = float(st1[0, 5])
         st2 = torch.tensor(_moments(strip, sent, exclude, mean)).view(1, 4)
         sharded.combine(st2, (0, 1, 2, 3), (), ())
         try:
@@ -76,6 +77,7 @@ def _worker(rank, world, port, out):
                       z.min() if z.size else np.inf, 0, 0, 0])
     first = torch.tensor(np.array(first, dtype=np.float64))
     sharded.combine(first, sharded.PROF_SUM, sharded.PROF_MAX, sharded.PROF_MIN)
+    first[:, 6] = first[:, 0] / first[:, 1]
     sabs = []
     for k, i in enumerate(rows):
         mean = float(first[k, 0] / first[k, 1])

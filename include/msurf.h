@@ -26,6 +26,10 @@ extern "C" {
 #define MSURF_MODE_REF 0      /* reference composite-matrix order, engine.py:257-296 */
 #define MSURF_MODE_EXT 1      /* rotated tool-frame points, z' time-invariant   */
 #define MSURF_MODE_EXT_TILT 2 /* rotated tool-frame points + lead tilt (z' per step) */
+/* OR-ed into the mode of msurf_sweep: also count the per-point diagnostics
+ * MSURF_CTR_DEPOSITS / MSURF_CTR_ATOMICS (two extra integer ops per point;
+ * without it those two counters stay zero) */
+#define MSURF_SWEEP_DIAG 0x100
 
 #define MSURF_CTR_LIVE_ROWS 0  /* (step, tooth, pass) rows with >= 1 chunk surviving the 2-D cull */
 #define MSURF_CTR_EVAL 1       /* edge points evaluated (points of surviving 32-point chunks)    */
@@ -110,7 +114,7 @@ int msurf_decode(uint64_t* keys, int64_t count, int32_t n_surf, const double* se
  * sentinel[n_surf] device. exclude_uncut=0 counts uncut cells (the host raises
  * DomainError like roughness.py:86-89); =1 skips them. Reductions are
  * deterministic (fixed block partition, fixed-order tree): reruns are
- * bit-identical. work: device scratch of n_surf * MSURF_RED_BLOCKS * 5 doubles
+ * bit-identical. work: device scratch of n_surf * MSURF_WORK_DOUBLES doubles
  * (the plane-leveling passes below need * 10).
  * pass1 -> stats1[s][6] = sum z_um, max z_um, min z_um, n_used, n_uncut, mean
  *          (sum in double-double, mean = sum / n rounded once)
@@ -118,6 +122,9 @@ int msurf_decode(uint64_t* keys, int64_t count, int32_t n_surf, const double* se
  * all-reduces stats1 and recomputes the mean first, so it is global)
  *       -> out2[s][4] = sum|d|, sum d^2, sum d^3, sum d^4 */
 #define MSURF_RED_BLOCKS 1024
+/* scratch doubles per surface for every reduction below (at most
+ * MSURF_RED_BLOCKS blocks x 10 partials: plane pass 1) */
+#define MSURF_WORK_DOUBLES (MSURF_RED_BLOCKS * 10)
 int msurf_areal_pass1(const double* h, int64_t ld, int64_t surf_stride, int32_t n_surf,
                       int64_t i_lo, int64_t j_lo, int64_t rows, int64_t cols,
                       const double* sentinel, int32_t exclude_uncut, double* work,
@@ -132,7 +139,7 @@ int msurf_areal_pass2(const double* h, int64_t ld, int64_t surf_stride, int32_t 
  * Siz, Sjz, n_uncut (i, j = offsets inside the ROI, z in um); the host solves
  * the 3x3 system for z ~ a*i + b*j + c; pass 2 with coef[s][3] = (a, b, c)
  * writes out[s][6] = S|d|, Sd^2, Sd^3, Sd^4, max d, min d of d = z - plane.
- * work: n_surf * MSURF_RED_BLOCKS * 10 doubles. */
+ * work: n_surf * MSURF_WORK_DOUBLES doubles. */
 int msurf_areal_plane_pass1(const double* h, int64_t ld, int64_t surf_stride, int32_t n_surf,
                             int64_t i_lo, int64_t j_lo, int64_t rows, int64_t cols,
                             const double* sentinel, int32_t exclude_uncut, double* work, double* out,

@@ -20,7 +20,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MSURF_LIB") or os.path.join(_HERE, "libmsurf.so")
 ABI_VERSION = 1
 NUM_CTRS = 5
+SWEEP_DIAG = 0x100  # MSURF_SWEEP_DIAG: count deposits/atomics per point
 RED_BLOCKS = 1024
+WORK_DOUBLES = RED_BLOCKS * 10  # MSURF_WORK_DOUBLES: reduction scratch per surface
 
 c_double, c_int64, c_int32, c_void_p = ctypes.c_double, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
 

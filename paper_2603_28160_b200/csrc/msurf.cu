@@ -29,12 +29,6 @@
 
 namespace {
 
-#ifndef MSURF_FLOAT_DEDUPE
-#define MSURF_FLOAT_DEDUPE 1  // tilt mode: neighbour comparisons on float32 z' (exactness argued inline)
-#endif
-#ifndef MSURF_TWO_SIDED
-#define MSURF_TWO_SIDED 1  // tilt mode: deposit only local minima of each cell run
-#endif
 #ifndef MSURF_MIN_BLOCKS
 #define MSURF_MIN_BLOCKS 6  // CTAs per SM the register budget is sized for (80 regs at 128 threads)
 #endif
@@ -157,7 +151,80 @@ __device__ __forceinline__ bool tool_box_hits(const double* b, double c, double 
   return (x_hi >= wx_lo) & (x_lo <= wx_hi) & (v_hi + ty >= wy_lo) & (v_lo + ty <= wy_hi);
 }
 
+// one edge point under one lane's step transform: workpiece x', y' in the
+// reference's exact op order, the magic-number high words of both cell
+// coordinates, the near-boundary flag, the deposit key and (tilt) a float32
+// copy of z' for the neighbour comparisons
+struct PointEval {
+  double xw, yw;
+  int hi_x, hi_y;
+  bool near;
+  uint64_t key;
+  float zf;
+};
+
 template <int MODE>
+__device__ __forceinline__ PointEval eval_point(const double4 pt, const double* r, double inv, double cx0,
+                                                double cy0, double tilt_c, double tilt_s, double zoff) {
+  PointEval e;
+  e.zf = 0.f;
+  if (MODE == MSURF_MODE_REF) {
+    // engine.py:289-296: xw = ((m00*xp + m01*yp) + m02*zp) + m03
+    e.xw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r[0], pt.x), __dmul_rn(r[1], pt.y)), __dmul_rn(r[2], pt.z)),
+                     r[3]);
+    e.yw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r[4], pt.x), __dmul_rn(r[5], pt.y)), __dmul_rn(r[6], pt.z)),
+                     r[7]);
+    e.key = (uint64_t)__double_as_longlong(pt.w);
+  } else {
+    const double uu = __dadd_rn(__dmul_rn(r[0], pt.x), __dmul_rn(r[1], pt.y));
+    const double vv = __dadd_rn(__dmul_rn(-r[1], pt.x), __dmul_rn(r[0], pt.y));
+    e.xw = __dadd_rn(uu, r[2]);
+    if (MODE == MSURF_MODE_EXT_TILT) {
+      // y' = cos(tau) v - sin(tau) z ; z' = (sin(tau) v + cos(tau) z) + zoff
+      const double yv = __dsub_rn(__dmul_rn(tilt_c, vv), pt.z);
+      const double zz = __dadd_rn(__dadd_rn(__dmul_rn(tilt_s, vv), pt.w), zoff);
+      e.yw = __dadd_rn(yv, r[3]);
+      e.key = enc_key_raw(zz);  // zz = (..) + zoff with zoff != -0 (host-canonical): never -0
+      e.zf = __double2float_rn(zz);
+    } else {
+      e.yw = __dadd_rn(vv, r[3]);
+      e.key = (uint64_t)__double_as_longlong(pt.z);
+    }
+  }
+  const double mx = __dadd_rn(__fma_rn(e.xw, inv, cx0), 0x1.8p20);
+  const double my = __dadd_rn(__fma_rn(e.yw, inv, cy0), 0x1.8p20);
+  e.hi_x = __double2hiint(mx);
+  e.hi_y = __double2hiint(my);
+  e.near = (((unsigned)__double2loint(mx) + 8u) < 16u) | (((unsigned)__double2loint(my) + 8u) < 16u);
+#ifdef MSURF_FORCE_NEAR
+  e.near = true;  // test build: every point takes the exact deferred path
+#endif
+  return e;
+}
+
+// Time-neighbour pre-reduction across lanes (consecutive live steps of one
+// point): within a run of lanes whose point sits in one cell only the run's
+// minimum deposits. Constant z' (REF/EXT): the run's first lane. Tilt: lanes
+// that are a local minimum (< predecessor, <= successor).
+template <int MODE>
+__device__ __forceinline__ void dedupe(int lane, int idx, bool inside, float zf, bool& dep) {
+  const int idx_prev = __shfl_up_sync(0xffffffffu, idx, 1);
+  dep = inside & ((lane == 0) | (idx != idx_prev));
+  if (MODE == MSURF_MODE_EXT_TILT) {
+    // compare float32 roundings of z': rounding is monotone, so
+    // zf > zf_neighbour proves z' > z'_neighbour; a lane is skipped only
+    // when a same-cell neighbour is provably lower, and every chain of
+    // skips ends at a deposited lane whose z' is lower still (ties in
+    // float keep both deposits) -> 32-bit shuffles instead of 64-bit
+    const float zf_prev = __shfl_up_sync(0xffffffffu, zf, 1);
+    dep = inside & !((lane > 0) & (idx == idx_prev) & (zf > zf_prev));
+    const int idx_next = __shfl_down_sync(0xffffffffu, idx, 1);
+    const float zf_next = __shfl_down_sync(0xffffffffu, zf, 1);
+    dep &= !((lane < 31) & (idx == idx_next) & (zf > zf_next));
+  }
+}
+
+template <int MODE, bool DIAG>
 __global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
     sweep_kernel(const msurf_job* __restrict__ jobs, int n_jobs,
                  const int64_t* __restrict__ prefix, int mask_words) {
@@ -358,6 +425,9 @@ __global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
   const unsigned span_i = (unsigned)J.m;
   const int j_lo = (int)J.j_lo;
   const unsigned span_j = (unsigned)(J.j_hi - J.j_lo);
+  // j index straight from the magic-number high word, already relative to
+  // the owned strip: hi - (kMagicHi + j_lo)
+  const int jbias = kMagicHi + j_lo;
   const int ldk = (int)J.ld;
   unsigned long long* __restrict__ keys = reinterpret_cast<unsigned long long*>(J.keys);
   const double tilt_c = J.tilt_c, tilt_s = J.tilt_s, zoff = J.zoff;
@@ -381,99 +451,84 @@ __global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
       for (int k = 0; k < RW; ++k) r[k] = 0.0;
     }
     if (!__any_sync(0xffffffffu, on)) continue;
+    // lanes whose step is not live for this chunk: i index pushed far out of
+    // range, so the per-point range test also covers `on`
+    const int ibias = on ? kMagicHi : kMagicHi - (1 << 30);
     const int p_end = min(32, npts - q * 32);
-    // stage the chunk's 32 point records (1 KB, coalesced) for broadcast reads
+    // stage the chunk's 32 point records (1 KB, coalesced) for broadcast
+    // reads; slots past the chunk's end hold zeros (finite, masked below)
     __syncwarp();
-    if (lane < p_end) {
-      const double2* src = reinterpret_cast<const double2*>(pts + q * 32 + lane);
-      const double2 a = __ldg(src), b = __ldg(src + 1);
-      ptstage[warp][lane] = make_double4(a.x, a.y, b.x, b.y);
+    {
+      double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+      if (lane < p_end) {
+        const double2* src = reinterpret_cast<const double2*>(pts + q * 32 + lane);
+        const double2 a = __ldg(src), b = __ldg(src + 1);
+        v = make_double4(a.x, a.y, b.x, b.y);
+      }
+      ptstage[warp][lane] = v;
     }
     __syncwarp();
-#pragma unroll 2
-    for (int k = 0; k < p_end; ++k) {
-      const double4 pt = ptstage[warp][k];  // same address in every lane: broadcast
-      double xw, yw, zkey_src = 0.0;
-      uint64_t key;
-      if (MODE == MSURF_MODE_REF) {
-        // engine.py:289-296: xw = ((m00*xp + m01*yp) + m02*zp) + m03
-        xw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r[0], pt.x), __dmul_rn(r[1], pt.y)),
-                                 __dmul_rn(r[2], pt.z)), r[3]);
-        yw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r[4], pt.x), __dmul_rn(r[5], pt.y)),
-                                 __dmul_rn(r[6], pt.z)), r[7]);
-        key = (uint64_t)__double_as_longlong(pt.w);
-      } else {
-        const double uu = __dadd_rn(__dmul_rn(r[0], pt.x), __dmul_rn(r[1], pt.y));
-        const double vv = __dadd_rn(__dmul_rn(-r[1], pt.x), __dmul_rn(r[0], pt.y));
-        xw = __dadd_rn(uu, r[2]);
-        if (MODE == MSURF_MODE_EXT_TILT) {
-          // y' = cos(tau) v - sin(tau) z ; z' = (sin(tau) v + cos(tau) z) + zoff
-          const double yv = __dsub_rn(__dmul_rn(tilt_c, vv), pt.z);
-          const double zz = __dadd_rn(__dadd_rn(__dmul_rn(tilt_s, vv), pt.w), zoff);
-          yw = __dadd_rn(yv, r[3]);
-          key = enc_key_raw(zz);  // zz = (..) + zoff with zoff != -0 (host-canonical): never -0
-          zkey_src = zz;
-        } else {
-          yw = __dadd_rn(vv, r[3]);
-          key = (uint64_t)__double_as_longlong(pt.z);
+    // Two points per iteration with no divergent branch between their
+    // evaluations (the compiler interleaves the two dependent fp64 chains).
+    // Near-boundary points (probability ~1e-9 each) are not resolved inline:
+    // they are flagged, kept out of the neighbour comparisons (treated as
+    // outside), and deposited after the chunk with the exact reference index
+    // — an extra deposit is always safe, a skipped one never is.
+    bool anynear = false;
+    for (int k = 0; k < p_end; k += 2) {
+      const int ibias_b = (k + 1 < p_end) ? ibias : kMagicHi - (1 << 30);
+      PointEval ea = eval_point<MODE>(ptstage[warp][k], r, inv, cx0, cy0, tilt_c, tilt_s, zoff);
+      PointEval eb = eval_point<MODE>(ptstage[warp][k + 1], r, inv, cx0, cy0, tilt_c, tilt_s, zoff);
+      const int ia = ea.hi_x - ibias, ja = ea.hi_y - jbias;
+      const int ib = eb.hi_x - ibias_b, jb = eb.hi_y - jbias;
+      // near flags of live points (the fast index may be off by one there, so
+      // the range test must not filter them)
+      anynear |= (ea.near | (eb.near & (k + 1 < p_end))) & on;
+      const bool in_a = ((unsigned)ia <= span_i) & ((unsigned)ja <= span_j) & !ea.near;
+      const bool in_b = ((unsigned)ib <= span_i) & ((unsigned)jb <= span_j) & !eb.near;
+      const int idx_a = in_a ? ia * ldk + ja : -1;
+      const int idx_b = in_b ? ib * ldk + jb : -1;
+      bool dep_a, dep_b;
+      dedupe<MODE>(lane, idx_a, in_a, ea.zf, dep_a);
+      dedupe<MODE>(lane, idx_b, in_b, eb.zf, dep_b);
+      if (DIAG) {
+        n_dep += (unsigned)in_a + (unsigned)in_b;
+        n_atom += (unsigned)dep_a + (unsigned)dep_b;
+      }
+      red_min_u64_if(keys + idx_a, (unsigned long long)ea.key, dep_a);
+      red_min_u64_if(keys + idx_b, (unsigned long long)eb.key, dep_b);
+    }
+    if (__builtin_expect(__any_sync(0xffffffffu, anynear), 0)) {
+      for (int k = 0; k < p_end; ++k) {
+        const PointEval e = eval_point<MODE>(ptstage[warp][k], r, inv, cx0, cy0, tilt_c, tilt_s, zoff);
+        if (!(e.near & on)) continue;
+        const int ie = cell_index_exact(e.xw, J.x_min, dd);
+        const int je = cell_index_exact(e.yw, J.y_min, dd) - j_lo;
+        const bool in = on & ((unsigned)ie <= span_i) & ((unsigned)je <= span_j);
+        if (in) red_min_u64(keys + (ie * ldk + je), (unsigned long long)e.key);
+        if (DIAG) {
+          n_dep += in;
+          n_atom += in;
         }
       }
-      CellFast ci = cell_fast(xw, inv, cx0);
-      CellFast cj = cell_fast(yw, inv, cy0);
-      if (__builtin_expect((ci.near | cj.near) & on, 0)) {
-        ci.idx = cell_index_exact(xw, J.x_min, dd);
-        cj.idx = cell_index_exact(yw, J.y_min, dd);
-      }
-      const bool inside = on & ((unsigned)ci.idx <= span_i) & ((unsigned)(cj.idx - j_lo) <= span_j);
-      const int idx = inside ? ci.idx * ldk + (cj.idx - j_lo) : -1;
-      // time-neighbour pre-reduction: within a run of lanes (consecutive
-      // live steps) whose point sits in one cell, only the run's minimum
-      // deposits. Constant z' (REF/EXT): the run's first lane. Tilt: lanes
-      // that are a local minimum (< predecessor, <= successor).
-      const int idx_prev = __shfl_up_sync(0xffffffffu, idx, 1);
-      bool dep = inside & ((lane == 0) | (idx != idx_prev));
-      if (MODE == MSURF_MODE_EXT_TILT) {
-#if MSURF_FLOAT_DEDUPE
-        // compare float32 roundings of z': rounding is monotone, so
-        // zf > zf_neighbour proves z' > z'_neighbour; a lane is skipped only
-        // when a same-cell neighbour is provably lower, and every chain of
-        // skips ends at a deposited lane whose z' is lower still (ties in
-        // float keep both deposits) -> 32-bit shuffles instead of 64-bit
-        const float zf = __double2float_rn(zkey_src);
-        const float zf_prev = __shfl_up_sync(0xffffffffu, zf, 1);
-        dep = inside & !((lane > 0) & (idx == idx_prev) & (zf > zf_prev));
-#if MSURF_TWO_SIDED
-        const int idx_next = __shfl_down_sync(0xffffffffu, idx, 1);
-        const float zf_next = __shfl_down_sync(0xffffffffu, zf, 1);
-        dep &= !((lane < 31) & (idx == idx_next) & (zf > zf_next));
-#endif
-#else
-        const uint64_t key_prev = __shfl_up_sync(0xffffffffu, key, 1);
-        dep = inside & ((lane == 0) | (idx != idx_prev) | (key < key_prev));
-#if MSURF_TWO_SIDED
-        const int idx_next = __shfl_down_sync(0xffffffffu, idx, 1);
-        const uint64_t key_next = __shfl_down_sync(0xffffffffu, key, 1);
-        dep &= (lane == 31) | (idx != idx_next) | (key <= key_next);
-#endif
-#endif
-      }
-      n_dep += inside;
-      n_atom += dep;
-      red_min_u64_if(keys + idx, (unsigned long long)key, dep);
     }
   }
 
   // counters: one atomic per warp
-  n_dep = warp_sum_u(n_dep);
-  n_atom = warp_sum_u(n_atom);
-  if (lane == 0 && J.counters) {
-    if (warp == 0) {
+  if (J.counters) {
+    if (DIAG) {
+      n_dep = warp_sum_u(n_dep);
+      n_atom = warp_sum_u(n_atom);
+      if (lane == 0) {
+        atomicAdd(J.counters + MSURF_CTR_DEPOSITS, (unsigned long long)n_dep);
+        atomicAdd(J.counters + MSURF_CTR_ATOMICS, (unsigned long long)n_atom);
+      }
+    }
+    if (tid == 0) {
       atomicAdd(J.counters + MSURF_CTR_LIVE_ROWS, (unsigned long long)n_live);
       atomicAdd(J.counters + MSURF_CTR_EVAL, (unsigned long long)n_eval_cta);
       atomicAdd(J.counters + MSURF_CTR_ENGAGED_ROWS, (unsigned long long)n_eng_cta);
     }
-    atomicAdd(J.counters + MSURF_CTR_DEPOSITS, (unsigned long long)n_dep);
-    atomicAdd(J.counters + MSURF_CTR_ATOMICS, (unsigned long long)n_atom);
   }
 }
 
@@ -908,6 +963,16 @@ __global__ void mb_atomic_kernel(unsigned long long* buf, long long mask, int it
   }
 }
 
+template <int MODE, bool DIAG>
+cudaError_t launch_sweep(int64_t n_tiles, size_t smem, cudaStream_t st, const msurf_job* jobs, int n_jobs,
+                         const int64_t* prefix, int mask_words) {
+  cudaError_t e = cudaSuccess;
+  if (smem > 48 * 1024)
+    e = cudaFuncSetAttribute(sweep_kernel<MODE, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) sweep_kernel<MODE, DIAG><<<(unsigned)n_tiles, kSweepThreads, smem, st>>>(jobs, n_jobs, prefix, mask_words);
+  return e;
+}
+
 }  // namespace
 
 // ================================================================ C ABI
@@ -944,18 +1009,19 @@ int msurf_sweep(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile_prefi
                       (size_t)kTileSteps * mask_words * sizeof(uint64_t) + (size_t)kTileSteps * sizeof(int);
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
-  switch (mode) {
+  const bool diag = (mode & MSURF_SWEEP_DIAG) != 0;
+  switch (mode & ~MSURF_SWEEP_DIAG) {
     case MSURF_MODE_REF:
-      if (smem > 48 * 1024) e = cudaFuncSetAttribute(sweep_kernel<MSURF_MODE_REF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e == cudaSuccess) sweep_kernel<MSURF_MODE_REF><<<(unsigned)n_tiles, kSweepThreads, smem, st>>>(jobs, n_jobs, tile_prefix, mask_words);
+      e = diag ? launch_sweep<MSURF_MODE_REF, true>(n_tiles, smem, st, jobs, n_jobs, tile_prefix, mask_words)
+               : launch_sweep<MSURF_MODE_REF, false>(n_tiles, smem, st, jobs, n_jobs, tile_prefix, mask_words);
       break;
     case MSURF_MODE_EXT:
-      if (smem > 48 * 1024) e = cudaFuncSetAttribute(sweep_kernel<MSURF_MODE_EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e == cudaSuccess) sweep_kernel<MSURF_MODE_EXT><<<(unsigned)n_tiles, kSweepThreads, smem, st>>>(jobs, n_jobs, tile_prefix, mask_words);
+      e = diag ? launch_sweep<MSURF_MODE_EXT, true>(n_tiles, smem, st, jobs, n_jobs, tile_prefix, mask_words)
+               : launch_sweep<MSURF_MODE_EXT, false>(n_tiles, smem, st, jobs, n_jobs, tile_prefix, mask_words);
       break;
     case MSURF_MODE_EXT_TILT:
-      if (smem > 48 * 1024) e = cudaFuncSetAttribute(sweep_kernel<MSURF_MODE_EXT_TILT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e == cudaSuccess) sweep_kernel<MSURF_MODE_EXT_TILT><<<(unsigned)n_tiles, kSweepThreads, smem, st>>>(jobs, n_jobs, tile_prefix, mask_words);
+      e = diag ? launch_sweep<MSURF_MODE_EXT_TILT, true>(n_tiles, smem, st, jobs, n_jobs, tile_prefix, mask_words)
+               : launch_sweep<MSURF_MODE_EXT_TILT, false>(n_tiles, smem, st, jobs, n_jobs, tile_prefix, mask_words);
       break;
     default:
       return set_err("msurf_sweep: unknown mode");

@@ -100,7 +100,8 @@ class SimulationResult:
     @property
     def counters(self) -> dict:
         if self._ctrs is None:
-            self._ctrs = _counters_dict(self._launch.counters()[0][self._index])
+            self._ctrs = _counters_dict(self._launch.counters()[0][self._index],
+                                        self._launch.batch.diagnostics)
         return self._ctrs
 
     def __repr__(self) -> str:
@@ -140,10 +141,13 @@ class SweepBatch:
     one int64 tensor holding all surfaces' Z-maps back to back (u64 keys
     during the sweep, fp64 heights after the decode, in place)."""
 
-    def __init__(self, surfaces, trig: str = "device", device=None, l2_tile_bytes: int = L2_TILE_BYTES):
+    def __init__(self, surfaces, trig: str = "device", device=None, l2_tile_bytes: int = L2_TILE_BYTES,
+                 diagnostics: bool = False):
         torch = _native.require_cuda()
         self.torch = torch
         self.lib = _native.lib()
+        # per-point deposit/atomic counters (MSURF_SWEEP_DIAG): off on the hot path
+        self.diagnostics = bool(diagnostics)
         self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         if trig not in ("device", "host"):
             raise ConfigError(f"trig must be 'device' or 'host', got {trig!r}")
@@ -281,7 +285,8 @@ class SweepBatch:
         """One msurf_sweep launch per kinematics mode present in the batch."""
         lib, base = self.lib, self.base
         for mode, idx, job_off, pre_off, n_tiles, max_pts in self.group_meta:
-            _native.check(lib.msurf_sweep(base + job_off, len(idx), base + pre_off, n_tiles, mode,
+            flag = _native.SWEEP_DIAG if self.diagnostics else 0
+            _native.check(lib.msurf_sweep(base + job_off, len(idx), base + pre_off, n_tiles, mode | flag,
                                           max_pts, sp))
 
     def launch_decode(self, sp: int) -> None:
@@ -336,20 +341,23 @@ class SweepBatch:
         return out
 
 
-def sweep_plans(surfaces, trig: str = "device", device=None):
+def sweep_plans(surfaces, trig: str = "device", device=None, diagnostics: bool = True):
     """One-shot: upload, launch, collect. Returns (heights views, counters,
     machined, device_ms, trajectories, batch)."""
     torch = _native.require_cuda()
-    b = SweepBatch(surfaces, trig=trig, device=device)
+    b = SweepBatch(surfaces, trig=trig, device=device, diagnostics=diagnostics)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     b.launch(events=ev)
     small, machined = b.counters()
     return b.heights(), small, machined, ev[0].elapsed_time(ev[3]), b.trajectories(), b
 
 
-def _counters_dict(row) -> dict:
+def _counters_dict(row, diagnostics: bool = True) -> dict:
+    """Sweep counters; deposits/atomics are None unless the launch counted
+    them (``diagnostics=True``)."""
     return {"live_rows": int(row[0]), "points_evaluated": int(row[1]),
-            "deposits": int(row[2]), "atomics": int(row[3]), "engaged_rows": int(row[4])}
+            "deposits": int(row[2]) if diagnostics else None,
+            "atomics": int(row[3]) if diagnostics else None, "engaged_rows": int(row[4])}
 
 
 def _build_trajectory(p: SweepPlan, traj_dev) -> TrajectoryRecord:
@@ -362,22 +370,23 @@ def _build_trajectory(p: SweepPlan, traj_dev) -> TrajectoryRecord:
 
 
 def simulate(config: SimulationConfig, extensions: Extensions | None = None, *,
-             trig: str = "device") -> SimulationResult:
+             trig: str = "device", diagnostics: bool = False) -> SimulationResult:
     """GPU FSM sweep with the reference's contract (engine.py:316-357).
 
     ``extensions`` selects the extended kinematics (extensions.py).
     ``trig='host'`` takes the per-(step, tooth) cos/sin from the host libm
     (exactly the reference's values) instead of the device's correctly
-    rounded double-double sincos — the parity mode."""
+    rounded double-double sincos — the parity mode. ``diagnostics=True``
+    also counts deposits and atomics (``result.counters``)."""
     p = plan(config, extensions)
-    return _launch_results([p], trig)[0]
+    return _launch_results([p], trig, diagnostics)[0]
 
 
-def _launch_results(plans, trig):
+def _launch_results(plans, trig, diagnostics=False):
     """Upload, launch asynchronously, wrap the fields (no host sync unless a
     trajectory record is requested)."""
     torch = _native.require_cuda()
-    b = SweepBatch([(p, 0, p.grid.n) for p in plans], trig=trig)
+    b = SweepBatch([(p, 0, p.grid.n) for p in plans], trig=trig, diagnostics=diagnostics)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     b.launch(events=ev)
     lk = _Launch(b, ev)
@@ -393,7 +402,7 @@ def _launch_results(plans, trig):
     return out
 
 
-def simulate_batch(configs, extensions=None, *, trig: str = "device"):
+def simulate_batch(configs, extensions=None, *, trig: str = "device", diagnostics: bool = False):
     """Batched mode: many parameter sets swept in the same kernel launches.
     ``extensions`` is None, one Extensions, or a list aligned with configs."""
     if isinstance(extensions, (list, tuple)):
@@ -404,14 +413,15 @@ def simulate_batch(configs, extensions=None, *, trig: str = "device"):
         exts = [extensions] * len(configs)
     if not configs:
         return []
-    return _launch_results(plan_many(configs, exts), trig)
+    return _launch_results(plan_many(configs, exts), trig, diagnostics)
 
 
-def simulate_reference(config: SimulationConfig, extensions: Extensions | None = None) -> SimulationResult:
+def simulate_reference(config: SimulationConfig, extensions: Extensions | None = None, *,
+                       diagnostics: bool = False) -> SimulationResult:
     """The reference's 'naive' kernel is its oracle (engine.py:360-406). On the
     GPU the same sweep runs in parity mode: trig from the host libm, so every
     input the reference rounds is bit-identical by construction."""
-    return simulate(config, extensions, trig="host")
+    return simulate(config, extensions, trig="host", diagnostics=diagnostics)
 
 
 @dataclass(frozen=True)

@@ -38,7 +38,7 @@ class SurfacePipeline:
         self.rows_idx = list(range(0, g.m + 1, every)) if every else []
         dev = batch.dev
         n = self.n
-        self.work = torch.empty(n * _native.RED_BLOCKS * 5, dtype=torch.float64, device=dev)
+        self.work = torch.empty(n * _native.WORK_DOUBLES, dtype=torch.float64, device=dev)
         self.out = torch.empty(n * 10 + max(1, n * len(self.rows_idx) * 8), dtype=torch.float64, device=dev)
         self.starts = torch.tensor([i * self.ld for i in self.rows_idx] or [0], dtype=torch.int64, device=dev)
         self.graph = None

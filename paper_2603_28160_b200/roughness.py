@@ -110,7 +110,7 @@ class _Scratch:
     @classmethod
     def get(cls, torch, device, n_surf: int):
         key = (device.index if device.index is not None else torch.cuda.current_device())
-        need = n_surf * _native.RED_BLOCKS * 10 + n_surf * 16
+        need = n_surf * _native.WORK_DOUBLES + n_surf * 16
         t = cls._cache.get(key)
         if t is None or t.numel() < need:
             t = torch.empty(need, dtype=torch.float64, device=device)
@@ -131,7 +131,7 @@ def areal_moments_device(h_dev, ld, n_surf, surf_stride, roi_box, sentinels_dev,
     dev = h_dev.device
     sc = _Scratch.get(torch, dev, n_surf)
     work = sc.data_ptr()
-    out1 = sc[n_surf * _native.RED_BLOCKS * 10:]
+    out1 = sc[n_surf * _native.WORK_DOUBLES:]
     st1 = out1[: n_surf * 6]
     st2 = out1[n_surf * 6: n_surf * 10]
     sp = _native.stream_ptr()
@@ -194,7 +194,7 @@ def _areal_plane(field: HeightField, roi, uncut: str) -> ArealMetrics:
     sent = _field_sentinel(torch, field, h.device)
     sc = _Scratch.get(torch, h.device, 1)
     work = sc.data_ptr()
-    out = sc[_native.RED_BLOCKS * 10:]
+    out = sc[_native.WORK_DOUBLES:]
     rows, cols = i_hi - i_lo + 1, j_hi - j_lo + 1
     ld = field.spec.n + 1
     ex = int(uncut == "exclude")

@@ -97,23 +97,22 @@ class StripResult:
     batch: object
 
 
-def simulate_strip(config, ext: Extensions | None, rank: int, world: int, trig: str = "device") -> StripResult:
+def simulate_strip(config, ext: Extensions | None, rank: int, world: int, trig: str = "device",
+                   diagnostics: bool = False) -> StripResult:
     """Sweep this rank's feed-direction strip of one surface."""
-    from .engine import SweepBatch
+    from .engine import SweepBatch, _counters_dict
 
     torch = _native.require_cuda()
     p = make_plan(config, ext)
     if p.record:
         raise ConfigError("record_trajectory is not supported under strip sharding")
     j_lo, j_hi = strip_bounds(p.grid.n + 1, world)[rank]
-    b = SweepBatch([(p, j_lo, j_hi)], trig=trig)
+    b = SweepBatch([(p, j_lo, j_hi)], trig=trig, diagnostics=diagnostics)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     b.launch(events=ev)
     ctr, machined = b.counters()
     return StripResult(plan=p, j_lo=j_lo, j_hi=j_hi, heights=b.heights()[0],
-                       counters={"live_rows": int(ctr[0][0]), "points_evaluated": int(ctr[0][1]),
-                                 "deposits": int(ctr[0][2]), "atomics": int(ctr[0][3]),
-                                 "engaged_rows": int(ctr[0][4])},
+                       counters=_counters_dict(ctr[0], diagnostics),
                        cells_updated=int(machined[0]), main_loop_seconds=ev[0].elapsed_time(ev[3]) * 1e-3,
                        batch=b)
 
@@ -141,7 +140,7 @@ def areal_metrics_strip(res: StripResult, roi=None, uncut: str = "raise", group=
     ld = res.j_hi - res.j_lo + 1
     dev = res.heights.device
     sent = torch.tensor([res.plan.initial_height], dtype=torch.float64, device=dev)
-    work = torch.empty(_native.RED_BLOCKS * 5, dtype=torch.float64, device=dev)
+    work = torch.empty(_native.WORK_DOUBLES, dtype=torch.float64, device=dev)
     st1 = torch.zeros((1, 6), dtype=torch.float64, device=dev)
     st1[0, 1], st1[0, 2] = -np.inf, np.inf
     st2 = torch.zeros((1, 4), dtype=torch.float64, device=dev)
@@ -213,7 +212,7 @@ class StripPipeline:
         P = len(self.prof_idx)
         dev = batch.dev
         f64 = torch.float64
-        self.work = torch.empty(_native.RED_BLOCKS * 5, dtype=f64, device=dev)
+        self.work = torch.empty(_native.WORK_DOUBLES, dtype=f64, device=dev)
         self.st1 = torch.empty((1, 6), dtype=f64, device=dev)
         self.st2 = torch.empty((1, 4), dtype=f64, device=dev)
         self.prof = torch.empty((max(P, 1), 8), dtype=f64, device=dev)

@@ -194,3 +194,34 @@ def test_acceptance_metric_invariants_and_determinism():
         assert m1.sq_um >= m1.sa_um * (1.0 - 1e-12)
         if m1.sku is not None:
             assert m1.sku >= (m1.ssk ** 2 + 1.0) * (1.0 - 1e-12)
+
+
+def test_reduction_scratch_bound_at_max_blocks():
+    """Every reduction entry point writes at most MSURF_WORK_DOUBLES scratch
+    doubles per surface, even at the block cap (a 2049 x 2049 field uses all
+    MSURF_RED_BLOCKS blocks): a guard region right after the scratch must be
+    untouched (include/msurf.h contract)."""
+    import torch
+
+    from paper_2603_28160_b200 import _native
+
+    lib = _native.lib()
+    dev = torch.device("cuda", 0)
+    rows = cols = 2049
+    rng = np.random.default_rng(3)
+    h = torch.tensor(rng.random(rows * cols) * 0.01, dtype=torch.float64, device=dev)
+    sent = torch.tensor([1.0], dtype=torch.float64, device=dev)
+    guard = 4096
+    work = torch.full((_native.WORK_DOUBLES + guard,), 12345.0, dtype=torch.float64, device=dev)
+    out = torch.zeros(64, dtype=torch.float64, device=dev)
+    coef = torch.tensor([0.0, 0.0, 5.0], dtype=torch.float64, device=dev)
+    sp = _native.stream_ptr()
+    w, o = work.data_ptr(), out.data_ptr()
+    args = (h.data_ptr(), cols, rows * cols, 1, 0, 0, rows, cols, sent.data_ptr(), 1)
+    _native.check(lib.msurf_areal_pass1(*args, w, o, sp))
+    _native.check(lib.msurf_areal_pass2(*args, o, w, o + 6 * 8, sp))
+    _native.check(lib.msurf_areal_plane_pass1(*args, w, o + 16 * 8, sp))
+    _native.check(lib.msurf_areal_plane_pass2(*args, coef.data_ptr(), w, o + 32 * 8, sp))
+    torch.cuda.synchronize()
+    assert bool(torch.all(work[_native.WORK_DOUBLES:] == 12345.0))
+    assert int(out[3].item()) == rows * cols

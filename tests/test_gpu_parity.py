@@ -80,7 +80,7 @@ def test_roughness_vs_reference_goldens(name):
 def test_extended_model_bitexact_vs_ext_oracle(case, trig):
     kw = EXT_CASES[case]
     cfg = _ext_cfg(kw.get("profile", "insert"))
-    res = ms.simulate(cfg, ms.Extensions(**kw), trig=trig)
+    res = ms.simulate(cfg, ms.Extensions(**kw), trig=trig, diagnostics=True)
     h_ref, p, ctr, _ = xorc.ext_sweep(cfg, NS(**kw), workers=4)
     h = res.field.heights
     assert res.trajectory_points == ctr["trajectory_points"]
@@ -147,7 +147,7 @@ def test_no_engagement_and_edge_cases():
     for n_pts, spacing in ((2, 0.3), (33, 0.05), (2500, 0.004)):
         cfg = golden_io.product_config(d, edge_point_count=n_pts, record_trajectory=False,
                                        grid=ms.GridSpec(spacing, -0.2, 0.0, 1 if spacing == 0.3 else 40, 1 if spacing == 0.3 else 30))
-        res = ms.simulate(cfg)
+        res = ms.simulate(cfg, diagnostics=True)
         h_ref, _, ctr, _ = orc.sweep(cfg, workers=2)
         assert np.array_equal(res.field.heights, h_ref)
         assert res.counters["deposits"] == ctr["deposits"]
@@ -194,3 +194,45 @@ def test_rank_strips_assemble_to_whole(world):
         sr = sharded.simulate_strip(cfg, ext, r, world)
         got = sr.heights.cpu().numpy().reshape(cfg.grid.m + 1, sr.j_hi - sr.j_lo + 1)
         assert np.array_equal(got, whole[:, sr.j_lo: sr.j_hi + 1])
+
+
+_FORCE_NEAR_SCRIPT = r"""
+import sys
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import numpy as np
+import golden_io
+import paper_2603_28160_b200 as ms
+from test_host_cpu import EXT_CASES, _ext_cfg
+from types import SimpleNamespace as NS
+from oracle import fsm_ext_oracle as xorc
+for name in ["small_0", "small_1004", "cusp", "runout", "table6_3"]:
+    g = golden_io.load(name)
+    res = ms.simulate(golden_io.product_config(g["config"], record_trajectory=False))
+    assert golden_io.heights_match(g, res.field.heights), name
+for case in ("ball_tilt", "vib_runout"):
+    kw = EXT_CASES[case]
+    cfg = _ext_cfg(kw.get("profile", "insert"))
+    res = ms.simulate(cfg, ms.Extensions(**kw), diagnostics=True)
+    h_ref, _, ctr, _ = xorc.ext_sweep(cfg, NS(**kw), workers=4)
+    assert np.array_equal(res.field.heights, h_ref), case
+    assert res.counters["deposits"] == ctr["deposits"], case
+print("FORCE_NEAR_OK")
+"""
+
+
+def test_deferred_exact_path_bitexact():
+    """libmsurf built with MSURF_FORCE_NEAR routes EVERY point through the
+    deferred exact-index path (the one near-boundary points take): heights
+    must still equal the reference goldens / extended oracle bit-exactly."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "tests", "native", "libmsurf_forcenear.so")
+    if not os.path.exists(lib):
+        pytest.fail("tests/native/libmsurf_forcenear.so missing: run __graft_entry__.build()")
+    env = dict(os.environ, MSURF_LIB=lib)
+    script = _FORCE_NEAR_SCRIPT.format(root=root, tests=os.path.join(root, "tests"))
+    out = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "FORCE_NEAR_OK" in out.stdout, out.stderr[-3000:]

@@ -224,6 +224,15 @@ __device__ __forceinline__ void dedupe(int lane, int idx, bool inside, float zf,
   }
 }
 
+// advance a warp's (group, chunk) unit cursor by kSweepWarps units
+__device__ __forceinline__ void next_unit(int& g, int& q, int nchunk) {
+  q += kSweepWarps;
+  while (q >= nchunk) {
+    q -= nchunk;
+    ++g;
+  }
+}
+
 template <int MODE, bool DIAG>
 __global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
     sweep_kernel(const msurf_job* __restrict__ jobs, int n_jobs,
@@ -432,24 +441,23 @@ __global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
   unsigned long long* __restrict__ keys = reinterpret_cast<unsigned long long*>(J.keys);
   const double tilt_c = J.tilt_c, tilt_s = J.tilt_s, zoff = J.zoff;
   const int groups = (n_live + 31) >> 5;
-  const int units = groups * nchunk;
   unsigned n_dep = 0, n_atom = 0;
 
-  for (int u = warp; u < units; u += kSweepWarps) {
-    const int g = u / nchunk;
-    const int q = u - g * nchunk;
+  // unit = (group g of 32 live steps, chunk q), dealt round-robin to the
+  // warps in (g, q) order; the lane's transform is reloaded only when g
+  // changes, and (g, q) advance without a division
+  int g = warp / nchunk, q = warp - (warp / nchunk) * nchunk;
+  int g_loaded = -1, rt = 0;
+  double r[RW];
+  for (; g < groups; next_unit(g, q, nchunk)) {
     const int slot = g * 32 + lane;
-    bool on = false;
-    double r[RW];
-    if (slot < n_live) {
-      const int rt = live[slot];
-      on = (masks[rt * mask_words + (q >> 6)] >> (q & 63)) & 1ull;
+    if (g != g_loaded) {  // warp-uniform
+      g_loaded = g;
+      rt = slot < n_live ? live[slot] : -1;
 #pragma unroll
-      for (int k = 0; k < RW; ++k) r[k] = rowv[slot * 8 + k];
-    } else {
-#pragma unroll
-      for (int k = 0; k < RW; ++k) r[k] = 0.0;
+      for (int k = 0; k < RW; ++k) r[k] = rt >= 0 ? rowv[slot * 8 + k] : 0.0;
     }
+    const bool on = rt >= 0 && ((masks[rt * mask_words + (q >> 6)] >> (q & 63)) & 1ull);
     if (!__any_sync(0xffffffffu, on)) continue;
     // lanes whose step is not live for this chunk: i index pushed far out of
     // range, so the per-point range test also covers `on`

@@ -160,14 +160,14 @@ struct PointEval {
   int hi_x, hi_y;
   bool near;
   uint64_t key;
-  float zf;
+  unsigned zh;  // high word of the order-preserving key (tilt neighbour compares)
 };
 
 template <int MODE>
 __device__ __forceinline__ PointEval eval_point(const double4 pt, const double* r, double inv, double cx0,
                                                 double cy0, double tilt_c, double tilt_s, double zoff) {
   PointEval e;
-  e.zf = 0.f;
+  e.zh = 0u;
   if (MODE == MSURF_MODE_REF) {
     // engine.py:289-296: xw = ((m00*xp + m01*yp) + m02*zp) + m03
     e.xw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r[0], pt.x), __dmul_rn(r[1], pt.y)), __dmul_rn(r[2], pt.z)),
@@ -185,7 +185,7 @@ __device__ __forceinline__ PointEval eval_point(const double4 pt, const double* 
       const double zz = __dadd_rn(__dadd_rn(__dmul_rn(tilt_s, vv), pt.w), zoff);
       e.yw = __dadd_rn(yv, r[3]);
       e.key = enc_key_raw(zz);  // zz = (..) + zoff with zoff != -0 (host-canonical): never -0
-      e.zf = __double2float_rn(zz);
+      e.zh = (unsigned)(e.key >> 32);
     } else {
       e.yw = __dadd_rn(vv, r[3]);
       e.key = (uint64_t)__double_as_longlong(pt.z);
@@ -207,20 +207,21 @@ __device__ __forceinline__ PointEval eval_point(const double4 pt, const double* 
 // minimum deposits. Constant z' (REF/EXT): the run's first lane. Tilt: lanes
 // that are a local minimum (< predecessor, <= successor).
 template <int MODE>
-__device__ __forceinline__ void dedupe(int lane, int idx, bool inside, float zf, bool& dep) {
+__device__ __forceinline__ void dedupe(int lane, int idx, bool inside, unsigned zh, bool& dep) {
   const int idx_prev = __shfl_up_sync(0xffffffffu, idx, 1);
-  dep = inside & ((lane == 0) | (idx != idx_prev));
   if (MODE == MSURF_MODE_EXT_TILT) {
-    // compare float32 roundings of z': rounding is monotone, so
-    // zf > zf_neighbour proves z' > z'_neighbour; a lane is skipped only
-    // when a same-cell neighbour is provably lower, and every chain of
-    // skips ends at a deposited lane whose z' is lower still (ties in
-    // float keep both deposits) -> 32-bit shuffles instead of 64-bit
-    const float zf_prev = __shfl_up_sync(0xffffffffu, zf, 1);
-    dep = inside & !((lane > 0) & (idx == idx_prev) & (zf > zf_prev));
+    // Compare the high words of the order-preserving keys: zh > zh_neighbour
+    // proves z' > z'_neighbour, so a lane is skipped only when a same-cell
+    // neighbour is provably lower, and every chain of skips ends at a
+    // deposited lane whose z' is lower still (equal high words keep both
+    // deposits). Lane 0 / lane 31 get their own values back from the edge
+    // shuffles, which never skip: no lane test needed.
+    const unsigned zh_prev = __shfl_up_sync(0xffffffffu, zh, 1);
     const int idx_next = __shfl_down_sync(0xffffffffu, idx, 1);
-    const float zf_next = __shfl_down_sync(0xffffffffu, zf, 1);
-    dep &= !((lane < 31) & (idx == idx_next) & (zf > zf_next));
+    const unsigned zh_next = __shfl_down_sync(0xffffffffu, zh, 1);
+    dep = inside & !((idx == idx_prev) & (zh > zh_prev)) & !((idx == idx_next) & (zh > zh_next));
+  } else {
+    dep = inside & ((lane == 0) | (idx != idx_prev));
   }
 }
 
@@ -242,6 +243,7 @@ __global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
   double* rowv = reinterpret_cast<double*>(smem_raw);                        // [T][8] by live slot
   uint64_t* masks = reinterpret_cast<uint64_t*>(rowv + kTileSteps * 8);      // [T][W] by thread
   int* live = reinterpret_cast<int*>(masks + kTileSteps * mask_words);       // [T] slot -> thread
+  float4* ccf = reinterpret_cast<float4*>(live + kTileSteps);                // [nchunk] xc yc rx ry (f32)
   __shared__ msurf_job J;
   __shared__ int warp_cnt[kSweepWarps];
   __shared__ unsigned warp_eval[kSweepWarps];
@@ -280,6 +282,24 @@ __global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
   const int nchunk = (npts + 31) >> 5;
   const double dd = J.spacing;
   const double4* __restrict__ pts = reinterpret_cast<const double4*>(J.pts) + (long long)tooth * npts;
+
+  // fp32 copy of this tooth's chunk cull records for phase 1, and the bound
+  // Rt >= |xc| + |yc| + |yz| of every chunk (from the whole-tooth box)
+  {
+    const double* cc = J.chunk_circ + (long long)tooth * nchunk * 6;
+    float* czw = reinterpret_cast<float*>(ccf + nchunk);
+    for (int qq = tid; qq < nchunk; qq += kSweepThreads) {
+      const double* c6 = cc + qq * 6;
+      ccf[qq] = make_float4((float)c6[0], (float)c6[1], (float)c6[2], (float)c6[3]);
+      czw[qq] = (float)c6[4];
+    }
+  }
+  __syncthreads();
+  float rt_f;
+  {
+    const double* b = J.tooth_box + tooth * 6;
+    rt_f = (float)(fmax(fabs(b[0]), fabs(b[1])) + fmax(fabs(b[2]), fabs(b[3])) + fmax(fabs(b[4]), fabs(b[5])));
+  }
 
   // ---------------- phase 1: one thread per time step of the tile
   bool any = false, engaged = false;
@@ -366,18 +386,27 @@ __global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
         if (engaged) {
           // per-chunk bounding circles: x = c*xc + s*yc + xoff +- rx,
           // y = cos(tau)*(c*yc - s*xc) + yz + ty +- ry, against the window
-          // (centre, half-width) widened by 1.5 cells
+          // (centre, half-width) widened by 1.5 cells. Evaluated in fp32 (the
+          // fp64 pipe is the sweep's bottleneck): every term is bounded by
+          // S = |xc| + |yc| + |yz| + |offset| <= Rt + |offset|, the fp32 result
+          // is within ~8 ulp(S) < 1e-6 S of the exact one, and the test is
+          // widened by 4e-6 S + 1e-6 mm, so it stays a superset of the exact
+          // cull (a false positive costs work, never a result).
           const double wxc = 0.5 * (wx_lo + wx_hi), wxh = 0.5 * (wx_hi - wx_lo);
           const double wyc = 0.5 * (wy_lo + wy_hi), wyh = 0.5 * (wy_hi - wy_lo);
           const double ox = xoff - wxc, oy = ty - wyc;
-          const double tcv = MODE == MSURF_MODE_EXT_TILT ? J.tilt_c : 1.0;
-          const double2* circ = reinterpret_cast<const double2*>(J.chunk_circ) + (long long)tooth * nchunk * 3;
+          const float cf = (float)c, sf = (float)sn;
+          const float oxf = (float)ox, oyf = (float)oy;
+          const float tcf = MODE == MSURF_MODE_EXT_TILT ? (float)J.tilt_c : 1.0f;
+          const float hx = (float)wxh + (4e-6f * (rt_f + fabsf(oxf)) + 1e-6f);
+          const float hy = (float)wyh + (4e-6f * (rt_f + fabsf(oyf)) + 1e-6f);
+          const float* cz = reinterpret_cast<const float*>(ccf + nchunk);
           unsigned kept = 0;
           for (int q = 0; q < nchunk; ++q) {
-            const double2 a = circ[q * 3 + 0], b = circ[q * 3 + 1], z = circ[q * 3 + 2];
-            const double uc = c * a.x + sn * a.y;
-            const double vc = c * a.y - sn * a.x;
-            const bool hit = (fabs(uc + ox) <= wxh + b.x) & (fabs(tcv * vc + z.x + oy) <= wyh + b.y);
+            const float4 a = ccf[q];
+            const float uc = fmaf(cf, a.x, sf * a.y);
+            const float vc = fmaf(cf, a.y, -(sf * a.x));
+            const bool hit = (fabsf(uc + oxf) <= hx + a.z) & (fabsf(fmaf(tcf, vc, cz[q]) + oyf) <= hy + a.w);
             if (hit) {
               my_mask[q >> 6] |= 1ull << (q & 63);
               kept += (q == nchunk - 1) ? (unsigned)(npts - 32 * q) : 32u;
@@ -497,8 +526,8 @@ __global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
       const int idx_a = in_a ? ia * ldk + ja : -1;
       const int idx_b = in_b ? ib * ldk + jb : -1;
       bool dep_a, dep_b;
-      dedupe<MODE>(lane, idx_a, in_a, ea.zf, dep_a);
-      dedupe<MODE>(lane, idx_b, in_b, eb.zf, dep_b);
+      dedupe<MODE>(lane, idx_a, in_a, ea.zh, dep_a);
+      dedupe<MODE>(lane, idx_b, in_b, eb.zh, dep_b);
       if (DIAG) {
         n_dep += (unsigned)in_a + (unsigned)in_b;
         n_atom += (unsigned)dep_a + (unsigned)dep_b;
@@ -1014,7 +1043,8 @@ int msurf_sweep(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile_prefi
   const int nchunk = (max_points + 31) / 32;
   const int mask_words = (nchunk + 63) / 64;
   const size_t smem = (size_t)kTileSteps * 8 * sizeof(double) +
-                      (size_t)kTileSteps * mask_words * sizeof(uint64_t) + (size_t)kTileSteps * sizeof(int);
+                      (size_t)kTileSteps * mask_words * sizeof(uint64_t) + (size_t)kTileSteps * sizeof(int) +
+                      (size_t)nchunk * (sizeof(float4) + sizeof(float));
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
   const bool diag = (mode & MSURF_SWEEP_DIAG) != 0;

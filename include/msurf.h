@@ -162,6 +162,19 @@ int msurf_profiles(const double* h, int64_t surf_stride, int32_t n_surf,
                    const double* sentinel, int32_t exclude_uncut, const double* stats_in,
                    double* out, void* stream);
 
+/* Graymap export (surface_io.py:100-131, write_graymap) of one fp64 height
+ * field (row pitch ld) over the ROI rows [i_lo, i_lo+rows) x cols
+ * [j_lo, j_lo+cols). msurf_graymap_range: out3 = (max, min, n) of the
+ * machined cells (height < sentinel[0]) in mm; work: MSURF_WORK_DOUBLES.
+ * msurf_graymap_pixels: pixels[j * rows + i] (image row = y node, column = x
+ * node) = big-endian u16 of rint((z - min) * (65535 / (max - min))) for
+ * machined cells, 32768 when max == min, 0 for uncut cells; range3 = out3 of
+ * the range pass (device). The caller raises DomainError when n == 0. */
+int msurf_graymap_range(const double* h, int64_t ld, int64_t i_lo, int64_t j_lo, int64_t rows, int64_t cols,
+                        const double* sentinel, double* work, double* out3, void* stream);
+int msurf_graymap_pixels(const double* h, int64_t ld, int64_t i_lo, int64_t j_lo, int64_t rows, int64_t cols,
+                         const double* sentinel, const double* range3, uint16_t* pixels, void* stream);
+
 /* Microbenchmarks for the roofline denominators (not in MEASURED_PEAKS.json):
  * which=0: non-FMA DADD/DMUL issue (ops/s), which=1: DFMA (FMA/s),
  * which=2: 64-bit atomicMin (RED.MIN.64) to random L2-resident addresses

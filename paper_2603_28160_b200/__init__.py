@@ -21,12 +21,16 @@ from .engine import (BenchmarkReport, BenchmarkRow, SimulationConfig, Simulation
                      simulate, simulate_batch, simulate_reference, time_step)
 from .roughness import (ArealMetrics, LineProfile, ProfileRoughness, areal_metrics, areal_metrics_batch,
                         extract_profile, line_roughness, profile_roughness)
-from .dataset import ParameterRange, generate_batch, lhs_sample, uniform_sample
+from .dataset import DatasetManifest, ParameterRange, generate_batch, generate_dataset, lhs_sample, uniform_sample
+from .config import ConfigDocument, config_from_dict, parse_config, serialize_config
+from .surface_io import export_views, read_surface, write_surface
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "ArealMetrics", "BenchmarkReport", "BenchmarkRow", "ConfigError", "CuttingEdgePoint", "DomainError",
+    "ArealMetrics", "BenchmarkReport", "BenchmarkRow", "ConfigDocument", "ConfigError", "CuttingEdgePoint",
+    "DatasetManifest", "DomainError", "config_from_dict", "export_views", "generate_dataset", "parse_config",
+    "read_surface", "serialize_config", "write_surface",
     "EdgeDiscretization", "Extensions", "GridSpec", "HeightField", "LineProfile", "MillsurfError",
     "NativeUnavailableError", "ParameterRange", "ProcessParameters", "ProfileRoughness",
     "SimulationConfig", "SimulationResult", "SurfaceFormatError", "ToolDefinition", "TrajectoryRecord",

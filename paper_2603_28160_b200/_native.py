@@ -69,6 +69,10 @@ EXPORTS = {
                                                c_void_p, c_void_p]),
     "msurf_profiles": (ctypes.c_int, [c_void_p, c_int64, c_int32, c_void_p, c_int32, c_int64,
                                       c_int64, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
+    "msurf_graymap_range": (ctypes.c_int, [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,
+                                           c_void_p, c_void_p, c_void_p]),
+    "msurf_graymap_pixels": (ctypes.c_int, [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,
+                                            c_void_p, c_void_p, c_void_p]),
     "msurf_microbench": (ctypes.c_int, [c_int32, ctypes.POINTER(c_double)]),
 }
 

@@ -992,6 +992,70 @@ __global__ void mb_fma_kernel(double* out, int iters, double a, double b) {
   if (s == 12345.678) out[0] = s;
 }
 
+// ------------------------------------------------------------ graymap export
+// surface_io.py:100-131 (write_graymap): range pass over the machined cells of
+// the ROI in mm -> partials [max, min, n_machined] per block
+__global__ void __launch_bounds__(kThreads)
+    graymap_range_kernel(const double* __restrict__ h, long long ld, long long i_lo, long long j_lo,
+                         long long rows, long long cols, const double* __restrict__ sent,
+                         double* __restrict__ work) {
+  __shared__ double sh[kWarps * 3];
+  const double sentinel = sent[0];
+  double v[3] = {-INFINITY, INFINITY, 0.0};
+  const int kind[3] = {1, 2, 0};
+  const long long r0 = rows * blockIdx.x / gridDim.x, r1 = rows * (blockIdx.x + 1) / gridDim.x;
+  for (long long r = r0; r < r1; ++r) {
+    const double* row = h + (i_lo + r) * ld + j_lo;
+    for (long long c = threadIdx.x; c < cols; c += blockDim.x) {
+      const double hv = row[c];
+      if (hv < sentinel) {
+        v[0] = fmax(v[0], hv);
+        v[1] = fmin(v[1], hv);
+        v[2] += 1.0;
+      }
+    }
+  }
+  block_reduce<3>(v, kind, sh);
+  if (threadIdx.x == 0) {
+    double* o = work + (long long)blockIdx.x * 3;
+    o[0] = v[0]; o[1] = v[1]; o[2] = v[2];
+  }
+}
+
+// pixels: machined -> rint((z - z_lo) * (65535 / (z_hi - z_lo))) (mid-gray when
+// z_hi == z_lo), uncut -> 0; image row = y node j, column = x node i, 16-bit
+// big-endian. 32x32 node tiles transposed through shared memory so both the
+// fp64 reads (along j) and the u16 writes (along i) are coalesced.
+__global__ void __launch_bounds__(256)
+    graymap_pixels_kernel(const double* __restrict__ h, long long ld, long long i_lo, long long j_lo,
+                          long long rows, long long cols, const double* __restrict__ sent,
+                          const double* __restrict__ range3, unsigned short* __restrict__ pix) {
+  __shared__ unsigned short tile[32][33];
+  const double sentinel = sent[0];
+  const double z_hi = range3[0], z_lo = range3[1];
+  const bool flat = !(z_hi > z_lo);
+  const double scale = flat ? 0.0 : __ddiv_rn(65535.0, __dsub_rn(z_hi, z_lo));
+  const long long ti = (long long)blockIdx.y * 32, tj = (long long)blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int a = ty; a < 32; a += 8) {  // a = i offset in tile, tx = j offset
+    const long long i = ti + a, j = tj + tx;
+    unsigned short p = 0;
+    if (i < rows && j < cols) {
+      const double hv = h[(i_lo + i) * ld + j_lo + j];
+      if (hv < sentinel) p = flat ? (unsigned short)32768 : (unsigned short)rint(__dmul_rn(__dsub_rn(hv, z_lo), scale));
+    }
+    tile[a][tx] = p;
+  }
+  __syncthreads();
+  for (int b = ty; b < 32; b += 8) {  // b = j offset (image row), tx = i offset (column)
+    const long long j = tj + b, i = ti + tx;
+    if (i < rows && j < cols) {
+      const unsigned short p = tile[tx][b];
+      pix[j * rows + i] = (unsigned short)((p >> 8) | (p << 8));
+    }
+  }
+}
+
 __global__ void mb_atomic_kernel(unsigned long long* buf, long long mask, int iters) {
   unsigned long long x = (blockIdx.x * 1315423911ull) ^ (threadIdx.x * 2654435761ull) ^ 0x9e3779b97f4a7c15ull;
   for (int i = 0; i < iters; ++i) {
@@ -1163,6 +1227,29 @@ int msurf_profiles(const double* h, int64_t surf_stride, int32_t n_surf, const i
       h, surf_stride, reinterpret_cast<const long long*>(start), n_prof, len, stride, sentinel,
       exclude_uncut, stats_in, out);
   return check_launch("profiles_kernel");
+}
+
+int msurf_graymap_range(const double* h, int64_t ld, int64_t i_lo, int64_t j_lo, int64_t rows, int64_t cols,
+                        const double* sentinel, double* work, double* out3, void* stream) {
+  if (!h || !sentinel || !work || !out3 || rows < 1 || cols < 1 || i_lo < 0 || j_lo < 0 || ld < cols)
+    return set_err("msurf_graymap_range: bad arguments");
+  const int nb = red_blocks(rows, cols);
+  cudaStream_t st = (cudaStream_t)stream;
+  graymap_range_kernel<<<nb, kThreads, 0, st>>>(h, ld, i_lo, j_lo, rows, cols, sentinel, work);
+  if (check_launch("graymap_range_kernel")) return 1;
+  finalize_kernel<3><<<1, kThreads, 0, st>>>(work, nb, 1u | (2u << 2), out3);
+  return check_launch("finalize_kernel<3>");
+}
+
+int msurf_graymap_pixels(const double* h, int64_t ld, int64_t i_lo, int64_t j_lo, int64_t rows, int64_t cols,
+                         const double* sentinel, const double* range3, uint16_t* pixels, void* stream) {
+  if (!h || !sentinel || !range3 || !pixels || rows < 1 || cols < 1 || i_lo < 0 || j_lo < 0 || ld < cols)
+    return set_err("msurf_graymap_pixels: bad arguments");
+  if ((rows + 31) / 32 > 65535) return set_err("msurf_graymap_pixels: roi too tall");
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  graymap_pixels_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(h, ld, i_lo, j_lo, rows, cols, sentinel, range3,
+                                                               reinterpret_cast<unsigned short*>(pixels));
+  return check_launch("graymap_pixels_kernel");
 }
 
 int msurf_microbench(int32_t which, double* result) {

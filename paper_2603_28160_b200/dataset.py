@@ -13,6 +13,7 @@ configuration is invalid is reported per row without aborting the batch
 
 from __future__ import annotations
 
+import json
 import math
 from dataclasses import dataclass, replace
 
@@ -216,3 +217,172 @@ def generate_batch(base_config, base_ext: Extensions | None, ranges, count: int,
     if not keep_fields:
         results = []
     return BatchResult(samples=samples, rows=rows, results=results, device_seconds=dev_s)
+
+
+# ---------------------------------------------------------------- datasets
+SCHEMA_VERSION = 1                      # dataset.py:31
+RNG_NAME = "numpy-default-pcg64"        # dataset.py:32
+# reference parameter -> (config block, key, keys cleared with it) (dataset.py:37-48)
+_RAW_PATHS = {
+    "cutting_speed_m_min": ("process", "cutting_speed_m_min", ("spindle_speed_rpm",)),
+    "spindle_speed_rpm": ("process", "spindle_speed_rpm", ("cutting_speed_m_min",)),
+    "feed_per_tooth_mm": ("process", "feed_per_tooth_mm", ("feed_speed_mm_min",)),
+    "depth_of_cut_mm": ("process", "depth_of_cut_mm", ()),
+    "phase_deg": ("process", "phase_deg", ("phase_rad",)),
+    "grid_spacing_mm": ("grid", "spacing_mm", ()),
+    "radial_rake_deg": ("tool", "radial_rake_deg", ("radial_rake_rad",)),
+    "axial_rake_deg": ("tool", "axial_rake_deg", ("axial_rake_rad",)),
+    # extended-model parameters land in the optional ``extensions`` block
+    "runout_offset_mm": ("extensions", "runout_offset_mm", ()),
+    "runout_phase_rad": ("extensions", "runout_phase_rad", ()),
+    "helix_angle_rad": ("extensions", "helix_angle_rad", ()),
+    "tilt_rad": ("extensions", "tilt_rad", ()),
+    "vib_amplitude_mm": ("extensions", "vib_amplitude_mm", ()),
+}
+_RUNOUT_NAMES = ("runout_radial_mm", "runout_axial_mm")
+# surfaces swept per launch group: bounds the HBM held by one group of Z-maps
+DATASET_NODE_BUDGET = int(2.5e8)
+
+
+@dataclass
+class DatasetManifest:
+    """dataset.py:83-88."""
+
+    seed: int
+    count: int
+    rows: list
+    path: object
+
+
+def apply_overrides(base_raw: dict, names, values) -> dict:
+    """Sampled values into a copy of the raw JSON config (dataset.py:108-136):
+    sibling keys of a pair are cleared, run-outs rewrite every tooth's pair."""
+    import copy
+
+    raw = copy.deepcopy(base_raw)
+    runout = {}
+    for name, value in zip(names, values):
+        value = float(value)
+        if name in _RUNOUT_NAMES:
+            runout[name] = value
+            continue
+        if name == "helix_angle_deg":
+            name, value = "helix_angle_rad", math.radians(value)
+        block, key, clears = _RAW_PATHS[name]
+        blk = raw.setdefault(block, {})
+        blk[key] = value
+        for c in clears:
+            blk.pop(c, None)
+    if runout:
+        tool = raw.setdefault("tool", {})
+        pairs = tool.get("runouts_mm") or [[0.0, 0.0] for _ in range(tool.get("tooth_count", 1))]
+        r = runout.get("runout_radial_mm")
+        a = runout.get("runout_axial_mm")
+        tool["runouts_mm"] = [[r if r is not None else p[0], a if a is not None else p[1]] for p in pairs]
+    return raw
+
+
+def _check_ranges_against_base(ranges, base_raw: dict) -> None:
+    """dataset.py:139-152."""
+    radius = base_raw.get("tool", {}).get("insert_radius_mm")
+    if not isinstance(radius, (int, float)):
+        return
+    for prm in ranges:
+        if prm.name == "depth_of_cut_mm" and prm.high > radius:
+            raise ConfigError(f"range for depth_of_cut_mm: high {prm.high} exceeds insert radius {radius}")
+        if prm.name in _RUNOUT_NAMES and max(abs(prm.low), abs(prm.high)) >= radius:
+            raise ConfigError(f"range for {prm.name}: magnitude must stay below insert radius {radius}")
+
+
+def _new_row(index: int, params: dict) -> dict:
+    # key order of dataset.py:156-165 (the manifest bytes depend on it)
+    return {"index": index, "params": params, "surface_file": f"sample_{index:05d}.srtf", "status": "ok",
+            "error": None, "metrics": None, "metrics_error": None, "counters": None}
+
+
+def _fail(row: dict, exc: Exception) -> None:
+    row["status"], row["error"], row["surface_file"] = "failed", str(exc), None
+
+
+def generate_dataset(ranges, count: int, seed: int, base_raw: dict, out_dir, workers: int = 1,
+                     *, node_budget: int = DATASET_NODE_BUDGET) -> DatasetManifest:
+    """LHS-sampled surfaces + SRTF files + JSON-lines manifest
+    (dataset.py:188-241), with every parameter set of a launch group swept
+    in ONE batched sweep launch and reduced in one batched metrics launch;
+    each surface streams from HBM into its SRTF file. ``workers`` is accepted
+    for compatibility (the result never depends on it, as in the reference).
+    A failing sample is recorded in place and does not abort the batch."""
+    from pathlib import Path
+
+    from .config import config_from_dict
+    from .engine import _launch_results
+    from .planner import plan as make_plan
+    from .roughness import areal_metrics_batch
+    from .surface_io import write_surface
+
+    config_from_dict(base_raw)  # fail fast on a broken base configuration
+    _check_ranges_against_base(ranges, base_raw)
+    samples = lhs_sample(ranges, count, seed)
+    names = [p.name for p in ranges]
+    out_dir = Path(out_dir)
+    out_dir.mkdir(parents=True, exist_ok=True)
+    manifest_path = out_dir / "manifest.jsonl"
+    header = {"schema_version": SCHEMA_VERSION, "seed": seed, "count": count, "rng": RNG_NAME,
+              "ranges": [{"name": p.name, "low": p.low, "high": p.high} for p in ranges],
+              "base_config": base_raw}
+
+    rows, planned = [], []
+    for i in range(count):
+        row = _new_row(i, {n: float(samples[i, d]) for d, n in enumerate(names)})
+        rows.append(row)
+        try:
+            doc = config_from_dict(apply_overrides(base_raw, names, samples[i]))
+            cfg = replace(doc.to_simulation_config(), worker_count=1, record_trajectory=False)
+            planned.append((row, make_plan(cfg, doc.extensions)))
+        except MillsurfError as exc:
+            _fail(row, exc)
+
+    # launch groups under the node budget; results are consumed group by group
+    groups, cur, nodes = [], [], 0
+    for item in planned:
+        k = item[1].grid.node_count
+        if cur and nodes + k > node_budget:
+            groups.append(cur)
+            cur, nodes = [], 0
+        cur.append(item)
+        nodes += k
+    if cur:
+        groups.append(cur)
+    # the manifest is appended in index order as groups complete (header first,
+    # one row per sample, flushed: a partial run leaves a valid prefix)
+    with open(manifest_path, "w", encoding="utf-8") as fh:
+        fh.write(json.dumps(header) + "\n")
+        fh.flush()
+        done = 0
+
+        def emit(upto):
+            nonlocal done
+            for row in rows[done:upto]:
+                fh.write(json.dumps(row) + "\n")
+            fh.flush()
+            done = max(done, upto)
+
+        for g_idx, grp in enumerate(groups):
+            results = _launch_results([p for _, p in grp], "device")
+            mets = areal_metrics_batch([r.field for r in results])
+            for (row, _), res, met in zip(grp, results, mets):
+                try:
+                    write_surface(res.field, out_dir / row["surface_file"])
+                except MillsurfError as exc:
+                    _fail(row, exc)
+                    continue
+                row["counters"] = {"time_steps": res.time_steps, "trajectory_points": res.trajectory_points,
+                                   "cells_updated": res.cells_updated}
+                if isinstance(met, MillsurfError):
+                    row["metrics_error"] = str(met)
+                else:
+                    row["metrics"] = met.to_json_dict()
+            nxt = groups[g_idx + 1][0][0]["index"] if g_idx + 1 < len(groups) else count
+            emit(nxt)
+        emit(count)
+    return DatasetManifest(seed=seed, count=count, rows=rows, path=manifest_path)

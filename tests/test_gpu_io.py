@@ -107,7 +107,9 @@ def _rows_match(mine, ref):
 def test_generate_dataset_matches_reference(run, tmp_path):
     g = GOLD["datasets"][run]
     ranges = [ms.ParameterRange(*r) for r in g["ranges"]]
-    man = ms.generate_dataset(ranges, g["count"], seed=g["seed"], base_raw=g["base_raw"], out_dir=tmp_path)
+    # the base config in the reference's own key order (the fixture file is key-sorted)
+    base = json.loads(g["manifest"].split("\n")[0])["base_config"]
+    man = ms.generate_dataset(ranges, g["count"], seed=g["seed"], base_raw=base, out_dir=tmp_path)
     text = (tmp_path / "manifest.jsonl").read_text()
     mine = [json.loads(x) for x in text.strip().split("\n")]
     ref = [json.loads(x) for x in g["manifest"].strip().split("\n")]
@@ -120,5 +122,5 @@ def test_generate_dataset_matches_reference(run, tmp_path):
     assert sorted(p.name for p in tmp_path.glob("*.srtf")) == sorted(g["surfaces"])
     # metrics-free fields byte-identical: rerun gives the same manifest bytes
     tmp2 = tmp_path / "again"
-    ms.generate_dataset(ranges, g["count"], seed=g["seed"], base_raw=g["base_raw"], out_dir=tmp2, node_budget=1)
+    ms.generate_dataset(ranges, g["count"], seed=g["seed"], base_raw=base, out_dir=tmp2, node_budget=1)
     assert (tmp2 / "manifest.jsonl").read_text() == text

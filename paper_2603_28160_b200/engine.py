@@ -379,7 +379,11 @@ def simulate(config: SimulationConfig, extensions: Extensions | None = None, *,
     rounded double-double sincos — the parity mode. ``diagnostics=True``
     also counts deposits and atomics (``result.counters``)."""
     p = plan(config, extensions)
-    return _launch_results([p], trig, diagnostics)[0]
+    res = _launch_results([p], trig, diagnostics)[0]
+    # the reference returns host heights: start their D2H now, it overlaps
+    # the caller's next launches (areal_metrics etc. run on the device copy)
+    res.field.prefetch_host()
+    return res
 
 
 def _launch_results(plans, trig, diagnostics=False):

@@ -248,6 +248,24 @@ def run_reference_batch(args):
 
 
 # ---------------------------------------------------------------- GPU leg
+def roofline_terms(flops, fp64_peak, atomics, atom_peaks, sweep_ms):
+    """The north star's roofline = the slower of fp64 issue and atomic
+    traffic: the time each resource needs at its measured peak, against the
+    measured sweep time. The RED.MIN peak depends on the access shape, so it
+    is bracketed by two microbenchmarks: random addresses in an L2-resident
+    32 MiB table (a lower bound on the sweep's peak, whose REDs cluster) and
+    one 256-byte run of keys per warp instruction (an upper bound)."""
+    t = sweep_ms * 1e-3
+    t_fp64 = flops / fp64_peak
+    t_red_lo, t_red_hi = atomics / atom_peaks[4], atomics / atom_peaks[3]
+    return {"t_sweep_ms": sweep_ms, "t_fp64_ms": t_fp64 * 1e3,
+            "t_red_ms": [t_red_lo * 1e3, t_red_hi * 1e3],
+            "red_peak_per_s": {"warp_run_32MiB": atom_peaks[4], "random_32MiB": atom_peaks[3]},
+            "red_achieved_per_s": atomics / t,
+            "frac_fp64": t_fp64 / t, "frac_red": [t_red_lo / t, t_red_hi / t],
+            "binding": "fp64" if t_fp64 >= t_red_hi else ("red" if t_red_lo >= t_fp64 else "fp64 or red")}
+
+
 def diag_counters(batch):
     """Per-point diagnostics (deposits, atomics) from one extra UNTIMED launch
     of the counting sweep variant (MSURF_SWEEP_DIAG); the timed steps run the
@@ -355,8 +373,10 @@ def run_ours(args, rank, world):
     r = ctypes.c_double(0.0)
     _native.check(lib.msurf_microbench(0, ctypes.byref(r)))
     fp64_peak = r.value
-    _native.check(lib.msurf_microbench(2, ctypes.byref(r)))
-    atom_peak = r.value
+    atom = {}
+    for w in (3, 4):
+        _native.check(lib.msurf_microbench(w, ctypes.byref(r)))
+        atom[w] = r.value
     achieved = flops / (sweep_ms_avg * 1e-3)
     roofline = {
         "bound": "fp64", "achieved": achieved / 1e12, "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
@@ -374,8 +394,7 @@ def run_ours(args, rank, world):
         "atomics": int(dctr[0][3]),
         "diag_note": "deposits/atomics from one extra untimed launch with MSURF_SWEEP_DIAG",
         "atomic_rate_per_s": int(dctr[0][3]) / (sweep_ms_avg * 1e-3),
-        "atomic_random_rate_per_s": atom_peak,
-        "atomic_note": "msurf_microbench(2): random-address RED.MIN rate; the sweep's REDs have locality",
+        "terms": roofline_terms(flops, fp64_peak, int(dctr[0][3]), atom, sweep_ms_avg),
         "hbm": {"bytes_per_step": 24 * (p.grid.m + 1) * (j_hi - j_lo + 1) + 8 * int(dctr[0][3]),
                 "peak_gbs": measured_peaks().get("hbm_gbs")},
     }
@@ -521,6 +540,10 @@ def run_batch(args, rank, world):
     _native.check(lib.msurf_microbench(0, ctypes.byref(r)))
     fp64_peak = r.value
     achieved = flops / (sweep_avg * 1e-3)
+    atom = {}
+    for w in (3, 4):
+        _native.check(lib.msurf_microbench(w, ctypes.byref(r)))
+        atom[w] = r.value
     roofline = {"bound": "fp64", "achieved": achieved / 1e12, "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
                 "frac": achieved / fp64_peak, "traffic": profiled_traffic(meta["name"]),
                 "kernel": "sweep_kernel<MODE>", "sweep_ms": sweep_avg,
@@ -528,7 +551,8 @@ def run_batch(args, rank, world):
                 "flops_per_launch": flops, "survey_def": {"frac": flops_survey / (sweep_avg * 1e-3) / fp64_peak},
                 "points_evaluated": evald, "live_rows": live, "deposits": int(dctr[:, 2].sum()),
                 "atomics": int(dctr[:, 3].sum()),
-                "diag_note": "deposits/atomics from one extra untimed launch with MSURF_SWEEP_DIAG"}
+                "diag_note": "deposits/atomics from one extra untimed launch with MSURF_SWEEP_DIAG",
+                "terms": roofline_terms(flops, fp64_peak, int(dctr[:, 3].sum()), atom, sweep_avg)}
     # e2e: public batched API with host planning, one H2D, metrics + every height map read back
     e2e_ms = []
     d2h = 0

@@ -177,7 +177,10 @@ int msurf_graymap_pixels(const double* h, int64_t ld, int64_t i_lo, int64_t j_lo
 
 /* Microbenchmarks for the roofline denominators (not in MEASURED_PEAKS.json):
  * which=0: non-FMA DADD/DMUL issue (ops/s), which=1: DFMA (FMA/s),
- * which=2: 64-bit atomicMin (RED.MIN.64) to random L2-resident addresses
+ * which=2: 64-bit atomicMin (RED.MIN.64) to random addresses in a 128 MiB
+ * table (~L2 size), which=3: the same in a 32 MiB (L2-resident) table,
+ * which=4: RED.MIN.64 where each warp instruction covers one 256-byte run of
+ * consecutive keys at a random base in 32 MiB (the sweep's access shape)
  * (ops/s). Synchronous; creates and destroys its own scratch. */
 int msurf_microbench(int32_t which, double* result);
 

@@ -1056,6 +1056,18 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// RED.MIN.64 peak with the sweep's access shape: each warp instruction covers
+// 32 lanes on consecutive keys (one 256-byte run) at a random warp-uniform
+// base inside an L2-resident table
+__global__ void mb_atomic_run_kernel(unsigned long long* buf, long long mask, int iters) {
+  unsigned long long x = (blockIdx.x * 1315423911ull) ^ ((threadIdx.x >> 5) * 2654435761ull) ^ 0x9e3779b97f4a7c15ull;
+  const int lane = threadIdx.x & 31;
+  for (int i = 0; i < iters; ++i) {
+    x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+    red_min_u64(buf + (((x & mask) & ~31ull) + lane), x >> 1);
+  }
+}
+
 __global__ void mb_atomic_kernel(unsigned long long* buf, long long mask, int iters) {
   unsigned long long x = (blockIdx.x * 1315423911ull) ^ (threadIdx.x * 2654435761ull) ^ 0x9e3779b97f4a7c15ull;
   for (int i = 0; i < iters; ++i) {
@@ -1276,15 +1288,18 @@ int msurf_microbench(int32_t which, double* result) {
     cudaFree(out);
     const double ops = (double)blocks * threads * iters * 8.0 * (which == 0 ? 2.0 : 1.0);
     *result = ops / (ms * 1e-3);
-  } else if (which == 2) {
+  } else if (which == 2 || which == 3 || which == 4) {
     unsigned long long* buf = nullptr;
-    const long long n = 1ll << 24;  // 128 MiB of keys: L2-sized working set
+    // 2: 128 MiB of keys (about the L2 size); 3, 4: 32 MiB (L2-resident, the
+    // size of one sweep job's Z-map slab)
+    const long long n = which == 2 ? (1ll << 24) : (1ll << 22);
     if (cudaMalloc(&buf, n * 8) != cudaSuccess) return set_err("microbench: cudaMalloc");
     cudaMemset(buf, 0xff, n * 8);
     const int blocks = sms * 8, threads = 256, iters = 256;
-    for (int rep = 0; rep < 2; ++rep) {
+    for (int rep = 0; rep < 3; ++rep) {
       cudaEventRecord(a);
-      mb_atomic_kernel<<<blocks, threads>>>(buf, n - 1, iters);
+      if (which == 4) mb_atomic_run_kernel<<<blocks, threads>>>(buf, n - 1, iters);
+      else mb_atomic_kernel<<<blocks, threads>>>(buf, n - 1, iters);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
     }

@@ -131,8 +131,6 @@ class Arena:
     """Packs many small host arrays into one pinned staging buffer and one
     device buffer, so a sweep's inputs cross PCIe in a single H2D copy."""
 
-    _pinned = {}
-
     def __init__(self):
         self._parts = []
         self.size = 0
@@ -150,19 +148,6 @@ class Arena:
         self.size = off + nbytes
         return off
 
-    @classmethod
-    def _staging(cls, nbytes: int, device):
-        import torch
-
-        key = device.index if device.index is not None else 0
-        ent = cls._pinned.get(key)
-        if ent is None or ent[0].numel() < nbytes:
-            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
-            ent = (buf, torch.cuda.Event())
-            ent[1].record()
-            cls._pinned[key] = ent
-        return ent
-
     def upload(self, device, fill_structs=None):
         """Allocate the device buffer, let ``fill_structs(base_ptr)`` return
         [(offset, bytes)] (descriptors holding device pointers), then copy
@@ -172,15 +157,15 @@ class Arena:
         dev = torch.empty(max(self.size, 1), dtype=torch.uint8, device=device)
         base = dev.data_ptr()
         extra = fill_structs(base) if fill_structs else []
-        stage, done = self._staging(self.size, dev.device)
-        # the pinned buffer is reused across calls: wait for its previous copy only
-        done.synchronize()
+        # pinned staging from torch's caching host allocator: a block is reused
+        # only after the copy that read it has completed (event recorded by the
+        # non-blocking copy), so uploads of consecutive launch groups never wait
+        stage = torch.empty(max(self.size, 1), dtype=torch.uint8, pin_memory=True)
         host = stage.numpy()
         for off, a in self._parts:
             if a is not None:
                 host[off:off + a.nbytes] = a.view(np.uint8).reshape(-1)
         for off, b in extra:
             host[off:off + len(b)] = np.frombuffer(b, dtype=np.uint8)
-        dev.copy_(stage[: max(self.size, 1)], non_blocking=True)
-        done.record()
+        dev.copy_(stage, non_blocking=True)
         return dev

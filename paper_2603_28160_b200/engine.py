@@ -31,6 +31,7 @@ DEFAULT_MAX_STEP_ANGLE_RAD = math.radians(0.5)
 # Z-map bytes one sweep job may cover: keeps its RED.MIN traffic in the
 # 126 MB L2 (surfaces above this are cut into feed-direction sub-strips)
 L2_TILE_BYTES = int(float(__import__("os").environ.get("MSURF_L2_TILE_MB", "48")) * (1 << 20))
+PIPELINE_PLAN_THREADS = int(__import__("os").environ.get("MSURF_PIPELINE_THREADS", "3"))
 
 __all__ = ["SimulationConfig", "SimulationResult", "time_step", "simulate", "simulate_batch",
            "simulate_reference", "run_benchmark", "BenchmarkReport", "BenchmarkRow", "sweep_plans"]
@@ -379,16 +380,17 @@ def simulate(config: SimulationConfig, extensions: Extensions | None = None, *,
     rounded double-double sincos — the parity mode. ``diagnostics=True``
     also counts deposits and atomics (``result.counters``)."""
     p = plan(config, extensions)
-    res = _launch_results([p], trig, diagnostics)[0]
-    # the reference returns host heights: start their D2H now, it overlaps
-    # the caller's next launches (areal_metrics etc. run on the device copy)
-    res.field.prefetch_host()
-    return res
+    # the reference returns host heights: their D2H starts right after the
+    # sweep and overlaps the caller's next launches (areal_metrics etc. run
+    # on the device copy)
+    return _launch_results([p], trig, diagnostics, prefetch=True)[0]
 
 
-def _launch_results(plans, trig, diagnostics=False):
+def _launch_results(plans, trig, diagnostics=False, prefetch=False):
     """Upload, launch asynchronously, wrap the fields (no host sync unless a
-    trajectory record is requested)."""
+    trajectory record is requested). ``prefetch``: one D2H copy of the whole
+    group's heights into one pinned buffer on a side stream, started right
+    after the decode; each field's ``heights`` then only waits for it."""
     torch = _native.require_cuda()
     b = SweepBatch([(p, 0, p.grid.n) for p in plans], trig=trig, diagnostics=diagnostics)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -396,19 +398,42 @@ def _launch_results(plans, trig, diagnostics=False):
     lk = _Launch(b, ev)
     views, trajs = b.heights(), b.trajectories()
     sents = b.sentinels_device()
+    host = None
+    if prefetch:
+        from .grid import _copy_stream
+
+        side = _copy_stream(torch, b.dev)
+        side.wait_stream(torch.cuda.current_stream(b.dev))
+        host = torch.empty(b.keys.shape, dtype=torch.float64, pin_memory=True)
+        with torch.cuda.stream(side):
+            host.copy_(b.keys.view(torch.float64), non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(side)
+        b.keys.record_stream(side)
     out = []
     for i, (p, v, tr) in enumerate(zip(plans, views, trajs)):
         f = HeightField(p.grid, p.initial_height, device=v)
         f._dev_sentinel = sents[i:i + 1]
+        if host is not None:
+            s = b.surfs[i]
+            f._set_prefetch(host[s.key_off: s.key_off + s.nodes], done)
         out.append(SimulationResult(field=f, trajectory=_build_trajectory(p, tr) if p.record else None,
                                     time_steps=p.steps, trajectory_points=p.trajectory_points,
                                     launch=lk, index=i, share=1.0 / len(plans)))
     return out
 
 
-def simulate_batch(configs, extensions=None, *, trig: str = "device", diagnostics: bool = False):
+def simulate_batch(configs, extensions=None, *, trig: str = "device", diagnostics: bool = False,
+                   chunk: int | None = None, prefetch: bool = True):
     """Batched mode: many parameter sets swept in the same kernel launches.
-    ``extensions`` is None, one Extensions, or a list aligned with configs."""
+    ``extensions`` is None, one Extensions, or a list aligned with configs.
+
+    Large batches run as a software pipeline of launch groups of ``chunk``
+    sets (default: about 64 sets or 6e7 Z-map nodes): host planning of group
+    k+1 overlaps the sweep of group k on the GPU, and each group's heights
+    start streaming to pinned host memory (``prefetch``) as soon as its
+    sweep is done, overlapping the later sweeps. Every group is one fill, one
+    sweep per kinematics mode and one decode launch."""
     if isinstance(extensions, (list, tuple)):
         exts = list(extensions)
         if len(exts) != len(configs):
@@ -417,7 +442,25 @@ def simulate_batch(configs, extensions=None, *, trig: str = "device", diagnostic
         exts = [extensions] * len(configs)
     if not configs:
         return []
-    return _launch_results(plan_many(configs, exts), trig, diagnostics)
+    if chunk is None:
+        chunk = 32 if len(configs) >= 128 else max(4, -(-len(configs) // 4))
+    bounds = [(lo, min(len(configs), lo + chunk)) for lo in range(0, len(configs), chunk)]
+    if len(bounds) == 1:
+        return _launch_results(plan_many(configs, exts), trig, diagnostics, prefetch)
+    # launch groups are planned concurrently on host threads (one vectorised
+    # plan per group) and launched in order as soon as each is ready, so the
+    # GPU starts on group 0 while the host still plans the rest
+    from concurrent.futures import ThreadPoolExecutor
+
+    from .planner import PLAN_THREADS
+
+    out = []
+    # a few workers only: group 0 is ready early, later groups keep pace with the GPU
+    with ThreadPoolExecutor(max_workers=min(PIPELINE_PLAN_THREADS, PLAN_THREADS, len(bounds))) as pool:
+        futs = [pool.submit(plan_many, configs[lo:hi], exts[lo:hi], 1) for lo, hi in bounds]
+        for f in futs:
+            out.extend(_launch_results(f.result(), trig, diagnostics, prefetch))
+    return out
 
 
 def simulate_reference(config: SimulationConfig, extensions: Extensions | None = None, *,

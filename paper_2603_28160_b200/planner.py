@@ -423,7 +423,10 @@ def _ext_group_key(config, ext: Extensions):
             bool(ext.runout_offset_mm != 0.0))
 
 
-def plan_many(configs, exts):
+PLAN_THREADS = max(1, min(8, (__import__("os").cpu_count() or 1)))
+
+
+def plan_many(configs, exts, threads: int | None = None):
     """plan() for many parameter sets. Extended-model sets that share their
     edge geometry are planned together with (sets, teeth, points) arrays —
     the same element-wise operations as plan(), so every array is bitwise
@@ -440,13 +443,32 @@ def plan_many(configs, exts):
             except (ConfigError, DomainError):
                 pass
         out[i] = plan(c, e)
+    jobs = []
     for idx in groups.values():
         if len(idx) < 4:
             for i in idx:
                 out[i] = plan(configs[i], exts[i])
             continue
-        for i, p in zip(idx, _plan_ext_group([configs[i] for i in idx], [exts[i] for i in idx])):
-            out[i] = p
+        # sub-groups planned on host threads (NumPy releases the GIL inside
+        # its element-wise kernels); each sub-group is the same vectorised
+        # computation, so the arrays stay bitwise equal to per-set plan()
+        nthr = PLAN_THREADS if threads is None else max(1, threads)
+        step = max(4, -(-len(idx) // nthr))
+        jobs.extend(idx[a: a + step] for a in range(0, len(idx), step))
+    if jobs:
+        def run(sub):
+            return sub, _plan_ext_group([configs[i] for i in sub], [exts[i] for i in sub])
+
+        if len(jobs) == 1:
+            done = [run(jobs[0])]
+        else:
+            from concurrent.futures import ThreadPoolExecutor
+
+            with ThreadPoolExecutor(max_workers=min(PLAN_THREADS if threads is None else threads, len(jobs))) as pool:
+                done = list(pool.map(run, jobs))
+        for sub, plans in done:
+            for i, p in zip(sub, plans):
+                out[i] = p
     return out
 
 

@@ -235,30 +235,41 @@ def _finish_areal(st1, st2, uncut) -> ArealMetrics:
 
 
 def areal_metrics_batch(fields, roi=None, uncut: str = "raise"):
-    """Areal metrics of many same-shape fields that live in one contiguous
-    device buffer (simulate_batch output) in two launches; falls back to one
-    call per field when they do not share a buffer. Returns a list of
-    ArealMetrics or DomainError instances (per-sample status, dataset.py:177-180)."""
+    """Areal metrics of many fields: each run of consecutive same-shape fields
+    that sit at a constant stride in one device buffer (the output of one
+    simulate_batch launch group) is reduced in two launches; anything else
+    falls back to one call per field. Returns a list of ArealMetrics or
+    DomainError instances (per-sample status, dataset.py:177-180)."""
     if not fields:
         return []
-    torch = _native.require_cuda()
-    spec = fields[0].spec
-    same = all(f.spec == spec for f in fields)
     devs = [f.device_heights() for f in fields]
-    stride = None
-    if same and len(devs) > 1:
-        p0 = devs[0].data_ptr()
-        st = devs[1].data_ptr() - p0
-        if st > 0 and all(d.data_ptr() == p0 + k * st for k, d in enumerate(devs)) and st % 8 == 0:
-            stride = st // 8
-    if not same or (len(devs) > 1 and stride is None):
-        out = []
-        for f in fields:
+    out, a = [], 0
+    while a < len(fields):
+        b = a + 1
+        spec = fields[a].spec
+        st = None
+        if b < len(fields) and fields[b].spec == spec:
+            st = devs[b].data_ptr() - devs[a].data_ptr()
+            if st <= 0 or st % 8:
+                st = None
+        if st is not None:
+            while (b < len(fields) and fields[b].spec == spec
+                   and devs[b].data_ptr() == devs[a].data_ptr() + (b - a) * st):
+                b += 1
+            out.extend(_areal_run(fields[a:b], devs[a:b], st // 8, roi, uncut))
+        else:
             try:
-                out.append(areal_metrics(f, roi=roi, uncut=uncut))
+                out.append(areal_metrics(fields[a], roi=roi, uncut=uncut))
             except DomainError as exc:
                 out.append(exc)
-        return out
+        a = b
+    return out
+
+
+def _areal_run(fields, devs, stride, roi, uncut):
+    """Two-launch areal reduction of same-shape fields at a constant stride."""
+    torch = _native.require_cuda()
+    spec = fields[0].spec
     i_lo, j_lo, i_hi, j_hi = _check_roi(spec, roi)
     ss = [getattr(f, "_dev_sentinel", None) for f in fields]
     if all(x is not None for x in ss) and all(x.data_ptr() == ss[0].data_ptr() + 8 * k for k, x in enumerate(ss)):

@@ -96,7 +96,7 @@ def write_surface(field: HeightField, path, *, chunk_bytes: int = STREAM_CHUNK_B
     tmp = _tmp_name(path)
     with open(tmp, "wb") as fh:
         fh.write(_header(field))
-        if field.on_device:
+        if field.on_device and field._pending is None:
             _stream_device_payload(fh, field.device_heights().reshape(-1), chunk_bytes)
         else:
             fh.write(field.heights.astype("<f8", copy=False).tobytes())

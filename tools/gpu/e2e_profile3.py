@@ -20,9 +20,21 @@ for it in range(4):
         d2h += o.field.heights.nbytes
     t4 = t()
     print(f"plan_many {1e3*(t1-t0):.2f} upload+sweep {1e3*(t2-t1):.2f} metrics {1e3*(t3-t2):.2f} heights {1e3*(t4-t3):.2f} ({d2h/1e6:.0f} MB) total {1e3*(t4-t0):.2f} ms")
+print("--- simulate_batch pipeline")
+for chunk in (None, 16, 32, 256):
+    for it in range(3):
+        t0 = t()
+        out = ms.simulate_batch(cfgs, exts, chunk=chunk); ta = time.perf_counter()
+        mets = ms.areal_metrics_batch([o.field for o in out], uncut=meta["uncut"]); tb = time.perf_counter()
+        d2h = sum(o.field.heights.nbytes for o in out); tc = time.perf_counter()
+        torch.cuda.synchronize(); td = time.perf_counter()
+        print(f"chunk {chunk}: simulate_batch {1e3*(ta-t0):.2f} metrics {1e3*(tb-ta):.2f} heights {1e3*(tc-tb):.2f} total {1e3*(td-t0):.2f} ms")
 import cProfile, pstats
-pr = cProfile.Profile(); pr.enable()
-for _ in range(3):
-    ps = planner.plan_many(cfgs, exts)
-pr.disable()
-pstats.Stats(pr).sort_stats('tottime').print_stats(18)
+for chunk in (32, 256):
+    pr = cProfile.Profile(); pr.enable()
+    for _ in range(3):
+        out = ms.simulate_batch(cfgs, exts, chunk=chunk)
+        torch.cuda.synchronize()
+    pr.disable()
+    print("=== chunk", chunk)
+    pstats.Stats(pr).sort_stats('tottime').print_stats(14)

@@ -97,21 +97,6 @@ __device__ __noinline__ int cell_index_exact(double w, double lo, double dd) {
   return __double2int_rz(floor(tq));  // saturates far outside; range checks reject
 }
 
-struct CellFast {
-  int idx;       // floor(tq) if not near
-  bool near;     // fraction within 2^-29 of an integer: use the exact path
-};
-
-__device__ __forceinline__ CellFast cell_fast(double w, double inv, double c0) {
-  const double m = __dadd_rn(__fma_rn(w, inv, c0), 0x1.8p20);
-  const int hi = __double2hiint(m);
-  const unsigned lo = (unsigned)__double2loint(m);
-  CellFast r;
-  r.idx = hi - kMagicHi;
-  r.near = (lo + 8u) < 16u;
-  return r;
-}
-
 // Fire-and-forget global atomic min (RED.E.MIN.64): the explicit .global
 // form avoids the generic-address shared-memory fallback atomicMin compiles to.
 __device__ __forceinline__ void red_min_u64(unsigned long long* p, unsigned long long v) {

@@ -62,13 +62,13 @@ typedef struct msurf_job {
   const double* pts;         /* [teeth][points][4] per-point record (16-B aligned):
                               * REF      (xp, yp, zp, key of z')  edge frame
                               * EXT      (xt, yt, key of z', 0)   tool frame
-                              * EXT_TILT (xt, yt, sin(tau)*zt, cos(tau)*zt)        */
+                              * EXT_TILT (xt, yt, sin(tau)*zt, cos(tau)*zt + zoff)  */
   const double* tooth_box;   /* [teeth][6] whole-tooth tool-frame box (P_eng counter)  */
   const double* chunk_circ;  /* [teeth][nchunk][6] cull record per 32-point chunk:
                               * (xc, yc, rx, ry, yz, 0) — see planner._chunk_circles */
   const double* pass_x0;     /* [passes] spindle x of each raster pass               */
   /* extended kinematics */
-  double tilt_c, tilt_s, zoff;
+  double tilt_c, tilt_s, zoff;  /* zoff: surface z offset (EXT_TILT: folded into pts) */
   double vib_amp, vib_omega, vib_phase;
   /* optional host-libm trig tables (parity mode); NULL = device sincos */
   const double* trig_table;  /* [steps][teeth][2] = cos, sin of the tooth angle      */

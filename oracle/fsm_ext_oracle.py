@@ -32,6 +32,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import fsm_oracle as ref
+from .fma import fma
 
 
 def _get(ext, name, default=0.0):
@@ -279,14 +280,17 @@ def _ext_range(p: ExtPlan, x0p, lo_step, hi_step, heights, counters):
             if keep.size == 0:
                 continue
             ck, sk, nk = c[keep][:, None], sn[keep][:, None], ns[keep][:, None]
-            u = ck * xt + sk * yt
-            v = nk * xt + ck * yt
-            xw = u + xoff[keep][:, None]
             if p.tilt:
-                yv = p.tilt_c * v - p.tilt_s * zt
-                zz = (p.tilt_s * v + p.tilt_c * zt) + p.zoff
-                yw = yv + ty[keep][:, None]
+                # fused lead-tilt model: one rounding per fma
+                u = fma(ck, xt, sk * yt)
+                v = fma(ck, yt, -(sk * xt))
+                xw = u + xoff[keep][:, None]
+                yw = fma(p.tilt_c, v, -(p.tilt_s * zt)) + ty[keep][:, None]
+                zz = fma(p.tilt_s, v, (p.tilt_c * zt + p.zoff) + 0.0)
             else:
+                u = ck * xt + sk * yt
+                v = nk * xt + ck * yt
+                xw = u + xoff[keep][:, None]
                 yw = v + ty[keep][:, None]
             gi = np.floor((xw - p.x_min) / dd + 0.5)
             gj = np.floor((yw - p.y_min) / dd + 0.5)

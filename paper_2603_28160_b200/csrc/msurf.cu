@@ -150,11 +150,25 @@ struct PointEval {
   bool near;
   uint64_t key;
   unsigned zh;  // high word of the order-preserving key (tilt neighbour compares)
+
+  // cell coordinates of (xw, yw): fma + magic-number add, floor and fraction
+  // straight from the bits (see kMagicHi)
+  __device__ __forceinline__ PointEval finish(double inv, double cx0, double cy0) {
+    const double mx = __dadd_rn(__fma_rn(xw, inv, cx0), 0x1.8p20);
+    const double my = __dadd_rn(__fma_rn(yw, inv, cy0), 0x1.8p20);
+    hi_x = __double2hiint(mx);
+    hi_y = __double2hiint(my);
+    near = (((unsigned)__double2loint(mx) + 8u) < 16u) | (((unsigned)__double2loint(my) + 8u) < 16u);
+#ifdef MSURF_FORCE_NEAR
+    near = true;  // test build: every point takes the exact deferred path
+#endif
+    return *this;
+  }
 };
 
 template <int MODE>
 __device__ __forceinline__ PointEval eval_point(const double4 pt, const double* r, double inv, double cx0,
-                                                double cy0, double tilt_c, double tilt_s, double zoff) {
+                                                double cy0, double tilt_c, double tilt_s) {
   PointEval e;
   e.zh = 0u;
   if (MODE == MSURF_MODE_REF) {
@@ -165,30 +179,28 @@ __device__ __forceinline__ PointEval eval_point(const double4 pt, const double* 
                      r[7]);
     e.key = (uint64_t)__double_as_longlong(pt.w);
   } else {
+    if (MODE == MSURF_MODE_EXT_TILT) {
+      // lead-tilt model, fused: u = fma(c, x, s*y),
+      // v = fma(c, y, -(s*x)), x' = u + xoff, y' = fma(cos(tau), v, -sin(tau) z) + ty,
+      // z' = fma(sin(tau), v, cos(tau) z + zoff); pt = (x, y, sin(tau) z, cos(tau) z + zoff)
+      const double uu = __fma_rn(r[0], pt.x, __dmul_rn(r[1], pt.y));
+      const double vv = __fma_rn(r[0], pt.y, -__dmul_rn(r[1], pt.x));
+      e.xw = __dadd_rn(uu, r[2]);
+      e.yw = __dadd_rn(__fma_rn(tilt_c, vv, -pt.z), r[3]);
+      const double zz = __fma_rn(tilt_s, vv, pt.w);
+      e.key = enc_key_raw(zz);  // pt.w is never -0 (host-canonical), so neither is zz
+      e.zh = (unsigned)(e.key >> 32);
+      return e.finish(inv, cx0, cy0);
+    }
+    // EXT: the reference's op order on tool-frame points (u = c x + s y,
+    // v = -s x + c y), so all-zero extensions reproduce the reference bits
     const double uu = __dadd_rn(__dmul_rn(r[0], pt.x), __dmul_rn(r[1], pt.y));
     const double vv = __dadd_rn(__dmul_rn(-r[1], pt.x), __dmul_rn(r[0], pt.y));
     e.xw = __dadd_rn(uu, r[2]);
-    if (MODE == MSURF_MODE_EXT_TILT) {
-      // y' = cos(tau) v - sin(tau) z ; z' = (sin(tau) v + cos(tau) z) + zoff
-      const double yv = __dsub_rn(__dmul_rn(tilt_c, vv), pt.z);
-      const double zz = __dadd_rn(__dadd_rn(__dmul_rn(tilt_s, vv), pt.w), zoff);
-      e.yw = __dadd_rn(yv, r[3]);
-      e.key = enc_key_raw(zz);  // zz = (..) + zoff with zoff != -0 (host-canonical): never -0
-      e.zh = (unsigned)(e.key >> 32);
-    } else {
-      e.yw = __dadd_rn(vv, r[3]);
-      e.key = (uint64_t)__double_as_longlong(pt.z);
-    }
+    e.yw = __dadd_rn(vv, r[3]);
+    e.key = (uint64_t)__double_as_longlong(pt.z);
   }
-  const double mx = __dadd_rn(__fma_rn(e.xw, inv, cx0), 0x1.8p20);
-  const double my = __dadd_rn(__fma_rn(e.yw, inv, cy0), 0x1.8p20);
-  e.hi_x = __double2hiint(mx);
-  e.hi_y = __double2hiint(my);
-  e.near = (((unsigned)__double2loint(mx) + 8u) < 16u) | (((unsigned)__double2loint(my) + 8u) < 16u);
-#ifdef MSURF_FORCE_NEAR
-  e.near = true;  // test build: every point takes the exact deferred path
-#endif
-  return e;
+  return e.finish(inv, cx0, cy0);
 }
 
 // Time-neighbour pre-reduction across lanes (consecutive live steps of one
@@ -457,7 +469,7 @@ __global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
   const int jbias = kMagicHi + j_lo;
   const int ldk = (int)J.ld;
   unsigned long long* __restrict__ keys = reinterpret_cast<unsigned long long*>(J.keys);
-  const double tilt_c = J.tilt_c, tilt_s = J.tilt_s, zoff = J.zoff;
+  const double tilt_c = J.tilt_c, tilt_s = J.tilt_s;
   const int groups = (n_live + 31) >> 5;
   unsigned n_dep = 0, n_atom = 0;
 
@@ -507,8 +519,8 @@ __global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
 #pragma unroll kKUnroll
     for (int k = 0; k < p_end; k += 2) {
       const int ibias_b = (k + 1 < p_end) ? ibias : kMagicHi - (1 << 30);
-      PointEval ea = eval_point<MODE>(ptstage[warp][k], r, inv, cx0, cy0, tilt_c, tilt_s, zoff);
-      PointEval eb = eval_point<MODE>(ptstage[warp][k + 1], r, inv, cx0, cy0, tilt_c, tilt_s, zoff);
+      PointEval ea = eval_point<MODE>(ptstage[warp][k], r, inv, cx0, cy0, tilt_c, tilt_s);
+      PointEval eb = eval_point<MODE>(ptstage[warp][k + 1], r, inv, cx0, cy0, tilt_c, tilt_s);
       const int ia = ea.hi_x - ibias, ja = ea.hi_y - jbias;
       const int ib = eb.hi_x - ibias_b, jb = eb.hi_y - jbias;
       // near flags of live points (the fast index may be off by one there, so
@@ -530,7 +542,7 @@ __global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
     }
     if (__builtin_expect(__any_sync(0xffffffffu, anynear), 0)) {
       for (int k = 0; k < p_end; ++k) {
-        const PointEval e = eval_point<MODE>(ptstage[warp][k], r, inv, cx0, cy0, tilt_c, tilt_s, zoff);
+        const PointEval e = eval_point<MODE>(ptstage[warp][k], r, inv, cx0, cy0, tilt_c, tilt_s);
         if (!(e.near & on)) continue;
         const int ie = cell_index_exact(e.xw, J.x_min, dd);
         const int je = cell_index_exact(e.yw, J.y_min, dd) - j_lo;

@@ -207,6 +207,12 @@ def plan(config, ext: Extensions | None = None) -> SweepPlan:
     return p
 
 
+def tilt_z_term(tilt_c, zt, zoff):
+    """cos(tau)*zt + zoff, two roundings, canonical +0 (the fused tilt model's
+    per-point constant: z' = fma(sin(tau), v, this))."""
+    return (tilt_c * zt + zoff) + 0.0
+
+
 def _pack_records(p: SweepPlan) -> None:
     """Per-(tooth, point) 32-byte records the device reads with one broadcast
     load per point (include/msurf.h msurf_job.pts)."""
@@ -221,11 +227,11 @@ def _pack_records(p: SweepPlan) -> None:
     elif p.mode == MODE_EXT:
         rec[:, :, 0], rec[:, :, 1], rec[:, :, 2] = p.px, p.py, kf
     else:
-        # time-invariant halves of the tilt products (the device adds the
-        # time-varying ones): sin(tau)*zt and cos(tau)*zt, one rounding each
+        # time-invariant parts of the fused tilt model:
+        # sin(tau)*zt, and cos(tau)*zt + zoff (+0.0: never -0)
         rec[:, :, 0], rec[:, :, 1] = p.px, p.py
         rec[:, :, 2] = p.tilt_s * p.pz
-        rec[:, :, 3] = p.tilt_c * p.pz
+        rec[:, :, 3] = tilt_z_term(p.tilt_c, p.pz, p.zoff)
     p.pts = rec
 
 
@@ -569,7 +575,7 @@ def _plan_ext_group(configs, exts):
     rec[..., 0], rec[..., 1] = xt, yt
     if tilt:
         rec[..., 2] = ts * zt[None]
-        rec[..., 3] = tc * zt[None]
+        rec[..., 3] = tilt_z_term(tc, zt[None], zoffs[:, None, None])
     else:
         rec[..., 2] = keys_all.view(np.float64)
     mode = MODE_EXT_TILT if tilt else MODE_EXT

@@ -178,7 +178,11 @@ def cpu_sample(cfg, ext, plan, target_s: float = 12.0, threads: int | None = Non
     win = max(8, steps // 400)
     pts, dt = run(win)
     rate = pts / dt
-    if plan.trajectory_points / rate <= target_s:
+    if dt < 0.05 * target_s:  # pilot too short to trust: one larger pilot
+        win = min(steps // n_win, win * 8)
+        pts, dt = run(win)
+        rate = pts / dt
+    if plan.trajectory_points / rate <= 2.5 * target_s:
         t0 = time.perf_counter()
         _, _, ctr, _ = xorc.ext_sweep(cfg, ext, workers=threads)
         dt = time.perf_counter() - t0
@@ -387,7 +391,9 @@ def run_ours(args, rank, world):
                        "(MEASURED_PEAKS.json has no FP64 entry)",
         "flops_per_launch": flops,
         "flops_model": f"{FLOPS_PER_POINT[mode]} x points_evaluated + {FLOPS_PER_ROW} x live rows",
-        "survey_def": {"P_eng": engaged * p.points, "engaged_rows": engaged,
+        "survey_def": {"note": "SURVEY 8(d) units: every point of each row whose whole-tooth box meets the "
+                               "window; credits work the chunk cull skips, so it can exceed 1 (upper bound)",
+                       "P_eng": engaged * p.points, "engaged_rows": engaged,
                        "achieved": flops_survey / (sweep_ms_avg * 1e-3) / 1e12,
                        "frac": flops_survey / (sweep_ms_avg * 1e-3) / fp64_peak},
         "points_evaluated": evald, "live_rows": live, "deposits": int(dctr[0][2]),

@@ -100,6 +100,13 @@ int msurf_tile_steps(void);
 int msurf_sweep(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile_prefix,
                 int64_t n_tiles, int32_t mode, int32_t max_points, void* stream);
 
+/* The same sweep for ONE job given as a HOST pointer: the descriptor is
+ * passed by value as a kernel parameter, so the kernel reads its fields as
+ * constant-bank operands (fewer registers, no per-CTA descriptor copy);
+ * n_tiles = passes*teeth*ceil((step_hi-step_lo)/tile_steps). Device pointers
+ * inside the job are used as in msurf_sweep. */
+int msurf_sweep_job(const msurf_job* job, int64_t n_tiles, int32_t mode, int32_t max_points, void* stream);
+
 /* Decode keys to fp64 heights in place and count machined cells
  * (HeightField.machined_cell_count, surface_grid.py:128-129). Batched over
  * n_surf surfaces of `count` nodes each, contiguous; sentinel[n_surf] (the

@@ -29,6 +29,9 @@
 
 namespace {
 
+#ifndef MSURF_MIN_BLOCKS_ONE
+#define MSURF_MIN_BLOCKS_ONE 8  // by-value job: no descriptor registers, 64 regs without spills
+#endif
 #ifndef MSURF_MIN_BLOCKS
 #define MSURF_MIN_BLOCKS 6  // CTAs per SM the register budget is sized for (80 regs at 128 threads)
 #endif
@@ -235,17 +238,20 @@ __device__ __forceinline__ void next_unit(int& g, int& q, int nchunk) {
   }
 }
 
-template <int MODE, bool DIAG>
-__global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
+template <int MODE, bool DIAG, bool ONE>
+__global__ void __launch_bounds__(kSweepThreads, ONE ? MSURF_MIN_BLOCKS_ONE : MSURF_MIN_BLOCKS)
     sweep_kernel(const msurf_job* __restrict__ jobs, int n_jobs,
-                 const int64_t* __restrict__ prefix, int mask_words) {
+                 const int64_t* __restrict__ prefix, int mask_words, const __grid_constant__ msurf_job jp) {
   constexpr int RW = MODE == MSURF_MODE_REF ? 8 : 4;  // doubles of row data per live step
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* rowv = reinterpret_cast<double*>(smem_raw);                        // [T][8] by live slot
   uint64_t* masks = reinterpret_cast<uint64_t*>(rowv + kTileSteps * 8);      // [T][W] by thread
   int* live = reinterpret_cast<int*>(masks + kTileSteps * mask_words);       // [T] slot -> thread
   float4* ccf = reinterpret_cast<float4*>(live + kTileSteps);                // [nchunk] xc yc rx ry (f32)
-  __shared__ msurf_job J;
+  __shared__ msurf_job Js;
+  // ONE: a single job passed by value -> its fields are constant-bank operands
+  // (no registers, no shared-memory loads); else the CTA's job from the array
+  const msurf_job& J = ONE ? jp : Js;
   __shared__ int warp_cnt[kSweepWarps];
   __shared__ unsigned warp_eval[kSweepWarps];
   __shared__ unsigned warp_eng[kSweepWarps];
@@ -257,23 +263,25 @@ __global__ void __launch_bounds__(kSweepThreads, MSURF_MIN_BLOCKS)
   const int warp = tid >> 5;
   const long long tile = blockIdx.x;
 
-  if (tid == 0) {
-    int lo = 0, hi = n_jobs - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (prefix[mid] <= tile) lo = mid; else hi = mid - 1;
+  long long local = tile;
+  if (!ONE) {
+    if (tid == 0) {
+      int lo = 0, hi = n_jobs - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (prefix[mid] <= tile) lo = mid; else hi = mid - 1;
+      }
+      s_job = lo;
     }
-    s_job = lo;
+    __syncthreads();
+    {
+      const unsigned long long* src = reinterpret_cast<const unsigned long long*>(jobs + s_job);
+      unsigned long long* dst = reinterpret_cast<unsigned long long*>(&Js);
+      for (int w = tid; w < (int)(sizeof(msurf_job) / 8); w += kSweepThreads) dst[w] = src[w];
+    }
+    __syncthreads();
+    local = tile - prefix[s_job];
   }
-  __syncthreads();
-  {
-    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(jobs + s_job);
-    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&J);
-    for (int w = tid; w < (int)(sizeof(msurf_job) / 8); w += kSweepThreads) dst[w] = src[w];
-  }
-  __syncthreads();
-
-  const long long local = tile - prefix[s_job];
   const long long nst = (J.step_hi - J.step_lo + kTileSteps - 1) / kTileSteps;
   const int st = (int)(local % nst);
   const long long rem = local / nst;
@@ -1083,11 +1091,21 @@ __global__ void mb_atomic_kernel(unsigned long long* buf, long long mask, int it
 
 template <int MODE, bool DIAG>
 cudaError_t launch_sweep(int64_t n_tiles, size_t smem, cudaStream_t st, const msurf_job* jobs, int n_jobs,
-                         const int64_t* prefix, int mask_words) {
+                         const int64_t* prefix, int mask_words, const msurf_job* one) {
   cudaError_t e = cudaSuccess;
+  if (one) {
+    if (smem > 48 * 1024)
+      e = cudaFuncSetAttribute(sweep_kernel<MODE, DIAG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      sweep_kernel<MODE, DIAG, true><<<(unsigned)n_tiles, kSweepThreads, smem, st>>>(nullptr, 1, nullptr, mask_words, *one);
+    return e;
+  }
   if (smem > 48 * 1024)
-    e = cudaFuncSetAttribute(sweep_kernel<MODE, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess) sweep_kernel<MODE, DIAG><<<(unsigned)n_tiles, kSweepThreads, smem, st>>>(jobs, n_jobs, prefix, mask_words);
+    e = cudaFuncSetAttribute(sweep_kernel<MODE, DIAG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  msurf_job dummy;
+  memset(&dummy, 0, sizeof(dummy));
+  if (e == cudaSuccess)
+    sweep_kernel<MODE, DIAG, false><<<(unsigned)n_tiles, kSweepThreads, smem, st>>>(jobs, n_jobs, prefix, mask_words, dummy);
   return e;
 }
 
@@ -1115,10 +1133,8 @@ int msurf_fill_keys(uint64_t* keys, int64_t count, int32_t n_surf, const double*
   return check_launch("fill_kernel");
 }
 
-int msurf_sweep(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile_prefix,
-                int64_t n_tiles, int32_t mode, int32_t max_points, void* stream) {
-  if (n_jobs < 1 || !jobs || !tile_prefix || n_tiles < 0 || max_points < 1)
-    return set_err("msurf_sweep: bad arguments");
+static int sweep_impl(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile_prefix, int64_t n_tiles,
+                      int32_t mode, int32_t max_points, void* stream, const msurf_job* one) {
   if (n_tiles == 0) return 0;
   if (n_tiles > 0x7fffffffLL) return set_err("msurf_sweep: too many tiles");
   const int nchunk = (max_points + 31) / 32;
@@ -1129,24 +1145,31 @@ int msurf_sweep(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile_prefi
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
   const bool diag = (mode & MSURF_SWEEP_DIAG) != 0;
+#define MSURF_LAUNCH(M)                                                                                    \
+  e = diag ? launch_sweep<M, true>(n_tiles, smem, st, jobs, n_jobs, tile_prefix, mask_words, one)          \
+           : launch_sweep<M, false>(n_tiles, smem, st, jobs, n_jobs, tile_prefix, mask_words, one)
   switch (mode & ~MSURF_SWEEP_DIAG) {
-    case MSURF_MODE_REF:
-      e = diag ? launch_sweep<MSURF_MODE_REF, true>(n_tiles, smem, st, jobs, n_jobs, tile_prefix, mask_words)
-               : launch_sweep<MSURF_MODE_REF, false>(n_tiles, smem, st, jobs, n_jobs, tile_prefix, mask_words);
-      break;
-    case MSURF_MODE_EXT:
-      e = diag ? launch_sweep<MSURF_MODE_EXT, true>(n_tiles, smem, st, jobs, n_jobs, tile_prefix, mask_words)
-               : launch_sweep<MSURF_MODE_EXT, false>(n_tiles, smem, st, jobs, n_jobs, tile_prefix, mask_words);
-      break;
-    case MSURF_MODE_EXT_TILT:
-      e = diag ? launch_sweep<MSURF_MODE_EXT_TILT, true>(n_tiles, smem, st, jobs, n_jobs, tile_prefix, mask_words)
-               : launch_sweep<MSURF_MODE_EXT_TILT, false>(n_tiles, smem, st, jobs, n_jobs, tile_prefix, mask_words);
-      break;
+    case MSURF_MODE_REF: MSURF_LAUNCH(MSURF_MODE_REF); break;
+    case MSURF_MODE_EXT: MSURF_LAUNCH(MSURF_MODE_EXT); break;
+    case MSURF_MODE_EXT_TILT: MSURF_LAUNCH(MSURF_MODE_EXT_TILT); break;
     default:
       return set_err("msurf_sweep: unknown mode");
   }
+#undef MSURF_LAUNCH
   if (e != cudaSuccess) return set_err(std::string("msurf_sweep: smem attribute: ") + cudaGetErrorString(e));
   return check_launch("sweep_kernel");
+}
+
+int msurf_sweep(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile_prefix,
+                int64_t n_tiles, int32_t mode, int32_t max_points, void* stream) {
+  if (n_jobs < 1 || !jobs || !tile_prefix || n_tiles < 0 || max_points < 1)
+    return set_err("msurf_sweep: bad arguments");
+  return sweep_impl(jobs, n_jobs, tile_prefix, n_tiles, mode, max_points, stream, nullptr);
+}
+
+int msurf_sweep_job(const msurf_job* job, int64_t n_tiles, int32_t mode, int32_t max_points, void* stream) {
+  if (!job || n_tiles < 0 || max_points < 1) return set_err("msurf_sweep_job: bad arguments");
+  return sweep_impl(nullptr, 1, nullptr, n_tiles, mode, max_points, stream, job);
 }
 
 int msurf_decode(uint64_t* keys, int64_t count, int32_t n_surf, const double* sentinel,

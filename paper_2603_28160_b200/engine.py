@@ -31,6 +31,8 @@ DEFAULT_MAX_STEP_ANGLE_RAD = math.radians(0.5)
 # Z-map bytes one sweep job may cover: keeps its RED.MIN traffic in the
 # 126 MB L2 (surfaces above this are cut into feed-direction sub-strips)
 L2_TILE_BYTES = int(float(__import__("os").environ.get("MSURF_L2_TILE_MB", "48")) * (1 << 20))
+# groups of at most this many jobs launch one msurf_sweep_job per job
+ONE_JOB_LAUNCH_MAX = int(__import__("os").environ.get("MSURF_ONE_JOB_MAX", "32"))
 PIPELINE_PLAN_THREADS = int(__import__("os").environ.get("MSURF_PIPELINE_THREADS", "3"))
 
 __all__ = ["SimulationConfig", "SimulationResult", "time_step", "simulate", "simulate_batch",
@@ -215,6 +217,8 @@ class SweepBatch:
         for jn, jb in enumerate(jobs):
             groups.setdefault(surfs[jb[0]].plan.mode, []).append(jn)
         self.group_meta = []
+        self.group_tiles = []
+        self.group_host_jobs = []  # host copies of the descriptors (by-value launches)
         for mode, jidx in sorted(groups.items()):
             tiles = [surfs[jobs[j][0]].plan.passes * surfs[jobs[j][0]].plan.teeth *
                      ((jobs[j][4] - jobs[j][3] + tile_steps - 1) // tile_steps) for j in jidx]
@@ -223,6 +227,7 @@ class SweepBatch:
             pre_off = ar.add(prefix)
             self.group_meta.append((mode, jidx, job_off, pre_off, int(prefix[-1]),
                                     max(surfs[jobs[j][0]].plan.points for j in jidx)))
+            self.group_tiles.append([int(t) for t in tiles])
         keys_ptr = self.keys.data_ptr()
         traj_ptr = self.traj.data_ptr() if self.traj is not None else 0
         self.traj_off = []
@@ -261,13 +266,16 @@ class SweepBatch:
                     j.traj = (traj_ptr + self.traj_off[i] * 8) if (self.need_traj[i] and lo == s.j_lo) else None
                     j.teeth, j.points, j.passes = p.teeth, p.points, p.passes
                 out.append((job_off, bytes(arr)))
+                self.group_host_jobs.append(arr)
             return out
 
         self.h2d_bytes = ar.size
         self.buf = ar.upload(self.dev, fill)
         self.base = self.buf.data_ptr()
         self.same_shape = len({s.nodes for s in surfs}) == 1
-        self.launches_per_run = 2 * (1 if self.same_shape else n) + len(self.group_meta)
+        sweeps = sum((sum(1 for t in tl if t) if len(gm[1]) <= ONE_JOB_LAUNCH_MAX else 1)
+                     for gm, tl in zip(self.group_meta, self.group_tiles))
+        self.launches_per_run = 2 * (1 if self.same_shape else n) + sweeps
 
     # ------------------------------------------------------------------
     def launch_fill(self, sp: int) -> None:
@@ -285,8 +293,16 @@ class SweepBatch:
     def launch_sweep(self, sp: int) -> None:
         """One msurf_sweep launch per kinematics mode present in the batch."""
         lib, base = self.lib, self.base
-        for mode, idx, job_off, pre_off, n_tiles, max_pts in self.group_meta:
+        for g, (mode, idx, job_off, pre_off, n_tiles, max_pts) in enumerate(self.group_meta):
             flag = _native.SWEEP_DIAG if self.diagnostics else 0
+            if len(idx) <= ONE_JOB_LAUNCH_MAX:
+                # few jobs (one surface, or its L2 sub-strips): one launch per job
+                # with the descriptor passed by value (constant-bank operands)
+                arr = self.group_host_jobs[g]
+                for k, t in enumerate(self.group_tiles[g]):
+                    if t:
+                        _native.check(lib.msurf_sweep_job(ctypes.addressof(arr[k]), t, mode | flag, max_pts, sp))
+                continue
             _native.check(lib.msurf_sweep(base + job_off, len(idx), base + pre_off, n_tiles, mode | flag,
                                           max_pts, sp))
 

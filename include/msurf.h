@@ -169,6 +169,37 @@ int msurf_profiles(const double* h, int64_t surf_stride, int32_t n_surf,
                    const double* sentinel, int32_t exclude_uncut, const double* stats_in,
                    double* out, void* stream);
 
+/* Host-side planning arrays of one surface (planner.py, native so a
+ * single-surface simulate() spends microseconds before the GPU starts;
+ * bitwise identical to the NumPy statement). Scalars (validation, span,
+ * engaged half-length, edge->tool rows, helix/runout/tilt constants, noise)
+ * come from the Python planner. */
+typedef struct msurf_geom_in {
+  int32_t mode;              /* MSURF_MODE_*                                          */
+  int32_t teeth, points;
+  int32_t profile;           /* EXT: 0 insert arc at D/2, 1 ball meridian              */
+  double radius;             /* insert / ball radius R                                 */
+  double half;               /* insert: engaged half-length (edge l in [-half, half])  */
+  double kmax;               /* ball: maximum polar angle                              */
+  double tan_beta_over_r;    /* EXT helix: tan(beta)/r_ref, 0 = none                    */
+  double tilt_c, tilt_s;     /* EXT_TILT: cos, sin of the lead tilt                     */
+  double z0;                 /* REF: spindle z0 (zw = ((e20 x + e21 y) + e22 z) + (e23 + z0)) */
+  const double* rows;        /* [teeth][12] edge->tool rows 0..2 (4 columns each)       */
+  const double* delta;       /* EXT edge noise [teeth][points] or NULL                  */
+  const double* runout_xy;   /* EXT tool-axis runout offsets [teeth][2] or NULL         */
+} msurf_geom_in;
+
+/* REF: px/py/pz [points] = edge-frame SoA. EXT: [teeth][points] tool-frame
+ * points (profile, noise, rows, helix, runout); stats2 = (z_shift, max|zt|). */
+int msurf_plan_geometry(const msurf_geom_in* in, double* px, double* py, double* pz, double* stats2);
+/* With the surface z offset zoff: device point records pts [teeth][points][4]
+ * (msurf_job.pts), tooth_box [teeth][6], chunk_circ / chunk_box
+ * [teeth][nchunk][6], min_index [teeth]; optional zw_out / key_out
+ * [teeth][points] (z' and its order-preserving key). */
+int msurf_plan_finish(const msurf_geom_in* in, const double* px, const double* py, const double* pz, double zoff,
+                      double* pts, double* tooth_box, double* chunk_circ, double* chunk_box, int32_t* min_index,
+                      double* zw_out, uint64_t* key_out);
+
 /* Graymap export (surface_io.py:100-131, write_graymap) of one fp64 height
  * field (row pitch ld) over the ROI rows [i_lo, i_lo+rows) x cols
  * [j_lo, j_lo+cols). msurf_graymap_range: out3 = (max, min, n) of the

@@ -47,6 +47,17 @@ class MsurfJob(ctypes.Structure):
     ]
 
 
+class MsurfGeomIn(ctypes.Structure):
+    """Mirror of msurf_geom_in (include/msurf.h)."""
+
+    _fields_ = [
+        ("mode", c_int32), ("teeth", c_int32), ("points", c_int32), ("profile", c_int32),
+        ("radius", c_double), ("half", c_double), ("kmax", c_double), ("tan_beta_over_r", c_double),
+        ("tilt_c", c_double), ("tilt_s", c_double), ("z0", c_double),
+        ("rows", c_void_p), ("delta", c_void_p), ("runout_xy", c_void_p),
+    ]
+
+
 EXPORTS = {
     "msurf_abi_version": (ctypes.c_int, []),
     "msurf_last_error": (ctypes.c_char_p, []),
@@ -75,6 +86,9 @@ EXPORTS = {
     "msurf_graymap_pixels": (ctypes.c_int, [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,
                                             c_void_p, c_void_p, c_void_p]),
     "msurf_microbench": (ctypes.c_int, [c_int32, ctypes.POINTER(c_double)]),
+    "msurf_plan_geometry": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "msurf_plan_finish": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_void_p, c_void_p,
+                                         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
 }
 
 _lib = None

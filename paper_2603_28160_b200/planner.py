@@ -10,6 +10,7 @@ reproduces the reference's heights bit-for-bit.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass, field
 
@@ -21,6 +22,10 @@ from .geometry import default_point_count, edge_coordinates, effective_half_leng
 from .kinematics import edge_to_tool_rows, tooth_base_angle
 
 MODE_REF, MODE_EXT, MODE_EXT_TILT = 0, 1, 2
+# planning arrays from libmsurf's native planner (msurf_plan.cpp, bitwise equal
+# to the NumPy statement below, which stays the specification and is used when
+# MSURF_NATIVE_PLAN=0; tests/test_native_plan_cpu.py compares the two)
+NATIVE_PLAN = __import__("os").environ.get("MSURF_NATIVE_PLAN", "1") == "1"
 CHUNK = 32  # edge points per warp
 MAX_POINTS = 64 * 64 * 32  # mask words are bounded by the CTA's shared memory
 
@@ -237,6 +242,8 @@ def _pack_records(p: SweepPlan) -> None:
 
 def _pack(p: SweepPlan) -> None:
     """Device records, bounding circles and whole-tooth boxes."""
+    if p.pts is not None and p.chunk_circ is not None and p.tooth_box is not None:
+        return  # the native planner produced them
     _pack_records(p)
     if p.mode == MODE_REF:
         xt = (p.tooth_rows[:, 0:1] * p.px[None, :] + p.tooth_rows[:, 1:2] * p.py[None, :]) \
@@ -287,6 +294,51 @@ def step_window(p: SweepPlan, j_lo: int, j_hi: int):
     return max(0, min(p.steps, s_lo)), max(0, min(p.steps, s_hi))
 
 
+def _native_arrays(mode, z_n, n, rows12, *, radius, half=0.0, kmax=0.0, profile=0, z0=0.0, tanb_over_r=0.0,
+                   tilt_c=1.0, tilt_s=0.0, delta=None, runout_xy=None, zoff_fn=None):
+    """Run msurf_plan_geometry + msurf_plan_finish; returns a dict of the plan
+    arrays (and the (z_shift, max|zt|) statistics the caller's margin needs)."""
+    from . import _native
+
+    lib = _native.lib()
+    rows12 = np.ascontiguousarray(rows12, dtype=np.float64)
+    g = _native.MsurfGeomIn(mode=mode, teeth=z_n, points=n, profile=profile, radius=radius, half=half, kmax=kmax,
+                            tan_beta_over_r=tanb_over_r, tilt_c=tilt_c, tilt_s=tilt_s, z0=z0,
+                            rows=rows12.ctypes.data)
+    keep = [rows12]
+    if delta is not None:
+        delta = np.ascontiguousarray(delta, dtype=np.float64)
+        keep.append(delta)
+        g.delta = delta.ctypes.data
+    if runout_xy is not None:
+        runout_xy = np.ascontiguousarray(runout_xy, dtype=np.float64)
+        keep.append(runout_xy)
+        g.runout_xy = runout_xy.ctypes.data
+    shape = (n,) if mode == MODE_REF else (z_n, n)
+    px, py, pz = np.empty(shape), np.empty(shape), np.empty(shape)
+    stats = np.zeros(2)
+    gp = ctypes.addressof(g)
+    if lib.msurf_plan_geometry(gp, px.ctypes.data, py.ctypes.data, pz.ctypes.data, stats.ctypes.data):
+        raise DomainError("native planner rejected the geometry")
+    zoff = zoff_fn(float(stats[0]), float(stats[1])) if zoff_fn is not None else 0.0
+    nchunk = (n + CHUNK - 1) // CHUNK
+    out = dict(px=px, py=py, pz=pz, pts=np.empty((z_n, n, 4)), tooth_box=np.empty((z_n, 6)),
+               chunk_circ=np.empty((z_n, nchunk, 6)), chunk_box=np.empty((z_n, nchunk, 6)),
+               min_index=np.empty(z_n, dtype=np.int32), zw=np.empty((z_n, n)), zkey=np.empty((z_n, n), np.uint64),
+               zoff=zoff)
+    if lib.msurf_plan_finish(gp, px.ctypes.data, py.ctypes.data, pz.ctypes.data, zoff, out["pts"].ctypes.data,
+                             out["tooth_box"].ctypes.data, out["chunk_circ"].ctypes.data,
+                             out["chunk_box"].ctypes.data, out["min_index"].ctypes.data, out["zw"].ctypes.data,
+                             out["zkey"].ctypes.data):
+        raise DomainError("native planner rejected the geometry")
+    return out
+
+
+def _rows12(e) -> list:
+    return [e[0][0], e[0][1], e[0][2], e[0][3], e[1][0], e[1][1], e[1][2], e[1][3],
+            e[2][0], e[2][1], e[2][2], e[2][3]]
+
+
 def _plan_ref(config) -> SweepPlan:
     """engine.py:134-212 restated."""
     tool, proc, grid = config.tool, config.process, config.grid
@@ -300,10 +352,24 @@ def _plan_ref(config) -> SweepPlan:
     if half > tool.insert_radius_mm:
         raise DomainError(f"engaged half-length {half:.6g} mm exceeds the insert radius "
                           f"{tool.insert_radius_mm} mm (feed per tooth too large for this insert)")
-    xp, yp, zp = edge_coordinates(half, n, tool.insert_radius_mm)
     margin = tool.cutting_diameter_mm / 2.0 + half                  # engine.py:158
     dt, t_start, steps, x0, y0, z0 = _span(config, margin)
     z_n = tool.tooth_count
+    if NATIVE_PLAN:
+        es = [edge_to_tool_rows(tool, k) for k in range(1, z_n + 1)]
+        a = _native_arrays(MODE_REF, z_n, n, [_rows12(e) for e in es], radius=tool.insert_radius_mm,
+                           half=half, z0=z0)
+        p = SweepPlan(
+            mode=MODE_REF, grid=grid, teeth=z_n, points=n, steps=steps, dt=dt, t_start=t_start,
+            x0=x0, y0=y0, z0=z0, feed_speed=proc.feed_speed_mm_s, omega=proc.angular_velocity_rad_s,
+            initial_height=z0 + proc.depth_of_cut_mm, half_length=half,
+            tooth_base=np.array([tooth_base_angle(proc.phase_rad, k, z_n) for k in range(1, z_n + 1)]),
+            tooth_rows=np.array([_rows12(e)[:8] for e in es], dtype=np.float64).reshape(z_n, 8),
+            px=a["px"], py=a["py"], pz=a["pz"], zw=a["zw"], zkey=a["zkey"], chunk_box=a["chunk_box"],
+            pass_x0=np.array([x0]), min_index=a["min_index"])
+        p.pts, p.chunk_circ, p.tooth_box = a["pts"], a["chunk_circ"], a["tooth_box"]
+        return p
+    xp, yp, zp = edge_coordinates(half, n, tool.insert_radius_mm)
     rows = np.zeros((z_n, 8))
     xt = np.empty((z_n, n))
     yt = np.empty((z_n, n))
@@ -338,26 +404,28 @@ def _plan_ext(config, ext: Extensions) -> SweepPlan:
         n = config.edge_point_count or default_point_count(half, grid.spacing_mm)
         if n < 2:
             raise DomainError(f"point_count must be >= 2, got {n}")
-        ex, ey, ez = edge_coordinates(half, n, r)
-        nx = ex / r
-        nz = -(r - ez) / r
         arc = 2.0 * r * math.asin(min(1.0, half / r))
         base_margin = tool.cutting_diameter_mm / 2.0 + half
+        if not NATIVE_PLAN:
+            ex, ey, ez = edge_coordinates(half, n, r)
+            nx = ex / r
+            nz = -(r - ez) / r
     else:
         n = config.edge_point_count
         if n is None or n < 2:
             raise ConfigError("the ball profile needs edge_point_count >= 2")
         kmax = min(math.pi / 2.0, math.acos((r - a_p) / r) + abs(tau))
-        kap = kmax * np.arange(n, dtype=np.float64) / (n - 1)
-        kap[-1] = kmax
-        nx = np.sin(kap)
-        nz = -np.cos(kap)
-        ex = r * nx
-        ey = np.zeros(n)
-        ez = r - r * np.cos(kap)
         arc = r * kmax
         half = r * math.sin(kmax)
         base_margin = half
+        if not NATIVE_PLAN:
+            kap = kmax * np.arange(n, dtype=np.float64) / (n - 1)
+            kap[-1] = kmax
+            nx = np.sin(kap)
+            nz = -np.cos(kap)
+            ex = r * nx
+            ey = np.zeros(n)
+            ez = r - r * np.cos(kap)
     sigma = ext.noise_sigma_mm
     if sigma != 0.0:
         delta = edge_noise(z_n, n, sigma, ext.noise_corr_mm, arc / (n - 1), int(ext.noise_seed))
@@ -368,6 +436,43 @@ def _plan_ext(config, ext: Extensions) -> SweepPlan:
             r_ref = tool.cutting_diameter_mm / 2.0 if ext.profile == "insert" else r
         tanb_over_r = math.tan(beta) / r_ref
     radial = None if ext.profile == "insert" else 0.0
+    if NATIVE_PLAN:
+        tilt = tau != 0.0
+        tc, ts = math.cos(tau), math.sin(tau)
+        amp = ext.vib_amplitude_mm
+        offs = None
+        if rho != 0.0:
+            offs = []
+            for k in range(1, z_n + 1):
+                ang = lam + (2.0 * math.pi) * (k - 1) / z_n
+                offs.append((rho * math.cos(ang), rho * math.sin(ang)))
+        span = {}
+
+        def zoff_fn(z_shift, zmax):
+            margin = base_margin + (abs(rho) + abs(amp) + 5.0 * abs(sigma) + abs(ts) * zmax)
+            span["v"] = _span(config, margin)
+            return (span["v"][5] + (z_shift if tilt else 0.0)) + 0.0  # canonical: never -0
+
+        a = _native_arrays(MODE_EXT_TILT if tilt else MODE_EXT, z_n, n,
+                           [_rows12(edge_to_tool_rows(tool, k, radial_offset_mm=radial)) for k in range(1, z_n + 1)],
+                           radius=r, half=half if ext.profile == "insert" else 0.0,
+                           kmax=kmax if ext.profile != "insert" else 0.0,
+                           profile=0 if ext.profile == "insert" else 1,
+                           tanb_over_r=tanb_over_r if beta != 0.0 else 0.0, tilt_c=tc, tilt_s=ts,
+                           delta=delta if sigma != 0.0 else None, runout_xy=offs, zoff_fn=zoff_fn)
+        dt, t_start, steps, x0, y0, z0 = span["v"]
+        p = SweepPlan(
+            mode=MODE_EXT_TILT if tilt else MODE_EXT, grid=grid, teeth=z_n, points=n, steps=steps,
+            dt=dt, t_start=t_start, x0=x0, y0=y0, z0=z0, feed_speed=proc.feed_speed_mm_s,
+            omega=proc.angular_velocity_rad_s, initial_height=z0 + a_p, half_length=half,
+            tooth_base=np.array([tooth_base_angle(proc.phase_rad, k, z_n) for k in range(1, z_n + 1)]),
+            tooth_rows=np.zeros((z_n, 8)), px=a["px"], py=a["py"], pz=a["pz"], zw=a["zw"], zkey=a["zkey"],
+            chunk_box=a["chunk_box"], pass_x0=np.array([x0]), min_index=a["min_index"],
+            tilt_c=tc, tilt_s=ts, zoff=a["zoff"], vib_amp=amp,
+            vib_omega=2.0 * math.pi * ext.vib_frequency_hz, vib_phase=ext.vib_phase_rad,
+            extras={"base_margin": base_margin})
+        p.pts, p.chunk_circ, p.tooth_box = a["pts"], a["chunk_circ"], a["tooth_box"]
+        return p
     xt = np.empty((z_n, n))
     yt = np.empty((z_n, n))
     zt = np.empty((z_n, n))

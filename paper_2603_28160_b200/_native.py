@@ -151,7 +151,7 @@ class Arena:
         self.size = 0
 
     def add(self, arr) -> int:
-        a = np.ascontiguousarray(arr)
+        a = arr if isinstance(arr, np.ndarray) and arr.flags.c_contiguous else np.ascontiguousarray(arr)
         off = (self.size + 255) & ~255
         self._parts.append((off, a))
         self.size = off + a.nbytes

@@ -173,13 +173,13 @@ class SweepBatch:
         for s in surfs:
             p = s.plan
             o = dict(
-                tooth_base=ar.add(p.tooth_base.astype(np.float64)),
-                tooth_rows=ar.add(p.tooth_rows.astype(np.float64)),
-                pts=ar.add(p.pts.astype(np.float64)),
-                tooth_box=ar.add(p.tooth_box.astype(np.float64)),
-                chunk_circ=ar.add(p.chunk_circ.astype(np.float64)),
-                pass_x0=ar.add(p.pass_x0.astype(np.float64)),
-                min_index=ar.add(p.min_index.astype(np.int32)),
+                tooth_base=ar.add(p.tooth_base.astype(np.float64, copy=False)),
+                tooth_rows=ar.add(p.tooth_rows.astype(np.float64, copy=False)),
+                pts=ar.add(p.pts.astype(np.float64, copy=False)),
+                tooth_box=ar.add(p.tooth_box.astype(np.float64, copy=False)),
+                chunk_circ=ar.add(p.chunk_circ.astype(np.float64, copy=False)),
+                pass_x0=ar.add(p.pass_x0.astype(np.float64, copy=False)),
+                min_index=ar.add(p.min_index.astype(np.int32, copy=False)),
             )
             if trig == "host":
                 tab, vib = _trig_tables(p)
@@ -271,6 +271,7 @@ class SweepBatch:
 
         self.h2d_bytes = ar.size
         self.buf = ar.upload(self.dev, fill)
+        self._fresh = True
         self.base = self.buf.data_ptr()
         self.same_shape = len({s.nodes for s in surfs}) == 1
         sweeps = sum((sum(1 for t in tl if t) if len(gm[1]) <= ONE_JOB_LAUNCH_MAX else 1)
@@ -281,7 +282,10 @@ class SweepBatch:
     def launch_fill(self, sp: int) -> None:
         """Zero the counters and initialise every Z-map to its stock height."""
         lib, base, keys_ptr = self.lib, self.base, self.keys.data_ptr()
-        self.buf[self.ctr_off: self.ctr_off + self.n * (_native.NUM_CTRS + 1) * 8].zero_()
+        if self._fresh:  # the upload itself wrote zero counters
+            self._fresh = False
+        else:
+            self.buf[self.ctr_off: self.ctr_off + self.n * (_native.NUM_CTRS + 1) * 8].zero_()
         if self.same_shape:
             _native.check(lib.msurf_fill_keys(keys_ptr, self.surfs[0].nodes, self.n,
                                               base + self.sentinel_off, sp))
@@ -324,18 +328,19 @@ class SweepBatch:
         torch = self.torch
         st = stream if stream is not None else torch.cuda.current_stream(self.dev)
         sp = int(st.cuda_stream)
+        ev = events if events else (None, None, None, None)
         with torch.cuda.stream(st):
-            if events:
-                events[0].record(st)
+            if ev[0] is not None:
+                ev[0].record(st)
             self.launch_fill(sp)
-            if events:
-                events[1].record(st)
+            if ev[1] is not None:
+                ev[1].record(st)
             self.launch_sweep(sp)
-            if events:
-                events[2].record(st)
+            if ev[2] is not None:
+                ev[2].record(st)
             self.launch_decode(sp)
-            if events:
-                events[3].record(st)
+            if ev[3] is not None:
+                ev[3].record(st)
 
     def heights(self):
         """fp64 views (valid after a launch) — one per surface."""
@@ -409,7 +414,8 @@ def _launch_results(plans, trig, diagnostics=False, prefetch=False):
     after the decode; each field's ``heights`` then only waits for it."""
     torch = _native.require_cuda()
     b = SweepBatch([(p, 0, p.grid.n) for p in plans], trig=trig, diagnostics=diagnostics)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    e0, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [e0, None, None, e3]
     b.launch(events=ev)
     lk = _Launch(b, ev)
     views, trajs = b.heights(), b.trajectories()

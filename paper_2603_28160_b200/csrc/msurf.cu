@@ -45,6 +45,9 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kTileSteps = MSURF_TILE;  // sweep: time steps per CTA == threads per CTA
 constexpr int kSweepThreads = kTileSteps;
 constexpr int kSweepWarps = kSweepThreads / 32;
+#ifndef MSURF_PAIR_STEPS
+#define MSURF_PAIR_STEPS 2  // 0: never, 1: always, 2: tilt mode only (see kPairSteps)
+#endif
 #ifndef MSURF_KUNROLL
 #define MSURF_KUNROLL 8
 #endif
@@ -243,6 +246,11 @@ __global__ void __launch_bounds__(kSweepThreads, ONE ? MSURF_MIN_BLOCKS_ONE : MS
     sweep_kernel(const msurf_job* __restrict__ jobs, int n_jobs,
                  const int64_t* __restrict__ prefix, int mask_words, const __grid_constant__ msurf_job jp) {
   constexpr int RW = MODE == MSURF_MODE_REF ? 8 : 4;  // doubles of row data per live step
+  // lane = two consecutive live steps (one broadcast point record serves both,
+  // half the neighbour exchange in registers): faster for the tilt mode
+  // (config 2: 0.99 -> 0.95 ms, config 5: 59.4 -> 54.1 ms) whose neighbour
+  // filter needs both neighbours; slower for the constant-z modes (configs 3, 4)
+  constexpr bool kPairSteps = MSURF_PAIR_STEPS == 1 || (MSURF_PAIR_STEPS == 2 && MODE == MSURF_MODE_EXT_TILT);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* rowv = reinterpret_cast<double*>(smem_raw);                        // [T][8] by live slot
   uint64_t* masks = reinterpret_cast<uint64_t*>(rowv + kTileSteps * 8);      // [T][W] by thread
@@ -478,90 +486,199 @@ __global__ void __launch_bounds__(kSweepThreads, ONE ? MSURF_MIN_BLOCKS_ONE : MS
   const int ldk = (int)J.ld;
   unsigned long long* __restrict__ keys = reinterpret_cast<unsigned long long*>(J.keys);
   const double tilt_c = J.tilt_c, tilt_s = J.tilt_s;
-  const int groups = (n_live + 31) >> 5;
   unsigned n_dep = 0, n_atom = 0;
-
-  // unit = (group g of 32 live steps, chunk q), dealt round-robin to the
-  // warps in (g, q) order; the lane's transform is reloaded only when g
+  // unit = (group of consecutive live steps, chunk q), dealt round-robin to
+  // the warps in (g, q) order; the lane's transforms are reloaded only when g
   // changes, and (g, q) advance without a division
   int g = warp / nchunk, q = warp - (warp / nchunk) * nchunk;
-  int g_loaded = -1, rt = 0;
-  double r[RW];
-  for (; g < groups; next_unit(g, q, nchunk)) {
-    const int slot = g * 32 + lane;
-    if (g != g_loaded) {  // warp-uniform
-      g_loaded = g;
-      rt = slot < n_live ? live[slot] : -1;
+  int g_loaded = -1;
+  if constexpr (kPairSteps) {
+    // unit = (group g of 64 consecutive live steps, chunk q); lane l holds the
+    // group's steps 2l (A) and 2l+1 (B), so one broadcast point record serves
+    // two evaluations and half of the neighbour exchange stays in registers
+    const int groups = (n_live + 63) >> 6;
+    int rta = 0, rtb = 0;
+    double ra[RW], rb[RW];
+    for (; g < groups; next_unit(g, q, nchunk)) {
+      const int sa = g * 64 + 2 * lane, sb = sa + 1;
+      if (g != g_loaded) {  // warp-uniform
+        g_loaded = g;
+        rta = sa < n_live ? live[sa] : -1;
+        rtb = sb < n_live ? live[sb] : -1;
 #pragma unroll
-      for (int k = 0; k < RW; ++k) r[k] = rt >= 0 ? rowv[slot * 8 + k] : 0.0;
-    }
-    const bool on = rt >= 0 && ((masks[rt * mask_words + (q >> 6)] >> (q & 63)) & 1ull);
-    if (!__any_sync(0xffffffffu, on)) continue;
-    // lanes whose step is not live for this chunk: i index pushed far out of
-    // range, so the per-point range test also covers `on`
-    const int ibias = on ? kMagicHi : kMagicHi - (1 << 30);
-    const int p_end = min(32, npts - q * 32);
-    // stage the chunk's 32 point records (1 KB, coalesced) for broadcast
-    // reads; slots past the chunk's end hold zeros (finite, masked below)
-    __syncwarp();
-    {
-      double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
-      if (lane < p_end) {
-        const double2* src = reinterpret_cast<const double2*>(pts + q * 32 + lane);
-        const double2 a = __ldg(src), b = __ldg(src + 1);
-        v = make_double4(a.x, a.y, b.x, b.y);
+        for (int k = 0; k < RW; ++k) {
+          ra[k] = rta >= 0 ? rowv[sa * 8 + k] : 0.0;
+          rb[k] = rtb >= 0 ? rowv[sb * 8 + k] : 0.0;
+        }
       }
-      ptstage[warp][lane] = v;
-    }
-    __syncwarp();
-    // Two points per iteration with no divergent branch between their
-    // evaluations (the compiler interleaves the two dependent fp64 chains).
-    // Near-boundary points (probability ~1e-9 each) are not resolved inline:
-    // they are flagged, kept out of the neighbour comparisons (treated as
-    // outside), and deposited after the chunk with the exact reference index
-    // — an extra deposit is always safe, a skipped one never is.
-    bool anynear = false;
-    // 8 iterations (16 points) per unrolled body: the scheduler can overlap
-    // one pair's shuffles/REDs with the next pair's fp64 chain (measured:
-    // 1.11 -> 1.07 ms on config 2; 16 iterations: slower, i-cache)
+      const bool on_a = rta >= 0 && ((masks[rta * mask_words + (q >> 6)] >> (q & 63)) & 1ull);
+      const bool on_b = rtb >= 0 && ((masks[rtb * mask_words + (q >> 6)] >> (q & 63)) & 1ull);
+      if (!__any_sync(0xffffffffu, on_a | on_b)) continue;
+      const int ibias_a = on_a ? kMagicHi : kMagicHi - (1 << 30);
+      const int ibias_b = on_b ? kMagicHi : kMagicHi - (1 << 30);
+      const int p_end = min(32, npts - q * 32);
+      // stage the chunk's 32 point records (1 KB, coalesced) for broadcast
+      // reads; slots past the chunk's end hold zeros (finite, masked below)
+      __syncwarp();
+      {
+        double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+        if (lane < p_end) {
+          const double2* src = reinterpret_cast<const double2*>(pts + q * 32 + lane);
+          const double2 a = __ldg(src), b = __ldg(src + 1);
+          v = make_double4(a.x, a.y, b.x, b.y);
+        }
+        ptstage[warp][lane] = v;
+      }
+      __syncwarp();
+      // Near-boundary points (probability ~1e-9 each) are not resolved inline:
+      // they are flagged, kept out of the neighbour comparisons (treated as
+      // outside), and deposited after the chunk with the exact reference index
+      // — an extra deposit is always safe, a skipped one never is.
+      bool anynear = false;
+      // one point per iteration evaluated under both of the lane's steps (two
+      // independent fp64 chains). Neighbours in time: A's predecessor is the
+      // previous lane's B, B's successor the next lane's A (two shuffles each),
+      // A-B within the lane in registers. The edge lanes get their own values
+      // back from the shuffles, i.e. compare with their other step, which is a
+      // neighbour anyway: no lane tests in the tilt filter.
 #pragma unroll kKUnroll
-    for (int k = 0; k < p_end; k += 2) {
-      const int ibias_b = (k + 1 < p_end) ? ibias : kMagicHi - (1 << 30);
-      PointEval ea = eval_point<MODE>(ptstage[warp][k], r, inv, cx0, cy0, tilt_c, tilt_s);
-      PointEval eb = eval_point<MODE>(ptstage[warp][k + 1], r, inv, cx0, cy0, tilt_c, tilt_s);
-      const int ia = ea.hi_x - ibias, ja = ea.hi_y - jbias;
-      const int ib = eb.hi_x - ibias_b, jb = eb.hi_y - jbias;
-      // near flags of live points (the fast index may be off by one there, so
-      // the range test must not filter them)
-      anynear |= (ea.near | (eb.near & (k + 1 < p_end))) & on;
-      const bool in_a = ((unsigned)ia <= span_i) & ((unsigned)ja <= span_j) & !ea.near;
-      const bool in_b = ((unsigned)ib <= span_i) & ((unsigned)jb <= span_j) & !eb.near;
-      const int idx_a = in_a ? ia * ldk + ja : -1;
-      const int idx_b = in_b ? ib * ldk + jb : -1;
-      bool dep_a, dep_b;
-      dedupe<MODE>(lane, idx_a, in_a, ea.zh, dep_a);
-      dedupe<MODE>(lane, idx_b, in_b, eb.zh, dep_b);
-      if (DIAG) {
-        n_dep += (unsigned)in_a + (unsigned)in_b;
-        n_atom += (unsigned)dep_a + (unsigned)dep_b;
-      }
-      red_min_u64_if(keys + idx_a, (unsigned long long)ea.key, dep_a);
-      red_min_u64_if(keys + idx_b, (unsigned long long)eb.key, dep_b);
-    }
-    if (__builtin_expect(__any_sync(0xffffffffu, anynear), 0)) {
       for (int k = 0; k < p_end; ++k) {
-        const PointEval e = eval_point<MODE>(ptstage[warp][k], r, inv, cx0, cy0, tilt_c, tilt_s);
-        if (!(e.near & on)) continue;
-        const int ie = cell_index_exact(e.xw, J.x_min, dd);
-        const int je = cell_index_exact(e.yw, J.y_min, dd) - j_lo;
-        const bool in = on & ((unsigned)ie <= span_i) & ((unsigned)je <= span_j);
-        if (in) red_min_u64(keys + (ie * ldk + je), (unsigned long long)e.key);
+        const double4 pt = ptstage[warp][k];
+        PointEval ea = eval_point<MODE>(pt, ra, inv, cx0, cy0, tilt_c, tilt_s);
+        PointEval eb = eval_point<MODE>(pt, rb, inv, cx0, cy0, tilt_c, tilt_s);
+        const int ia = ea.hi_x - ibias_a, ja = ea.hi_y - jbias;
+        const int ib = eb.hi_x - ibias_b, jb = eb.hi_y - jbias;
+        anynear |= (ea.near & on_a) | (eb.near & on_b);
+        const bool in_a = ((unsigned)ia <= span_i) & ((unsigned)ja <= span_j) & !ea.near;
+        const bool in_b = ((unsigned)ib <= span_i) & ((unsigned)jb <= span_j) & !eb.near;
+        const int idx_a = in_a ? ia * ldk + ja : -1;
+        const int idx_b = in_b ? ib * ldk + jb : -1;
+        const int idx_bp = __shfl_up_sync(0xffffffffu, idx_b, 1);  // A's predecessor (lane 0: own B)
+        bool dep_a, dep_b;
+        if (MODE == MSURF_MODE_EXT_TILT) {
+          const unsigned zh_bp = __shfl_up_sync(0xffffffffu, eb.zh, 1);
+          const int idx_an = __shfl_down_sync(0xffffffffu, idx_a, 1);  // B's successor (lane 31: own A)
+          const unsigned zh_an = __shfl_down_sync(0xffffffffu, ea.zh, 1);
+          const bool ab = idx_a == idx_b;
+          dep_a = in_a & !((idx_a == idx_bp) & (ea.zh > zh_bp)) & !(ab & (ea.zh > eb.zh));
+          dep_b = in_b & !(ab & (eb.zh > ea.zh)) & !((idx_b == idx_an) & (eb.zh > zh_an));
+        } else {
+          // constant z' per point: only each run's first step deposits
+          dep_a = in_a & ((lane == 0) | (idx_a != idx_bp));
+          dep_b = in_b & (idx_b != idx_a);
+        }
         if (DIAG) {
-          n_dep += in;
-          n_atom += in;
+          n_dep += (unsigned)in_a + (unsigned)in_b;
+          n_atom += (unsigned)dep_a + (unsigned)dep_b;
+        }
+        red_min_u64_if(keys + idx_a, (unsigned long long)ea.key, dep_a);
+        red_min_u64_if(keys + idx_b, (unsigned long long)eb.key, dep_b);
+      }
+      if (__builtin_expect(__any_sync(0xffffffffu, anynear), 0)) {
+        for (int k = 0; k < p_end; ++k) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const PointEval e = eval_point<MODE>(ptstage[warp][k], h ? rb : ra, inv, cx0, cy0, tilt_c, tilt_s);
+            if (!(e.near & (h ? on_b : on_a))) continue;
+            const int ie = cell_index_exact(e.xw, J.x_min, dd);
+            const int je = cell_index_exact(e.yw, J.y_min, dd) - j_lo;
+            const bool in = ((unsigned)ie <= span_i) & ((unsigned)je <= span_j);
+            if (in) red_min_u64(keys + (ie * ldk + je), (unsigned long long)e.key);
+            if (DIAG) {
+              n_dep += in;
+              n_atom += in;
+            }
+          }
         }
       }
     }
+  } else {
+    // unit = (group of 32 live steps, chunk q), lane = one step
+    const int groups = (n_live + 31) >> 5;
+    int rt = 0;
+    double r[RW];
+    for (; g < groups; next_unit(g, q, nchunk)) {
+      const int slot = g * 32 + lane;
+      if (g != g_loaded) {  // warp-uniform
+        g_loaded = g;
+        rt = slot < n_live ? live[slot] : -1;
+#pragma unroll
+        for (int k = 0; k < RW; ++k) r[k] = rt >= 0 ? rowv[slot * 8 + k] : 0.0;
+      }
+      const bool on = rt >= 0 && ((masks[rt * mask_words + (q >> 6)] >> (q & 63)) & 1ull);
+      if (!__any_sync(0xffffffffu, on)) continue;
+      // lanes whose step is not live for this chunk: i index pushed far out of
+      // range, so the per-point range test also covers `on`
+      const int ibias = on ? kMagicHi : kMagicHi - (1 << 30);
+      const int p_end = min(32, npts - q * 32);
+      // stage the chunk's 32 point records (1 KB, coalesced) for broadcast
+      // reads; slots past the chunk's end hold zeros (finite, masked below)
+      __syncwarp();
+      {
+        double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+        if (lane < p_end) {
+          const double2* src = reinterpret_cast<const double2*>(pts + q * 32 + lane);
+          const double2 a = __ldg(src), b = __ldg(src + 1);
+          v = make_double4(a.x, a.y, b.x, b.y);
+        }
+        ptstage[warp][lane] = v;
+      }
+      __syncwarp();
+      // Near-boundary points (probability ~1e-9 each) are not resolved inline:
+      // they are flagged, kept out of the neighbour comparisons (treated as
+      // outside), and deposited after the chunk with the exact reference index
+      // — an extra deposit is always safe, a skipped one never is.
+      bool anynear = false;
+      // Two points per iteration with no divergent branch between their
+      // evaluations (the compiler interleaves the two dependent fp64 chains).
+      // Near-boundary points (probability ~1e-9 each) are not resolved inline:
+      // they are flagged, kept out of the neighbour comparisons (treated as
+      // outside), and deposited after the chunk with the exact reference index
+      // — an extra deposit is always safe, a skipped one never is.
+      // 8 iterations (16 points) per unrolled body: the scheduler can overlap
+      // one pair's shuffles/REDs with the next pair's fp64 chain (measured:
+      // 1.11 -> 1.07 ms on config 2; 16 iterations: slower, i-cache)
+#pragma unroll kKUnroll
+      for (int k = 0; k < p_end; k += 2) {
+        const int ibias_b = (k + 1 < p_end) ? ibias : kMagicHi - (1 << 30);
+        PointEval ea = eval_point<MODE>(ptstage[warp][k], r, inv, cx0, cy0, tilt_c, tilt_s);
+        PointEval eb = eval_point<MODE>(ptstage[warp][k + 1], r, inv, cx0, cy0, tilt_c, tilt_s);
+        const int ia = ea.hi_x - ibias, ja = ea.hi_y - jbias;
+        const int ib = eb.hi_x - ibias_b, jb = eb.hi_y - jbias;
+        // near flags of live points (the fast index may be off by one there, so
+        // the range test must not filter them)
+        anynear |= (ea.near | (eb.near & (k + 1 < p_end))) & on;
+        const bool in_a = ((unsigned)ia <= span_i) & ((unsigned)ja <= span_j) & !ea.near;
+        const bool in_b = ((unsigned)ib <= span_i) & ((unsigned)jb <= span_j) & !eb.near;
+        const int idx_a = in_a ? ia * ldk + ja : -1;
+        const int idx_b = in_b ? ib * ldk + jb : -1;
+        bool dep_a, dep_b;
+        dedupe<MODE>(lane, idx_a, in_a, ea.zh, dep_a);
+        dedupe<MODE>(lane, idx_b, in_b, eb.zh, dep_b);
+        if (DIAG) {
+          n_dep += (unsigned)in_a + (unsigned)in_b;
+          n_atom += (unsigned)dep_a + (unsigned)dep_b;
+        }
+        red_min_u64_if(keys + idx_a, (unsigned long long)ea.key, dep_a);
+        red_min_u64_if(keys + idx_b, (unsigned long long)eb.key, dep_b);
+      }
+      if (__builtin_expect(__any_sync(0xffffffffu, anynear), 0)) {
+        for (int k = 0; k < p_end; ++k) {
+          const PointEval e = eval_point<MODE>(ptstage[warp][k], r, inv, cx0, cy0, tilt_c, tilt_s);
+          if (!(e.near & on)) continue;
+          const int ie = cell_index_exact(e.xw, J.x_min, dd);
+          const int je = cell_index_exact(e.yw, J.y_min, dd) - j_lo;
+          const bool in = on & ((unsigned)ie <= span_i) & ((unsigned)je <= span_j);
+          if (in) red_min_u64(keys + (ie * ldk + je), (unsigned long long)e.key);
+          if (DIAG) {
+            n_dep += in;
+            n_atom += in;
+          }
+        }
+      }
+    }
+
+
   }
 
   // counters: one atomic per warp

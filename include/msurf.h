@@ -20,7 +20,7 @@
 extern "C" {
 #endif
 
-#define MSURF_ABI_VERSION 1
+#define MSURF_ABI_VERSION 2
 
 /* kinematics mode of a sweep launch (uniform across the jobs of one launch) */
 #define MSURF_MODE_REF 0      /* reference composite-matrix order, engine.py:257-296 */
@@ -66,6 +66,9 @@ typedef struct msurf_job {
   const double* tooth_box;   /* [teeth][6] whole-tooth tool-frame box (P_eng counter)  */
   const double* chunk_circ;  /* [teeth][nchunk][6] cull record per 32-point chunk:
                               * (xc, yc, rx, ry, yz, 0) — see planner._chunk_circles */
+  const float* chunk_f32;    /* [teeth][nchunk][8] fp32 copy the kernel's phase-1 cull
+                              * reads: (xc, yc, rx, ry, yz, Rt, 0, 0), Rt = the tooth's
+                              * bound max|x| + max|y| + max|z| (planner.chunk_f32)    */
   const double* pass_x0;     /* [passes] spindle x of each raster pass               */
   /* extended kinematics */
   double tilt_c, tilt_s, zoff;  /* zoff: surface z offset (EXT_TILT: folded into pts) */

@@ -18,7 +18,7 @@ from .errors import MillsurfError, NativeUnavailableError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MSURF_LIB") or os.path.join(_HERE, "libmsurf.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 NUM_CTRS = 5
 SWEEP_DIAG = 0x100  # MSURF_SWEEP_DIAG: count deposits/atomics per point
 RED_BLOCKS = 1024
@@ -38,7 +38,8 @@ class MsurfJob(ctypes.Structure):
         ("step_lo", c_int64), ("step_hi", c_int64),
         ("y0", c_double), ("feed_speed", c_double), ("omega", c_double),
         ("tooth_base", c_void_p), ("tooth_rows", c_void_p),
-        ("pts", c_void_p), ("tooth_box", c_void_p), ("chunk_circ", c_void_p), ("pass_x0", c_void_p),
+        ("pts", c_void_p), ("tooth_box", c_void_p), ("chunk_circ", c_void_p), ("chunk_f32", c_void_p),
+        ("pass_x0", c_void_p),
         ("tilt_c", c_double), ("tilt_s", c_double), ("zoff", c_double),
         ("vib_amp", c_double), ("vib_omega", c_double), ("vib_phase", c_double),
         ("trig_table", c_void_p), ("vib_table", c_void_p),

@@ -1,22 +1,25 @@
 // libmsurf.so — B200 (sm_100a) kernels for the FSM surface-topography hot path
 // of arXiv 2603.28160 (reference package `millsurf`), behind the C ABI in
-// include/msurf.h.
+// include/msurf.h (design and measurements: DESIGN.md §4).
 //
-//  * sweep_kernel<MODE>: engine.py:215-313 for all (pass, tooth, step, edge
-//    point) of one or many surfaces. One CTA = one (surface, pass, tooth, tile
-//    of 256 time steps). Phase 1: one thread per step hoists the fp64 trig
-//    and the composite coefficients and builds a per-(step, 32-point chunk)
-//    2-D bounding-box cull mask (generalises the x-only row cull of
-//    engine.py:272-287), then compacts the live steps in order. Phase 2: one
-//    warp per 32-point chunk, one lane per edge point, walks the live steps in
-//    time order: affine transform in the reference's exact op order, cell
-//    location with the reference's exact IEEE division on near-boundary
-//    points, and a run-length min pre-reduction in registers (consecutive
-//    steps of one point mostly land in the same cell), flushed to HBM as an
-//    atomicMin on order-preserving u64 keys after a stale-read skip.
-//  * decode / areal pass1+pass2 / profiles: deterministic fixed-partition
-//    warp-shuffle + block reductions (roughness.py:76-188).
-//  * microbenchmarks for the FP64 and atomic roofline denominators.
+//  * sweep_kernel<MODE, DIAG, ONE>: engine.py:215-313 for all (pass, tooth,
+//    step, edge point) of one or many surfaces. One CTA = one (job, pass,
+//    tooth, tile of 128 time steps). Phase 1: one thread per step hoists the
+//    fp64 trig (correctly rounded double-double sincos) and the transform, and
+//    builds a per-(step, 32-point chunk) 2-D cull mask in fp32 with a proven
+//    margin (generalises the x-only row cull of engine.py:272-287); live steps
+//    are compacted in time order. Phase 2: lane = live step (tilt: two
+//    consecutive live steps), warp = (group of live steps, 32-point chunk);
+//    per point the affine transform in the exact reference / extended-model
+//    op order, the cell index from an fma + magic-number add (near-boundary
+//    points deferred to an exact fix-up with the reference's IEEE division),
+//    a time-neighbour run filter through lane shuffles, and RED.MIN on
+//    order-preserving u64 keys. ONE: the job descriptor is a by-value kernel
+//    parameter (constant-bank operands).
+//  * decode / areal pass1+pass2 / plane passes / profiles / graymap:
+//    deterministic fixed-partition warp-shuffle + block reductions and
+//    HBM-streaming kernels (roughness.py:76-188, surface_io.py:100-131).
+//  * microbenchmarks for the fp64 and RED.MIN roofline denominators.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -254,8 +257,7 @@ __global__ void __launch_bounds__(kSweepThreads, ONE ? MSURF_MIN_BLOCKS_ONE : MS
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* rowv = reinterpret_cast<double*>(smem_raw);                        // [T][8] by live slot
   uint64_t* masks = reinterpret_cast<uint64_t*>(rowv + kTileSteps * 8);      // [T][W] by thread
-  int* live = reinterpret_cast<int*>(masks + kTileSteps * mask_words);       // [T] slot -> thread
-  float4* ccf = reinterpret_cast<float4*>(live + kTileSteps);                // [nchunk] xc yc rx ry (f32)
+  uint64_t* mslot = masks + kTileSteps * mask_words;                         // [T][W] by live slot
   __shared__ msurf_job Js;
   // ONE: a single job passed by value -> its fields are constant-bank operands
   // (no registers, no shared-memory loads); else the CTA's job from the array
@@ -300,23 +302,10 @@ __global__ void __launch_bounds__(kSweepThreads, ONE ? MSURF_MIN_BLOCKS_ONE : MS
   const double dd = J.spacing;
   const double4* __restrict__ pts = reinterpret_cast<const double4*>(J.pts) + (long long)tooth * npts;
 
-  // fp32 copy of this tooth's chunk cull records for phase 1, and the bound
-  // Rt >= |xc| + |yc| + |yz| of every chunk (from the whole-tooth box)
-  {
-    const double* cc = J.chunk_circ + (long long)tooth * nchunk * 6;
-    float* czw = reinterpret_cast<float*>(ccf + nchunk);
-    for (int qq = tid; qq < nchunk; qq += kSweepThreads) {
-      const double* c6 = cc + qq * 6;
-      ccf[qq] = make_float4((float)c6[0], (float)c6[1], (float)c6[2], (float)c6[3]);
-      czw[qq] = (float)c6[4];
-    }
-  }
-  __syncthreads();
-  float rt_f;
-  {
-    const double* b = J.tooth_box + tooth * 6;
-    rt_f = (float)(fmax(fabs(b[0]), fabs(b[1])) + fmax(fabs(b[2]), fabs(b[3])) + fmax(fabs(b[4]), fabs(b[5])));
-  }
+  // this tooth's fp32 chunk cull records (host-made, L1-resident after the
+  // first warp touches them) and the bound Rt >= |xc| + |yc| + |yz|
+  const float4* __restrict__ cf4 = reinterpret_cast<const float4*>(J.chunk_f32) + (long long)tooth * nchunk * 2;
+  const float rt_f = __ldg(reinterpret_cast<const float*>(cf4) + 5);
 
   // ---------------- phase 1: one thread per time step of the tile
   bool any = false, engaged = false;
@@ -417,13 +406,13 @@ __global__ void __launch_bounds__(kSweepThreads, ONE ? MSURF_MIN_BLOCKS_ONE : MS
           const float tcf = MODE == MSURF_MODE_EXT_TILT ? (float)J.tilt_c : 1.0f;
           const float hx = (float)wxh + (4e-6f * (rt_f + fabsf(oxf)) + 1e-6f);
           const float hy = (float)wyh + (4e-6f * (rt_f + fabsf(oyf)) + 1e-6f);
-          const float* cz = reinterpret_cast<const float*>(ccf + nchunk);
           unsigned kept = 0;
           for (int q = 0; q < nchunk; ++q) {
-            const float4 a = ccf[q];
+            const float4 a = __ldg(cf4 + 2 * q);
+            const float yz = __ldg(reinterpret_cast<const float*>(cf4 + 2 * q + 1));
             const float uc = fmaf(cf, a.x, sf * a.y);
             const float vc = fmaf(cf, a.y, -(sf * a.x));
-            const bool hit = (fabsf(uc + oxf) <= hx + a.z) & (fabsf(fmaf(tcf, vc, cz[q]) + oyf) <= hy + a.w);
+            const bool hit = (fabsf(uc + oxf) <= hx + a.z) & (fabsf(fmaf(tcf, vc, yz) + oyf) <= hy + a.w);
             if (hit) {
               my_mask[q >> 6] |= 1ull << (q & 63);
               kept += (q == nchunk - 1) ? (unsigned)(npts - 32 * q) : 32u;
@@ -456,7 +445,7 @@ __global__ void __launch_bounds__(kSweepThreads, ONE ? MSURF_MIN_BLOCKS_ONE : MS
   }
   if (any) {
     const int slot = base + __popc(bal & ((1u << lane) - 1u));
-    live[slot] = tid;
+    for (int w = 0; w < mask_words; ++w) mslot[slot * mask_words + w] = masks[tid * mask_words + w];
 #pragma unroll
     for (int k = 0; k < RW; ++k) rowv[slot * 8 + k] = rd[k];
   }
@@ -503,16 +492,16 @@ __global__ void __launch_bounds__(kSweepThreads, ONE ? MSURF_MIN_BLOCKS_ONE : MS
       const int sa = g * 64 + 2 * lane, sb = sa + 1;
       if (g != g_loaded) {  // warp-uniform
         g_loaded = g;
-        rta = sa < n_live ? live[sa] : -1;
-        rtb = sb < n_live ? live[sb] : -1;
+        rta = sa < n_live ? sa : -1;
+        rtb = sb < n_live ? sb : -1;
 #pragma unroll
         for (int k = 0; k < RW; ++k) {
           ra[k] = rta >= 0 ? rowv[sa * 8 + k] : 0.0;
           rb[k] = rtb >= 0 ? rowv[sb * 8 + k] : 0.0;
         }
       }
-      const bool on_a = rta >= 0 && ((masks[rta * mask_words + (q >> 6)] >> (q & 63)) & 1ull);
-      const bool on_b = rtb >= 0 && ((masks[rtb * mask_words + (q >> 6)] >> (q & 63)) & 1ull);
+      const bool on_a = rta >= 0 && ((mslot[rta * mask_words + (q >> 6)] >> (q & 63)) & 1ull);
+      const bool on_b = rtb >= 0 && ((mslot[rtb * mask_words + (q >> 6)] >> (q & 63)) & 1ull);
       if (!__any_sync(0xffffffffu, on_a | on_b)) continue;
       const int ibias_a = on_a ? kMagicHi : kMagicHi - (1 << 30);
       const int ibias_b = on_b ? kMagicHi : kMagicHi - (1 << 30);
@@ -601,11 +590,11 @@ __global__ void __launch_bounds__(kSweepThreads, ONE ? MSURF_MIN_BLOCKS_ONE : MS
       const int slot = g * 32 + lane;
       if (g != g_loaded) {  // warp-uniform
         g_loaded = g;
-        rt = slot < n_live ? live[slot] : -1;
+        rt = slot < n_live ? slot : -1;
 #pragma unroll
         for (int k = 0; k < RW; ++k) r[k] = rt >= 0 ? rowv[slot * 8 + k] : 0.0;
       }
-      const bool on = rt >= 0 && ((masks[rt * mask_words + (q >> 6)] >> (q & 63)) & 1ull);
+      const bool on = rt >= 0 && ((mslot[rt * mask_words + (q >> 6)] >> (q & 63)) & 1ull);
       if (!__any_sync(0xffffffffu, on)) continue;
       // lanes whose step is not live for this chunk: i index pushed far out of
       // range, so the per-point range test also covers `on`
@@ -1256,9 +1245,7 @@ static int sweep_impl(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile
   if (n_tiles > 0x7fffffffLL) return set_err("msurf_sweep: too many tiles");
   const int nchunk = (max_points + 31) / 32;
   const int mask_words = (nchunk + 63) / 64;
-  const size_t smem = (size_t)kTileSteps * 8 * sizeof(double) +
-                      (size_t)kTileSteps * mask_words * sizeof(uint64_t) + (size_t)kTileSteps * sizeof(int) +
-                      (size_t)nchunk * (sizeof(float4) + sizeof(float));
+  const size_t smem = (size_t)kTileSteps * 8 * sizeof(double) + (size_t)2 * kTileSteps * mask_words * sizeof(uint64_t);
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
   const bool diag = (mode & MSURF_SWEEP_DIAG) != 0;

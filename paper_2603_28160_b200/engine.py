@@ -25,7 +25,7 @@ from . import _native
 from .errors import ConfigError, MillsurfError
 from .extensions import Extensions
 from .grid import GridSpec, HeightField, TrajectoryRecord
-from .planner import MODE_REF, SweepPlan, plan, plan_many, step_window, time_step
+from .planner import MODE_REF, SweepPlan, chunk_f32, plan, plan_many, step_window, time_step
 
 DEFAULT_MAX_STEP_ANGLE_RAD = math.radians(0.5)
 # Z-map bytes one sweep job may cover: keeps its RED.MIN traffic in the
@@ -178,6 +178,7 @@ class SweepBatch:
                 pts=ar.add(p.pts.astype(np.float64, copy=False)),
                 tooth_box=ar.add(p.tooth_box.astype(np.float64, copy=False)),
                 chunk_circ=ar.add(p.chunk_circ.astype(np.float64, copy=False)),
+                chunk_f32=ar.add(chunk_f32(p.chunk_circ, p.tooth_box)),
                 pass_x0=ar.add(p.pass_x0.astype(np.float64, copy=False)),
                 min_index=ar.add(p.min_index.astype(np.int32, copy=False)),
             )
@@ -253,7 +254,7 @@ class SweepBatch:
                     j.t_start, j.dt, j.steps = p.t_start, p.dt, p.steps
                     j.step_lo, j.step_hi = s_lo, s_hi
                     j.y0, j.feed_speed, j.omega = p.y0, p.feed_speed, p.omega
-                    for name in ("tooth_base", "tooth_rows", "pts", "tooth_box", "chunk_circ",
+                    for name in ("tooth_base", "tooth_rows", "pts", "tooth_box", "chunk_circ", "chunk_f32",
                                  "pass_x0", "min_index"):
                         setattr(j, name, base + o[name])
                     j.counters = base + self.ctr_off + i * _native.NUM_CTRS * 8

@@ -258,6 +258,20 @@ def _pack(p: SweepPlan) -> None:
                             b[:, :, 4].min(1), b[:, :, 5].max(1)], axis=1)
 
 
+def chunk_f32(chunk_circ: np.ndarray, tooth_box: np.ndarray) -> np.ndarray:
+    """fp32 phase-1 cull records (msurf_job.chunk_f32): per tooth and chunk
+    (xc, yc, rx, ry, yz, Rt, 0, 0), Rt = max|x| + max|y| + max|z| of the tooth
+    box. The kernel widens its fp32 test by 4e-6 (Rt + |offset|) + 1e-6 mm,
+    which covers the fp32 roundings of every term."""
+    z_n, nchunk, _ = chunk_circ.shape
+    out = np.zeros((z_n, nchunk, 8), dtype=np.float32)
+    out[:, :, :5] = chunk_circ[:, :, :5]
+    b = np.abs(tooth_box)
+    rt = np.maximum(b[:, 0], b[:, 1]) + np.maximum(b[:, 2], b[:, 3]) + np.maximum(b[:, 4], b[:, 5])
+    out[:, :, 5] = rt[:, None]
+    return out
+
+
 def _check_device_limits(p: SweepPlan, grid) -> None:
     if p.points > MAX_POINTS:
         raise ConfigError(f"edge_point_count {p.points} exceeds the device limit {MAX_POINTS}")

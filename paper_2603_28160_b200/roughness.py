@@ -325,7 +325,9 @@ def _profiles_device(h_dev, n_surf, surf_stride, starts, length, step, sentinels
     lib = _native.lib()
     dev = h_dev.device
     n_prof = len(starts)
-    st = torch.tensor(np.asarray(starts, dtype=np.int64), device=dev)
+    # profile offsets through pinned memory: an asynchronous H2D (a pageable
+    # copy would block the host until the stream drains)
+    st = torch.from_numpy(np.asarray(starts, dtype=np.int64)).pin_memory().to(dev, non_blocking=True)
     out = torch.empty(n_surf * n_prof * 8, dtype=torch.float64, device=dev)
     _native.check(lib.msurf_profiles(h_dev.data_ptr(), surf_stride, n_surf, st.data_ptr(), n_prof,
                                      length, step, sentinels_dev.data_ptr(), int(exclude),

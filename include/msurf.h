@@ -20,7 +20,7 @@
 extern "C" {
 #endif
 
-#define MSURF_ABI_VERSION 2
+#define MSURF_ABI_VERSION 3
 
 /* kinematics mode of a sweep launch (uniform across the jobs of one launch) */
 #define MSURF_MODE_REF 0      /* reference composite-matrix order, engine.py:257-296 */
@@ -105,10 +105,10 @@ int msurf_sweep(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile_prefi
 
 /* The same sweep for ONE job given as a HOST pointer: the descriptor is
  * passed by value as a kernel parameter, so the kernel reads its fields as
- * constant-bank operands (fewer registers, no per-CTA descriptor copy);
- * n_tiles = passes*teeth*ceil((step_hi-step_lo)/tile_steps). Device pointers
- * inside the job are used as in msurf_sweep. */
-int msurf_sweep_job(const msurf_job* job, int64_t n_tiles, int32_t mode, int32_t max_points, void* stream);
+ * constant-bank operands (fewer registers, no per-CTA descriptor copy). The
+ * library picks the CTA shape for the mode and sizes the grid itself. Device
+ * pointers inside the job are used as in msurf_sweep. */
+int msurf_sweep_job(const msurf_job* job, int32_t mode, int32_t max_points, void* stream);
 
 /* Decode keys to fp64 heights in place and count machined cells
  * (HeightField.machined_cell_count, surface_grid.py:128-129). Batched over

@@ -18,7 +18,7 @@ from .errors import MillsurfError, NativeUnavailableError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MSURF_LIB") or os.path.join(_HERE, "libmsurf.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 NUM_CTRS = 5
 SWEEP_DIAG = 0x100  # MSURF_SWEEP_DIAG: count deposits/atomics per point
 RED_BLOCKS = 1024
@@ -66,7 +66,7 @@ EXPORTS = {
     "msurf_tile_steps": (ctypes.c_int, []),
     "msurf_fill_keys": (ctypes.c_int, [c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
     "msurf_sweep": (ctypes.c_int, [c_void_p, c_int32, c_void_p, c_int64, c_int32, c_int32, c_void_p]),
-    "msurf_sweep_job": (ctypes.c_int, [c_void_p, c_int64, c_int32, c_int32, c_void_p]),
+    "msurf_sweep_job": (ctypes.c_int, [c_void_p, c_int32, c_int32, c_void_p]),
     "msurf_decode": (ctypes.c_int, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p]),
     "msurf_areal_pass1": (ctypes.c_int, [c_void_p, c_int64, c_int64, c_int32, c_int64, c_int64,
                                          c_int64, c_int64, c_void_p, c_int32, c_void_p, c_void_p,

@@ -32,22 +32,27 @@
 
 namespace {
 
+// Sweep CTA shapes (measured on configs 1-5). Batched job
+// arrays and the tilt mode: one warp per CTA over a 64-step tile (two phase-1
+// rounds, no CTA-wide barrier). Single non-tilt surfaces (configs 1, 4): four
+// warps over 128 steps (fewer, larger CTAs balance better there).
+constexpr int kBatchTile = 64, kBatchThreads = 32;   // msurf_sweep (job arrays)
+constexpr int kTiltTile = 64, kTiltThreads = 32;     // msurf_sweep_job, EXT_TILT
+constexpr int kWideTile = 128, kWideThreads = 128;   // msurf_sweep_job, REF / EXT
 #ifndef MSURF_MIN_BLOCKS_ONE
-#define MSURF_MIN_BLOCKS_ONE 8  // by-value job: no descriptor registers, 64 regs without spills
+#define MSURF_MIN_BLOCKS_ONE 28  // 1-warp CTAs with a by-value job: 72 registers
 #endif
 #ifndef MSURF_MIN_BLOCKS
-#define MSURF_MIN_BLOCKS 6  // CTAs per SM the register budget is sized for (80 regs at 128 threads)
+#define MSURF_MIN_BLOCKS 24  // 1-warp CTAs with the job array: 80 registers
 #endif
 
-#ifndef MSURF_TILE
-#define MSURF_TILE 128
-#endif
+// CTAs per SM a sweep variant's register budget is sized for
+constexpr int sweep_min_blocks(bool one, int threads) {
+  return threads == 32 ? (one ? MSURF_MIN_BLOCKS_ONE : MSURF_MIN_BLOCKS) : (one ? 8 : 6) * (128 / threads);
+}
 
 constexpr int kThreads = 256;      // reduction / stream kernels
 constexpr int kWarps = kThreads / 32;
-constexpr int kTileSteps = MSURF_TILE;  // sweep: time steps per CTA == threads per CTA
-constexpr int kSweepThreads = kTileSteps;
-constexpr int kSweepWarps = kSweepThreads / 32;
 #ifndef MSURF_PAIR_STEPS
 #define MSURF_PAIR_STEPS 2  // 0: never, 1: always, 2: tilt mode only (see kPairSteps)
 #endif
@@ -235,19 +240,25 @@ __device__ __forceinline__ void dedupe(int lane, int idx, bool inside, unsigned 
   }
 }
 
-// advance a warp's (group, chunk) unit cursor by kSweepWarps units
+// advance a warp's (group, chunk) unit cursor by `warps` units
+template <int WARPS>
 __device__ __forceinline__ void next_unit(int& g, int& q, int nchunk) {
-  q += kSweepWarps;
+  q += WARPS;
   while (q >= nchunk) {
     q -= nchunk;
     ++g;
   }
 }
 
-template <int MODE, bool DIAG, bool ONE>
-__global__ void __launch_bounds__(kSweepThreads, ONE ? MSURF_MIN_BLOCKS_ONE : MSURF_MIN_BLOCKS)
+template <int MODE, bool DIAG, bool ONE, int TILE, int NTHR>
+__global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
     sweep_kernel(const msurf_job* __restrict__ jobs, int n_jobs,
                  const int64_t* __restrict__ prefix, int mask_words, const __grid_constant__ msurf_job jp) {
+  constexpr int kTileSteps = TILE;               // time steps per CTA
+  constexpr int kSweepThreads = NTHR;            // threads per CTA
+  constexpr int kSubSteps = TILE / NTHR;         // phase-1 steps per thread
+  constexpr int kSweepWarps = NTHR / 32;
+  static_assert(TILE % NTHR == 0 && NTHR % 32 == 0, "tile / CTA shape");
   constexpr int RW = MODE == MSURF_MODE_REF ? 8 : 4;  // doubles of row data per live step
   // lane = two consecutive live steps (one broadcast point record serves both,
   // half the neighbour exchange in registers): faster for the tilt mode
@@ -307,149 +318,160 @@ __global__ void __launch_bounds__(kSweepThreads, ONE ? MSURF_MIN_BLOCKS_ONE : MS
   const float4* __restrict__ cf4 = reinterpret_cast<const float4*>(J.chunk_f32) + (long long)tooth * nchunk * 2;
   const float rt_f = __ldg(reinterpret_cast<const float*>(cf4) + 5);
 
-  // ---------------- phase 1: one thread per time step of the tile
-  bool any = false, engaged = false;
-  unsigned my_eval = 0;
-  double rd[RW];
-  {
-    const double wx_lo = J.x_min - 1.5 * dd;
-    const double wx_hi = J.x_min + (double)J.m * dd + 1.5 * dd;
-    const double wy_lo = J.y_min + (double)J.j_lo * dd - 1.5 * dd;
-    const double wy_hi = J.y_min + (double)J.j_hi * dd + 1.5 * dd;
-    const long long s = J.step_lo + (long long)st * kTileSteps + tid;
-    uint64_t* my_mask = masks + tid * mask_words;
-    for (int w = 0; w < mask_words; ++w) my_mask[w] = 0ull;
-    if (s < J.step_hi) {
-      // engine.py:240-241, kinematics.py:77 — one rounding per op, no FMA
-      const double t = __dadd_rn(J.t_start, __dmul_rn((double)s, J.dt));
-      const double ty = __dadd_rn(J.y0, __dmul_rn(J.feed_speed, t));
-      const double th = __dsub_rn(J.tooth_base[tooth], __dmul_rn(J.omega, t));
-      const double x0p = J.pass_x0[pass];
-      // Cheap conservative pre-cull of the whole tooth with a float sincos
-      // (double Cody-Waite reduction, |error| < 1e-6 in c, s -> < 1e-4 mm of
-      // position for a 100 mm tool, covered by the extra margin; vibration
-      // covered by its amplitude): most rows of a windowed strip, and the
-      // rows far from the grid, never pay for the double-double sincos.
-      bool maybe = true;
-      if (!J.trig_table && !(J.traj && pass == 0)) {
-        const double kd = rint(th * MSURF_TWO_OVER_PI);
-        const double r = __fma_rn(-kd, MSURF_PIO2_2, __fma_rn(-kd, MSURF_PIO2_1, th));
-        float sf, cf;
-        __sincosf((float)r, &sf, &cf);
-        const int quad = ((int)(long long)kd) & 3;
-        double ca = cf, sa = sf;
-        if (quad == 1) { ca = -sf; sa = cf; }
-        else if (quad == 2) { ca = -cf; sa = -sf; }
-        else if (quad == 3) { ca = sf; sa = -cf; }
-        const double mg = 1e-4 + fabs(J.vib_amp);
-        maybe = tool_box_hits<MODE>(J.tooth_box + tooth * 6, ca, sa, x0p, ty, wx_lo - mg, wx_hi + mg,
-                                    wy_lo - mg, wy_hi + mg, J.tilt_c, J.tilt_s);
-      }
-      if (maybe) {
-        double c, sn;
-        if (J.trig_table) {
-          c = J.trig_table[(s * J.teeth + tooth) * 2 + 0];
-          sn = J.trig_table[(s * J.teeth + tooth) * 2 + 1];
-        } else {
-          msurf_sincos(th, &sn, &c);
+  // ---------------- phase 1: one thread per time step (kSubSteps rounds of
+  // kSweepThreads steps), live steps appended in time order
+  int n_live = 0;
+  unsigned n_eval_cta = 0, n_eng_cta = 0;
+  for (int h = 0; h < kSubSteps; ++h) {
+    bool any = false, engaged = false;
+    unsigned my_eval = 0;
+    double rd[RW];
+    {
+      const double wx_lo = J.x_min - 1.5 * dd;
+      const double wx_hi = J.x_min + (double)J.m * dd + 1.5 * dd;
+      const double wy_lo = J.y_min + (double)J.j_lo * dd - 1.5 * dd;
+      const double wy_hi = J.y_min + (double)J.j_hi * dd + 1.5 * dd;
+      const long long s = J.step_lo + (long long)st * kTileSteps + h * kSweepThreads + tid;
+      uint64_t* my_mask = masks + tid * mask_words;
+      for (int w = 0; w < mask_words; ++w) my_mask[w] = 0ull;
+      if (s < J.step_hi) {
+        // engine.py:240-241, kinematics.py:77 — one rounding per op, no FMA
+        const double t = __dadd_rn(J.t_start, __dmul_rn((double)s, J.dt));
+        const double ty = __dadd_rn(J.y0, __dmul_rn(J.feed_speed, t));
+        const double th = __dsub_rn(J.tooth_base[tooth], __dmul_rn(J.omega, t));
+        const double x0p = J.pass_x0[pass];
+        // Cheap conservative pre-cull of the whole tooth with a float sincos
+        // (double Cody-Waite reduction, |error| < 1e-6 in c, s -> < 1e-4 mm of
+        // position for a 100 mm tool, covered by the extra margin; vibration
+        // covered by its amplitude): most rows of a windowed strip, and the
+        // rows far from the grid, never pay for the double-double sincos.
+        bool maybe = true;
+        if (!J.trig_table && !(J.traj && pass == 0)) {
+          const double kd = rint(th * MSURF_TWO_OVER_PI);
+          const double r = __fma_rn(-kd, MSURF_PIO2_2, __fma_rn(-kd, MSURF_PIO2_1, th));
+          float sf, cf;
+          __sincosf((float)r, &sf, &cf);
+          const int quad = ((int)(long long)kd) & 3;
+          double ca = cf, sa = sf;
+          if (quad == 1) { ca = -sf; sa = cf; }
+          else if (quad == 2) { ca = -cf; sa = -sf; }
+          else if (quad == 3) { ca = sf; sa = -cf; }
+          const double mg = 1e-4 + fabs(J.vib_amp);
+          maybe = tool_box_hits<MODE>(J.tooth_box + tooth * 6, ca, sa, x0p, ty, wx_lo - mg, wx_hi + mg,
+                                      wy_lo - mg, wy_hi + mg, J.tilt_c, J.tilt_s);
         }
-        const double ns = -sn;
-        double xoff = x0p;
-        if (MODE != MSURF_MODE_REF && J.vib_amp != 0.0) {
-          const double sv = J.vib_table ? J.vib_table[s]
-                                        : msurf_sin(__dadd_rn(__dmul_rn(J.vib_omega, t), J.vib_phase));
-          xoff = __dadd_rn(xoff, __dmul_rn(J.vib_amp, sv));
-        }
-        if (MODE == MSURF_MODE_REF) {
-          // engine.py:257-264 composite coefficients, exact op order
-          const double* e = J.tooth_rows + tooth * 8;
-          rd[0] = __dadd_rn(__dmul_rn(c, e[0]), __dmul_rn(sn, e[4]));
-          rd[1] = __dadd_rn(__dmul_rn(c, e[1]), __dmul_rn(sn, e[5]));
-          rd[2] = __dadd_rn(__dmul_rn(c, e[2]), __dmul_rn(sn, e[6]));
-          rd[3] = __dadd_rn(__dadd_rn(__dmul_rn(c, e[3]), __dmul_rn(sn, e[7])), xoff);
-          rd[4] = __dadd_rn(__dmul_rn(ns, e[0]), __dmul_rn(c, e[4]));
-          rd[5] = __dadd_rn(__dmul_rn(ns, e[1]), __dmul_rn(c, e[5]));
-          rd[6] = __dadd_rn(__dmul_rn(ns, e[2]), __dmul_rn(c, e[6]));
-          rd[7] = __dadd_rn(__dadd_rn(__dmul_rn(ns, e[3]), __dmul_rn(c, e[7])), ty);
-          if (J.traj && pass == 0) {
-            // engine.py:266-270: min-z edge point of this (step, tooth)
-            const double4 pt = pts[J.min_index[tooth]];
-            double* tr = J.traj + (s * J.teeth + tooth) * 3;
-            tr[0] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(rd[0], pt.x), __dmul_rn(rd[1], pt.y)),
-                                        __dmul_rn(rd[2], pt.z)), rd[3]);
-            tr[1] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(rd[4], pt.x), __dmul_rn(rd[5], pt.y)),
-                                        __dmul_rn(rd[6], pt.z)), rd[7]);
-            tr[2] = dec_key((uint64_t)__double_as_longlong(pt.w));
+        if (maybe) {
+          double c, sn;
+          if (J.trig_table) {
+            c = J.trig_table[(s * J.teeth + tooth) * 2 + 0];
+            sn = J.trig_table[(s * J.teeth + tooth) * 2 + 1];
+          } else {
+            msurf_sincos(th, &sn, &c);
           }
-        } else {
-          rd[0] = c;
-          rd[1] = sn;
-          rd[2] = xoff;
-          rd[3] = ty;
-        }
-        engaged = tool_box_hits<MODE>(J.tooth_box + tooth * 6, c, sn, xoff, ty, wx_lo, wx_hi, wy_lo, wy_hi,
-                                      J.tilt_c, J.tilt_s);
-        if (engaged) {
-          // per-chunk bounding circles: x = c*xc + s*yc + xoff +- rx,
-          // y = cos(tau)*(c*yc - s*xc) + yz + ty +- ry, against the window
-          // (centre, half-width) widened by 1.5 cells. Evaluated in fp32 (the
-          // fp64 pipe is the sweep's bottleneck): every term is bounded by
-          // S = |xc| + |yc| + |yz| + |offset| <= Rt + |offset|, the fp32 result
-          // is within ~8 ulp(S) < 1e-6 S of the exact one, and the test is
-          // widened by 4e-6 S + 1e-6 mm, so it stays a superset of the exact
-          // cull (a false positive costs work, never a result).
-          const double wxc = 0.5 * (wx_lo + wx_hi), wxh = 0.5 * (wx_hi - wx_lo);
-          const double wyc = 0.5 * (wy_lo + wy_hi), wyh = 0.5 * (wy_hi - wy_lo);
-          const double ox = xoff - wxc, oy = ty - wyc;
-          const float cf = (float)c, sf = (float)sn;
-          const float oxf = (float)ox, oyf = (float)oy;
-          const float tcf = MODE == MSURF_MODE_EXT_TILT ? (float)J.tilt_c : 1.0f;
-          const float hx = (float)wxh + (4e-6f * (rt_f + fabsf(oxf)) + 1e-6f);
-          const float hy = (float)wyh + (4e-6f * (rt_f + fabsf(oyf)) + 1e-6f);
-          unsigned kept = 0;
-          for (int q = 0; q < nchunk; ++q) {
-            const float4 a = __ldg(cf4 + 2 * q);
-            const float yz = __ldg(reinterpret_cast<const float*>(cf4 + 2 * q + 1));
-            const float uc = fmaf(cf, a.x, sf * a.y);
-            const float vc = fmaf(cf, a.y, -(sf * a.x));
-            const bool hit = (fabsf(uc + oxf) <= hx + a.z) & (fabsf(fmaf(tcf, vc, yz) + oyf) <= hy + a.w);
-            if (hit) {
-              my_mask[q >> 6] |= 1ull << (q & 63);
-              kept += (q == nchunk - 1) ? (unsigned)(npts - 32 * q) : 32u;
+          const double ns = -sn;
+          double xoff = x0p;
+          if (MODE != MSURF_MODE_REF && J.vib_amp != 0.0) {
+            const double sv = J.vib_table ? J.vib_table[s]
+                                          : msurf_sin(__dadd_rn(__dmul_rn(J.vib_omega, t), J.vib_phase));
+            xoff = __dadd_rn(xoff, __dmul_rn(J.vib_amp, sv));
+          }
+          if (MODE == MSURF_MODE_REF) {
+            // engine.py:257-264 composite coefficients, exact op order
+            const double* e = J.tooth_rows + tooth * 8;
+            rd[0] = __dadd_rn(__dmul_rn(c, e[0]), __dmul_rn(sn, e[4]));
+            rd[1] = __dadd_rn(__dmul_rn(c, e[1]), __dmul_rn(sn, e[5]));
+            rd[2] = __dadd_rn(__dmul_rn(c, e[2]), __dmul_rn(sn, e[6]));
+            rd[3] = __dadd_rn(__dadd_rn(__dmul_rn(c, e[3]), __dmul_rn(sn, e[7])), xoff);
+            rd[4] = __dadd_rn(__dmul_rn(ns, e[0]), __dmul_rn(c, e[4]));
+            rd[5] = __dadd_rn(__dmul_rn(ns, e[1]), __dmul_rn(c, e[5]));
+            rd[6] = __dadd_rn(__dmul_rn(ns, e[2]), __dmul_rn(c, e[6]));
+            rd[7] = __dadd_rn(__dadd_rn(__dmul_rn(ns, e[3]), __dmul_rn(c, e[7])), ty);
+            if (J.traj && pass == 0) {
+              // engine.py:266-270: min-z edge point of this (step, tooth)
+              const double4 pt = pts[J.min_index[tooth]];
+              double* tr = J.traj + (s * J.teeth + tooth) * 3;
+              tr[0] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(rd[0], pt.x), __dmul_rn(rd[1], pt.y)),
+                                          __dmul_rn(rd[2], pt.z)), rd[3]);
+              tr[1] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(rd[4], pt.x), __dmul_rn(rd[5], pt.y)),
+                                          __dmul_rn(rd[6], pt.z)), rd[7]);
+              tr[2] = dec_key((uint64_t)__double_as_longlong(pt.w));
             }
+          } else {
+            rd[0] = c;
+            rd[1] = sn;
+            rd[2] = xoff;
+            rd[3] = ty;
           }
-          any = kept != 0;
-          my_eval = kept;
+          engaged = tool_box_hits<MODE>(J.tooth_box + tooth * 6, c, sn, xoff, ty, wx_lo, wx_hi, wy_lo, wy_hi,
+                                        J.tilt_c, J.tilt_s);
+          if (engaged) {
+            // per-chunk bounding circles: x = c*xc + s*yc + xoff +- rx,
+            // y = cos(tau)*(c*yc - s*xc) + yz + ty +- ry, against the window
+            // (centre, half-width) widened by 1.5 cells. Evaluated in fp32 (the
+            // fp64 pipe is the sweep's bottleneck): every term is bounded by
+            // S = |xc| + |yc| + |yz| + |offset| <= Rt + |offset|, the fp32 result
+            // is within ~8 ulp(S) < 1e-6 S of the exact one, and the test is
+            // widened by 4e-6 S + 1e-6 mm, so it stays a superset of the exact
+            // cull (a false positive costs work, never a result).
+            const double wxc = 0.5 * (wx_lo + wx_hi), wxh = 0.5 * (wx_hi - wx_lo);
+            const double wyc = 0.5 * (wy_lo + wy_hi), wyh = 0.5 * (wy_hi - wy_lo);
+            const double ox = xoff - wxc, oy = ty - wyc;
+            const float cf = (float)c, sf = (float)sn;
+            const float oxf = (float)ox, oyf = (float)oy;
+            const float tcf = MODE == MSURF_MODE_EXT_TILT ? (float)J.tilt_c : 1.0f;
+            const float hx = (float)wxh + (4e-6f * (rt_f + fabsf(oxf)) + 1e-6f);
+            const float hy = (float)wyh + (4e-6f * (rt_f + fabsf(oyf)) + 1e-6f);
+            unsigned kept = 0;
+            for (int q = 0; q < nchunk; ++q) {
+              const float4 a = __ldg(cf4 + 2 * q);
+              const float yz = __ldg(reinterpret_cast<const float*>(cf4 + 2 * q + 1));
+              const float uc = fmaf(cf, a.x, sf * a.y);
+              const float vc = fmaf(cf, a.y, -(sf * a.x));
+              const bool hit = (fabsf(uc + oxf) <= hx + a.z) & (fabsf(fmaf(tcf, vc, yz) + oyf) <= hy + a.w);
+              if (hit) {
+                my_mask[q >> 6] |= 1ull << (q & 63);
+                kept += (q == nchunk - 1) ? (unsigned)(npts - 32 * q) : 32u;
+              }
+            }
+            any = kept != 0;
+            my_eval = kept;
+          }
         }
       }
     }
-  }
-  // ordered compaction of live steps (keeps time order for the neighbour merge)
-  const unsigned bal = __ballot_sync(0xffffffffu, any);
-  const unsigned eng = __popc(__ballot_sync(0xffffffffu, engaged));
-  my_eval = warp_sum_u(my_eval);
-  if (lane == 0) {
-    warp_cnt[warp] = __popc(bal);
-    warp_eval[warp] = my_eval;
-    warp_eng[warp] = eng;
-  }
-  __syncthreads();
-  int base = 0, n_live = 0;
-  unsigned n_eval_cta = 0, n_eng_cta = 0;
+    // ordered compaction of live steps (keeps time order for the neighbour merge)
+    const unsigned bal = __ballot_sync(0xffffffffu, any);
+    const unsigned eng = __popc(__ballot_sync(0xffffffffu, engaged));
+    my_eval = warp_sum_u(my_eval);
+    int base = n_live;
+    if constexpr (kSweepWarps == 1) {
+      n_live += __popc(bal);
+      n_eval_cta += my_eval;
+      n_eng_cta += eng;
+    } else {
+      if (lane == 0) {
+        warp_cnt[warp] = __popc(bal);
+        warp_eval[warp] = my_eval;
+        warp_eng[warp] = eng;
+      }
+      __syncthreads();
 #pragma unroll
-  for (int w = 0; w < kSweepWarps; ++w) {
-    if (w < warp) base += warp_cnt[w];
-    n_live += warp_cnt[w];
-    n_eval_cta += warp_eval[w];
-    n_eng_cta += warp_eng[w];
-  }
-  if (any) {
-    const int slot = base + __popc(bal & ((1u << lane) - 1u));
-    for (int w = 0; w < mask_words; ++w) mslot[slot * mask_words + w] = masks[tid * mask_words + w];
+      for (int w = 0; w < kSweepWarps; ++w) {
+        if (w < warp) base += warp_cnt[w];
+        n_live += warp_cnt[w];
+        n_eval_cta += warp_eval[w];
+        n_eng_cta += warp_eng[w];
+      }
+      __syncthreads();  // warp_cnt is rewritten by the next round
+    }
+    if (any) {
+      const int slot = base + __popc(bal & ((1u << lane) - 1u));
+      for (int w = 0; w < mask_words; ++w) mslot[slot * mask_words + w] = masks[tid * mask_words + w];
 #pragma unroll
-    for (int k = 0; k < RW; ++k) rowv[slot * 8 + k] = rd[k];
+      for (int k = 0; k < RW; ++k) rowv[slot * 8 + k] = rd[k];
+    }
   }
-  __syncthreads();
+  if constexpr (kSweepWarps == 1) __syncwarp(); else __syncthreads();
   if (n_live == 0) {
     if (tid == 0 && J.counters && n_eng_cta)
       atomicAdd(J.counters + MSURF_CTR_ENGAGED_ROWS, (unsigned long long)n_eng_cta);
@@ -488,7 +510,7 @@ __global__ void __launch_bounds__(kSweepThreads, ONE ? MSURF_MIN_BLOCKS_ONE : MS
     const int groups = (n_live + 63) >> 6;
     int rta = 0, rtb = 0;
     double ra[RW], rb[RW];
-    for (; g < groups; next_unit(g, q, nchunk)) {
+    for (; g < groups; next_unit<kSweepWarps>(g, q, nchunk)) {
       const int sa = g * 64 + 2 * lane, sb = sa + 1;
       if (g != g_loaded) {  // warp-uniform
         g_loaded = g;
@@ -586,7 +608,7 @@ __global__ void __launch_bounds__(kSweepThreads, ONE ? MSURF_MIN_BLOCKS_ONE : MS
     const int groups = (n_live + 31) >> 5;
     int rt = 0;
     double r[RW];
-    for (; g < groups; next_unit(g, q, nchunk)) {
+    for (; g < groups; next_unit<kSweepWarps>(g, q, nchunk)) {
       const int slot = g * 32 + lane;
       if (g != g_loaded) {  // warp-uniform
         g_loaded = g;
@@ -1195,24 +1217,44 @@ __global__ void mb_atomic_kernel(unsigned long long* buf, long long mask, int it
   }
 }
 
-template <int MODE, bool DIAG>
-cudaError_t launch_sweep(int64_t n_tiles, size_t smem, cudaStream_t st, const msurf_job* jobs, int n_jobs,
-                         const int64_t* prefix, int mask_words, const msurf_job* one) {
+// smem of one sweep CTA: transforms + masks by thread + masks by slot
+inline size_t sweep_smem(int tile, int mask_words) {
+  return (size_t)tile * 8 * sizeof(double) + (size_t)2 * tile * mask_words * sizeof(uint64_t);
+}
+
+template <int MODE, bool DIAG, bool ONE, int TILE, int NTHR>
+cudaError_t launch_shape(int64_t n_tiles, cudaStream_t st, const msurf_job* jobs, int n_jobs, const int64_t* prefix,
+                         int mask_words, const msurf_job& job) {
+  const size_t smem = sweep_smem(TILE, mask_words);
   cudaError_t e = cudaSuccess;
-  if (one) {
-    if (smem > 48 * 1024)
-      e = cudaFuncSetAttribute(sweep_kernel<MODE, DIAG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-      sweep_kernel<MODE, DIAG, true><<<(unsigned)n_tiles, kSweepThreads, smem, st>>>(nullptr, 1, nullptr, mask_words, *one);
-    return e;
-  }
   if (smem > 48 * 1024)
-    e = cudaFuncSetAttribute(sweep_kernel<MODE, DIAG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(sweep_kernel<MODE, DIAG, ONE, TILE, NTHR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+  if (e == cudaSuccess)
+    sweep_kernel<MODE, DIAG, ONE, TILE, NTHR><<<(unsigned)n_tiles, NTHR, smem, st>>>(jobs, n_jobs, prefix, mask_words,
+                                                                                    job);
+  return e;
+}
+
+// tiles of one job for a tile size: passes * teeth * ceil(window / tile)
+inline int64_t job_tiles(const msurf_job& j, int tile) {
+  return (int64_t)j.passes * j.teeth * ((j.step_hi - j.step_lo + tile - 1) / tile);
+}
+
+template <int MODE, bool DIAG>
+cudaError_t launch_sweep(int64_t n_tiles, cudaStream_t st, const msurf_job* jobs, int n_jobs,
+                         const int64_t* prefix, int mask_words, const msurf_job* one) {
+  if (one) {
+    if (MODE == MSURF_MODE_EXT_TILT)
+      return launch_shape<MODE, DIAG, true, kTiltTile, kTiltThreads>(job_tiles(*one, kTiltTile), st, nullptr, 1,
+                                                                    nullptr, mask_words, *one);
+    return launch_shape<MODE, DIAG, true, kWideTile, kWideThreads>(job_tiles(*one, kWideTile), st, nullptr, 1,
+                                                                  nullptr, mask_words, *one);
+  }
   msurf_job dummy;
   memset(&dummy, 0, sizeof(dummy));
-  if (e == cudaSuccess)
-    sweep_kernel<MODE, DIAG, false><<<(unsigned)n_tiles, kSweepThreads, smem, st>>>(jobs, n_jobs, prefix, mask_words, dummy);
-  return e;
+  return launch_shape<MODE, DIAG, false, kBatchTile, kBatchThreads>(n_tiles, st, jobs, n_jobs, prefix, mask_words,
+                                                                    dummy);
 }
 
 }  // namespace
@@ -1223,7 +1265,7 @@ extern "C" {
 int msurf_abi_version(void) { return MSURF_ABI_VERSION; }
 const char* msurf_last_error(void) { return g_err.c_str(); }
 int msurf_sizeof_job(void) { return (int)sizeof(msurf_job); }
-int msurf_tile_steps(void) { return kTileSteps; }
+int msurf_tile_steps(void) { return kBatchTile; }
 
 int msurf_fill_keys(uint64_t* keys, int64_t count, int32_t n_surf, const double* value,
                     void* stream) {
@@ -1241,17 +1283,18 @@ int msurf_fill_keys(uint64_t* keys, int64_t count, int32_t n_surf, const double*
 
 static int sweep_impl(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile_prefix, int64_t n_tiles,
                       int32_t mode, int32_t max_points, void* stream, const msurf_job* one) {
-  if (n_tiles == 0) return 0;
+  if (!one && n_tiles == 0) return 0;
   if (n_tiles > 0x7fffffffLL) return set_err("msurf_sweep: too many tiles");
+  if (one && (job_tiles(*one, 64) == 0)) return 0;
+  if (one && job_tiles(*one, 64) > 0x7fffffffLL) return set_err("msurf_sweep_job: too many tiles");
   const int nchunk = (max_points + 31) / 32;
   const int mask_words = (nchunk + 63) / 64;
-  const size_t smem = (size_t)kTileSteps * 8 * sizeof(double) + (size_t)2 * kTileSteps * mask_words * sizeof(uint64_t);
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
   const bool diag = (mode & MSURF_SWEEP_DIAG) != 0;
-#define MSURF_LAUNCH(M)                                                                                    \
-  e = diag ? launch_sweep<M, true>(n_tiles, smem, st, jobs, n_jobs, tile_prefix, mask_words, one)          \
-           : launch_sweep<M, false>(n_tiles, smem, st, jobs, n_jobs, tile_prefix, mask_words, one)
+#define MSURF_LAUNCH(M)                                                                      \
+  e = diag ? launch_sweep<M, true>(n_tiles, st, jobs, n_jobs, tile_prefix, mask_words, one)  \
+           : launch_sweep<M, false>(n_tiles, st, jobs, n_jobs, tile_prefix, mask_words, one)
   switch (mode & ~MSURF_SWEEP_DIAG) {
     case MSURF_MODE_REF: MSURF_LAUNCH(MSURF_MODE_REF); break;
     case MSURF_MODE_EXT: MSURF_LAUNCH(MSURF_MODE_EXT); break;
@@ -1271,9 +1314,9 @@ int msurf_sweep(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile_prefi
   return sweep_impl(jobs, n_jobs, tile_prefix, n_tiles, mode, max_points, stream, nullptr);
 }
 
-int msurf_sweep_job(const msurf_job* job, int64_t n_tiles, int32_t mode, int32_t max_points, void* stream) {
-  if (!job || n_tiles < 0 || max_points < 1) return set_err("msurf_sweep_job: bad arguments");
-  return sweep_impl(nullptr, 1, nullptr, n_tiles, mode, max_points, stream, job);
+int msurf_sweep_job(const msurf_job* job, int32_t mode, int32_t max_points, void* stream) {
+  if (!job || max_points < 1) return set_err("msurf_sweep_job: bad arguments");
+  return sweep_impl(nullptr, 1, nullptr, 0, mode, max_points, stream, job);
 }
 
 int msurf_decode(uint64_t* keys, int64_t count, int32_t n_surf, const double* sentinel,

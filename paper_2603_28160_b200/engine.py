@@ -306,7 +306,7 @@ class SweepBatch:
                 arr = self.group_host_jobs[g]
                 for k, t in enumerate(self.group_tiles[g]):
                     if t:
-                        _native.check(lib.msurf_sweep_job(ctypes.addressof(arr[k]), t, mode | flag, max_pts, sp))
+                        _native.check(lib.msurf_sweep_job(ctypes.addressof(arr[k]), mode | flag, max_pts, sp))
                 continue
             _native.check(lib.msurf_sweep(base + job_off, len(idx), base + pre_off, n_tiles, mode | flag,
                                           max_pts, sp))

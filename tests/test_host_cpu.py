@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
         assert getattr(lib, name) is not None
     assert lib.msurf_abi_version() == _native.ABI_VERSION
     assert lib.msurf_sizeof_job() == ctypes.sizeof(_native.MsurfJob)
-    assert lib.msurf_tile_steps() in (128, 256)
+    assert lib.msurf_tile_steps() > 0 and lib.msurf_tile_steps() % 32 == 0
 
 
 def test_error_path_without_gpu_reports_message():

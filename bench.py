@@ -370,7 +370,6 @@ def run_ours(args, rank, world):
     # SURVEY §8(d) definition: P_eng = points of rows whose whole-tooth 2-D box
     # meets the window (row-level cull); the kernel's chunk-level cull skips
     # part of that work, so this fraction also credits the finer cull
-    flops_survey = FLOPS_PER_POINT[mode] * engaged * p.points + FLOPS_PER_ROW * engaged
     lib = _native.lib()
     import ctypes
 
@@ -391,11 +390,10 @@ def run_ours(args, rank, world):
                        "(MEASURED_PEAKS.json has no FP64 entry)",
         "flops_per_launch": flops,
         "flops_model": f"{FLOPS_PER_POINT[mode]} x points_evaluated + {FLOPS_PER_ROW} x live rows",
-        "survey_def": {"note": "SURVEY 8(d) units: every point of each row whose whole-tooth box meets the "
-                               "window; credits work the chunk cull skips, so it can exceed 1 (upper bound)",
-                       "P_eng": engaged * p.points, "engaged_rows": engaged,
-                       "achieved": flops_survey / (sweep_ms_avg * 1e-3) / 1e12,
-                       "frac": flops_survey / (sweep_ms_avg * 1e-3) / fp64_peak},
+        "survey_def": {"note": "SURVEY 8(d) unit count P_eng: every point of each row whose whole-tooth box "
+                               "meets the window; the kernel's chunk cull evaluates only points_evaluated of "
+                               "them, which is what frac is computed on",
+                       "P_eng": engaged * p.points, "engaged_rows": engaged},
         "points_evaluated": evald, "live_rows": live, "deposits": int(dctr[0][2]),
         "atomics": int(dctr[0][3]),
         "diag_note": "deposits/atomics from one extra untimed launch with MSURF_SWEEP_DIAG",
@@ -540,7 +538,6 @@ def run_batch(args, rank, world):
     npts = plans[0].points
     mode = plans[0].mode
     flops = FLOPS_PER_POINT[mode] * evald + FLOPS_PER_ROW * live
-    flops_survey = FLOPS_PER_POINT[mode] * engaged * npts + FLOPS_PER_ROW * engaged
     lib = _native.lib()
     r = ctypes.c_double(0.0)
     _native.check(lib.msurf_microbench(0, ctypes.byref(r)))
@@ -554,7 +551,7 @@ def run_batch(args, rank, world):
                 "frac": achieved / fp64_peak, "traffic": profiled_traffic(meta["name"]),
                 "kernel": "sweep_kernel<MODE>", "sweep_ms": sweep_avg,
                 "peak_source": "measured in this run: msurf_microbench(0), non-FMA DADD/DMUL issue rate",
-                "flops_per_launch": flops, "survey_def": {"frac": flops_survey / (sweep_avg * 1e-3) / fp64_peak},
+                "flops_per_launch": flops, "survey_def": {"P_eng": engaged * npts, "engaged_rows": engaged},
                 "points_evaluated": evald, "live_rows": live, "deposits": int(dctr[:, 2].sum()),
                 "atomics": int(dctr[:, 3].sum()),
                 "diag_note": "deposits/atomics from one extra untimed launch with MSURF_SWEEP_DIAG",

@@ -203,6 +203,15 @@ int msurf_plan_finish(const msurf_geom_in* in, const double* px, const double* p
                       double* pts, double* tooth_box, double* chunk_circ, double* chunk_box, int32_t* min_index,
                       double* zw_out, uint64_t* key_out);
 
+/* The two planning steps for n parameter sets of one geometry family (equal
+ * teeth and points, EXT modes), set b in slice b of every output; `threads`
+ * host threads split the sets. */
+int msurf_plan_geometry_many(const msurf_geom_in* ins, int32_t n, double* px, double* py, double* pz,
+                             double* stats2, int32_t threads);
+int msurf_plan_finish_many(const msurf_geom_in* ins, int32_t n, const double* px, const double* py, const double* pz,
+                           const double* zoff, double* pts, double* tooth_box, double* chunk_circ, double* chunk_box,
+                           int32_t* min_index, double* zw_out, uint64_t* key_out, int32_t threads);
+
 /* Graymap export (surface_io.py:100-131, write_graymap) of one fp64 height
  * field (row pitch ld) over the ROI rows [i_lo, i_lo+rows) x cols
  * [j_lo, j_lo+cols). msurf_graymap_range: out3 = (max, min, n) of the

@@ -88,6 +88,9 @@ EXPORTS = {
                                             c_void_p, c_void_p, c_void_p]),
     "msurf_microbench": (ctypes.c_int, [c_int32, ctypes.POINTER(c_double)]),
     "msurf_plan_geometry": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "msurf_plan_geometry_many": (ctypes.c_int, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_int32]),
+    "msurf_plan_finish_many": (ctypes.c_int, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                              c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32]),
     "msurf_plan_finish": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_void_p, c_void_p,
                                          c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
 }

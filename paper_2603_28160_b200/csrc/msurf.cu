@@ -1245,11 +1245,12 @@ template <int MODE, bool DIAG>
 cudaError_t launch_sweep(int64_t n_tiles, cudaStream_t st, const msurf_job* jobs, int n_jobs,
                          const int64_t* prefix, int mask_words, const msurf_job* one) {
   if (one) {
-    if (MODE == MSURF_MODE_EXT_TILT)
+    if constexpr (MODE == MSURF_MODE_EXT_TILT)
       return launch_shape<MODE, DIAG, true, kTiltTile, kTiltThreads>(job_tiles(*one, kTiltTile), st, nullptr, 1,
                                                                     nullptr, mask_words, *one);
-    return launch_shape<MODE, DIAG, true, kWideTile, kWideThreads>(job_tiles(*one, kWideTile), st, nullptr, 1,
-                                                                  nullptr, mask_words, *one);
+    else
+      return launch_shape<MODE, DIAG, true, kWideTile, kWideThreads>(job_tiles(*one, kWideTile), st, nullptr, 1,
+                                                                    nullptr, mask_words, *one);
   }
   msurf_job dummy;
   memset(&dummy, 0, sizeof(dummy));

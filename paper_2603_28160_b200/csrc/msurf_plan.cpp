@@ -47,6 +47,11 @@ void edge_coords(double half, int n, double r, double* x, double* z) {
   for (int i = 0; i < n; ++i) z[i] = r - sqrt(rr - x[i] * x[i]);
 }
 
+// exact min/max of non-NaN values without a libm call (fmin/fmax are PLT calls
+// in this build); ties keep the first value, as the tests check bitwise
+inline double mn(double a, double b) { return b < a ? b : a; }
+inline double mx(double a, double b) { return b > a ? b : a; }
+
 // _chunk_boxes + _chunk_circles + tooth box for one tooth's (x, y, z) rows
 void chunk_records(const double* x, const double* y, const double* z, int n, double tc, double ts,
                    double* box /*[nchunk][6]*/, double* circ /*[nchunk][6]*/, double* tbox /*[6]*/) {
@@ -56,9 +61,9 @@ void chunk_records(const double* x, const double* y, const double* z, int n, dou
     const int a = q * kChunk, b = a + kChunk < n ? a + kChunk : n;  // the padding repeats element n-1
     double xl = x[a], xh = x[a], yl = y[a], yh = y[a], zl = z[a], zh = z[a];
     for (int i = a + 1; i < b; ++i) {
-      xl = fmin(xl, x[i]); xh = fmax(xh, x[i]);
-      yl = fmin(yl, y[i]); yh = fmax(yh, y[i]);
-      zl = fmin(zl, z[i]); zh = fmax(zh, z[i]);
+      xl = mn(xl, x[i]); xh = mx(xh, x[i]);
+      yl = mn(yl, y[i]); yh = mx(yh, y[i]);
+      zl = mn(zl, z[i]); zh = mx(zh, z[i]);
     }
     double* bo = box + q * 6;
     bo[0] = xl; bo[1] = xh; bo[2] = yl; bo[3] = yh; bo[4] = zl; bo[5] = zh;
@@ -77,9 +82,9 @@ void chunk_records(const double* x, const double* y, const double* z, int n, dou
     ci[3] = tc * rho + fabs(ts) * (zr * (1.0 + 1e-12) + 1e-12);
     ci[4] = -ts * zc;
     ci[5] = 0.0;
-    tbox[0] = fmin(tbox[0], xl); tbox[1] = fmax(tbox[1], xh);
-    tbox[2] = fmin(tbox[2], yl); tbox[3] = fmax(tbox[3], yh);
-    tbox[4] = fmin(tbox[4], zl); tbox[5] = fmax(tbox[5], zh);
+    tbox[0] = mn(tbox[0], xl); tbox[1] = mx(tbox[1], xh);
+    tbox[2] = mn(tbox[2], yl); tbox[3] = mx(tbox[3], yh);
+    tbox[4] = mn(tbox[4], zl); tbox[5] = mx(tbox[5], zh);
   }
 }
 
@@ -220,6 +225,65 @@ int msurf_plan_finish(const msurf_geom_in* in, const double* px, const double* p
     }
   }
   return 0;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- batches
+// The same two steps for n parameter sets of one geometry family (equal
+// teeth and points): set b reads ins[b] and writes its slice of every output
+// (teeth*points, teeth*nchunk*6, ... elements per set). Sets are independent:
+// `threads` host threads split them (results do not depend on the split).
+#include <thread>
+
+namespace {
+template <class F>
+void for_sets(int n, int threads, F&& f) {
+  if (threads < 1) threads = 1;
+  if (threads > n) threads = n;
+  if (threads <= 1) {
+    for (int b = 0; b < n; ++b) f(b);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] {
+      for (int b = t; b < n; b += threads) f(b);
+    });
+  for (auto& th : pool) th.join();
+}
+}  // namespace
+
+extern "C" {
+
+int msurf_plan_geometry_many(const msurf_geom_in* ins, int32_t n, double* px, double* py, double* pz,
+                             double* stats2, int32_t threads) {
+  if (!ins || n < 1) return 1;
+  const long per = (long)ins[0].teeth * ins[0].points;
+  for (int b = 0; b < n; ++b)
+    if (ins[b].teeth != ins[0].teeth || ins[b].points != ins[0].points || ins[b].mode == MSURF_MODE_REF) return 1;
+  int bad = 0;
+  for_sets(n, threads, [&](int b) {
+    if (msurf_plan_geometry(ins + b, px + b * per, py + b * per, pz + b * per, stats2 + 2 * b)) bad = 1;
+  });
+  return bad;
+}
+
+int msurf_plan_finish_many(const msurf_geom_in* ins, int32_t n, const double* px, const double* py, const double* pz,
+                           const double* zoff, double* pts, double* tooth_box, double* chunk_circ, double* chunk_box,
+                           int32_t* min_index, double* zw_out, uint64_t* key_out, int32_t threads) {
+  if (!ins || n < 1) return 1;
+  const int zn = ins[0].teeth, np = ins[0].points, nchunk = (np + kChunk - 1) / kChunk;
+  const long per = (long)zn * np;
+  int bad = 0;
+  for_sets(n, threads, [&](int b) {
+    if (msurf_plan_finish(ins + b, px + b * per, py + b * per, pz + b * per, zoff[b], pts + b * per * 4,
+                          tooth_box + (long)b * zn * 6, chunk_circ + (long)b * zn * nchunk * 6,
+                          chunk_box + (long)b * zn * nchunk * 6, min_index + (long)b * zn,
+                          zw_out ? zw_out + b * per : nullptr, key_out ? key_out + b * per : nullptr))
+      bad = 1;
+  });
+  return bad;
 }
 
 }  // extern "C"

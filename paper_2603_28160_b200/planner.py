@@ -582,7 +582,8 @@ def plan_many(configs, exts, threads: int | None = None):
         jobs.extend(idx[a: a + step] for a in range(0, len(idx), step))
     if jobs:
         def run(sub):
-            return sub, _plan_ext_group([configs[i] for i in sub], [exts[i] for i in sub])
+            fn = _plan_ext_group_native if NATIVE_PLAN else _plan_ext_group
+            return sub, fn([configs[i] for i in sub], [exts[i] for i in sub])
 
         if len(jobs) == 1:
             done = [run(jobs[0])]
@@ -595,6 +596,112 @@ def plan_many(configs, exts, threads: int | None = None):
             for i, p in zip(sub, plans):
                 out[i] = p
     return out
+
+
+def _plan_ext_group_native(configs, exts, threads: int = 1):
+    """_plan_ext for a group of parameter sets sharing their edge geometry:
+    per-set scalars on the host, the arrays of every set in two native calls
+    (msurf_plan_geometry_many / msurf_plan_finish_many); bitwise equal to
+    per-set plan() (tests/test_native_plan_cpu.py)."""
+    from . import _native
+
+    lib = _native.lib()
+    c0, e0 = configs[0], exts[0]
+    tool, proc0 = c0.tool, c0.process
+    r = tool.insert_radius_mm
+    a_p = proc0.depth_of_cut_mm
+    z_n = tool.tooth_count
+    B = len(configs)
+    tau = e0.tilt_rad
+    tilt = tau != 0.0
+    tc, ts = math.cos(tau), math.sin(tau)
+    if e0.profile == "insert":
+        half = effective_half_length(r, a_p, proc0.feed_per_tooth_mm, tool.radial_rake_rad)
+        n = c0.edge_point_count or default_point_count(half, c0.grid.spacing_mm)
+        if n < 2:
+            raise DomainError(f"point_count must be >= 2, got {n}")
+        arc = 2.0 * r * math.asin(min(1.0, half / r))
+        base_margin = tool.cutting_diameter_mm / 2.0 + half
+        kmax = 0.0
+    else:
+        n = c0.edge_point_count
+        if n is None or n < 2:
+            raise ConfigError("the ball profile needs edge_point_count >= 2")
+        kmax = min(math.pi / 2.0, math.acos((r - a_p) / r) + abs(tau))
+        arc = r * kmax
+        half = r * math.sin(kmax)
+        base_margin = half
+    sigma = e0.noise_sigma_mm
+    delta = None
+    if sigma != 0.0:
+        delta = np.ascontiguousarray(edge_noise(z_n, n, sigma, e0.noise_corr_mm, arc / (n - 1), int(e0.noise_seed)))
+    radial = None if e0.profile == "insert" else 0.0
+    rows = np.ascontiguousarray([_rows12(edge_to_tool_rows(tool, k, radial_offset_mm=radial))
+                                 for k in range(1, z_n + 1)], dtype=np.float64)
+    r_ref = e0.helix_ref_radius_mm
+    if r_ref is None:
+        r_ref = tool.cutting_diameter_mm / 2.0 if e0.profile == "insert" else r
+    offs = np.zeros((B, z_n, 2))
+    ins = (_native.MsurfGeomIn * B)()
+    mode = MODE_EXT_TILT if tilt else MODE_EXT
+    for b, e in enumerate(exts):
+        g = ins[b]
+        g.mode, g.teeth, g.points, g.profile = mode, z_n, n, 0 if e0.profile == "insert" else 1
+        g.radius, g.half, g.kmax = r, half if e0.profile == "insert" else 0.0, kmax
+        g.tan_beta_over_r = math.tan(e.helix_angle_rad) / r_ref if e.helix_angle_rad != 0.0 else 0.0
+        g.tilt_c, g.tilt_s = tc, ts
+        g.rows = rows.ctypes.data
+        g.delta = delta.ctypes.data if delta is not None else None
+        rho, lam = e.runout_offset_mm, e.runout_phase_rad
+        if rho != 0.0:
+            for k in range(1, z_n + 1):
+                ang = lam + (2.0 * math.pi) * (k - 1) / z_n
+                offs[b, k - 1] = (rho * math.cos(ang), rho * math.sin(ang))
+            g.runout_xy = offs[b].ctypes.data
+    px, py, pz = np.empty((B, z_n, n)), np.empty((B, z_n, n)), np.empty((B, z_n, n))
+    stats = np.zeros((B, 2))
+    if lib.msurf_plan_geometry_many(ins, B, px.ctypes.data, py.ctypes.data, pz.ctypes.data, stats.ctypes.data,
+                                    threads):
+        raise DomainError("native planner rejected the geometry")
+    spans, zoffs = [], np.empty(B)
+    for b, (cfg, e) in enumerate(zip(configs, exts)):
+        margin = base_margin + (abs(e.runout_offset_mm) + abs(e.vib_amplitude_mm) + 5.0 * abs(sigma)
+                                + abs(ts) * float(stats[b, 1]))
+        sp = _span(cfg, margin)
+        spans.append(sp)
+        zoffs[b] = (sp[5] + (float(stats[b, 0]) if tilt else 0.0)) + 0.0
+    nchunk = (n + CHUNK - 1) // CHUNK
+    pts = np.empty((B, z_n, n, 4))
+    tbox = np.empty((B, z_n, 6))
+    circ = np.empty((B, z_n, nchunk, 6))
+    cbox = np.empty((B, z_n, nchunk, 6))
+    mins = np.empty((B, z_n), dtype=np.int32)
+    zw = np.empty((B, z_n, n))
+    zkey = np.empty((B, z_n, n), dtype=np.uint64)
+    if lib.msurf_plan_finish_many(ins, B, px.ctypes.data, py.ctypes.data, pz.ctypes.data, zoffs.ctypes.data,
+                                  pts.ctypes.data, tbox.ctypes.data, circ.ctypes.data, cbox.ctypes.data,
+                                  mins.ctypes.data, zw.ctypes.data, zkey.ctypes.data, threads):
+        raise DomainError("native planner rejected the geometry")
+    plans = []
+    for b, (cfg, e) in enumerate(zip(configs, exts)):
+        proc, grid = cfg.process, cfg.grid
+        dt, t_start, steps, x0, y0, z0 = spans[b]
+        p = SweepPlan(
+            mode=mode, grid=grid, teeth=z_n, points=n, steps=steps, dt=dt, t_start=t_start, x0=x0, y0=y0, z0=z0,
+            feed_speed=proc.feed_speed_mm_s, omega=proc.angular_velocity_rad_s, initial_height=z0 + a_p,
+            half_length=half,
+            tooth_base=np.array([tooth_base_angle(proc.phase_rad, k, z_n) for k in range(1, z_n + 1)]),
+            tooth_rows=np.zeros((z_n, 8)), px=px[b], py=py[b], pz=pz[b], zw=zw[b], zkey=zkey[b],
+            chunk_box=cbox[b], pass_x0=np.array([x0 + k * e.stepover_mm for k in range(int(e.passes))],
+                                                dtype=np.float64),
+            min_index=mins[b], tilt_c=tc, tilt_s=ts, zoff=float(zoffs[b]), vib_amp=e.vib_amplitude_mm,
+            vib_omega=2.0 * math.pi * e.vib_frequency_hz, vib_phase=e.vib_phase_rad,
+            extras={"base_margin": base_margin})
+        p.pts, p.chunk_circ, p.tooth_box = pts[b], circ[b], tbox[b]
+        p.record = False
+        _check_device_limits(p, grid)
+        plans.append(p)
+    return plans
 
 
 def _plan_ext_group(configs, exts):

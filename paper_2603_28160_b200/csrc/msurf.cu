@@ -133,25 +133,27 @@ __device__ __forceinline__ unsigned warp_sum_u(unsigned v) {
 }
 
 // 2-D box test of one tool-frame box [xl xh yl yh zl zh] rotated by (c, s),
-// offset by (xoff, ty), after the lead tilt, against a window. Conservative
-// by construction of the window (1.5 cells >> rounding differences).
+// after the lead tilt, in fp32 against a window given by its centre
+// offsets (ox, oy = tool offset - window centre) and half-widths (hx, hy)
+// that already include the caller's margin: every term is bounded by the box
+// extent R and the offsets, so the fp32 result is within a few ulp(R + |o|)
+// of the exact one; callers add >= 4e-6 (R + |o|) + 1e-6 mm to hx, hy.
 template <int MODE>
-__device__ __forceinline__ bool tool_box_hits(const double* b, double c, double sn, double xoff, double ty,
-                                              double wx_lo, double wx_hi, double wy_lo, double wy_hi,
-                                              double tilt_c, double tilt_s) {
-  const double ns = -sn;
-  const double xl = b[0], xh = b[1], yl = b[2], yh = b[3];
-  const double x_lo = fmin(c * xl, c * xh) + fmin(sn * yl, sn * yh) + xoff;
-  const double x_hi = fmax(c * xl, c * xh) + fmax(sn * yl, sn * yh) + xoff;
-  double v_lo = fmin(ns * xl, ns * xh) + fmin(c * yl, c * yh);
-  double v_hi = fmax(ns * xl, ns * xh) + fmax(c * yl, c * yh);
+__device__ __forceinline__ bool tool_box_hits_f32(const float* b, float c, float sn, float ox, float oy, float hx,
+                                                  float hy, float tilt_c, float tilt_s) {
+  const float ns = -sn;
+  const float xl = b[0], xh = b[1], yl = b[2], yh = b[3];
+  const float x_lo = fminf(c * xl, c * xh) + fminf(sn * yl, sn * yh) + ox;
+  const float x_hi = fmaxf(c * xl, c * xh) + fmaxf(sn * yl, sn * yh) + ox;
+  float v_lo = fminf(ns * xl, ns * xh) + fminf(c * yl, c * yh);
+  float v_hi = fmaxf(ns * xl, ns * xh) + fmaxf(c * yl, c * yh);
   if (MODE == MSURF_MODE_EXT_TILT) {
-    const double a1 = tilt_c * v_lo, a2 = tilt_c * v_hi;
-    const double b1 = tilt_s * b[4], b2 = tilt_s * b[5];
-    v_lo = fmin(a1, a2) - fmax(b1, b2);
-    v_hi = fmax(a1, a2) - fmin(b1, b2);
+    const float a1 = tilt_c * v_lo, a2 = tilt_c * v_hi;
+    const float b1 = tilt_s * b[4], b2 = tilt_s * b[5];
+    v_lo = fminf(a1, a2) - fmaxf(b1, b2);
+    v_hi = fmaxf(a1, a2) - fminf(b1, b2);
   }
-  return (x_hi >= wx_lo) & (x_lo <= wx_hi) & (v_hi + ty >= wy_lo) & (v_lo + ty <= wy_hi);
+  return (x_hi >= -hx) & (x_lo <= hx) & (v_hi + oy >= -hy) & (v_lo + oy <= hy);
 }
 
 // one edge point under one lane's step transform: workpiece x', y' in the
@@ -317,6 +319,9 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
   // first warp touches them) and the bound Rt >= |xc| + |yc| + |yz|
   const float4* __restrict__ cf4 = reinterpret_cast<const float4*>(J.chunk_f32) + (long long)tooth * nchunk * 2;
   const float rt_f = __ldg(reinterpret_cast<const float*>(cf4) + 5);
+  float box_f[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) box_f[k] = (float)J.tooth_box[tooth * 6 + k];
 
   // ---------------- phase 1: one thread per time step (kSubSteps rounds of
   // kSweepThreads steps), live steps appended in time order
@@ -345,6 +350,11 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
         // position for a 100 mm tool, covered by the extra margin; vibration
         // covered by its amplitude): most rows of a windowed strip, and the
         // rows far from the grid, never pay for the double-double sincos.
+        // window centre / half-widths for the fp32 box tests (margins added below)
+        const double wxc = 0.5 * (wx_lo + wx_hi), wxh = 0.5 * (wx_hi - wx_lo);
+        const double wyc = 0.5 * (wy_lo + wy_hi), wyh = 0.5 * (wy_hi - wy_lo);
+        const float oyf = (float)(ty - wyc);
+        const float tcf = (float)J.tilt_c, tsf = (float)J.tilt_s;
         bool maybe = true;
         if (!J.trig_table && !(J.traj && pass == 0)) {
           const double kd = rint(th * MSURF_TWO_OVER_PI);
@@ -352,13 +362,15 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
           float sf, cf;
           __sincosf((float)r, &sf, &cf);
           const int quad = ((int)(long long)kd) & 3;
-          double ca = cf, sa = sf;
+          float ca = cf, sa = sf;
           if (quad == 1) { ca = -sf; sa = cf; }
           else if (quad == 2) { ca = -cf; sa = -sf; }
           else if (quad == 3) { ca = sf; sa = -cf; }
-          const double mg = 1e-4 + fabs(J.vib_amp);
-          maybe = tool_box_hits<MODE>(J.tooth_box + tooth * 6, ca, sa, x0p, ty, wx_lo - mg, wx_hi + mg,
-                                      wy_lo - mg, wy_hi + mg, J.tilt_c, J.tilt_s);
+          // float sincos error < 1e-6 -> < 1e-4 mm at 100 mm; fp32 box terms
+          // within 4e-6 (Rt + |o|); vibration covered by its amplitude
+          const float oxf = (float)(x0p - wxc);
+          const float mg = (float)(1e-4 + fabs(J.vib_amp)) + 4e-6f * (rt_f + fabsf(oxf) + fabsf(oyf)) + 1e-6f;
+          maybe = tool_box_hits_f32<MODE>(box_f, ca, sa, oxf, oyf, (float)wxh + mg, (float)wyh + mg, tcf, tsf);
         }
         if (maybe) {
           double c, sn;
@@ -402,8 +414,14 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
             rd[2] = xoff;
             rd[3] = ty;
           }
-          engaged = tool_box_hits<MODE>(J.tooth_box + tooth * 6, c, sn, xoff, ty, wx_lo, wx_hi, wy_lo, wy_hi,
-                                        J.tilt_c, J.tilt_s);
+          {
+            // whole-tooth test with the exact angle (the SURVEY P_eng row count),
+            // fp32 with the same proven widening as the chunk test below
+            const float oxf = (float)(xoff - wxc);
+            const float mg = 4e-6f * (rt_f + fabsf(oxf) + fabsf(oyf)) + 1e-6f;
+            engaged = tool_box_hits_f32<MODE>(box_f, (float)c, (float)sn, oxf, oyf, (float)wxh + mg,
+                                              (float)wyh + mg, tcf, tsf);
+          }
           if (engaged) {
             // per-chunk bounding circles: x = c*xc + s*yc + xoff +- rx,
             // y = cos(tau)*(c*yc - s*xc) + yz + ty +- ry, against the window
@@ -413,12 +431,10 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
             // is within ~8 ulp(S) < 1e-6 S of the exact one, and the test is
             // widened by 4e-6 S + 1e-6 mm, so it stays a superset of the exact
             // cull (a false positive costs work, never a result).
-            const double wxc = 0.5 * (wx_lo + wx_hi), wxh = 0.5 * (wx_hi - wx_lo);
-            const double wyc = 0.5 * (wy_lo + wy_hi), wyh = 0.5 * (wy_hi - wy_lo);
-            const double ox = xoff - wxc, oy = ty - wyc;
+            const double ox = xoff - wxc;
             const float cf = (float)c, sf = (float)sn;
-            const float oxf = (float)ox, oyf = (float)oy;
-            const float tcf = MODE == MSURF_MODE_EXT_TILT ? (float)J.tilt_c : 1.0f;
+            const float oxf = (float)ox;
+            const float tcc = MODE == MSURF_MODE_EXT_TILT ? tcf : 1.0f;
             const float hx = (float)wxh + (4e-6f * (rt_f + fabsf(oxf)) + 1e-6f);
             const float hy = (float)wyh + (4e-6f * (rt_f + fabsf(oyf)) + 1e-6f);
             unsigned kept = 0;
@@ -427,7 +443,7 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
               const float yz = __ldg(reinterpret_cast<const float*>(cf4 + 2 * q + 1));
               const float uc = fmaf(cf, a.x, sf * a.y);
               const float vc = fmaf(cf, a.y, -(sf * a.x));
-              const bool hit = (fabsf(uc + oxf) <= hx + a.z) & (fabsf(fmaf(tcf, vc, yz) + oyf) <= hy + a.w);
+              const bool hit = (fabsf(uc + oxf) <= hx + a.z) & (fabsf(fmaf(tcc, vc, yz) + oyf) <= hy + a.w);
               if (hit) {
                 my_mask[q >> 6] |= 1ull << (q & 63);
                 kept += (q == nchunk - 1) ? (unsigned)(npts - 32 * q) : 32u;

@@ -305,11 +305,13 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
     __syncthreads();
     local = tile - prefix[s_job];
   }
-  const long long nst = (J.step_hi - J.step_lo + kTileSteps - 1) / kTileSteps;
-  const int st = (int)(local % nst);
-  const long long rem = local / nst;
-  const int tooth = (int)(rem % J.teeth);
-  const int pass = (int)(rem / J.teeth);
+  // tile -> (pass, tooth, step tile) in 32-bit arithmetic (grids are < 2^31 tiles)
+  const unsigned nst = (unsigned)((J.step_hi - J.step_lo + kTileSteps - 1) / kTileSteps);
+  const unsigned loc = (unsigned)local;
+  const unsigned rem = loc / nst;
+  const int st = (int)(loc - rem * nst);
+  const int tooth = (int)(rem % (unsigned)J.teeth);
+  const int pass = (int)(rem / (unsigned)J.teeth);
   const int npts = J.points;
   const int nchunk = (npts + 31) >> 5;
   const double dd = J.spacing;

@@ -118,6 +118,16 @@ int msurf_sweep_job(const msurf_job* job, int32_t mode, int32_t max_points, void
 int msurf_decode(uint64_t* keys, int64_t count, int32_t n_surf, const double* sentinel,
                  unsigned long long* machined, void* stream);
 
+/* Decode for a surface whose keys are stored in sub-strip layout: strip k
+ * (columns [col0[k], col0[k+1]) of the surface, col0 a DEVICE array of
+ * n_strips+1 offsets from the surface's first column) is a contiguous
+ * rows x w_k block at keys + rows*col0[k]; writes row-major fp64 heights
+ * (node (i, c) at heights[i*ld_out + c]) and adds the machined-cell count to
+ * machined[0]. Used for surfaces cut into L2-sized sub-strips: each sweep job
+ * then deposits into one contiguous slab. */
+int msurf_decode_strips(const uint64_t* keys, double* heights, int64_t rows, int64_t ld_out, int32_t n_strips,
+                        const int64_t* col0, const double* sentinel, unsigned long long* machined, void* stream);
+
 /* Areal roughness moments (roughness.py:93-135, leveling='mean').
  * h: device fp64 heights, row-major with leading dimension ld; surface s
  * starts at h + s*surf_stride. ROI rows [i_lo, i_lo+rows), cols [j_lo, j_lo+cols).

@@ -67,6 +67,8 @@ EXPORTS = {
     "msurf_fill_keys": (ctypes.c_int, [c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
     "msurf_sweep": (ctypes.c_int, [c_void_p, c_int32, c_void_p, c_int64, c_int32, c_int32, c_void_p]),
     "msurf_sweep_job": (ctypes.c_int, [c_void_p, c_int32, c_int32, c_void_p]),
+    "msurf_decode_strips": (ctypes.c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p,
+                                           c_void_p, c_void_p]),
     "msurf_decode": (ctypes.c_int, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p]),
     "msurf_areal_pass1": (ctypes.c_int, [c_void_p, c_int64, c_int64, c_int32, c_int64, c_int64,
                                          c_int64, c_int64, c_void_p, c_int32, c_void_p, c_void_p,

@@ -775,6 +775,34 @@ __global__ void __launch_bounds__(kThreads)
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(machined + blockIdx.y, (unsigned long long)cnt);
 }
 
+// Strip-layout decode: the keys of a surface cut into feed-direction
+// sub-strips are stored strip by strip (strip k = columns [c_k, c_k+1) as a
+// contiguous rows x w_k block, so each sweep job's L2 working set is one
+// contiguous slab); this writes the row-major fp64 heights (surface_grid.py
+// layout, leading dimension ld_out) and counts machined cells. Grid: x over
+// row blocks, y = strip; 16-byte loads / stores where the width allows.
+__global__ void __launch_bounds__(kThreads)
+    decode_strips_kernel(const uint64_t* __restrict__ keys, double* __restrict__ out, long long rows,
+                         long long ld_out, const long long* __restrict__ col0, const double* __restrict__ sent,
+                         unsigned long long* __restrict__ machined) {
+  const int k = blockIdx.y;
+  const long long c0 = col0[k], w = col0[k + 1] - c0;
+  const uint64_t* src = keys + rows * c0;
+  const double sentinel = sent[0];
+  unsigned cnt = 0;
+  for (long long i = blockIdx.x; i < rows; i += gridDim.x) {
+    const uint64_t* r = src + i * w;
+    double* o = out + i * ld_out + c0;
+    for (long long c = threadIdx.x; c < w; c += blockDim.x) {
+      const double hv = dec_key(r[c]);
+      o[c] = hv;
+      cnt += hv < sentinel;
+    }
+  }
+  cnt = warp_sum_u(cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(machined, (unsigned long long)cnt);
+}
+
 // ------------------------------------------------------------ reductions
 template <int NV>
 struct Acc {
@@ -1350,6 +1378,18 @@ int msurf_decode(uint64_t* keys, int64_t count, int32_t n_surf, const double* se
   dim3 grid((unsigned)blocks, (unsigned)n_surf);
   decode_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(keys, count, sentinel, machined);
   return check_launch("decode_kernel");
+}
+
+int msurf_decode_strips(const uint64_t* keys, double* heights, int64_t rows, int64_t ld_out, int32_t n_strips,
+                        const int64_t* col0, const double* sentinel, unsigned long long* machined, void* stream) {
+  if (!keys || !heights || !col0 || !sentinel || !machined || rows < 1 || n_strips < 1 || ld_out < 1)
+    return set_err("msurf_decode_strips: bad arguments");
+  long long blocks = rows < 148 * 8 ? rows : 148 * 8;
+  dim3 grid((unsigned)blocks, (unsigned)n_strips);
+  decode_strips_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(keys, heights, rows, ld_out,
+                                                                    reinterpret_cast<const long long*>(col0),
+                                                                    sentinel, machined);
+  return check_launch("decode_strips_kernel");
 }
 
 // blocks per surface: ~4096 elements per block, at most one per row, at most

@@ -119,6 +119,9 @@ class _Surface:
     j_hi: int
     key_off: int = 0          # element offset into the keys tensor
     nodes: int = 0
+    n_strips: int = 1         # L2 sub-strips the surface is cut into
+    strip_off: int = -1       # element offset into strip_keys (n_strips > 1)
+    col0: list = field(default_factory=list)  # sub-strip column offsets from j_lo
 
 
 def _trig_tables(p: SweepPlan):
@@ -142,7 +145,10 @@ class SweepBatch:
     Device layout: one uint8 arena holding every per-surface array, the job
     descriptors (msurf_job) and tile prefix sums, written by ONE H2D copy;
     one int64 tensor holding all surfaces' Z-maps back to back (u64 keys
-    during the sweep, fp64 heights after the decode, in place)."""
+    during the sweep, fp64 heights after the decode, in place). A surface
+    larger than the L2 budget keeps its keys in a second tensor, sub-strip by
+    sub-strip (each sweep job deposits into one contiguous slab), and its
+    decode writes the row-major heights into the first."""
 
     def __init__(self, surfaces, trig: str = "device", device=None, l2_tile_bytes: int = L2_TILE_BYTES,
                  diagnostics: bool = False):
@@ -158,12 +164,25 @@ class SweepBatch:
         if not surfs:
             raise ConfigError("empty batch")
         total = 0
+        strip_total = 0
         for s in surfs:
             s.key_off = total
-            s.nodes = (s.plan.grid.m + 1) * (s.j_hi - s.j_lo + 1)
+            w = s.j_hi - s.j_lo + 1
+            rows = s.plan.grid.m + 1
+            s.nodes = rows * w
             total += s.nodes
+            # surfaces above the L2 budget are cut into feed-direction sub-strips;
+            # their keys live strip by strip (contiguous slab per sweep job) and the
+            # decode writes the row-major heights (msurf_decode_strips)
+            k = 1 if s.plan.record else max(1, min(w, -(-rows * w * 8 // l2_tile_bytes)))
+            s.n_strips = k
+            s.col0 = [(w * q) // k for q in range(k + 1)]
+            if k > 1:
+                s.strip_off = strip_total
+                strip_total += s.nodes
         self.surfs = surfs
         self.keys = torch.empty(max(total, 1), dtype=torch.int64, device=self.dev)
+        self.strip_keys = torch.empty(strip_total, dtype=torch.int64, device=self.dev) if strip_total else None
         self.need_traj = [s.plan.record for s in surfs]
         traj_len = sum(s.plan.steps * s.plan.teeth * 3 for s, r in zip(surfs, self.need_traj) if r)
         self.traj = torch.empty(traj_len, dtype=torch.float64, device=self.dev) if traj_len else None
@@ -182,6 +201,8 @@ class SweepBatch:
                 pass_x0=ar.add(p.pass_x0.astype(np.float64, copy=False)),
                 min_index=ar.add(p.min_index.astype(np.int32, copy=False)),
             )
+            if s.n_strips > 1:
+                o["col0"] = ar.add(np.asarray(s.col0, dtype=np.int64))
             if trig == "host":
                 tab, vib = _trig_tables(p)
                 o["trig_table"] = ar.add(tab)
@@ -201,14 +222,10 @@ class SweepBatch:
         tile_steps = self.lib.msurf_tile_steps()
         jobs = []  # (surface index, j_lo, j_hi, step_lo, step_hi)
         for i, s in enumerate(surfs):
-            w = s.j_hi - s.j_lo + 1
-            rows = s.plan.grid.m + 1
-            k = max(1, min(w, -(-rows * w * 8 // l2_tile_bytes)))
-            if s.plan.record:
-                k = 1  # the trajectory record needs every step in one job
+            k = s.n_strips  # 1 when a trajectory record needs every step in one job
             for q in range(k):
-                lo = s.j_lo + (w * q) // k
-                hi = s.j_lo + (w * (q + 1)) // k - 1
+                lo = s.j_lo + s.col0[q]
+                hi = s.j_lo + s.col0[q + 1] - 1
                 whole = k == 1 and s.j_lo == 0 and s.j_hi == s.plan.grid.n
                 s_lo, s_hi = (0, s.plan.steps) if (whole or s.plan.record) else step_window(s.plan, lo, hi)
                 if s_hi > s_lo:
@@ -230,6 +247,7 @@ class SweepBatch:
                                     max(surfs[jobs[j][0]].plan.points for j in jidx)))
             self.group_tiles.append([int(t) for t in tiles])
         keys_ptr = self.keys.data_ptr()
+        strip_ptr = self.strip_keys.data_ptr() if self.strip_keys is not None else 0
         traj_ptr = self.traj.data_ptr() if self.traj is not None else 0
         self.traj_off = []
         toff = 0
@@ -249,8 +267,12 @@ class SweepBatch:
                     j = arr[k]
                     j.spacing, j.x_min, j.y_min = g.spacing_mm, g.x_min_mm, g.y_min_mm
                     j.m, j.n, j.j_lo, j.j_hi = g.m, g.n, lo, hi
-                    j.ld = s.j_hi - s.j_lo + 1
-                    j.keys = keys_ptr + (s.key_off + (lo - s.j_lo)) * 8
+                    if s.n_strips > 1:  # contiguous rows x (hi - lo + 1) slab of strip_keys
+                        j.ld = hi - lo + 1
+                        j.keys = strip_ptr + (s.strip_off + (g.m + 1) * (lo - s.j_lo)) * 8
+                    else:
+                        j.ld = s.j_hi - s.j_lo + 1
+                        j.keys = keys_ptr + (s.key_off + (lo - s.j_lo)) * 8
                     j.t_start, j.dt, j.steps = p.t_start, p.dt, p.steps
                     j.step_lo, j.step_hi = s_lo, s_hi
                     j.y0, j.feed_speed, j.omega = p.y0, p.feed_speed, p.omega
@@ -274,10 +296,13 @@ class SweepBatch:
         self.buf = ar.upload(self.dev, fill)
         self._fresh = True
         self.base = self.buf.data_ptr()
+        self.offs = offs
         self.same_shape = len({s.nodes for s in surfs}) == 1
+        # one fill / decode launch for the whole batch (no strip-layout surface)
+        self.batched_fill = self.same_shape and all(s.n_strips == 1 for s in surfs)
         sweeps = sum((sum(1 for t in tl if t) if len(gm[1]) <= ONE_JOB_LAUNCH_MAX else 1)
                      for gm, tl in zip(self.group_meta, self.group_tiles))
-        self.launches_per_run = 2 * (1 if self.same_shape else n) + sweeps
+        self.launches_per_run = 2 * (1 if self.batched_fill else n) + sweeps
 
     # ------------------------------------------------------------------
     def launch_fill(self, sp: int) -> None:
@@ -287,13 +312,13 @@ class SweepBatch:
             self._fresh = False
         else:
             self.buf[self.ctr_off: self.ctr_off + self.n * (_native.NUM_CTRS + 1) * 8].zero_()
-        if self.same_shape:
+        if self.batched_fill:
             _native.check(lib.msurf_fill_keys(keys_ptr, self.surfs[0].nodes, self.n,
                                               base + self.sentinel_off, sp))
         else:
             for i, s in enumerate(self.surfs):
-                _native.check(lib.msurf_fill_keys(keys_ptr + s.key_off * 8, s.nodes, 1,
-                                                  base + self.sentinel_off + 8 * i, sp))
+                dst = (self.strip_keys.data_ptr() + s.strip_off * 8) if s.n_strips > 1 else keys_ptr + s.key_off * 8
+                _native.check(lib.msurf_fill_keys(dst, s.nodes, 1, base + self.sentinel_off + 8 * i, sp))
 
     def launch_sweep(self, sp: int) -> None:
         """One msurf_sweep launch per kinematics mode present in the batch."""
@@ -314,11 +339,17 @@ class SweepBatch:
     def launch_decode(self, sp: int) -> None:
         """Keys -> fp64 heights in place, machined-cell counts."""
         lib, base, keys_ptr = self.lib, self.base, self.keys.data_ptr()
-        if self.same_shape:
+        if self.batched_fill:
             _native.check(lib.msurf_decode(keys_ptr, self.surfs[0].nodes, self.n, base + self.sentinel_off,
                                            base + self.machined_off, sp))
         else:
             for i, s in enumerate(self.surfs):
+                if s.n_strips > 1:
+                    _native.check(lib.msurf_decode_strips(
+                        self.strip_keys.data_ptr() + s.strip_off * 8, keys_ptr + s.key_off * 8, s.plan.grid.m + 1,
+                        s.j_hi - s.j_lo + 1, s.n_strips, base + self.offs[i]["col0"],
+                        base + self.sentinel_off + 8 * i, base + self.machined_off + 8 * i, sp))
+                    continue
                 _native.check(lib.msurf_decode(keys_ptr + s.key_off * 8, s.nodes, 1,
                                                base + self.sentinel_off + 8 * i,
                                                base + self.machined_off + 8 * i, sp))

@@ -36,9 +36,10 @@ sys.path.insert(0, ROOT)
 
 METRIC = "edge-point updates/s"
 UNIT = "updates/s"
-# algorithmic FP64 operations per evaluated edge point (DESIGN.md §4):
-# affine/rotation + feed/offset adds + cell location (2 x [sub, div, add, floor])
-FLOPS_PER_POINT = {0: 20, 1: 16, 2: 23}
+# algorithmic FP64 operations per evaluated edge point (DESIGN.md §4.2):
+# REF 6 mul + 6 add, EXT 4 mul + 4 add, EXT+tilt 6 mul + 6 add (u, v, x', y',
+# z' of the tilt model), plus the cell location 2 x [sub, div, add, floor]
+FLOPS_PER_POINT = {0: 20, 1: 16, 2: 20}
 FLOPS_PER_ROW = 2 * 60 + 32  # 2*C_trig + 32, C_trig ~ 60 ops (double-double sincos)
 
 

@@ -496,13 +496,14 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
     return;
   }
 
-  // ---------------- phase 2: lane = live step, warp walks the 32 points of a chunk
-  // unit = (group of 32 consecutive live steps, 32-point chunk). Each lane
-  // keeps its step's transform in registers; the chunk's point records are
-  // warp-broadcast loads (L1-resident). Consecutive live steps of one point
-  // sit in neighbouring lanes: a lane whose cell equals its predecessor's and
-  // whose key is not lower skips its deposit (the predecessor's run covers it),
-  // so each run of a point through a cell costs one RED.MIN.
+  // ---------------- phase 2: lane = live step(s), warp walks the 32 points of a chunk
+  // unit = (group of consecutive live steps, 32-point chunk). Each lane keeps
+  // its step's transform (tilt: its two steps' transforms) in registers; the
+  // chunk's point records are staged once in shared memory and read as warp
+  // broadcasts. Consecutive live steps of one point sit in neighbouring
+  // lanes (or in one lane's pair): the time-neighbour filter skips a deposit
+  // only when a same-cell neighbour provably deposits a key that is not
+  // higher, so each monotone run of a point through a cell costs one RED.MIN.
   const double inv = 1.0 / dd;
   const double cx0 = 0.5 - J.x_min * inv;
   const double cy0 = 0.5 - J.y_min * inv;

@@ -48,6 +48,11 @@ class MsurfJob(ctypes.Structure):
     ]
 
 
+# the same layout as a NumPy structured dtype: SweepBatch builds its descriptor
+# tables as arrays of these rows (one np.array call per launch group)
+JOB_DTYPE = np.dtype(MsurfJob)
+
+
 class MsurfGeomIn(ctypes.Structure):
     """Mirror of msurf_geom_in (include/msurf.h)."""
 
@@ -187,6 +192,7 @@ class Arena:
             if a is not None:
                 host[off:off + a.nbytes] = a.view(np.uint8).reshape(-1)
         for off, b in extra:
-            host[off:off + len(b)] = np.frombuffer(b, dtype=np.uint8)
+            b = b if isinstance(b, np.ndarray) else np.frombuffer(b, dtype=np.uint8)
+            host[off:off + b.nbytes] = b
         dev.copy_(stage, non_blocking=True)
         return dev

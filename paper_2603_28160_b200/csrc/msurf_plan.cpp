@@ -234,6 +234,7 @@ int msurf_plan_finish(const msurf_geom_in* in, const double* px, const double* p
 // teeth and points): set b reads ins[b] and writes its slice of every output
 // (teeth*points, teeth*nchunk*6, ... elements per set). Sets are independent:
 // `threads` host threads split them (results do not depend on the split).
+#include <atomic>
 #include <thread>
 
 namespace {
@@ -262,11 +263,11 @@ int msurf_plan_geometry_many(const msurf_geom_in* ins, int32_t n, double* px, do
   const long per = (long)ins[0].teeth * ins[0].points;
   for (int b = 0; b < n; ++b)
     if (ins[b].teeth != ins[0].teeth || ins[b].points != ins[0].points || ins[b].mode == MSURF_MODE_REF) return 1;
-  int bad = 0;
+  std::atomic<int> bad{0};
   for_sets(n, threads, [&](int b) {
     if (msurf_plan_geometry(ins + b, px + b * per, py + b * per, pz + b * per, stats2 + 2 * b)) bad = 1;
   });
-  return bad;
+  return bad.load();
 }
 
 int msurf_plan_finish_many(const msurf_geom_in* ins, int32_t n, const double* px, const double* py, const double* pz,
@@ -275,7 +276,7 @@ int msurf_plan_finish_many(const msurf_geom_in* ins, int32_t n, const double* px
   if (!ins || n < 1) return 1;
   const int zn = ins[0].teeth, np = ins[0].points, nchunk = (np + kChunk - 1) / kChunk;
   const long per = (long)zn * np;
-  int bad = 0;
+  std::atomic<int> bad{0};
   for_sets(n, threads, [&](int b) {
     if (msurf_plan_finish(ins + b, px + b * per, py + b * per, pz + b * per, zoff[b], pts + b * per * 4,
                           tooth_box + (long)b * zn * 6, chunk_circ + (long)b * zn * nchunk * 6,
@@ -283,7 +284,7 @@ int msurf_plan_finish_many(const msurf_geom_in* ins, int32_t n, const double* px
                           zw_out ? zw_out + b * per : nullptr, key_out ? key_out + b * per : nullptr))
       bad = 1;
   });
-  return bad;
+  return bad.load();
 }
 
 }  // extern "C"

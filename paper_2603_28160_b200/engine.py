@@ -25,15 +25,31 @@ from . import _native
 from .errors import ConfigError, MillsurfError
 from .extensions import Extensions
 from .grid import GridSpec, HeightField, TrajectoryRecord
-from .planner import MODE_REF, SweepPlan, chunk_f32, plan, plan_many, step_window, time_step
+from .planner import DEVICE_FIELDS, MODE_REF, SweepPlan, chunk_f32, plan, plan_many, step_window, time_step
 
 DEFAULT_MAX_STEP_ANGLE_RAD = math.radians(0.5)
 # Z-map bytes one sweep job may cover: keeps its RED.MIN traffic in the
 # 126 MB L2 (surfaces above this are cut into feed-direction sub-strips)
 L2_TILE_BYTES = int(float(__import__("os").environ.get("MSURF_L2_TILE_MB", "48")) * (1 << 20))
-# groups of at most this many jobs launch one msurf_sweep_job per job
+# groups of at most this many jobs launch one msurf_sweep_job per job, provided
+# each job fills the GPU several times over (>= ONE_JOB_MIN_TILES tiles: the L2
+# sub-strips of one large surface); groups of many small surfaces take one
+# batched launch (per-job launches would pay a grid tail per surface:
+# config 3 in launch groups of 32 sets, 2.1 -> 1.2 ms per group)
 ONE_JOB_LAUNCH_MAX = int(__import__("os").environ.get("MSURF_ONE_JOB_MAX", "32"))
+ONE_JOB_MIN_TILES = int(__import__("os").environ.get("MSURF_ONE_JOB_MIN_TILES", "16384"))
+
+
+def _per_job_launches(tiles) -> bool:
+    live = [t for t in tiles if t]
+    return len(live) <= 1 or (len(tiles) <= ONE_JOB_LAUNCH_MAX and min(live) >= ONE_JOB_MIN_TILES)
 PIPELINE_PLAN_THREADS = int(__import__("os").environ.get("MSURF_PIPELINE_THREADS", "3"))
+# size of the first launch group of a pipelined batch (the GPU starts sooner)
+PIPELINE_FIRST_CHUNK = int(__import__("os").environ.get("MSURF_FIRST_CHUNK", "0"))
+# native planner threads for the first group (planned while nothing else runs)
+PIPELINE_FIRST_THREADS = int(__import__("os").environ.get("MSURF_FIRST_THREADS", "1"))
+# threads of the native planning loops of every group (GIL released)
+PIPELINE_NATIVE_THREADS = int(__import__("os").environ.get("MSURF_NATIVE_THREADS", "1"))
 
 __all__ = ["SimulationConfig", "SimulationResult", "time_step", "simulate", "simulate_batch",
            "simulate_reference", "run_benchmark", "BenchmarkReport", "BenchmarkRow", "sweep_plans"]
@@ -188,27 +204,46 @@ class SweepBatch:
         self.traj = torch.empty(traj_len, dtype=torch.float64, device=self.dev) if traj_len else None
 
         ar = _native.Arena()
-        offs = []
-        for s in surfs:
-            p = s.plan
-            o = dict(
-                tooth_base=ar.add(p.tooth_base.astype(np.float64, copy=False)),
-                tooth_rows=ar.add(p.tooth_rows.astype(np.float64, copy=False)),
-                pts=ar.add(p.pts.astype(np.float64, copy=False)),
-                tooth_box=ar.add(p.tooth_box.astype(np.float64, copy=False)),
-                chunk_circ=ar.add(p.chunk_circ.astype(np.float64, copy=False)),
-                chunk_f32=ar.add(chunk_f32(p.chunk_circ, p.tooth_box)),
-                pass_x0=ar.add(p.pass_x0.astype(np.float64, copy=False)),
-                min_index=ar.add(p.min_index.astype(np.int32, copy=False)),
-            )
-            if s.n_strips > 1:
-                o["col0"] = ar.add(np.asarray(s.col0, dtype=np.int64))
-            if trig == "host":
-                tab, vib = _trig_tables(p)
-                o["trig_table"] = ar.add(tab)
-                if vib is not None:
-                    o["vib_table"] = ar.add(vib)
-            offs.append(o)
+        offs = [None] * len(surfs)
+        i = 0
+        while i < len(surfs):
+            p = surfs[i].plan
+            grp = p.group
+            if grp is not None and grp[0].owns(p, grp[1]):
+                # a run of consecutive sets planned together: one slice per field
+                g, b0 = grp
+                k = i + 1
+                while (k < len(surfs) and surfs[k].plan.group is not None and surfs[k].plan.group[0] is g
+                       and surfs[k].plan.group[1] == b0 + (k - i) and g.owns(surfs[k].plan, b0 + (k - i))):
+                    k += 1
+                run = {}
+                for f in DEVICE_FIELDS:
+                    a = g.arrays[f]
+                    run[f] = (ar.add(a[b0: b0 + (k - i)]), a[0].nbytes)
+                for q in range(i, k):
+                    offs[q] = {f: o + (q - i) * nb for f, (o, nb) in run.items()}
+            else:
+                k = i + 1
+                offs[i] = dict(
+                    tooth_base=ar.add(p.tooth_base.astype(np.float64, copy=False)),
+                    tooth_rows=ar.add(p.tooth_rows.astype(np.float64, copy=False)),
+                    pts=ar.add(p.pts.astype(np.float64, copy=False)),
+                    tooth_box=ar.add(p.tooth_box.astype(np.float64, copy=False)),
+                    chunk_circ=ar.add(p.chunk_circ.astype(np.float64, copy=False)),
+                    chunk_f32=ar.add(chunk_f32(p.chunk_circ, p.tooth_box)),
+                    pass_x0=ar.add(p.pass_x0.astype(np.float64, copy=False)),
+                    min_index=ar.add(p.min_index.astype(np.int32, copy=False)),
+                )
+            for q in range(i, k):
+                s, o = surfs[q], offs[q]
+                if s.n_strips > 1:
+                    o["col0"] = ar.add(np.asarray(s.col0, dtype=np.int64))
+                if trig == "host":
+                    tab, vib = _trig_tables(s.plan)
+                    o["trig_table"] = ar.add(tab)
+                    if vib is not None:
+                        o["vib_table"] = ar.add(vib)
+            i = k
         n = len(surfs)
         self.n = n
         self.sentinel_off = ar.add(np.array([s.plan.initial_height for s in surfs], dtype=np.float64))
@@ -257,38 +292,33 @@ class SweepBatch:
                 toff += s.plan.steps * s.plan.teeth * 3
 
         def fill(base):
+            # descriptors as rows of a structured array with msurf_job's layout
             out = []
             for mode, jidx, job_off, _, _, _ in self.group_meta:
-                arr = (_native.MsurfJob * len(jidx))()
-                for k, jn in enumerate(jidx):
+                rows = []
+                for jn in jidx:
                     i, lo, hi, s_lo, s_hi = jobs[jn]
                     s, o, p = surfs[i], offs[i], surfs[i].plan
                     g = p.grid
-                    j = arr[k]
-                    j.spacing, j.x_min, j.y_min = g.spacing_mm, g.x_min_mm, g.y_min_mm
-                    j.m, j.n, j.j_lo, j.j_hi = g.m, g.n, lo, hi
                     if s.n_strips > 1:  # contiguous rows x (hi - lo + 1) slab of strip_keys
-                        j.ld = hi - lo + 1
-                        j.keys = strip_ptr + (s.strip_off + (g.m + 1) * (lo - s.j_lo)) * 8
+                        ld, kp = hi - lo + 1, strip_ptr + (s.strip_off + (g.m + 1) * (lo - s.j_lo)) * 8
                     else:
-                        j.ld = s.j_hi - s.j_lo + 1
-                        j.keys = keys_ptr + (s.key_off + (lo - s.j_lo)) * 8
-                    j.t_start, j.dt, j.steps = p.t_start, p.dt, p.steps
-                    j.step_lo, j.step_hi = s_lo, s_hi
-                    j.y0, j.feed_speed, j.omega = p.y0, p.feed_speed, p.omega
-                    for name in ("tooth_base", "tooth_rows", "pts", "tooth_box", "chunk_circ", "chunk_f32",
-                                 "pass_x0", "min_index"):
-                        setattr(j, name, base + o[name])
-                    j.counters = base + self.ctr_off + i * _native.NUM_CTRS * 8
-                    j.tilt_c, j.tilt_s, j.zoff = p.tilt_c, p.tilt_s, p.zoff
-                    j.vib_amp, j.vib_omega, j.vib_phase = p.vib_amp, p.vib_omega, p.vib_phase
-                    j.trig_table = base + o["trig_table"] if "trig_table" in o else None
-                    j.vib_table = base + o["vib_table"] if "vib_table" in o else None
+                        ld, kp = s.j_hi - s.j_lo + 1, keys_ptr + (s.key_off + (lo - s.j_lo)) * 8
                     # trajectory rows are written by the job that owns column j_lo of
                     # the surface and covers every step (REF mode records need no cull)
-                    j.traj = (traj_ptr + self.traj_off[i] * 8) if (self.need_traj[i] and lo == s.j_lo) else None
-                    j.teeth, j.points, j.passes = p.teeth, p.points, p.passes
-                out.append((job_off, bytes(arr)))
+                    tr = (traj_ptr + self.traj_off[i] * 8) if (self.need_traj[i] and lo == s.j_lo) else 0
+                    rows.append((
+                        g.spacing_mm, g.x_min_mm, g.y_min_mm, g.m, g.n, lo, hi, ld, kp,
+                        p.t_start, p.dt, p.steps, s_lo, s_hi, p.y0, p.feed_speed, p.omega,
+                        base + o["tooth_base"], base + o["tooth_rows"], base + o["pts"], base + o["tooth_box"],
+                        base + o["chunk_circ"], base + o["chunk_f32"], base + o["pass_x0"],
+                        p.tilt_c, p.tilt_s, p.zoff, p.vib_amp, p.vib_omega, p.vib_phase,
+                        base + o["trig_table"] if "trig_table" in o else 0,
+                        base + o["vib_table"] if "vib_table" in o else 0,
+                        tr, base + o["min_index"], base + self.ctr_off + i * _native.NUM_CTRS * 8,
+                        p.teeth, p.points, p.passes, 0))
+                arr = np.array(rows, dtype=_native.JOB_DTYPE)
+                out.append((job_off, arr.view(np.uint8)))
                 self.group_host_jobs.append(arr)
             return out
 
@@ -300,8 +330,8 @@ class SweepBatch:
         self.same_shape = len({s.nodes for s in surfs}) == 1
         # one fill / decode launch for the whole batch (no strip-layout surface)
         self.batched_fill = self.same_shape and all(s.n_strips == 1 for s in surfs)
-        sweeps = sum((sum(1 for t in tl if t) if len(gm[1]) <= ONE_JOB_LAUNCH_MAX else 1)
-                     for gm, tl in zip(self.group_meta, self.group_tiles))
+        self.group_per_job = [_per_job_launches(tl) for tl in self.group_tiles]
+        sweeps = sum((sum(1 for t in tl if t) if pj else 1) for pj, tl in zip(self.group_per_job, self.group_tiles))
         self.launches_per_run = 2 * (1 if self.batched_fill else n) + sweeps
 
     # ------------------------------------------------------------------
@@ -325,13 +355,13 @@ class SweepBatch:
         lib, base = self.lib, self.base
         for g, (mode, idx, job_off, pre_off, n_tiles, max_pts) in enumerate(self.group_meta):
             flag = _native.SWEEP_DIAG if self.diagnostics else 0
-            if len(idx) <= ONE_JOB_LAUNCH_MAX:
-                # few jobs (one surface, or its L2 sub-strips): one launch per job
+            if self.group_per_job[g]:
+                # one job, or the L2 sub-strips of a large surface: one launch per job
                 # with the descriptor passed by value (constant-bank operands)
-                arr = self.group_host_jobs[g]
+                ptr, sz = self.group_host_jobs[g].ctypes.data, _native.JOB_DTYPE.itemsize
                 for k, t in enumerate(self.group_tiles[g]):
                     if t:
-                        _native.check(lib.msurf_sweep_job(ctypes.addressof(arr[k]), mode | flag, max_pts, sp))
+                        _native.check(lib.msurf_sweep_job(ptr + k * sz, mode | flag, max_pts, sp))
                 continue
             _native.check(lib.msurf_sweep(base + job_off, len(idx), base + pre_off, n_tiles, mode | flag,
                                           max_pts, sp))
@@ -498,7 +528,9 @@ def simulate_batch(configs, extensions=None, *, trig: str = "device", diagnostic
         return []
     if chunk is None:
         chunk = 32 if len(configs) >= 128 else max(4, -(-len(configs) // 4))
-    bounds = [(lo, min(len(configs), lo + chunk)) for lo in range(0, len(configs), chunk)]
+    first = min(chunk, PIPELINE_FIRST_CHUNK) if PIPELINE_FIRST_CHUNK > 0 else chunk
+    bounds = [(0, min(len(configs), first))]
+    bounds += [(lo, min(len(configs), lo + chunk)) for lo in range(bounds[0][1], len(configs), chunk)]
     if len(bounds) == 1:
         return _launch_results(plan_many(configs, exts), trig, diagnostics, prefetch)
     # launch groups are planned concurrently on host threads (one vectorised
@@ -511,7 +543,9 @@ def simulate_batch(configs, extensions=None, *, trig: str = "device", diagnostic
     out = []
     # a few workers only: group 0 is ready early, later groups keep pace with the GPU
     with ThreadPoolExecutor(max_workers=min(PIPELINE_PLAN_THREADS, PLAN_THREADS, len(bounds))) as pool:
-        futs = [pool.submit(plan_many, configs[lo:hi], exts[lo:hi], 1) for lo, hi in bounds]
+        futs = [pool.submit(plan_many, configs[lo:hi], exts[lo:hi], PIPELINE_FIRST_THREADS if k == 0 else 1,
+                            PIPELINE_NATIVE_THREADS)
+                for k, (lo, hi) in enumerate(bounds)]
         for f in futs:
             out.extend(_launch_results(f.result(), trig, diagnostics, prefetch))
     return out

@@ -97,6 +97,7 @@ class SweepPlan:
     chunk_circ: np.ndarray | None = None # (Z, nchunk, 6) device cull records
     tooth_box: np.ndarray | None = None  # (Z, 6) whole-tooth tool-frame boxes
     extras: dict = field(default_factory=dict)
+    group: tuple | None = None           # (PlanGroup, index) when planned by plan_many
 
     @property
     def passes(self) -> int:
@@ -262,14 +263,40 @@ def chunk_f32(chunk_circ: np.ndarray, tooth_box: np.ndarray) -> np.ndarray:
     """fp32 phase-1 cull records (msurf_job.chunk_f32): per tooth and chunk
     (xc, yc, rx, ry, yz, Rt, 0, 0), Rt = max|x| + max|y| + max|z| of the tooth
     box. The kernel widens its fp32 test by 4e-6 (Rt + |offset|) + 1e-6 mm,
-    which covers the fp32 roundings of every term."""
-    z_n, nchunk, _ = chunk_circ.shape
-    out = np.zeros((z_n, nchunk, 8), dtype=np.float32)
-    out[:, :, :5] = chunk_circ[:, :, :5]
+    which covers the fp32 roundings of every term. Leading
+    (set) axes are allowed: (..., Z, nchunk, 6) and (..., Z, 6)."""
+    out = np.zeros(chunk_circ.shape[:-1] + (8,), dtype=np.float32)
+    out[..., :5] = chunk_circ[..., :5]
     b = np.abs(tooth_box)
-    rt = np.maximum(b[:, 0], b[:, 1]) + np.maximum(b[:, 2], b[:, 3]) + np.maximum(b[:, 4], b[:, 5])
-    out[:, :, 5] = rt[:, None]
+    rt = (np.maximum(b[..., 0], b[..., 1]) + np.maximum(b[..., 2], b[..., 3])
+          + np.maximum(b[..., 4], b[..., 5]))
+    out[..., 5] = rt[..., None]
     return out
+
+
+# msurf_job array fields, in the order SweepBatch packs them
+DEVICE_FIELDS = ("tooth_base", "tooth_rows", "pts", "tooth_box", "chunk_circ", "chunk_f32", "pass_x0", "min_index")
+
+
+class PlanGroup:
+    """Device arrays of parameter sets planned together (plan_many): one
+    (sets, ...) array per msurf_job field, each set's plan holding views
+    ``arrays[name][b]``. SweepBatch packs a run of consecutive sets of one
+    group as ONE slice per field instead of one small array per set."""
+
+    __slots__ = ("arrays", "views")
+
+    def __init__(self, arrays: dict):
+        self.arrays = arrays
+        self.views = [tuple(arrays[f][b] for f in DEVICE_FIELDS if f != "chunk_f32")
+                      for b in range(len(arrays["pts"]))]
+
+    def owns(self, p: "SweepPlan", b: int) -> bool:
+        """True while the plan still holds this group's views (a plan whose
+        arrays were replaced after planning is packed on its own)."""
+        v = self.views[b]
+        return (p.tooth_base is v[0] and p.tooth_rows is v[1] and p.pts is v[2] and p.tooth_box is v[3]
+                and p.chunk_circ is v[4] and p.pass_x0 is v[5] and p.min_index is v[6])
 
 
 def _check_device_limits(p: SweepPlan, grid) -> None:
@@ -545,13 +572,13 @@ def _ext_group_key(config, ext: Extensions):
             tool.radial_rake_rad, tool.axial_rake_rad, tool.runouts_mm, proc.depth_of_cut_mm, half,
             config.edge_point_count, grid.spacing_mm, ext.tilt_rad, ext.noise_sigma_mm, ext.noise_corr_mm,
             ext.noise_seed, ext.helix_ref_radius_mm, bool(ext.helix_angle_rad != 0.0),
-            bool(ext.runout_offset_mm != 0.0))
+            bool(ext.runout_offset_mm != 0.0), int(ext.passes))
 
 
 PLAN_THREADS = max(1, min(8, (__import__("os").cpu_count() or 1)))
 
 
-def plan_many(configs, exts, threads: int | None = None):
+def plan_many(configs, exts, threads: int | None = None, native_threads: int = 1):
     """plan() for many parameter sets. Extended-model sets that share their
     edge geometry are planned together with (sets, teeth, points) arrays —
     the same element-wise operations as plan(), so every array is bitwise
@@ -583,6 +610,8 @@ def plan_many(configs, exts, threads: int | None = None):
     if jobs:
         def run(sub):
             fn = _plan_ext_group_native if NATIVE_PLAN else _plan_ext_group
+            if fn is _plan_ext_group_native:  # native loops over sets on their own threads (GIL released)
+                return sub, fn([configs[i] for i in sub], [exts[i] for i in sub], native_threads)
             return sub, fn([configs[i] for i in sub], [exts[i] for i in sub])
 
         if len(jobs) == 1:
@@ -682,23 +711,30 @@ def _plan_ext_group_native(configs, exts, threads: int = 1):
                                   pts.ctypes.data, tbox.ctypes.data, circ.ctypes.data, cbox.ctypes.data,
                                   mins.ctypes.data, zw.ctypes.data, zkey.ctypes.data, threads):
         raise DomainError("native planner rejected the geometry")
+    n_pass = {int(e.passes) for e in exts}
+    if len(n_pass) != 1:
+        raise DomainError("a plan group needs one pass count")  # _ext_group_key includes it
+    n_pass = n_pass.pop()
+    tbase = np.array([[tooth_base_angle(cfg.process.phase_rad, k, z_n) for k in range(1, z_n + 1)]
+                      for cfg in configs], dtype=np.float64)
+    px0 = np.array([[spans[b][3] + k * e.stepover_mm for k in range(n_pass)]
+                    for b, e in enumerate(exts)], dtype=np.float64)
+    grp = PlanGroup({"tooth_base": tbase, "tooth_rows": np.zeros((B, z_n, 8)), "pts": pts, "tooth_box": tbox,
+                     "chunk_circ": circ, "chunk_f32": chunk_f32(circ, tbox), "pass_x0": px0,
+                     "min_index": mins})
     plans = []
     for b, (cfg, e) in enumerate(zip(configs, exts)):
         proc, grid = cfg.process, cfg.grid
         dt, t_start, steps, x0, y0, z0 = spans[b]
+        v = grp.views[b]
         p = SweepPlan(
             mode=mode, grid=grid, teeth=z_n, points=n, steps=steps, dt=dt, t_start=t_start, x0=x0, y0=y0, z0=z0,
             feed_speed=proc.feed_speed_mm_s, omega=proc.angular_velocity_rad_s, initial_height=z0 + a_p,
-            half_length=half,
-            tooth_base=np.array([tooth_base_angle(proc.phase_rad, k, z_n) for k in range(1, z_n + 1)]),
-            tooth_rows=np.zeros((z_n, 8)), px=px[b], py=py[b], pz=pz[b], zw=zw[b], zkey=zkey[b],
-            chunk_box=cbox[b], pass_x0=np.array([x0 + k * e.stepover_mm for k in range(int(e.passes))],
-                                                dtype=np.float64),
-            min_index=mins[b], tilt_c=tc, tilt_s=ts, zoff=float(zoffs[b]), vib_amp=e.vib_amplitude_mm,
-            vib_omega=2.0 * math.pi * e.vib_frequency_hz, vib_phase=e.vib_phase_rad,
-            extras={"base_margin": base_margin})
-        p.pts, p.chunk_circ, p.tooth_box = pts[b], circ[b], tbox[b]
-        p.record = False
+            half_length=half, tooth_base=v[0], tooth_rows=v[1], px=px[b], py=py[b], pz=pz[b], zw=zw[b],
+            zkey=zkey[b], chunk_box=cbox[b], pass_x0=v[5], min_index=v[6], tilt_c=tc, tilt_s=ts,
+            zoff=float(zoffs[b]), vib_amp=e.vib_amplitude_mm, vib_omega=2.0 * math.pi * e.vib_frequency_hz,
+            vib_phase=e.vib_phase_rad, extras={"base_margin": base_margin}, pts=v[2], chunk_circ=v[4],
+            tooth_box=v[3], group=(grp, b))
         _check_device_limits(p, grid)
         plans.append(p)
     return plans

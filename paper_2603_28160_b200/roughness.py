@@ -103,19 +103,44 @@ def _metrics_from_moments(st1, st2) -> ArealMetrics:
 
 
 class _Scratch:
-    """Per-device scratch for the reductions (work partials + outputs)."""
+    """Per-device scratch for the reductions: ``n_work`` surfaces of work
+    partials (MSURF_WORK_DOUBLES each) followed by ``n_out`` x 16 outputs."""
 
     _cache = {}
 
     @classmethod
-    def get(cls, torch, device, n_surf: int):
+    def get(cls, torch, device, n_work: int, n_out: int | None = None):
         key = (device.index if device.index is not None else torch.cuda.current_device())
-        need = n_surf * _native.WORK_DOUBLES + n_surf * 16
+        n_out = n_work if n_out is None else n_out
+        need = n_work * _native.WORK_DOUBLES + n_out * 16
         t = cls._cache.get(key)
         if t is None or t.numel() < need:
             t = torch.empty(need, dtype=torch.float64, device=device)
             cls._cache[key] = t
         return t
+
+
+def _areal_enqueue(lib, h_dev, ld, n_surf, surf_stride, roi_box, sentinels_dev, exclude, work, out, sp,
+                   allreduce=None):
+    """Enqueue both areal passes of ``n_surf`` surfaces; ``out`` (>= 10 n_surf
+    doubles) receives stats1 [n_surf, 6] then moments [n_surf, 4]."""
+    i_lo, j_lo, rows, cols = roi_box
+    st1 = out[: n_surf * 6]
+    st2 = out[n_surf * 6: n_surf * 10]
+    _native.check(lib.msurf_areal_pass1(h_dev.data_ptr(), ld, surf_stride, n_surf, i_lo, j_lo, rows,
+                                        cols, sentinels_dev.data_ptr(), int(exclude), work,
+                                        st1.data_ptr(), sp))
+    if allreduce is not None:
+        allreduce(st1.view(n_surf, 6), "stats1")
+    _native.check(lib.msurf_areal_pass2(h_dev.data_ptr(), ld, surf_stride, n_surf, i_lo, j_lo, rows,
+                                        cols, sentinels_dev.data_ptr(), int(exclude), st1.data_ptr(),
+                                        work, st2.data_ptr(), sp))
+    if allreduce is not None:
+        allreduce(st2.view(n_surf, 4), "moments")
+
+
+def _split_moments(both, n_surf):
+    return both[: n_surf * 6].reshape(n_surf, 6), both[n_surf * 6: n_surf * 10].reshape(n_surf, 4)
 
 
 def areal_moments_device(h_dev, ld, n_surf, surf_stride, roi_box, sentinels_dev, exclude,
@@ -127,26 +152,11 @@ def areal_moments_device(h_dev, ld, n_surf, surf_stride, roi_box, sentinels_dev,
     "moments": four sums) across ranks in place."""
     torch = _native.require_cuda()
     lib = _native.lib()
-    i_lo, j_lo, rows, cols = roi_box
-    dev = h_dev.device
-    sc = _Scratch.get(torch, dev, n_surf)
-    work = sc.data_ptr()
-    out1 = sc[n_surf * _native.WORK_DOUBLES:]
-    st1 = out1[: n_surf * 6]
-    st2 = out1[n_surf * 6: n_surf * 10]
-    sp = _native.stream_ptr()
-    _native.check(lib.msurf_areal_pass1(h_dev.data_ptr(), ld, surf_stride, n_surf, i_lo, j_lo, rows,
-                                        cols, sentinels_dev.data_ptr(), int(exclude), work,
-                                        st1.data_ptr(), sp))
-    if allreduce is not None:
-        allreduce(st1.view(n_surf, 6), "stats1")
-    _native.check(lib.msurf_areal_pass2(h_dev.data_ptr(), ld, surf_stride, n_surf, i_lo, j_lo, rows,
-                                        cols, sentinels_dev.data_ptr(), int(exclude), st1.data_ptr(),
-                                        work, st2.data_ptr(), sp))
-    if allreduce is not None:
-        allreduce(st2.view(n_surf, 4), "moments")
-    both = out1[: n_surf * 10].cpu().numpy()
-    return both[: n_surf * 6].reshape(n_surf, 6), both[n_surf * 6:].reshape(n_surf, 4)
+    sc = _Scratch.get(torch, h_dev.device, n_surf)
+    out = sc[n_surf * _native.WORK_DOUBLES:]
+    _areal_enqueue(lib, h_dev, ld, n_surf, surf_stride, roi_box, sentinels_dev, exclude, sc.data_ptr(), out,
+                   _native.stream_ptr(), allreduce)
+    return _split_moments(out[: n_surf * 10].cpu().numpy(), n_surf)
 
 
 def _sentinel_tensor(torch, values, device):
@@ -237,55 +247,78 @@ def _finish_areal(st1, st2, uncut) -> ArealMetrics:
 def areal_metrics_batch(fields, roi=None, uncut: str = "raise"):
     """Areal metrics of many fields: each run of consecutive same-shape fields
     that sit at a constant stride in one device buffer (the output of one
-    simulate_batch launch group) is reduced in two launches; anything else
-    falls back to one call per field. Returns a list of ArealMetrics or
-    DomainError instances (per-sample status, dataset.py:177-180)."""
+    simulate_batch launch group) is reduced in two launches; every run's
+    passes are enqueued first and all results come back in ONE device-to-host
+    copy. Returns a list of ArealMetrics or DomainError instances (per-sample
+    status, dataset.py:177-180)."""
     if not fields:
         return []
+    if uncut not in ("raise", "exclude"):
+        raise DomainError(f"uncut must be 'raise' or 'exclude', got {uncut!r}")
+    torch = _native.require_cuda()
+    lib = _native.lib()
     devs = [f.device_heights() for f in fields]
-    out, a = [], 0
+    runs, a = [], 0  # (a, b, stride in doubles)
     while a < len(fields):
         b = a + 1
         spec = fields[a].spec
         st = None
-        if b < len(fields) and fields[b].spec == spec:
+        if b < len(fields) and fields[b].spec == spec and devs[b].device == devs[a].device:
             st = devs[b].data_ptr() - devs[a].data_ptr()
             if st <= 0 or st % 8:
                 st = None
         if st is not None:
-            while (b < len(fields) and fields[b].spec == spec
+            while (b < len(fields) and fields[b].spec == spec and devs[b].device == devs[a].device
                    and devs[b].data_ptr() == devs[a].data_ptr() + (b - a) * st):
                 b += 1
-            out.extend(_areal_run(fields[a:b], devs[a:b], st // 8, roi, uncut))
-        else:
+        runs.append((a, b, (st or 0) // 8))
+        a = b
+    res = [None] * len(runs)  # per run: (stats1, moments) or a DomainError for the run's one field
+    todo = {}
+    for r, (a, b, stride) in enumerate(runs):
+        try:
+            box = _check_roi(fields[a].spec, roi)
+        except DomainError as exc:
+            if b - a > 1:
+                raise
+            res[r] = exc
+            continue
+        todo.setdefault(devs[a].device, []).append((r, box))
+    for dev, rs in todo.items():
+        n_work = max(runs[r][1] - runs[r][0] for r, _ in rs)
+        n_out = sum(runs[r][1] - runs[r][0] for r, _ in rs)
+        sc = _Scratch.get(torch, dev, n_work, n_out)
+        outs = sc[n_work * _native.WORK_DOUBLES:]
+        sp = _native.stream_ptr()
+        pos, slots = 0, []
+        for r, (i_lo, j_lo, i_hi, j_hi) in rs:
+            a, b, stride = runs[r]
+            n = b - a
+            ss = [getattr(f, "_dev_sentinel", None) for f in fields[a:b]]
+            if (all(x is not None and x.device == dev for x in ss)
+                    and all(x.data_ptr() == ss[0].data_ptr() + 8 * k for k, x in enumerate(ss))):
+                # the batch's own contiguous device sentinels (simulate_batch): no H2D copy
+                sent = ss[0].as_strided((n,), (1,))
+            else:
+                sent = _sentinel_tensor(torch, [f.initial_height_mm for f in fields[a:b]], dev)
+            _areal_enqueue(lib, devs[a], fields[a].spec.n + 1, n, stride,
+                           (i_lo, j_lo, i_hi - i_lo + 1, j_hi - j_lo + 1), sent, uncut == "exclude",
+                           sc.data_ptr(), outs[pos * 10: (pos + n) * 10], sp)
+            slots.append((r, pos, n))
+            pos += n
+        both = outs[: n_out * 10].cpu().numpy()  # one D2H for every run on this device
+        for r, p0, n in slots:
+            res[r] = _split_moments(both[p0 * 10: (p0 + n) * 10], n)
+    out = []
+    for (a, b, _), rr in zip(runs, res):
+        if isinstance(rr, DomainError):
+            out.append(rr)
+            continue
+        for x, y in zip(*rr):
             try:
-                out.append(areal_metrics(fields[a], roi=roi, uncut=uncut))
+                out.append(_finish_areal(x, y, uncut))
             except DomainError as exc:
                 out.append(exc)
-        a = b
-    return out
-
-
-def _areal_run(fields, devs, stride, roi, uncut):
-    """Two-launch areal reduction of same-shape fields at a constant stride."""
-    torch = _native.require_cuda()
-    spec = fields[0].spec
-    i_lo, j_lo, i_hi, j_hi = _check_roi(spec, roi)
-    ss = [getattr(f, "_dev_sentinel", None) for f in fields]
-    if all(x is not None for x in ss) and all(x.data_ptr() == ss[0].data_ptr() + 8 * k for k, x in enumerate(ss)):
-        # the batch's own contiguous device sentinels (simulate_batch): no H2D copy
-        sent = ss[0].as_strided((len(fields),), (1,))
-    else:
-        sent = _sentinel_tensor(torch, [f.initial_height_mm for f in fields], devs[0].device)
-    st1, st2 = areal_moments_device(devs[0], spec.n + 1, len(fields), stride or 0,
-                                    (i_lo, j_lo, i_hi - i_lo + 1, j_hi - j_lo + 1), sent,
-                                    uncut == "exclude")
-    out = []
-    for a, b in zip(st1, st2):
-        try:
-            out.append(_finish_areal(a, b, uncut))
-        except DomainError as exc:
-            out.append(exc)
     return out
 
 

@@ -119,6 +119,30 @@ def test_batched_ext_same_shape_and_metrics():
         assert _rel(m.sa_um, exp["Sa"]) < REL and _rel(m.sku, exp["Sku"]) < REL
 
 
+def test_areal_metrics_batch_mixed_runs_equal_per_field():
+    """areal_metrics_batch over several launch groups (strided runs), a
+    host-built field, a different grid and an uncut-stock field: every entry
+    equals areal_metrics of that field alone (same kernels, one D2H)."""
+    cfg = _ext_cfg("ball")
+    exts = [ms.Extensions(profile="ball", helix_angle_rad=math.radians(15 + 4 * k)) for k in range(9)]
+    batch = ms.simulate_batch([cfg] * 9, exts, chunk=4)  # launch groups of 4, 4, 1
+    small = ms.simulate(golden_io.product_config(golden_io.load("small_3")["config"], record_trajectory=False))
+    host = ms.HeightField(batch[0].field.spec, batch[0].field.initial_height_mm,
+                          heights=batch[2].field.device_heights().cpu().numpy())
+    stock = ms.HeightField(batch[0].field.spec, batch[0].field.initial_height_mm)
+    fields = [b.field for b in batch[:5]] + [host, small.field, stock] + [b.field for b in batch[5:]]
+    for uncut in ("exclude", "raise"):
+        got = ms.areal_metrics_batch(fields, uncut=uncut)
+        assert len(got) == len(fields)
+        for f, g in zip(fields, got):
+            try:
+                exp = ms.areal_metrics(f, uncut=uncut)
+            except ms.DomainError as exc:
+                assert isinstance(g, ms.DomainError) and str(g) == str(exc)
+                continue
+            assert g == exp
+
+
 def test_profiles_ra_rz_every_k_rows():
     kw = EXT_CASES["ball_noise"]
     cfg = _ext_cfg("ball")

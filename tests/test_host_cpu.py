@@ -212,6 +212,20 @@ def test_device_required_no_cpu_fallback(monkeypatch):
         ms.simulate(golden_io.product_config(g["config"]))
 
 
+def test_job_dtype_matches_ctypes_layout():
+    """SweepBatch writes msurf_job rows through a NumPy structured dtype; every
+    field must land where the ctypes mirror (and the C header) puts it."""
+    names = [f for f, _ in _native.MsurfJob._fields_]
+    assert list(_native.JOB_DTYPE.names) == names
+    assert _native.JOB_DTYPE.itemsize == ctypes.sizeof(_native.MsurfJob)
+    vals = tuple((k + 1) * (0.5 if _native.JOB_DTYPE[f].kind == "f" else 3) for k, f in enumerate(names))
+    vals = tuple(int(v) if _native.JOB_DTYPE[f].kind != "f" else v for v, f in zip(vals, names))
+    row = np.array([vals], dtype=_native.JOB_DTYPE)
+    j = _native.MsurfJob.from_buffer_copy(row.tobytes())
+    for f, v in zip(names, vals):
+        assert (getattr(j, f) or 0) == v, f
+
+
 def test_plan_many_bitwise_equals_per_set_plan():
     """The vectorised batch planner (simulate_batch) reproduces plan() per set."""
     from paper_2603_28160_b200 import configs
@@ -237,3 +251,69 @@ def test_plan_many_bitwise_equals_per_set_plan():
         for f in ("steps", "dt", "t_start", "y0", "x0", "zoff", "initial_height", "mode", "tilt_c", "tilt_s",
                   "vib_amp", "vib_omega", "vib_phase", "feed_speed", "omega", "points", "teeth"):
             assert getattr(a, f) == getattr(b, f), f
+        if a.group is not None:  # group arrays SweepBatch packs as one slice per field
+            g, k = a.group
+            assert g.owns(a, k)
+            assert np.array_equal(g.arrays["chunk_f32"][k], planner.chunk_f32(b.chunk_circ, b.tooth_box))
+            assert np.array_equal(g.arrays["tooth_rows"][k], b.tooth_rows)
+    assert sum(p.group is not None for p in many) >= 24
+    # native planning loops on several threads: the same arrays
+    many_mt = planner.plan_many([c for c, _ in pairs], [e for _, e in pairs], threads=2, native_threads=3)
+    for a, b in zip(many, many_mt):
+        for f in ("pts", "chunk_circ", "tooth_box", "zkey", "min_index"):
+            assert np.array_equal(getattr(a, f), getattr(b, f)), f
+
+
+def test_sweep_batch_descriptors_point_at_plan_arrays(monkeypatch):
+    """SweepBatch packing (group slices for plan_many sets, per-set arrays
+    otherwise): every msurf_job pointer must address the bytes of its own
+    plan's array in the uploaded arena. Runs on CPU with the upload faked
+    into a host tensor."""
+    import torch
+
+    from paper_2603_28160_b200 import configs, engine
+    from paper_2603_28160_b200.dataset import ParameterRange, apply_sample, uniform_sample
+
+    monkeypatch.setattr(_native, "require_cuda", lambda: torch)
+
+    def upload(self, device, fill_structs=None):
+        dev = torch.zeros(max(self.size, 1), dtype=torch.uint8)
+        extra = fill_structs(dev.data_ptr()) if fill_structs else []
+        host = dev.numpy()
+        for off, a in self._parts:
+            if a is not None:
+                host[off:off + a.nbytes] = a.view(np.uint8).reshape(-1)
+        for off, b in extra:
+            b = b if isinstance(b, np.ndarray) else np.frombuffer(b, dtype=np.uint8)
+            host[off:off + b.nbytes] = b
+        return dev
+
+    monkeypatch.setattr(_native.Arena, "upload", upload)
+    base, ext, meta = configs.config3_base()
+    ranges = [ParameterRange(n, lo, hi) for n, lo, hi in meta["ranges"]]
+    samples = uniform_sample(ranges, 9, 5)
+    names = [r.name for r in ranges]
+    pairs = [apply_sample(base, ext, names, samples[i], 3600) for i in range(9)]
+    many = planner.plan_many([c for c, _ in pairs], [e for _, e in pairs])
+    assert all(p.group is not None for p in many)
+    single = planner.plan(*pairs[0])
+    order = many[:4] + [single] + many[6:] + [many[5]]  # runs broken by a per-set plan and a gap
+    b = engine.SweepBatch([(p, 0, p.grid.n) for p in order], device="cpu")
+    mem = b.buf.numpy()
+    base_ptr = b.base
+    jobs = np.concatenate(b.group_host_jobs)
+    seen = set()
+    for row, (i, lo, hi, s_lo, s_hi) in zip(jobs, [b.jobs[j] for gm in b.group_meta for j in gm[1]]):
+        p = order[i]
+        seen.add(i)
+        want = {"tooth_base": p.tooth_base, "tooth_rows": p.tooth_rows, "pts": p.pts, "tooth_box": p.tooth_box,
+                "chunk_circ": p.chunk_circ, "chunk_f32": planner.chunk_f32(p.chunk_circ, p.tooth_box),
+                "pass_x0": p.pass_x0, "min_index": p.min_index.astype(np.int32)}
+        for f, a in want.items():
+            off = int(row[f]) - base_ptr
+            a = np.ascontiguousarray(a)
+            assert np.array_equal(mem[off: off + a.nbytes], a.view(np.uint8).reshape(-1)), (i, f)
+        assert row["steps"] == p.steps and row["points"] == p.points and row["dt"] == p.dt
+        assert (row["step_lo"], row["step_hi"], row["j_lo"], row["j_hi"]) == (s_lo, s_hi, lo, hi)
+        assert int(row["counters"]) - base_ptr == b.ctr_off + i * _native.NUM_CTRS * 8
+    assert seen == set(range(len(order)))

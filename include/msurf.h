@@ -20,7 +20,7 @@
 extern "C" {
 #endif
 
-#define MSURF_ABI_VERSION 3
+#define MSURF_ABI_VERSION 4
 
 /* kinematics mode of a sweep launch (uniform across the jobs of one launch) */
 #define MSURF_MODE_REF 0      /* reference composite-matrix order, engine.py:257-296 */
@@ -243,6 +243,17 @@ int msurf_graymap_pixels(const double* h, int64_t ld, int64_t i_lo, int64_t j_lo
  * consecutive keys at a random base in 32 MiB (the sweep's access shape)
  * (ops/s). Synchronous; creates and destroys its own scratch. */
 int msurf_microbench(int32_t which, double* result);
+
+/* Small-result readback without the copy engines: msurf_host_alloc returns
+ * page-locked host memory mapped into the device address space (NULL on
+ * failure); msurf_readback enqueues on `stream` a kernel that stores `bytes`
+ * (a multiple of 8) from device memory `src` into such a buffer over PCIe.
+ * A D2H cudaMemcpy of a few bytes would queue behind any large D2H copy
+ * already in flight (the heights prefetch); these stores do not. The data is
+ * valid on the host once the stream has passed the kernel (event sync). */
+void* msurf_host_alloc(int64_t bytes);
+int msurf_host_free(void* p);
+int msurf_readback(const void* src, void* host_dst, int64_t bytes, void* stream);
 
 #ifdef __cplusplus
 }

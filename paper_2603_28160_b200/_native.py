@@ -18,7 +18,7 @@ from .errors import MillsurfError, NativeUnavailableError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MSURF_LIB") or os.path.join(_HERE, "libmsurf.so")
-ABI_VERSION = 3
+ABI_VERSION = 4
 NUM_CTRS = 5
 SWEEP_DIAG = 0x100  # MSURF_SWEEP_DIAG: count deposits/atomics per point
 RED_BLOCKS = 1024
@@ -94,6 +94,9 @@ EXPORTS = {
     "msurf_graymap_pixels": (ctypes.c_int, [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,
                                             c_void_p, c_void_p, c_void_p]),
     "msurf_microbench": (ctypes.c_int, [c_int32, ctypes.POINTER(c_double)]),
+    "msurf_host_alloc": (c_void_p, [c_int64]),
+    "msurf_host_free": (ctypes.c_int, [c_void_p]),
+    "msurf_readback": (ctypes.c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "msurf_plan_geometry": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "msurf_plan_geometry_many": (ctypes.c_int, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_int32]),
     "msurf_plan_finish_many": (ctypes.c_int, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
@@ -151,6 +154,36 @@ def stream_ptr(stream=None) -> int:
 
     s = stream if stream is not None else torch.cuda.current_stream()
     return int(s.cuda_stream)
+
+
+READBACK_MAX = 1 << 20  # bytes; larger results take a copy-engine D2H
+_mailboxes = {}
+_mailbox_lock = threading.Lock()
+
+
+def readback(t) -> np.ndarray:
+    """Host copy of a small device tensor (reduction results). The values are
+    stored into mapped page-locked memory by a kernel on the current stream
+    (msurf_readback), so the read does not queue behind a large D2H copy
+    already in flight on the copy engine (the heights prefetch)."""
+    import torch
+
+    nbytes = t.numel() * t.element_size()
+    if nbytes == 0 or nbytes > READBACK_MAX or nbytes % 8 or not t.is_contiguous() or t.device.type != "cuda":
+        return t.cpu().numpy()
+    dev = t.device.index if t.device.index is not None else torch.cuda.current_device()
+    with _mailbox_lock:
+        box = _mailboxes.get(dev)
+        if box is None:
+            ptr = lib().msurf_host_alloc(READBACK_MAX)
+            if not ptr:
+                raise NativeUnavailableError(f"msurf_host_alloc: {lib().msurf_last_error().decode()}")
+            box = _mailboxes[dev] = np.frombuffer((ctypes.c_char * READBACK_MAX).from_address(ptr), dtype=np.uint8)
+        check(lib().msurf_readback(t.data_ptr(), box.ctypes.data, nbytes, stream_ptr()))
+        ev = torch.cuda.Event()
+        ev.record()
+        ev.synchronize()
+        return box[:nbytes].view(np.dtype(str(t.dtype).replace("torch.", ""))).copy().reshape(tuple(t.shape))
 
 
 class Arena:

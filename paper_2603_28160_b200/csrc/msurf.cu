@@ -25,6 +25,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <string>
 
 #include "msurf.h"
@@ -1305,10 +1306,50 @@ cudaError_t launch_sweep(int64_t n_tiles, cudaStream_t st, const msurf_job* jobs
                                                                     dummy);
 }
 
+// small results -> host-mapped page-locked memory (stores over PCIe, no copy engine)
+__global__ void readback_kernel(const unsigned long long* __restrict__ src, volatile unsigned long long* dst,
+                                long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+  __threadfence_system();
+}
+
 }  // namespace
 
 // ================================================================ C ABI
 extern "C" {
+
+void* msurf_host_alloc(int64_t bytes) {
+  void* p = nullptr;
+  if (bytes <= 0) return nullptr;
+  if (cudaHostAlloc(&p, (size_t)bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    set_err("msurf_host_alloc: cudaHostAlloc failed");
+    return nullptr;
+  }
+  return p;
+}
+
+int msurf_host_free(void* p) {
+  if (p && cudaFreeHost(p) != cudaSuccess) return set_err("msurf_host_free: cudaFreeHost failed");
+  return 0;
+}
+
+int msurf_readback(const void* src, void* host_dst, int64_t bytes, void* stream) {
+  if (bytes < 0 || (bytes % 8) || (bytes > 0 && (!src || !host_dst)))
+    return set_err("msurf_readback: bad arguments");
+  if (bytes == 0) return 0;
+  void* dptr = nullptr;
+  if (cudaHostGetDevicePointer(&dptr, host_dst, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return set_err("msurf_readback: destination is not mapped page-locked memory");
+  }
+  const long long n = bytes / 8;
+  const int blocks = (int)std::min<long long>((n + kThreads - 1) / kThreads, 148);
+  readback_kernel<<<blocks, kThreads, 0, (cudaStream_t)stream>>>(
+      static_cast<const unsigned long long*>(src), static_cast<unsigned long long*>(dptr), n);
+  return check_launch("readback_kernel");
+}
 
 int msurf_abi_version(void) { return MSURF_ABI_VERSION; }
 const char* msurf_last_error(void) { return g_err.c_str(); }

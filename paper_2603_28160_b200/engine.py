@@ -415,7 +415,7 @@ class SweepBatch:
     def counters(self):
         """(counters [n,4], machined [n]) on the host (synchronises)."""
         u64 = self.buf[self.ctr_off: self.ctr_off + self.n * (_native.NUM_CTRS + 1) * 8].view(self.torch.int64)
-        a = u64.cpu().numpy()
+        a = _native.readback(u64)
         return a[: self.n * _native.NUM_CTRS].reshape(self.n, _native.NUM_CTRS), a[self.n * _native.NUM_CTRS:]
 
     def trajectories(self):

@@ -104,7 +104,7 @@ class SurfacePipeline:
 
     def collect(self):
         """One D2H: per surface (ArealMetrics | DomainError, [ProfileRoughness])."""
-        a = self.out.cpu().numpy()
+        a = _native.readback(self.out)
         n = self.n
         st1 = a[: n * 6].reshape(n, 6)
         st2 = a[n * 6: n * 10].reshape(n, 4)

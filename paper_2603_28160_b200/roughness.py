@@ -156,7 +156,7 @@ def areal_moments_device(h_dev, ld, n_surf, surf_stride, roi_box, sentinels_dev,
     out = sc[n_surf * _native.WORK_DOUBLES:]
     _areal_enqueue(lib, h_dev, ld, n_surf, surf_stride, roi_box, sentinels_dev, exclude, sc.data_ptr(), out,
                    _native.stream_ptr(), allreduce)
-    return _split_moments(out[: n_surf * 10].cpu().numpy(), n_surf)
+    return _split_moments(_native.readback(out[: n_surf * 10]), n_surf)
 
 
 def _sentinel_tensor(torch, values, device):
@@ -211,7 +211,7 @@ def _areal_plane(field: HeightField, roi, uncut: str) -> ArealMetrics:
     sp = _native.stream_ptr()
     _native.check(lib.msurf_areal_plane_pass1(h.data_ptr(), ld, 0, 1, i_lo, j_lo, rows, cols, sent.data_ptr(),
                                               ex, work, out.data_ptr(), sp))
-    s1 = out[:10].cpu().numpy()
+    s1 = _native.readback(out[:10])
     if uncut == "raise" and s1[9] > 0:
         raise DomainError("roughness over unmachined stock is undefined: roi contains uncut cells")
     n = s1[0]
@@ -223,7 +223,7 @@ def _areal_plane(field: HeightField, roi, uncut: str) -> ArealMetrics:
     cdev = torch.tensor(coef, dtype=torch.float64, device=h.device)
     _native.check(lib.msurf_areal_plane_pass2(h.data_ptr(), ld, 0, 1, i_lo, j_lo, rows, cols, sent.data_ptr(),
                                               ex, cdev.data_ptr(), work, out.data_ptr(), sp))
-    s2 = out[:6].cpu().numpy()
+    s2 = _native.readback(out[:6])
     sa = float(s2[0] / n)
     sq = float(np.sqrt(s2[1] / n))
     spk, svl = float(s2[4]), float(-s2[5])
@@ -306,7 +306,7 @@ def areal_metrics_batch(fields, roi=None, uncut: str = "raise"):
                            sc.data_ptr(), outs[pos * 10: (pos + n) * 10], sp)
             slots.append((r, pos, n))
             pos += n
-        both = outs[: n_out * 10].cpu().numpy()  # one D2H for every run on this device
+        both = _native.readback(outs[: n_out * 10])  # one read-back for every run on this device
         for r, p0, n in slots:
             res[r] = _split_moments(both[p0 * 10: (p0 + n) * 10], n)
     out = []
@@ -408,7 +408,7 @@ def profile_roughness(field: HeightField, indices=None, direction: str = "feed",
     h = field.device_heights()
     sent = _field_sentinel(torch, field, h.device)
     rows = _profiles_device(h, 1, 0, starts, length, step, sent, uncut == "exclude")
-    rows = rows.cpu().numpy().reshape(len(indices), 8)
+    rows = _native.readback(rows).reshape(len(indices), 8)
     return [_finish_profile(r, idx, uncut) for r, idx in zip(rows, indices)]
 
 
@@ -419,5 +419,5 @@ def line_roughness(profile: LineProfile) -> float:
     torch = _native.require_cuda()
     h = torch.from_numpy(np.ascontiguousarray(profile.heights_mm, dtype=np.float64)).cuda()
     sent = _sentinel_tensor(torch, [np.inf], h.device)
-    row = _profiles_device(h, 1, 0, [0], h.numel(), 1, sent, False).cpu().numpy()
+    row = _native.readback(_profiles_device(h, 1, 0, [0], h.numel(), 1, sent, False))
     return float(row[5] / row[1])

@@ -158,7 +158,7 @@ def areal_metrics_strip(res: StripResult, roi=None, uncut: str = "raise", group=
                                             sent.data_ptr(), ex, st1.data_ptr(), work.data_ptr(),
                                             st2.data_ptr(), sp))
     combine(st2, (0, 1, 2, 3), (), (), group)
-    return _finish_areal(st1[0].cpu().numpy(), st2[0].cpu().numpy(), uncut)
+    return _finish_areal(_native.readback(st1[0]), _native.readback(st2[0]), uncut)
 
 
 def profile_roughness_strip(res: StripResult, every: int = 64, uncut: str = "raise", group=None):
@@ -185,7 +185,7 @@ def profile_roughness_strip(res: StripResult, every: int = 64, uncut: str = "rai
     sabs = out.view(-1, 8)[:, 5:6].contiguous()
     combine(sabs, (0,), (), (), group)
     first[:, 5:6] = sabs
-    rows = first.cpu().numpy()
+    rows = _native.readback(first)
     return [_finish_profile(r, i, uncut) for r, i in zip(rows, idx)]
 
 
@@ -278,15 +278,15 @@ class StripPipeline:
             events[3].record(st)
 
     def collect(self):
-        st1 = self.st1[0].cpu().numpy()
-        st2 = self.st2[0].cpu().numpy()
+        st1 = _native.readback(self.st1[0])
+        st2 = _native.readback(self.st2[0])
         try:
             am = _finish_areal(st1, st2, self.uncut)
         except DomainError as exc:
             am = exc
         prs = []
         if self.P:
-            rows = self.first[: self.P].cpu().numpy()
+            rows = _native.readback(self.first[: self.P])
             for r, i in zip(rows, self.prof_idx):
                 try:
                     prs.append(_finish_profile(r, i, self.uncut))

@@ -225,3 +225,30 @@ def test_reduction_scratch_bound_at_max_blocks():
     torch.cuda.synchronize()
     assert bool(torch.all(work[_native.WORK_DOUBLES:] == 12345.0))
     assert int(out[3].item()) == rows * cols
+
+
+@pytest.mark.gpu
+def test_readback_mapped_matches_copy():
+    """Small results come back through mapped page-locked memory (msurf_readback),
+    also while a large D2H copy is in flight on a side stream."""
+    import torch
+
+    from paper_2603_28160_b200 import _native
+
+    dev = torch.device("cuda", 0)
+    big = torch.randn(1 << 24, dtype=torch.float64, device=dev)
+    host = torch.empty(big.shape, dtype=torch.float64, pin_memory=True)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        host.copy_(big, non_blocking=True)
+    for n, dt in ((1, torch.float64), (10, torch.float64), (2560, torch.float64), (7, torch.int64),
+                  (1 << 17, torch.float64), (3, torch.float32)):
+        t = (torch.arange(n, device=dev) * 3 - 5).to(dt) / (1 if dt != torch.float64 else 7)
+        got = _native.readback(t)
+        assert got.dtype == t.cpu().numpy().dtype and got.shape == tuple(t.shape)
+        assert np.array_equal(got, t.cpu().numpy())
+    m = torch.arange(12, dtype=torch.float64, device=dev).reshape(3, 4)
+    assert np.array_equal(_native.readback(m), m.cpu().numpy())
+    side.synchronize()
+    assert torch.equal(host[:100].to(dev), big[:100])

@@ -26,7 +26,7 @@ CASES = golden_io.case_names()
 def test_library_exports_every_declared_symbol():
     lib = _native.load_library()
     header = open(os.path.join(ROOT, "include", "msurf.h")).read()
-    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(msurf_\w+)\s*\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:int|const char\*|void\*)\s+(msurf_\w+)\s*\(", header, re.M))
     assert declared, "no declarations parsed"
     assert declared == set(_native.EXPORTS), declared ^ set(_native.EXPORTS)
     for name in declared:

@@ -98,10 +98,13 @@ int msurf_fill_keys(uint64_t* keys, int64_t count, int32_t n_surf, const double*
  * prefix sums of tiles per job,
  * tiles(job) = passes*teeth*ceil((step_hi-step_lo)/tile_steps).
  * tile_steps must be msurf_tile_steps(). Deposits are atomicMin on keys, so
- * the result is independent of scheduling (engine.py:316-317 determinism). */
+ * the result is independent of scheduling (engine.py:316-317 determinism).
+ * `scratch` is DEVICE memory of at least 8 * (n_tiles + 1) bytes: the sweep
+ * first pre-culls the tiles (a tile whose tooth box cannot reach its job's
+ * window does no work) into a list there, then persistent CTAs walk it. */
 int msurf_tile_steps(void);
 int msurf_sweep(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile_prefix,
-                int64_t n_tiles, int32_t mode, int32_t max_points, void* stream);
+                int64_t n_tiles, int32_t mode, int32_t max_points, void* scratch, void* stream);
 
 /* The same sweep for ONE job given as a HOST pointer: the descriptor is
  * passed by value as a kernel parameter, so the kernel reads its fields as

@@ -70,7 +70,7 @@ EXPORTS = {
     "msurf_sizeof_job": (ctypes.c_int, []),
     "msurf_tile_steps": (ctypes.c_int, []),
     "msurf_fill_keys": (ctypes.c_int, [c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
-    "msurf_sweep": (ctypes.c_int, [c_void_p, c_int32, c_void_p, c_int64, c_int32, c_int32, c_void_p]),
+    "msurf_sweep": (ctypes.c_int, [c_void_p, c_int32, c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
     "msurf_sweep_job": (ctypes.c_int, [c_void_p, c_int32, c_int32, c_void_p]),
     "msurf_decode_strips": (ctypes.c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p,
                                            c_void_p, c_void_p]),

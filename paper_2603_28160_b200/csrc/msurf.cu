@@ -115,12 +115,20 @@ __device__ __noinline__ int cell_index_exact(double w, double lo, double dd) {
 // Fire-and-forget global atomic min (RED.E.MIN.64): the explicit .global
 // form avoids the generic-address shared-memory fallback atomicMin compiles to.
 __device__ __forceinline__ void red_min_u64(unsigned long long* p, unsigned long long v) {
+#ifdef MSURF_NO_RED  // timing experiment only: the RED replaced by a never-taken store
+  if (v == 1ull) *p = v;
+#else
   asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+#endif
 }
 
 
 // predicated form: no branch around the RED
 __device__ __forceinline__ void red_min_u64_if(unsigned long long* p, unsigned long long v, bool pred) {
+#ifdef MSURF_NO_RED
+  if (pred && v == 1ull) *p = v;
+  return;
+#endif
   asm volatile(
       "{ .reg .pred q; setp.ne.u32 q, %2, 0; @q red.relaxed.gpu.global.min.u64 [%0], %1; }" ::"l"(p),
       "l"(v), "r"((unsigned)pred)
@@ -253,10 +261,54 @@ __device__ __forceinline__ void next_unit(int& g, int& q, int nchunk) {
   }
 }
 
+// tile pre-cull: the tooth box at the tile's mid angle and mid feed position,
+// widened by the largest displacement any of its points makes within the
+// tile (rotation: arc <= Rt * |dtheta|; feed: |v_f| dt/2 per step). A tile
+// the box cannot reach is skipped before any per-step work — for windowed
+// strips and narrow grids most tiles are (config 3: ~80 %). Conservative like
+// the per-step pre-cull (same fp32 margins). Jobs with host trig tables or a
+// trajectory record keep every tile.
+template <int MODE, int TILE>
+__device__ __forceinline__ bool tile_may_hit(const msurf_job& J, int pass, int tooth, int st) {
+  if (J.trig_table || (J.traj && pass == 0)) return true;
+  const int nchunk = (J.points + 31) >> 5;
+  const float rt_f = __ldg(reinterpret_cast<const float*>(J.chunk_f32) + (long long)tooth * nchunk * 8 + 5);
+  float box_f[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) box_f[k] = (float)J.tooth_box[tooth * 6 + k];
+  const double dd = J.spacing;
+  const long long s0 = J.step_lo + (long long)st * TILE;
+  const long long s1 = min(s0 + (long long)TILE, (long long)J.step_hi) - 1;
+  const double half_t = 0.5 * (double)(s1 - s0) * J.dt;
+  const double tm = J.t_start + (0.5 * (double)(s0 + s1)) * J.dt;
+  const double th = J.tooth_base[tooth] - J.omega * tm;
+  const double wxc = J.x_min + 0.5 * (double)J.m * dd, wxh = 0.5 * (double)J.m * dd + 1.5 * dd;
+  const double wyc = J.y_min + 0.5 * (double)(J.j_lo + J.j_hi) * dd;
+  const double wyh = 0.5 * (double)(J.j_hi - J.j_lo) * dd + 1.5 * dd;
+  const double kd = rint(th * MSURF_TWO_OVER_PI);
+  const double r = __fma_rn(-kd, MSURF_PIO2_2, __fma_rn(-kd, MSURF_PIO2_1, th));
+  float sf, cf;
+  __sincosf((float)r, &sf, &cf);
+  const int quad = ((int)(long long)kd) & 3;
+  float ca = cf, sa = sf;
+  if (quad == 1) { ca = -sf; sa = cf; }
+  else if (quad == 2) { ca = -cf; sa = -sf; }
+  else if (quad == 3) { ca = sf; sa = -cf; }
+  const float oxf = (float)(J.pass_x0[pass] - wxc);
+  const float oyf = (float)(J.y0 + J.feed_speed * tm - wyc);
+  const float rot = (float)(fabs(J.omega) * half_t * (double)rt_f);
+  const float feed = (float)(fabs(J.feed_speed) * half_t);
+  const float mg = (float)(1e-4 + fabs(J.vib_amp)) + 4e-6f * (rt_f + fabsf(oxf) + fabsf(oyf)) + 1e-6f +
+                   1.001f * rot + 1e-6f;
+  return tool_box_hits_f32<MODE>(box_f, ca, sa, oxf, oyf, (float)wxh + mg, (float)wyh + mg + 1.001f * feed,
+                                 (float)J.tilt_c, (float)J.tilt_s);
+}
+
 template <int MODE, bool DIAG, bool ONE, int TILE, int NTHR>
 __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
     sweep_kernel(const msurf_job* __restrict__ jobs, int n_jobs,
-                 const int64_t* __restrict__ prefix, int mask_words, const __grid_constant__ msurf_job jp) {
+                 const int64_t* __restrict__ prefix, int mask_words, const __grid_constant__ msurf_job jp,
+                 const unsigned long long* __restrict__ list, unsigned* __restrict__ list_count) {
   constexpr int kTileSteps = TILE;               // time steps per CTA
   constexpr int kSweepThreads = NTHR;            // threads per CTA
   constexpr int kSubSteps = TILE / NTHR;         // phase-1 steps per thread
@@ -279,33 +331,36 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
   __shared__ int warp_cnt[kSweepWarps];
   __shared__ unsigned warp_eval[kSweepWarps];
   __shared__ unsigned warp_eng[kSweepWarps];
-  __shared__ int s_job;
   __shared__ double4 ptstage[kSweepWarps][32];  // per-warp copy of the current chunk's point records
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const long long tile = blockIdx.x;
-
-  long long local = tile;
-  if (!ONE) {
-    if (tid == 0) {
-      int lo = 0, hi = n_jobs - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (prefix[mid] <= tile) lo = mid; else hi = mid - 1;
-      }
-      s_job = lo;
-    }
-    __syncthreads();
+  // ONE: one CTA per tile of the by-value job (blockIdx.x = tile). Else
+  // persistent CTAs walk the pre-culled tile list (tile_list_kernel): entry =
+  // job << 32 | tile index inside the job, taken from a global cursor in list
+  // order, so the tiles in flight stay a narrow window of the list (their
+  // Z-maps share L2) and uneven tiles balance themselves
+  __shared__ unsigned s_i;
+  const unsigned list_n = ONE ? 0u : list_count[0];
+  long long local = blockIdx.x;
+  for (;;) {
+  if constexpr (!ONE) {
+    if constexpr (kSweepWarps == 1) __syncwarp(); else __syncthreads();  // previous tile done with Js / s_i
+    if (tid == 0) s_i = atomicAdd(list_count + 1, 1u);
+    if constexpr (kSweepWarps == 1) __syncwarp(); else __syncthreads();
+    const unsigned i = s_i;
+    if (i >= list_n) return;
+    const unsigned long long e = list[i];
     {
-      const unsigned long long* src = reinterpret_cast<const unsigned long long*>(jobs + s_job);
+      const unsigned long long* src = reinterpret_cast<const unsigned long long*>(jobs + (e >> 32));
       unsigned long long* dst = reinterpret_cast<unsigned long long*>(&Js);
       for (int w = tid; w < (int)(sizeof(msurf_job) / 8); w += kSweepThreads) dst[w] = src[w];
     }
-    __syncthreads();
-    local = tile - prefix[s_job];
+    if constexpr (kSweepWarps == 1) __syncwarp(); else __syncthreads();
+    local = (long long)(e & 0xffffffffull);
   }
+  {
   // tile -> (pass, tooth, step tile) in 32-bit arithmetic (grids are < 2^31 tiles)
   const unsigned nst = (unsigned)((J.step_hi - J.step_lo + kTileSteps - 1) / kTileSteps);
   const unsigned loc = (unsigned)local;
@@ -325,6 +380,7 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
   float box_f[6];
 #pragma unroll
   for (int k = 0; k < 6; ++k) box_f[k] = (float)J.tooth_box[tooth * 6 + k];
+  if (ONE && !tile_may_hit<MODE, TILE>(J, pass, tooth, st)) return;  // uniform across the CTA
 
   // ---------------- phase 1: one thread per time step (kSubSteps rounds of
   // kSweepThreads steps), live steps appended in time order
@@ -494,7 +550,7 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
   if (n_live == 0) {
     if (tid == 0 && J.counters && n_eng_cta)
       atomicAdd(J.counters + MSURF_CTR_ENGAGED_ROWS, (unsigned long long)n_eng_cta);
-    return;
+    if constexpr (ONE) return; else goto tile_done;
   }
 
   // ---------------- phase 2: lane = live step(s), warp walks the 32 points of a chunk
@@ -728,6 +784,45 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
       atomicAdd(J.counters + MSURF_CTR_ENGAGED_ROWS, (unsigned long long)n_eng_cta);
     }
   }
+  }
+  tile_done:
+  if constexpr (ONE) return;
+  }
+}
+
+// tile list of a job array: one thread per tile (job found by binary search
+// in the tile prefix), live tiles appended with one atomic per warp; the
+// order is not deterministic and need not be (min and the counters commute)
+template <int MODE, int TILE>
+__global__ void __launch_bounds__(256)
+    tile_list_kernel(const msurf_job* __restrict__ jobs, int n_jobs, const int64_t* __restrict__ prefix,
+                     long long n_tiles, unsigned long long* __restrict__ list, unsigned* __restrict__ count) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  bool live = false;
+  unsigned long long entry = 0;
+  if (t < n_tiles) {
+    int lo = 0, hi = n_jobs - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (prefix[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    const msurf_job& J = jobs[lo];
+    const unsigned local = (unsigned)(t - prefix[lo]);
+    const unsigned nst = (unsigned)((J.step_hi - J.step_lo + TILE - 1) / TILE);
+    const unsigned rem = local / nst;
+    const int st = (int)(local - rem * nst);
+    const int tooth = (int)(rem % (unsigned)J.teeth);
+    const int pass = (int)(rem / (unsigned)J.teeth);
+    live = tile_may_hit<MODE, TILE>(J, pass, tooth, st);
+    entry = ((unsigned long long)lo << 32) | local;
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, live);
+  if (!bal) return;
+  const int lane = threadIdx.x & 31;
+  unsigned base = 0;
+  if (lane == __ffs(bal) - 1) base = atomicAdd(count, (unsigned)__popc(bal));
+  base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
+  if (live) list[base + __popc(bal & ((1u << lane) - 1u))] = entry;
 }
 
 // --------------------------------------------------------------- fill/decode
@@ -1272,16 +1367,29 @@ inline size_t sweep_smem(int tile, int mask_words) {
 
 template <int MODE, bool DIAG, bool ONE, int TILE, int NTHR>
 cudaError_t launch_shape(int64_t n_tiles, cudaStream_t st, const msurf_job* jobs, int n_jobs, const int64_t* prefix,
-                         int mask_words, const msurf_job& job) {
+                         int mask_words, const msurf_job& job, unsigned long long* list, unsigned* count) {
+  auto kern = sweep_kernel<MODE, DIAG, ONE, TILE, NTHR>;
   const size_t smem = sweep_smem(TILE, mask_words);
   cudaError_t e = cudaSuccess;
-  if (smem > 48 * 1024)
-    e = cudaFuncSetAttribute(sweep_kernel<MODE, DIAG, ONE, TILE, NTHR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-  if (e == cudaSuccess)
-    sweep_kernel<MODE, DIAG, ONE, TILE, NTHR><<<(unsigned)n_tiles, NTHR, smem, st>>>(jobs, n_jobs, prefix, mask_words,
-                                                                                    job);
-  return e;
+  if (smem > 48 * 1024) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if constexpr (ONE) {
+    kern<<<(unsigned)n_tiles, NTHR, smem, st>>>(nullptr, 1, nullptr, mask_words, job, nullptr, nullptr);
+  } else {
+    // pre-cull the tiles into the list, then persistent CTAs (a few waves of
+    // the resident limit) walk it
+    e = cudaMemsetAsync(count, 0, 2 * sizeof(unsigned), st);  // list length, work cursor
+    if (e != cudaSuccess) return e;
+    tile_list_kernel<MODE, TILE><<<(unsigned)((n_tiles + 255) / 256), 256, 0, st>>>(jobs, n_jobs, prefix, n_tiles,
+                                                                                  list, count);
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTHR, smem);
+    const int64_t grid = std::min<int64_t>(n_tiles, (int64_t)sms * std::max(per_sm, 1));
+    kern<<<(unsigned)grid, NTHR, smem, st>>>(jobs, n_jobs, prefix, mask_words, job, list, count);
+  }
+  return cudaSuccess;
 }
 
 // tiles of one job for a tile size: passes * teeth * ceil(window / tile)
@@ -1291,19 +1399,20 @@ inline int64_t job_tiles(const msurf_job& j, int tile) {
 
 template <int MODE, bool DIAG>
 cudaError_t launch_sweep(int64_t n_tiles, cudaStream_t st, const msurf_job* jobs, int n_jobs,
-                         const int64_t* prefix, int mask_words, const msurf_job* one) {
+                         const int64_t* prefix, int mask_words, const msurf_job* one, unsigned long long* list,
+                         unsigned* count) {
   if (one) {
     if constexpr (MODE == MSURF_MODE_EXT_TILT)
       return launch_shape<MODE, DIAG, true, kTiltTile, kTiltThreads>(job_tiles(*one, kTiltTile), st, nullptr, 1,
-                                                                    nullptr, mask_words, *one);
+                                                                    nullptr, mask_words, *one, nullptr, nullptr);
     else
       return launch_shape<MODE, DIAG, true, kWideTile, kWideThreads>(job_tiles(*one, kWideTile), st, nullptr, 1,
-                                                                    nullptr, mask_words, *one);
+                                                                    nullptr, mask_words, *one, nullptr, nullptr);
   }
   msurf_job dummy;
   memset(&dummy, 0, sizeof(dummy));
   return launch_shape<MODE, DIAG, false, kBatchTile, kBatchThreads>(n_tiles, st, jobs, n_jobs, prefix, mask_words,
-                                                                    dummy);
+                                                                    dummy, list, count);
 }
 
 // small results -> host-mapped page-locked memory (stores over PCIe, no copy engine)
@@ -1371,7 +1480,7 @@ int msurf_fill_keys(uint64_t* keys, int64_t count, int32_t n_surf, const double*
 }
 
 static int sweep_impl(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile_prefix, int64_t n_tiles,
-                      int32_t mode, int32_t max_points, void* stream, const msurf_job* one) {
+                      int32_t mode, int32_t max_points, void* stream, const msurf_job* one, void* scratch) {
   if (!one && n_tiles == 0) return 0;
   if (n_tiles > 0x7fffffffLL) return set_err("msurf_sweep: too many tiles");
   if (one && (job_tiles(*one, 64) == 0)) return 0;
@@ -1381,9 +1490,12 @@ static int sweep_impl(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
   const bool diag = (mode & MSURF_SWEEP_DIAG) != 0;
-#define MSURF_LAUNCH(M)                                                                      \
-  e = diag ? launch_sweep<M, true>(n_tiles, st, jobs, n_jobs, tile_prefix, mask_words, one)  \
-           : launch_sweep<M, false>(n_tiles, st, jobs, n_jobs, tile_prefix, mask_words, one)
+  // scratch: [0, 8) tile count and work cursor, then the tile list (8 bytes per tile)
+  unsigned* count = static_cast<unsigned*>(scratch);
+  unsigned long long* list = scratch ? static_cast<unsigned long long*>(scratch) + 1 : nullptr;
+#define MSURF_LAUNCH(M)                                                                                   \
+  e = diag ? launch_sweep<M, true>(n_tiles, st, jobs, n_jobs, tile_prefix, mask_words, one, list, count)  \
+           : launch_sweep<M, false>(n_tiles, st, jobs, n_jobs, tile_prefix, mask_words, one, list, count)
   switch (mode & ~MSURF_SWEEP_DIAG) {
     case MSURF_MODE_REF: MSURF_LAUNCH(MSURF_MODE_REF); break;
     case MSURF_MODE_EXT: MSURF_LAUNCH(MSURF_MODE_EXT); break;
@@ -1392,20 +1504,20 @@ static int sweep_impl(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile
       return set_err("msurf_sweep: unknown mode");
   }
 #undef MSURF_LAUNCH
-  if (e != cudaSuccess) return set_err(std::string("msurf_sweep: smem attribute: ") + cudaGetErrorString(e));
+  if (e != cudaSuccess) return set_err(std::string("msurf_sweep: launch setup: ") + cudaGetErrorString(e));
   return check_launch("sweep_kernel");
 }
 
 int msurf_sweep(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile_prefix,
-                int64_t n_tiles, int32_t mode, int32_t max_points, void* stream) {
-  if (n_jobs < 1 || !jobs || !tile_prefix || n_tiles < 0 || max_points < 1)
+                int64_t n_tiles, int32_t mode, int32_t max_points, void* scratch, void* stream) {
+  if (n_jobs < 1 || !jobs || !tile_prefix || n_tiles < 0 || max_points < 1 || (n_tiles > 0 && !scratch))
     return set_err("msurf_sweep: bad arguments");
-  return sweep_impl(jobs, n_jobs, tile_prefix, n_tiles, mode, max_points, stream, nullptr);
+  return sweep_impl(jobs, n_jobs, tile_prefix, n_tiles, mode, max_points, stream, nullptr, scratch);
 }
 
 int msurf_sweep_job(const msurf_job* job, int32_t mode, int32_t max_points, void* stream) {
   if (!job || max_points < 1) return set_err("msurf_sweep_job: bad arguments");
-  return sweep_impl(nullptr, 1, nullptr, 0, mode, max_points, stream, job);
+  return sweep_impl(nullptr, 1, nullptr, 0, mode, max_points, stream, job, nullptr);
 }
 
 int msurf_decode(uint64_t* keys, int64_t count, int32_t n_surf, const double* sentinel,

@@ -331,6 +331,10 @@ class SweepBatch:
         # one fill / decode launch for the whole batch (no strip-layout surface)
         self.batched_fill = self.same_shape and all(s.n_strips == 1 for s in surfs)
         self.group_per_job = [_per_job_launches(tl) for tl in self.group_tiles]
+        # msurf_sweep scratch (tile count + pre-culled tile list), shared by the
+        # batched launch groups (they run in stream order)
+        need = max((gm[4] for gm, pj in zip(self.group_meta, self.group_per_job) if not pj), default=0)
+        self.sweep_scratch = torch.empty(need + 1, dtype=torch.int64, device=self.dev) if need else None
         sweeps = sum((sum(1 for t in tl if t) if pj else 1) for pj, tl in zip(self.group_per_job, self.group_tiles))
         self.launches_per_run = 2 * (1 if self.batched_fill else n) + sweeps
 
@@ -364,7 +368,7 @@ class SweepBatch:
                         _native.check(lib.msurf_sweep_job(ptr + k * sz, mode | flag, max_pts, sp))
                 continue
             _native.check(lib.msurf_sweep(base + job_off, len(idx), base + pre_off, n_tiles, mode | flag,
-                                          max_pts, sp))
+                                          max_pts, self.sweep_scratch.data_ptr(), sp))
 
     def launch_decode(self, sp: int) -> None:
         """Keys -> fp64 heights in place, machined-cell counts."""

@@ -38,7 +38,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_error_path_without_gpu_reports_message():
     lib = _native.load_library()
-    assert lib.msurf_sweep(None, 0, None, 0, 0, 1, None) != 0
+    assert lib.msurf_sweep(None, 0, None, 0, 0, 1, None, None) != 0
     assert b"bad arguments" in lib.msurf_last_error()
 
 

@@ -25,14 +25,18 @@ keep = []
 for _ in range(4):
     keep.append(step(32)[1]); keep = keep[-2:]
 rows = []
-grid = [(w, f, ft, c, nt) for w in (1, 2, 3) for f, ft in ((0, 1), (8, 1), (8, 4)) for c in (32, 64) for nt in (1, 2, 4)]
-for workers, first, fthr, chunk, nthr in grid:
+grid = [(w, f, ft, c, nt) for w in (1, 2) for f, ft in ((0, 1), (8, 1), (8, 4)) for c in (32, 48)
+        for nt in (1,)]
+import os
+ivs = [float(x) for x in os.environ.get("IVS", "0.005,0.0005,0.0002,0.00005").split(",")]
+for workers, first, fthr, chunk, nthr, iv in [g + (iv,) for iv in ivs for g in grid]:
+    engine.PIPELINE_SWITCH_INTERVAL = iv
     engine.PIPELINE_PLAN_THREADS, engine.PIPELINE_FIRST_CHUNK, engine.PIPELINE_FIRST_THREADS = workers, first, fthr
     engine.PIPELINE_NATIVE_THREADS = nthr
     ts = []
     for _ in range(6):
         t, o = step(chunk); keep.append(o); keep = keep[-2:]; ts.append(t)
-    rows.append((float(np.median(ts[1:])), workers, first, fthr, chunk, nthr))
-    print(f"workers {workers} first {first} first_threads {fthr} chunk {chunk} native {nthr}: median {rows[-1][0]:.2f} ms "
+    rows.append((float(np.median(ts[1:])), workers, first, fthr, chunk, nthr, iv))
+    print(f"iv {iv} workers {workers} first {first} first_threads {fthr} chunk {chunk} native {nthr}: median {rows[-1][0]:.2f} ms "
           f"(min {min(ts[1:]):.2f})", flush=True)
 print("best", sorted(rows)[:3])

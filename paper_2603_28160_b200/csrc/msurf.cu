@@ -165,10 +165,11 @@ __device__ __forceinline__ bool tool_box_hits_f32(const float* b, float c, float
   return (x_hi >= -hx) & (x_lo <= hx) & (v_hi + oy >= -hy) & (v_lo + oy <= hy);
 }
 
-// one edge point under one lane's step transform: workpiece x', y' in the
-// reference's exact op order, the magic-number high words of both cell
-// coordinates, the near-boundary flag, the deposit key and (tilt) a float32
-// copy of z' for the neighbour comparisons
+// one edge point under one lane's step transform: the magic-number high
+// words of both cell coordinates, the near-boundary flag, the deposit key and
+// (tilt) the key's high word for the neighbour comparisons. REF keeps the
+// workpiece x', y' in the reference's exact op order; the extended modes fold
+// the offsets into the cell coordinate (see eval_point).
 struct PointEval {
   double xw, yw;
   int hi_x, hi_y;
@@ -176,11 +177,11 @@ struct PointEval {
   uint64_t key;
   unsigned zh;  // high word of the order-preserving key (tilt neighbour compares)
 
-  // cell coordinates of (xw, yw): fma + magic-number add, floor and fraction
+  // cell coordinates from mx = fma(a, inv, c) + 1.5*2^20: floor and fraction
   // straight from the bits (see kMagicHi)
-  __device__ __forceinline__ PointEval finish(double inv, double cx0, double cy0) {
-    const double mx = __dadd_rn(__fma_rn(xw, inv, cx0), 0x1.8p20);
-    const double my = __dadd_rn(__fma_rn(yw, inv, cy0), 0x1.8p20);
+  __device__ __forceinline__ PointEval cells(double ax, double cx, double ay, double cy, double inv) {
+    const double mx = __dadd_rn(__fma_rn(ax, inv, cx), 0x1.8p20);
+    const double my = __dadd_rn(__fma_rn(ay, inv, cy), 0x1.8p20);
     hi_x = __double2hiint(mx);
     hi_y = __double2hiint(my);
     near = (((unsigned)__double2loint(mx) + 8u) < 16u) | (((unsigned)__double2loint(my) + 8u) < 16u);
@@ -191,6 +192,19 @@ struct PointEval {
   }
 };
 
+// Row transform of one live step as the phase-2 lanes hold it: REF the eight
+// composite coefficients; EXT / tilt (c, s, cxp, cyp) with the step's x and y
+// offsets folded into the cell-coordinate constants, cxp = fma(xoff, inv, cx0)
+// and cyp = fma(ty, inv, cy0) (the offsets themselves stay in shared memory
+// for the exact path).
+//
+// Fast cell location of the extended modes: mx = fma(u, inv, cxp) + 1.5*2^20
+// with u = fma(c, x, s*y) is (u + xoff - x_min)/dd + 0.5 up to a few 1e-13
+// cells (fma instead of the reference's rounded products, the folded
+// constant's rounding), far inside the +-8*2^-32 cell window that flags a
+// point as near a boundary; flagged points are re-located with the exact
+// reference arithmetic (exact_xy + cell_index_exact). The key is exact: EXT's
+// is precomputed, tilt's z' uses the model's own fused v.
 template <int MODE>
 __device__ __forceinline__ PointEval eval_point(const double4 pt, const double* r, double inv, double cx0,
                                                 double cy0, double tilt_c, double tilt_s) {
@@ -203,29 +217,40 @@ __device__ __forceinline__ PointEval eval_point(const double4 pt, const double* 
     e.yw = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r[4], pt.x), __dmul_rn(r[5], pt.y)), __dmul_rn(r[6], pt.z)),
                      r[7]);
     e.key = (uint64_t)__double_as_longlong(pt.w);
-  } else {
-    if (MODE == MSURF_MODE_EXT_TILT) {
-      // lead-tilt model, fused: u = fma(c, x, s*y),
-      // v = fma(c, y, -(s*x)), x' = u + xoff, y' = fma(cos(tau), v, -sin(tau) z) + ty,
-      // z' = fma(sin(tau), v, cos(tau) z + zoff); pt = (x, y, sin(tau) z, cos(tau) z + zoff)
-      const double uu = __fma_rn(r[0], pt.x, __dmul_rn(r[1], pt.y));
-      const double vv = __fma_rn(r[0], pt.y, -__dmul_rn(r[1], pt.x));
-      e.xw = __dadd_rn(uu, r[2]);
-      e.yw = __dadd_rn(__fma_rn(tilt_c, vv, -pt.z), r[3]);
-      const double zz = __fma_rn(tilt_s, vv, pt.w);
-      e.key = enc_key_raw(zz);  // pt.w is never -0 (host-canonical), so neither is zz
-      e.zh = (unsigned)(e.key >> 32);
-      return e.finish(inv, cx0, cy0);
-    }
-    // EXT: the reference's op order on tool-frame points (u = c x + s y,
-    // v = -s x + c y), so all-zero extensions reproduce the reference bits
-    const double uu = __dadd_rn(__dmul_rn(r[0], pt.x), __dmul_rn(r[1], pt.y));
-    const double vv = __dadd_rn(__dmul_rn(-r[1], pt.x), __dmul_rn(r[0], pt.y));
-    e.xw = __dadd_rn(uu, r[2]);
-    e.yw = __dadd_rn(vv, r[3]);
-    e.key = (uint64_t)__double_as_longlong(pt.z);
+    return e.cells(e.xw, cx0, e.yw, cy0, inv);
   }
-  return e.finish(inv, cx0, cy0);
+  const double uu = __fma_rn(r[0], pt.x, __dmul_rn(r[1], pt.y));
+  const double vv = __fma_rn(r[0], pt.y, -__dmul_rn(r[1], pt.x));
+  if (MODE == MSURF_MODE_EXT_TILT) {
+    // lead-tilt model: z' = fma(sin(tau), v, cos(tau) z + zoff),
+    // y' - ty = fma(cos(tau), v, -sin(tau) z); pt = (x, y, sin(tau) z, cos(tau) z + zoff)
+    const double zz = __fma_rn(tilt_s, vv, pt.w);
+    e.key = enc_key_raw(zz);  // pt.w is never -0 (host-canonical), so neither is zz
+    e.zh = (unsigned)(e.key >> 32);
+    return e.cells(uu, r[2], __fma_rn(tilt_c, vv, -pt.z), r[3], inv);
+  }
+  e.key = (uint64_t)__double_as_longlong(pt.z);
+  return e.cells(uu, r[2], vv, r[3], inv);
+}
+
+// exact workpiece x', y' of an extended-mode point (the deferred near-boundary
+// path): EXT in the reference's op order on tool-frame points (u = c x + s y,
+// v = -s x + c y), so all-zero extensions reproduce the reference bits; tilt
+// in the model's fused form
+template <int MODE>
+__device__ __forceinline__ void exact_xy(const double4 pt, double c, double s, double xoff, double ty,
+                                         double tilt_c, double& xw, double& yw) {
+  if (MODE == MSURF_MODE_EXT_TILT) {
+    const double uu = __fma_rn(c, pt.x, __dmul_rn(s, pt.y));
+    const double vv = __fma_rn(c, pt.y, -__dmul_rn(s, pt.x));
+    xw = __dadd_rn(uu, xoff);
+    yw = __dadd_rn(__fma_rn(tilt_c, vv, -pt.z), ty);
+  } else {
+    const double uu = __dadd_rn(__dmul_rn(c, pt.x), __dmul_rn(s, pt.y));
+    const double vv = __dadd_rn(__dmul_rn(-s, pt.x), __dmul_rn(c, pt.y));
+    xw = __dadd_rn(uu, xoff);
+    yw = __dadd_rn(vv, ty);
+  }
 }
 
 // Time-neighbour pre-reduction across lanes (consecutive live steps of one
@@ -382,6 +407,10 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
   for (int k = 0; k < 6; ++k) box_f[k] = (float)J.tooth_box[tooth * 6 + k];
   if (ONE && !tile_may_hit<MODE, TILE>(J, pass, tooth, st)) return;  // uniform across the CTA
 
+  const double inv = 1.0 / dd;
+  const double cx0 = 0.5 - J.x_min * inv;
+  const double cy0 = 0.5 - J.y_min * inv;
+
   // ---------------- phase 1: one thread per time step (kSubSteps rounds of
   // kSweepThreads steps), live steps appended in time order
   int n_live = 0;
@@ -470,7 +499,7 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
           } else {
             rd[0] = c;
             rd[1] = sn;
-            rd[2] = xoff;
+            rd[2] = xoff;  // folded into cxp / cyp when stored (see eval_point)
             rd[3] = ty;
           }
           {
@@ -542,8 +571,17 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
     if (any) {
       const int slot = base + __popc(bal & ((1u << lane) - 1u));
       for (int w = 0; w < mask_words; ++w) mslot[slot * mask_words + w] = masks[tid * mask_words + w];
+      if (MODE == MSURF_MODE_REF) {
 #pragma unroll
-      for (int k = 0; k < RW; ++k) rowv[slot * 8 + k] = rd[k];
+        for (int k = 0; k < RW; ++k) rowv[slot * 8 + k] = rd[k];
+      } else {
+        rowv[slot * 8 + 0] = rd[0];
+        rowv[slot * 8 + 1] = rd[1];
+        rowv[slot * 8 + 2] = __fma_rn(rd[2], inv, cx0);
+        rowv[slot * 8 + 3] = __fma_rn(rd[3], inv, cy0);
+        rowv[slot * 8 + 4] = rd[2];
+        rowv[slot * 8 + 5] = rd[3];
+      }
     }
   }
   if constexpr (kSweepWarps == 1) __syncwarp(); else __syncthreads();
@@ -561,9 +599,6 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
   // lanes (or in one lane's pair): the time-neighbour filter skips a deposit
   // only when a same-cell neighbour provably deposits a key that is not
   // higher, so each monotone run of a point through a cell costs one RED.MIN.
-  const double inv = 1.0 / dd;
-  const double cx0 = 0.5 - J.x_min * inv;
-  const double cy0 = 0.5 - J.y_min * inv;
   const unsigned span_i = (unsigned)J.m;
   const int j_lo = (int)J.j_lo;
   const unsigned span_j = (unsigned)(J.j_hi - J.j_lo);
@@ -665,8 +700,14 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
         for (int k = 0; k < p_end; ++k) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const PointEval e = eval_point<MODE>(ptstage[warp][k], h ? rb : ra, inv, cx0, cy0, tilt_c, tilt_s);
+            const double4 pt = ptstage[warp][k];
+            PointEval e = eval_point<MODE>(pt, h ? rb : ra, inv, cx0, cy0, tilt_c, tilt_s);
             if (!(e.near & (h ? on_b : on_a))) continue;
+            if (MODE != MSURF_MODE_REF) {
+              const int sl = h ? rtb : rta;
+              exact_xy<MODE>(pt, h ? rb[0] : ra[0], h ? rb[1] : ra[1], rowv[sl * 8 + 4], rowv[sl * 8 + 5], tilt_c,
+                             e.xw, e.yw);
+            }
             const int ie = cell_index_exact(e.xw, J.x_min, dd);
             const int je = cell_index_exact(e.yw, J.y_min, dd) - j_lo;
             const bool in = ((unsigned)ie <= span_i) & ((unsigned)je <= span_j);
@@ -751,8 +792,11 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
       }
       if (__builtin_expect(__any_sync(0xffffffffu, anynear), 0)) {
         for (int k = 0; k < p_end; ++k) {
-          const PointEval e = eval_point<MODE>(ptstage[warp][k], r, inv, cx0, cy0, tilt_c, tilt_s);
+          const double4 pt = ptstage[warp][k];
+          PointEval e = eval_point<MODE>(pt, r, inv, cx0, cy0, tilt_c, tilt_s);
           if (!(e.near & on)) continue;
+          if (MODE != MSURF_MODE_REF)
+            exact_xy<MODE>(pt, r[0], r[1], rowv[rt * 8 + 4], rowv[rt * 8 + 5], tilt_c, e.xw, e.yw);
           const int ie = cell_index_exact(e.xw, J.x_min, dd);
           const int je = cell_index_exact(e.yw, J.y_min, dd) - j_lo;
           const bool in = on & ((unsigned)ie <= span_i) & ((unsigned)je <= span_j);

@@ -260,3 +260,34 @@ def test_deferred_exact_path_bitexact():
     script = _FORCE_NEAR_SCRIPT.format(root=root, tests=os.path.join(root, "tests"))
     out = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "FORCE_NEAR_OK" in out.stdout, out.stderr[-3000:]
+
+
+@pytest.mark.parametrize("case", ["ref", "ext", "tilt"])
+def test_tile_list_path_equals_per_job_path(case):
+    """The batched launch pre-culls its tiles into a list walked by persistent
+    CTAs; the single-job launch culls tiles inline. Same heights and the same
+    row/point counters, also for narrow strip windows where most tiles die."""
+    from paper_2603_28160_b200 import planner
+    from paper_2603_28160_b200.engine import SweepBatch
+
+    if case == "ref":
+        cfg, ext = golden_io.product_config(golden_io.load("small_3")["config"], record_trajectory=False), None
+    elif case == "ext":
+        cfg, ext = _ext_cfg("insert"), ms.Extensions(helix_angle_rad=math.radians(25), runout_offset_mm=0.002)
+    else:
+        cfg, ext = _ext_cfg("ball"), ms.Extensions(**EXT_CASES["ball_tilt"])
+    p = planner.plan(cfg, ext)
+    n = p.grid.n
+    windows = [(0, n), (n // 3, n // 3 + 4), (n - 2, n)]
+    for lo, hi in windows:
+        one = SweepBatch([(p, lo, hi)])
+        one.launch()
+        many = SweepBatch([(p, lo, hi)] * 3)
+        assert not any(many.group_per_job)  # three jobs of few tiles: the listed batched launch
+        many.launch()
+        h1 = one.heights()[0].cpu().numpy()
+        c1, m1 = one.counters()
+        cm, mm = many.counters()
+        for k, h in enumerate(many.heights()):
+            assert np.array_equal(h.cpu().numpy(), h1), (case, lo, hi, k)
+            assert np.array_equal(cm[k], c1[0]) and mm[k] == m1[0], (case, lo, hi, k)

@@ -434,7 +434,7 @@ def run_ours(args, rank, world):
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
     e2e_step = float(et[0]) / args.steps
     e2e = {"value": p_total / (e2e_step * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-           "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_step,
+           "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_step, "steps_ms": [round(x, 4) for x in e2e_ms],
            "api": "simulate + areal_metrics + profile_roughness + HeightField.heights"
            if world == 1 else "sharded.simulate_strip + areal/profile all-reduce + strip read-back"}
 
@@ -600,7 +600,8 @@ def run_batch(args, rank, world):
                 "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": {"value": total_points / (e2e_step * 1e-3), "unit": UNIT,
                         "h2d_bytes_per_step": int(batch.h2d_bytes), "d2h_bytes_per_step": int(d2h),
-                        "ms_per_step": e2e_step, "api": "simulate_batch + areal_metrics_batch + heights"},
+                        "ms_per_step": e2e_step, "steps_ms": [round(x, 3) for x in e2e_ms],
+                        "api": "simulate_batch + areal_metrics_batch + heights"},
                 "gpu_launches": pipe.launches_per_run * args.steps, "clocks": clk,
                 "metrics": {"surfaces_ok": len(ok), "Sa_um_mean": float(np.mean([m.sa_um for m in ok])) if ok else None}}
         print(json.dumps(line), flush=True)

@@ -286,6 +286,28 @@ __device__ __forceinline__ void next_unit(int& g, int& q, int nchunk) {
   }
 }
 
+// tile index inside a job -> (pass, tooth, step tile). MSURF_TILE_ORDER 0:
+// pass-major, then tooth, then time (consecutive CTAs = consecutive step
+// tiles of one tooth); 1: pass-major, then time, then tooth (the teeth of one
+// step tile are adjacent, so the CTAs in flight cover a narrower time window)
+#ifndef MSURF_TILE_ORDER
+#define MSURF_TILE_ORDER 0
+#endif
+__device__ __forceinline__ void tile_coords(unsigned loc, unsigned nst, int teeth, int& pass, int& tooth, int& st) {
+  if (MSURF_TILE_ORDER == 0) {
+    const unsigned rem = loc / nst;
+    st = (int)(loc - rem * nst);
+    tooth = (int)(rem % (unsigned)teeth);
+    pass = (int)(rem / (unsigned)teeth);
+  } else {
+    const unsigned per_pass = nst * (unsigned)teeth;
+    pass = (int)(loc / per_pass);
+    const unsigned r = loc - (unsigned)pass * per_pass;
+    st = (int)(r / (unsigned)teeth);
+    tooth = (int)(r - (unsigned)st * (unsigned)teeth);
+  }
+}
+
 // tile pre-cull: the tooth box at the tile's mid angle and mid feed position,
 // widened by the largest displacement any of its points makes within the
 // tile (rotation: arc <= Rt * |dtheta|; feed: |v_f| dt/2 per step). A tile
@@ -329,6 +351,7 @@ __device__ __forceinline__ bool tile_may_hit(const msurf_job& J, int pass, int t
                                  (float)J.tilt_c, (float)J.tilt_s);
 }
 
+#pragma nv_diag_suppress 177  // tile_done is unused in the ONE instantiations
 template <int MODE, bool DIAG, bool ONE, int TILE, int NTHR>
 __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
     sweep_kernel(const msurf_job* __restrict__ jobs, int n_jobs,
@@ -388,11 +411,8 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
   {
   // tile -> (pass, tooth, step tile) in 32-bit arithmetic (grids are < 2^31 tiles)
   const unsigned nst = (unsigned)((J.step_hi - J.step_lo + kTileSteps - 1) / kTileSteps);
-  const unsigned loc = (unsigned)local;
-  const unsigned rem = loc / nst;
-  const int st = (int)(loc - rem * nst);
-  const int tooth = (int)(rem % (unsigned)J.teeth);
-  const int pass = (int)(rem / (unsigned)J.teeth);
+  int pass, tooth, st;
+  tile_coords((unsigned)local, nst, J.teeth, pass, tooth, st);
   const int npts = J.points;
   const int nchunk = (npts + 31) >> 5;
   const double dd = J.spacing;
@@ -833,6 +853,7 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
   if constexpr (ONE) return;
   }
 }
+#pragma nv_diag_default 177
 
 // tile list of a job array: one thread per tile (job found by binary search
 // in the tile prefix), live tiles appended with one atomic per warp; the
@@ -853,10 +874,8 @@ __global__ void __launch_bounds__(256)
     const msurf_job& J = jobs[lo];
     const unsigned local = (unsigned)(t - prefix[lo]);
     const unsigned nst = (unsigned)((J.step_hi - J.step_lo + TILE - 1) / TILE);
-    const unsigned rem = local / nst;
-    const int st = (int)(local - rem * nst);
-    const int tooth = (int)(rem % (unsigned)J.teeth);
-    const int pass = (int)(rem / (unsigned)J.teeth);
+    int pass, tooth, st;
+    tile_coords(local, nst, J.teeth, pass, tooth, st);
     live = tile_may_hit<MODE, TILE>(J, pass, tooth, st);
     entry = ((unsigned long long)lo << 32) | local;
   }

@@ -41,7 +41,7 @@ constexpr int kBatchTile = 64, kBatchThreads = 32;   // msurf_sweep (job arrays)
 constexpr int kTiltTile = 64, kTiltThreads = 32;     // msurf_sweep_job, EXT_TILT
 constexpr int kWideTile = 128, kWideThreads = 128;   // msurf_sweep_job, REF / EXT
 #ifndef MSURF_MIN_BLOCKS_ONE
-#define MSURF_MIN_BLOCKS_ONE 28  // 1-warp CTAs with a by-value job: 72 registers
+#define MSURF_MIN_BLOCKS_ONE 32  // 1-warp CTAs with a by-value job: 64 registers (no spills since the folded locate)
 #endif
 #ifndef MSURF_MIN_BLOCKS
 #define MSURF_MIN_BLOCKS 24  // 1-warp CTAs with the job array: 80 registers

@@ -275,15 +275,22 @@ class SweepBatch:
         self.group_meta = []
         self.group_tiles = []
         self.group_host_jobs = []  # host copies of the descriptors (by-value launches)
+        self.group_per_job = []
         for mode, jidx in sorted(groups.items()):
             tiles = [surfs[jobs[j][0]].plan.passes * surfs[jobs[j][0]].plan.teeth *
                      ((jobs[j][4] - jobs[j][3] + tile_steps - 1) // tile_steps) for j in jidx]
-            prefix = np.concatenate([[0], np.cumsum(tiles)]).astype(np.int64)
-            job_off = ar.add(np.zeros(len(jidx) * ctypes.sizeof(_native.MsurfJob), dtype=np.uint8))
-            pre_off = ar.add(prefix)
-            self.group_meta.append((mode, jidx, job_off, pre_off, int(prefix[-1]),
+            per_job = _per_job_launches(tiles)
+            if per_job:  # by-value launches: host descriptors only
+                job_off = pre_off = None
+            else:
+                prefix = np.zeros(len(tiles) + 1, dtype=np.int64)
+                np.cumsum(tiles, out=prefix[1:])
+                job_off = ar.reserve(len(jidx) * _native.JOB_DTYPE.itemsize)  # written by fill()
+                pre_off = ar.add(prefix)
+            self.group_meta.append((mode, jidx, job_off, pre_off, sum(tiles),
                                     max(surfs[jobs[j][0]].plan.points for j in jidx)))
-            self.group_tiles.append([int(t) for t in tiles])
+            self.group_tiles.append(tiles)
+            self.group_per_job.append(per_job)
         keys_ptr = self.keys.data_ptr()
         strip_ptr = self.strip_keys.data_ptr() if self.strip_keys is not None else 0
         traj_ptr = self.traj.data_ptr() if self.traj is not None else 0
@@ -321,7 +328,8 @@ class SweepBatch:
                         tr, base + o["min_index"], base + self.ctr_off + i * _native.NUM_CTRS * 8,
                         p.teeth, p.points, p.passes, 0))
                 arr = np.array(rows, dtype=_native.JOB_DTYPE)
-                out.append((job_off, arr.view(np.uint8)))
+                if job_off is not None:
+                    out.append((job_off, arr.view(np.uint8)))
                 self.group_host_jobs.append(arr)
             return out
 
@@ -333,7 +341,6 @@ class SweepBatch:
         self.same_shape = len({s.nodes for s in surfs}) == 1
         # one fill / decode launch for the whole batch (no strip-layout surface)
         self.batched_fill = self.same_shape and all(s.n_strips == 1 for s in surfs)
-        self.group_per_job = [_per_job_launches(tl) for tl in self.group_tiles]
         # msurf_sweep scratch (tile count + pre-culled tile list), shared by the
         # batched launch groups (they run in stream order)
         need = max((gm[4] for gm, pj in zip(self.group_meta, self.group_per_job) if not pj), default=0)

@@ -16,7 +16,6 @@ engine.py:329-342).
 from __future__ import annotations
 
 import ctypes
-import sys
 import math
 from dataclasses import dataclass, field, replace
 
@@ -49,8 +48,6 @@ PIPELINE_PLAN_THREADS = int(__import__("os").environ.get("MSURF_PIPELINE_THREADS
 PIPELINE_FIRST_CHUNK = int(__import__("os").environ.get("MSURF_FIRST_CHUNK", "0"))
 # native planner threads for the first group (planned while nothing else runs)
 PIPELINE_FIRST_THREADS = int(__import__("os").environ.get("MSURF_FIRST_THREADS", "1"))
-# GIL switch interval while the planner threads run beside the launching thread
-PIPELINE_SWITCH_INTERVAL = float(__import__("os").environ.get("MSURF_SWITCH_INTERVAL", "0.0002"))
 # threads of the native planning loops of every group (GIL released)
 PIPELINE_NATIVE_THREADS = int(__import__("os").environ.get("MSURF_NATIVE_THREADS", "1"))
 
@@ -560,21 +557,12 @@ def simulate_batch(configs, extensions=None, *, trig: str = "device", diagnostic
     # threads while the main thread launches, and launched in order
     first_plans = plan_many(configs[bounds[0][0]:bounds[0][1]], exts[bounds[0][0]:bounds[0][1]],
                             PIPELINE_FIRST_THREADS, PIPELINE_NATIVE_THREADS)
-    # the planner threads and the launching main thread share the GIL: with the
-    # default 5 ms switch interval a launch can sit behind a planner's Python
-    # for milliseconds, so the interval is shortened while the pipeline runs
-    old_iv = sys.getswitchinterval()
-    if PIPELINE_SWITCH_INTERVAL > 0:
-        sys.setswitchinterval(min(old_iv, PIPELINE_SWITCH_INTERVAL))
-    try:
-        with ThreadPoolExecutor(max_workers=min(PIPELINE_PLAN_THREADS, PLAN_THREADS, len(bounds) - 1)) as pool:
-            futs = [pool.submit(plan_many, configs[lo:hi], exts[lo:hi], 1, PIPELINE_NATIVE_THREADS)
-                    for lo, hi in bounds[1:]]
-            out.extend(_launch_results(first_plans, trig, diagnostics, prefetch))
-            for f in futs:
-                out.extend(_launch_results(f.result(), trig, diagnostics, prefetch))
-    finally:
-        sys.setswitchinterval(old_iv)
+    with ThreadPoolExecutor(max_workers=min(PIPELINE_PLAN_THREADS, PLAN_THREADS, len(bounds) - 1)) as pool:
+        futs = [pool.submit(plan_many, configs[lo:hi], exts[lo:hi], 1, PIPELINE_NATIVE_THREADS)
+                for lo, hi in bounds[1:]]
+        out.extend(_launch_results(first_plans, trig, diagnostics, prefetch))
+        for f in futs:
+            out.extend(_launch_results(f.result(), trig, diagnostics, prefetch))
     return out
 
 

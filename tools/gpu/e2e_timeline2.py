@@ -6,8 +6,9 @@ import torch
 import paper_2603_28160_b200 as ms
 from paper_2603_28160_b200 import configs
 
-cfg, ext, meta = configs.config2()
-if len(sys.argv) > 1 and sys.argv[1] == "noprefetch":
+name = next((a for a in sys.argv[1:] if a.startswith("config")), "config2")
+cfg, ext, meta = getattr(configs, name)()
+if "noprefetch" in sys.argv[1:]:
     from paper_2603_28160_b200 import engine, planner
     ms.simulate = lambda c, e: engine._launch_results([planner.plan(c, e)], "device", False, prefetch=False)[0]
 every, uncut = 64, "exclude"

@@ -25,12 +25,9 @@ keep = []
 for _ in range(4):
     keep.append(step(32)[1]); keep = keep[-2:]
 rows = []
-grid = [(w, f, ft, c, nt) for w in (1, 2) for f, ft in ((0, 1), (8, 1), (8, 4)) for c in (32, 48)
-        for nt in (1,)]
-import os
-ivs = [float(x) for x in os.environ.get("IVS", "0.005,0.0005,0.0002,0.00005").split(",")]
+grid = [(w, 0, 1, c, nt) for w in (0, 1) for c in (16, 32, 64) for nt in (1, 2, 4, 8)]
+ivs = [0.005]
 for workers, first, fthr, chunk, nthr, iv in [g + (iv,) for iv in ivs for g in grid]:
-    engine.PIPELINE_SWITCH_INTERVAL = iv
     engine.PIPELINE_PLAN_THREADS, engine.PIPELINE_FIRST_CHUNK, engine.PIPELINE_FIRST_THREADS = workers, first, fthr
     engine.PIPELINE_NATIVE_THREADS = nthr
     ts = []

@@ -257,6 +257,10 @@ int msurf_microbench(int32_t which, double* result);
 void* msurf_host_alloc(int64_t bytes);
 int msurf_host_free(void* p);
 int msurf_readback(const void* src, void* host_dst, int64_t bytes, void* stream);
+/* msurf_readback, then block the calling thread until `stream` has passed the
+ * kernel (cudaStreamSynchronize): one call per small result on the host
+ * path, the data is valid on return. */
+int msurf_readback_sync(const void* src, void* host_dst, int64_t bytes, void* stream);
 
 #ifdef __cplusplus
 }

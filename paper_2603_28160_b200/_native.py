@@ -97,6 +97,7 @@ EXPORTS = {
     "msurf_host_alloc": (c_void_p, [c_int64]),
     "msurf_host_free": (ctypes.c_int, [c_void_p]),
     "msurf_readback": (ctypes.c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "msurf_readback_sync": (ctypes.c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "msurf_plan_geometry": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "msurf_plan_geometry_many": (ctypes.c_int, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_int32]),
     "msurf_plan_finish_many": (ctypes.c_int, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
@@ -140,20 +141,30 @@ def check(rc: int) -> None:
         raise MillsurfError("libmsurf: " + lib().msurf_last_error().decode())
 
 
+_torch_ok = None
+
+
 def require_cuda():
+    global _torch_ok
+    if _torch_ok is not None:
+        return _torch_ok
     import torch
 
     if not torch.cuda.is_available():
         raise NativeUnavailableError("no CUDA device: the FSM sweep runs only on the GPU")
     lib()
+    _torch_ok = torch
     return torch
 
 
 def stream_ptr(stream=None) -> int:
+    """Raw cudaStream_t of ``stream`` or of the current stream (the raw query
+    skips building a torch.cuda.Stream object: ~0.3 us instead of ~8 us)."""
+    if stream is not None:
+        return int(stream.cuda_stream)
     import torch
 
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return int(s.cuda_stream)
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 READBACK_MAX = 1 << 20  # bytes; larger results take a copy-engine D2H
@@ -173,17 +184,23 @@ def readback(t) -> np.ndarray:
         return t.cpu().numpy()
     dev = t.device.index if t.device.index is not None else torch.cuda.current_device()
     with _mailbox_lock:
-        box = _mailboxes.get(dev)
-        if box is None:
+        mb = _mailboxes.get(dev)
+        if mb is None:
             ptr = lib().msurf_host_alloc(READBACK_MAX)
             if not ptr:
                 raise NativeUnavailableError(f"msurf_host_alloc: {lib().msurf_last_error().decode()}")
-            box = _mailboxes[dev] = np.frombuffer((ctypes.c_char * READBACK_MAX).from_address(ptr), dtype=np.uint8)
-        check(lib().msurf_readback(t.data_ptr(), box.ctypes.data, nbytes, stream_ptr()))
-        ev = torch.cuda.Event()
-        ev.record()
-        ev.synchronize()
-        return box[:nbytes].view(np.dtype(str(t.dtype).replace("torch.", ""))).copy().reshape(tuple(t.shape))
+            mb = _mailboxes[dev] = (np.frombuffer((ctypes.c_char * READBACK_MAX).from_address(ptr), dtype=np.uint8),
+                                    ptr)
+        box, ptr = mb
+        # kernel + stream sync in one foreign call (ctypes drops the GIL meanwhile)
+        check(lib().msurf_readback_sync(t.data_ptr(), ptr, nbytes, stream_ptr()))
+        dt = _NP_DTYPES.get(t.dtype)
+        if dt is None:
+            dt = _NP_DTYPES[t.dtype] = np.dtype(str(t.dtype).replace("torch.", ""))
+        return box[:nbytes].view(dt).copy().reshape(tuple(t.shape))
+
+
+_NP_DTYPES = {}
 
 
 class Arena:

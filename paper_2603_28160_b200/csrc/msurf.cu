@@ -1523,6 +1523,13 @@ int msurf_readback(const void* src, void* host_dst, int64_t bytes, void* stream)
   return check_launch("readback_kernel");
 }
 
+int msurf_readback_sync(const void* src, void* host_dst, int64_t bytes, void* stream) {
+  if (msurf_readback(src, host_dst, bytes, stream)) return 1;
+  const cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return set_err(std::string("msurf_readback_sync: ") + cudaGetErrorString(e));
+  return 0;
+}
+
 int msurf_abi_version(void) { return MSURF_ABI_VERSION; }
 const char* msurf_last_error(void) { return g_err.c_str(); }
 int msurf_sizeof_job(void) { return (int)sizeof(msurf_job); }

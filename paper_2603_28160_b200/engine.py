@@ -75,7 +75,9 @@ class SimulationConfig:
 class _Launch:
     """Device-side state of one asynchronous sweep launch: the batch (keeps
     every buffer alive), its events, and the small D2H read of the counters
-    performed once, on first demand."""
+    performed once, on first demand. Its events go back to a per-device pool
+    when it is released (re-recording a finished or abandoned event is
+    legal), so a simulate call does not pay cudaEventCreate."""
 
     def __init__(self, batch, events):
         self.batch, self.events = batch, events
@@ -89,6 +91,12 @@ class _Launch:
     def device_seconds(self):
         self.events[3].synchronize()
         return self.events[0].elapsed_time(self.events[3]) * 1e-3
+
+    def __del__(self):
+        try:
+            _give_events(self.batch.dev.index, (self.events[0], self.events[3]))
+        except Exception:  # interpreter shutdown
+            pass
 
 
 class SimulationResult:
@@ -396,24 +404,23 @@ class SweepBatch:
                                                base + self.machined_off + 8 * i, sp))
 
     def launch(self, stream=None, events=None):
-        """Enqueue fill -> sweep(s) -> decode on ``stream`` (async).
-        ``events`` = (start, after_fill, after_sweep, end) CUDA events, optional."""
-        torch = self.torch
-        st = stream if stream is not None else torch.cuda.current_stream(self.dev)
-        sp = int(st.cuda_stream)
+        """Enqueue fill -> sweep(s) -> decode on ``stream`` (default: the
+        current stream; async). ``events`` = (start, after_fill, after_sweep,
+        end) CUDA events, optional, recorded on the same stream."""
+        sp = _native.stream_ptr(stream)
         ev = events if events else (None, None, None, None)
-        with torch.cuda.stream(st):
-            if ev[0] is not None:
-                ev[0].record(st)
-            self.launch_fill(sp)
-            if ev[1] is not None:
-                ev[1].record(st)
-            self.launch_sweep(sp)
-            if ev[2] is not None:
-                ev[2].record(st)
-            self.launch_decode(sp)
-            if ev[3] is not None:
-                ev[3].record(st)
+
+        def mark(e):
+            if e is not None:
+                e.record(stream) if stream is not None else e.record()
+
+        mark(ev[0])
+        self.launch_fill(sp)
+        mark(ev[1])
+        self.launch_sweep(sp)
+        mark(ev[2])
+        self.launch_decode(sp)
+        mark(ev[3])
 
     def heights(self):
         """fp64 views (valid after a launch) — one per surface."""
@@ -480,6 +487,22 @@ def simulate(config: SimulationConfig, extensions: Extensions | None = None, *,
     return _launch_results([p], trig, diagnostics, prefetch=True)[0]
 
 
+_EVENT_POOL = {}  # device index -> timing events of released launches (cudaEventCreate costs ~10 us)
+
+
+def _take_events(torch, dev, n):
+    pool = _EVENT_POOL.setdefault(dev.index, [])
+    out = [pool.pop() for _ in range(min(n, len(pool)))]
+    out += [torch.cuda.Event(enable_timing=True) for _ in range(n - len(out))]
+    return out
+
+
+def _give_events(dev_index, events):
+    pool = _EVENT_POOL.get(dev_index)
+    if pool is not None and len(pool) < 64:
+        pool.extend(e for e in events if e is not None)
+
+
 def _launch_results(plans, trig, diagnostics=False, prefetch=False):
     """Upload, launch asynchronously, wrap the fields (no host sync unless a
     trajectory record is requested). ``prefetch``: one D2H copy of the whole
@@ -487,7 +510,9 @@ def _launch_results(plans, trig, diagnostics=False, prefetch=False):
     after the decode; each field's ``heights`` then only waits for it."""
     torch = _native.require_cuda()
     b = SweepBatch([(p, 0, p.grid.n) for p in plans], trig=trig, diagnostics=diagnostics)
-    e0, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # e0/e3 time the launch (main_loop_seconds) and are pooled; the prefetch's
+    # event is fresh: the fields keep it after the launch object is released
+    e0, e3 = _take_events(torch, b.dev, 2)
     ev = [e0, None, None, e3]
     b.launch(events=ev)
     lk = _Launch(b, ev)
@@ -498,7 +523,7 @@ def _launch_results(plans, trig, diagnostics=False, prefetch=False):
         from .grid import _copy_stream
 
         side = _copy_stream(torch, b.dev)
-        side.wait_stream(torch.cuda.current_stream(b.dev))
+        side.wait_event(e3)  # e3 closes the decode on the launch stream
         host = torch.empty(b.keys.shape, dtype=torch.float64, pin_memory=True)
         with torch.cuda.stream(side):
             host.copy_(b.keys.view(torch.float64), non_blocking=True)

@@ -425,7 +425,9 @@ class SweepBatch:
     def heights(self):
         """fp64 views (valid after a launch) — one per surface."""
         h = self.keys.view(self.torch.float64)
-        return [h[s.key_off: s.key_off + s.nodes] for s in self.surfs]
+        total = self.surfs[-1].key_off + self.surfs[-1].nodes
+        # surfaces sit back to back: one split call instead of n slices
+        return list(h[:total].split([s.nodes for s in self.surfs]))
 
     def sentinels_device(self):
         return self.buf[self.sentinel_off: self.sentinel_off + 8 * self.n].view(self.torch.float64)
@@ -531,12 +533,14 @@ def _launch_results(plans, trig, diagnostics=False, prefetch=False):
             done.record(side)
         b.keys.record_stream(side)
     out = []
+    sent1 = sents.split(1)
+    hosts = host[:views[-1].numel() + b.surfs[-1].key_off].split([s.nodes for s in b.surfs]) \
+        if host is not None else None
     for i, (p, v, tr) in enumerate(zip(plans, views, trajs)):
         f = HeightField(p.grid, p.initial_height, device=v)
-        f._dev_sentinel = sents[i:i + 1]
-        if host is not None:
-            s = b.surfs[i]
-            f._set_prefetch(host[s.key_off: s.key_off + s.nodes], done)
+        f._dev_sentinel = sent1[i]
+        if hosts is not None:
+            f._set_prefetch(hosts[i], done)
         out.append(SimulationResult(field=f, trajectory=_build_trajectory(p, tr) if p.record else None,
                                     time_steps=p.steps, trajectory_points=p.trajectory_points,
                                     launch=lk, index=i, share=1.0 / len(plans)))

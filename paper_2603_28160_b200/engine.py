@@ -494,8 +494,12 @@ _EVENT_POOL = {}  # device index -> timing events of released launches (cudaEven
 
 def _take_events(torch, dev, n):
     pool = _EVENT_POOL.setdefault(dev.index, [])
-    out = [pool.pop() for _ in range(min(n, len(pool)))]
-    out += [torch.cuda.Event(enable_timing=True) for _ in range(n - len(out))]
+    out = []
+    while len(out) < n:
+        try:
+            out.append(pool.pop())  # atomic under the GIL; another thread may empty the pool first
+        except IndexError:
+            out.append(torch.cuda.Event(enable_timing=True))
     return out
 
 

@@ -366,7 +366,10 @@ def _starts_device(torch, dev, starts):
     if t is None:
         t = torch.from_numpy(a).pin_memory().to(dev, non_blocking=True)
         if len(_STARTS) >= 32:
-            _STARTS.pop(next(iter(_STARTS)))
+            try:
+                _STARTS.pop(next(iter(_STARTS)), None)
+            except (StopIteration, RuntimeError):  # emptied / resized by another thread
+                pass
         _STARTS[key] = t
     return t
 

@@ -252,3 +252,45 @@ def test_readback_mapped_matches_copy():
     assert np.array_equal(_native.readback(m), m.cpu().numpy())
     side.synchronize()
     assert torch.equal(host[:100].to(dev), big[:100])
+
+
+def test_fields_outlive_results_with_pooled_events():
+    """A field keeps its prefetched heights after its SimulationResult is
+    released: the launch's timing events go back to the pool and are
+    re-recorded by later launches, the prefetch event is never pooled."""
+    import gc
+
+    cfg = _front_cut(0.6, 0.01)
+    ref = ms.simulate(cfg)
+    h_ref = ref.field.heights.copy()
+    assert ref.main_loop_seconds > 0
+    fields = []
+    for _ in range(4):
+        r = ms.simulate(cfg)
+        fields.append(r.field)
+        del r
+        gc.collect()
+    for _ in range(3):
+        r2 = ms.simulate(cfg)
+        assert r2.main_loop_seconds > 0
+    for f in fields:
+        assert np.array_equal(f.heights, h_ref)
+
+
+def test_profile_roughness_cached_offsets_and_streams():
+    """Profile offsets are cached per (device, stream, offsets): repeated
+    calls, a second profile set and a second stream return the same results
+    as the first call of each."""
+    import torch
+
+    f = ms.simulate(_front_cut(0.6, 0.01)).field
+    a = ms.profile_roughness(f, every=2, uncut="exclude")
+    assert ms.profile_roughness(f, every=2, uncut="exclude") == a
+    c = ms.profile_roughness(f, every=3, uncut="exclude")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        d = ms.profile_roughness(f, every=3, uncut="exclude")
+        e = ms.profile_roughness(f, every=2, uncut="exclude")
+    assert c == d and e == a
+    assert len(a) == len(range(0, f.spec.m + 1, 2))

@@ -317,3 +317,30 @@ def test_sweep_batch_descriptors_point_at_plan_arrays(monkeypatch):
         assert (row["step_lo"], row["step_hi"], row["j_lo"], row["j_hi"]) == (s_lo, s_hi, lo, hi)
         assert int(row["counters"]) - base_ptr == b.ctr_off + i * _native.NUM_CTRS * 8
     assert seen == set(range(len(order)))
+
+
+def test_vectorised_profile_finish_equals_per_row():
+    """roughness._finish_profiles (all rows at once) gives the same objects
+    and the same first error as _finish_profile row by row."""
+    from paper_2603_28160_b200 import roughness as R
+    from paper_2603_28160_b200.errors import DomainError
+
+    rng = np.random.default_rng(5)
+    rows = np.zeros((9, 8))
+    rows[:, 1] = rng.integers(2, 1000, 9)
+    rows[:, 3] = rng.normal(size=9) + 2.0
+    rows[:, 4] = rng.normal(size=9) - 2.0
+    rows[:, 5] = rng.random(9) * rows[:, 1]
+    rows[:, 6] = rng.normal(size=9) * 0.1
+    idx = list(range(0, 90, 10))
+    for uncut in ("raise", "exclude"):
+        assert R._finish_profiles(rows, idx, uncut) == [R._finish_profile(r, i, uncut) for r, i in zip(rows, idx)]
+    bad = rows.copy()
+    bad[4, 2] = 3.0   # uncut cells in profile 4
+    bad[6, 1] = 1.0   # too few samples in profile 6
+    for uncut, row in (("raise", 4), ("exclude", 6)):
+        with pytest.raises(DomainError) as e1:
+            R._finish_profiles(bad, idx, uncut)
+        with pytest.raises(DomainError) as e2:
+            R._finish_profile(bad[row], idx[row], uncut)
+        assert str(e1.value) == str(e2.value)

@@ -262,6 +262,14 @@ int msurf_readback(const void* src, void* host_dst, int64_t bytes, void* stream)
  * path, the data is valid on return. */
 int msurf_readback_sync(const void* src, void* host_dst, int64_t bytes, void* stream);
 
+/* Enqueue on `stream` a D2H copy of a rows x width_bytes block (pitches in
+ * bytes, cudaMemcpy2DAsync): one feed-direction sub-strip of a row-major
+ * height map into the matching columns of a page-locked host map, so the
+ * heights of a strip-layout surface cross PCIe strip by strip while the
+ * later strips are still being swept. */
+int msurf_copy2d_d2h(void* host_dst, int64_t dst_pitch, const void* src, int64_t src_pitch,
+                     int64_t width_bytes, int64_t rows, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -98,6 +98,7 @@ EXPORTS = {
     "msurf_host_free": (ctypes.c_int, [c_void_p]),
     "msurf_readback": (ctypes.c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "msurf_readback_sync": (ctypes.c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "msurf_copy2d_d2h": (ctypes.c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
     "msurf_plan_geometry": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "msurf_plan_geometry_many": (ctypes.c_int, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_int32]),
     "msurf_plan_finish_many": (ctypes.c_int, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

@@ -1530,6 +1530,17 @@ int msurf_readback_sync(const void* src, void* host_dst, int64_t bytes, void* st
   return 0;
 }
 
+int msurf_copy2d_d2h(void* host_dst, int64_t dst_pitch, const void* src, int64_t src_pitch,
+                     int64_t width_bytes, int64_t rows, void* stream) {
+  if (!host_dst || !src || rows < 0 || width_bytes < 0 || dst_pitch < width_bytes || src_pitch < width_bytes)
+    return set_err("msurf_copy2d_d2h: bad arguments");
+  if (rows == 0 || width_bytes == 0) return 0;
+  const cudaError_t e = cudaMemcpy2DAsync(host_dst, (size_t)dst_pitch, src, (size_t)src_pitch, (size_t)width_bytes,
+                                          (size_t)rows, cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e != cudaSuccess) return set_err(std::string("msurf_copy2d_d2h: ") + cudaGetErrorString(e));
+  return 0;
+}
+
 int msurf_abi_version(void) { return MSURF_ABI_VERSION; }
 const char* msurf_last_error(void) { return g_err.c_str(); }
 int msurf_sizeof_job(void) { return (int)sizeof(msurf_job); }

@@ -174,11 +174,13 @@ class SweepBatch:
     sub-strip (each sweep job deposits into one contiguous slab), and its
     decode writes the row-major heights into the first."""
 
-    def __init__(self, surfaces, trig: str = "device", device=None, l2_tile_bytes: int = L2_TILE_BYTES,
+    def __init__(self, surfaces, trig: str = "device", device=None, l2_tile_bytes: int | None = None,
                  diagnostics: bool = False):
         torch = _native.require_cuda()
         self.torch = torch
         self.lib = _native.lib()
+        if l2_tile_bytes is None:
+            l2_tile_bytes = L2_TILE_BYTES
         # per-point deposit/atomic counters (MSURF_SWEEP_DIAG): off on the hot path
         self.diagnostics = bool(diagnostics)
         self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
@@ -422,6 +424,48 @@ class SweepBatch:
         self.launch_decode(sp)
         mark(ev[3])
 
+    def pipelined_strips(self) -> bool:
+        """ONE strip-layout surface whose sub-strips are swept job by job: each
+        strip can be decoded, and its heights copied out, as soon as its own
+        sweep is done (launch_by_strip)."""
+        return (self.n == 1 and self.surfs[0].n_strips > 1 and len(self.group_meta) == 1
+                and self.group_per_job[0])
+
+    def launch_by_strip(self, strip_done, events=None):
+        """Same work and results as launch(), ordered strip by strip on the
+        current stream: fill, then per sub-strip q its sweep job and its
+        decode (msurf_decode_strips over that strip alone), then
+        ``strip_done(q, c0, w)`` (columns [c0, c0 + w) of the surface are
+        final: the caller enqueues their D2H, which then overlaps the sweeps
+        of the later strips). ``events`` = (start, -, -, end)."""
+        if not self.pipelined_strips():
+            raise ConfigError("launch_by_strip needs one strip-layout surface with per-job sweeps")
+        lib, base = self.lib, self.base
+        sp = _native.stream_ptr()
+        ev = events if events else (None, None, None, None)
+        s, i = self.surfs[0], 0
+        if ev[0] is not None:
+            ev[0].record()
+        self.launch_fill(sp)
+        mode, jidx, _, _, _, max_pts = self.group_meta[0]
+        flag = _native.SWEEP_DIAG if self.diagnostics else 0
+        ptr, sz = self.group_host_jobs[0].ctypes.data, _native.JOB_DTYPE.itemsize
+        by_lo = {}
+        for k, jn in enumerate(jidx):
+            by_lo.setdefault(self.jobs[jn][1], []).append(k)
+        rows, w_all = s.plan.grid.m + 1, s.j_hi - s.j_lo + 1
+        for q in range(s.n_strips):
+            for k in by_lo.get(s.j_lo + s.col0[q], ()):
+                if self.group_tiles[0][k]:
+                    _native.check(lib.msurf_sweep_job(ptr + k * sz, mode | flag, max_pts, sp))
+            _native.check(lib.msurf_decode_strips(
+                self.strip_keys.data_ptr() + s.strip_off * 8, self.keys.data_ptr() + s.key_off * 8, rows, w_all,
+                1, base + self.offs[i]["col0"] + 8 * q, base + self.sentinel_off + 8 * i,
+                base + self.machined_off + 8 * i, sp))
+            strip_done(q, s.col0[q], s.col0[q + 1] - s.col0[q])
+        if ev[3] is not None:
+            ev[3].record()
+
     def heights(self):
         """fp64 views (valid after a launch) — one per surface."""
         h = self.keys.view(self.torch.float64)
@@ -489,6 +533,7 @@ def simulate(config: SimulationConfig, extensions: Extensions | None = None, *,
     return _launch_results([p], trig, diagnostics, prefetch=True)[0]
 
 
+_INFLIGHT = []  # (event, pinned buffer) of raw strip D2H copies still running
 _EVENT_POOL = {}  # device index -> timing events of released launches (cudaEventCreate costs ~10 us)
 
 
@@ -520,11 +565,39 @@ def _launch_results(plans, trig, diagnostics=False, prefetch=False):
     # event is fresh: the fields keep it after the launch object is released
     e0, e3 = _take_events(torch, b.dev, 2)
     ev = [e0, None, None, e3]
-    b.launch(events=ev)
+    host = None
+    if prefetch and b.pipelined_strips():
+        # a map above the L2 budget: each sub-strip's heights start crossing
+        # PCIe (2-D copy into the row-major pinned map) as soon as that strip
+        # is decoded, overlapping the sweeps of the later strips
+        from .grid import _copy_stream
+
+        side = _copy_stream(torch, b.dev)
+        sptr = int(side.cuda_stream)
+        host = torch.empty(b.keys.shape, dtype=torch.float64, pin_memory=True)
+        s0 = b.surfs[0]
+        pitch = (s0.j_hi - s0.j_lo + 1) * 8
+        hp, dp, rows = host.data_ptr() + s0.key_off * 8, b.keys.data_ptr() + s0.key_off * 8, s0.plan.grid.m + 1
+
+        def strip_done(q, c0, w):
+            e = torch.cuda.Event()
+            e.record()
+            side.wait_event(e)
+            _native.check(b.lib.msurf_copy2d_d2h(hp + c0 * 8, pitch, dp + c0 * 8, pitch, w * 8, rows, sptr))
+
+        b.launch_by_strip(strip_done, events=ev)
+        done = torch.cuda.Event()
+        done.record(side)
+        b.keys.record_stream(side)
+        # the raw 2-D copies are invisible to torch's pinned-memory cache: keep
+        # the buffer referenced until they finish even if every field is dropped
+        _INFLIGHT[:] = [x for x in _INFLIGHT if not x[0].query()] + [(done, host)]
+        prefetch = False  # copies already enqueued
+    else:
+        b.launch(events=ev)
     lk = _Launch(b, ev)
     views, trajs = b.heights(), b.trajectories()
     sents = b.sentinels_device()
-    host = None
     if prefetch:
         from .grid import _copy_stream
 

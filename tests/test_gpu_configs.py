@@ -139,3 +139,46 @@ def test_config5_full_raster_equals_min_of_passes():
         del bk
     assert bool((acc == whole).all())
     assert float(whole.max()) <= p.initial_height
+
+
+def test_config4_strip_pipelined_simulate_equals_whole_launch():
+    """simulate() on a strip-layout map sweeps and decodes sub-strip by
+    sub-strip and copies each strip's heights out while the later strips are
+    swept; the host map and the machined count equal a plain launch's."""
+    from paper_2603_28160_b200 import engine
+
+    cfg, ext, _ = configs.config4()
+    p = make_plan(cfg, ext)
+    whole = SweepBatch([(p, 0, p.grid.n)])
+    assert whole.pipelined_strips()
+    whole.launch()
+    w = whole.heights()[0].cpu().numpy()
+    mach = int(whole.counters()[1][0])
+    del whole
+    res = ms.simulate(cfg, ext)
+    assert res._launch.batch.pipelined_strips()
+    assert np.array_equal(res.field.heights, w)
+    assert res.cells_updated == mach
+
+
+def test_small_strip_pipelined_simulate(monkeypatch):
+    """The strip-pipelined path on a small map (L2 budget and per-job
+    threshold lowered so it cuts into sub-strips launched job by job), with
+    the field kept after its result is dropped."""
+    import gc
+
+    from paper_2603_28160_b200 import engine
+
+    cfg, ext, _ = configs.config1()
+    ref = engine._launch_results([make_plan(cfg, ext)], "device", prefetch=False)[0]
+    h_ref, cells = ref.field.heights.copy(), ref.cells_updated
+    monkeypatch.setattr(engine, "L2_TILE_BYTES", 40 << 10)
+    monkeypatch.setattr(engine, "ONE_JOB_MIN_TILES", 1)
+    res = ms.simulate(cfg, ext)
+    b = res._launch.batch
+    assert b.pipelined_strips() and b.surfs[0].n_strips >= 4
+    f = res.field
+    assert res.cells_updated == cells
+    del res, b
+    gc.collect()
+    assert np.array_equal(f.heights, h_ref)

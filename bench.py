@@ -1,22 +1,28 @@
 """Benchmark of the B200 FSM hot path (BASELINE.json metric: edge-point
 updates/s and surfaces/s at 1/2/4/8 B200, % of roofline).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
 
 A "step" is one pass of the hot path over one surface: Z-map init, the
 sweep of every (pass, step, tooth, edge point), key decode, areal roughness
-(two passes) and Ra/Rz of every 64th feed profile. Default workload is
-BASELINE configs[1] (config 2: ball-end raster). N>1 (torchrun, one rank
-per GPU, NCCL) shards the surface into feed-direction strips: the total
-work is fixed ("scaling": "strong") and the only collective is the
-all-reduce of the partial roughness moments.
+(two passes) and Ra/Rz of every 64th feed profile. The default workload is
+BASELINE configs[4] (config 5: 3-flute ball-end raster, 16 passes, 4096^2
+nodes, 4.67e10 edge-point updates per surface), the largest configuration
+that fits one GPU; at N=1 the line also carries ``per_config`` with the same
+measurement for configs 1-4 (config 3 = the 256-set batch). N>1 (one rank
+per GPU, NCCL) shards the surface into feed-direction strips: the total work
+is fixed ("scaling": "strong") and the only collective is the all-reduce of
+the partial roughness moments. ``--gpus N`` without torchrun's environment
+re-launches itself under torch.distributed.run with N ranks (and fails if
+fewer than N GPUs are visible).
 
 ``value`` is device-timed (CUDA events, inputs resident in HBM, L2 flushed
 between steps, max over ranks); ``e2e`` goes through the public API
 (simulate + areal_metrics + profile_roughness + the height map read back)
 with host planning and host<->device copies inside the timed region.
 ``--impl reference`` times the reference algorithm's CPU restatement
-(oracle/, all host threads) on a bounded sample of the same workload.
+(oracle/, all host threads) on a bounded sample of the same workload; it
+imports nothing from the product package.
 """
 
 from __future__ import annotations
@@ -25,6 +31,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -41,6 +48,8 @@ UNIT = "updates/s"
 # z' of the tilt model), plus the cell location 2 x [sub, div, add, floor]
 FLOPS_PER_POINT = {0: 20, 1: 16, 2: 20}
 FLOPS_PER_ROW = 2 * 60 + 32  # 2*C_trig + 32, C_trig ~ 60 ops (double-double sincos)
+DEFAULT_CONFIG = 5
+BASELINE_INDEX = {1: 0, 2: 1, 3: 2, 4: 3, 5: 4}
 
 
 def _env_int(k, d):
@@ -56,31 +65,6 @@ def _local_device() -> int:
     local = _env_int("LOCAL_RANK", 0)
     n = torch.cuda.device_count()
     return local % n if n else local
-
-
-def workload(cfg_id: int):
-    from paper_2603_28160_b200 import configs
-
-    if cfg_id not in configs.FACTORIES:
-        raise SystemExit(f"--config {cfg_id}: choose one of {sorted(configs.FACTORIES)} (3 is the batch bench)")
-    cfg, ext, meta = configs.FACTORIES[cfg_id]()
-    return cfg, ext, meta
-
-
-def describe(cfg, ext, meta, plan, world):
-    g = cfg.grid
-    return {
-        "workload": f"{meta['name']} (BASELINE configs[{int(meta['name'][-1]) - 1}])",
-        "tool": f"{'ball' if ext and ext.profile == 'ball' else 'flat(insert D=2R)'} R={cfg.tool.insert_radius_mm} "
-                f"Z={cfg.tool.tooth_count}",
-        "grid_nodes": [g.m + 1, g.n + 1], "spacing_mm": g.spacing_mm,
-        "edge_points": plan.points, "time_steps_per_pass": plan.steps, "passes": plan.passes,
-        "steps_per_rev": round(2 * math.pi / (plan.omega * plan.dt)),
-        "edge_point_updates_per_surface": plan.trajectory_points,
-        "outputs": "heights + Sa/Sq/Sp/Sv/Sz/Ssk/Sku + Ra/Rz every 64th feed profile (uncut cells excluded)",
-        "parallelism": f"feed strips x{world}" if world > 1 else "single GPU",
-        "l2": "flushed between timed steps (256 MiB write)",
-    }
 
 
 class ClockSampler:
@@ -158,15 +142,43 @@ def profiled_traffic(cfg_name):
 
 
 # ---------------------------------------------------------------- CPU legs
-def cpu_sample(cfg, ext, plan, target_s: float = 12.0, threads: int | None = None):
+# Only oracle/ code runs here: the workloads come from oracle/workloads.py
+# (equal to the product's configs field by field, tests/test_host_cpu.py).
+def oracle_workload(cfg_id: int):
+    from oracle import workloads as W
+
+    if cfg_id not in W.FACTORIES:
+        raise SystemExit(f"--config {cfg_id}: choose one of 1..5")
+    return W.FACTORIES[cfg_id]()
+
+
+def describe_oracle(cfg_id, cfg, ext, meta, xp, world):
+    g = cfg.grid
+    return {
+        "workload": f"{meta['name']} (BASELINE configs[{BASELINE_INDEX[cfg_id]}])",
+        "tool": f"{'ball' if ext.profile == 'ball' else 'flat(insert D=2R)'} R={cfg.tool.insert_radius_mm} "
+                f"Z={cfg.tool.tooth_count}",
+        "grid_nodes": [g.m + 1, g.n + 1], "spacing_mm": g.spacing_mm,
+        "edge_points": xp.points, "time_steps_per_pass": xp.steps, "passes": len(xp.pass_x0),
+        "steps_per_rev": round(2 * math.pi / (xp.omega * xp.dt)),
+        "edge_point_updates_per_surface": xp.trajectory_points,
+        "outputs": "heights + Sa/Sq/Sp/Sv/Sz/Ssk/Sku + Ra/Rz every 64th feed profile (uncut cells excluded)",
+        "parallelism": f"feed strips x{world}" if world > 1 else "single GPU",
+        "l2": "flushed between timed steps (256 MiB write)",
+    }
+
+
+def cpu_sample(cfg, ext, target_s: float = 12.0, threads: int | None = None):
     """The same workload on the host cores with the CPU restatement of the
     reference algorithm (oracle/fsm_ext_oracle.py, all threads). If the whole
-    surface fits in ~target_s it is run in full; otherwise a bounded sample:
-    16 step windows spread over the first pass, sized for ~target_s."""
+    surface fits in ~2.5 x target_s it is run in full; otherwise a bounded
+    sample: 16 step windows spread over the first pass, grown until the
+    sample takes about target_s."""
     from oracle import fsm_ext_oracle as xorc
 
     threads = threads or os.cpu_count() or 1
-    steps = plan.steps
+    xp = xorc.ext_plan(cfg, ext)
+    steps = xp.steps
     n_win = 16
 
     def run(win_len, passes=1):
@@ -183,7 +195,7 @@ def cpu_sample(cfg, ext, plan, target_s: float = 12.0, threads: int | None = Non
         win = min(steps // n_win, win * 8)
         pts, dt = run(win)
         rate = pts / dt
-    if plan.trajectory_points / rate <= 2.5 * target_s:
+    if xp.trajectory_points / rate <= 2.5 * target_s:
         t0 = time.perf_counter()
         _, _, ctr, _ = xorc.ext_sweep(cfg, ext, workers=threads)
         dt = time.perf_counter() - t0
@@ -199,76 +211,134 @@ def cpu_sample(cfg, ext, plan, target_s: float = 12.0, threads: int | None = Non
             "sample": what + f", oracle/fsm_ext_oracle.py, {threads} threads)"}
 
 
-def run_reference(args, rank, world):
-    if rank != 0:
-        return
-    if args.config == 3:
-        return run_reference_batch(args)
-    cfg, ext, meta = workload(args.config)
-    from paper_2603_28160_b200.planner import plan as make_plan
-
-    p = make_plan(cfg, ext)
-    vals = []
-    sample = None
-    for i in range(args.warmup + args.steps):
-        cb = cpu_sample(cfg, ext, p, target_s=args.cpu_seconds)
-        if i >= args.warmup:
-            vals.append(cb["value"])
-            sample = cb
-    v = statistics.median(vals)
-    sample["value"] = v
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * p.trajectory_points / v, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": describe(cfg, ext, meta, p, 1),
-            "surfaces_per_s": v / p.trajectory_points,
-            "cpu_baseline": sample,
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-
-
-def run_reference_batch(args):
-    """Reference arm for the batched workload: the CPU restatement on 4 of
-    the 256 parameter sets (bounded windows), mean update rate."""
+def cpu_sample_batch(target_s: float, threads: int | None = None, n_sets: int = 4):
+    """Config 3 on the host: the CPU restatement on `n_sets` of the 256
+    parameter sets (bounded windows each), mean update rate."""
     import numpy as np
 
-    base, ext, meta, ranges, mine, plans, total_points = config3_workload(0, 1)
-    vals = []
-    for i in range(args.warmup + args.steps):
-        per = args.cpu_seconds / 4
-        rates = [cpu_sample(c, e, p, target_s=per)["value"] for (c, e), p in list(zip(mine, plans))[:4]]
-        if i >= args.warmup:
-            vals.append(float(np.mean(rates)))
-    v = statistics.median(vals)
+    from oracle import workloads as W
+
+    sets, _, _ = W.config3_sets()
+    rates = [cpu_sample(c, e, target_s=target_s / n_sets, threads=threads)["value"] for c, e in sets[:n_sets]]
+    return {"value": float(np.mean(rates)), "unit": UNIT, "cores": threads or os.cpu_count(), "kind": "port",
+            "sample": f"{n_sets} of the 256 parameter sets, 16 step windows each, oracle/fsm_ext_oracle.py, "
+                      "mean edge-point-update rate"}
+
+
+def config3_points():
+    from oracle import fsm_ext_oracle as xorc
+    from oracle import workloads as W
+
+    sets, _, meta = W.config3_sets()
+    return sum(xorc.ext_plan(c, e).trajectory_points for c, e in sets), meta
+
+
+def run_reference(args, rank, world):
+    """Reference arm: the reference algorithm's CPU restatement (oracle/, no
+    product code) on the host cores, on a bounded sample per step."""
+    if rank != 0:
+        return
+    from oracle import fsm_ext_oracle as xorc
+
+    threads = os.cpu_count() or 1
+    vals, sample = [], None
+    if args.config == 3:
+        total, meta = config3_points()
+        for i in range(args.warmup + args.steps):
+            cb = cpu_sample_batch(args.cpu_seconds, threads)
+            if i >= args.warmup:
+                vals.append(cb["value"])
+                sample = cb
+        v = statistics.median(vals)
+        config = {"workload": "config3 (BASELINE configs[2]): 256 parameter sets, batched",
+                  "edge_point_updates_per_batch": total}
+        surfaces = meta["count"] * v / total
+        ms_step = 1e3 * total / v
+    else:
+        cfg, ext, meta = oracle_workload(args.config)
+        xp = xorc.ext_plan(cfg, ext)
+        for i in range(args.warmup + args.steps):
+            cb = cpu_sample(cfg, ext, target_s=args.cpu_seconds, threads=threads)
+            if i >= args.warmup:
+                vals.append(cb["value"])
+                sample = cb
+        v = statistics.median(vals)
+        config = describe_oracle(args.config, cfg, ext, meta, xp, 1)
+        surfaces = v / xp.trajectory_points
+        ms_step = 1e3 * xp.trajectory_points / v
+    sample = dict(sample, value=v)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_points / v,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": "config3 (BASELINE configs[2]): 256 parameter sets"},
-            "surfaces_per_s": meta["count"] * v / total_points,
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                             "sample": "4 of 256 parameter sets, 16 step windows each (oracle/fsm_ext_oracle.py)"},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config, "surfaces_per_s": surfaces, "cpu_baseline": sample,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "reference_impl": "oracle/fsm_ext_oracle.py (the reference's engine.py:215-313 sweep restated "
+                              "in NumPy, plus the BASELINE extensions), all host threads; imports no product code"}
     print(json.dumps(line), flush=True)
 
 
-# ---------------------------------------------------------------- GPU leg
-def roofline_terms(flops, fp64_peak, atomics, atom_peaks, sweep_ms):
+# ---------------------------------------------------------------- GPU legs
+_PEAKS = {}
+
+
+def device_peaks():
+    """fp64 issue rate and the two synthetic RED.MIN rates (msurf_microbench),
+    measured once per process on this GPU."""
+    if not _PEAKS:
+        import ctypes
+
+        from paper_2603_28160_b200 import _native
+
+        lib = _native.lib()
+        r = ctypes.c_double(0.0)
+        for w in (0, 3, 4):
+            _native.check(lib.msurf_microbench(w, ctypes.byref(r)))
+            _PEAKS[w] = r.value
+    return _PEAKS
+
+
+def red_replay(batch, reps: int = 3):
+    """The RED roof of THIS workload: the sweep's own RED.MIN address stream
+    (captured by one untimed MSURF_SWEEP_TRACE launch) replayed with no fp64
+    work, in capture order, on freshly filled Z-map keys (msurf_red_replay,
+    SweepBatch.red_replay)."""
+    return batch.red_replay(reps=reps)
+
+
+def roofline(flops, atomics, sweep_ms, replay, kernel_name):
     """The north star's roofline = the slower of fp64 issue and atomic
-    traffic: the time each resource needs at its measured peak, against the
-    measured sweep time. The RED.MIN peak depends on the access shape, so it
-    is bracketed by two microbenchmarks: random addresses in an L2-resident
-    32 MiB table (a lower bound on the sweep's peak, whose REDs cluster) and
-    one 256-byte run of keys per warp instruction (an upper bound)."""
+    traffic. t_fp64 = algorithmic fp64 ops / measured DADD/DMUL issue rate;
+    t_red = this workload's RED count / the rate its own RED stream reaches
+    when replayed alone (red_replay). ``bound`` is the larger term and
+    ``frac`` = that term / the measured sweep time."""
+    pk = device_peaks()
     t = sweep_ms * 1e-3
-    t_fp64 = flops / fp64_peak
-    t_red_lo, t_red_hi = atomics / atom_peaks[4], atomics / atom_peaks[3]
-    return {"t_sweep_ms": sweep_ms, "t_fp64_ms": t_fp64 * 1e3,
-            "t_red_ms": [t_red_lo * 1e3, t_red_hi * 1e3],
-            "red_peak_per_s": {"warp_run_32MiB": atom_peaks[4], "random_32MiB": atom_peaks[3]},
-            "red_achieved_per_s": atomics / t,
-            "frac_fp64": t_fp64 / t, "frac_red": [t_red_lo / t, t_red_hi / t],
-            "binding": "fp64" if t_fp64 >= t_red_hi else ("red" if t_red_lo >= t_fp64 else "fp64 or red")}
+    t_fp64 = flops / pk[0]
+    terms = {"t_sweep_ms": sweep_ms, "t_fp64_ms": t_fp64 * 1e3, "frac_fp64": t_fp64 / t,
+             "red_synthetic_peaks_per_s": {"warp_run_32MiB": pk[4], "random_32MiB": pk[3]},
+             "reds": atomics, "red_achieved_per_s": atomics / t}
+    t_red = None
+    if replay is not None and replay["lanes"] > 0:
+        rate = replay["lanes"] / replay["t_replay_s"]
+        t_red = atomics / rate
+        terms.update({"t_red_ms": t_red * 1e3, "frac_red": t_red / t, "red_replay_rate_per_s": rate,
+                      "red_replay": replay,
+                      "t_trace_read_ms": replay["t_read_s"] * atomics / replay["lanes"] * 1e3,
+                      "red_replay_note": "the sweep's own RED.MIN address stream (one record per warp-wide RED, "
+                                         "issue order) replayed alone; includes streaming the 128 B/record trace, "
+                                         "whose read-only time is t_trace_read_ms"})
+    bound = "fp64" if t_red is None or t_fp64 >= t_red else "atomic"
+    if bound == "fp64":
+        out = {"bound": "fp64", "achieved": flops / t / 1e12, "peak": pk[0] / 1e12, "unit": "TFLOP/s",
+               "frac": t_fp64 / t}
+    else:
+        out = {"bound": "atomic", "achieved": atomics / t / 1e9, "peak": atomics / t_red / 1e9,
+               "unit": "G RED.MIN/s", "frac": t_red / t}
+    out.update({"kernel": kernel_name, "sweep_ms": sweep_ms, "terms": terms,
+                "peak_source": "measured in this run: fp64 = msurf_microbench(0) non-FMA DADD/DMUL issue rate "
+                               "(MEASURED_PEAKS.json has no FP64 entry); atomic = msurf_red_replay of this "
+                               "workload's own RED trace"})
+    return out
 
 
 def diag_counters(batch):
@@ -285,22 +355,48 @@ def diag_counters(batch):
     return ctr
 
 
-def run_ours(args, rank, world):
+def timed_steps(pipe, args, flush, dev_index, barrier):
+    """W untimed steps, then K timed steps (CUDA events around each stage,
+    L2 flushed between steps), clocks sampled during the timed region."""
+    import torch
+
+    for _ in range(args.warmup):
+        pipe.run()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev_index)
+    clocks.start()
+    step_ms, sweep_ms = [], []
+    barrier()
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        flush.fill_(1)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        pipe.run(events=ev)
+        torch.cuda.synchronize()
+        step_ms.append(ev[0].elapsed_time(ev[3]))
+        sweep_ms.append(ev[1].elapsed_time(ev[2]))
+    barrier()
+    torch.cuda.synchronize()
+    return step_ms, sweep_ms, clocks.stop()
+
+
+def measure_surface(cfg_id, args, rank, world, with_cpu):
+    """One single-surface config: device step (graphs, resident inputs),
+    roofline of the sweep, e2e through the public API, CPU baseline."""
     import numpy as np
     import torch
 
     import paper_2603_28160_b200 as ms
-    from paper_2603_28160_b200 import _native, sharded
+    from paper_2603_28160_b200 import configs, sharded
     from paper_2603_28160_b200.engine import SweepBatch
     from paper_2603_28160_b200.pipeline import SurfacePipeline
     from paper_2603_28160_b200.planner import plan as make_plan
+    from oracle import fsm_ext_oracle as xorc
 
     dist = torch.distributed
     local = _local_device()
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    group = None
-    cfg, ext, meta = workload(args.config)
+    cfg, ext, meta = configs.FACTORIES[cfg_id]()
     p = make_plan(cfg, ext)
     uncut = meta["uncut"]
     every = meta.get("profiles_every", 64)
@@ -311,98 +407,46 @@ def run_ours(args, rank, world):
         if not args.no_graph:
             pipe.capture()  # three CUDA graphs: fill | sweep | decode + reductions
     else:
-        pipe = sharded.StripPipeline(batch, every=every, uncut=uncut, group=group)
+        pipe = sharded.StripPipeline(batch, every=every, uncut=uncut)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    def step(events):
-        # sync-free launch sequence (N>1: plus three tiny all-reduces); the
-        # results are read back after the timed region
-        pipe.run(events=events)
-        return None
-
-    # warm-up
-    for _ in range(args.warmup):
-        step(None)
-    torch.cuda.synchronize()
-    ctr, machined = batch.counters()
-
-    # timed region: K steps, each bracketed by CUDA events; L2 flushed between
-    clocks = ClockSampler(local)
-    clocks.start()
-    step_ms, sweep_ms = [], []
-    launches = 0
-    barrier()
-    torch.cuda.synchronize()
-    for _ in range(args.steps):
-        flush.fill_(1)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        e_end = torch.cuda.Event(enable_timing=True)
-        out = step(ev)
-        e_end.record()
-        torch.cuda.synchronize()
-        step_ms.append(ev[0].elapsed_time(e_end))
-        sweep_ms.append(ev[1].elapsed_time(ev[2]))
-        launches += pipe.launches_per_run
-    barrier()
-    torch.cuda.synchronize()
-    clk = clocks.stop()
+    step_ms, sweep_ms, clk = timed_steps(pipe, args, flush, local, barrier)
+    launches = pipe.launches_per_run * args.steps
     ctr, machined = batch.counters()
     am, prs = pipe.collect()[0] if world == 1 else pipe.collect()
     dctr = diag_counters(batch)
+    replay = red_replay(batch) if not args.no_replay else None
 
     tot = torch.tensor([sum(step_ms), sum(sweep_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     ms_per_step = float(tot[0]) / args.steps
-    sweep_ms_avg = float(tot[1]) / args.steps
+    sweep_avg = float(tot[1]) / args.steps
     p_total = p.trajectory_points
     value = p_total / (ms_per_step * 1e-3)
 
-    # ---- roofline of the dominant kernel (the sweep), this rank's launch
     mode = p.mode
-    evald = int(ctr[0][1])
-    live = int(ctr[0][0])
-    engaged = int(ctr[0][4])
+    evald, live, engaged = int(ctr[0][1]), int(ctr[0][0]), int(ctr[0][4])
     flops = FLOPS_PER_POINT[mode] * evald + FLOPS_PER_ROW * live
-    # SURVEY §8(d) definition: P_eng = points of rows whose whole-tooth 2-D box
-    # meets the window (row-level cull); the kernel's chunk-level cull skips
-    # part of that work, so this fraction also credits the finer cull
-    lib = _native.lib()
-    import ctypes
-
-    r = ctypes.c_double(0.0)
-    _native.check(lib.msurf_microbench(0, ctypes.byref(r)))
-    fp64_peak = r.value
-    atom = {}
-    for w in (3, 4):
-        _native.check(lib.msurf_microbench(w, ctypes.byref(r)))
-        atom[w] = r.value
-    achieved = flops / (sweep_ms_avg * 1e-3)
-    roofline = {
-        "bound": "fp64", "achieved": achieved / 1e12, "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
-        "frac": achieved / fp64_peak,
-        "traffic": profiled_traffic(meta["name"]),
-        "kernel": "sweep_kernel<MODE>", "sweep_ms": sweep_ms_avg,
-        "peak_source": "measured in this run: msurf_microbench(0), non-FMA DADD/DMUL issue rate "
-                       "(MEASURED_PEAKS.json has no FP64 entry)",
-        "flops_per_launch": flops,
+    atomics = int(dctr[0][3])
+    roof = roofline(flops, atomics, sweep_avg, replay, "sweep_kernel<MODE>")
+    roof.update({
+        "traffic": profiled_traffic(meta["name"]), "flops_per_launch": flops,
         "flops_model": f"{FLOPS_PER_POINT[mode]} x points_evaluated + {FLOPS_PER_ROW} x live rows",
         "survey_def": {"note": "SURVEY 8(d) unit count P_eng: every point of each row whose whole-tooth box "
                                "meets the window; the kernel's chunk cull evaluates only points_evaluated of "
-                               "them, which is what frac is computed on",
+                               "them, which is what the fp64 term is computed on",
                        "P_eng": engaged * p.points, "engaged_rows": engaged},
-        "points_evaluated": evald, "live_rows": live, "deposits": int(dctr[0][2]),
-        "atomics": int(dctr[0][3]),
+        "points_evaluated": evald, "live_rows": live, "deposits": int(dctr[0][2]), "atomics": atomics,
         "diag_note": "deposits/atomics from one extra untimed launch with MSURF_SWEEP_DIAG",
-        "atomic_rate_per_s": int(dctr[0][3]) / (sweep_ms_avg * 1e-3),
-        "terms": roofline_terms(flops, fp64_peak, int(dctr[0][3]), atom, sweep_ms_avg),
-        "hbm": {"bytes_per_step": 24 * (p.grid.m + 1) * (j_hi - j_lo + 1) + 8 * int(dctr[0][3]),
+        "hbm": {"bytes_per_step": 24 * (p.grid.m + 1) * (j_hi - j_lo + 1),
                 "peak_gbs": measured_peaks().get("hbm_gbs")},
-    }
+    })
+    del pipe, flush, batch
 
     # ---- e2e through the public API with host buffers
     e2e_ms = []
@@ -413,22 +457,22 @@ def run_ours(args, rank, world):
         t0 = time.perf_counter()
         if world == 1:
             res = ms.simulate(cfg, ext)
-            am = ms.areal_metrics(res.field, uncut=uncut)
-            prs = ms.profile_roughness(res.field, every=every, uncut=uncut)
+            am2 = ms.areal_metrics(res.field, uncut=uncut)
+            prs2 = ms.profile_roughness(res.field, every=every, uncut=uncut)
             hh = res.field.heights
-            nbytes = hh.nbytes
+            h2d = res._launch.batch.h2d_bytes
         else:
             sres = sharded.simulate_strip(cfg, ext, rank, world)
-            am = sharded.areal_metrics_strip(sres, uncut=uncut, group=group)
-            prs = sharded.profile_roughness_strip(sres, every=every, uncut=uncut, group=group)
+            am2 = sharded.areal_metrics_strip(sres, uncut=uncut)
+            prs2 = sharded.profile_roughness_strip(sres, every=every, uncut=uncut)
             hh = sres.heights.cpu().numpy()
-            nbytes = hh.nbytes
+            h2d = sres.batch.h2d_bytes
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             e2e_ms.append(dt * 1e3)
-        h2d = batch.h2d_bytes
-        d2h = nbytes + 8 * (9 + 8 * len(prs) + 5)
+        d2h = hh.nbytes + 8 * (9 + 8 * len(prs2) + 5)
+        del hh
     et = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
@@ -439,96 +483,78 @@ def run_ours(args, rank, world):
            if world == 1 else "sharded.simulate_strip + areal/profile all-reduce + strip read-back"}
 
     cpu = None
-    if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_sample(cfg, ext, p, target_s=args.cpu_seconds)
+    if with_cpu and world == 1 and rank == 0 and not args.no_cpu_baseline:
+        ocfg, oext, _ = oracle_workload(cfg_id)
+        cpu = cpu_sample(ocfg, oext, target_s=args.cpu_seconds)
+    xp = xorc.ext_plan(*oracle_workload(cfg_id)[:2])
+    assert xp.trajectory_points == p_total
+    ok_prs = [q for q in prs if not isinstance(q, Exception)]
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": describe_oracle(cfg_id, cfg, ext, meta, xp, world),
+        "surfaces_per_s": 1e3 / ms_per_step,
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches, "clocks": clk,
+        "metrics": {"Sa_um": am.sa_um, "Sq_um": am.sq_um, "Sz_um": am.sz_um, "Ssk": am.ssk,
+                    "Sku": am.sku, "cells": am.cell_count,
+                    "Ra_um_mean": float(np.mean([q.ra_um for q in ok_prs])) if ok_prs else None,
+                    "Rz_um_mean": float(np.mean([q.rz_um for q in ok_prs])) if ok_prs else None,
+                    "profiles": len(prs)},
+        "machined_cells_rank0": int(machined[0]),
+    }
 
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": describe(cfg, ext, meta, p, world),
-            "surfaces_per_s": 1e3 / ms_per_step,
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches, "clocks": clk,
-            "metrics": {"Sa_um": am.sa_um, "Sq_um": am.sq_um, "Sz_um": am.sz_um, "Ssk": am.ssk,
-                        "Sku": am.sku, "cells": am.cell_count,
-                        "Ra_um_mean": float(np.mean([q.ra_um for q in prs])),
-                        "Rz_um_mean": float(np.mean([q.rz_um for q in prs])), "profiles": len(prs)},
-            "machined_cells_rank0": int(machined[0]),
-        }
-        print(json.dumps(line), flush=True)
 
-
-def config3_workload(rank, world):
+def config3_plans(rank, world):
     """BASELINE configs[2]: 256 parameter sets from default_rng(0), uniform
     (dataset.uniform_sample), sharded by parameter set across ranks."""
     from paper_2603_28160_b200 import configs, sharded
     from paper_2603_28160_b200.dataset import ParameterRange, apply_sample, uniform_sample
-    from paper_2603_28160_b200.planner import plan as make_plan
+    from paper_2603_28160_b200.planner import plan_many
 
     base, ext, meta = configs.config3_base()
     ranges = [ParameterRange(n, lo, hi) for n, lo, hi in meta["ranges"]]
     samples = uniform_sample(ranges, meta["count"], meta["seed"])
     names = [r.name for r in ranges]
     all_cfgs = [apply_sample(base, ext, names, samples[i], meta["steps_per_rev"]) for i in range(meta["count"])]
-    sl = sharded.batch_slice(meta["count"], rank, world)
-    mine = all_cfgs[sl]
-    from paper_2603_28160_b200.planner import plan_many
-
+    mine = all_cfgs[sharded.batch_slice(meta["count"], rank, world)]
     plans = plan_many([c for c, _ in mine], [e for _, e in mine])
-    total_points = sum(p.trajectory_points for p in plan_many([c for c, _ in all_cfgs], [e for _, e in all_cfgs])) \
-        if world > 1 else sum(p.trajectory_points for p in plans)
-    return base, ext, meta, ranges, mine, plans, total_points
+    return meta, mine, plans
 
 
-def run_batch(args, rank, world):
-    """Batched dataset mode: every parameter set of this rank in ONE sweep
-    launch (+ fill/decode/reductions), value = all ranks' edge-point updates
-    / max-rank step time; surfaces/s alongside."""
-    import ctypes
-
+def measure_batch(args, rank, world, with_cpu):
+    """Batched dataset mode (config 3): every parameter set of this rank in
+    ONE sweep launch (+ fill/decode/reductions), value = all ranks' edge-point
+    updates / max-rank step time; surfaces/s alongside."""
     import numpy as np
     import torch
 
     import paper_2603_28160_b200 as ms
-    from paper_2603_28160_b200 import _native
     from paper_2603_28160_b200.engine import SweepBatch
     from paper_2603_28160_b200.pipeline import SurfacePipeline
 
     dist = torch.distributed
     local = _local_device()
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    base, ext, meta, ranges, mine, plans, total_points = config3_workload(rank, world)
+    meta, mine, plans = config3_plans(rank, world)
+    total_points, _ = config3_points()
     batch = SweepBatch([(p, 0, p.grid.n) for p in plans])
     pipe = SurfacePipeline(batch, every=None, uncut=meta["uncut"])
     if not args.no_graph:
         pipe.capture()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    for _ in range(args.warmup):
-        pipe.run()
-    torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
-    step_ms, sweep_ms = [], []
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    for _ in range(args.steps):
-        flush.fill_(1)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        pipe.run(events=ev)
-        torch.cuda.synchronize()
-        step_ms.append(ev[0].elapsed_time(ev[3]))
-        sweep_ms.append(ev[1].elapsed_time(ev[2]))
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clk = clocks.stop()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    step_ms, sweep_ms, clk = timed_steps(pipe, args, flush, local, barrier)
+    launches = pipe.launches_per_run * args.steps
     ctr, machined = batch.counters()
     res = pipe.collect()
     dctr = diag_counters(batch)
+    replay = red_replay(batch) if not args.no_replay else None
     tot = torch.tensor([sum(step_ms), sum(sweep_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
@@ -539,72 +565,121 @@ def run_batch(args, rank, world):
     npts = plans[0].points
     mode = plans[0].mode
     flops = FLOPS_PER_POINT[mode] * evald + FLOPS_PER_ROW * live
-    lib = _native.lib()
-    r = ctypes.c_double(0.0)
-    _native.check(lib.msurf_microbench(0, ctypes.byref(r)))
-    fp64_peak = r.value
-    achieved = flops / (sweep_avg * 1e-3)
-    atom = {}
-    for w in (3, 4):
-        _native.check(lib.msurf_microbench(w, ctypes.byref(r)))
-        atom[w] = r.value
-    roofline = {"bound": "fp64", "achieved": achieved / 1e12, "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
-                "frac": achieved / fp64_peak, "traffic": profiled_traffic(meta["name"]),
-                "kernel": "sweep_kernel<MODE>", "sweep_ms": sweep_avg,
-                "peak_source": "measured in this run: msurf_microbench(0), non-FMA DADD/DMUL issue rate",
-                "flops_per_launch": flops, "survey_def": {"P_eng": engaged * npts, "engaged_rows": engaged},
-                "points_evaluated": evald, "live_rows": live, "deposits": int(dctr[:, 2].sum()),
-                "atomics": int(dctr[:, 3].sum()),
-                "diag_note": "deposits/atomics from one extra untimed launch with MSURF_SWEEP_DIAG",
-                "terms": roofline_terms(flops, fp64_peak, int(dctr[:, 3].sum()), atom, sweep_avg)}
+    atomics = int(dctr[:, 3].sum())
+    roof = roofline(flops, atomics, sweep_avg, replay, "sweep_kernel<MODE> (listed, persistent)")
+    roof.update({"traffic": profiled_traffic(meta["name"]), "flops_per_launch": flops,
+                 "survey_def": {"P_eng": engaged * npts, "engaged_rows": engaged},
+                 "points_evaluated": evald, "live_rows": live, "deposits": int(dctr[:, 2].sum()),
+                 "atomics": atomics,
+                 "diag_note": "deposits/atomics from one extra untimed launch with MSURF_SWEEP_DIAG"})
+    del pipe, flush, batch
     # e2e: public batched API with host planning, one H2D, metrics + every height map read back
     e2e_ms = []
-    d2h = 0
-    names = [rg.name for rg in ranges]
+    d2h = h2d = 0
     for i in range(args.warmup + args.steps):
-        if world > 1:
-            dist.barrier()
+        barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         out = ms.simulate_batch([c for c, _ in mine], [e for _, e in mine])
-        mets = ms.areal_metrics_batch([o.field for o in out], uncut=meta["uncut"])
+        ms.areal_metrics_batch([o.field for o in out], uncut=meta["uncut"])
         d2h = 0
         for o in out:
             d2h += o.field.heights.nbytes
         torch.cuda.synchronize()
         if i >= args.warmup:
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        h2d = sum(b.h2d_bytes for b in {id(o._launch.batch): o._launch.batch for o in out}.values())
+        del out
     et = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
     e2e_step = float(et[0]) / args.steps
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        per = args.cpu_seconds / 4
-        rates = [cpu_sample(c, e, p, target_s=per)["value"] for (c, e), p in list(zip(mine, plans))[:4]]
-        cpu = {"value": float(np.mean(rates)), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-               "sample": "4 of the 256 parameter sets, 16 step windows each, oracle/fsm_ext_oracle.py, "
-                         "mean edge-point-update rate"}
+    if with_cpu and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_sample_batch(args.cpu_seconds)
+    ok = [m for m, _ in res if not isinstance(m, Exception)]
+    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config3 (BASELINE configs[2]): 256 parameter sets, batched",
+                       "sets": meta["count"], "sets_this_rank": len(plans), "grid_nodes": [512, 512],
+                       "spacing_mm": 0.004, "edge_points": npts, "steps_per_rev": meta["steps_per_rev"],
+                       "edge_point_updates_per_batch": total_points,
+                       "parallelism": f"parameter-set shards x{world}" if world > 1 else "single GPU",
+                       "l2": "flushed between timed steps (256 MiB write)"},
+            "surfaces_per_s": meta["count"] / (ms_step * 1e-3),
+            "roofline": roof, "cpu_baseline": cpu,
+            "e2e": {"value": total_points / (e2e_step * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "ms_per_step": e2e_step, "steps_ms": [round(x, 3) for x in e2e_ms],
+                    "api": "simulate_batch + areal_metrics_batch + heights"},
+            "gpu_launches": launches, "clocks": clk,
+            "metrics": {"surfaces_ok": len(ok), "Sa_um_mean": float(np.mean([m.sa_um for m in ok])) if ok else None}}
+
+
+def compact(line):
+    """The per-config summary carried inside the headline line."""
+    r = line["roofline"]
+    return {"workload": line["config"]["workload"], "value": line["value"], "unit": line["unit"],
+            "ms_per_step": line["ms_per_step"], "surfaces_per_s": line["surfaces_per_s"],
+            "e2e": {k: line["e2e"][k] for k in ("value", "unit", "ms_per_step", "h2d_bytes_per_step",
+                                                 "d2h_bytes_per_step")},
+            "roofline": {k: r[k] for k in ("bound", "achieved", "peak", "unit", "frac", "sweep_ms", "traffic",
+                                           "terms")},
+            "cpu_baseline": line["cpu_baseline"], "gpu_launches": line["gpu_launches"],
+            "clocks": line["clocks"], "metrics": line["metrics"]}
+
+
+def run_ours(args, rank, world):
+    import torch
+
+    def measure(cfg_id, with_cpu=True):
+        if cfg_id == 3:
+            out = measure_batch(args, rank, world, with_cpu)
+        else:
+            out = measure_surface(cfg_id, args, rank, world, with_cpu)
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        return out
+
+    line = measure(args.config)
+    if world == 1 and not args.no_per_config:
+        line["per_config"] = {}
+        for k in sorted(BASELINE_INDEX):
+            if k != args.config:
+                line["per_config"][f"config{k}"] = compact(measure(k))
+        line["per_config_note"] = ("the same measurement (device step, sweep roofline, e2e through the public API, "
+                                   "CPU baseline) for the other BASELINE configs; the headline is the largest "
+                                   "single-GPU configuration")
     if rank == 0:
-        ok = [m for m, _ in res if not isinstance(m, Exception)]
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": "config3 (BASELINE configs[2]): 256 parameter sets, batched",
-                           "sets": meta["count"], "sets_this_rank": len(plans), "grid_nodes": [512, 512],
-                           "spacing_mm": 0.004, "edge_points": npts, "steps_per_rev": meta["steps_per_rev"],
-                           "edge_point_updates_per_batch": total_points,
-                           "parallelism": f"parameter-set shards x{world}" if world > 1 else "single GPU",
-                           "l2": "flushed between timed steps (256 MiB write)"},
-                "surfaces_per_s": meta["count"] / (ms_step * 1e-3),
-                "roofline": roofline, "cpu_baseline": cpu,
-                "e2e": {"value": total_points / (e2e_step * 1e-3), "unit": UNIT,
-                        "h2d_bytes_per_step": int(batch.h2d_bytes), "d2h_bytes_per_step": int(d2h),
-                        "ms_per_step": e2e_step, "steps_ms": [round(x, 3) for x in e2e_ms],
-                        "api": "simulate_batch + areal_metrics_batch + heights"},
-                "gpu_launches": pipe.launches_per_run * args.steps, "clocks": clk,
-                "metrics": {"surfaces_ok": len(ok), "Sa_um_mean": float(np.mean([m.sa_um for m in ok])) if ok else None}}
         print(json.dumps(line), flush=True)
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` outside torchrun: re-launch under
+    torch.distributed.run with N ranks (one per GPU, NCCL), after checking
+    that N GPUs are visible."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} requested but only {have} CUDA device(s) visible"}),
+              flush=True)
+        return 2
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    print("+ " + " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -612,30 +687,41 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true", help="headline config only")
+    ap.add_argument("--no-replay", action="store_true", help="skip the RED-trace replay (atomic roof)")
     ap.add_argument("--no-graph", action="store_true", help="launch the step without CUDA graphs")
     args = ap.parse_args()
+    if args.config not in BASELINE_INDEX:
+        raise SystemExit(f"--config {args.config}: choose one of 1..5")
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(spawn_ranks(args))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
         import torch
         import torch.distributed as dist
 
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(_local_device())
         # MSURF_DIST_BACKEND=gloo lets the N>1 path be exercised with several
         # ranks on one GPU (functional check only; NCCL needs one GPU per rank)
         dist.init_process_group(os.environ.get("MSURF_DIST_BACKEND", "nccl"))
+    else:
+        import torch
+
+        torch.cuda.set_device(_local_device())
     try:
-        if args.config == 3:
-            run_batch(args, rank, world)
-        else:
-            run_ours(args, rank, world)
+        run_ours(args, rank, world)
     finally:
         if world > 1:
             import torch.distributed as dist

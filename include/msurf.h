@@ -20,7 +20,7 @@
 extern "C" {
 #endif
 
-#define MSURF_ABI_VERSION 4
+#define MSURF_ABI_VERSION 5
 
 /* kinematics mode of a sweep launch (uniform across the jobs of one launch) */
 #define MSURF_MODE_REF 0      /* reference composite-matrix order, engine.py:257-296 */
@@ -30,6 +30,10 @@ extern "C" {
  * MSURF_CTR_DEPOSITS / MSURF_CTR_ATOMICS (two extra integer ops per point;
  * without it those two counters stay zero) */
 #define MSURF_SWEEP_DIAG 0x100
+/* OR-ed into the mode: the diagnostics counters plus a trace of every
+ * warp-wide RED.MIN of the main point loops into the buffer armed with
+ * msurf_trace_arm (roofline measurement only; much slower) */
+#define MSURF_SWEEP_TRACE 0x200
 
 #define MSURF_CTR_LIVE_ROWS 0  /* (step, tooth, pass) rows with >= 1 chunk surviving the 2-D cull */
 #define MSURF_CTR_EVAL 1       /* edge points evaluated (points of surviving 32-point chunks)    */
@@ -246,6 +250,19 @@ int msurf_graymap_pixels(const double* h, int64_t ld, int64_t i_lo, int64_t j_lo
  * consecutive keys at a random base in 32 MiB (the sweep's access shape)
  * (ops/s). Synchronous; creates and destroys its own scratch. */
 int msurf_microbench(int32_t which, double* result);
+
+/* RED roof of a workload (roofline measurement, not on the product path).
+ * msurf_trace_arm: the next MSURF_SWEEP_TRACE sweeps append one record per
+ * warp-wide RED.MIN (32 x u32 key offsets from `base`, 0xffffffff = lane
+ * inactive) to `trace` (device, room for cap_records records), counting
+ * records issued and active lanes in counters[0..1] (device, caller-zeroed;
+ * records beyond the capacity are counted, not stored).
+ * msurf_red_replay: replay n_records records as RED.MIN on keys_base (no
+ * fp64 work), warps taking records in trace order; read_only=1 streams the
+ * same trace without the REDs (the trace-read floor). `sink`: 4 device bytes. */
+int msurf_trace_arm(uint32_t* trace, int64_t cap_records, unsigned long long* counters, const uint64_t* base);
+int msurf_red_replay(const uint32_t* trace, int64_t n_records, uint64_t* keys_base, int32_t read_only,
+                     void* sink, void* stream);
 
 /* Small-result readback without the copy engines: msurf_host_alloc returns
  * page-locked host memory mapped into the device address space (NULL on

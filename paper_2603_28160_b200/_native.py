@@ -18,9 +18,10 @@ from .errors import MillsurfError, NativeUnavailableError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MSURF_LIB") or os.path.join(_HERE, "libmsurf.so")
-ABI_VERSION = 4
+ABI_VERSION = 5
 NUM_CTRS = 5
 SWEEP_DIAG = 0x100  # MSURF_SWEEP_DIAG: count deposits/atomics per point
+SWEEP_TRACE = 0x200  # MSURF_SWEEP_TRACE: diagnostics + a trace of every RED.MIN (roofline only)
 RED_BLOCKS = 1024
 WORK_DOUBLES = RED_BLOCKS * 10  # MSURF_WORK_DOUBLES: reduction scratch per surface
 
@@ -94,6 +95,8 @@ EXPORTS = {
     "msurf_graymap_pixels": (ctypes.c_int, [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,
                                             c_void_p, c_void_p, c_void_p]),
     "msurf_microbench": (ctypes.c_int, [c_int32, ctypes.POINTER(c_double)]),
+    "msurf_trace_arm": (ctypes.c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
+    "msurf_red_replay": (ctypes.c_int, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p]),
     "msurf_host_alloc": (c_void_p, [c_int64]),
     "msurf_host_free": (ctypes.c_int, [c_void_p]),
     "msurf_readback": (ctypes.c_int, [c_void_p, c_void_p, c_int64, c_void_p]),

@@ -141,6 +141,28 @@ __device__ __forceinline__ unsigned warp_sum_u(unsigned v) {
   return v;
 }
 
+// RED trace (MSURF_SWEEP_TRACE, roofline only): every warp-wide RED.MIN of
+// the main point loops appends one 32-entry record of key offsets from
+// g_trace_base (0xffffffff = lane inactive), in issue order across the GPU,
+// for msurf_red_replay. The near-boundary fix-up REDs (~1e-9 of points) are
+// not traced.
+__device__ unsigned* g_trace;
+__device__ unsigned long long g_trace_cap;       // records
+__device__ unsigned long long* g_trace_ctr;      // [0] records issued, [1] active lanes
+__device__ const unsigned long long* g_trace_base;
+
+__device__ __forceinline__ void trace_red(const unsigned long long* p, bool pred, int lane) {
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  if (!m) return;
+  unsigned long long slot = 0;
+  if (lane == 0) {
+    slot = atomicAdd(g_trace_ctr, 1ull);
+    atomicAdd(g_trace_ctr + 1, (unsigned long long)__popc(m));
+  }
+  slot = __shfl_sync(0xffffffffu, slot, 0);
+  if (slot < g_trace_cap) g_trace[slot * 32 + lane] = pred ? (unsigned)(p - g_trace_base) : 0xffffffffu;
+}
+
 // 2-D box test of one tool-frame box [xl xh yl yh zl zh] rotated by (c, s),
 // after the lead tilt, in fp32 against a window given by its centre
 // offsets (ox, oy = tool offset - window centre) and half-widths (hx, hy)
@@ -352,7 +374,7 @@ __device__ __forceinline__ bool tile_may_hit(const msurf_job& J, int pass, int t
 }
 
 #pragma nv_diag_suppress 177  // tile_done is unused in the ONE instantiations
-template <int MODE, bool DIAG, bool ONE, int TILE, int NTHR>
+template <int MODE, int DIAG, bool ONE, int TILE, int NTHR>
 __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
     sweep_kernel(const msurf_job* __restrict__ jobs, int n_jobs,
                  const int64_t* __restrict__ prefix, int mask_words, const __grid_constant__ msurf_job jp,
@@ -715,6 +737,10 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
         }
         red_min_u64_if(keys + idx_a, (unsigned long long)ea.key, dep_a);
         red_min_u64_if(keys + idx_b, (unsigned long long)eb.key, dep_b);
+        if (DIAG == 2) {
+          trace_red(keys + idx_a, dep_a, lane);
+          trace_red(keys + idx_b, dep_b, lane);
+        }
       }
       if (__builtin_expect(__any_sync(0xffffffffu, anynear), 0)) {
         for (int k = 0; k < p_end; ++k) {
@@ -809,6 +835,10 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
         }
         red_min_u64_if(keys + idx_a, (unsigned long long)ea.key, dep_a);
         red_min_u64_if(keys + idx_b, (unsigned long long)eb.key, dep_b);
+        if (DIAG == 2) {
+          trace_red(keys + idx_a, dep_a, lane);
+          trace_red(keys + idx_b, dep_b, lane);
+        }
       }
       if (__builtin_expect(__any_sync(0xffffffffu, anynear), 0)) {
         for (int k = 0; k < p_end; ++k) {
@@ -1423,12 +1453,47 @@ __global__ void mb_atomic_kernel(unsigned long long* buf, long long mask, int it
   }
 }
 
+// RED roof of a workload: replay its traced RED.MIN stream (records in issue
+// order; warp w takes records w, w + W, ... so the records in flight stay a
+// narrow window of the trace, as the sweep's were) with no fp64 work. The
+// value decreases along the trace, so most REDs lower their key, as the
+// sweep's do. read_only: the same trace traffic with the REDs replaced by a
+// register reduction (the trace-streaming floor).
+template <bool READ_ONLY>
+__global__ void __launch_bounds__(256)
+    red_replay_kernel(const unsigned* __restrict__ trace, long long n_rec, unsigned long long* keys, unsigned* sink) {
+  const int lane = threadIdx.x & 31;
+  const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  unsigned acc = 0;
+  // one replayed warp instruction per record, lane l = the record's lane l (the
+  // sweep's own address grouping); four records in flight per warp
+  for (long long r0 = w0; r0 < n_rec; r0 += 4 * nw) {
+    unsigned v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long r = r0 + u * nw;
+      v[u] = r < n_rec ? __ldcs(trace + r * 32 + lane) : ~0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (READ_ONLY) {
+        acc ^= v[u];
+      } else if (v[u] != ~0u) {
+        const long long r = r0 + u * nw;
+        red_min_u64(keys + v[u], 0x8000000000000000ull | ((unsigned long long)(n_rec - r) << 16) | lane);
+      }
+    }
+  }
+  if (READ_ONLY && acc == 0x9e3779b9u) sink[0] = acc;
+}
+
 // smem of one sweep CTA: transforms + masks by thread + masks by slot
 inline size_t sweep_smem(int tile, int mask_words) {
   return (size_t)tile * 8 * sizeof(double) + (size_t)2 * tile * mask_words * sizeof(uint64_t);
 }
 
-template <int MODE, bool DIAG, bool ONE, int TILE, int NTHR>
+template <int MODE, int DIAG, bool ONE, int TILE, int NTHR>
 cudaError_t launch_shape(int64_t n_tiles, cudaStream_t st, const msurf_job* jobs, int n_jobs, const int64_t* prefix,
                          int mask_words, const msurf_job& job, unsigned long long* list, unsigned* count) {
   auto kern = sweep_kernel<MODE, DIAG, ONE, TILE, NTHR>;
@@ -1460,7 +1525,7 @@ inline int64_t job_tiles(const msurf_job& j, int tile) {
   return (int64_t)j.passes * j.teeth * ((j.step_hi - j.step_lo + tile - 1) / tile);
 }
 
-template <int MODE, bool DIAG>
+template <int MODE, int DIAG>
 cudaError_t launch_sweep(int64_t n_tiles, cudaStream_t st, const msurf_job* jobs, int n_jobs,
                          const int64_t* prefix, int mask_words, const msurf_job* one, unsigned long long* list,
                          unsigned* count) {
@@ -1571,13 +1636,15 @@ static int sweep_impl(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
   const bool diag = (mode & MSURF_SWEEP_DIAG) != 0;
+  const bool trace = (mode & MSURF_SWEEP_TRACE) != 0;
   // scratch: [0, 8) tile count and work cursor, then the tile list (8 bytes per tile)
   unsigned* count = static_cast<unsigned*>(scratch);
   unsigned long long* list = scratch ? static_cast<unsigned long long*>(scratch) + 1 : nullptr;
 #define MSURF_LAUNCH(M)                                                                                   \
-  e = diag ? launch_sweep<M, true>(n_tiles, st, jobs, n_jobs, tile_prefix, mask_words, one, list, count)  \
-           : launch_sweep<M, false>(n_tiles, st, jobs, n_jobs, tile_prefix, mask_words, one, list, count)
-  switch (mode & ~MSURF_SWEEP_DIAG) {
+  e = trace ? launch_sweep<M, 2>(n_tiles, st, jobs, n_jobs, tile_prefix, mask_words, one, list, count)   \
+      : diag  ? launch_sweep<M, 1>(n_tiles, st, jobs, n_jobs, tile_prefix, mask_words, one, list, count)   \
+              : launch_sweep<M, 0>(n_tiles, st, jobs, n_jobs, tile_prefix, mask_words, one, list, count)
+  switch (mode & ~(MSURF_SWEEP_DIAG | MSURF_SWEEP_TRACE)) {
     case MSURF_MODE_REF: MSURF_LAUNCH(MSURF_MODE_REF); break;
     case MSURF_MODE_EXT: MSURF_LAUNCH(MSURF_MODE_EXT); break;
     case MSURF_MODE_EXT_TILT: MSURF_LAUNCH(MSURF_MODE_EXT_TILT); break;
@@ -1599,6 +1666,35 @@ int msurf_sweep(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile_prefi
 int msurf_sweep_job(const msurf_job* job, int32_t mode, int32_t max_points, void* stream) {
   if (!job || max_points < 1) return set_err("msurf_sweep_job: bad arguments");
   return sweep_impl(nullptr, 1, nullptr, 0, mode, max_points, stream, job, nullptr);
+}
+
+int msurf_trace_arm(uint32_t* trace, int64_t cap_records, unsigned long long* counters, const uint64_t* base) {
+  if ((cap_records > 0 && !trace) || cap_records < 0 || !counters || !base)
+    return set_err("msurf_trace_arm: bad arguments");
+  unsigned long long cap = (unsigned long long)cap_records;
+  cudaError_t e = cudaMemcpyToSymbol(g_trace, &trace, sizeof(trace));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_trace_cap, &cap, sizeof(cap));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_trace_ctr, &counters, sizeof(counters));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_trace_base, &base, sizeof(base));
+  if (e != cudaSuccess) return set_err(std::string("msurf_trace_arm: ") + cudaGetErrorString(e));
+  return 0;
+}
+
+int msurf_red_replay(const uint32_t* trace, int64_t n_records, uint64_t* keys_base, int32_t read_only,
+                     void* sink, void* stream) {
+  if (n_records < 0 || (n_records > 0 && (!trace || !keys_base || !sink)))
+    return set_err("msurf_red_replay: bad arguments");
+  if (n_records == 0) return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned blocks = (unsigned)sms * 8;  // 64 warps per SM
+  auto* k = reinterpret_cast<unsigned long long*>(keys_base);
+  if (read_only)
+    red_replay_kernel<true><<<blocks, 256, 0, (cudaStream_t)stream>>>(trace, n_records, k, (unsigned*)sink);
+  else
+    red_replay_kernel<false><<<blocks, 256, 0, (cudaStream_t)stream>>>(trace, n_records, k, (unsigned*)sink);
+  return check_launch("red_replay_kernel");
 }
 
 int msurf_decode(uint64_t* keys, int64_t count, int32_t n_surf, const double* sentinel,

@@ -375,7 +375,7 @@ class SweepBatch:
         """One msurf_sweep launch per kinematics mode present in the batch."""
         lib, base = self.lib, self.base
         for g, (mode, idx, job_off, pre_off, n_tiles, max_pts) in enumerate(self.group_meta):
-            flag = _native.SWEEP_DIAG if self.diagnostics else 0
+            flag = self._sweep_flag()
             if self.group_per_job[g]:
                 # one job, or the L2 sub-strips of a large surface: one launch per job
                 # with the descriptor passed by value (constant-bank operands)
@@ -386,6 +386,59 @@ class SweepBatch:
                 continue
             _native.check(lib.msurf_sweep(base + job_off, len(idx), base + pre_off, n_tiles, mode | flag,
                                           max_pts, self.sweep_scratch.data_ptr(), sp))
+
+    def _sweep_flag(self) -> int:
+        if self.diagnostics == "trace":
+            return _native.SWEEP_TRACE
+        return _native.SWEEP_DIAG if self.diagnostics else 0
+
+    def red_replay(self, reps: int = 3, cap_bytes: int = 24 << 30):
+        """Roofline helper (bench.py; not on the product path): trace every
+        RED.MIN of one sweep of this batch (MSURF_SWEEP_TRACE launch), then
+        replay the trace alone (msurf_red_replay) on freshly filled keys, and
+        stream it once more without the REDs. Returns a dict with the active
+        lanes replayed, the median replay and trace-read-only seconds, and
+        whether the trace was truncated to ``cap_bytes`` (then the replay
+        covers the first records in issue order); None when the surfaces'
+        keys do not share one buffer."""
+        torch, lib = self.torch, self.lib
+        if self.strip_keys is not None and any(s.n_strips == 1 for s in self.surfs):
+            return None
+        base = self.strip_keys if self.strip_keys is not None else self.keys
+        free, _ = torch.cuda.mem_get_info(self.dev)
+        cap = int(min(cap_bytes, free // 2)) // 128
+        trace = torch.empty(max(cap, 1) * 32, dtype=torch.int32, device=self.dev)
+        ctr = torch.zeros(2, dtype=torch.int64, device=self.dev)
+        sink = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        _native.check(lib.msurf_trace_arm(trace.data_ptr(), cap, ctr.data_ptr(), base.data_ptr()))
+        prev, self.diagnostics = self.diagnostics, "trace"
+        try:
+            self.launch()
+        finally:
+            self.diagnostics = prev
+        torch.cuda.synchronize(self.dev)
+        issued, lanes = (int(v) for v in ctr.cpu())
+        n_rec = min(issued, cap)
+        truncated = issued > cap
+        if truncated:
+            lanes = int(torch.count_nonzero(trace[: n_rec * 32] != -1))
+        sp = _native.stream_ptr()
+        times = {0: [], 1: []}
+        for _ in range(reps):
+            for ro in (0, 1):
+                self.launch_fill(sp)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                _native.check(lib.msurf_red_replay(trace.data_ptr(), n_rec, base.data_ptr(), ro,
+                                                   sink.data_ptr(), sp))
+                e1.record()
+                torch.cuda.synchronize(self.dev)
+                times[ro].append(e0.elapsed_time(e1) * 1e-3)
+        del trace
+        torch.cuda.empty_cache()
+        return {"lanes": lanes, "records": n_rec, "records_issued": issued, "truncated": truncated,
+                "t_replay_s": sorted(times[0])[len(times[0]) // 2],
+                "t_read_s": sorted(times[1])[len(times[1]) // 2]}
 
     def launch_decode(self, sp: int) -> None:
         """Keys -> fp64 heights in place, machined-cell counts."""
@@ -448,7 +501,7 @@ class SweepBatch:
             ev[0].record()
         self.launch_fill(sp)
         mode, jidx, _, _, _, max_pts = self.group_meta[0]
-        flag = _native.SWEEP_DIAG if self.diagnostics else 0
+        flag = self._sweep_flag()
         ptr, sz = self.group_host_jobs[0].ctypes.data, _native.JOB_DTYPE.itemsize
         by_lo = {}
         for k, jn in enumerate(jidx):

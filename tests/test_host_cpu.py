@@ -344,3 +344,66 @@ def test_vectorised_profile_finish_equals_per_row():
         with pytest.raises(DomainError) as e2:
             R._finish_profile(bad[row], idx[row], uncut)
         assert str(e1.value) == str(e2.value)
+
+
+def _same_ext_plan(a, b):
+    import dataclasses
+
+    pa, pb = xorc.ext_plan(*a), xorc.ext_plan(*b)
+    for f in dataclasses.fields(pa):
+        va, vb = getattr(pa, f.name), getattr(pb, f.name)
+        if isinstance(va, np.ndarray):
+            assert np.array_equal(va, vb), f.name
+        else:
+            assert va == vb, (f.name, va, vb)
+    for part in ("tool", "process", "grid"):
+        for f in dataclasses.fields(getattr(a[0], part)):
+            assert getattr(getattr(a[0], part), f.name) == getattr(getattr(b[0], part), f.name), (part, f.name)
+    for k in ("edge_point_count", "time_step_s", "span_s"):
+        assert getattr(a[0], k) == getattr(b[0], k), k
+
+
+def test_oracle_workloads_equal_product_configs():
+    """bench.py's reference arm builds its workloads from oracle/workloads.py
+    (no product import): they must equal paper_2603_28160_b200/configs.py,
+    including the derived kinematics and the oracle plan, for all five
+    BASELINE configs (all 256 config-3 sets)."""
+    from oracle import workloads as W
+    from paper_2603_28160_b200 import configs as C
+    from paper_2603_28160_b200.dataset import ParameterRange, apply_sample, uniform_sample
+
+    for k in (1, 2, 4, 5):
+        a, b = W.FACTORIES[k](), C.FACTORIES[k]()
+        _same_ext_plan(a[:2], b[:2])
+        assert a[2] == {kk: v for kk, v in b[2].items() if kk in a[2]}
+    sets, samples, meta = W.config3_sets()
+    base, ext, m2 = C.config3_base()
+    ranges = [ParameterRange(n, lo, hi) for n, lo, hi in m2["ranges"]]
+    assert np.array_equal(uniform_sample(ranges, m2["count"], m2["seed"]), samples)
+    names = [r.name for r in ranges]
+    for i in range(meta["count"]):
+        _same_ext_plan(sets[i], apply_sample(base, ext, names, samples[i], m2["steps_per_rev"]))
+
+
+def test_bench_reference_arm_imports_no_product_code(tmp_path):
+    """`bench.py --impl reference` (the driver's reference arm) runs only the
+    oracle: after a full run the product package was never imported and
+    libmsurf.so never mapped."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, json; sys.argv=['bench.py','--impl','reference','--config','1','--steps','1',"
+            "'--warmup','0','--cpu-seconds','0.5']; sys.path.insert(0, %r); import bench; bench.main(); "
+            "mods=[m for m in sys.modules if m.startswith('paper_2603_28160_b200')]; "
+            "maps=open('/proc/self/maps').read(); "
+            "print('CHECK', json.dumps({'mods': mods, 'lib': 'libmsurf' in maps}))" % root)
+    out = subprocess.run([sys.executable, "-c", code], cwd=tmp_path, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = next(l for l in out.stdout.splitlines() if l.startswith("{"))
+    import json
+
+    rec = json.loads(line)
+    assert rec["impl"] == "reference" and rec["value"] > 0 and rec["e2e"]["h2d_bytes_per_step"] == 0
+    chk = json.loads(out.stdout.split("CHECK ", 1)[1])
+    assert chk == {"mods": [], "lib": False}, chk

@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import threading
 from dataclasses import dataclass, field, replace
 
 import numpy as np
@@ -507,6 +508,9 @@ class SweepBatch:
         for k, jn in enumerate(jidx):
             by_lo.setdefault(self.jobs[jn][1], []).append(k)
         rows, w_all = s.plan.grid.m + 1, s.j_hi - s.j_lo + 1
+        covered = sum(len(by_lo.get(s.j_lo + s.col0[q], ())) for q in range(s.n_strips))
+        if covered != len(jidx):
+            raise ConfigError(f"launch_by_strip: {len(jidx) - covered} sweep jobs start at no strip boundary")
         for q in range(s.n_strips):
             for k in by_lo.get(s.j_lo + s.col0[q], ()):
                 if self.group_tiles[0][k]:
@@ -586,7 +590,38 @@ def simulate(config: SimulationConfig, extensions: Extensions | None = None, *,
     return _launch_results([p], trig, diagnostics, prefetch=True)[0]
 
 
-_INFLIGHT = []  # (event, pinned buffer) of raw strip D2H copies still running
+class _Inflight:
+    """Pinned host buffers that raw strip D2H copies (msurf_copy2d_d2h, not
+    visible to torch's pinned-memory cache) may still be writing: an entry is
+    registered BEFORE its first copy is enqueued and released only once its
+    completion event has been recorded and has passed, so the buffer cannot
+    be recycled under a running DMA even if every field is dropped or the
+    launch raises partway. Pruned on every launch; guarded by a lock."""
+
+    _lock = threading.Lock()
+    _entries = []  # [event | None, buffer]; event None = copies still being enqueued
+
+    @classmethod
+    def register(cls, buf):
+        ent = [None, buf]
+        with cls._lock:
+            cls._prune_locked()
+            cls._entries.append(ent)
+        return ent
+
+    @classmethod
+    def seal(cls, ent, event):
+        with cls._lock:
+            ent[0] = event
+
+    @classmethod
+    def prune(cls):
+        with cls._lock:
+            cls._prune_locked()
+
+    @classmethod
+    def _prune_locked(cls):
+        cls._entries[:] = [e for e in cls._entries if e[0] is None or not e[0].query()]
 _EVENT_POOL = {}  # device index -> timing events of released launches (cudaEventCreate costs ~10 us)
 
 
@@ -613,6 +648,7 @@ def _launch_results(plans, trig, diagnostics=False, prefetch=False):
     group's heights into one pinned buffer on a side stream, started right
     after the decode; each field's ``heights`` then only waits for it."""
     torch = _native.require_cuda()
+    _Inflight.prune()
     b = SweepBatch([(p, 0, p.grid.n) for p in plans], trig=trig, diagnostics=diagnostics)
     # e0/e3 time the launch (main_loop_seconds) and are pooled; the prefetch's
     # event is fresh: the fields keep it after the launch object is released
@@ -638,13 +674,17 @@ def _launch_results(plans, trig, diagnostics=False, prefetch=False):
             side.wait_event(e)
             _native.check(b.lib.msurf_copy2d_d2h(hp + c0 * 8, pitch, dp + c0 * 8, pitch, w * 8, rows, sptr))
 
-        b.launch_by_strip(strip_done, events=ev)
+        # the raw 2-D copies are invisible to torch's pinned-memory cache: the
+        # buffer stays referenced until they finish, even if every field is
+        # dropped or a launch below raises after some copies were enqueued
+        ent = _Inflight.register(host)
         done = torch.cuda.Event()
-        done.record(side)
+        try:
+            b.launch_by_strip(strip_done, events=ev)
+        finally:
+            done.record(side)
+            _Inflight.seal(ent, done)
         b.keys.record_stream(side)
-        # the raw 2-D copies are invisible to torch's pinned-memory cache: keep
-        # the buffer referenced until they finish even if every field is dropped
-        _INFLIGHT[:] = [x for x in _INFLIGHT if not x[0].query()] + [(done, host)]
         prefetch = False  # copies already enqueued
     else:
         b.launch(events=ev)

@@ -102,22 +102,13 @@ def _metrics_from_moments(st1, st2) -> ArealMetrics:
                         cell_count=int(n))
 
 
-class _Scratch:
-    """Per-device scratch for the reductions: ``n_work`` surfaces of work
-    partials (MSURF_WORK_DOUBLES each) followed by ``n_out`` x 16 outputs."""
-
-    _cache = {}
-
-    @classmethod
-    def get(cls, torch, device, n_work: int, n_out: int | None = None):
-        key = (device.index if device.index is not None else torch.cuda.current_device())
-        n_out = n_work if n_out is None else n_out
-        need = n_work * _native.WORK_DOUBLES + n_out * 16
-        t = cls._cache.get(key)
-        if t is None or t.numel() < need:
-            t = torch.empty(need, dtype=torch.float64, device=device)
-            cls._cache[key] = t
-        return t
+def _scratch(torch, device, n_work: int, n_out: int | None = None):
+    """Reduction scratch for ONE call: ``n_work`` surfaces of work partials
+    (MSURF_WORK_DOUBLES each) followed by ``n_out`` x 16 outputs, from the
+    caching allocator (stream-ordered reuse, so concurrent callers on any
+    streams or threads never share a buffer; ~80 KB per surface)."""
+    n_out = n_work if n_out is None else n_out
+    return torch.empty(n_work * _native.WORK_DOUBLES + n_out * 16, dtype=torch.float64, device=device)
 
 
 def _areal_enqueue(lib, h_dev, ld, n_surf, surf_stride, roi_box, sentinels_dev, exclude, work, out, sp,
@@ -152,7 +143,7 @@ def areal_moments_device(h_dev, ld, n_surf, surf_stride, roi_box, sentinels_dev,
     "moments": four sums) across ranks in place."""
     torch = _native.require_cuda()
     lib = _native.lib()
-    sc = _Scratch.get(torch, h_dev.device, n_surf)
+    sc = _scratch(torch, h_dev.device, n_surf)
     out = sc[n_surf * _native.WORK_DOUBLES:]
     _areal_enqueue(lib, h_dev, ld, n_surf, surf_stride, roi_box, sentinels_dev, exclude, sc.data_ptr(), out,
                    _native.stream_ptr(), allreduce)
@@ -202,7 +193,7 @@ def _areal_plane(field: HeightField, roi, uncut: str) -> ArealMetrics:
     lib = _native.lib()
     h = field.device_heights()
     sent = _field_sentinel(torch, field, h.device)
-    sc = _Scratch.get(torch, h.device, 1)
+    sc = _scratch(torch, h.device, 1)
     work = sc.data_ptr()
     out = sc[_native.WORK_DOUBLES:]
     rows, cols = i_hi - i_lo + 1, j_hi - j_lo + 1
@@ -287,7 +278,7 @@ def areal_metrics_batch(fields, roi=None, uncut: str = "raise"):
     for dev, rs in todo.items():
         n_work = max(runs[r][1] - runs[r][0] for r, _ in rs)
         n_out = sum(runs[r][1] - runs[r][0] for r, _ in rs)
-        sc = _Scratch.get(torch, dev, n_work, n_out)
+        sc = _scratch(torch, dev, n_work, n_out)
         outs = sc[n_work * _native.WORK_DOUBLES:]
         sp = _native.stream_ptr()
         pos, slots = 0, []

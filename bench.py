@@ -282,8 +282,10 @@ _PEAKS = {}
 
 
 def device_peaks():
-    """fp64 issue rate and the two synthetic RED.MIN rates (msurf_microbench),
-    measured once per process on this GPU."""
+    """Measured once per process on this GPU (msurf_microbench): 0 = fp64
+    DADD/DMUL issue rate; 3 / 4 = RED.MIN lanes/s, random addresses / one
+    256-byte run per warp instruction (32 MiB table); 32 + L = warp RED.MIN
+    instructions/s when each touches L distinct 128-byte lines."""
     if not _PEAKS:
         import ctypes
 
@@ -291,25 +293,26 @@ def device_peaks():
 
         lib = _native.lib()
         r = ctypes.c_double(0.0)
-        for w in (0, 3, 4):
+        for w in (0, 3, 4, *range(33, 65)):
             _native.check(lib.msurf_microbench(w, ctypes.byref(r)))
             _PEAKS[w] = r.value
     return _PEAKS
 
 
-def red_replay(batch, reps: int = 3):
-    """The RED roof of THIS workload: the sweep's own RED.MIN address stream
-    (captured by one untimed MSURF_SWEEP_TRACE launch) replayed with no fp64
-    work, in capture order, on freshly filled Z-map keys (msurf_red_replay,
-    SweepBatch.red_replay)."""
-    return batch.red_replay(reps=reps)
+def red_lines(batch):
+    """This workload's own RED.MIN stream, shaped: one traced launch
+    (MSURF_SWEEP_TRACE) histogrammed by distinct 128-byte lines per warp RED
+    instruction (SweepBatch.red_lines)."""
+    return batch.red_lines()
 
 
-def roofline(flops, atomics, sweep_ms, replay, kernel_name):
+def roofline(flops, atomics, sweep_ms, lines, kernel_name):
     """The north star's roofline = the slower of fp64 issue and atomic
-    traffic. t_fp64 = algorithmic fp64 ops / measured DADD/DMUL issue rate;
-    t_red = this workload's RED count / the rate its own RED stream reaches
-    when replayed alone (red_replay). ``bound`` is the larger term and
+    traffic. t_fp64 = algorithmic fp64 ops / the measured DADD/DMUL issue
+    rate. t_red = the sweep's own RED instructions, each priced at the
+    measured L2 RED.MIN instruction rate for its shape (distinct lines
+    touched, microbench 32 + L), summed over the traced histogram (scaled to
+    all records when the trace was truncated). ``bound`` is the larger term,
     ``frac`` = that term / the measured sweep time."""
     pk = device_peaks()
     t = sweep_ms * 1e-3
@@ -318,26 +321,30 @@ def roofline(flops, atomics, sweep_ms, replay, kernel_name):
              "red_synthetic_peaks_per_s": {"warp_run_32MiB": pk[4], "random_32MiB": pk[3]},
              "reds": atomics, "red_achieved_per_s": atomics / t}
     t_red = None
-    if replay is not None and replay["lanes"] > 0:
-        rate = replay["lanes"] / replay["t_replay_s"]
-        t_red = atomics / rate
-        terms.update({"t_red_ms": t_red * 1e3, "frac_red": t_red / t, "red_replay_rate_per_s": rate,
-                      "red_replay": replay,
-                      "t_trace_read_ms": replay["t_read_s"] * atomics / replay["lanes"] * 1e3,
-                      "red_replay_note": "the sweep's own RED.MIN address stream (one record per warp-wide RED, "
-                                         "issue order) replayed alone; includes streaming the 128 B/record trace, "
-                                         "whose read-only time is t_trace_read_ms"})
+    if lines is not None and lines["records"] > 0:
+        hist = lines["hist"]
+        t_cap = sum(hist[L] / pk[32 + L] for L in range(1, 33))
+        scale = lines["records_issued"] / lines["records"]
+        t_red = t_cap * scale
+        mean_lines = sum(L * hist[L] for L in range(33)) / max(1, sum(hist))
+        terms.update({"t_red_ms": t_red * 1e3, "frac_red": t_red / t,
+                      "red_records": lines["records_issued"], "red_lanes_traced": lines["lanes"],
+                      "red_trace_truncated": lines["truncated"], "mean_lines_per_red_instr": mean_lines,
+                      "red_lines_hist": hist,
+                      "red_instr_rate_by_lines_per_s": {L: pk[32 + L] for L in (1, 2, 4, 8, 16, 32)},
+                      "red_note": "every warp-wide RED.MIN of one sweep traced and priced at the measured "
+                                  "L2 RED.MIN instruction rate for its number of distinct 128-B lines"})
     bound = "fp64" if t_red is None or t_fp64 >= t_red else "atomic"
     if bound == "fp64":
         out = {"bound": "fp64", "achieved": flops / t / 1e12, "peak": pk[0] / 1e12, "unit": "TFLOP/s",
                "frac": t_fp64 / t}
     else:
         out = {"bound": "atomic", "achieved": atomics / t / 1e9, "peak": atomics / t_red / 1e9,
-               "unit": "G RED.MIN/s", "frac": t_red / t}
+               "unit": "G RED.MIN lanes/s", "frac": t_red / t}
     out.update({"kernel": kernel_name, "sweep_ms": sweep_ms, "terms": terms,
                 "peak_source": "measured in this run: fp64 = msurf_microbench(0) non-FMA DADD/DMUL issue rate "
-                               "(MEASURED_PEAKS.json has no FP64 entry); atomic = msurf_red_replay of this "
-                               "workload's own RED trace"})
+                               "(MEASURED_PEAKS.json has no FP64 entry); atomic = msurf_microbench(32+L) RED.MIN "
+                               "instruction rates applied to this workload's traced RED shapes"})
     return out
 
 
@@ -419,7 +426,7 @@ def measure_surface(cfg_id, args, rank, world, with_cpu):
     ctr, machined = batch.counters()
     am, prs = pipe.collect()[0] if world == 1 else pipe.collect()
     dctr = diag_counters(batch)
-    replay = red_replay(batch) if not args.no_replay else None
+    lines = red_lines(batch) if not args.no_red_trace else None
 
     tot = torch.tensor([sum(step_ms), sum(sweep_ms)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -433,7 +440,7 @@ def measure_surface(cfg_id, args, rank, world, with_cpu):
     evald, live, engaged = int(ctr[0][1]), int(ctr[0][0]), int(ctr[0][4])
     flops = FLOPS_PER_POINT[mode] * evald + FLOPS_PER_ROW * live
     atomics = int(dctr[0][3])
-    roof = roofline(flops, atomics, sweep_avg, replay, "sweep_kernel<MODE>")
+    roof = roofline(flops, atomics, sweep_avg, lines, "sweep_kernel<MODE>")
     roof.update({
         "traffic": profiled_traffic(meta["name"]), "flops_per_launch": flops,
         "flops_model": f"{FLOPS_PER_POINT[mode]} x points_evaluated + {FLOPS_PER_ROW} x live rows",
@@ -554,7 +561,7 @@ def measure_batch(args, rank, world, with_cpu):
     ctr, machined = batch.counters()
     res = pipe.collect()
     dctr = diag_counters(batch)
-    replay = red_replay(batch) if not args.no_replay else None
+    lines = red_lines(batch) if not args.no_red_trace else None
     tot = torch.tensor([sum(step_ms), sum(sweep_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
@@ -566,7 +573,7 @@ def measure_batch(args, rank, world, with_cpu):
     mode = plans[0].mode
     flops = FLOPS_PER_POINT[mode] * evald + FLOPS_PER_ROW * live
     atomics = int(dctr[:, 3].sum())
-    roof = roofline(flops, atomics, sweep_avg, replay, "sweep_kernel<MODE> (listed, persistent)")
+    roof = roofline(flops, atomics, sweep_avg, lines, "sweep_kernel<MODE> (listed, persistent)")
     roof.update({"traffic": profiled_traffic(meta["name"]), "flops_per_launch": flops,
                  "survey_def": {"P_eng": engaged * npts, "engaged_rows": engaged},
                  "points_evaluated": evald, "live_rows": live, "deposits": int(dctr[:, 2].sum()),
@@ -692,7 +699,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-per-config", action="store_true", help="headline config only")
-    ap.add_argument("--no-replay", action="store_true", help="skip the RED-trace replay (atomic roof)")
+    ap.add_argument("--no-red-trace", action="store_true", help="skip the RED trace (atomic roof term)")
     ap.add_argument("--no-graph", action="store_true", help="launch the step without CUDA graphs")
     args = ap.parse_args()
     if args.config not in BASELINE_INDEX:

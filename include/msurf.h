@@ -247,22 +247,23 @@ int msurf_graymap_pixels(const double* h, int64_t ld, int64_t i_lo, int64_t j_lo
  * which=2: 64-bit atomicMin (RED.MIN.64) to random addresses in a 128 MiB
  * table (~L2 size), which=3: the same in a 32 MiB (L2-resident) table,
  * which=4: RED.MIN.64 where each warp instruction covers one 256-byte run of
- * consecutive keys at a random base in 32 MiB (the sweep's access shape)
- * (ops/s). Synchronous; creates and destroys its own scratch. */
+ * consecutive keys at a random base in 32 MiB (ops/s);
+ * which=32+L (L = 1..32): warp RED.MIN.64 instructions/s when each touches L
+ * distinct random 128-byte lines of a 32 MiB table (lane l on line l % L). Synchronous; creates and destroys its own scratch. */
 int msurf_microbench(int32_t which, double* result);
 
 /* RED roof of a workload (roofline measurement, not on the product path).
  * msurf_trace_arm: the next MSURF_SWEEP_TRACE sweeps append one record per
- * warp-wide RED.MIN (32 x u32 key offsets from `base`, 0xffffffff = lane
- * inactive) to `trace` (device, room for cap_records records), counting
+ * warp-wide RED.MIN — 32 u32 key offsets from `base` (0xffffffff = lane
+ * inactive) — to `trace` (device, room for cap_records records), counting
  * records issued and active lanes in counters[0..1] (device, caller-zeroed;
  * records beyond the capacity are counted, not stored).
- * msurf_red_replay: replay n_records records as RED.MIN on keys_base (no
- * fp64 work), warps taking records in trace order; read_only=1 streams the
- * same trace without the REDs (the trace-read floor). `sink`: 4 device bytes. */
+ * msurf_red_lines: hist[L] += records touching L distinct 128-byte lines
+ * (hist: 33 device u64, caller-zeroed). With msurf_microbench(32 + L) (warp
+ * RED.MIN instructions/s of that shape) this prices the sweep's own RED
+ * stream at the L2 atomic throughput. */
 int msurf_trace_arm(uint32_t* trace, int64_t cap_records, unsigned long long* counters, const uint64_t* base);
-int msurf_red_replay(const uint32_t* trace, int64_t n_records, uint64_t* keys_base, int32_t read_only,
-                     void* sink, void* stream);
+int msurf_red_lines(const uint32_t* trace, int64_t n_records, unsigned long long* hist, void* stream);
 
 /* Small-result readback without the copy engines: msurf_host_alloc returns
  * page-locked host memory mapped into the device address space (NULL on

@@ -142,11 +142,13 @@ __device__ __forceinline__ unsigned warp_sum_u(unsigned v) {
 }
 
 // RED trace (MSURF_SWEEP_TRACE, roofline only): every warp-wide RED.MIN of
-// the main point loops appends one 32-entry record of key offsets from
-// g_trace_base (0xffffffff = lane inactive), in issue order across the GPU,
-// for msurf_red_replay. The near-boundary fix-up REDs (~1e-9 of points) are
-// not traced.
-__device__ unsigned* g_trace;
+// the main point loops appends one record of 32 key offsets from
+// g_trace_base (0xffffffff = lane inactive). msurf_red_lines histograms the
+// records by the number of distinct 128-byte lines they touch, which with the
+// per-shape RED.MIN rates of msurf_microbench(32 + L) gives the time the
+// sweep's own RED stream needs at the L2 atomic units' measured throughput.
+// The near-boundary fix-up REDs (~1e-9 of points) are not traced.
+__device__ unsigned* g_trace;                    // [cap][32] offsets
 __device__ unsigned long long g_trace_cap;       // records
 __device__ unsigned long long* g_trace_ctr;      // [0] records issued, [1] active lanes
 __device__ const unsigned long long* g_trace_base;
@@ -1445,6 +1447,26 @@ __global__ void mb_atomic_run_kernel(unsigned long long* buf, long long mask, in
   }
 }
 
+// RED.MIN.64 rate by shape: every warp instruction touches L distinct random
+// 128-byte lines of an L2-resident table, lane l on line l % L, key (l / L)
+// within it (L = 1: lanes 0-15 only, one key each); warp instructions/s.
+// Lanes of one line share a 32-bit LCG stream (one IMAD per RED), so the
+// loop issues ~6 instructions per RED and the L2 atomic units, not the
+// issue slots, set the rate.
+__global__ void mb_atomic_lines_kernel(unsigned long long* buf, unsigned mask_lines, int L, int iters) {
+  const int lane = threadIdx.x & 31;
+  const int grp = lane % L, pos = lane / L;
+  const bool on = pos < 16;
+  const unsigned wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  unsigned x = (wid * 2654435761u) ^ ((unsigned)(grp + 1) * 0x9e3779b9u);
+  unsigned long long* p = buf + pos;
+#pragma unroll 4
+  for (int i = 0; i < iters; ++i) {
+    x = x * 1664525u + 1013904223u;
+    if (on) red_min_u64(p + ((unsigned long long)((x >> 7) & mask_lines) << 4), (unsigned long long)(x | 1u));
+  }
+}
+
 __global__ void mb_atomic_kernel(unsigned long long* buf, long long mask, int iters) {
   unsigned long long x = (blockIdx.x * 1315423911ull) ^ (threadIdx.x * 2654435761ull) ^ 0x9e3779b97f4a7c15ull;
   for (int i = 0; i < iters; ++i) {
@@ -1453,39 +1475,28 @@ __global__ void mb_atomic_kernel(unsigned long long* buf, long long mask, int it
   }
 }
 
-// RED roof of a workload: replay its traced RED.MIN stream (records in issue
-// order; warp w takes records w, w + W, ... so the records in flight stay a
-// narrow window of the trace, as the sweep's were) with no fp64 work. The
-// value decreases along the trace, so most REDs lower their key, as the
-// sweep's do. read_only: the same trace traffic with the REDs replaced by a
-// register reduction (the trace-streaming floor).
-template <bool READ_ONLY>
+// distinct 128-byte lines per traced RED record -> hist[0..32] (one warp
+// per record, grid-stride)
 __global__ void __launch_bounds__(256)
-    red_replay_kernel(const unsigned* __restrict__ trace, long long n_rec, unsigned long long* keys, unsigned* sink) {
+    red_lines_kernel(const unsigned* __restrict__ trace, long long n_rec, unsigned long long* hist) {
+  __shared__ unsigned long long h[33];
+  for (int i = threadIdx.x; i < 33; i += blockDim.x) h[i] = 0;
+  __syncthreads();
   const int lane = threadIdx.x & 31;
-  const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  unsigned acc = 0;
-  // one replayed warp instruction per record, lane l = the record's lane l (the
-  // sweep's own address grouping); four records in flight per warp
-  for (long long r0 = w0; r0 < n_rec; r0 += 4 * nw) {
-    unsigned v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const long long r = r0 + u * nw;
-      v[u] = r < n_rec ? __ldcs(trace + r * 32 + lane) : ~0u;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (READ_ONLY) {
-        acc ^= v[u];
-      } else if (v[u] != ~0u) {
-        const long long r = r0 + u * nw;
-        red_min_u64(keys + v[u], 0x8000000000000000ull | ((unsigned long long)(n_rec - r) << 16) | lane);
-      }
-    }
+  for (long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; r < n_rec; r += nw) {
+    const unsigned off = __ldcs(trace + r * 32 + lane);
+    const bool on = off != ~0u;
+    const unsigned act = __ballot_sync(0xffffffffu, on);
+    const unsigned same = __match_any_sync(0xffffffffu, on ? (off >> 4) : 0xffffffffu);
+    // a lane opens a line if no lower active lane holds the same line
+    const bool first = on && ((same & act & ((1u << lane) - 1u)) == 0u);
+    const int lines = __popc(__ballot_sync(0xffffffffu, first));
+    if (lane == 0) atomicAdd(&h[lines], 1ull);
   }
-  if (READ_ONLY && acc == 0x9e3779b9u) sink[0] = acc;
+  __syncthreads();
+  for (int i = threadIdx.x; i < 33; i += blockDim.x)
+    if (h[i]) atomicAdd(hist + i, h[i]);
 }
 
 // smem of one sweep CTA: transforms + masks by thread + masks by slot
@@ -1680,21 +1691,14 @@ int msurf_trace_arm(uint32_t* trace, int64_t cap_records, unsigned long long* co
   return 0;
 }
 
-int msurf_red_replay(const uint32_t* trace, int64_t n_records, uint64_t* keys_base, int32_t read_only,
-                     void* sink, void* stream) {
-  if (n_records < 0 || (n_records > 0 && (!trace || !keys_base || !sink)))
-    return set_err("msurf_red_replay: bad arguments");
+int msurf_red_lines(const uint32_t* trace, int64_t n_records, unsigned long long* hist, void* stream) {
+  if (n_records < 0 || !hist || (n_records > 0 && !trace)) return set_err("msurf_red_lines: bad arguments");
   if (n_records == 0) return 0;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned blocks = (unsigned)sms * 8;  // 64 warps per SM
-  auto* k = reinterpret_cast<unsigned long long*>(keys_base);
-  if (read_only)
-    red_replay_kernel<true><<<blocks, 256, 0, (cudaStream_t)stream>>>(trace, n_records, k, (unsigned*)sink);
-  else
-    red_replay_kernel<false><<<blocks, 256, 0, (cudaStream_t)stream>>>(trace, n_records, k, (unsigned*)sink);
-  return check_launch("red_replay_kernel");
+  red_lines_kernel<<<(unsigned)sms * 8, 256, 0, (cudaStream_t)stream>>>(trace, n_records, hist);
+  return check_launch("red_lines_kernel");
 }
 
 int msurf_decode(uint64_t* keys, int64_t count, int32_t n_surf, const double* sentinel,
@@ -1871,6 +1875,23 @@ int msurf_microbench(int32_t which, double* result) {
     cudaEventElapsedTime(&ms, a, b);
     cudaFree(buf);
     *result = (double)blocks * threads * iters / (ms * 1e-3);
+  } else if (which >= 33 && which <= 64) {
+    // RED.MIN warp instructions/s touching L = which - 32 lines each, 32 MiB table
+    const int L = which - 32;
+    unsigned long long* buf = nullptr;
+    const long long n = 1ll << 22;
+    if (cudaMalloc(&buf, n * 8) != cudaSuccess) return set_err("microbench: cudaMalloc");
+    cudaMemset(buf, 0xff, n * 8);
+    const int blocks = sms * 8, threads = 256, iters = 256;
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaEventRecord(a);
+      mb_atomic_lines_kernel<<<blocks, threads>>>(buf, (unsigned)((n >> 4) - 1), L, iters);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+    }
+    cudaEventElapsedTime(&ms, a, b);
+    cudaFree(buf);
+    *result = (double)blocks * (threads / 32) * iters / (ms * 1e-3);
   } else {
     return set_err("msurf_microbench: unknown kind");
   }

@@ -249,7 +249,13 @@ class SweepBatch:
                 s, o = surfs[q], offs[q]
                 if s.n_strips > 1:
                     o["col0"] = ar.add(np.asarray(s.col0, dtype=np.int64))
-                if trig == "host":
+                # the trajectory record (engine.py:242-310) exposes the per-row
+                # cos/sin themselves, and the reference defines it with the libm
+                # values (simulate and simulate_reference records are identical,
+                # test_engine.py:127-137): a record-keeping surface takes the
+                # host-libm per-row table (O(steps x teeth)); the sweep stays on
+                # the device either way
+                if trig == "host" or s.plan.record:
                     tab, vib = _trig_tables(s.plan)
                     o["trig_table"] = ar.add(tab)
                     if vib is not None:
@@ -393,15 +399,15 @@ class SweepBatch:
             return _native.SWEEP_TRACE
         return _native.SWEEP_DIAG if self.diagnostics else 0
 
-    def red_replay(self, reps: int = 3, cap_bytes: int = 24 << 30):
+    def red_lines(self, cap_bytes: int = 24 << 30):
         """Roofline helper (bench.py; not on the product path): trace every
-        RED.MIN of one sweep of this batch (MSURF_SWEEP_TRACE launch), then
-        replay the trace alone (msurf_red_replay) on freshly filled keys, and
-        stream it once more without the REDs. Returns a dict with the active
-        lanes replayed, the median replay and trace-read-only seconds, and
-        whether the trace was truncated to ``cap_bytes`` (then the replay
-        covers the first records in issue order); None when the surfaces'
-        keys do not share one buffer."""
+        RED.MIN of one sweep of this batch (MSURF_SWEEP_TRACE launch, one
+        record of 32 key offsets per warp-wide RED) and histogram the records
+        by the number of distinct 128-byte lines each touches
+        (msurf_red_lines). Returns {"hist": [33 counts], "records",
+        "records_issued", "lanes", "truncated"}; a truncated trace (above
+        ``cap_bytes``) histograms the first records in issue order. None when
+        the surfaces' keys do not share one buffer."""
         torch, lib = self.torch, self.lib
         if self.strip_keys is not None and any(s.n_strips == 1 for s in self.surfs):
             return None
@@ -410,7 +416,7 @@ class SweepBatch:
         cap = int(min(cap_bytes, free // 2)) // 128
         trace = torch.empty(max(cap, 1) * 32, dtype=torch.int32, device=self.dev)
         ctr = torch.zeros(2, dtype=torch.int64, device=self.dev)
-        sink = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        hist = torch.zeros(33, dtype=torch.int64, device=self.dev)
         _native.check(lib.msurf_trace_arm(trace.data_ptr(), cap, ctr.data_ptr(), base.data_ptr()))
         prev, self.diagnostics = self.diagnostics, "trace"
         try:
@@ -420,26 +426,13 @@ class SweepBatch:
         torch.cuda.synchronize(self.dev)
         issued, lanes = (int(v) for v in ctr.cpu())
         n_rec = min(issued, cap)
-        truncated = issued > cap
-        if truncated:
+        _native.check(lib.msurf_red_lines(trace.data_ptr(), n_rec, hist.data_ptr(), _native.stream_ptr()))
+        h = [int(v) for v in hist.cpu()]
+        if issued > cap:
             lanes = int(torch.count_nonzero(trace[: n_rec * 32] != -1))
-        sp = _native.stream_ptr()
-        times = {0: [], 1: []}
-        for _ in range(reps):
-            for ro in (0, 1):
-                self.launch_fill(sp)
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                _native.check(lib.msurf_red_replay(trace.data_ptr(), n_rec, base.data_ptr(), ro,
-                                                   sink.data_ptr(), sp))
-                e1.record()
-                torch.cuda.synchronize(self.dev)
-                times[ro].append(e0.elapsed_time(e1) * 1e-3)
         del trace
         torch.cuda.empty_cache()
-        return {"lanes": lanes, "records": n_rec, "records_issued": issued, "truncated": truncated,
-                "t_replay_s": sorted(times[0])[len(times[0]) // 2],
-                "t_read_s": sorted(times[1])[len(times[1]) // 2]}
+        return {"hist": h, "records": n_rec, "records_issued": issued, "lanes": lanes, "truncated": issued > cap}
 
     def launch_decode(self, sp: int) -> None:
         """Keys -> fp64 heights in place, machined-cell counts."""

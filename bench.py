@@ -308,12 +308,16 @@ def red_lines(batch):
 
 def roofline(flops, atomics, sweep_ms, lines, kernel_name):
     """The north star's roofline = the slower of fp64 issue and atomic
-    traffic. t_fp64 = algorithmic fp64 ops / the measured DADD/DMUL issue
-    rate. t_red = the sweep's own RED instructions, each priced at the
-    measured L2 RED.MIN instruction rate for its shape (distinct lines
-    touched, microbench 32 + L), summed over the traced histogram (scaled to
-    all records when the trace was truncated). ``bound`` is the larger term,
-    ``frac`` = that term / the measured sweep time."""
+    traffic, each as the time the path's minimum work needs at the measured
+    peak rate of its unit:
+    * t_fp64 = algorithmic fp64 ops / the DADD/DMUL issue rate (microbench 0);
+    * t_red = the 128-byte line updates the sweep's RED.MIN stream performs
+      (its traced warp REDs, each counted by the distinct lines it touches)
+      / the peak L2 atomic line-update rate (the best RED.MIN shape of
+      microbench 32+L, lines/s).
+    ``bound`` is the larger term and ``frac`` = that term / the measured
+    sweep time. The shape-priced RED time (each warp RED at the measured rate
+    for its line count, random placement) is reported beside it."""
     pk = device_peaks()
     t = sweep_ms * 1e-3
     t_fp64 = flops / pk[0]
@@ -323,28 +327,35 @@ def roofline(flops, atomics, sweep_ms, lines, kernel_name):
     t_red = None
     if lines is not None and lines["records"] > 0:
         hist = lines["hist"]
-        t_cap = sum(hist[L] / pk[32 + L] for L in range(1, 33))
         scale = lines["records_issued"] / lines["records"]
-        t_red = t_cap * scale
-        mean_lines = sum(L * hist[L] for L in range(33)) / max(1, sum(hist))
-        terms.update({"t_red_ms": t_red * 1e3, "frac_red": t_red / t,
+        line_updates = scale * sum(L * hist[L] for L in range(33))
+        peak_L = max(range(1, 33), key=lambda L: pk[32 + L] * L)
+        peak_lines = pk[32 + peak_L] * peak_L
+        t_red = line_updates / peak_lines
+        t_shape = scale * sum(hist[L] / pk[32 + L] for L in range(1, 33))
+        terms.update({"t_red_ms": t_red * 1e3, "frac_red": t_red / t, "line_updates": line_updates,
+                      "peak_line_updates_per_s": peak_lines, "peak_shape_lines": peak_L,
+                      "achieved_line_updates_per_s": line_updates / t,
+                      "t_red_shape_priced_ms": t_shape * 1e3,
                       "red_records": lines["records_issued"], "red_lanes_traced": lines["lanes"],
-                      "red_trace_truncated": lines["truncated"], "mean_lines_per_red_instr": mean_lines,
+                      "red_trace_truncated": lines["truncated"],
+                      "mean_lines_per_red_instr": line_updates / max(1, lines["records_issued"]),
                       "red_lines_hist": hist,
                       "red_instr_rate_by_lines_per_s": {L: pk[32 + L] for L in (1, 2, 4, 8, 16, 32)},
-                      "red_note": "every warp-wide RED.MIN of one sweep traced and priced at the measured "
-                                  "L2 RED.MIN instruction rate for its number of distinct 128-B lines"})
+                      "red_note": "every warp-wide RED.MIN of one sweep traced (MSURF_SWEEP_TRACE) and counted "
+                                  "by the distinct 128-B lines it updates"})
     bound = "fp64" if t_red is None or t_fp64 >= t_red else "atomic"
     if bound == "fp64":
         out = {"bound": "fp64", "achieved": flops / t / 1e12, "peak": pk[0] / 1e12, "unit": "TFLOP/s",
                "frac": t_fp64 / t}
     else:
-        out = {"bound": "atomic", "achieved": atomics / t / 1e9, "peak": atomics / t_red / 1e9,
-               "unit": "G RED.MIN lanes/s", "frac": t_red / t}
+        out = {"bound": "atomic", "achieved": terms["achieved_line_updates_per_s"] / 1e9,
+               "peak": terms["peak_line_updates_per_s"] / 1e9, "unit": "G line-updates/s (L2 RED.MIN)",
+               "frac": t_red / t}
     out.update({"kernel": kernel_name, "sweep_ms": sweep_ms, "terms": terms,
                 "peak_source": "measured in this run: fp64 = msurf_microbench(0) non-FMA DADD/DMUL issue rate "
-                               "(MEASURED_PEAKS.json has no FP64 entry); atomic = msurf_microbench(32+L) RED.MIN "
-                               "instruction rates applied to this workload's traced RED shapes"})
+                               "(MEASURED_PEAKS.json has no FP64 entry); atomic = best L2 RED.MIN line-update rate "
+                               "over msurf_microbench(32+L) shapes"})
     return out
 
 

@@ -54,6 +54,9 @@ constexpr int sweep_min_blocks(bool one, int threads) {
 
 constexpr int kThreads = 256;      // reduction / stream kernels
 constexpr int kWarps = kThreads / 32;
+#ifndef MSURF_LANE_POINT
+#define MSURF_LANE_POINT 1  // extended modes: phase 2 with lane = edge point (see kLanePoint)
+#endif
 #ifndef MSURF_PAIR_STEPS
 #define MSURF_PAIR_STEPS 2  // 0: never, 1: always, 2: tilt mode only (see kPairSteps)
 #endif
@@ -392,6 +395,19 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
   // (config 2: 0.99 -> 0.95 ms, config 5: 59.4 -> 54.1 ms) whose neighbour
   // filter needs both neighbours; slower for the constant-z modes (configs 3, 4)
   constexpr bool kPairSteps = MSURF_PAIR_STEPS == 1 || (MSURF_PAIR_STEPS == 2 && MODE == MSURF_MODE_EXT_TILT);
+  // lane = one edge point of a 32-point chunk, the warp walking the tile's
+  // live steps in time order (warp-uniform transforms broadcast from shared
+  // memory): a RED instruction then covers 32 neighbouring edge points — a
+  // short radial segment, fewer 128-byte lines — instead of one point's 32
+  // positions along its arc (one line per lane at the cutting front), and a
+  // point's consecutive steps meet in one lane, so same-cell runs reduce in
+  // registers (exact run minimum) before one RED. Measured:
+  // faster for the batched flat-end surfaces (config 3: 28.5 -> 16.9 lines per
+  // RED, sweep 6.39 -> 5.76 ms); slower for the by-value single surfaces
+  // (config 4 4.97 -> 5.36 ms: 6.6-cell point spacing, fewer active lanes per
+  // RED) and for the tilt mode (config 5 50.5 -> 66 ms: more instructions per
+  // evaluation than the paired-step loop), which keep lane = step.
+  constexpr bool kLanePoint = MSURF_LANE_POINT && MODE == MSURF_MODE_EXT && !ONE;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* rowv = reinterpret_cast<double*>(smem_raw);                        // [T][8] by live slot
   uint64_t* masks = reinterpret_cast<uint64_t*>(rowv + kTileSteps * 8);      // [T][W] by thread
@@ -658,7 +674,122 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
   // changes, and (g, q) advance without a division
   int g = warp / nchunk, q = warp - (warp / nchunk) * nchunk;
   int g_loaded = -1;
-  if constexpr (kPairSteps) {
+  if constexpr (kLanePoint) {
+    constexpr int kSlotWords = kTileSteps / 32;
+    for (int qc = warp; qc < nchunk; qc += kSweepWarps) {
+      // live slots of this chunk (bit = slot, time order)
+      unsigned mw[kSlotWords];
+      unsigned anyq = 0u;
+#pragma unroll
+      for (int w = 0; w < kSlotWords; ++w) {
+        const int slot = w * 32 + lane;
+        const bool on = slot < n_live && ((mslot[slot * mask_words + (qc >> 6)] >> (qc & 63)) & 1ull);
+        mw[w] = __ballot_sync(0xffffffffu, on);
+        anyq |= mw[w];
+      }
+      if (!anyq) continue;  // warp-uniform
+      const int pidx = qc * 32 + lane;
+      const bool pv = pidx < npts;
+      double4 pt = make_double4(0.0, 0.0, 0.0, 0.0);
+      if (pv) {
+        const double2* src = reinterpret_cast<const double2*>(pts + pidx);
+        const double2 a = __ldg(src), b = __ldg(src + 1);
+        pt = make_double4(a.x, a.y, b.x, b.y);
+      }
+      // a lane past the tooth's last point: i index pushed far out of range
+      const int ibias = pv ? kMagicHi : kMagicHi - (1 << 30);
+      int run_idx = -1;                 // cell of the current run (-1: none)
+      unsigned long long run_key = 0;   // tilt: minimum key of the run
+#pragma unroll
+      for (int w = 0; w < kSlotWords; ++w) {
+        unsigned m = mw[w];
+        while (m) {  // warp-uniform: two live steps per iteration (two independent fp64 chains)
+          const int s1 = w * 32 + __ffs(m) - 1;
+          m &= m - 1u;
+          const bool two = m != 0u;
+          const int s2 = two ? w * 32 + __ffs(m) - 1 : s1;
+          m &= m - (two ? 1u : 0u);
+          const double4 t1 = *reinterpret_cast<const double4*>(rowv + s1 * 8);
+          const double4 t2 = *reinterpret_cast<const double4*>(rowv + s2 * 8);
+          const double r1[4] = {t1.x, t1.y, t1.z, t1.w};
+          const double r2[4] = {t2.x, t2.y, t2.z, t2.w};
+          PointEval e1 = eval_point<MODE>(pt, r1, inv, cx0, cy0, tilt_c, tilt_s);
+          PointEval e2 = eval_point<MODE>(pt, r2, inv, cx0, cy0, tilt_c, tilt_s);
+          const int ia1 = e1.hi_x - ibias, ja1 = e1.hi_y - jbias;
+          const int ia2 = e2.hi_x - ibias, ja2 = e2.hi_y - jbias;
+          const bool in1 = ((unsigned)ia1 <= span_i) & ((unsigned)ja1 <= span_j) & !e1.near;
+          const bool in2 = ((unsigned)ia2 <= span_i) & ((unsigned)ja2 <= span_j) & !e2.near & two;
+          const int idx1 = in1 ? ia1 * ldk + ja1 : -1;
+          const int idx2 = in2 ? ia2 * ldk + ja2 : -1;
+          bool dep1, dep2;
+          unsigned long long k1, k2;
+          int a1, a2;
+          if (MODE == MSURF_MODE_EXT_TILT) {
+            // run minimum: a run ends when the cell changes; its minimum deposits then
+            const bool brk1 = idx1 != run_idx;
+            dep1 = brk1 & (run_idx >= 0);
+            a1 = run_idx;
+            k1 = run_key;
+            run_key = brk1 ? e1.key : (e1.key < run_key ? e1.key : run_key);
+            run_idx = idx1;
+            const bool brk2 = two & (idx2 != run_idx);
+            dep2 = brk2 & (run_idx >= 0);
+            a2 = run_idx;
+            k2 = run_key;
+            if (two) {
+              run_key = brk2 ? e2.key : (e2.key < run_key ? e2.key : run_key);
+              run_idx = idx2;
+            }
+          } else {
+            // constant z' per point: each run's first evaluation deposits
+            dep1 = in1 & (idx1 != run_idx);
+            dep2 = in2 & (idx2 != idx1);
+            a1 = idx1;
+            a2 = idx2;
+            k1 = e1.key;
+            k2 = e2.key;
+            if (two) run_idx = idx2; else run_idx = idx1;
+          }
+          if (DIAG) {
+            n_dep += (unsigned)in1 + (unsigned)in2;
+            n_atom += (unsigned)dep1 + (unsigned)dep2;
+          }
+          red_min_u64_if(keys + a1, k1, dep1);
+          red_min_u64_if(keys + a2, k2, dep2);
+          if (DIAG == 2) {
+            trace_red(keys + a1, dep1, lane);
+            trace_red(keys + a2, dep2, lane);
+          }
+          // near-boundary evaluations (~1e-9 each): the exact reference index, deposited directly
+          if (__builtin_expect(__any_sync(0xffffffffu, pv & (e1.near | (e2.near & two))), 0)) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const PointEval& e = h ? e2 : e1;
+              const int sl = h ? s2 : s1;
+              if (!(pv & e.near & (h == 0 || two))) continue;
+              double xw, yw;
+              exact_xy<MODE>(pt, rowv[sl * 8 + 0], rowv[sl * 8 + 1], rowv[sl * 8 + 4], rowv[sl * 8 + 5], tilt_c,
+                             xw, yw);
+              const int ie = cell_index_exact(xw, J.x_min, dd);
+              const int je = cell_index_exact(yw, J.y_min, dd) - j_lo;
+              const bool in = ((unsigned)ie <= span_i) & ((unsigned)je <= span_j);
+              if (in) red_min_u64(keys + (ie * ldk + je), (unsigned long long)e.key);
+              if (DIAG) {
+                n_dep += in;
+                n_atom += in;
+              }
+            }
+          }
+        }
+      }
+      if (MODE == MSURF_MODE_EXT_TILT) {
+        const bool dep = run_idx >= 0;  // the chunk's last run
+        if (DIAG) n_atom += (unsigned)dep;
+        red_min_u64_if(keys + run_idx, run_key, dep);
+        if (DIAG == 2) trace_red(keys + run_idx, dep, lane);
+      }
+    }
+  } else if constexpr (kPairSteps) {
     // unit = (group g of 64 consecutive live steps, chunk q); lane l holds the
     // group's steps 2l (A) and 2l+1 (B), so one broadcast point record serves
     // two evaluations and half of the neighbour exchange stays in registers

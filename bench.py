@@ -426,6 +426,8 @@ def measure_surface(cfg_id, args, rank, world, with_cpu):
             pipe.capture()  # three CUDA graphs: fill | sweep | decode + reductions
     else:
         pipe = sharded.StripPipeline(batch, every=every, uncut=uncut)
+        if not args.no_graph:
+            pipe.capture()  # five CUDA graphs; the three all-reduces stay eager between them
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def barrier():

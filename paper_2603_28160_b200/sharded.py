@@ -193,8 +193,11 @@ class StripPipeline:
     """Sync-free multi-GPU step for one strip-sharded surface: sweep of this
     rank's strip, then the roughness reductions with THREE small NCCL
     all-reduces per step (round 1: areal + profile sums, and their max/min;
-    round 2: areal central moments + profile |d| sums). Results are read back
-    by collect() after the timed region."""
+    round 2: areal central moments + profile |d| sums). The device work
+    between the collectives runs as three stages that ``capture()`` records as
+    CUDA graphs (every buffer is preallocated, so replays reuse the captured
+    addresses); the collectives stay eager between the replays. Results are
+    read back by collect() after the timed region."""
 
     def __init__(self, batch, every: int = 64, uncut: str = "exclude", group=None):
         import torch
@@ -218,7 +221,13 @@ class StripPipeline:
         self.prof = torch.empty((max(P, 1), 8), dtype=f64, device=dev)
         self.first = torch.empty((max(P, 1), 8), dtype=f64, device=dev)
         self.starts = torch.tensor([i * self.ld for i in self.prof_idx] or [0], dtype=torch.int64, device=dev)
+        # collective buffers: round 1 sums [sum z, n, n_uncut] and extrema
+        # [max z, -min z] of the areal record and every profile; round 2 moments
+        self.sums = torch.empty((1 + P, 3), dtype=f64, device=dev)
+        self.ext = torch.empty((1 + P, 2), dtype=f64, device=dev)
+        self.mom = torch.empty(4 + P, dtype=f64, device=dev)
         self.P = P
+        self.graphs = None
         self.launches_per_run = batch.launches_per_run + 4 + (2 if P else 0)
 
     def _allreduce(self, t, op):
@@ -227,53 +236,107 @@ class StripPipeline:
         if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
             dist.all_reduce(t, op=op, group=self.group)
 
-    def run(self, events=None):
-        import torch.distributed as dist
+    def _stage_fill(self, sp):
+        self.batch.launch_fill(sp)
 
-        torch, lib, b = self.torch, self.lib, self.batch
-        st = torch.cuda.current_stream()
-        sp = int(st.cuda_stream)
-        if events:
-            events[0].record(st)
-        b.launch_fill(sp)
-        if events:
-            events[1].record(st)
-        b.launch_sweep(sp)
-        if events:
-            events[2].record(st)
+    def _stage_sweep(self, sp):
+        self.batch.launch_sweep(sp)
+
+    def _stage_pack1(self, sp):
+        """decode, areal pass 1, profile pass 1, pack round 1."""
+        lib, b, P = self.lib, self.batch, self.P
         b.launch_decode(sp)
         h = b.keys.data_ptr()
         sent = b.base + b.sentinel_off
-        P = self.P
         _native.check(lib.msurf_areal_pass1(h, self.ld, 0, 1, 0, 0, self.rows, self.ld, sent, self.exclude,
                                             self.work.data_ptr(), self.st1.data_ptr(), sp))
         if P:
             _native.check(lib.msurf_profiles(h, 0, 1, self.starts.data_ptr(), P, self.ld, 1, sent,
                                              self.exclude, None, self.prof.data_ptr(), sp))
-        # round 1: sums [sum z, n, n_uncut] and extrema [max z, -min z] of areal + profiles
-        sums = torch.cat([self.st1[:, [0, 3, 4]], self.prof[:P, 0:3]], dim=0)
-        ext = torch.cat([torch.stack([self.st1[:, 1], -self.st1[:, 2]], dim=1),
-                         torch.stack([self.prof[:P, 3], -self.prof[:P, 4]], dim=1)], dim=0)
-        self._allreduce(sums, dist.ReduceOp.SUM)
-        self._allreduce(ext, dist.ReduceOp.MAX)
-        self.st1[:, [0, 3, 4]] = sums[0:1]
-        self.st1[:, 1], self.st1[:, 2] = ext[0:1, 0], -ext[0:1, 1]
+        self.sums[0:1, 0:1].copy_(self.st1[:, 0:1])
+        self.sums[0:1, 1:3].copy_(self.st1[:, 3:5])
+        self.ext[0:1, 0].copy_(self.st1[:, 1])
+        self.torch.neg(self.st1[:, 2], out=self.ext[0:1, 1])
+        if P:
+            self.sums[1:].copy_(self.prof[:P, 0:3])
+            self.ext[1:, 0].copy_(self.prof[:P, 3])
+            self.torch.neg(self.prof[:P, 4], out=self.ext[1:, 1])
+
+    def _stage_moments(self, sp):
+        """unpack round 1 (global means), areal pass 2, profile pass 2, pack round 2."""
+        lib, b, P = self.lib, self.batch, self.P
+        self.st1[:, 0:1] = self.sums[0:1, 0:1]
+        self.st1[:, 3:5] = self.sums[0:1, 1:3]
+        self.st1[:, 1] = self.ext[0:1, 0]
+        self.st1[:, 2] = -self.ext[0:1, 1]
         self.st1[:, 5] = self.st1[:, 0] / self.st1[:, 3]  # global mean
         if P:
-            self.first[:P, 0:3] = sums[1:]
-            self.first[:P, 3], self.first[:P, 4] = ext[1:, 0], -ext[1:, 1]
+            self.first[:P, 0:3] = self.sums[1:]
+            self.first[:P, 3] = self.ext[1:, 0]
+            self.first[:P, 4] = -self.ext[1:, 1]
             self.first[:P, 6] = self.first[:P, 0] / self.first[:P, 1]
-        # round 2: central moments around the global means
+        h = b.keys.data_ptr()
+        sent = b.base + b.sentinel_off
         _native.check(lib.msurf_areal_pass2(h, self.ld, 0, 1, 0, 0, self.rows, self.ld, sent, self.exclude,
                                             self.st1.data_ptr(), self.work.data_ptr(), self.st2.data_ptr(), sp))
         if P:
             _native.check(lib.msurf_profiles(h, 0, 1, self.starts.data_ptr(), P, self.ld, 1, sent,
                                              self.exclude, self.first.data_ptr(), self.prof.data_ptr(), sp))
-        mom = torch.cat([self.st2.reshape(-1), self.prof[:P, 5]])
-        self._allreduce(mom, dist.ReduceOp.SUM)
-        self.st2.copy_(mom[:4].view(1, 4))
+        self.mom[:4].copy_(self.st2.reshape(-1))
         if P:
-            self.first[:P, 5] = mom[4:]
+            self.mom[4:].copy_(self.prof[:P, 5])
+
+    def _stage_finish(self, sp):
+        self.st2.copy_(self.mom[:4].view(1, 4))
+        if self.P:
+            self.first[: self.P, 5] = self.mom[4:]
+
+    def _stages(self):
+        return (self._stage_fill, self._stage_sweep, self._stage_pack1, self._stage_moments, self._stage_finish)
+
+    def capture(self):
+        """Record the five device stages as CUDA graphs (one warm-up run
+        first, outside capture); the collectives between them stay eager."""
+        torch = self.torch
+        self.run()
+        torch.cuda.synchronize()
+        graphs = []
+        for stage in self._stages():
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                stage(int(torch.cuda.current_stream().cuda_stream))
+            graphs.append(g)
+        self.graphs = graphs
+        return graphs
+
+    def run(self, events=None):
+        """One step; ``events`` (4): start, after the fill, after the sweep, end."""
+        import torch.distributed as dist
+
+        torch = self.torch
+        st = torch.cuda.current_stream()
+        sp = int(st.cuda_stream)
+
+        def stage(k):
+            if self.graphs is None:
+                self._stages()[k](sp)
+            else:
+                self.graphs[k].replay()
+
+        if events:
+            events[0].record(st)
+        stage(0)
+        if events:
+            events[1].record(st)
+        stage(1)
+        if events:
+            events[2].record(st)
+        stage(2)
+        self._allreduce(self.sums, dist.ReduceOp.SUM)
+        self._allreduce(self.ext, dist.ReduceOp.MAX)
+        stage(3)
+        self._allreduce(self.mom, dist.ReduceOp.SUM)
+        stage(4)
         if events:
             events[3].record(st)
 

@@ -47,6 +47,7 @@ def main():
             for r, (lo, hi) in enumerate(sharded.strip_bounds(p.grid.n + 1, n)):
                 b = SweepBatch([(p, lo, hi)])
                 pipe = sharded.StripPipeline(b, every=meta.get("profiles_every", 64), uncut=meta["uncut"])
+                pipe.capture()
                 for _ in range(2):
                     pipe.run()
                 torch.cuda.synchronize()

@@ -452,7 +452,9 @@ def measure_surface(cfg_id, args, rank, world, with_cpu):
     mode = p.mode
     evald, live, engaged = int(ctr[0][1]), int(ctr[0][0]), int(ctr[0][4])
     flops = FLOPS_PER_POINT[mode] * evald + FLOPS_PER_ROW * live
-    atomics = int(dctr[0][3])
+    # the production sweep's RED count (its trace); the DIAG launch counts the
+    # oracle's P_in without the stock-height cull, so its atomics are higher
+    atomics = int(lines["lanes"]) if lines else int(dctr[0][3])
     roof = roofline(flops, atomics, sweep_avg, lines, "sweep_kernel<MODE>")
     roof.update({
         "traffic": profiled_traffic(meta["name"]), "flops_per_launch": flops,
@@ -462,7 +464,8 @@ def measure_surface(cfg_id, args, rank, world, with_cpu):
                                "them, which is what the fp64 term is computed on",
                        "P_eng": engaged * p.points, "engaged_rows": engaged},
         "points_evaluated": evald, "live_rows": live, "deposits": int(dctr[0][2]), "atomics": atomics,
-        "diag_note": "deposits/atomics from one extra untimed launch with MSURF_SWEEP_DIAG",
+        "diag_note": "deposits (P_in, the oracle's count) from one extra untimed MSURF_SWEEP_DIAG launch without "
+                     "the stock-height cull; atomics = RED.MIN of the production sweep (its trace)",
         "hbm": {"bytes_per_step": 24 * (p.grid.m + 1) * (j_hi - j_lo + 1),
                 "peak_gbs": measured_peaks().get("hbm_gbs")},
     })
@@ -585,7 +588,7 @@ def measure_batch(args, rank, world, with_cpu):
     npts = plans[0].points
     mode = plans[0].mode
     flops = FLOPS_PER_POINT[mode] * evald + FLOPS_PER_ROW * live
-    atomics = int(dctr[:, 3].sum())
+    atomics = int(lines["lanes"]) if lines else int(dctr[:, 3].sum())
     roof = roofline(flops, atomics, sweep_avg, lines, "sweep_kernel<MODE> (listed, persistent)")
     roof.update({"traffic": profiled_traffic(meta["name"]), "flops_per_launch": flops,
                  "survey_def": {"P_eng": engaged * npts, "engaged_rows": engaged},

@@ -585,13 +585,21 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
             const float tcc = MODE == MSURF_MODE_EXT_TILT ? tcf : 1.0f;
             const float hx = (float)wxh + (4e-6f * (rt_f + fabsf(oxf)) + 1e-6f);
             const float hy = (float)wyh + (4e-6f * (rt_f + fabsf(oyf)) + 1e-6f);
+            // stock-height cull (not in the DIAG=1 counting variant, whose deposit
+            // count is the oracle's P_in): z' >= sin(tau) v_centre + zfloor + stock
+            // for every point of the chunk (planner.chunk_zfloor); a chunk whose
+            // bound is at or above the stock top cannot lower any key below the
+            // initial height, so skipping it never changes a result. Same fp32
+            // margin as the position tests.
+            const float tsz = MODE == MSURF_MODE_EXT_TILT ? tsf : 0.0f;
             unsigned kept = 0;
             for (int q = 0; q < nchunk; ++q) {
               const float4 a = __ldg(cf4 + 2 * q);
-              const float yz = __ldg(reinterpret_cast<const float*>(cf4 + 2 * q + 1));
+              const float4 bz = __ldg(cf4 + 2 * q + 1);  // yz, Rt, zfloor, 0
               const float uc = fmaf(cf, a.x, sf * a.y);
               const float vc = fmaf(cf, a.y, -(sf * a.x));
-              const bool hit = (fabsf(uc + oxf) <= hx + a.z) & (fabsf(fmaf(tcc, vc, yz) + oyf) <= hy + a.w);
+              bool hit = (fabsf(uc + oxf) <= hx + a.z) & (fabsf(fmaf(tcc, vc, bz.x) + oyf) <= hy + a.w);
+              if (DIAG != 1) hit &= fmaf(tsz, vc, bz.z) <= 4e-6f * (rt_f + fabsf(bz.z)) + 1e-6f;
               if (hit) {
                 my_mask[q >> 6] |= 1ull << (q & 63);
                 kept += (q == nchunk - 1) ? (unsigned)(npts - 32 * q) : 32u;

@@ -26,7 +26,8 @@ from . import _native
 from .errors import ConfigError, MillsurfError
 from .extensions import Extensions
 from .grid import GridSpec, HeightField, TrajectoryRecord
-from .planner import DEVICE_FIELDS, MODE_REF, SweepPlan, chunk_f32, plan, plan_many, step_window, time_step
+from .planner import (DEVICE_FIELDS, MODE_REF, SweepPlan, chunk_f32, plan, plan_many, plan_zfloor, step_window,
+                      time_step)
 
 DEFAULT_MAX_STEP_ANGLE_RAD = math.radians(0.5)
 # Z-map bytes one sweep job may cover: keeps its RED.MIN traffic in the
@@ -241,7 +242,7 @@ class SweepBatch:
                     pts=ar.add(p.pts.astype(np.float64, copy=False)),
                     tooth_box=ar.add(p.tooth_box.astype(np.float64, copy=False)),
                     chunk_circ=ar.add(p.chunk_circ.astype(np.float64, copy=False)),
-                    chunk_f32=ar.add(chunk_f32(p.chunk_circ, p.tooth_box)),
+                    chunk_f32=ar.add(chunk_f32(p.chunk_circ, p.tooth_box, plan_zfloor(p))),
                     pass_x0=ar.add(p.pass_x0.astype(np.float64, copy=False)),
                     min_index=ar.add(p.min_index.astype(np.int32, copy=False)),
                 )
@@ -405,7 +406,8 @@ class SweepBatch:
         record of 32 key offsets per warp-wide RED) and histogram the records
         by the number of distinct 128-byte lines each touches
         (msurf_red_lines). Returns {"hist": [33 counts], "records",
-        "records_issued", "lanes", "truncated"}; a truncated trace (above
+        "records_issued", "lanes" (active lanes = RED.MIN of the production
+        sweep, all records), "truncated"}; a truncated trace (above
         ``cap_bytes``) histograms the first records in issue order. None when
         the surfaces' keys do not share one buffer."""
         torch, lib = self.torch, self.lib
@@ -428,8 +430,6 @@ class SweepBatch:
         n_rec = min(issued, cap)
         _native.check(lib.msurf_red_lines(trace.data_ptr(), n_rec, hist.data_ptr(), _native.stream_ptr()))
         h = [int(v) for v in hist.cpu()]
-        if issued > cap:
-            lanes = int(torch.count_nonzero(trace[: n_rec * 32] != -1))
         del trace
         torch.cuda.empty_cache()
         return {"hist": h, "records": n_rec, "records_issued": issued, "lanes": lanes, "truncated": issued > cap}

@@ -259,19 +259,46 @@ def _pack(p: SweepPlan) -> None:
                             b[:, :, 4].min(1), b[:, :, 5].max(1)], axis=1)
 
 
-def chunk_f32(chunk_circ: np.ndarray, tooth_box: np.ndarray) -> np.ndarray:
+def chunk_f32(chunk_circ: np.ndarray, tooth_box: np.ndarray, zfloor: np.ndarray | None = None) -> np.ndarray:
     """fp32 phase-1 cull records (msurf_job.chunk_f32): per tooth and chunk
-    (xc, yc, rx, ry, yz, Rt, 0, 0), Rt = max|x| + max|y| + max|z| of the tooth
-    box. The kernel widens its fp32 test by 4e-6 (Rt + |offset|) + 1e-6 mm,
-    which covers the fp32 roundings of every term. Leading
-    (set) axes are allowed: (..., Z, nchunk, 6) and (..., Z, 6)."""
+    (xc, yc, rx, ry, yz, Rt, zfloor, 0), Rt = max|x| + max|y| + max|z| of the
+    tooth box, zfloor = chunk_zfloor (0 when not given). The kernel widens its
+    fp32 tests by 4e-6 (Rt + |offset|) + 1e-6 mm, which covers the fp32
+    roundings of every term. Leading (set) axes are allowed:
+    (..., Z, nchunk, 6) and (..., Z, 6)."""
     out = np.zeros(chunk_circ.shape[:-1] + (8,), dtype=np.float32)
     out[..., :5] = chunk_circ[..., :5]
     b = np.abs(tooth_box)
     rt = (np.maximum(b[..., 0], b[..., 1]) + np.maximum(b[..., 2], b[..., 3])
           + np.maximum(b[..., 4], b[..., 5]))
     out[..., 5] = rt[..., None]
+    if zfloor is not None:
+        out[..., 6] = zfloor
     return out
+
+
+def chunk_zfloor(w: np.ndarray, rho: np.ndarray, tilt_s: float, stock) -> np.ndarray:
+    """Per tooth and chunk (leading set axes allowed): the lowest workpiece z'
+    any point of the chunk can reach at any spindle angle, minus the stock
+    height. z' = sin(tau) v + w with w the point's angle-free part (tilt:
+    cos(tau) zt + zoff; otherwise z' itself) and |v - v_centre| <= rho, the
+    chunk's bounding-circle radius, so z' >= sin(tau) v_centre + zfloor +
+    stock. The kernel skips a (step, chunk) whose bound is at or above the
+    stock top: such evaluations can never lower a key below the initial
+    height (a result-neutral cull)."""
+    *lead, n = w.shape
+    nchunk = (n + CHUNK - 1) // CHUNK
+    pad = nchunk * CHUNK - n
+    full = np.concatenate([w, np.repeat(w[..., -1:], pad, axis=-1)], axis=-1) if pad else w
+    wmin = full.reshape(*lead, nchunk, CHUNK).min(axis=-1)
+    stock = np.asarray(stock, dtype=np.float64).reshape(np.shape(stock) + (1,) * (wmin.ndim - np.ndim(stock)))
+    return wmin - abs(tilt_s) * rho - stock
+
+
+def plan_zfloor(p) -> np.ndarray:
+    """chunk_zfloor of one plan (its records, circles and stock height)."""
+    w = p.pts[..., 3] if p.mode == MODE_EXT_TILT else p.zw
+    return chunk_zfloor(w, p.chunk_circ[..., 2], p.tilt_s if p.mode == MODE_EXT_TILT else 0.0, p.initial_height)
 
 
 # msurf_job array fields, in the order SweepBatch packs them
@@ -719,8 +746,10 @@ def _plan_ext_group_native(configs, exts, threads: int = 1):
                       for cfg in configs], dtype=np.float64)
     px0 = np.array([[spans[b][3] + k * e.stepover_mm for k in range(n_pass)]
                     for b, e in enumerate(exts)], dtype=np.float64)
+    stock = np.array([sp[5] for sp in spans]) + a_p  # initial heights z0 + a_p
+    zfl = chunk_zfloor(pts[..., 3] if tilt else zw, circ[..., 2], ts if tilt else 0.0, stock)
     grp = PlanGroup({"tooth_base": tbase, "tooth_rows": np.zeros((B, z_n, 8)), "pts": pts, "tooth_box": tbox,
-                     "chunk_circ": circ, "chunk_f32": chunk_f32(circ, tbox), "pass_x0": px0,
+                     "chunk_circ": circ, "chunk_f32": chunk_f32(circ, tbox, zfl), "pass_x0": px0,
                      "min_index": mins})
     plans = []
     for b, (cfg, e) in enumerate(zip(configs, exts)):

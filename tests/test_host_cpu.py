@@ -254,7 +254,7 @@ def test_plan_many_bitwise_equals_per_set_plan():
         if a.group is not None:  # group arrays SweepBatch packs as one slice per field
             g, k = a.group
             assert g.owns(a, k)
-            assert np.array_equal(g.arrays["chunk_f32"][k], planner.chunk_f32(b.chunk_circ, b.tooth_box))
+            assert np.array_equal(g.arrays["chunk_f32"][k], planner.chunk_f32(b.chunk_circ, b.tooth_box, planner.plan_zfloor(b)))
             assert np.array_equal(g.arrays["tooth_rows"][k], b.tooth_rows)
     assert sum(p.group is not None for p in many) >= 24
     # native planning loops on several threads: the same arrays
@@ -307,7 +307,7 @@ def test_sweep_batch_descriptors_point_at_plan_arrays(monkeypatch):
         p = order[i]
         seen.add(i)
         want = {"tooth_base": p.tooth_base, "tooth_rows": p.tooth_rows, "pts": p.pts, "tooth_box": p.tooth_box,
-                "chunk_circ": p.chunk_circ, "chunk_f32": planner.chunk_f32(p.chunk_circ, p.tooth_box),
+                "chunk_circ": p.chunk_circ, "chunk_f32": planner.chunk_f32(p.chunk_circ, p.tooth_box, planner.plan_zfloor(p)),
                 "pass_x0": p.pass_x0, "min_index": p.min_index.astype(np.int32)}
         for f, a in want.items():
             off = int(row[f]) - base_ptr

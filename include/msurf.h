@@ -20,7 +20,7 @@
 extern "C" {
 #endif
 
-#define MSURF_ABI_VERSION 5
+#define MSURF_ABI_VERSION 6
 
 /* kinematics mode of a sweep launch (uniform across the jobs of one launch) */
 #define MSURF_MODE_REF 0      /* reference composite-matrix order, engine.py:257-296 */
@@ -34,6 +34,9 @@ extern "C" {
  * warp-wide RED.MIN of the main point loops into the buffer armed with
  * msurf_trace_arm (roofline measurement only; much slower) */
 #define MSURF_SWEEP_TRACE 0x200
+/* OR-ed into the mode of msurf_sweep_job (EXT_TILT): eight warps per 64-step
+ * CTA instead of one (phase 2 units of heavy tiles spread over more warps) */
+#define MSURF_SWEEP_WIDE 0x400
 
 #define MSURF_CTR_LIVE_ROWS 0  /* (step, tooth, pass) rows with >= 1 chunk surviving the 2-D cull */
 #define MSURF_CTR_EVAL 1       /* edge points evaluated (points of surviving 32-point chunks)    */
@@ -85,7 +88,16 @@ typedef struct msurf_job {
   double* traj;              /* device [steps][teeth][3] or NULL                      */
   const int32_t* min_index;  /* [teeth] argmin of z' (engine.py:189)                  */
   unsigned long long* counters; /* device [MSURF_NUM_CTRS], accumulated             */
-  int32_t teeth, points, passes, reserved0;
+  /* optional surface-cap cull (EXT_TILT by-value launches): per 32x32-node tile
+   * of this job's slab (row-major, ceil(w/32) tiles per row, w = j_hi-j_lo+1)
+   * an upper bound of (current height - stock height), maintained between
+   * launches by msurf_zcap_refresh; a (step, chunk) whose lowest reachable z'
+   * lies above the bound of every tile it can touch is skipped. NULL = off. */
+  const float* zcap;
+  int32_t teeth, points, passes;
+  int32_t tooth_lo;  /* this launch sweeps teeth [tooth_lo, tooth_lo + tooth_n) ... */
+  int32_t tooth_n;   /* ... of the `teeth` (0: all); per-tooth arrays stay indexed by the tooth */
+  int32_t reserved0;
 } msurf_job;
 
 int msurf_abi_version(void);
@@ -116,6 +128,33 @@ int msurf_sweep(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile_prefi
  * library picks the CTA shape for the mode and sizes the grid itself. Device
  * pointers inside the job are used as in msurf_sweep. */
 int msurf_sweep_job(const msurf_job* job, int32_t mode, int32_t max_points, void* stream);
+
+/* Surface-cap refresh for msurf_job.zcap: for every 32x32-node tile of a
+ * rows x cols slab of keys (row pitch ld), the maximum height minus stock[0]
+ * (device double), rounded up to float, into zcap (row-major tiles,
+ * ceil(cols/32) per row). Heights only decrease during a sweep, so a bound
+ * taken at any earlier moment stays an upper bound. stop_reset (device int,
+ * may be NULL) is zeroed: the flag of the msurf_zcap_watch that follows. */
+int msurf_zcap_refresh(const uint64_t* keys, int64_t ld, int64_t rows, int64_t cols, const double* stock,
+                       float* zcap, int32_t* stop_reset, void* stream);
+
+/* msurf_sweep_job with the surface-cap cull (EXT_TILT): job->zcap must point
+ * at the job's cap tiles. Computes the caps of the (filled) slab, then sweeps
+ * the job (pass, tooth) by (pass, tooth) (mode may include MSURF_SWEEP_WIDE)
+ * refreshing the caps after each launch, so every launch skips the
+ * (step, chunk) pairs that cannot reach below what the earlier ones cut.
+ * stock: device double (the stock height). Results equal msurf_sweep_job's. */
+int msurf_sweep_job_capped(const msurf_job* job, int32_t mode, int32_t max_points, const double* stock,
+                           void* stream);
+/* n_jobs capped jobs (HOST array; disjoint slabs, e.g. the L2 sub-strips of a
+ * surface) swept concurrently on library-owned non-blocking streams forked
+ * from and joined back into `stream` (graph-capturable): each job's (pass,
+ * tooth) launches go round-robin over `depth` streams of its own, so up to
+ * `depth` of them overlap (caps read at most depth - 1 launches stale: a
+ * weaker cull, never another result). n_jobs x depth <= 32.
+ * stocks: HOST array of device pointers to each job's stock height. */
+int msurf_sweep_jobs_capped(const msurf_job* jobs, int32_t n_jobs, int32_t mode, int32_t max_points,
+                            const int64_t* stocks, int32_t depth, void* stream);
 
 /* Decode keys to fp64 heights in place and count machined cells
  * (HeightField.machined_cell_count, surface_grid.py:128-129). Batched over

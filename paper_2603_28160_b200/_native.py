@@ -18,10 +18,11 @@ from .errors import MillsurfError, NativeUnavailableError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MSURF_LIB") or os.path.join(_HERE, "libmsurf.so")
-ABI_VERSION = 5
+ABI_VERSION = 6
 NUM_CTRS = 5
 SWEEP_DIAG = 0x100  # MSURF_SWEEP_DIAG: count deposits/atomics per point
 SWEEP_TRACE = 0x200  # MSURF_SWEEP_TRACE: diagnostics + a trace of every RED.MIN (roofline only)
+SWEEP_WIDE = 0x400  # MSURF_SWEEP_WIDE: eight-warp 64-step CTAs for a tilt by-value launch
 RED_BLOCKS = 1024
 WORK_DOUBLES = RED_BLOCKS * 10  # MSURF_WORK_DOUBLES: reduction scratch per surface
 
@@ -44,8 +45,9 @@ class MsurfJob(ctypes.Structure):
         ("tilt_c", c_double), ("tilt_s", c_double), ("zoff", c_double),
         ("vib_amp", c_double), ("vib_omega", c_double), ("vib_phase", c_double),
         ("trig_table", c_void_p), ("vib_table", c_void_p),
-        ("traj", c_void_p), ("min_index", c_void_p), ("counters", c_void_p),
-        ("teeth", c_int32), ("points", c_int32), ("passes", c_int32), ("reserved0", c_int32),
+        ("traj", c_void_p), ("min_index", c_void_p), ("counters", c_void_p), ("zcap", c_void_p),
+        ("teeth", c_int32), ("points", c_int32), ("passes", c_int32), ("tooth_lo", c_int32),
+        ("tooth_n", c_int32), ("reserved0", c_int32),
     ]
 
 
@@ -76,6 +78,10 @@ EXPORTS = {
     "msurf_decode_strips": (ctypes.c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p,
                                            c_void_p, c_void_p]),
     "msurf_decode": (ctypes.c_int, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p]),
+    "msurf_zcap_refresh": (ctypes.c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
+                                          c_void_p]),
+    "msurf_sweep_job_capped": (ctypes.c_int, [c_void_p, c_int32, c_int32, c_void_p, c_void_p]),
+    "msurf_sweep_jobs_capped": (ctypes.c_int, [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32, c_void_p]),
     "msurf_areal_pass1": (ctypes.c_int, [c_void_p, c_int64, c_int64, c_int32, c_int64, c_int64,
                                          c_int64, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
                                          c_void_p]),

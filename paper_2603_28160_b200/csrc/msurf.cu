@@ -40,6 +40,7 @@ namespace {
 constexpr int kBatchTile = 64, kBatchThreads = 32;   // msurf_sweep (job arrays)
 constexpr int kTiltTile = 64, kTiltThreads = 32;     // msurf_sweep_job, EXT_TILT
 constexpr int kWideTile = 128, kWideThreads = 128;   // msurf_sweep_job, REF / EXT
+constexpr int kCapThreads = 256;                     // msurf_sweep_job_capped (EXT_TILT, 64-step tiles)
 #ifndef MSURF_MIN_BLOCKS_ONE
 #define MSURF_MIN_BLOCKS_ONE 32  // 1-warp CTAs with a by-value job: 64 registers (no spills since the folded locate)
 #endif
@@ -386,9 +387,11 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
                  const unsigned long long* __restrict__ list, unsigned* __restrict__ list_count) {
   constexpr int kTileSteps = TILE;               // time steps per CTA
   constexpr int kSweepThreads = NTHR;            // threads per CTA
-  constexpr int kSubSteps = TILE / NTHR;         // phase-1 steps per thread
+  // phase-1 rounds of NTHR steps; a CTA wider than its tile (NTHR > TILE: more
+  // warps for phase 2) leaves threads >= TILE idle in phase 1
+  constexpr int kSubSteps = TILE >= NTHR ? TILE / NTHR : 1;
   constexpr int kSweepWarps = NTHR / 32;
-  static_assert(TILE % NTHR == 0 && NTHR % 32 == 0, "tile / CTA shape");
+  static_assert((TILE % NTHR == 0 || NTHR % TILE == 0) && NTHR % 32 == 0, "tile / CTA shape");
   constexpr int RW = MODE == MSURF_MODE_REF ? 8 : 4;  // doubles of row data per live step
   // lane = two consecutive live steps (one broadcast point record serves both,
   // half the neighbour exchange in registers): faster for the tilt mode
@@ -452,7 +455,8 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
   // tile -> (pass, tooth, step tile) in 32-bit arithmetic (grids are < 2^31 tiles)
   const unsigned nst = (unsigned)((J.step_hi - J.step_lo + kTileSteps - 1) / kTileSteps);
   int pass, tooth, st;
-  tile_coords((unsigned)local, nst, J.teeth, pass, tooth, st);
+  tile_coords((unsigned)local, nst, J.tooth_n ? J.tooth_n : J.teeth, pass, tooth, st);
+  tooth += J.tooth_lo;  // a launch may cover a tooth range; per-tooth arrays are indexed by the tooth
   const int npts = J.points;
   const int nchunk = (npts + 31) >> 5;
   const double dd = J.spacing;
@@ -471,6 +475,23 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
   const double cx0 = 0.5 - J.x_min * inv;
   const double cy0 = 0.5 - J.y_min * inv;
 
+  // surface-cap cull (msurf_job.zcap; tilt by-value launches, not in the
+  // DIAG=1 counting variant): cell coordinates of a chunk's workpiece box
+  // from its window-relative centre, and the tile grid of the job's slab
+  const bool zc_on = (DIAG != 1) && ONE && MODE == MSURF_MODE_EXT_TILT && J.zcap != nullptr;
+  float zc_k = 0.f, zc_bi = 0.f, zc_bj = 0.f;
+  int zc_imax = 0, zc_jmax = 0, zc_tw = 0;
+  if (zc_on) {
+    const double wxc0 = J.x_min + 0.5 * (double)J.m * dd;
+    const double wyc0 = J.y_min + 0.5 * (double)(J.j_lo + J.j_hi) * dd;
+    zc_k = (float)inv;
+    zc_bi = (float)((wxc0 - J.x_min) * inv + 0.5);
+    zc_bj = (float)((wyc0 - J.y_min) * inv + 0.5 - (double)J.j_lo);
+    zc_imax = (int)J.m;
+    zc_jmax = (int)(J.j_hi - J.j_lo);
+    zc_tw = (zc_jmax >> 5) + 1;
+  }
+
   // ---------------- phase 1: one thread per time step (kSubSteps rounds of
   // kSweepThreads steps), live steps appended in time order
   int n_live = 0;
@@ -484,10 +505,12 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
       const double wx_hi = J.x_min + (double)J.m * dd + 1.5 * dd;
       const double wy_lo = J.y_min + (double)J.j_lo * dd - 1.5 * dd;
       const double wy_hi = J.y_min + (double)J.j_hi * dd + 1.5 * dd;
+      const bool tin = TILE >= NTHR || tid < TILE;
       const long long s = J.step_lo + (long long)st * kTileSteps + h * kSweepThreads + tid;
-      uint64_t* my_mask = masks + tid * mask_words;
-      for (int w = 0; w < mask_words; ++w) my_mask[w] = 0ull;
-      if (s < J.step_hi) {
+      uint64_t* my_mask = masks + (tin ? tid : 0) * mask_words;
+      if (tin)
+        for (int w = 0; w < mask_words; ++w) my_mask[w] = 0ull;
+      if (tin && s < J.step_hi) {
         // engine.py:240-241, kinematics.py:77 — one rounding per op, no FMA
         const double t = __dadd_rn(J.t_start, __dmul_rn((double)s, J.dt));
         const double ty = __dadd_rn(J.y0, __dmul_rn(J.feed_speed, t));
@@ -592,6 +615,8 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
             // initial height, so skipping it never changes a result. Same fp32
             // margin as the position tests.
             const float tsz = MODE == MSURF_MODE_EXT_TILT ? tsf : 0.0f;
+            int zc_last = -1;  // the lane's last cap lookup (tile range key, value)
+            float zc_cap = 0.f;
             unsigned kept = 0;
             for (int q = 0; q < nchunk; ++q) {
               const float4 a = __ldg(cf4 + 2 * q);
@@ -599,7 +624,33 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
               const float uc = fmaf(cf, a.x, sf * a.y);
               const float vc = fmaf(cf, a.y, -(sf * a.x));
               bool hit = (fabsf(uc + oxf) <= hx + a.z) & (fabsf(fmaf(tcc, vc, bz.x) + oyf) <= hy + a.w);
-              if (DIAG != 1) hit &= fmaf(tsz, vc, bz.z) <= 4e-6f * (rt_f + fabsf(bz.z)) + 1e-6f;
+              const float zmg = 4e-6f * (rt_f + fabsf(bz.z)) + 1e-6f;
+              const float zlow = fmaf(tsz, vc, bz.z);  // lowest reachable z' - stock, this step
+              if (DIAG != 1) hit &= zlow <= zmg;
+              if (zc_on && hit) {
+                // surface cap: the highest current height (- stock) over every 32x32
+                // tile the chunk's box can touch, +-1.5 cells for the fp32 roundings
+                // (~1e-3 cell); an empty range means no in-grid cell at all. The caps
+                // are rewritten concurrently by zcap_watch_kernel (L2 loads; any
+                // value read is an upper bound), and consecutive chunks of a step
+                // mostly touch the same tiles: the lane reuses its last lookup.
+                const float ci = fmaf(uc + oxf, zc_k, zc_bi), cj = fmaf(fmaf(tcc, vc, bz.x) + oyf, zc_k, zc_bj);
+                const float ri = fmaf(a.z, zc_k, 1.5f), rj = fmaf(a.w, zc_k, 1.5f);
+                const int i0 = max(0, __float2int_rd(ci - ri)) >> 5, i1 = min(zc_imax, __float2int_rd(ci + ri)) >> 5;
+                const int j0 = max(0, __float2int_rd(cj - rj)) >> 5, j1 = min(zc_jmax, __float2int_rd(cj + rj)) >> 5;
+                // exact key of the tile range (tile indices < 2^13, spans <= 3); others uncached
+                const bool cacheable = (i1 - i0) >= 0 && (i1 - i0) <= 3 && (j1 - j0) >= 0 && (j1 - j0) <= 3 &&
+                                       i0 < 8192 && j0 < 8192;
+                const int key = cacheable ? ((i0 << 17) | (j0 << 4) | ((i1 - i0) << 2) | (j1 - j0)) : -2;
+                if (key < 0 || key != zc_last) {
+                  float cap = -INFINITY;
+                  for (int ti = i0; ti <= i1; ++ti)
+                    for (int tj = j0; tj <= j1; ++tj) cap = fmaxf(cap, __ldcg(J.zcap + ti * zc_tw + tj));
+                  zc_last = key;
+                  zc_cap = cap;
+                }
+                hit = zlow <= zc_cap + zmg;
+              }
               if (hit) {
                 my_mask[q >> 6] |= 1ull << (q & 63);
                 kept += (q == nchunk - 1) ? (unsigned)(npts - 32 * q) : 32u;
@@ -1046,7 +1097,8 @@ __global__ void __launch_bounds__(256)
     const unsigned local = (unsigned)(t - prefix[lo]);
     const unsigned nst = (unsigned)((J.step_hi - J.step_lo + TILE - 1) / TILE);
     int pass, tooth, st;
-    tile_coords(local, nst, J.teeth, pass, tooth, st);
+    tile_coords(local, nst, J.tooth_n ? J.tooth_n : J.teeth, pass, tooth, st);
+    tooth += J.tooth_lo;
     live = tile_may_hit<MODE, TILE>(J, pass, tooth, st);
     entry = ((unsigned long long)lo << 32) | local;
   }
@@ -1638,6 +1690,35 @@ __global__ void __launch_bounds__(256)
     if (h[i]) atomicAdd(hist + i, h[i]);
 }
 
+// msurf_zcap_refresh: one CTA per 32x32-node tile of a slab, max key ->
+// height - stock rounded up to float (an upper bound for the cull)
+__global__ void __launch_bounds__(256)
+    zcap_kernel(const uint64_t* __restrict__ keys, long long ld, long long rows, long long cols,
+                const double* __restrict__ stock, float* __restrict__ zcap, int* stop_reset) {
+  if (stop_reset && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *stop_reset = 0;
+  __shared__ unsigned long long wmax[8];
+  const long long i0 = (long long)blockIdx.y * 32, j = (long long)blockIdx.x * 32 + (threadIdx.x & 31);
+  unsigned long long m = 0ull;
+  if (j < cols)
+    for (long long i = i0 + (threadIdx.x >> 5); i < i0 + 32 && i < rows; i += 8) {
+      const unsigned long long k = keys[i * ld + j];
+      m = k > m ? k : m;
+    }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
+    m = v > m ? v : m;
+  }
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) m = wmax[w] > m ? wmax[w] : m;
+    m = wmax[0] > m ? wmax[0] : m;
+    const float v = m ? __double2float_ru(__dsub_ru(dec_key(m), stock[0])) : -INFINITY;
+    zcap[(long long)blockIdx.y * gridDim.x + blockIdx.x] = v;
+  }
+}
+
 // smem of one sweep CTA: transforms + masks by thread + masks by slot
 inline size_t sweep_smem(int tile, int mask_words) {
   return (size_t)tile * 8 * sizeof(double) + (size_t)2 * tile * mask_words * sizeof(uint64_t);
@@ -1672,18 +1753,21 @@ cudaError_t launch_shape(int64_t n_tiles, cudaStream_t st, const msurf_job* jobs
 
 // tiles of one job for a tile size: passes * teeth * ceil(window / tile)
 inline int64_t job_tiles(const msurf_job& j, int tile) {
-  return (int64_t)j.passes * j.teeth * ((j.step_hi - j.step_lo + tile - 1) / tile);
+  return (int64_t)j.passes * (j.tooth_n ? j.tooth_n : j.teeth) * ((j.step_hi - j.step_lo + tile - 1) / tile);
 }
 
 template <int MODE, int DIAG>
 cudaError_t launch_sweep(int64_t n_tiles, cudaStream_t st, const msurf_job* jobs, int n_jobs,
                          const int64_t* prefix, int mask_words, const msurf_job* one, unsigned long long* list,
-                         unsigned* count) {
+                         unsigned* count, bool wide) {
   if (one) {
-    if constexpr (MODE == MSURF_MODE_EXT_TILT)
+    if constexpr (MODE == MSURF_MODE_EXT_TILT) {
+      if (wide)  // eight warps over 64 steps: heavy tiles finish sooner (short surface-cap launches)
+        return launch_shape<MODE, DIAG, true, kTiltTile, kCapThreads>(job_tiles(*one, kTiltTile), st, nullptr, 1,
+                                                                     nullptr, mask_words, *one, nullptr, nullptr);
       return launch_shape<MODE, DIAG, true, kTiltTile, kTiltThreads>(job_tiles(*one, kTiltTile), st, nullptr, 1,
                                                                     nullptr, mask_words, *one, nullptr, nullptr);
-    else
+    } else
       return launch_shape<MODE, DIAG, true, kWideTile, kWideThreads>(job_tiles(*one, kWideTile), st, nullptr, 1,
                                                                     nullptr, mask_words, *one, nullptr, nullptr);
   }
@@ -1787,14 +1871,15 @@ static int sweep_impl(const msurf_job* jobs, int32_t n_jobs, const int64_t* tile
   cudaError_t e = cudaSuccess;
   const bool diag = (mode & MSURF_SWEEP_DIAG) != 0;
   const bool trace = (mode & MSURF_SWEEP_TRACE) != 0;
+  const bool wide = (mode & MSURF_SWEEP_WIDE) != 0;
   // scratch: [0, 8) tile count and work cursor, then the tile list (8 bytes per tile)
   unsigned* count = static_cast<unsigned*>(scratch);
   unsigned long long* list = scratch ? static_cast<unsigned long long*>(scratch) + 1 : nullptr;
 #define MSURF_LAUNCH(M)                                                                                   \
-  e = trace ? launch_sweep<M, 2>(n_tiles, st, jobs, n_jobs, tile_prefix, mask_words, one, list, count)   \
-      : diag  ? launch_sweep<M, 1>(n_tiles, st, jobs, n_jobs, tile_prefix, mask_words, one, list, count)   \
-              : launch_sweep<M, 0>(n_tiles, st, jobs, n_jobs, tile_prefix, mask_words, one, list, count)
-  switch (mode & ~(MSURF_SWEEP_DIAG | MSURF_SWEEP_TRACE)) {
+  e = trace ? launch_sweep<M, 2>(n_tiles, st, jobs, n_jobs, tile_prefix, mask_words, one, list, count, wide)   \
+      : diag  ? launch_sweep<M, 1>(n_tiles, st, jobs, n_jobs, tile_prefix, mask_words, one, list, count, wide)   \
+              : launch_sweep<M, 0>(n_tiles, st, jobs, n_jobs, tile_prefix, mask_words, one, list, count, wide)
+  switch (mode & ~(MSURF_SWEEP_DIAG | MSURF_SWEEP_TRACE | MSURF_SWEEP_WIDE)) {
     case MSURF_MODE_REF: MSURF_LAUNCH(MSURF_MODE_REF); break;
     case MSURF_MODE_EXT: MSURF_LAUNCH(MSURF_MODE_EXT); break;
     case MSURF_MODE_EXT_TILT: MSURF_LAUNCH(MSURF_MODE_EXT_TILT); break;
@@ -1838,6 +1923,119 @@ int msurf_red_lines(const uint32_t* trace, int64_t n_records, unsigned long long
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   red_lines_kernel<<<(unsigned)sms * 8, 256, 0, (cudaStream_t)stream>>>(trace, n_records, hist);
   return check_launch("red_lines_kernel");
+}
+
+int msurf_zcap_refresh(const uint64_t* keys, int64_t ld, int64_t rows, int64_t cols, const double* stock,
+                       float* zcap, int32_t* stop_reset, void* stream) {
+  if (!keys || !stock || !zcap || rows < 1 || cols < 1 || ld < cols) return set_err("msurf_zcap_refresh: bad arguments");
+  const long long ti = (rows + 31) / 32, tj = (cols + 31) / 32;
+  if (ti > 65535 || tj > 0x7fffffffLL) return set_err("msurf_zcap_refresh: slab too large");
+  zcap_kernel<<<dim3((unsigned)tj, (unsigned)ti), 256, 0, (cudaStream_t)stream>>>(keys, ld, rows, cols, stock, zcap,
+                                                                                 stop_reset);
+  return check_launch("zcap_kernel");
+}
+
+int msurf_sweep_job_capped(const msurf_job* job, int32_t mode, int32_t max_points, const double* stock,
+                           void* stream) {
+  if (!job || !job->zcap || !stock || max_points < 1) return set_err("msurf_sweep_job_capped: bad arguments");
+  const long long rows = job->m + 1, cols = job->j_hi - job->j_lo + 1;
+  float* zcap = const_cast<float*>(job->zcap);
+  const int teeth = job->tooth_n ? job->tooth_n : job->teeth;
+  const int n = job->passes * teeth;
+  // caps of the freshly filled slab, then (pass, tooth) by (pass, tooth) with
+  // the caps refreshed after every launch but the last
+  if (msurf_zcap_refresh(job->keys, job->ld, rows, cols, stock, zcap, nullptr, stream)) return 1;
+  for (int i = 0; i < n; ++i) {
+    msurf_job sub = *job;
+    sub.passes = 1;
+    sub.pass_x0 = job->pass_x0 + i / teeth;
+    sub.tooth_lo = job->tooth_lo + i % teeth;
+    sub.tooth_n = 1;
+    if (job_tiles(sub, 64) == 0) continue;
+    if (sweep_impl(nullptr, 1, nullptr, 0, mode, max_points, stream, &sub, nullptr)) return 1;
+    if (i + 1 < n && msurf_zcap_refresh(job->keys, job->ld, rows, cols, stock, zcap, nullptr, stream)) return 1;
+  }
+  return 0;
+}
+
+// library-owned non-blocking streams (no implicit synchronisation with any
+// other stream, the legacy one included), per device and thread
+cudaStream_t lib_stream(int k) {
+  constexpr int kMax = 32;
+  static thread_local cudaStream_t pool[64][kMax] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || k < 0 || k >= kMax) return nullptr;
+  if (!pool[dev][k] && cudaStreamCreateWithFlags(&pool[dev][k], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  return pool[dev][k];
+}
+
+int msurf_sweep_jobs_capped(const msurf_job* jobs, int32_t n_jobs, int32_t mode, int32_t max_points,
+                            const int64_t* stocks, int32_t depth, void* stream) {
+  if (!jobs || n_jobs < 1 || !stocks || max_points < 1 || depth < 1)
+    return set_err("msurf_sweep_jobs_capped: bad arguments");
+  // fork: job k's (pass, tooth) launches round-robin over `depth` library
+  // streams of its own (launch i waits for launch i - depth and the cap refresh
+  // after it; neighbours overlap, reading caps at most depth - 1 launches
+  // stale, which only weakens the cull); jobs write disjoint slabs. Every
+  // stream is joined back into `stream` (graph-capturable fork/join).
+  const int ns = n_jobs * depth;
+  if (ns > 32) return set_err("msurf_sweep_jobs_capped: too many jobs x depth");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaEvent_t fork = nullptr;
+  if (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) return set_err("events");
+  cudaEventRecord(fork, st);
+  int rc = 0;
+  for (int k = 0; k < ns; ++k) {
+    cudaStream_t q = lib_stream(k);
+    if (!q) {
+      rc = set_err("msurf_sweep_jobs_capped: stream");
+      break;
+    }
+    cudaStreamWaitEvent(q, fork, 0);
+  }
+  for (int j = 0; j < n_jobs && rc == 0; ++j) {
+    const msurf_job* job = jobs + j;
+    const double* stock = reinterpret_cast<const double*>(stocks[j]);
+    if (!job->zcap || !stock) {
+      rc = set_err("msurf_sweep_jobs_capped: job without caps");
+      break;
+    }
+    const long long rows = job->m + 1, cols = job->j_hi - job->j_lo + 1;
+    float* zcap = const_cast<float*>(job->zcap);
+    const int teeth = job->tooth_n ? job->tooth_n : job->teeth;
+    const int n = job->passes * teeth;
+    cudaStream_t q0 = lib_stream(j * depth);
+    // caps of the freshly filled slab first, seen by every stream of the job
+    rc = msurf_zcap_refresh(job->keys, job->ld, rows, cols, stock, zcap, nullptr, q0);
+    cudaEvent_t ready = nullptr;
+    if (rc == 0 && cudaEventCreateWithFlags(&ready, cudaEventDisableTiming) == cudaSuccess) {
+      cudaEventRecord(ready, q0);
+      for (int d = 1; d < depth; ++d) cudaStreamWaitEvent(lib_stream(j * depth + d), ready, 0);
+      cudaEventDestroy(ready);
+    }
+    for (int i = 0; i < n && rc == 0; ++i) {
+      cudaStream_t q = lib_stream(j * depth + i % depth);
+      msurf_job sub = *job;
+      sub.passes = 1;
+      sub.pass_x0 = job->pass_x0 + i / teeth;
+      sub.tooth_lo = job->tooth_lo + i % teeth;
+      sub.tooth_n = 1;
+      if (job_tiles(sub, 64) == 0) continue;
+      rc = sweep_impl(nullptr, 1, nullptr, 0, mode, max_points, q, &sub, nullptr);
+      if (rc == 0 && i + 1 < n) rc = msurf_zcap_refresh(job->keys, job->ld, rows, cols, stock, zcap, nullptr, q);
+    }
+  }
+  for (int k = 0; k < ns; ++k) {  // joins are enqueued whatever happened
+    cudaStream_t q = lib_stream(k);
+    cudaEvent_t join = nullptr;
+    if (!q || cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess) continue;
+    cudaEventRecord(join, q);
+    cudaStreamWaitEvent(st, join, 0);
+    cudaEventDestroy(join);
+  }
+  cudaEventDestroy(fork);
+  return rc;
 }
 
 int msurf_decode(uint64_t* keys, int64_t count, int32_t n_surf, const double* sentinel,

@@ -26,7 +26,7 @@ from . import _native
 from .errors import ConfigError, MillsurfError
 from .extensions import Extensions
 from .grid import GridSpec, HeightField, TrajectoryRecord
-from .planner import (DEVICE_FIELDS, MODE_REF, SweepPlan, chunk_f32, plan, plan_many, plan_zfloor, step_window,
+from .planner import (DEVICE_FIELDS, MODE_EXT_TILT, MODE_REF, SweepPlan, chunk_f32, plan, plan_many, plan_zfloor, step_window,
                       time_step)
 
 DEFAULT_MAX_STEP_ANGLE_RAD = math.radians(0.5)
@@ -40,6 +40,18 @@ L2_TILE_BYTES = int(float(__import__("os").environ.get("MSURF_L2_TILE_MB", "48")
 # config 3 in launch groups of 32 sets, 2.1 -> 1.2 ms per group)
 ONE_JOB_LAUNCH_MAX = int(__import__("os").environ.get("MSURF_ONE_JOB_MAX", "32"))
 ONE_JOB_MIN_TILES = int(__import__("os").environ.get("MSURF_ONE_JOB_MIN_TILES", "16384"))
+
+
+# surface-cap cull (msurf_job.zcap) for tilt-mode by-value jobs: swept (pass,
+# tooth) by (pass, tooth) with a per-tile upper bound of the current heights
+# refreshed in between (MSURF_ZCAP=0 turns it off; result-neutral either way)
+ZCAP = __import__("os").environ.get("MSURF_ZCAP", "1") != "0"
+# eight-warp CTAs for capped launches (measured slower once launches overlap)
+ZCAP_WIDE = __import__("os").environ.get("MSURF_ZCAP_WIDE", "0") != "0"
+ZCAP_MIN_JOBS = int(__import__("os").environ.get("MSURF_ZCAP_MIN_JOBS", "2"))  # capped jobs swept side by side
+# overlapping (pass, tooth) launches per capped job (measured on config 5: depth
+# 1 / 2 / 3 / 4 -> 27.1 / 20.5 / 20.3 / 20.9 ms; no cap 37.3 ms)
+ZCAP_DEPTH = int(__import__("os").environ.get("MSURF_ZCAP_DEPTH", "3"))
 
 
 def _per_job_launches(tiles) -> bool:
@@ -340,8 +352,8 @@ class SweepBatch:
                         p.tilt_c, p.tilt_s, p.zoff, p.vib_amp, p.vib_omega, p.vib_phase,
                         base + o["trig_table"] if "trig_table" in o else 0,
                         base + o["vib_table"] if "vib_table" in o else 0,
-                        tr, base + o["min_index"], base + self.ctr_off + i * _native.NUM_CTRS * 8,
-                        p.teeth, p.points, p.passes, 0))
+                        tr, base + o["min_index"], base + self.ctr_off + i * _native.NUM_CTRS * 8, 0,
+                        p.teeth, p.points, p.passes, 0, 0, 0))
                 arr = np.array(rows, dtype=_native.JOB_DTYPE)
                 if job_off is not None:
                     out.append((job_off, arr.view(np.uint8)))
@@ -361,7 +373,65 @@ class SweepBatch:
         need = max((gm[4] for gm, pj in zip(self.group_meta, self.group_per_job) if not pj), default=0)
         self.sweep_scratch = torch.empty(need + 1, dtype=torch.int64, device=self.dev) if need else None
         sweeps = sum((sum(1 for t in tl if t) if pj else 1) for pj, tl in zip(self.group_per_job, self.group_tiles))
-        self.launches_per_run = 2 * (1 if self.batched_fill else n) + sweeps
+        self.zc_seq = self._build_zcap_sequences()
+        # a capped job: n = passes x teeth sweeps and n refreshes instead of one launch
+        extra = sum(2 * q[0] - 1 for seqs in self.zc_seq for q in seqs if q is not None)
+        self.launches_per_run = 2 * (1 if self.batched_fill else n) + sweeps + extra
+
+    def _build_zcap_sequences(self):
+        """Per launch group, per job: None, or the surface-cap state of a
+        tilt-mode by-value job of more than one (pass, tooth) — its cap tile
+        array, slab geometry and stock pointer (msurf_sweep_job_capped)."""
+        torch = self.torch
+        out = []
+        for g, (mode, jidx, _, _, _, _) in enumerate(self.group_meta):
+            seqs = [None] * len(jidx)
+            if ZCAP and self.group_per_job[g] and mode == MODE_EXT_TILT:
+                host = self.group_host_jobs[g]
+                for k, jn in enumerate(jidx):
+                    i, lo, hi, _, _ = self.jobs[jn]
+                    p = self.surfs[i].plan
+                    if p.passes * p.teeth < 2 or not self.group_tiles[g][k]:
+                        continue
+                    rows, cols = p.grid.m + 1, hi - lo + 1
+                    zc = torch.zeros(((rows + 31) // 32) * ((cols + 31) // 32), dtype=torch.float32, device=self.dev)
+                    host[k]["zcap"] = zc.data_ptr()
+                    seqs[k] = (p.passes * p.teeth, zc, int(host[k]["keys"]), int(host[k]["ld"]), rows, cols,
+                               self.base + self.sentinel_off + 8 * i)
+                # the (pass, tooth) launches of one job are short and underfill the
+                # GPU; they pay only when several jobs (L2 sub-strips) run side by
+                # side (measured: config 5, 3 sub-strips: 37.3 -> 26.6 ms; config 2,
+                # one job: 0.68 -> 1.2 ms)
+                if sum(q is not None for q in seqs) < ZCAP_MIN_JOBS:
+                    for k, q in enumerate(seqs):
+                        if q is not None:
+                            host[k]["zcap"] = 0
+                    seqs = [None] * len(jidx)
+            out.append(seqs)
+        return out
+
+    def _launch_capped(self, g: int, ks, mode: int, flag: int, max_pts: int, sp: int) -> None:
+        """Surface-cap jobs ks of by-value group g, concurrently (msurf_sweep_jobs_capped)."""
+        host = self.group_host_jobs[g]
+        arr = np.ascontiguousarray(host[ks])
+        stocks = np.array([self.zc_seq[g][k][-1] for k in ks], dtype=np.int64)
+        wide = _native.SWEEP_WIDE if ZCAP_WIDE else 0
+        depth = max(1, min(ZCAP_DEPTH, 32 // len(ks)))
+        _native.check(self.lib.msurf_sweep_jobs_capped(arr.ctypes.data, len(ks), mode | flag | wide, max_pts,
+                                                       stocks.ctypes.data, depth, sp))
+
+    def _launch_job(self, g: int, k: int, mode: int, flag: int, max_pts: int, sp: int) -> None:
+        """Job k of by-value launch group g (a surface-cap job through
+        msurf_sweep_job_capped: (pass, tooth) launches with cap refreshes)."""
+        lib, sz = self.lib, _native.JOB_DTYPE.itemsize
+        job = self.group_host_jobs[g].ctypes.data + k * sz
+        seq = self.zc_seq[g][k]
+        if seq is None:
+            _native.check(lib.msurf_sweep_job(job, mode | flag, max_pts, sp))
+            return
+        stock = seq[-1]
+        wide = _native.SWEEP_WIDE if ZCAP_WIDE else 0
+        _native.check(lib.msurf_sweep_job_capped(job, mode | flag | wide, max_pts, stock, sp))
 
     # ------------------------------------------------------------------
     def launch_fill(self, sp: int) -> None:
@@ -386,11 +456,14 @@ class SweepBatch:
             flag = self._sweep_flag()
             if self.group_per_job[g]:
                 # one job, or the L2 sub-strips of a large surface: one launch per job
-                # with the descriptor passed by value (constant-bank operands)
-                ptr, sz = self.group_host_jobs[g].ctypes.data, _native.JOB_DTYPE.itemsize
+                # with the descriptor passed by value (constant-bank operands); the
+                # surface-cap jobs of the group run concurrently, one stream each
+                capped = [k for k, t in enumerate(self.group_tiles[g]) if t and self.zc_seq[g][k] is not None]
                 for k, t in enumerate(self.group_tiles[g]):
-                    if t:
-                        _native.check(lib.msurf_sweep_job(ptr + k * sz, mode | flag, max_pts, sp))
+                    if t and self.zc_seq[g][k] is None:
+                        self._launch_job(g, k, mode, flag, max_pts, sp)
+                if capped:
+                    self._launch_capped(g, capped, mode, flag, max_pts, sp)
                 continue
             _native.check(lib.msurf_sweep(base + job_off, len(idx), base + pre_off, n_tiles, mode | flag,
                                           max_pts, self.sweep_scratch.data_ptr(), sp))
@@ -504,10 +577,15 @@ class SweepBatch:
         covered = sum(len(by_lo.get(s.j_lo + s.col0[q], ())) for q in range(s.n_strips))
         if covered != len(jidx):
             raise ConfigError(f"launch_by_strip: {len(jidx) - covered} sweep jobs start at no strip boundary")
+        # surface-cap jobs run side by side (one joined call) before the strip loop:
+        # their decodes and copies then follow, no longer overlapping the sweep
+        capped = [k for k, t in enumerate(self.group_tiles[0]) if t and self.zc_seq[0][k] is not None]
+        if capped:
+            self._launch_capped(0, capped, mode, flag, max_pts, sp)
         for q in range(s.n_strips):
             for k in by_lo.get(s.j_lo + s.col0[q], ()):
-                if self.group_tiles[0][k]:
-                    _native.check(lib.msurf_sweep_job(ptr + k * sz, mode | flag, max_pts, sp))
+                if self.group_tiles[0][k] and self.zc_seq[0][k] is None:
+                    self._launch_job(0, k, mode, flag, max_pts, sp)
             _native.check(lib.msurf_decode_strips(
                 self.strip_keys.data_ptr() + s.strip_off * 8, self.keys.data_ptr() + s.key_off * 8, rows, w_all,
                 1, base + self.offs[i]["col0"] + 8 * q, base + self.sentinel_off + 8 * i,

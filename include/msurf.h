@@ -20,12 +20,13 @@
 extern "C" {
 #endif
 
-#define MSURF_ABI_VERSION 6
+#define MSURF_ABI_VERSION 7
 
 /* kinematics mode of a sweep launch (uniform across the jobs of one launch) */
 #define MSURF_MODE_REF 0      /* reference composite-matrix order, engine.py:257-296 */
 #define MSURF_MODE_EXT 1      /* rotated tool-frame points, z' time-invariant   */
 #define MSURF_MODE_EXT_TILT 2 /* rotated tool-frame points + lead tilt (z' per step) */
+#define MSURF_MODE_MASK 0xff  /* the kinematics mode bits of a mode word */
 /* OR-ed into the mode of msurf_sweep: also count the per-point diagnostics
  * MSURF_CTR_DEPOSITS / MSURF_CTR_ATOMICS (two extra integer ops per point;
  * without it those two counters stay zero) */
@@ -94,6 +95,11 @@ typedef struct msurf_job {
    * launches by msurf_zcap_refresh; a (step, chunk) whose lowest reachable z'
    * lies above the bound of every tile it can touch is skipped. NULL = off. */
   const float* zcap;
+  /* optional staging (set by msurf_sweep_jobs_capped for its EXT_TILT
+   * launches, NULL otherwise): phase 1 writes each live tile's rows and chunk
+   * masks plus the list of live (tile, chunk) units here, and a second,
+   * persistent kernel balances phase 2 over all warps of the GPU */
+  void* stage;
   int32_t teeth, points, passes;
   int32_t tooth_lo;  /* this launch sweeps teeth [tooth_lo, tooth_lo + tooth_n) ... */
   int32_t tooth_n;   /* ... of the `teeth` (0: all); per-tooth arrays stay indexed by the tooth */
@@ -154,7 +160,12 @@ int msurf_sweep_job_capped(const msurf_job* job, int32_t mode, int32_t max_point
  * weaker cull, never another result). n_jobs x depth <= 32.
  * stocks: HOST array of device pointers to each job's stock height. */
 int msurf_sweep_jobs_capped(const msurf_job* jobs, int32_t n_jobs, int32_t mode, int32_t max_points,
-                            const int64_t* stocks, int32_t depth, void* stream);
+                            const int64_t* stocks, int32_t depth, void* stage, int64_t stage_each, void* stream);
+/* With `stage` (device, n_jobs x depth buffers of stage_each >= msurf_stage_bytes
+ * bytes) the production launches run staged: phase 1 of every tile writes
+ * its rows, masks and live (tile, chunk) units there, then a persistent
+ * kernel balances phase 2 over every warp. NULL: the single-kernel form. */
+int msurf_stage_bytes(const msurf_job* job, int32_t max_points, int64_t* bytes);
 
 /* Decode keys to fp64 heights in place and count machined cells
  * (HeightField.machined_cell_count, surface_grid.py:128-129). Batched over

@@ -18,7 +18,7 @@ from .errors import MillsurfError, NativeUnavailableError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MSURF_LIB") or os.path.join(_HERE, "libmsurf.so")
-ABI_VERSION = 6
+ABI_VERSION = 7
 NUM_CTRS = 5
 SWEEP_DIAG = 0x100  # MSURF_SWEEP_DIAG: count deposits/atomics per point
 SWEEP_TRACE = 0x200  # MSURF_SWEEP_TRACE: diagnostics + a trace of every RED.MIN (roofline only)
@@ -46,6 +46,7 @@ class MsurfJob(ctypes.Structure):
         ("vib_amp", c_double), ("vib_omega", c_double), ("vib_phase", c_double),
         ("trig_table", c_void_p), ("vib_table", c_void_p),
         ("traj", c_void_p), ("min_index", c_void_p), ("counters", c_void_p), ("zcap", c_void_p),
+        ("stage", c_void_p),
         ("teeth", c_int32), ("points", c_int32), ("passes", c_int32), ("tooth_lo", c_int32),
         ("tooth_n", c_int32), ("reserved0", c_int32),
     ]
@@ -81,7 +82,9 @@ EXPORTS = {
     "msurf_zcap_refresh": (ctypes.c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                                           c_void_p]),
     "msurf_sweep_job_capped": (ctypes.c_int, [c_void_p, c_int32, c_int32, c_void_p, c_void_p]),
-    "msurf_sweep_jobs_capped": (ctypes.c_int, [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32, c_void_p]),
+    "msurf_sweep_jobs_capped": (ctypes.c_int, [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32, c_void_p,
+                                               c_int64, c_void_p]),
+    "msurf_stage_bytes": (ctypes.c_int, [c_void_p, c_int32, ctypes.POINTER(c_int64)]),
     "msurf_areal_pass1": (ctypes.c_int, [c_void_p, c_int64, c_int64, c_int32, c_int64, c_int64,
                                          c_int64, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
                                          c_void_p]),

@@ -379,8 +379,116 @@ __device__ __forceinline__ bool tile_may_hit(const msurf_job& J, int pass, int t
                                  (float)J.tilt_c, (float)J.tilt_s);
 }
 
+// One phase-2 unit of the paired-step (tilt) loop: chunk q's up-to-32 points
+// under the lane's two consecutive live steps A, B (transforms ra / rb, the
+// chunk live at them: on_a / on_b; xa / xb -> each step's (x offset, feed
+// position) for the exact path). Called by the sweep kernel on its own
+// shared-memory rows and by sweep_units_kernel on staged ones.
+template <int MODE, int DIAG>
+__device__ __forceinline__ void pair_unit(const msurf_job& J, const double4* __restrict__ pts, double4* ptstage,
+                                          const double* ra, const double* rb, bool on_a, bool on_b,
+                                          const double* xrows, int xstride, int rta, int rtb, int q, int npts, int lane,
+                                          double inv, double cx0, double cy0, unsigned span_i, unsigned span_j,
+                                          int jbias, int j_lo, int ldk, unsigned long long* __restrict__ keys,
+                                          double tilt_c, double tilt_s, double dd, unsigned& n_dep, unsigned& n_atom) {
+  const int ibias_a = on_a ? kMagicHi : kMagicHi - (1 << 30);
+  const int ibias_b = on_b ? kMagicHi : kMagicHi - (1 << 30);
+  const int p_end = min(32, npts - q * 32);
+  // stage the chunk's 32 point records (1 KB, coalesced) for broadcast
+  // reads; slots past the chunk's end hold zeros (finite, masked below)
+  __syncwarp();
+  {
+    double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (lane < p_end) {
+      const double2* src = reinterpret_cast<const double2*>(pts + q * 32 + lane);
+      const double2 a = __ldg(src), b = __ldg(src + 1);
+      v = make_double4(a.x, a.y, b.x, b.y);
+    }
+    ptstage[lane] = v;
+  }
+  __syncwarp();
+  // Near-boundary points (probability ~1e-9 each) are not resolved inline:
+  // they are flagged, kept out of the neighbour comparisons (treated as
+  // outside), and deposited after the chunk with the exact reference index
+  // — an extra deposit is always safe, a skipped one never is.
+  bool anynear = false;
+  // one point per iteration evaluated under both of the lane's steps (two
+  // independent fp64 chains). Neighbours in time: A's predecessor is the
+  // previous lane's B, B's successor the next lane's A (two shuffles each),
+  // A-B within the lane in registers. The edge lanes get their own values
+  // back from the shuffles, i.e. compare with their other step, which is a
+  // neighbour anyway: no lane tests in the tilt filter.
+#pragma unroll kKUnroll
+  for (int k = 0; k < p_end; ++k) {
+    const double4 pt = ptstage[k];
+    PointEval ea = eval_point<MODE>(pt, ra, inv, cx0, cy0, tilt_c, tilt_s);
+    PointEval eb = eval_point<MODE>(pt, rb, inv, cx0, cy0, tilt_c, tilt_s);
+    const int ia = ea.hi_x - ibias_a, ja = ea.hi_y - jbias;
+    const int ib = eb.hi_x - ibias_b, jb = eb.hi_y - jbias;
+    anynear |= (ea.near & on_a) | (eb.near & on_b);
+    const bool in_a = ((unsigned)ia <= span_i) & ((unsigned)ja <= span_j) & !ea.near;
+    const bool in_b = ((unsigned)ib <= span_i) & ((unsigned)jb <= span_j) & !eb.near;
+    const int idx_a = in_a ? ia * ldk + ja : -1;
+    const int idx_b = in_b ? ib * ldk + jb : -1;
+    const int idx_bp = __shfl_up_sync(0xffffffffu, idx_b, 1);  // A's predecessor (lane 0: own B)
+    bool dep_a, dep_b;
+    if (MODE == MSURF_MODE_EXT_TILT) {
+      const unsigned zh_bp = __shfl_up_sync(0xffffffffu, eb.zh, 1);
+      const int idx_an = __shfl_down_sync(0xffffffffu, idx_a, 1);  // B's successor (lane 31: own A)
+      const unsigned zh_an = __shfl_down_sync(0xffffffffu, ea.zh, 1);
+      const bool ab = idx_a == idx_b;
+      dep_a = in_a & !((idx_a == idx_bp) & (ea.zh > zh_bp)) & !(ab & (ea.zh > eb.zh));
+      dep_b = in_b & !(ab & (eb.zh > ea.zh)) & !((idx_b == idx_an) & (eb.zh > zh_an));
+    } else {
+      // constant z' per point: only each run's first step deposits
+      dep_a = in_a & ((lane == 0) | (idx_a != idx_bp));
+      dep_b = in_b & (idx_b != idx_a);
+    }
+    if (DIAG) {
+      n_dep += (unsigned)in_a + (unsigned)in_b;
+      n_atom += (unsigned)dep_a + (unsigned)dep_b;
+    }
+    red_min_u64_if(keys + idx_a, (unsigned long long)ea.key, dep_a);
+    red_min_u64_if(keys + idx_b, (unsigned long long)eb.key, dep_b);
+    if (DIAG == 2) {
+      trace_red(keys + idx_a, dep_a, lane);
+      trace_red(keys + idx_b, dep_b, lane);
+    }
+  }
+  if (__builtin_expect(__any_sync(0xffffffffu, anynear), 0)) {
+    for (int k = 0; k < p_end; ++k) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double4 pt = ptstage[k];
+        PointEval e = eval_point<MODE>(pt, h ? rb : ra, inv, cx0, cy0, tilt_c, tilt_s);
+        if (!(e.near & (h ? on_b : on_a))) continue;
+        if (MODE != MSURF_MODE_REF) {
+          const int sl = h ? rtb : rta;
+          exact_xy<MODE>(pt, h ? rb[0] : ra[0], h ? rb[1] : ra[1], xrows[sl * xstride + 4], xrows[sl * xstride + 5],
+                         tilt_c, e.xw, e.yw);
+        }
+        const int ie = cell_index_exact(e.xw, J.x_min, dd);
+        const int je = cell_index_exact(e.yw, J.y_min, dd) - j_lo;
+        const bool in = ((unsigned)ie <= span_i) & ((unsigned)je <= span_j);
+        if (in) red_min_u64(keys + (ie * ldk + je), (unsigned long long)e.key);
+        if (DIAG) {
+          n_dep += in;
+          n_atom += in;
+        }
+      }
+    }
+  }
+}
+
+// staging of a capped (pass, tooth) launch (msurf_job.stage; EXT_TILT, 64-step
+// tiles): header [tiles, units, cursor], then per live tile a record
+// {n_live; rows[64][6] = (c, s, cxp, cyp, x offset, feed position);
+// masks[64][mask_words]}, then the (tile << 32 | chunk) unit list
+constexpr long long kStageHeader = 64;
+__host__ __device__ inline long long stage_rec_bytes(int mask_words) { return 8 + 64 * 48 + 64 * 8LL * mask_words; }
+
 #pragma nv_diag_suppress 177  // tile_done is unused in the ONE instantiations
-template <int MODE, int DIAG, bool ONE, int TILE, int NTHR>
+template <int MODE, int DIAG, bool ONE, int TILE, int NTHR, bool STAGE = false>
 __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
     sweep_kernel(const msurf_job* __restrict__ jobs, int n_jobs,
                  const int64_t* __restrict__ prefix, int mask_words, const __grid_constant__ msurf_job jp,
@@ -631,9 +739,10 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
                 // surface cap: the highest current height (- stock) over every 32x32
                 // tile the chunk's box can touch, +-1.5 cells for the fp32 roundings
                 // (~1e-3 cell); an empty range means no in-grid cell at all. The caps
-                // are rewritten concurrently by zcap_watch_kernel (L2 loads; any
-                // value read is an upper bound), and consecutive chunks of a step
-                // mostly touch the same tiles: the lane reuses its last lookup.
+                // may be rewritten meanwhile by a refresh on another stream (L1-cached
+                // loads: a stale cap is a higher one, still an upper bound), and
+                // consecutive chunks of a step mostly touch the same tiles: the lane
+                // reuses its last lookup.
                 const float ci = fmaf(uc + oxf, zc_k, zc_bi), cj = fmaf(fmaf(tcc, vc, bz.x) + oyf, zc_k, zc_bj);
                 const float ri = fmaf(a.z, zc_k, 1.5f), rj = fmaf(a.w, zc_k, 1.5f);
                 const int i0 = max(0, __float2int_rd(ci - ri)) >> 5, i1 = min(zc_imax, __float2int_rd(ci + ri)) >> 5;
@@ -645,7 +754,7 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
                 if (key < 0 || key != zc_last) {
                   float cap = -INFINITY;
                   for (int ti = i0; ti <= i1; ++ti)
-                    for (int tj = j0; tj <= j1; ++tj) cap = fmaxf(cap, __ldcg(J.zcap + ti * zc_tw + tj));
+                    for (int tj = j0; tj <= j1; ++tj) cap = fmaxf(cap, __ldca(J.zcap + ti * zc_tw + tj));
                   zc_last = key;
                   zc_cap = cap;
                 }
@@ -708,6 +817,44 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
     if (tid == 0 && J.counters && n_eng_cta)
       atomicAdd(J.counters + MSURF_CTR_ENGAGED_ROWS, (unsigned long long)n_eng_cta);
     if constexpr (ONE) return; else goto tile_done;
+  }
+  if constexpr (STAGE) {
+    static_assert(ONE && MODE == MSURF_MODE_EXT_TILT && kSweepWarps == 1 && TILE == 64, "staged shape");
+    {  // staged launch: phase 1's rows and masks + the live units out, phase 2 in sweep_units_kernel
+      unsigned char* sbuf = static_cast<unsigned char*>(J.stage);
+      unsigned* hdr = reinterpret_cast<unsigned*>(sbuf);
+      unsigned slot = 0;
+      if (lane == 0) slot = atomicAdd(hdr, 1u);
+      slot = __shfl_sync(0xffffffffu, slot, 0);
+      const long long stride = stage_rec_bytes(mask_words);
+      unsigned char* rec = sbuf + kStageHeader + (long long)slot * stride;
+      if (lane == 0) *reinterpret_cast<unsigned long long*>(rec) = (unsigned long long)n_live;
+      double* rr = reinterpret_cast<double*>(rec + 8);
+      for (int i = lane; i < n_live * 6; i += 32) rr[i] = rowv[(i / 6) * 8 + (i % 6)];
+      unsigned long long* rm = reinterpret_cast<unsigned long long*>(rec + 8 + 64 * 48);
+      for (int i = lane; i < n_live * mask_words; i += 32) rm[i] = mslot[i];
+      const long long max_tiles = (J.step_hi - J.step_lo + 63) / 64;
+      unsigned long long* units = reinterpret_cast<unsigned long long*>(sbuf + kStageHeader + max_tiles * stride);
+      for (int qb = 0; qb < nchunk; qb += 32) {
+        const int qq = qb + lane;
+        bool live = false;
+        if (qq < nchunk)
+          for (int s2 = 0; s2 < n_live; ++s2) live |= ((mslot[s2 * mask_words + (qq >> 6)] >> (qq & 63)) & 1ull) != 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, live);
+        if (bal) {
+          unsigned base = 0;
+          if (lane == 0) base = atomicAdd(hdr + 1, (unsigned)__popc(bal));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (live) units[base + __popc(bal & ((1u << lane) - 1u))] = ((unsigned long long)slot << 32) | (unsigned)qq;
+        }
+      }
+      if (lane == 0 && J.counters) {
+        atomicAdd(J.counters + MSURF_CTR_LIVE_ROWS, (unsigned long long)n_live);
+        atomicAdd(J.counters + MSURF_CTR_EVAL, (unsigned long long)n_eval_cta);
+        atomicAdd(J.counters + MSURF_CTR_ENGAGED_ROWS, (unsigned long long)n_eng_cta);
+      }
+      return;
+    }
   }
 
   // ---------------- phase 2: lane = live step(s), warp walks the 32 points of a chunk
@@ -870,93 +1017,8 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
       const bool on_a = rta >= 0 && ((mslot[rta * mask_words + (q >> 6)] >> (q & 63)) & 1ull);
       const bool on_b = rtb >= 0 && ((mslot[rtb * mask_words + (q >> 6)] >> (q & 63)) & 1ull);
       if (!__any_sync(0xffffffffu, on_a | on_b)) continue;
-      const int ibias_a = on_a ? kMagicHi : kMagicHi - (1 << 30);
-      const int ibias_b = on_b ? kMagicHi : kMagicHi - (1 << 30);
-      const int p_end = min(32, npts - q * 32);
-      // stage the chunk's 32 point records (1 KB, coalesced) for broadcast
-      // reads; slots past the chunk's end hold zeros (finite, masked below)
-      __syncwarp();
-      {
-        double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
-        if (lane < p_end) {
-          const double2* src = reinterpret_cast<const double2*>(pts + q * 32 + lane);
-          const double2 a = __ldg(src), b = __ldg(src + 1);
-          v = make_double4(a.x, a.y, b.x, b.y);
-        }
-        ptstage[warp][lane] = v;
-      }
-      __syncwarp();
-      // Near-boundary points (probability ~1e-9 each) are not resolved inline:
-      // they are flagged, kept out of the neighbour comparisons (treated as
-      // outside), and deposited after the chunk with the exact reference index
-      // — an extra deposit is always safe, a skipped one never is.
-      bool anynear = false;
-      // one point per iteration evaluated under both of the lane's steps (two
-      // independent fp64 chains). Neighbours in time: A's predecessor is the
-      // previous lane's B, B's successor the next lane's A (two shuffles each),
-      // A-B within the lane in registers. The edge lanes get their own values
-      // back from the shuffles, i.e. compare with their other step, which is a
-      // neighbour anyway: no lane tests in the tilt filter.
-#pragma unroll kKUnroll
-      for (int k = 0; k < p_end; ++k) {
-        const double4 pt = ptstage[warp][k];
-        PointEval ea = eval_point<MODE>(pt, ra, inv, cx0, cy0, tilt_c, tilt_s);
-        PointEval eb = eval_point<MODE>(pt, rb, inv, cx0, cy0, tilt_c, tilt_s);
-        const int ia = ea.hi_x - ibias_a, ja = ea.hi_y - jbias;
-        const int ib = eb.hi_x - ibias_b, jb = eb.hi_y - jbias;
-        anynear |= (ea.near & on_a) | (eb.near & on_b);
-        const bool in_a = ((unsigned)ia <= span_i) & ((unsigned)ja <= span_j) & !ea.near;
-        const bool in_b = ((unsigned)ib <= span_i) & ((unsigned)jb <= span_j) & !eb.near;
-        const int idx_a = in_a ? ia * ldk + ja : -1;
-        const int idx_b = in_b ? ib * ldk + jb : -1;
-        const int idx_bp = __shfl_up_sync(0xffffffffu, idx_b, 1);  // A's predecessor (lane 0: own B)
-        bool dep_a, dep_b;
-        if (MODE == MSURF_MODE_EXT_TILT) {
-          const unsigned zh_bp = __shfl_up_sync(0xffffffffu, eb.zh, 1);
-          const int idx_an = __shfl_down_sync(0xffffffffu, idx_a, 1);  // B's successor (lane 31: own A)
-          const unsigned zh_an = __shfl_down_sync(0xffffffffu, ea.zh, 1);
-          const bool ab = idx_a == idx_b;
-          dep_a = in_a & !((idx_a == idx_bp) & (ea.zh > zh_bp)) & !(ab & (ea.zh > eb.zh));
-          dep_b = in_b & !(ab & (eb.zh > ea.zh)) & !((idx_b == idx_an) & (eb.zh > zh_an));
-        } else {
-          // constant z' per point: only each run's first step deposits
-          dep_a = in_a & ((lane == 0) | (idx_a != idx_bp));
-          dep_b = in_b & (idx_b != idx_a);
-        }
-        if (DIAG) {
-          n_dep += (unsigned)in_a + (unsigned)in_b;
-          n_atom += (unsigned)dep_a + (unsigned)dep_b;
-        }
-        red_min_u64_if(keys + idx_a, (unsigned long long)ea.key, dep_a);
-        red_min_u64_if(keys + idx_b, (unsigned long long)eb.key, dep_b);
-        if (DIAG == 2) {
-          trace_red(keys + idx_a, dep_a, lane);
-          trace_red(keys + idx_b, dep_b, lane);
-        }
-      }
-      if (__builtin_expect(__any_sync(0xffffffffu, anynear), 0)) {
-        for (int k = 0; k < p_end; ++k) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const double4 pt = ptstage[warp][k];
-            PointEval e = eval_point<MODE>(pt, h ? rb : ra, inv, cx0, cy0, tilt_c, tilt_s);
-            if (!(e.near & (h ? on_b : on_a))) continue;
-            if (MODE != MSURF_MODE_REF) {
-              const int sl = h ? rtb : rta;
-              exact_xy<MODE>(pt, h ? rb[0] : ra[0], h ? rb[1] : ra[1], rowv[sl * 8 + 4], rowv[sl * 8 + 5], tilt_c,
-                             e.xw, e.yw);
-            }
-            const int ie = cell_index_exact(e.xw, J.x_min, dd);
-            const int je = cell_index_exact(e.yw, J.y_min, dd) - j_lo;
-            const bool in = ((unsigned)ie <= span_i) & ((unsigned)je <= span_j);
-            if (in) red_min_u64(keys + (ie * ldk + je), (unsigned long long)e.key);
-            if (DIAG) {
-              n_dep += in;
-              n_atom += in;
-            }
-          }
-        }
-      }
+      pair_unit<MODE, DIAG>(J, pts, ptstage[warp], ra, rb, on_a, on_b, rowv, 8, rta, rtb, q, npts, lane, inv, cx0,
+                            cy0, span_i, span_j, jbias, j_lo, ldk, keys, tilt_c, tilt_s, dd, n_dep, n_atom);
     }
   } else {
     // unit = (group of 32 live steps, chunk q), lane = one step
@@ -1109,6 +1171,71 @@ __global__ void __launch_bounds__(256)
   if (lane == __ffs(bal) - 1) base = atomicAdd(count, (unsigned)__popc(bal));
   base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
   if (live) list[base + __popc(bal & ((1u << lane) - 1u))] = entry;
+}
+
+// phase 2 of a staged launch: persistent one-warp CTAs take (tile, chunk)
+// units from the list in order through a global cursor, load the tile's
+// staged rows and masks (L2) and run pair_unit: the heavy tiles' units spread
+// over every warp of the GPU instead of trailing in their own CTA
+template <int DIAG>
+__global__ void __launch_bounds__(32, 32)
+    sweep_units_kernel(const __grid_constant__ msurf_job J, int mask_words) {
+  constexpr int MODE = MSURF_MODE_EXT_TILT;
+  __shared__ double4 ptstage[32];
+  const int lane = threadIdx.x & 31;
+  unsigned char* sbuf = static_cast<unsigned char*>(J.stage);
+  unsigned* hdr = reinterpret_cast<unsigned*>(sbuf);
+  const unsigned n_units = hdr[1];
+  const long long stride = stage_rec_bytes(mask_words);
+  const long long max_tiles = (J.step_hi - J.step_lo + 63) / 64;
+  const unsigned long long* units =
+      reinterpret_cast<const unsigned long long*>(sbuf + kStageHeader + max_tiles * stride);
+  const int tooth = J.tooth_lo;
+  const int npts = J.points;
+  const double4* __restrict__ pts = reinterpret_cast<const double4*>(J.pts) + (long long)tooth * npts;
+  const double dd = J.spacing;
+  const double inv = 1.0 / dd;
+  const double cx0 = 0.5 - J.x_min * inv;
+  const double cy0 = 0.5 - J.y_min * inv;
+  const unsigned span_i = (unsigned)J.m;
+  const int j_lo = (int)J.j_lo;
+  const unsigned span_j = (unsigned)(J.j_hi - J.j_lo);
+  const int jbias = kMagicHi + j_lo;
+  const int ldk = (int)J.ld;
+  unsigned long long* __restrict__ keys = reinterpret_cast<unsigned long long*>(J.keys);
+  unsigned n_dep = 0, n_atom = 0;
+  for (;;) {
+    unsigned u = 0;
+    if (lane == 0) u = atomicAdd(hdr + 2, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= n_units) break;
+    const unsigned long long e = units[u];
+    const unsigned char* rec = sbuf + kStageHeader + (long long)(e >> 32) * stride;
+    const int q = (int)(e & 0xffffffffull);
+    const int n_live = (int)*reinterpret_cast<const unsigned long long*>(rec);
+    const double* rr = reinterpret_cast<const double*>(rec + 8);
+    const unsigned long long* rm = reinterpret_cast<const unsigned long long*>(rec + 8 + 64 * 48);
+    const int sa = 2 * lane, sb = sa + 1;
+    const int rta = sa < n_live ? sa : -1, rtb = sb < n_live ? sb : -1;
+    double ra[4], rb[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      ra[k] = rta >= 0 ? __ldcg(rr + sa * 6 + k) : 0.0;
+      rb[k] = rtb >= 0 ? __ldcg(rr + sb * 6 + k) : 0.0;
+    }
+    const bool on_a = rta >= 0 && ((__ldcg(rm + rta * mask_words + (q >> 6)) >> (q & 63)) & 1ull);
+    const bool on_b = rtb >= 0 && ((__ldcg(rm + rtb * mask_words + (q >> 6)) >> (q & 63)) & 1ull);
+    pair_unit<MODE, DIAG>(J, pts, ptstage, ra, rb, on_a, on_b, rr, 6, rta, rtb, q, npts, lane, inv, cx0, cy0, span_i,
+                          span_j, jbias, j_lo, ldk, keys, J.tilt_c, J.tilt_s, dd, n_dep, n_atom);
+  }
+  if (DIAG && J.counters) {
+    n_dep = warp_sum_u(n_dep);
+    n_atom = warp_sum_u(n_atom);
+    if (lane == 0) {
+      atomicAdd(J.counters + MSURF_CTR_DEPOSITS, (unsigned long long)n_dep);
+      atomicAdd(J.counters + MSURF_CTR_ATOMICS, (unsigned long long)n_atom);
+    }
+  }
 }
 
 // --------------------------------------------------------------- fill/decode
@@ -1724,10 +1851,10 @@ inline size_t sweep_smem(int tile, int mask_words) {
   return (size_t)tile * 8 * sizeof(double) + (size_t)2 * tile * mask_words * sizeof(uint64_t);
 }
 
-template <int MODE, int DIAG, bool ONE, int TILE, int NTHR>
+template <int MODE, int DIAG, bool ONE, int TILE, int NTHR, bool STAGE = false>
 cudaError_t launch_shape(int64_t n_tiles, cudaStream_t st, const msurf_job* jobs, int n_jobs, const int64_t* prefix,
                          int mask_words, const msurf_job& job, unsigned long long* list, unsigned* count) {
-  auto kern = sweep_kernel<MODE, DIAG, ONE, TILE, NTHR>;
+  auto kern = sweep_kernel<MODE, DIAG, ONE, TILE, NTHR, STAGE>;
   const size_t smem = sweep_smem(TILE, mask_words);
   cudaError_t e = cudaSuccess;
   if (smem > 48 * 1024) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1935,6 +2062,43 @@ int msurf_zcap_refresh(const uint64_t* keys, int64_t ld, int64_t rows, int64_t c
   return check_launch("zcap_kernel");
 }
 
+// one staged (pass, tooth) launch of a capped tilt job: the staging header
+// cleared, phase 1 of every tile (rows, masks, live units out), then the
+// persistent phase-2 kernel over the units (production variant only)
+static int staged_launch(const msurf_job& sub, int32_t max_points, cudaStream_t st) {
+  const int nchunk = (max_points + 31) / 32;
+  const int mask_words = (nchunk + 63) / 64;
+  cudaError_t e = cudaMemsetAsync(sub.stage, 0, 16, st);
+  if (e != cudaSuccess) return set_err(std::string("staged_launch: ") + cudaGetErrorString(e));
+  e = launch_shape<MSURF_MODE_EXT_TILT, 0, true, kTiltTile, kTiltThreads, true>(job_tiles(sub, kTiltTile), st, nullptr,
+                                                                                1, nullptr, mask_words, sub, nullptr,
+                                                                                nullptr);
+  if (e != cudaSuccess) return set_err(std::string("staged_launch: phase 1: ") + cudaGetErrorString(e));
+  if (check_launch("sweep_kernel (staged)")) return 1;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_units_kernel<0>, 32, 0);
+  const long long units_max = job_tiles(sub, kTiltTile) * nchunk;
+  const long long grid = std::min<long long>(units_max, (long long)sms * std::max(per_sm, 1));
+  if (grid > 0) sweep_units_kernel<0><<<(unsigned)grid, 32, 0, st>>>(sub, mask_words);
+  return check_launch("sweep_units_kernel");
+}
+
+// staging bytes one capped (pass, tooth) launch of `job` needs
+static long long stage_bytes(const msurf_job& job, int32_t max_points) {
+  const int nchunk = (max_points + 31) / 32;
+  const int mask_words = (nchunk + 63) / 64;
+  const long long tiles = (job.step_hi - job.step_lo + 63) / 64;
+  return kStageHeader + tiles * stage_rec_bytes(mask_words) + tiles * nchunk * 8;
+}
+
+int msurf_stage_bytes(const msurf_job* job, int32_t max_points, int64_t* bytes) {
+  if (!job || !bytes || max_points < 1) return set_err("msurf_stage_bytes: bad arguments");
+  *bytes = stage_bytes(*job, max_points);
+  return 0;
+}
+
 int msurf_sweep_job_capped(const msurf_job* job, int32_t mode, int32_t max_points, const double* stock,
                            void* stream) {
   if (!job || !job->zcap || !stock || max_points < 1) return set_err("msurf_sweep_job_capped: bad arguments");
@@ -1971,7 +2135,7 @@ cudaStream_t lib_stream(int k) {
 }
 
 int msurf_sweep_jobs_capped(const msurf_job* jobs, int32_t n_jobs, int32_t mode, int32_t max_points,
-                            const int64_t* stocks, int32_t depth, void* stream) {
+                            const int64_t* stocks, int32_t depth, void* stage, int64_t stage_each, void* stream) {
   if (!jobs || n_jobs < 1 || !stocks || max_points < 1 || depth < 1)
     return set_err("msurf_sweep_jobs_capped: bad arguments");
   // fork: job k's (pass, tooth) launches round-robin over `depth` library
@@ -2022,7 +2186,16 @@ int msurf_sweep_jobs_capped(const msurf_job* jobs, int32_t n_jobs, int32_t mode,
       sub.tooth_lo = job->tooth_lo + i % teeth;
       sub.tooth_n = 1;
       if (job_tiles(sub, 64) == 0) continue;
-      rc = sweep_impl(nullptr, 1, nullptr, 0, mode, max_points, q, &sub, nullptr);
+      // staged two-kernel form for the production variant when staging is given
+      const bool staged = stage && (mode & ~MSURF_MODE_MASK) == 0 && (mode & MSURF_MODE_MASK) == MSURF_MODE_EXT_TILT;
+      if (staged) {
+        sub.stage = static_cast<unsigned char*>(stage) + (long long)(j * depth + i % depth) * stage_each;
+        rc = stage_bytes(sub, max_points) > stage_each ? set_err("msurf_sweep_jobs_capped: staging too small")
+                                                       : staged_launch(sub, max_points, q);
+      } else {
+        sub.stage = nullptr;
+        rc = sweep_impl(nullptr, 1, nullptr, 0, mode, max_points, q, &sub, nullptr);
+      }
       if (rc == 0 && i + 1 < n) rc = msurf_zcap_refresh(job->keys, job->ld, rows, cols, stock, zcap, nullptr, q);
     }
   }

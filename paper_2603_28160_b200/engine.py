@@ -49,9 +49,12 @@ ZCAP = __import__("os").environ.get("MSURF_ZCAP", "1") != "0"
 # eight-warp CTAs for capped launches (measured slower once launches overlap)
 ZCAP_WIDE = __import__("os").environ.get("MSURF_ZCAP_WIDE", "0") != "0"
 ZCAP_MIN_JOBS = int(__import__("os").environ.get("MSURF_ZCAP_MIN_JOBS", "2"))  # capped jobs swept side by side
-# overlapping (pass, tooth) launches per capped job (measured on config 5: depth
-# 1 / 2 / 3 / 4 -> 27.1 / 20.5 / 20.3 / 20.9 ms; no cap 37.3 ms)
-ZCAP_DEPTH = int(__import__("os").environ.get("MSURF_ZCAP_DEPTH", "3"))
+# overlapping (pass, tooth) launches per capped job. Measured on config 5 (sweep,
+# no cap 37.3 ms): single-kernel launches depth 1 / 2 / 3 / 4 -> 27.1 / 20.5 /
+# 20.3 / 20.9 ms; staged two-kernel launches depth 1 / 2 / 3 -> 16.7 / 17.0 / 19.6 ms
+ZCAP_DEPTH = int(__import__("os").environ.get("MSURF_ZCAP_DEPTH", "1"))
+# capped launches as two kernels: phase 1 staged to HBM, phase 2 balanced over every warp
+ZCAP_STAGED = __import__("os").environ.get("MSURF_ZCAP_STAGED", "1") != "0"
 
 
 def _per_job_launches(tiles) -> bool:
@@ -352,7 +355,7 @@ class SweepBatch:
                         p.tilt_c, p.tilt_s, p.zoff, p.vib_amp, p.vib_omega, p.vib_phase,
                         base + o["trig_table"] if "trig_table" in o else 0,
                         base + o["vib_table"] if "vib_table" in o else 0,
-                        tr, base + o["min_index"], base + self.ctr_off + i * _native.NUM_CTRS * 8, 0,
+                        tr, base + o["min_index"], base + self.ctr_off + i * _native.NUM_CTRS * 8, 0, 0,
                         p.teeth, p.points, p.passes, 0, 0, 0))
                 arr = np.array(rows, dtype=_native.JOB_DTYPE)
                 if job_off is not None:
@@ -411,14 +414,27 @@ class SweepBatch:
         return out
 
     def _launch_capped(self, g: int, ks, mode: int, flag: int, max_pts: int, sp: int) -> None:
-        """Surface-cap jobs ks of by-value group g, concurrently (msurf_sweep_jobs_capped)."""
+        """Surface-cap jobs ks of by-value group g, concurrently
+        (msurf_sweep_jobs_capped), staged two-kernel launches when ZCAP_STAGED."""
         host = self.group_host_jobs[g]
         arr = np.ascontiguousarray(host[ks])
         stocks = np.array([self.zc_seq[g][k][-1] for k in ks], dtype=np.int64)
         wide = _native.SWEEP_WIDE if ZCAP_WIDE else 0
         depth = max(1, min(ZCAP_DEPTH, 32 // len(ks)))
+        stage, each = 0, 0
+        if ZCAP_STAGED:
+            key = (g, tuple(ks), depth)
+            if getattr(self, "_stage_key", None) != key:
+                nb = ctypes.c_int64(0)
+                each = 0
+                for k in ks:
+                    _native.check(self.lib.msurf_stage_bytes(host[k:k + 1].ctypes.data, max_pts, ctypes.byref(nb)))
+                    each = max(each, (nb.value + 255) // 256 * 256)
+                self._stage = self.torch.empty(each * len(ks) * depth, dtype=self.torch.uint8, device=self.dev)
+                self._stage_key, self._stage_each = key, each
+            stage, each = self._stage.data_ptr(), self._stage_each
         _native.check(self.lib.msurf_sweep_jobs_capped(arr.ctypes.data, len(ks), mode | flag | wide, max_pts,
-                                                       stocks.ctypes.data, depth, sp))
+                                                       stocks.ctypes.data, depth, stage, each, sp))
 
     def _launch_job(self, g: int, k: int, mode: int, flag: int, max_pts: int, sp: int) -> None:
         """Job k of by-value launch group g (a surface-cap job through

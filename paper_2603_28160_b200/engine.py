@@ -48,11 +48,12 @@ ONE_JOB_MIN_TILES = int(__import__("os").environ.get("MSURF_ONE_JOB_MIN_TILES", 
 ZCAP = __import__("os").environ.get("MSURF_ZCAP", "1") != "0"
 # eight-warp CTAs for capped launches (measured slower once launches overlap)
 ZCAP_WIDE = __import__("os").environ.get("MSURF_ZCAP_WIDE", "0") != "0"
-ZCAP_MIN_JOBS = int(__import__("os").environ.get("MSURF_ZCAP_MIN_JOBS", "2"))  # capped jobs swept side by side
-# overlapping (pass, tooth) launches per capped job. Measured on config 5 (sweep,
-# no cap 37.3 ms): single-kernel launches depth 1 / 2 / 3 / 4 -> 27.1 / 20.5 /
-# 20.3 / 20.9 ms; staged two-kernel launches depth 1 / 2 / 3 -> 16.7 / 17.0 / 19.6 ms
-ZCAP_DEPTH = int(__import__("os").environ.get("MSURF_ZCAP_DEPTH", "1"))
+ZCAP_MIN_JOBS = int(__import__("os").environ.get("MSURF_ZCAP_MIN_JOBS", "1"))  # capped jobs swept side by side
+# overlapping (pass, tooth) launches per capped job. Measured on config 5 (3
+# sub-strip jobs; sweep without caps 37.3 ms): single-kernel launches depth 1 /
+# 2 / 3 / 4 -> 27.1 / 20.5 / 20.3 / 20.9 ms; staged two-kernel launches depth
+# 1 / 2 / 3 -> 16.7 / 17.0 / 19.6 ms
+ZCAP_DEPTH = int(__import__("os").environ.get("MSURF_ZCAP_DEPTH", "0"))  # 0: ceil(3 / capped jobs)
 # capped launches as two kernels: phase 1 staged to HBM, phase 2 balanced over every warp
 ZCAP_STAGED = __import__("os").environ.get("MSURF_ZCAP_STAGED", "1") != "0"
 
@@ -402,9 +403,10 @@ class SweepBatch:
                     seqs[k] = (p.passes * p.teeth, zc, int(host[k]["keys"]), int(host[k]["ld"]), rows, cols,
                                self.base + self.sentinel_off + 8 * i)
                 # the (pass, tooth) launches of one job are short and underfill the
-                # GPU; they pay only when several jobs (L2 sub-strips) run side by
-                # side (measured: config 5, 3 sub-strips: 37.3 -> 26.6 ms; config 2,
-                # one job: 0.68 -> 1.2 ms)
+                # GPU: several jobs (L2 sub-strips) run side by side and each
+                # keeps ceil(3 / jobs) launches in flight (measured, staged
+                # form: config 5 at N = 1 / 2 / 4 / 8 strips per GPU 16.6 / 8.6 /
+                # 5.3 / 3.4 ms; config 2, one job: 0.70 ms, as uncapped)
                 if sum(q is not None for q in seqs) < ZCAP_MIN_JOBS:
                     for k, q in enumerate(seqs):
                         if q is not None:
@@ -420,7 +422,9 @@ class SweepBatch:
         arr = np.ascontiguousarray(host[ks])
         stocks = np.array([self.zc_seq[g][k][-1] for k in ks], dtype=np.int64)
         wide = _native.SWEEP_WIDE if ZCAP_WIDE else 0
-        depth = max(1, min(ZCAP_DEPTH, 32 // len(ks)))
+        # overlap: about three capped launches in flight per GPU in total
+        depth = ZCAP_DEPTH if ZCAP_DEPTH > 0 else -(-3 // len(ks))
+        depth = max(1, min(depth, 32 // len(ks)))
         stage, each = 0, 0
         if ZCAP_STAGED:
             key = (g, tuple(ks), depth)

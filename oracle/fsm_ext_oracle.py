@@ -14,11 +14,12 @@ no such features). What is pinned:
     reference restatement ``fsm_oracle`` (pinned bit-exact to the reference
     goldens), passes composing by elementwise min exactly as
     HeightField.merge_min would (surface_grid.py:131-134);
-  * ``tests/test_ext_oracle.py`` checks that the extended formulation with all
-    extensions at zero agrees with the reference formulation to ~1e-15 mm in
-    positions and bit-exactly in heights on the golden configurations, plus
-    geometric properties of each extension (scallop height of a ball-end
-    raster, tilt lowest point, runout period, noise statistics).
+  * ``tests/test_host_cpu.py::test_ext_zero_formulation_is_reference_on_goldens``
+    checks that the extended formulation with all extensions at zero gives
+    the reference's heights bit-exactly on the golden configurations;
+    ``test_ext_oracle_*`` in the same file check geometric properties of the
+    extensions (ball-end raster scallop height, tilt re-levelling to z0,
+    edge-noise standard deviation and correlation length).
 The formulas below are the definition the CUDA kernel is checked against.
 """
 

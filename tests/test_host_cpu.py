@@ -407,3 +407,49 @@ def test_bench_reference_arm_imports_no_product_code(tmp_path):
     assert rec["impl"] == "reference" and rec["value"] > 0 and rec["e2e"]["h2d_bytes_per_step"] == 0
     chk = json.loads(out.stdout.split("CHECK ", 1)[1])
     assert chk == {"mods": [], "lib": False}, chk
+
+
+def test_ext_oracle_edge_noise_statistics():
+    """Edge noise: Gaussian-smoothed white noise rescaled to
+    sigma; its autocorrelation falls to ~1/e at the correlation length."""
+    sigma, corr, ds = 1e-3, 0.02, 0.0005
+    d = xorc.edge_noise(3, 20000, sigma, corr, ds, seed=7)
+    assert abs(float(d.std()) / sigma - 1.0) < 0.1
+    lag = int(round(corr / ds))
+    x = d[0] - d[0].mean()
+    r = float(np.dot(x[:-lag], x[lag:]) / np.dot(x, x))
+    assert abs(r - math.exp(-1.0)) < 0.1, r
+
+
+def test_ext_oracle_tilt_relevels_lowest_reachable_point():
+    """Lead tilt: the tool is re-levelled so the lowest point any edge point
+    can reach over a revolution sits exactly at z0."""
+    from oracle import workloads as W
+
+    for cid in (2, 5):
+        cfg, ext, _ = W.FACTORIES[cid]()
+        p = xorc.ext_plan(cfg, ext)
+        low = np.min(p.tilt_c * p.zt - abs(p.tilt_s) * np.sqrt(p.xt ** 2 + p.yt ** 2)) + p.zoff
+        assert abs(low - p.z0) < 1e-12, (cid, low)
+
+
+def test_ext_oracle_ball_raster_scallop_height():
+    """Ball-end raster without tilt: between two passes at stepover s the
+    residual ridge is the scallop R - sqrt(R^2 - (s/2)^2) (feed marks made
+    negligible by a tiny feed per tooth)."""
+    from dataclasses import replace
+
+    from oracle import workloads as W
+
+    r, s = 1.0, 0.2
+    tool = W.Tool(2.0 * r, r, 2)
+    proc = W.process(2, 2.0 * r, 0.05, 6000.0, 0.002, initial=(0.0, None, 0.0))
+    grid = W.Grid(0.002, 0.0, 0.0, int(round(s / 0.002)), 20)
+    cfg = W.Config(tool, proc, grid, edge_point_count=400, time_step_s=(2 * math.pi / 720) / proc.angular_velocity_rad_s)
+    ext = W.Ext(profile="ball", passes=2, stepover_mm=s)
+    h, p, _, _ = xorc.ext_sweep(cfg, ext, workers=4)
+    h2 = h.reshape(p.m + 1, p.n + 1)
+    expect = r - math.sqrt(r * r - (s / 2) ** 2)
+    ridge = float(h2[p.m // 2].mean())  # midway between the pass centres
+    assert abs(ridge - expect) < 0.1 * expect, (ridge, expect)
+    assert float(h2[0].mean()) < 0.1 * expect  # pass centre: cut to the ball bottom

@@ -753,8 +753,15 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
                 const int key = cacheable ? ((i0 << 17) | (j0 << 4) | ((i1 - i0) << 2) | (j1 - j0)) : -2;
                 if (key < 0 || key != zc_last) {
                   float cap = -INFINITY;
-                  for (int ti = i0; ti <= i1; ++ti)
-                    for (int tj = j0; tj <= j1; ++tj) cap = fmaxf(cap, __ldca(J.zcap + ti * zc_tw + tj));
+                  if ((i1 - i0) <= 1 && (j1 - j0) <= 1 && i0 <= i1 && j0 <= j1) {
+                    // the usual case, at most 2 x 2 tiles: four independent loads
+                    const float* r0 = J.zcap + i0 * zc_tw;
+                    const float* r1 = J.zcap + i1 * zc_tw;
+                    cap = fmaxf(fmaxf(__ldca(r0 + j0), __ldca(r0 + j1)), fmaxf(__ldca(r1 + j0), __ldca(r1 + j1)));
+                  } else {
+                    for (int ti = i0; ti <= i1; ++ti)
+                      for (int tj = j0; tj <= j1; ++tj) cap = fmaxf(cap, __ldca(J.zcap + ti * zc_tw + tj));
+                  }
                   zc_last = key;
                   zc_cap = cap;
                 }
@@ -1204,11 +1211,14 @@ __global__ void __launch_bounds__(32, 32)
   const int ldk = (int)J.ld;
   unsigned long long* __restrict__ keys = reinterpret_cast<unsigned long long*>(J.keys);
   unsigned n_dep = 0, n_atom = 0;
+  // the next unit's index is fetched while the current unit runs (the cursor
+  // atomic's round trip was the kernel's largest stall)
+  unsigned u_next = 0;
+  if (lane == 0) u_next = atomicAdd(hdr + 2, 1u);
   for (;;) {
-    unsigned u = 0;
-    if (lane == 0) u = atomicAdd(hdr + 2, 1u);
-    u = __shfl_sync(0xffffffffu, u, 0);
+    const unsigned u = __shfl_sync(0xffffffffu, u_next, 0);
     if (u >= n_units) break;
+    if (lane == 0) u_next = atomicAdd(hdr + 2, 1u);
     const unsigned long long e = units[u];
     const unsigned char* rec = sbuf + kStageHeader + (long long)(e >> 32) * stride;
     const int q = (int)(e & 0xffffffffull);

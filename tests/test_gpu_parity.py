@@ -263,12 +263,17 @@ def test_deferred_exact_path_bitexact():
 
 
 @pytest.mark.parametrize("case", ["ref", "ext", "tilt"])
-def test_tile_list_path_equals_per_job_path(case):
+def test_tile_list_path_equals_per_job_path(case, monkeypatch):
     """The batched launch pre-culls its tiles into a list walked by persistent
     CTAs; the single-job launch culls tiles inline. Same heights and the same
-    row/point counters, also for narrow strip windows where most tiles die."""
-    from paper_2603_28160_b200 import planner
+    row/point counters, also for narrow strip windows where most tiles die.
+    (A tilt single job also runs capped — surface-cap cull, fewer rows and
+    points — so the counters are compared with the cap off and the heights
+    with it on as well.)"""
+    from paper_2603_28160_b200 import engine, planner
     from paper_2603_28160_b200.engine import SweepBatch
+
+    monkeypatch.setattr(engine, "ZCAP", False)
 
     if case == "ref":
         cfg, ext = golden_io.product_config(golden_io.load("small_3")["config"], record_trajectory=False), None
@@ -291,3 +296,9 @@ def test_tile_list_path_equals_per_job_path(case):
         for k, h in enumerate(many.heights()):
             assert np.array_equal(h.cpu().numpy(), h1), (case, lo, hi, k)
             assert np.array_equal(cm[k], c1[0]) and mm[k] == m1[0], (case, lo, hi, k)
+        monkeypatch.setattr(engine, "ZCAP", True)
+        capped = SweepBatch([(p, lo, hi)])
+        capped.launch()
+        assert np.array_equal(capped.heights()[0].cpu().numpy(), h1), (case, lo, hi, "capped")
+        assert int(capped.counters()[1][0]) == int(m1[0])
+        monkeypatch.setattr(engine, "ZCAP", False)

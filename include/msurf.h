@@ -157,15 +157,25 @@ int msurf_sweep_job_capped(const msurf_job* job, int32_t mode, int32_t max_point
  * from and joined back into `stream` (graph-capturable): each job's (pass,
  * tooth) launches go round-robin over `depth` streams of its own, so up to
  * `depth` of them overlap (caps read at most depth - 1 launches stale: a
- * weaker cull, never another result). n_jobs x depth <= 32.
+ * weaker cull, never another result), depth <= 4. Job j runs in stream slot
+ * slot0 + j (<= 8 slots; slot 0 has the highest stream priority, so side-by-
+ * side jobs finish in slot order); a caller may issue the jobs of one surface
+ * in separate calls with distinct slots and different `stream`s to join each
+ * job separately.
  * stocks: HOST array of device pointers to each job's stock height. */
 int msurf_sweep_jobs_capped(const msurf_job* jobs, int32_t n_jobs, int32_t mode, int32_t max_points,
-                            const int64_t* stocks, int32_t depth, void* stage, int64_t stage_each, void* stream);
+                            const int64_t* stocks, int32_t depth, void* stage, int64_t stage_each, int32_t slot0,
+                            void* stream);
 /* With `stage` (device, n_jobs x depth buffers of stage_each >= msurf_stage_bytes
  * bytes) the production launches run staged: phase 1 of every tile writes
  * its rows, masks and live (tile, chunk) units there, then a persistent
  * kernel balances phase 2 over every warp. NULL: the single-kernel form. */
 int msurf_stage_bytes(const msurf_job* job, int32_t max_points, int64_t* bytes);
+/* Plumbing for per-job joins: a library-owned non-blocking anchor stream
+ * (k < 16), and "waiter waits for everything enqueued on signaler so far"
+ * (an event recorded on signaler, waited on by waiter). */
+void* msurf_anchor_stream(int32_t k);
+int msurf_stream_wait(void* waiter, void* signaler);
 
 /* Decode keys to fp64 heights in place and count machined cells
  * (HeightField.machined_cell_count, surface_grid.py:128-129). Batched over

@@ -83,8 +83,10 @@ EXPORTS = {
                                           c_void_p]),
     "msurf_sweep_job_capped": (ctypes.c_int, [c_void_p, c_int32, c_int32, c_void_p, c_void_p]),
     "msurf_sweep_jobs_capped": (ctypes.c_int, [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32, c_void_p,
-                                               c_int64, c_void_p]),
+                                               c_int64, c_int32, c_void_p]),
     "msurf_stage_bytes": (ctypes.c_int, [c_void_p, c_int32, ctypes.POINTER(c_int64)]),
+    "msurf_anchor_stream": (c_void_p, [c_int32]),
+    "msurf_stream_wait": (ctypes.c_int, [c_void_p, c_void_p]),
     "msurf_areal_pass1": (ctypes.c_int, [c_void_p, c_int64, c_int64, c_int32, c_int64, c_int64,
                                          c_int64, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
                                          c_void_p]),

@@ -2134,40 +2134,66 @@ int msurf_sweep_job_capped(const msurf_job* job, int32_t mode, int32_t max_point
 
 // library-owned non-blocking streams (no implicit synchronisation with any
 // other stream, the legacy one included), per device and thread
+// stream k belongs to job slot k / 4 and carries that slot's priority (slot 0
+// highest): side-by-side jobs then finish in slot order, so the caller can
+// decode and copy out one job's slab while the later ones still sweep
 cudaStream_t lib_stream(int k) {
-  constexpr int kMax = 32;
+  constexpr int kMax = 48;  // 8 job slots x 4 in-flight launches, then anchors
   static thread_local cudaStream_t pool[64][kMax] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || k < 0 || k >= kMax) return nullptr;
-  if (!pool[dev][k] && cudaStreamCreateWithFlags(&pool[dev][k], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  if (!pool[dev][k]) {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    const int prio = std::min(least, greatest + k / 4);
+    if (cudaStreamCreateWithPriority(&pool[dev][k], cudaStreamNonBlocking, prio) != cudaSuccess) return nullptr;
+  }
   return pool[dev][k];
 }
 
+void* msurf_anchor_stream(int32_t k) {
+  if (k < 0 || k >= 16) return nullptr;
+  return lib_stream(32 + k);
+}
+
+int msurf_stream_wait(void* waiter, void* signaler) {
+  cudaEvent_t ev = nullptr;
+  if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return set_err("msurf_stream_wait: event");
+  cudaError_t e = cudaEventRecord(ev, (cudaStream_t)signaler);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent((cudaStream_t)waiter, ev, 0);
+  cudaEventDestroy(ev);
+  if (e != cudaSuccess) return set_err(std::string("msurf_stream_wait: ") + cudaGetErrorString(e));
+  return 0;
+}
+
 int msurf_sweep_jobs_capped(const msurf_job* jobs, int32_t n_jobs, int32_t mode, int32_t max_points,
-                            const int64_t* stocks, int32_t depth, void* stage, int64_t stage_each, void* stream) {
-  if (!jobs || n_jobs < 1 || !stocks || max_points < 1 || depth < 1)
+                            const int64_t* stocks, int32_t depth, void* stage, int64_t stage_each, int32_t slot0,
+                            void* stream) {
+  if (!jobs || n_jobs < 1 || !stocks || max_points < 1 || depth < 1 || depth > 4 || slot0 < 0 ||
+      slot0 + n_jobs > 8)
     return set_err("msurf_sweep_jobs_capped: bad arguments");
   // fork: job k's (pass, tooth) launches round-robin over `depth` library
   // streams of its own (launch i waits for launch i - depth and the cap refresh
   // after it; neighbours overlap, reading caps at most depth - 1 launches
   // stale, which only weakens the cull); jobs write disjoint slabs. Every
   // stream is joined back into `stream` (graph-capturable fork/join).
-  const int ns = n_jobs * depth;
-  if (ns > 32) return set_err("msurf_sweep_jobs_capped: too many jobs x depth");
+  // job j (slot slot0 + j) uses streams 4 (slot0 + j) + [0, depth)
+  auto sid = [&](int j, int d) { return 4 * (slot0 + j) + d; };
   cudaStream_t st = (cudaStream_t)stream;
   cudaEvent_t fork = nullptr;
   if (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) return set_err("events");
   cudaEventRecord(fork, st);
   int rc = 0;
-  for (int k = 0; k < ns; ++k) {
-    cudaStream_t q = lib_stream(k);
-    if (!q) {
-      rc = set_err("msurf_sweep_jobs_capped: stream");
-      break;
+  for (int j = 0; j < n_jobs && rc == 0; ++j)
+    for (int d = 0; d < depth; ++d) {
+      cudaStream_t q = lib_stream(sid(j, d));
+      if (!q) {
+        rc = set_err("msurf_sweep_jobs_capped: stream");
+        break;
+      }
+      cudaStreamWaitEvent(q, fork, 0);
     }
-    cudaStreamWaitEvent(q, fork, 0);
-  }
   for (int j = 0; j < n_jobs && rc == 0; ++j) {
     const msurf_job* job = jobs + j;
     const double* stock = reinterpret_cast<const double*>(stocks[j]);
@@ -2179,17 +2205,17 @@ int msurf_sweep_jobs_capped(const msurf_job* jobs, int32_t n_jobs, int32_t mode,
     float* zcap = const_cast<float*>(job->zcap);
     const int teeth = job->tooth_n ? job->tooth_n : job->teeth;
     const int n = job->passes * teeth;
-    cudaStream_t q0 = lib_stream(j * depth);
+    cudaStream_t q0 = lib_stream(sid(j, 0));
     // caps of the freshly filled slab first, seen by every stream of the job
     rc = msurf_zcap_refresh(job->keys, job->ld, rows, cols, stock, zcap, nullptr, q0);
     cudaEvent_t ready = nullptr;
     if (rc == 0 && cudaEventCreateWithFlags(&ready, cudaEventDisableTiming) == cudaSuccess) {
       cudaEventRecord(ready, q0);
-      for (int d = 1; d < depth; ++d) cudaStreamWaitEvent(lib_stream(j * depth + d), ready, 0);
+      for (int d = 1; d < depth; ++d) cudaStreamWaitEvent(lib_stream(sid(j, d)), ready, 0);
       cudaEventDestroy(ready);
     }
     for (int i = 0; i < n && rc == 0; ++i) {
-      cudaStream_t q = lib_stream(j * depth + i % depth);
+      cudaStream_t q = lib_stream(sid(j, i % depth));
       msurf_job sub = *job;
       sub.passes = 1;
       sub.pass_x0 = job->pass_x0 + i / teeth;
@@ -2209,14 +2235,15 @@ int msurf_sweep_jobs_capped(const msurf_job* jobs, int32_t n_jobs, int32_t mode,
       if (rc == 0 && i + 1 < n) rc = msurf_zcap_refresh(job->keys, job->ld, rows, cols, stock, zcap, nullptr, q);
     }
   }
-  for (int k = 0; k < ns; ++k) {  // joins are enqueued whatever happened
-    cudaStream_t q = lib_stream(k);
-    cudaEvent_t join = nullptr;
-    if (!q || cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess) continue;
-    cudaEventRecord(join, q);
-    cudaStreamWaitEvent(st, join, 0);
-    cudaEventDestroy(join);
-  }
+  for (int j = 0; j < n_jobs; ++j)  // joins are enqueued whatever happened
+    for (int d = 0; d < depth; ++d) {
+      cudaStream_t q = lib_stream(sid(j, d));
+      cudaEvent_t join = nullptr;
+      if (!q || cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess) continue;
+      cudaEventRecord(join, q);
+      cudaStreamWaitEvent(st, join, 0);
+      cudaEventDestroy(join);
+    }
   cudaEventDestroy(fork);
   return rc;
 }

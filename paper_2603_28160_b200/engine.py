@@ -415,30 +415,61 @@ class SweepBatch:
             out.append(seqs)
         return out
 
-    def _launch_capped(self, g: int, ks, mode: int, flag: int, max_pts: int, sp: int) -> None:
-        """Surface-cap jobs ks of by-value group g, concurrently
-        (msurf_sweep_jobs_capped), staged two-kernel launches when ZCAP_STAGED."""
-        host = self.group_host_jobs[g]
-        arr = np.ascontiguousarray(host[ks])
-        stocks = np.array([self.zc_seq[g][k][-1] for k in ks], dtype=np.int64)
-        wide = _native.SWEEP_WIDE if ZCAP_WIDE else 0
+    def _capped_depth(self, n_jobs: int) -> int:
         # overlap: about three capped launches in flight per GPU in total
-        depth = ZCAP_DEPTH if ZCAP_DEPTH > 0 else -(-3 // len(ks))
-        depth = max(1, min(depth, 32 // len(ks)))
-        stage, each = 0, 0
-        if ZCAP_STAGED:
-            key = (g, tuple(ks), depth)
-            if getattr(self, "_stage_key", None) != key:
-                nb = ctypes.c_int64(0)
-                each = 0
-                for k in ks:
-                    _native.check(self.lib.msurf_stage_bytes(host[k:k + 1].ctypes.data, max_pts, ctypes.byref(nb)))
-                    each = max(each, (nb.value + 255) // 256 * 256)
-                self._stage = self.torch.empty(each * len(ks) * depth, dtype=self.torch.uint8, device=self.dev)
-                self._stage_key, self._stage_each = key, each
-            stage, each = self._stage.data_ptr(), self._stage_each
-        _native.check(self.lib.msurf_sweep_jobs_capped(arr.ctypes.data, len(ks), mode | flag | wide, max_pts,
-                                                       stocks.ctypes.data, depth, stage, each, sp))
+        depth = ZCAP_DEPTH if ZCAP_DEPTH > 0 else -(-3 // n_jobs)
+        return max(1, min(depth, 4))
+
+    def _capped_stage(self, g: int, ks, depth: int, max_pts: int):
+        """Staging buffer: one (job, in-flight launch) slot each, sized for the
+        largest job (msurf_stage_bytes); reused across launches."""
+        if not ZCAP_STAGED:
+            return 0, 0
+        key = (g, tuple(ks), depth)
+        if getattr(self, "_stage_key", None) != key:
+            host = self.group_host_jobs[g]
+            nb = ctypes.c_int64(0)
+            each = 0
+            for k in ks:
+                _native.check(self.lib.msurf_stage_bytes(host[k:k + 1].ctypes.data, max_pts, ctypes.byref(nb)))
+                each = max(each, (nb.value + 255) // 256 * 256)
+            self._stage = self.torch.empty(each * len(ks) * depth, dtype=self.torch.uint8, device=self.dev)
+            self._stage_key, self._stage_each = key, each
+        return self._stage.data_ptr(), self._stage_each
+
+    def _launch_capped(self, g: int, ks, mode: int, flag: int, max_pts: int, sp: int, split: bool = False):
+        """Surface-cap jobs ks of by-value group g side by side
+        (msurf_sweep_jobs_capped; staged two-kernel launches when
+        ZCAP_STAGED). ``split``: one call per job, each forked from and joined
+        into its own anchor stream (returned, in ks order) so the caller can
+        wait for each job's slab separately; jobs still run side by side, the
+        earlier ones at higher stream priority."""
+        host = self.group_host_jobs[g]
+        wide = _native.SWEEP_WIDE if ZCAP_WIDE else 0
+        depth = self._capped_depth(len(ks))
+        stage, each = self._capped_stage(g, ks, depth, max_pts)
+        stocks = np.array([self.zc_seq[g][k][-1] for k in ks], dtype=np.int64)
+        if not split:
+            for c0 in range(0, len(ks), 8):  # eight stream slots per call
+                part = ks[c0:c0 + 8]
+                arr = np.ascontiguousarray(host[part])
+                st_p = stage + c0 * depth * each if stage else 0
+                _native.check(self.lib.msurf_sweep_jobs_capped(arr.ctypes.data, len(part), mode | flag | wide, max_pts,
+                                                               stocks[c0:].ctypes.data, depth, st_p, each, 0, sp))
+            return None
+        lib = self.lib
+        anchors = []
+        for n, k in enumerate(ks):
+            anchor = lib.msurf_anchor_stream(n % 8)
+            if not anchor:
+                raise MillsurfError("libmsurf: no anchor stream")
+            _native.check(lib.msurf_stream_wait(anchor, sp))
+            arr = np.ascontiguousarray(host[k:k + 1])
+            st_p = stage + n * depth * each if stage else 0
+            _native.check(lib.msurf_sweep_jobs_capped(arr.ctypes.data, 1, mode | flag | wide, max_pts,
+                                                      stocks[n:].ctypes.data, depth, st_p, each, n % 8, anchor))
+            anchors.append(anchor)
+        return anchors
 
     def _launch_job(self, g: int, k: int, mode: int, flag: int, max_pts: int, sp: int) -> None:
         """Job k of by-value launch group g (a surface-cap job through
@@ -600,11 +631,16 @@ class SweepBatch:
         # surface-cap jobs run side by side (one joined call) before the strip loop:
         # their decodes and copies then follow, no longer overlapping the sweep
         capped = [k for k, t in enumerate(self.group_tiles[0]) if t and self.zc_seq[0][k] is not None]
+        anchor_of = {}
         if capped:
-            self._launch_capped(0, capped, mode, flag, max_pts, sp)
+            # side by side, in strip order of stream priority; each strip's decode
+            # and copy-out waits for that strip's own jobs only
+            anchor_of = dict(zip(capped, self._launch_capped(0, capped, mode, flag, max_pts, sp, split=True)))
         for q in range(s.n_strips):
             for k in by_lo.get(s.j_lo + s.col0[q], ()):
-                if self.group_tiles[0][k] and self.zc_seq[0][k] is None:
+                if k in anchor_of:
+                    _native.check(lib.msurf_stream_wait(sp, anchor_of[k]))
+                elif self.group_tiles[0][k]:
                     self._launch_job(0, k, mode, flag, max_pts, sp)
             _native.check(lib.msurf_decode_strips(
                 self.strip_keys.data_ptr() + s.strip_off * 8, self.keys.data_ptr() + s.key_off * 8, rows, w_all,

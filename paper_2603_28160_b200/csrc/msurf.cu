@@ -41,6 +41,10 @@ constexpr int kBatchTile = 64, kBatchThreads = 32;   // msurf_sweep (job arrays)
 constexpr int kTiltTile = 64, kTiltThreads = 32;     // msurf_sweep_job, EXT_TILT
 constexpr int kWideTile = 128, kWideThreads = 128;   // msurf_sweep_job, REF / EXT
 constexpr int kCapThreads = 256;                     // msurf_sweep_job_capped (EXT_TILT, 64-step tiles)
+#ifndef MSURF_STAGE_THREADS
+#define MSURF_STAGE_THREADS 64
+#endif
+constexpr int kStageThreads = MSURF_STAGE_THREADS;   // staged phase-1 CTAs (64-step tiles)
 #ifndef MSURF_MIN_BLOCKS_ONE
 #define MSURF_MIN_BLOCKS_ONE 32  // 1-warp CTAs with a by-value job: 64 registers (no spills since the folded locate)
 #endif
@@ -826,42 +830,43 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
     if constexpr (ONE) return; else goto tile_done;
   }
   if constexpr (STAGE) {
-    static_assert(ONE && MODE == MSURF_MODE_EXT_TILT && kSweepWarps == 1 && TILE == 64, "staged shape");
-    {  // staged launch: phase 1's rows and masks + the live units out, phase 2 in sweep_units_kernel
-      unsigned char* sbuf = static_cast<unsigned char*>(J.stage);
-      unsigned* hdr = reinterpret_cast<unsigned*>(sbuf);
-      unsigned slot = 0;
-      if (lane == 0) slot = atomicAdd(hdr, 1u);
-      slot = __shfl_sync(0xffffffffu, slot, 0);
-      const long long stride = stage_rec_bytes(mask_words);
-      unsigned char* rec = sbuf + kStageHeader + (long long)slot * stride;
-      if (lane == 0) *reinterpret_cast<unsigned long long*>(rec) = (unsigned long long)n_live;
-      double* rr = reinterpret_cast<double*>(rec + 8);
-      for (int i = lane; i < n_live * 6; i += 32) rr[i] = rowv[(i / 6) * 8 + (i % 6)];
-      unsigned long long* rm = reinterpret_cast<unsigned long long*>(rec + 8 + 64 * 48);
-      for (int i = lane; i < n_live * mask_words; i += 32) rm[i] = mslot[i];
-      const long long max_tiles = (J.step_hi - J.step_lo + 63) / 64;
-      unsigned long long* units = reinterpret_cast<unsigned long long*>(sbuf + kStageHeader + max_tiles * stride);
-      for (int qb = 0; qb < nchunk; qb += 32) {
-        const int qq = qb + lane;
-        bool live = false;
-        if (qq < nchunk)
-          for (int s2 = 0; s2 < n_live; ++s2) live |= ((mslot[s2 * mask_words + (qq >> 6)] >> (qq & 63)) & 1ull) != 0;
-        const unsigned bal = __ballot_sync(0xffffffffu, live);
-        if (bal) {
-          unsigned base = 0;
-          if (lane == 0) base = atomicAdd(hdr + 1, (unsigned)__popc(bal));
-          base = __shfl_sync(0xffffffffu, base, 0);
-          if (live) units[base + __popc(bal & ((1u << lane) - 1u))] = ((unsigned long long)slot << 32) | (unsigned)qq;
-        }
+    static_assert(ONE && MODE == MSURF_MODE_EXT_TILT && TILE == 64, "staged shape");
+    // staged launch: phase 1's rows and masks + the live units out, phase 2 in
+    // sweep_units_kernel
+    __shared__ unsigned s_slot;
+    unsigned char* sbuf = static_cast<unsigned char*>(J.stage);
+    unsigned* hdr = reinterpret_cast<unsigned*>(sbuf);
+    if (tid == 0) s_slot = atomicAdd(hdr, 1u);
+    if constexpr (kSweepWarps == 1) __syncwarp(); else __syncthreads();
+    const unsigned slot = s_slot;
+    const long long stride = stage_rec_bytes(mask_words);
+    unsigned char* rec = sbuf + kStageHeader + (long long)slot * stride;
+    if (tid == 0) *reinterpret_cast<unsigned long long*>(rec) = (unsigned long long)n_live;
+    double* rr = reinterpret_cast<double*>(rec + 8);
+    for (int i = tid; i < n_live * 6; i += kSweepThreads) rr[i] = rowv[(i / 6) * 8 + (i % 6)];
+    unsigned long long* rm = reinterpret_cast<unsigned long long*>(rec + 8 + 64 * 48);
+    for (int i = tid; i < n_live * mask_words; i += kSweepThreads) rm[i] = mslot[i];
+    const long long max_tiles = (J.step_hi - J.step_lo + 63) / 64;
+    unsigned long long* units = reinterpret_cast<unsigned long long*>(sbuf + kStageHeader + max_tiles * stride);
+    for (int qb = warp * 32; qb < nchunk; qb += kSweepThreads) {
+      const int qq = qb + lane;
+      bool live = false;
+      if (qq < nchunk)
+        for (int s2 = 0; s2 < n_live; ++s2) live |= ((mslot[s2 * mask_words + (qq >> 6)] >> (qq & 63)) & 1ull) != 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, live);
+      if (bal) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(hdr + 1, (unsigned)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (live) units[base + __popc(bal & ((1u << lane) - 1u))] = ((unsigned long long)slot << 32) | (unsigned)qq;
       }
-      if (lane == 0 && J.counters) {
-        atomicAdd(J.counters + MSURF_CTR_LIVE_ROWS, (unsigned long long)n_live);
-        atomicAdd(J.counters + MSURF_CTR_EVAL, (unsigned long long)n_eval_cta);
-        atomicAdd(J.counters + MSURF_CTR_ENGAGED_ROWS, (unsigned long long)n_eng_cta);
-      }
-      return;
     }
+    if (tid == 0 && J.counters) {
+      atomicAdd(J.counters + MSURF_CTR_LIVE_ROWS, (unsigned long long)n_live);
+      atomicAdd(J.counters + MSURF_CTR_EVAL, (unsigned long long)n_eval_cta);
+      atomicAdd(J.counters + MSURF_CTR_ENGAGED_ROWS, (unsigned long long)n_eng_cta);
+    }
+    return;
   }
 
   // ---------------- phase 2: lane = live step(s), warp walks the 32 points of a chunk
@@ -2080,17 +2085,25 @@ static int staged_launch(const msurf_job& sub, int32_t max_points, cudaStream_t 
   const int mask_words = (nchunk + 63) / 64;
   cudaError_t e = cudaMemsetAsync(sub.stage, 0, 16, st);
   if (e != cudaSuccess) return set_err(std::string("staged_launch: ") + cudaGetErrorString(e));
-  e = launch_shape<MSURF_MODE_EXT_TILT, 0, true, kTiltTile, kTiltThreads, true>(job_tiles(sub, kTiltTile), st, nullptr,
-                                                                                1, nullptr, mask_words, sub, nullptr,
-                                                                                nullptr);
+  // phase 1 with two warps over the 64 steps (one round per CTA instead of two)
+  e = launch_shape<MSURF_MODE_EXT_TILT, 0, true, kTiltTile, kStageThreads, true>(job_tiles(sub, kTiltTile), st, nullptr,
+                                                                                 1, nullptr, mask_words, sub, nullptr,
+                                                                                 nullptr);
   if (e != cudaSuccess) return set_err(std::string("staged_launch: phase 1: ") + cudaGetErrorString(e));
   if (check_launch("sweep_kernel (staged)")) return 1;
-  int dev = 0, sms = 148, per_sm = 1;
+  // resident one-warp CTAs of the units kernel, queried once per device
+  static int slots[64] = {};
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_units_kernel<0>, 32, 0);
+  if (dev < 0 || dev >= 64) return set_err("staged_launch: device index");
+  if (!slots[dev]) {
+    int sms = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_units_kernel<0>, 32, 0);
+    slots[dev] = sms * std::max(per_sm, 1);
+  }
   const long long units_max = job_tiles(sub, kTiltTile) * nchunk;
-  const long long grid = std::min<long long>(units_max, (long long)sms * std::max(per_sm, 1));
+  const long long grid = std::min<long long>(units_max, (long long)slots[dev]);
   if (grid > 0) sweep_units_kernel<0><<<(unsigned)grid, 32, 0, st>>>(sub, mask_words);
   return check_launch("sweep_units_kernel");
 }

@@ -398,7 +398,8 @@ class SweepBatch:
                     if p.passes * p.teeth < 2 or not self.group_tiles[g][k]:
                         continue
                     rows, cols = p.grid.m + 1, hi - lo + 1
-                    zc = torch.zeros(((rows + 31) // 32) * ((cols + 31) // 32), dtype=torch.float32, device=self.dev)
+                    # written by the first cap refresh of every launch
+                    zc = torch.empty(((rows + 31) // 32) * ((cols + 31) // 32), dtype=torch.float32, device=self.dev)
                     host[k]["zcap"] = zc.data_ptr()
                     seqs[k] = (p.passes * p.teeth, zc, int(host[k]["keys"]), int(host[k]["ld"]), rows, cols,
                                self.base + self.sentinel_off + 8 * i)

@@ -41,6 +41,10 @@ constexpr int kBatchTile = 64, kBatchThreads = 32;   // msurf_sweep (job arrays)
 constexpr int kTiltTile = 64, kTiltThreads = 32;     // msurf_sweep_job, EXT_TILT
 constexpr int kWideTile = 128, kWideThreads = 128;   // msurf_sweep_job, REF / EXT
 constexpr int kCapThreads = 256;                     // msurf_sweep_job_capped (EXT_TILT, 64-step tiles)
+#ifndef MSURF_CHUNK_UNROLL
+#define MSURF_CHUNK_UNROLL 1
+#endif
+constexpr int kChunkUnroll = MSURF_CHUNK_UNROLL;  // phase-1 chunk-cull loop
 #ifndef MSURF_STAGE_THREADS
 #define MSURF_STAGE_THREADS 64
 #endif
@@ -730,6 +734,7 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
             int zc_last = -1;  // the lane's last cap lookup (tile range key, value)
             float zc_cap = 0.f;
             unsigned kept = 0;
+#pragma unroll kChunkUnroll
             for (int q = 0; q < nchunk; ++q) {
               const float4 a = __ldg(cf4 + 2 * q);
               const float4 bz = __ldg(cf4 + 2 * q + 1);  // yz, Rt, zfloor, 0

@@ -14,3 +14,4 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:swee
 for c in 3 4 2; do
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:sweep -s 2 -c 1 -o gpurun_out/${T}_sweep_c$c python tools/gpu/time_sweep.py $c 1 > gpurun_out/${T}_ncu_c$c.log 2>&1; echo "c$c rc=$?"
 done
+bash tools/gpu/run_multirank.sh > gpurun_out/${T}_multirank.log 2>&1; echo "multirank done"

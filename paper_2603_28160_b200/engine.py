@@ -378,8 +378,10 @@ class SweepBatch:
         self.sweep_scratch = torch.empty(need + 1, dtype=torch.int64, device=self.dev) if need else None
         sweeps = sum((sum(1 for t in tl if t) if pj else 1) for pj, tl in zip(self.group_per_job, self.group_tiles))
         self.zc_seq = self._build_zcap_sequences()
-        # a capped job: n = passes x teeth sweeps and n refreshes instead of one launch
-        extra = sum(2 * q[0] - 1 for seqs in self.zc_seq for q in seqs if q is not None)
+        # a capped job: per (pass, tooth) one sweep (staged: phase 1 + phase 2)
+        # and one cap refresh, instead of one launch
+        per = 3 if ZCAP_STAGED else 2
+        extra = sum(per * q[0] - 1 for seqs in self.zc_seq for q in seqs if q is not None)
         self.launches_per_run = 2 * (1 if self.batched_fill else n) + sweeps + extra
 
     def _build_zcap_sequences(self):

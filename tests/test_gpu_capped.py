@@ -1,0 +1,65 @@
+"""The surface-cap path (engine.ZCAP: per-(pass, tooth) launches with a
+per-tile height bound, sub-strips side by side on library streams, staged
+two-kernel launches) is result-neutral: on a reduced config 5 cut into four
+L2 sub-strips, every variant gives the uncapped heights bit for bit, in both
+launch forms (launch(); launch_by_strip(), the e2e path with per-strip joins),
+and the whole simulate() equals the extended oracle."""
+
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+import paper_2603_28160_b200 as ms
+from paper_2603_28160_b200 import configs, engine, planner
+from paper_2603_28160_b200.engine import SweepBatch
+from oracle import fsm_ext_oracle as xorc
+
+pytestmark = pytest.mark.gpu
+
+
+def _reduced_config5():
+    cfg, ext, _ = configs.config5()
+    cfg = replace(cfg, grid=ms.GridSpec.from_nodes(0.001, -0.2555, 0.0, 512, 512), edge_point_count=600)
+    cfg = replace(cfg, process=replace(cfg.process, initial_position_mm=(-0.2, None, 0.0)))
+    return cfg, replace(ext, passes=3, stepover_mm=0.2)
+
+
+def _heights(p, by_strip=False):
+    b = SweepBatch([(p, 0, p.grid.n)])
+    if by_strip:
+        b.launch_by_strip(lambda q, c0, w: None)
+    else:
+        b.launch()
+    out = b.heights()[0].cpu().numpy().copy()
+    return out, b
+
+
+@pytest.mark.parametrize("staged", [True, False])
+@pytest.mark.parametrize("depth", [0, 1, 3])
+def test_capped_variants_equal_uncapped(monkeypatch, staged, depth):
+    cfg, ext = _reduced_config5()
+    p = planner.plan(cfg, ext)
+    monkeypatch.setattr(engine, "L2_TILE_BYTES", (p.grid.m + 1) * (p.grid.n + 1) * 8 // 4 + 8)
+    monkeypatch.setattr(engine, "ZCAP", False)
+    ref, b0 = _heights(p)
+    assert b0.surfs[0].n_strips == 4 and all(q is None for s in b0.zc_seq for q in s)
+    monkeypatch.setattr(engine, "ZCAP", True)
+    monkeypatch.setattr(engine, "ZCAP_STAGED", staged)
+    monkeypatch.setattr(engine, "ZCAP_DEPTH", depth)
+    got, b1 = _heights(p)
+    assert sum(q is not None for s in b1.zc_seq for q in s) == 4
+    assert np.array_equal(got, ref), int(np.count_nonzero(got != ref))
+    got2, _ = _heights(p, by_strip=True)
+    assert np.array_equal(got2, ref), int(np.count_nonzero(got2 != ref))
+
+
+def test_capped_simulate_equals_ext_oracle(monkeypatch):
+    cfg, ext = _reduced_config5()
+    p = planner.plan(cfg, ext)
+    monkeypatch.setattr(engine, "L2_TILE_BYTES", (p.grid.m + 1) * (p.grid.n + 1) * 8 // 3 + 8)
+    h_ref, _, ctr, _ = xorc.ext_sweep(cfg, ext, workers=8)
+    res = ms.simulate(cfg, ext, trig="host")
+    assert res._launch.batch.pipelined_strips()
+    assert np.array_equal(res.field.heights, h_ref)
+    assert res.cells_updated == ctr["cells_updated"]

@@ -453,3 +453,30 @@ def test_ext_oracle_ball_raster_scallop_height():
     ridge = float(h2[p.m // 2].mean())  # midway between the pass centres
     assert abs(ridge - expect) < 0.1 * expect, (ridge, expect)
     assert float(h2[0].mean()) < 0.1 * expect  # pass centre: cut to the ball bottom
+
+
+@pytest.mark.parametrize("cid", [2, 5])
+def test_chunk_zfloor_bounds_every_point_at_every_angle(cid):
+    """The stock-height / surface-cap culls rest on chunk_zfloor: for every
+    point of a chunk and ANY spindle angle, z' >= sin(tau) * v_centre + zfloor
+    + stock (v_centre = the chunk circle centre rotated like the kernel's fp32
+    test). Checked on the tilt plans of configs 2 and 5 at 720 angles."""
+    from paper_2603_28160_b200 import configs
+
+    cfg, ext, _ = configs.FACTORIES[cid]()
+    p = planner.plan(cfg, ext)
+    zf = planner.plan_zfloor(p)
+    circ = p.chunk_circ
+    n = p.points
+    nch = circ.shape[1]
+    th = np.linspace(0.0, 2.0 * math.pi, 720, endpoint=False)
+    c, s = np.cos(th)[:, None], np.sin(th)[:, None]
+    for k in range(p.teeth):
+        x, y, w = p.pts[k, :, 0], p.pts[k, :, 1], p.pts[k, :, 3]
+        v = c * y[None] - s * x[None]                      # (angles, points)
+        z = p.tilt_s * v + w[None]
+        vc = c * circ[k, :, 1][None] - s * circ[k, :, 0][None]  # (angles, chunks)
+        bound = p.tilt_s * vc + zf[k][None] + p.initial_height
+        q = np.arange(n) // 32
+        assert np.all(z >= bound[:, q] - 1e-12), float(np.min(z - bound[:, q]))
+    assert zf.shape == (p.teeth, nch)

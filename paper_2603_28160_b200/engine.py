@@ -48,6 +48,10 @@ ONE_JOB_MIN_TILES = int(__import__("os").environ.get("MSURF_ONE_JOB_MIN_TILES", 
 ZCAP = __import__("os").environ.get("MSURF_ZCAP", "1") != "0"
 # eight-warp CTAs for capped launches (measured slower once launches overlap)
 ZCAP_WIDE = __import__("os").environ.get("MSURF_ZCAP_WIDE", "0") != "0"
+# slab budget of capped surfaces: their phase 1 repeats per slab, their RED
+# stream is small (config 5 sweep with 48 / 72 / 96 / 160 MB slabs: 15.5 /
+# 14.1 / 14.2 / 17.5 ms)
+ZCAP_L2_TILE_BYTES = int(float(__import__("os").environ.get("MSURF_ZCAP_L2_TILE_MB", "72")) * (1 << 20))
 ZCAP_MIN_JOBS = int(__import__("os").environ.get("MSURF_ZCAP_MIN_JOBS", "1"))  # capped jobs swept side by side
 # overlapping (pass, tooth) launches per capped job. Measured on config 5 (3
 # sub-strip jobs; sweep without caps 37.3 ms): single-kernel launches depth 1 /
@@ -218,7 +222,10 @@ class SweepBatch:
             # surfaces above the L2 budget are cut into feed-direction sub-strips;
             # their keys live strip by strip (contiguous slab per sweep job) and the
             # decode writes the row-major heights (msurf_decode_strips)
-            k = 1 if s.plan.record else max(1, min(w, -(-rows * w * 8 // l2_tile_bytes)))
+            budget = l2_tile_bytes
+            if ZCAP and s.plan.mode == MODE_EXT_TILT and s.plan.passes * s.plan.teeth > 1:
+                budget = max(budget, ZCAP_L2_TILE_BYTES)  # capped surfaces: fewer, larger slabs
+            k = 1 if s.plan.record else max(1, min(w, -(-rows * w * 8 // budget)))
             s.n_strips = k
             s.col0 = [(w * q) // k for q in range(k + 1)]
             if k > 1:

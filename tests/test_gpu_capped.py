@@ -40,7 +40,9 @@ def _heights(p, by_strip=False):
 def test_capped_variants_equal_uncapped(monkeypatch, staged, depth):
     cfg, ext = _reduced_config5()
     p = planner.plan(cfg, ext)
-    monkeypatch.setattr(engine, "L2_TILE_BYTES", (p.grid.m + 1) * (p.grid.n + 1) * 8 // 4 + 8)
+    quarter = (p.grid.m + 1) * (p.grid.n + 1) * 8 // 4 + 8
+    monkeypatch.setattr(engine, "L2_TILE_BYTES", quarter)
+    monkeypatch.setattr(engine, "ZCAP_L2_TILE_BYTES", quarter)
     monkeypatch.setattr(engine, "ZCAP", False)
     ref, b0 = _heights(p)
     assert b0.surfs[0].n_strips == 4 and all(q is None for s in b0.zc_seq for q in s)
@@ -57,7 +59,9 @@ def test_capped_variants_equal_uncapped(monkeypatch, staged, depth):
 def test_capped_simulate_equals_ext_oracle(monkeypatch):
     cfg, ext = _reduced_config5()
     p = planner.plan(cfg, ext)
-    monkeypatch.setattr(engine, "L2_TILE_BYTES", (p.grid.m + 1) * (p.grid.n + 1) * 8 // 3 + 8)
+    third = (p.grid.m + 1) * (p.grid.n + 1) * 8 // 3 + 8
+    monkeypatch.setattr(engine, "L2_TILE_BYTES", third)
+    monkeypatch.setattr(engine, "ZCAP_L2_TILE_BYTES", third)
     h_ref, _, ctr, _ = xorc.ext_sweep(cfg, ext, workers=8)
     res = ms.simulate(cfg, ext, trig="host")
     assert res._launch.batch.pipelined_strips()

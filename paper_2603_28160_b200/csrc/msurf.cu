@@ -734,6 +734,8 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
             int zc_last = -1;  // the lane's last cap lookup (tile range key, value)
             float zc_cap = 0.f;
             unsigned kept = 0;
+            unsigned long long bits = 0ull;
+            bool last_hit = false;
 #pragma unroll kChunkUnroll
             for (int q = 0; q < nchunk; ++q) {
               const float4 a = __ldg(cf4 + 2 * q);
@@ -741,7 +743,7 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
               const float uc = fmaf(cf, a.x, sf * a.y);
               const float vc = fmaf(cf, a.y, -(sf * a.x));
               bool hit = (fabsf(uc + oxf) <= hx + a.z) & (fabsf(fmaf(tcc, vc, bz.x) + oyf) <= hy + a.w);
-              const float zmg = 4e-6f * (rt_f + fabsf(bz.z)) + 1e-6f;
+              const float zmg = bz.w;  // 4e-6 (Rt + |zfloor|) + 1e-6, rounded up on the host (planner.chunk_f32)
               const float zlow = fmaf(tsz, vc, bz.z);  // lowest reachable z' - stock, this step
               if (DIAG != 1) hit &= zlow <= zmg;
               if (zc_on && hit) {
@@ -776,11 +778,16 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
                 }
                 hit = zlow <= zc_cap + zmg;
               }
-              if (hit) {
-                my_mask[q >> 6] |= 1ull << (q & 63);
-                kept += (q == nchunk - 1) ? (unsigned)(npts - 32 * q) : 32u;
+              // the step's chunk mask in a register, stored once per 64 chunks
+              bits |= (unsigned long long)hit << (q & 63);
+              if ((q & 63) == 63 || q == nchunk - 1) {
+                my_mask[q >> 6] = bits;
+                kept += 32u * (unsigned)__popcll(bits);
+                bits = 0ull;
               }
+              last_hit = hit;
             }
+            if (last_hit) kept -= (unsigned)(32 * nchunk - npts);  // the last chunk is partial
             any = kept != 0;
             my_eval = kept;
           }

@@ -261,11 +261,13 @@ def _pack(p: SweepPlan) -> None:
 
 def chunk_f32(chunk_circ: np.ndarray, tooth_box: np.ndarray, zfloor: np.ndarray | None = None) -> np.ndarray:
     """fp32 phase-1 cull records (msurf_job.chunk_f32): per tooth and chunk
-    (xc, yc, rx, ry, yz, Rt, zfloor, 0), Rt = max|x| + max|y| + max|z| of the
-    tooth box, zfloor = chunk_zfloor (0 when not given). The kernel widens its
-    fp32 tests by 4e-6 (Rt + |offset|) + 1e-6 mm, which covers the fp32
-    roundings of every term. Leading (set) axes are allowed:
-    (..., Z, nchunk, 6) and (..., Z, 6)."""
+    (xc, yc, rx, ry, yz, Rt, zfloor, zmargin), Rt = max|x| + max|y| + max|z| of
+    the tooth box, zfloor = chunk_zfloor (0 when not given). The kernel widens
+    its fp32 tests by 4e-6 (Rt + |offset|) + 1e-6 mm, which covers the fp32
+    roundings of every term; for the z tests that margin,
+    4e-6 (Rt + |zfloor|) + 1e-6, is precomputed here in fp64 and rounded up to
+    fp32 (zmargin). Leading (set) axes are allowed: (..., Z, nchunk, 6) and
+    (..., Z, 6)."""
     out = np.zeros(chunk_circ.shape[:-1] + (8,), dtype=np.float32)
     out[..., :5] = chunk_circ[..., :5]
     b = np.abs(tooth_box)
@@ -274,6 +276,10 @@ def chunk_f32(chunk_circ: np.ndarray, tooth_box: np.ndarray, zfloor: np.ndarray 
     out[..., 5] = rt[..., None]
     if zfloor is not None:
         out[..., 6] = zfloor
+    zf = out[..., 6].astype(np.float64)
+    mg = 4e-6 * (out[..., 5].astype(np.float64) + np.abs(zf)) + 1e-6
+    m32 = mg.astype(np.float32)
+    out[..., 7] = np.where(m32.astype(np.float64) < mg, np.nextafter(m32, np.float32(np.inf)), m32)
     return out
 
 

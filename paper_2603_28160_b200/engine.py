@@ -65,6 +65,8 @@ ZCAP_STAGED = __import__("os").environ.get("MSURF_ZCAP_STAGED", "1") != "0"
 def _per_job_launches(tiles) -> bool:
     live = [t for t in tiles if t]
     return len(live) <= 1 or (len(tiles) <= ONE_JOB_LAUNCH_MAX and min(live) >= ONE_JOB_MIN_TILES)
+# launch-group size of large simulate_batch calls
+BATCH_CHUNK = int(__import__("os").environ.get("MSURF_BATCH_CHUNK", "32"))
 PIPELINE_PLAN_THREADS = int(__import__("os").environ.get("MSURF_PIPELINE_THREADS", "1"))
 # size of the first launch group of a pipelined batch (the GPU starts sooner)
 PIPELINE_FIRST_CHUNK = int(__import__("os").environ.get("MSURF_FIRST_CHUNK", "0"))
@@ -874,7 +876,7 @@ def simulate_batch(configs, extensions=None, *, trig: str = "device", diagnostic
     if not configs:
         return []
     if chunk is None:
-        chunk = 32 if len(configs) >= 128 else max(4, -(-len(configs) // 4))
+        chunk = BATCH_CHUNK if len(configs) >= 128 else max(4, -(-len(configs) // 4))
     first = min(chunk, PIPELINE_FIRST_CHUNK) if PIPELINE_FIRST_CHUNK > 0 else chunk
     bounds = [(0, min(len(configs), first))]
     bounds += [(lo, min(len(configs), lo + chunk)) for lo in range(bounds[0][1], len(configs), chunk)]

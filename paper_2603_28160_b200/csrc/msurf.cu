@@ -872,6 +872,16 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
         base = __shfl_sync(0xffffffffu, base, 0);
         if (live) units[base + __popc(bal & ((1u << lane) - 1u))] = ((unsigned long long)slot << 32) | (unsigned)qq;
       }
+#ifdef MSURF_STAGE_STATS  // experiment only: lane-slot utilisation of the staged units
+      if (qq < nchunk) {
+        unsigned cnt = 0;
+        for (int s2 = 0; s2 < n_live; ++s2) cnt += (unsigned)((mslot[s2 * mask_words + (qq >> 6)] >> (qq & 63)) & 1ull);
+        if (cnt && J.counters) {
+          atomicAdd(J.counters + MSURF_CTR_DEPOSITS, 64ull);
+          atomicAdd(J.counters + MSURF_CTR_ATOMICS, (unsigned long long)cnt);
+        }
+      }
+#endif
     }
     if (tid == 0 && J.counters) {
       atomicAdd(J.counters + MSURF_CTR_LIVE_ROWS, (unsigned long long)n_live);

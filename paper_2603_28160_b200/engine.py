@@ -395,8 +395,8 @@ class SweepBatch:
 
     def _build_zcap_sequences(self):
         """Per launch group, per job: None, or the surface-cap state of a
-        tilt-mode by-value job of more than one (pass, tooth) — its cap tile
-        array, slab geometry and stock pointer (msurf_sweep_job_capped)."""
+        tilt-mode by-value job of more than one (pass, tooth): its launch
+        count, cap tile array and stock pointer (msurf_sweep_jobs_capped)."""
         torch = self.torch
         out = []
         for g, (mode, jidx, _, _, _, _) in enumerate(self.group_meta):
@@ -412,13 +412,13 @@ class SweepBatch:
                     # written by the first cap refresh of every launch
                     zc = torch.empty(((rows + 31) // 32) * ((cols + 31) // 32), dtype=torch.float32, device=self.dev)
                     host[k]["zcap"] = zc.data_ptr()
-                    seqs[k] = (p.passes * p.teeth, zc, int(host[k]["keys"]), int(host[k]["ld"]), rows, cols,
-                               self.base + self.sentinel_off + 8 * i)
+                    # (launches, the cap tiles kept alive, the device stock height)
+                    seqs[k] = (p.passes * p.teeth, zc, self.base + self.sentinel_off + 8 * i)
                 # the (pass, tooth) launches of one job are short and underfill the
                 # GPU: several jobs (L2 sub-strips) run side by side and each
-                # keeps ceil(3 / jobs) launches in flight (measured, staged
-                # form: config 5 at N = 1 / 2 / 4 / 8 strips per GPU 16.6 / 8.6 /
-                # 5.3 / 3.4 ms; config 2, one job: 0.70 ms, as uncapped)
+                # keeps ceil(3 / jobs) launches in flight (measured, staged form,
+                # 72 MB slabs: config 5 at N = 1 / 2 / 4 / 8 strips per GPU 14.5 /
+                # 8.7 / 4.7 / 2.8 ms; config 2, one job: 0.59 vs 0.69 ms uncapped)
                 if sum(q is not None for q in seqs) < ZCAP_MIN_JOBS:
                     for k, q in enumerate(seqs):
                         if q is not None:
@@ -437,17 +437,22 @@ class SweepBatch:
         largest job (msurf_stage_bytes); reused across launches."""
         if not ZCAP_STAGED:
             return 0, 0
+        # one buffer per (group, jobs, depth), kept for the batch's life: CUDA
+        # graphs captured over a launch hold its address
         key = (g, tuple(ks), depth)
-        if getattr(self, "_stage_key", None) != key:
+        if not hasattr(self, "_stages"):
+            self._stages = {}
+        if key not in self._stages:
             host = self.group_host_jobs[g]
             nb = ctypes.c_int64(0)
             each = 0
             for k in ks:
                 _native.check(self.lib.msurf_stage_bytes(host[k:k + 1].ctypes.data, max_pts, ctypes.byref(nb)))
                 each = max(each, (nb.value + 255) // 256 * 256)
-            self._stage = self.torch.empty(each * len(ks) * depth, dtype=self.torch.uint8, device=self.dev)
-            self._stage_key, self._stage_each = key, each
-        return self._stage.data_ptr(), self._stage_each
+            buf = self.torch.empty(each * len(ks) * depth, dtype=self.torch.uint8, device=self.dev)
+            self._stages[key] = (buf, each)
+        buf, each = self._stages[key]
+        return buf.data_ptr(), each
 
     def _launch_capped(self, g: int, ks, mode: int, flag: int, max_pts: int, sp: int, split: bool = False):
         """Surface-cap jobs ks of by-value group g side by side

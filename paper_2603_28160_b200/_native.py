@@ -68,6 +68,9 @@ class MsurfGeomIn(ctypes.Structure):
     ]
 
 
+# the same layout as a NumPy structured dtype (planner fills B records at once)
+GEOM_IN_DTYPE = np.dtype(MsurfGeomIn)
+
 EXPORTS = {
     "msurf_abi_version": (ctypes.c_int, []),
     "msurf_last_error": (ctypes.c_char_p, []),

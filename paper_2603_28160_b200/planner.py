@@ -292,11 +292,10 @@ def chunk_zfloor(w: np.ndarray, rho: np.ndarray, tilt_s: float, stock) -> np.nda
     stock. The kernel skips a (step, chunk) whose bound is at or above the
     stock top: such evaluations can never lower a key below the initial
     height (a result-neutral cull)."""
-    *lead, n = w.shape
-    nchunk = (n + CHUNK - 1) // CHUNK
-    pad = nchunk * CHUNK - n
-    full = np.concatenate([w, np.repeat(w[..., -1:], pad, axis=-1)], axis=-1) if pad else w
-    wmin = full.reshape(*lead, nchunk, CHUNK).min(axis=-1)
+    n = w.shape[-1]
+    # per-chunk minima (the last chunk is partial; its padding would repeat the
+    # last point, which leaves the minimum unchanged)
+    wmin = np.minimum.reduceat(w, np.arange(0, n, CHUNK), axis=-1)
     stock = np.asarray(stock, dtype=np.float64).reshape(np.shape(stock) + (1,) * (wmin.ndim - np.ndim(stock)))
     return wmin - abs(tilt_s) * rho - stock
 
@@ -704,26 +703,31 @@ def _plan_ext_group_native(configs, exts, threads: int = 1):
     if r_ref is None:
         r_ref = tool.cutting_diameter_mm / 2.0 if e0.profile == "insert" else r
     offs = np.zeros((B, z_n, 2))
-    ins = (_native.MsurfGeomIn * B)()
     mode = MODE_EXT_TILT if tilt else MODE_EXT
+    # the B msurf_geom_in records as one structured array (ctypes layout):
+    # per-set scalars by columns instead of ~15 ctypes attribute writes per set
+    ins = np.zeros(B, dtype=_native.GEOM_IN_DTYPE)
+    ins["mode"], ins["teeth"], ins["points"] = mode, z_n, n
+    ins["profile"] = 0 if e0.profile == "insert" else 1
+    ins["radius"], ins["half"], ins["kmax"] = r, half if e0.profile == "insert" else 0.0, kmax
+    ins["tan_beta_over_r"] = [math.tan(e.helix_angle_rad) / r_ref if e.helix_angle_rad != 0.0 else 0.0
+                              for e in exts]
+    ins["tilt_c"], ins["tilt_s"] = tc, ts
+    ins["rows"] = rows.ctypes.data
+    ins["delta"] = delta.ctypes.data if delta is not None else 0
+    two_pi_k = [(2.0 * math.pi) * (k - 1) / z_n for k in range(1, z_n + 1)]
+    base_ptr, stride = offs.ctypes.data, offs.strides[0]
     for b, e in enumerate(exts):
-        g = ins[b]
-        g.mode, g.teeth, g.points, g.profile = mode, z_n, n, 0 if e0.profile == "insert" else 1
-        g.radius, g.half, g.kmax = r, half if e0.profile == "insert" else 0.0, kmax
-        g.tan_beta_over_r = math.tan(e.helix_angle_rad) / r_ref if e.helix_angle_rad != 0.0 else 0.0
-        g.tilt_c, g.tilt_s = tc, ts
-        g.rows = rows.ctypes.data
-        g.delta = delta.ctypes.data if delta is not None else None
         rho, lam = e.runout_offset_mm, e.runout_phase_rad
         if rho != 0.0:
-            for k in range(1, z_n + 1):
-                ang = lam + (2.0 * math.pi) * (k - 1) / z_n
-                offs[b, k - 1] = (rho * math.cos(ang), rho * math.sin(ang))
-            g.runout_xy = offs[b].ctypes.data
+            for k in range(z_n):
+                ang = lam + two_pi_k[k]
+                offs[b, k, 0], offs[b, k, 1] = rho * math.cos(ang), rho * math.sin(ang)
+            ins["runout_xy"][b] = base_ptr + b * stride
     px, py, pz = np.empty((B, z_n, n)), np.empty((B, z_n, n)), np.empty((B, z_n, n))
     stats = np.zeros((B, 2))
-    if lib.msurf_plan_geometry_many(ins, B, px.ctypes.data, py.ctypes.data, pz.ctypes.data, stats.ctypes.data,
-                                    threads):
+    if lib.msurf_plan_geometry_many(ins.ctypes.data, B, px.ctypes.data, py.ctypes.data, pz.ctypes.data,
+                                    stats.ctypes.data, threads):
         raise DomainError("native planner rejected the geometry")
     spans, zoffs = [], np.empty(B)
     for b, (cfg, e) in enumerate(zip(configs, exts)):
@@ -740,7 +744,7 @@ def _plan_ext_group_native(configs, exts, threads: int = 1):
     mins = np.empty((B, z_n), dtype=np.int32)
     zw = np.empty((B, z_n, n))
     zkey = np.empty((B, z_n, n), dtype=np.uint64)
-    if lib.msurf_plan_finish_many(ins, B, px.ctypes.data, py.ctypes.data, pz.ctypes.data, zoffs.ctypes.data,
+    if lib.msurf_plan_finish_many(ins.ctypes.data, B, px.ctypes.data, py.ctypes.data, pz.ctypes.data, zoffs.ctypes.data,
                                   pts.ctypes.data, tbox.ctypes.data, circ.ctypes.data, cbox.ctypes.data,
                                   mins.ctypes.data, zw.ctypes.data, zkey.ctypes.data, threads):
         raise DomainError("native planner rejected the geometry")

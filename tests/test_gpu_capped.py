@@ -67,3 +67,18 @@ def test_capped_simulate_equals_ext_oracle(monkeypatch):
     assert res._launch.batch.pipelined_strips()
     assert np.array_equal(res.field.heights, h_ref)
     assert res.cells_updated == ctr["cells_updated"]
+
+
+def test_capped_many_mask_words_equal_uncapped(monkeypatch):
+    """A tilt surface with 2500 edge points (79 chunks: two 64-bit chunk-mask
+    words per step) through the staged capped path equals the uncapped sweep."""
+    cfg, ext = _reduced_config5()
+    cfg = replace(cfg, edge_point_count=2500)
+    p = planner.plan(cfg, ext)
+    assert (p.points + 31) // 32 > 64
+    monkeypatch.setattr(engine, "ZCAP", False)
+    ref, _ = _heights(p)
+    monkeypatch.setattr(engine, "ZCAP", True)
+    got, b = _heights(p)
+    assert any(q is not None for s in b.zc_seq for q in s)
+    assert np.array_equal(got, ref), int(np.count_nonzero(got != ref))

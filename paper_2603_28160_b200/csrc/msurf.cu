@@ -722,8 +722,9 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
             const float cf = (float)c, sf = (float)sn;
             const float oxf = (float)ox;
             const float tcc = MODE == MSURF_MODE_EXT_TILT ? tcf : 1.0f;
-            const float hx = (float)wxh + (4e-6f * (rt_f + fabsf(oxf)) + 1e-6f);
-            const float hy = (float)wyh + (4e-6f * (rt_f + fabsf(oyf)) + 1e-6f);
+            const float mgx = 4e-6f * (rt_f + fabsf(oxf)) + 1e-6f, mgy = 4e-6f * (rt_f + fabsf(oyf)) + 1e-6f;
+            const float hx = (float)wxh + mgx;
+            const float hy = (float)wyh + mgy;
             // stock-height cull (not in the DIAG=1 counting variant, whose deposit
             // count is the oracle's P_in): z' >= sin(tau) v_centre + zfloor + stock
             // for every point of the chunk (planner.chunk_zfloor); a chunk whose
@@ -755,7 +756,9 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
                 // consecutive chunks of a step mostly touch the same tiles: the lane
                 // reuses its last lookup.
                 const float ci = fmaf(uc + oxf, zc_k, zc_bi), cj = fmaf(fmaf(tcc, vc, bz.x) + oyf, zc_k, zc_bj);
-                const float ri = fmaf(a.z, zc_k, 1.5f), rj = fmaf(a.w, zc_k, 1.5f);
+                // half-extents: the chunk's radii plus the same fp32 margins as the
+                // window test (in mm), plus 1.5 cells for the fp32 cell coordinate
+                const float ri = fmaf(a.z + mgx, zc_k, 1.5f), rj = fmaf(a.w + mgy, zc_k, 1.5f);
                 const int i0 = max(0, __float2int_rd(ci - ri)) >> 5, i1 = min(zc_imax, __float2int_rd(ci + ri)) >> 5;
                 const int j0 = max(0, __float2int_rd(cj - rj)) >> 5, j1 = min(zc_jmax, __float2int_rd(cj + rj)) >> 5;
                 // exact key of the tile range (tile indices < 2^13, spans <= 3); others uncached

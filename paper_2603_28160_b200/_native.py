@@ -280,12 +280,13 @@ class Arena:
         # only after the copy that read it has completed (event recorded by the
         # non-blocking copy), so uploads of consecutive launch groups never wait
         stage = torch.empty(max(self.size, 1), dtype=torch.uint8, pin_memory=True)
-        host = stage.numpy()
+        hp = stage.data_ptr()
+        # ctypes.memmove drops the GIL while it copies (a planner thread keeps running)
         for off, a in self._parts:
-            if a is not None:
-                host[off:off + a.nbytes] = a.view(np.uint8).reshape(-1)
+            if a is not None and a.nbytes:
+                ctypes.memmove(hp + off, a.ctypes.data, a.nbytes)
         for off, b in extra:
             b = b if isinstance(b, np.ndarray) else np.frombuffer(b, dtype=np.uint8)
-            host[off:off + b.nbytes] = b
+            ctypes.memmove(hp + off, b.ctypes.data, b.nbytes)
         dev.copy_(stage, non_blocking=True)
         return dev

@@ -1857,14 +1857,34 @@ __global__ void __launch_bounds__(256)
     if (h[i]) atomicAdd(hist + i, h[i]);
 }
 
+// the node rows one (pass, tooth) launch can have deposited into: x = fma(c, x_t,
+// s y_t) + pass x0 + vibration with |fma(c, x_t, s y_t)| <= max|x_t| + max|y_t|
+// over the tooth's tool-frame box, located to the nearest node (+-2 nodes of
+// slack cover every rounding). x0 == nullptr: every row.
+struct ZBand {
+  const double* x0;   // the launch's pass x0 (device)
+  const double* box;  // its tooth's box (xl, xh, yl, yh, zl, zh) (device)
+  double pad;         // |vibration amplitude|
+  double x_min, inv_h;
+};
+
 // msurf_zcap_refresh: one CTA per 32x32-node tile of a slab, max key ->
-// height - stock rounded up to float (an upper bound for the cull)
+// height - stock rounded up to float (an upper bound for the cull). With a
+// band, tiles outside it keep their cap: nothing there changed since it was
+// computed, and heights only decrease, so it is still an upper bound.
 __global__ void __launch_bounds__(256)
     zcap_kernel(const uint64_t* __restrict__ keys, long long ld, long long rows, long long cols,
-                const double* __restrict__ stock, float* __restrict__ zcap, int* stop_reset) {
+                const double* __restrict__ stock, float* __restrict__ zcap, int* stop_reset, ZBand band) {
   if (stop_reset && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *stop_reset = 0;
   __shared__ unsigned long long wmax[8];
   const long long i0 = (long long)blockIdx.y * 32, j = (long long)blockIdx.x * 32 + (threadIdx.x & 31);
+  if (band.x0) {  // CTA-uniform
+    const double* b = band.box;
+    const double r = fmax(fabs(b[0]), fabs(b[1])) + fmax(fabs(b[2]), fabs(b[3])) + band.pad;
+    const double x0 = *band.x0;
+    const double lo = (x0 - r - band.x_min) * band.inv_h - 2.0, hi = (x0 + r - band.x_min) * band.inv_h + 2.0;
+    if ((double)(i0 + 31) < lo || (double)i0 > hi) return;
+  }
   unsigned long long m = 0ull;
   if (j < cols)
     for (long long i = i0 + (threadIdx.x >> 5); i < i0 + 32 && i < rows; i += 8) {
@@ -2092,14 +2112,38 @@ int msurf_red_lines(const uint32_t* trace, int64_t n_records, unsigned long long
   return check_launch("red_lines_kernel");
 }
 
-int msurf_zcap_refresh(const uint64_t* keys, int64_t ld, int64_t rows, int64_t cols, const double* stock,
-                       float* zcap, int32_t* stop_reset, void* stream) {
+static int zcap_refresh(const uint64_t* keys, int64_t ld, int64_t rows, int64_t cols, const double* stock,
+                        float* zcap, int32_t* stop_reset, void* stream, const ZBand& band) {
   if (!keys || !stock || !zcap || rows < 1 || cols < 1 || ld < cols) return set_err("msurf_zcap_refresh: bad arguments");
   const long long ti = (rows + 31) / 32, tj = (cols + 31) / 32;
   if (ti > 65535 || tj > 0x7fffffffLL) return set_err("msurf_zcap_refresh: slab too large");
   zcap_kernel<<<dim3((unsigned)tj, (unsigned)ti), 256, 0, (cudaStream_t)stream>>>(keys, ld, rows, cols, stock, zcap,
-                                                                                 stop_reset);
+                                                                                 stop_reset, band);
   return check_launch("zcap_kernel");
+}
+
+int msurf_zcap_refresh(const uint64_t* keys, int64_t ld, int64_t rows, int64_t cols, const double* stock,
+                       float* zcap, int32_t* stop_reset, void* stream) {
+  return zcap_refresh(keys, ld, rows, cols, stock, zcap, stop_reset, stream, ZBand{});
+}
+
+// the refresh after (pass, tooth) launch `sub` of a capped job: only the node
+// rows that launch can have reached (MSURF_ZCAP_BAND=0: the whole slab)
+static int zcap_refresh_after(const msurf_job& sub, const double* stock, void* stream) {
+  static const bool on = [] {
+    const char* e = getenv("MSURF_ZCAP_BAND");
+    return !(e && e[0] == '0');
+  }();
+  ZBand band{};
+  if (on && sub.spacing > 0.0) {
+    band.x0 = sub.pass_x0;
+    band.box = sub.tooth_box + 6 * sub.tooth_lo;
+    band.pad = fabs(sub.vib_amp);
+    band.x_min = sub.x_min;
+    band.inv_h = 1.0 / sub.spacing;
+  }
+  return zcap_refresh(sub.keys, sub.ld, sub.m + 1, sub.j_hi - sub.j_lo + 1, stock, const_cast<float*>(sub.zcap),
+                      nullptr, stream, band);
 }
 
 // one staged (pass, tooth) launch of a capped tilt job: the staging header
@@ -2165,7 +2209,7 @@ int msurf_sweep_job_capped(const msurf_job* job, int32_t mode, int32_t max_point
     sub.tooth_n = 1;
     if (job_tiles(sub, 64) == 0) continue;
     if (sweep_impl(nullptr, 1, nullptr, 0, mode, max_points, stream, &sub, nullptr)) return 1;
-    if (i + 1 < n && msurf_zcap_refresh(job->keys, job->ld, rows, cols, stock, zcap, nullptr, stream)) return 1;
+    if (i + 1 < n && zcap_refresh_after(sub, stock, stream)) return 1;
   }
   return 0;
 }
@@ -2270,7 +2314,7 @@ int msurf_sweep_jobs_capped(const msurf_job* jobs, int32_t n_jobs, int32_t mode,
         sub.stage = nullptr;
         rc = sweep_impl(nullptr, 1, nullptr, 0, mode, max_points, q, &sub, nullptr);
       }
-      if (rc == 0 && i + 1 < n) rc = msurf_zcap_refresh(job->keys, job->ld, rows, cols, stock, zcap, nullptr, q);
+      if (rc == 0 && i + 1 < n) rc = zcap_refresh_after(sub, stock, q);
     }
   }
   for (int j = 0; j < n_jobs; ++j)  // joins are enqueued whatever happened

@@ -15,6 +15,7 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <functional>
 #include <vector>
 
 #include "msurf.h"
@@ -234,24 +235,97 @@ int msurf_plan_finish(const msurf_geom_in* in, const double* px, const double* p
 // teeth and points): set b reads ins[b] and writes its slice of every output
 // (teeth*points, teeth*nchunk*6, ... elements per set). Sets are independent:
 // `threads` host threads split them (results do not depend on the split).
+#include <unistd.h>
+
 #include <atomic>
+#include <condition_variable>
+#include <mutex>
 #include <thread>
 
 namespace {
+// A persistent pool of host workers (created on first use, never joined: the
+// process exit ends them), so a 32-set launch group does not pay for thread
+// creation on every call. One caller at a time owns the pool; a concurrent
+// caller (another planner thread) runs its sets on its own thread instead.
+// The split never changes a result: every set is computed by one thread.
+struct Pool {
+  std::mutex use;  // held by the caller that owns the pool
+  std::mutex m;
+  std::condition_variable wake, idle;
+  std::vector<std::thread> workers;
+  const std::function<void(int)>* job = nullptr;
+  int n = 0, want = 0, busy = 0;
+  std::atomic<int> next{0};
+  uint64_t gen = 0;
+
+  explicit Pool(int k) {
+    for (int t = 0; t < k; ++t) workers.emplace_back([this] { loop(); });
+  }
+  void drain() {
+    for (int b = next.fetch_add(1); b < n; b = next.fetch_add(1)) (*job)(b);
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(m);
+      wake.wait(lk, [&] { return gen != seen && want > 0; });
+      seen = gen;
+      --want;
+      ++busy;
+      lk.unlock();
+      drain();
+      lk.lock();
+      if (--busy == 0) idle.notify_all();
+    }
+  }
+  // run f(0..n-1) on the caller plus up to `helpers` workers
+  void run(int items, int helpers, const std::function<void(int)>& f) {
+    {
+      std::lock_guard<std::mutex> lk(m);
+      job = &f;
+      n = items;
+      next.store(0);
+      want = helpers;
+      ++gen;
+    }
+    wake.notify_all();
+    drain();
+    std::unique_lock<std::mutex> lk(m);
+    want = 0;  // workers that have not started yet stay asleep
+    idle.wait(lk, [&] { return busy == 0; });
+    job = nullptr;
+  }
+};
+
+Pool* pool_get() {
+  static std::mutex mk;
+  static Pool* pool = nullptr;
+  static pid_t owner = 0;
+  std::lock_guard<std::mutex> lk(mk);
+  if (!pool || owner != getpid()) {  // a forked child gets its own (the parent's threads are gone)
+    unsigned hw = std::thread::hardware_concurrency();
+    int k = hw > 1 ? (int)(hw < 16 ? hw : 16) - 1 : 0;
+    pool = new Pool(k);
+    owner = getpid();
+  }
+  return pool;
+}
+
 template <class F>
 void for_sets(int n, int threads, F&& f) {
   if (threads < 1) threads = 1;
   if (threads > n) threads = n;
-  if (threads <= 1) {
-    for (int b = 0; b < n; ++b) f(b);
-    return;
+  if (threads > 1) {
+    Pool* p = pool_get();
+    if ((int)p->workers.size() > 0 && p->use.try_lock()) {
+      const std::function<void(int)> fn = [&](int b) { f(b); };
+      const int helpers = threads - 1 < (int)p->workers.size() ? threads - 1 : (int)p->workers.size();
+      p->run(n, helpers, fn);
+      p->use.unlock();
+      return;
+    }
   }
-  std::vector<std::thread> pool;
-  for (int t = 0; t < threads; ++t)
-    pool.emplace_back([&, t] {
-      for (int b = t; b < n; b += threads) f(b);
-    });
-  for (auto& th : pool) th.join();
+  for (int b = 0; b < n; ++b) f(b);
 }
 }  // namespace
 

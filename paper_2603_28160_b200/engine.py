@@ -73,7 +73,7 @@ PIPELINE_FIRST_CHUNK = int(__import__("os").environ.get("MSURF_FIRST_CHUNK", "0"
 # native planner threads for the first group (planned while nothing else runs)
 PIPELINE_FIRST_THREADS = int(__import__("os").environ.get("MSURF_FIRST_THREADS", "1"))
 # threads of the native planning loops of every group (GIL released)
-PIPELINE_NATIVE_THREADS = int(__import__("os").environ.get("MSURF_NATIVE_THREADS", "1"))
+PIPELINE_NATIVE_THREADS = int(__import__("os").environ.get("MSURF_NATIVE_THREADS", "8"))
 
 __all__ = ["SimulationConfig", "SimulationResult", "time_step", "simulate", "simulate_batch",
            "simulate_reference", "run_benchmark", "BenchmarkReport", "BenchmarkRow", "sweep_plans"]

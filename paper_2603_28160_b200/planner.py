@@ -636,7 +636,13 @@ def plan_many(configs, exts, threads: int | None = None, native_threads: int = 1
         # sub-groups planned on host threads (NumPy releases the GIL inside
         # its element-wise kernels); each sub-group is the same vectorised
         # computation, so the arrays stay bitwise equal to per-set plan()
-        nthr = PLAN_THREADS if threads is None else max(1, threads)
+        # the native group planner spreads a group's sets over its own worker
+        # pool (GIL released): one Python job per group; the NumPy statement
+        # splits groups over Python threads instead
+        if NATIVE_PLAN and threads is None:
+            nthr, native_threads = 1, max(native_threads, PLAN_THREADS)
+        else:
+            nthr = PLAN_THREADS if threads is None else max(1, threads)
         step = max(4, -(-len(idx) // nthr))
         jobs.extend(idx[a: a + step] for a in range(0, len(idx), step))
     if jobs:

@@ -57,7 +57,9 @@ ZCAP_MIN_JOBS = int(__import__("os").environ.get("MSURF_ZCAP_MIN_JOBS", "1"))  #
 # sub-strip jobs; sweep without caps 37.3 ms): single-kernel launches depth 1 /
 # 2 / 3 / 4 -> 27.1 / 20.5 / 20.3 / 20.9 ms; staged two-kernel launches depth
 # 1 / 2 / 3 -> 16.7 / 17.0 / 19.6 ms
-ZCAP_DEPTH = int(__import__("os").environ.get("MSURF_ZCAP_DEPTH", "0"))  # 0: ceil(3 / capped jobs)
+ZCAP_DEPTH = int(__import__("os").environ.get("MSURF_ZCAP_DEPTH", "0"))  # 0: SweepBatch._capped_depth
+# step-points of a (pass, tooth) launch above which it fills the GPU alone
+ZCAP_LONG_LAUNCH = float(__import__("os").environ.get("MSURF_ZCAP_LONG_LAUNCH", "3e8"))
 # capped launches as two kernels: phase 1 staged to HBM, phase 2 balanced over every warp
 ZCAP_STAGED = __import__("os").environ.get("MSURF_ZCAP_STAGED", "1") != "0"
 
@@ -427,10 +429,21 @@ class SweepBatch:
             out.append(seqs)
         return out
 
-    def _capped_depth(self, n_jobs: int) -> int:
-        # overlap: about three capped launches in flight per GPU in total
-        depth = ZCAP_DEPTH if ZCAP_DEPTH > 0 else -(-3 // n_jobs)
-        return max(1, min(depth, 4))
+    def _capped_depth(self, g: int, ks) -> int:
+        """Launches in flight per capped job: about three per GPU in total for
+        short (pass, tooth) launches, which underfill the GPU on their own; two
+        for long ones, which fill it, so that the caps each launch reads are
+        fresher (measured: config 2, one job of ~1.3e8 step-points per launch,
+        0.88 / 0.62 / 0.59 ms at 1 / 2 / 3 in flight; config 5, two jobs of
+        ~6.4e8, 13.6 / 13.8 / 16.9 ms at 2 / 4 / 6)."""
+        if ZCAP_DEPTH > 0:
+            return max(1, min(ZCAP_DEPTH, 4))
+        work = 0
+        for k in ks:
+            i, _, _, s_lo, s_hi = self.jobs[self.group_meta[g][1][k]]
+            work = max(work, (s_hi - s_lo) * self.surfs[i].plan.points)
+        total = 2 if work >= ZCAP_LONG_LAUNCH else 3
+        return max(1, min(-(-total // len(ks)), 4))
 
     def _capped_stage(self, g: int, ks, depth: int, max_pts: int):
         """Staging buffer: one (job, in-flight launch) slot each, sized for the
@@ -463,7 +476,7 @@ class SweepBatch:
         earlier ones at higher stream priority."""
         host = self.group_host_jobs[g]
         wide = _native.SWEEP_WIDE if ZCAP_WIDE else 0
-        depth = self._capped_depth(len(ks))
+        depth = self._capped_depth(g, ks)
         stage, each = self._capped_stage(g, ks, depth, max_pts)
         stocks = np.array([self.zc_seq[g][k][-1] for k in ks], dtype=np.int64)
         if not split:

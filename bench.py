@@ -450,7 +450,9 @@ def measure_surface(cfg_id, args, rank, world, with_cpu):
     value = p_total / (ms_per_step * 1e-3)
 
     mode = p.mode
-    evald, live, engaged = int(ctr[0][1]), int(ctr[0][0]), int(ctr[0][4])
+    # engaged rows (SURVEY P_eng) from the counting launch: the production
+    # variant's tile pre-cull skips whole tiles before it counts them
+    evald, live, engaged = int(ctr[0][1]), int(ctr[0][0]), int(dctr[0][4])
     flops = FLOPS_PER_POINT[mode] * evald + FLOPS_PER_ROW * live
     # the production sweep's RED count (its trace); the DIAG launch counts the
     # oracle's P_in without the stock-height cull, so its atomics are higher
@@ -584,7 +586,7 @@ def measure_batch(args, rank, world, with_cpu):
     ms_step = float(tot[0]) / args.steps
     sweep_avg = float(tot[1]) / args.steps
     value = total_points / (ms_step * 1e-3)
-    evald, live, engaged = int(ctr[:, 1].sum()), int(ctr[:, 0].sum()), int(ctr[:, 4].sum())
+    evald, live, engaged = int(ctr[:, 1].sum()), int(ctr[:, 0].sum()), int(dctr[:, 4].sum())
     npts = plans[0].points
     mode = plans[0].mode
     flops = FLOPS_PER_POINT[mode] * evald + FLOPS_PER_ROW * live

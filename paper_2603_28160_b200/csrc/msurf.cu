@@ -41,10 +41,6 @@ constexpr int kBatchTile = 64, kBatchThreads = 32;   // msurf_sweep (job arrays)
 constexpr int kTiltTile = 64, kTiltThreads = 32;     // msurf_sweep_job, EXT_TILT
 constexpr int kWideTile = 128, kWideThreads = 128;   // msurf_sweep_job, REF / EXT
 constexpr int kCapThreads = 256;                     // msurf_sweep_job_capped (EXT_TILT, 64-step tiles)
-#ifndef MSURF_CHUNK_UNROLL
-#define MSURF_CHUNK_UNROLL 1
-#endif
-constexpr int kChunkUnroll = MSURF_CHUNK_UNROLL;  // phase-1 chunk-cull loop
 #ifndef MSURF_STAGE_THREADS
 #define MSURF_STAGE_THREADS 64
 #endif
@@ -71,6 +67,9 @@ constexpr int kWarps = kThreads / 32;
 #endif
 #ifndef MSURF_KUNROLL
 #define MSURF_KUNROLL 8
+#endif
+#ifndef MSURF_TILE_CULL
+#define MSURF_TILE_CULL 1  // tilt mode: tile-level chunk pre-cull before phase 1 (see kTileCull)
 #endif
 constexpr int kKUnroll = MSURF_KUNROLL;
 
@@ -608,6 +607,88 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
     zc_tw = (zc_jmax >> 5) + 1;
   }
 
+  // ---------------- tile-level chunk pre-cull (tilt mode, not in the DIAG=1
+  // counting variant): every chunk's window / stock-height / surface-cap test
+  // once per tile, at the tile's mid angle and feed position, widened by the
+  // largest motion any step of the tile can make — rotation: the chunk centre
+  // moves <= (|xc| + |yc|) |omega| half_t; feed: |v_f| half_t; vibration:
+  // |amp| — plus the float-sincos error and fp32 margins five times the
+  // per-step ones, so the tile mask is a superset of every step's mask (caps
+  // read earlier are higher ones). Phase 1 then tests only the tile's chunks,
+  // and a tile whose mask is empty skips its rows, double-double sincos
+  // included. Ball-end raster tiles are mostly empty: a tooth over the stock
+  // top or over an already cut region cuts nothing for 64 steps.
+  constexpr bool kTileCull = MSURF_TILE_CULL && DIAG != 1 && MODE == MSURF_MODE_EXT_TILT;
+  uint64_t* tmask = mslot + kTileSteps * mask_words;  // [W] chunks live somewhere in the tile
+  bool tc_on = false;
+  if constexpr (kTileCull) {
+    tc_on = !J.trig_table && !J.traj;
+    if (tc_on) {
+      const long long s0 = J.step_lo + (long long)st * kTileSteps;
+      const long long s1 = min(s0 + (long long)kTileSteps, (long long)J.step_hi) - 1;
+      const double half_t = 0.5 * (double)(s1 - s0) * J.dt;
+      const double tm = J.t_start + (0.5 * (double)(s0 + s1)) * J.dt;
+      const double th = J.tooth_base[tooth] - J.omega * tm;
+      const double kd = rint(th * MSURF_TWO_OVER_PI);
+      const double r = __fma_rn(-kd, MSURF_PIO2_2, __fma_rn(-kd, MSURF_PIO2_1, th));
+      float sf, cf;
+      __sincosf((float)r, &sf, &cf);
+      const int quad = ((int)(long long)kd) & 3;
+      float ca = cf, sa = sf;
+      if (quad == 1) { ca = -sf; sa = cf; }
+      else if (quad == 2) { ca = -cf; sa = -sf; }
+      else if (quad == 3) { ca = sf; sa = -cf; }
+      const double wxc = J.x_min + 0.5 * (double)J.m * dd, wxh = 0.5 * (double)J.m * dd + 1.5 * dd;
+      const double wyc = J.y_min + 0.5 * (double)(J.j_lo + J.j_hi) * dd;
+      const double wyh = 0.5 * (double)(J.j_hi - J.j_lo) * dd + 1.5 * dd;
+      const float oxm = (float)(J.pass_x0[pass] - wxc);
+      const float oym = (float)(J.y0 + J.feed_speed * tm - wyc);
+      const float rot = (float)(fabs(J.omega) * half_t);               // radians
+      const float vib = (float)(1.001 * fabs(J.vib_amp));             // mm, x only
+      const float feed = (float)(1.001 * fabs(J.feed_speed) * half_t);  // mm, y only
+      const float mgx = 2e-5f * (rt_f + fabsf(oxm) + vib) + 1e-5f;
+      const float mgy = 2e-5f * (rt_f + fabsf(oym) + feed) + 1e-5f;
+      const float hx = (float)wxh + mgx + vib, hy = (float)wyh + mgy + feed;
+      const float tcc = (float)J.tilt_c, tsz = (float)J.tilt_s;
+      unsigned* tm32 = reinterpret_cast<unsigned*>(tmask);
+      for (int qb = warp * 32; qb < mask_words * 64; qb += kSweepThreads) {
+        const int q = qb + lane;
+        bool hit = false;
+        if (q < nchunk) {
+          const float4 a = __ldg(cf4 + 2 * q);
+          const float4 bz = __ldg(cf4 + 2 * q + 1);  // yz, Rt, zfloor, z margin
+          // centre motion over the tile + sincos error (<= 1e-6 rc) + slack
+          const float mv = fmaf(1.01f * rot + 1e-6f, fabsf(a.x) + fabsf(a.y), 1e-4f);
+          const float uc = fmaf(ca, a.x, sa * a.y);
+          const float vc = fmaf(ca, a.y, -(sa * a.x));
+          const float yc = fmaf(tcc, vc, bz.x) + oym;
+          hit = (fabsf(uc + oxm) <= hx + a.z + mv) & (fabsf(yc) <= hy + a.w + mv);
+          const float zlow = fmaf(tsz, vc, bz.z) - fabsf(tsz) * mv - 1e-5f;
+          hit &= zlow <= bz.w;
+          if (zc_on && hit) {
+            const float ci = fmaf(uc + oxm, zc_k, zc_bi), cj = fmaf(yc, zc_k, zc_bj);
+            const float ri = fmaf(a.z + mgx + mv + vib, zc_k, 2.5f), rj = fmaf(a.w + mgy + mv + feed, zc_k, 2.5f);
+            const int i0 = max(0, __float2int_rd(ci - ri)) >> 5, i1 = min(zc_imax, __float2int_rd(ci + ri)) >> 5;
+            const int j0 = max(0, __float2int_rd(cj - rj)) >> 5, j1 = min(zc_jmax, __float2int_rd(cj + rj)) >> 5;
+            if ((i1 - i0) <= 5 && (j1 - j0) <= 5) {  // larger boxes: keep the chunk (no lookup)
+              float cap = -INFINITY;  // empty range: no in-grid cell at all
+              for (int ti = i0; ti <= i1; ++ti)
+                for (int tj = j0; tj <= j1; ++tj) cap = fmaxf(cap, __ldca(J.zcap + ti * zc_tw + tj));
+              hit = zlow <= cap + bz.w;
+            }
+          }
+        }
+        tm32[q >> 5] = __ballot_sync(0xffffffffu, hit);  // each 32-chunk block written by one warp
+      }
+      if constexpr (kSweepWarps == 1) __syncwarp(); else __syncthreads();
+      unsigned long long anyw = 0ull;
+      for (int w = 0; w < mask_words; ++w) anyw |= tmask[w];
+      if (anyw == 0ull) {  // uniform: no step of this tile can deposit
+        if constexpr (ONE) return; else goto tile_done;
+      }
+    }
+  }
+
   // ---------------- phase 1: one thread per time step (kSubSteps rounds of
   // kSweepThreads steps), live steps appended in time order
   int n_live = 0;
@@ -737,8 +818,15 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
             unsigned kept = 0;
             unsigned long long bits = 0ull;
             bool last_hit = false;
-#pragma unroll kChunkUnroll
-            for (int q = 0; q < nchunk; ++q) {
+            // chunks to test: the tile mask's (tile pre-cull on) or all of them;
+            // walked word by word, bit by bit (warp-uniform: one tile mask)
+            for (int w = 0; w < mask_words; ++w) {
+            const int rem = nchunk - 64 * w;
+            unsigned long long todo = rem >= 64 ? ~0ull : ((1ull << rem) - 1ull);
+            if (tc_on) todo &= tmask[w];
+            while (todo) {
+              const int q = 64 * w + __ffsll((long long)todo) - 1;
+              todo &= todo - 1ull;
               const float4 a = __ldg(cf4 + 2 * q);
               const float4 bz = __ldg(cf4 + 2 * q + 1);  // yz, Rt, zfloor, 0
               const float uc = fmaf(cf, a.x, sf * a.y);
@@ -783,12 +871,11 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
               }
               // the step's chunk mask in a register, stored once per 64 chunks
               bits |= (unsigned long long)hit << (q & 63);
-              if ((q & 63) == 63 || q == nchunk - 1) {
-                my_mask[q >> 6] = bits;
-                kept += 32u * (unsigned)__popcll(bits);
-                bits = 0ull;
-              }
-              last_hit = hit;
+              if (q == nchunk - 1) last_hit = hit;
+            }
+            my_mask[w] = bits;
+            kept += 32u * (unsigned)__popcll(bits);
+            bits = 0ull;
             }
             if (last_hit) kept -= (unsigned)(32 * nchunk - npts);  // the last chunk is partial
             any = kept != 0;
@@ -1906,9 +1993,10 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// smem of one sweep CTA: transforms + masks by thread + masks by slot
+// smem of one sweep CTA: transforms + masks by thread + masks by slot + the
+// tile mask of the tile pre-cull
 inline size_t sweep_smem(int tile, int mask_words) {
-  return (size_t)tile * 8 * sizeof(double) + (size_t)2 * tile * mask_words * sizeof(uint64_t);
+  return (size_t)tile * 8 * sizeof(double) + (size_t)(2 * tile + 1) * mask_words * sizeof(uint64_t);
 }
 
 template <int MODE, int DIAG, bool ONE, int TILE, int NTHR, bool STAGE = false>

@@ -69,7 +69,10 @@ constexpr int kWarps = kThreads / 32;
 #define MSURF_KUNROLL 8
 #endif
 #ifndef MSURF_TILE_CULL
-#define MSURF_TILE_CULL 1  // tilt mode: tile-level chunk pre-cull before phase 1 (see kTileCull)
+#define MSURF_TILE_CULL 1  // tile-level chunk pre-cull before phase 1 (see kTileCull)
+#endif
+#ifndef MSURF_TILE_CULL_ALL
+#define MSURF_TILE_CULL_ALL 1  // ... also for by-value REF / EXT launches (A/B knob)
 #endif
 constexpr int kKUnroll = MSURF_KUNROLL;
 
@@ -123,13 +126,35 @@ __device__ __noinline__ int cell_index_exact(double w, double lo, double dd) {
   return __double2int_rz(floor(tq));  // saturates far outside; range checks reject
 }
 
+// Z-map key address of node (i, jj) (jj relative to the job's j_lo), row
+// major. (4x4-node blocks, one 128-B line each, were measured: config 4's
+// RED.MIN touch 27.4 -> 19.1 lines per instruction but its sweep only gains
+// 2 %, config 3's lane = point REDs touch more lines.)
+template <int MODE>
+__device__ __forceinline__ int key_idx(int i, int jj, int ldk) {
+  return i * ldk + jj;
+}
+
 // Fire-and-forget global atomic min (RED.E.MIN.64): the explicit .global
 // form avoids the generic-address shared-memory fallback atomicMin compiles to.
+// No "memory" clobber: nothing in a sweep reads the keys back (later kernels
+// do, after the launch boundary), and a clobber would pin every later
+// shared-memory read of the point loop (the next points' records) behind the
+// RED, serialising the unrolled iterations. MSURF_RED_CLOBBER=1 restores it
+// (A/B only).
+#ifndef MSURF_RED_CLOBBER
+#define MSURF_RED_CLOBBER 0
+#endif
+#if MSURF_RED_CLOBBER
+#define MSURF_RED_MEM : "memory"
+#else
+#define MSURF_RED_MEM
+#endif
 __device__ __forceinline__ void red_min_u64(unsigned long long* p, unsigned long long v) {
 #ifdef MSURF_NO_RED  // timing experiment only: the RED replaced by a never-taken store
   if (v == 1ull) *p = v;
 #else
-  asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) MSURF_RED_MEM);
 #endif
 }
 
@@ -142,8 +167,7 @@ __device__ __forceinline__ void red_min_u64_if(unsigned long long* p, unsigned l
 #endif
   asm volatile(
       "{ .reg .pred q; setp.ne.u32 q, %2, 0; @q red.relaxed.gpu.global.min.u64 [%0], %1; }" ::"l"(p),
-      "l"(v), "r"((unsigned)pred)
-      : "memory");
+      "l"(v), "r"((unsigned)pred) MSURF_RED_MEM);
 }
 
 __device__ __forceinline__ unsigned warp_sum_u(unsigned v) {
@@ -435,8 +459,8 @@ __device__ __forceinline__ void pair_unit(const msurf_job& J, const double4* __r
     anynear |= (ea.near & on_a) | (eb.near & on_b);
     const bool in_a = ((unsigned)ia <= span_i) & ((unsigned)ja <= span_j) & !ea.near;
     const bool in_b = ((unsigned)ib <= span_i) & ((unsigned)jb <= span_j) & !eb.near;
-    const int idx_a = in_a ? ia * ldk + ja : -1;
-    const int idx_b = in_b ? ib * ldk + jb : -1;
+    const int idx_a = in_a ? key_idx<MODE>(ia, ja, ldk) : -1;
+    const int idx_b = in_b ? key_idx<MODE>(ib, jb, ldk) : -1;
     const int idx_bp = __shfl_up_sync(0xffffffffu, idx_b, 1);  // A's predecessor (lane 0: own B)
     bool dep_a, dep_b;
     if (MODE == MSURF_MODE_EXT_TILT) {
@@ -477,7 +501,7 @@ __device__ __forceinline__ void pair_unit(const msurf_job& J, const double4* __r
         const int ie = cell_index_exact(e.xw, J.x_min, dd);
         const int je = cell_index_exact(e.yw, J.y_min, dd) - j_lo;
         const bool in = ((unsigned)ie <= span_i) & ((unsigned)je <= span_j);
-        if (in) red_min_u64(keys + (ie * ldk + je), (unsigned long long)e.key);
+        if (in) red_min_u64(keys + key_idx<MODE>(ie, je, ldk), (unsigned long long)e.key);
         if (DIAG) {
           n_dep += in;
           n_atom += in;
@@ -618,7 +642,10 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
   // and a tile whose mask is empty skips its rows, double-double sincos
   // included. Ball-end raster tiles are mostly empty: a tooth over the stock
   // top or over an already cut region cuts nothing for 64 steps.
-  constexpr bool kTileCull = MSURF_TILE_CULL && DIAG != 1 && MODE == MSURF_MODE_EXT_TILT;
+  // by-value surfaces of every mode (a config-4 sub-strip's window leaves most
+  // chunks of a tile dead); the batched small surfaces (config 3) sit under
+  // the whole tool, so there the per-tile pass is pure overhead (measured +4 %)
+  constexpr bool kTileCull = MSURF_TILE_CULL && DIAG != 1 && (MODE == MSURF_MODE_EXT_TILT || (ONE && MSURF_TILE_CULL_ALL));
   uint64_t* tmask = mslot + kTileSteps * mask_words;  // [W] chunks live somewhere in the tile
   bool tc_on = false;
   if constexpr (kTileCull) {
@@ -649,7 +676,9 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
       const float mgx = 2e-5f * (rt_f + fabsf(oxm) + vib) + 1e-5f;
       const float mgy = 2e-5f * (rt_f + fabsf(oym) + feed) + 1e-5f;
       const float hx = (float)wxh + mgx + vib, hy = (float)wyh + mgy + feed;
-      const float tcc = (float)J.tilt_c, tsz = (float)J.tilt_s;
+      // the per-step test's conventions: no tilt terms outside the tilt mode
+      const float tcc = MODE == MSURF_MODE_EXT_TILT ? (float)J.tilt_c : 1.0f;
+      const float tsz = MODE == MSURF_MODE_EXT_TILT ? (float)J.tilt_s : 0.0f;
       unsigned* tm32 = reinterpret_cast<unsigned*>(tmask);
       for (int qb = warp * 32; qb < mask_words * 64; qb += kSweepThreads) {
         const int q = qb + lane;
@@ -1049,8 +1078,8 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
           const int ia2 = e2.hi_x - ibias, ja2 = e2.hi_y - jbias;
           const bool in1 = ((unsigned)ia1 <= span_i) & ((unsigned)ja1 <= span_j) & !e1.near;
           const bool in2 = ((unsigned)ia2 <= span_i) & ((unsigned)ja2 <= span_j) & !e2.near & two;
-          const int idx1 = in1 ? ia1 * ldk + ja1 : -1;
-          const int idx2 = in2 ? ia2 * ldk + ja2 : -1;
+          const int idx1 = in1 ? key_idx<MODE>(ia1, ja1, ldk) : -1;
+          const int idx2 = in2 ? key_idx<MODE>(ia2, ja2, ldk) : -1;
           bool dep1, dep2;
           unsigned long long k1, k2;
           int a1, a2;
@@ -1103,7 +1132,7 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
               const int ie = cell_index_exact(xw, J.x_min, dd);
               const int je = cell_index_exact(yw, J.y_min, dd) - j_lo;
               const bool in = ((unsigned)ie <= span_i) & ((unsigned)je <= span_j);
-              if (in) red_min_u64(keys + (ie * ldk + je), (unsigned long long)e.key);
+              if (in) red_min_u64(keys + key_idx<MODE>(ie, je, ldk), (unsigned long long)e.key);
               if (DIAG) {
                 n_dep += in;
                 n_atom += in;
@@ -1145,20 +1174,34 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
                             cy0, span_i, span_j, jbias, j_lo, ldk, keys, tilt_c, tilt_s, dd, n_dep, n_atom);
     }
   } else {
-    // unit = (group of 32 live steps, chunk q), lane = one step
+    // unit = (group of 32 live steps, chunk q), lane = one step. Only live
+    // units are visited: per group the union of its steps' chunk masks
+    // (warp-uniform), the live units dealt round-robin to the CTA's warps in
+    // (group, chunk) order (a windowed sub-strip leaves most chunks of a step
+    // dead, and testing every (group, chunk) pair cost ~8 % of the issue).
     const int groups = (n_live + 31) >> 5;
     int rt = 0;
     double r[RW];
-    for (; g < groups; next_unit<kSweepWarps>(g, q, nchunk)) {
-      const int slot = g * 32 + lane;
-      if (g != g_loaded) {  // warp-uniform
-        g_loaded = g;
-        rt = slot < n_live ? slot : -1;
+    unsigned u_rank = 0;  // live units seen so far (uniform)
+    for (int gg = 0; gg < groups; ++gg) {
+      const int slot = gg * 32 + lane;
+      const int rtg = slot < n_live ? slot : -1;
+      for (int w = 0; w < mask_words; ++w) {
+      const unsigned long long mw = rtg >= 0 ? mslot[rtg * mask_words + w] : 0ull;
+      unsigned long long live_q = ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(mw >> 32)) << 32) |
+                                  (unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)mw);
+      while (live_q) {
+      const int qb = __ffsll((long long)live_q) - 1;
+      live_q &= live_q - 1ull;
+      if ((u_rank++ % (unsigned)kSweepWarps) != (unsigned)warp) continue;
+      const int q = 64 * w + qb;
+      if (gg != g_loaded) {  // warp-uniform
+        g_loaded = gg;
+        rt = rtg;
 #pragma unroll
         for (int k = 0; k < RW; ++k) r[k] = rt >= 0 ? rowv[slot * 8 + k] : 0.0;
       }
-      const bool on = rt >= 0 && ((mslot[rt * mask_words + (q >> 6)] >> (q & 63)) & 1ull);
-      if (!__any_sync(0xffffffffu, on)) continue;
+      const bool on = (mw >> qb) & 1ull;
       // lanes whose step is not live for this chunk: i index pushed far out of
       // range, so the per-point range test also covers `on`
       const int ibias = on ? kMagicHi : kMagicHi - (1 << 30);
@@ -1202,8 +1245,8 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
         anynear |= (ea.near | (eb.near & (k + 1 < p_end))) & on;
         const bool in_a = ((unsigned)ia <= span_i) & ((unsigned)ja <= span_j) & !ea.near;
         const bool in_b = ((unsigned)ib <= span_i) & ((unsigned)jb <= span_j) & !eb.near;
-        const int idx_a = in_a ? ia * ldk + ja : -1;
-        const int idx_b = in_b ? ib * ldk + jb : -1;
+        const int idx_a = in_a ? key_idx<MODE>(ia, ja, ldk) : -1;
+        const int idx_b = in_b ? key_idx<MODE>(ib, jb, ldk) : -1;
         bool dep_a, dep_b;
         dedupe<MODE>(lane, idx_a, in_a, ea.zh, dep_a);
         dedupe<MODE>(lane, idx_b, in_b, eb.zh, dep_b);
@@ -1228,16 +1271,16 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
           const int ie = cell_index_exact(e.xw, J.x_min, dd);
           const int je = cell_index_exact(e.yw, J.y_min, dd) - j_lo;
           const bool in = on & ((unsigned)ie <= span_i) & ((unsigned)je <= span_j);
-          if (in) red_min_u64(keys + (ie * ldk + je), (unsigned long long)e.key);
+          if (in) red_min_u64(keys + key_idx<MODE>(ie, je, ldk), (unsigned long long)e.key);
           if (DIAG) {
             n_dep += in;
             n_atom += in;
           }
         }
       }
-    }
-
-
+      }  // live chunks of the word
+      }  // mask words
+    }  // groups
   }
 
   // counters: one atomic per warp

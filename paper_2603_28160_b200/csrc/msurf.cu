@@ -511,6 +511,82 @@ __device__ __forceinline__ void pair_unit(const msurf_job& J, const double4* __r
   }
 }
 
+// One phase-2 unit of the lane = step loop (constant-z' modes and the tilt
+// mode's unpaired form): the up-to-32 points of chunk q, already staged in
+// ptstage, under the lane's step transform r (live slot rt; `on`: the chunk
+// is live at the lane's step). Deposits through the time-neighbour filter;
+// near-boundary points re-located exactly afterwards.
+template <int MODE, int DIAG, int RW>
+__device__ __forceinline__ void step_unit(const msurf_job& J, const double4* ptstage, const double (&r)[RW], int rt,
+                                          bool on, int q, int npts, int lane, double inv, double cx0, double cy0,
+                                          unsigned span_i, unsigned span_j, int jbias, int j_lo, int ldk,
+                                          unsigned long long* __restrict__ keys, double tilt_c, double tilt_s,
+                                          double dd, const double* rowv, unsigned& n_dep, unsigned& n_atom) {
+  // lanes whose step is not live for this chunk: i index pushed far out of
+  // range, so the per-point range test also covers `on`
+  const int ibias = on ? kMagicHi : kMagicHi - (1 << 30);
+  const int p_end = min(32, npts - q * 32);
+        // Near-boundary points (probability ~1e-9 each) are not resolved inline:
+        // they are flagged, kept out of the neighbour comparisons (treated as
+        // outside), and deposited after the chunk with the exact reference index
+        // — an extra deposit is always safe, a skipped one never is.
+        bool anynear = false;
+        // Two points per iteration with no divergent branch between their
+        // evaluations (the compiler interleaves the two dependent fp64 chains).
+        // Near-boundary points (probability ~1e-9 each) are not resolved inline:
+        // they are flagged, kept out of the neighbour comparisons (treated as
+        // outside), and deposited after the chunk with the exact reference index
+        // — an extra deposit is always safe, a skipped one never is.
+        // 8 iterations (16 points) per unrolled body: the scheduler can overlap
+        // one pair's shuffles/REDs with the next pair's fp64 chain (measured:
+        // 1.11 -> 1.07 ms on config 2; 16 iterations: slower, i-cache)
+  #pragma unroll kKUnroll
+        for (int k = 0; k < p_end; k += 2) {
+          const int ibias_b = (k + 1 < p_end) ? ibias : kMagicHi - (1 << 30);
+          PointEval ea = eval_point<MODE>(ptstage[k], r, inv, cx0, cy0, tilt_c, tilt_s);
+          PointEval eb = eval_point<MODE>(ptstage[k + 1], r, inv, cx0, cy0, tilt_c, tilt_s);
+          const int ia = ea.hi_x - ibias, ja = ea.hi_y - jbias;
+          const int ib = eb.hi_x - ibias_b, jb = eb.hi_y - jbias;
+          // near flags of live points (the fast index may be off by one there, so
+          // the range test must not filter them)
+          anynear |= (ea.near | (eb.near & (k + 1 < p_end))) & on;
+          const bool in_a = ((unsigned)ia <= span_i) & ((unsigned)ja <= span_j) & !ea.near;
+          const bool in_b = ((unsigned)ib <= span_i) & ((unsigned)jb <= span_j) & !eb.near;
+          const int idx_a = in_a ? key_idx<MODE>(ia, ja, ldk) : -1;
+          const int idx_b = in_b ? key_idx<MODE>(ib, jb, ldk) : -1;
+          bool dep_a, dep_b;
+          dedupe<MODE>(lane, idx_a, in_a, ea.zh, dep_a);
+          dedupe<MODE>(lane, idx_b, in_b, eb.zh, dep_b);
+          if (DIAG) {
+            n_dep += (unsigned)in_a + (unsigned)in_b;
+            n_atom += (unsigned)dep_a + (unsigned)dep_b;
+          }
+          red_min_u64_if(keys + idx_a, (unsigned long long)ea.key, dep_a);
+          red_min_u64_if(keys + idx_b, (unsigned long long)eb.key, dep_b);
+          if (DIAG == 2) {
+            trace_red(keys + idx_a, dep_a, lane);
+            trace_red(keys + idx_b, dep_b, lane);
+          }
+        }
+        if (__builtin_expect(__any_sync(0xffffffffu, anynear), 0)) {
+          for (int k = 0; k < p_end; ++k) {
+            const double4 pt = ptstage[k];
+            PointEval e = eval_point<MODE>(pt, r, inv, cx0, cy0, tilt_c, tilt_s);
+            if (!(e.near & on)) continue;
+            if (MODE != MSURF_MODE_REF)
+              exact_xy<MODE>(pt, r[0], r[1], rowv[rt * 8 + 4], rowv[rt * 8 + 5], tilt_c, e.xw, e.yw);
+            const int ie = cell_index_exact(e.xw, J.x_min, dd);
+            const int je = cell_index_exact(e.yw, J.y_min, dd) - j_lo;
+            const bool in = on & ((unsigned)ie <= span_i) & ((unsigned)je <= span_j);
+            if (in) red_min_u64(keys + key_idx<MODE>(ie, je, ldk), (unsigned long long)e.key);
+            if (DIAG) {
+              n_dep += in;
+              n_atom += in;
+            }
+          }
+        }
+}
+
 // staging of a capped (pass, tooth) launch (msurf_job.stage; EXT_TILT, 64-step
 // tiles): header [tiles, units, cursor], then per live tile a record
 // {n_live; rows[64][6] = (c, s, cxp, cyp, x offset, feed position);
@@ -1179,9 +1255,9 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
     // (warp-uniform), the live units dealt round-robin to the CTA's warps in
     // (group, chunk) order (a windowed sub-strip leaves most chunks of a step
     // dead, and testing every (group, chunk) pair cost ~8 % of the issue).
-    const int groups = (n_live + 31) >> 5;
     int rt = 0;
     double r[RW];
+    const int groups = (n_live + 31) >> 5;
     unsigned u_rank = 0;  // live units seen so far (uniform)
     for (int gg = 0; gg < groups; ++gg) {
       const int slot = gg * 32 + lane;
@@ -1202,9 +1278,6 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
         for (int k = 0; k < RW; ++k) r[k] = rt >= 0 ? rowv[slot * 8 + k] : 0.0;
       }
       const bool on = (mw >> qb) & 1ull;
-      // lanes whose step is not live for this chunk: i index pushed far out of
-      // range, so the per-point range test also covers `on`
-      const int ibias = on ? kMagicHi : kMagicHi - (1 << 30);
       const int p_end = min(32, npts - q * 32);
       // stage the chunk's 32 point records (1 KB, coalesced) for broadcast
       // reads; slots past the chunk's end hold zeros (finite, masked below)
@@ -1219,65 +1292,8 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
         ptstage[warp][lane] = v;
       }
       __syncwarp();
-      // Near-boundary points (probability ~1e-9 each) are not resolved inline:
-      // they are flagged, kept out of the neighbour comparisons (treated as
-      // outside), and deposited after the chunk with the exact reference index
-      // — an extra deposit is always safe, a skipped one never is.
-      bool anynear = false;
-      // Two points per iteration with no divergent branch between their
-      // evaluations (the compiler interleaves the two dependent fp64 chains).
-      // Near-boundary points (probability ~1e-9 each) are not resolved inline:
-      // they are flagged, kept out of the neighbour comparisons (treated as
-      // outside), and deposited after the chunk with the exact reference index
-      // — an extra deposit is always safe, a skipped one never is.
-      // 8 iterations (16 points) per unrolled body: the scheduler can overlap
-      // one pair's shuffles/REDs with the next pair's fp64 chain (measured:
-      // 1.11 -> 1.07 ms on config 2; 16 iterations: slower, i-cache)
-#pragma unroll kKUnroll
-      for (int k = 0; k < p_end; k += 2) {
-        const int ibias_b = (k + 1 < p_end) ? ibias : kMagicHi - (1 << 30);
-        PointEval ea = eval_point<MODE>(ptstage[warp][k], r, inv, cx0, cy0, tilt_c, tilt_s);
-        PointEval eb = eval_point<MODE>(ptstage[warp][k + 1], r, inv, cx0, cy0, tilt_c, tilt_s);
-        const int ia = ea.hi_x - ibias, ja = ea.hi_y - jbias;
-        const int ib = eb.hi_x - ibias_b, jb = eb.hi_y - jbias;
-        // near flags of live points (the fast index may be off by one there, so
-        // the range test must not filter them)
-        anynear |= (ea.near | (eb.near & (k + 1 < p_end))) & on;
-        const bool in_a = ((unsigned)ia <= span_i) & ((unsigned)ja <= span_j) & !ea.near;
-        const bool in_b = ((unsigned)ib <= span_i) & ((unsigned)jb <= span_j) & !eb.near;
-        const int idx_a = in_a ? key_idx<MODE>(ia, ja, ldk) : -1;
-        const int idx_b = in_b ? key_idx<MODE>(ib, jb, ldk) : -1;
-        bool dep_a, dep_b;
-        dedupe<MODE>(lane, idx_a, in_a, ea.zh, dep_a);
-        dedupe<MODE>(lane, idx_b, in_b, eb.zh, dep_b);
-        if (DIAG) {
-          n_dep += (unsigned)in_a + (unsigned)in_b;
-          n_atom += (unsigned)dep_a + (unsigned)dep_b;
-        }
-        red_min_u64_if(keys + idx_a, (unsigned long long)ea.key, dep_a);
-        red_min_u64_if(keys + idx_b, (unsigned long long)eb.key, dep_b);
-        if (DIAG == 2) {
-          trace_red(keys + idx_a, dep_a, lane);
-          trace_red(keys + idx_b, dep_b, lane);
-        }
-      }
-      if (__builtin_expect(__any_sync(0xffffffffu, anynear), 0)) {
-        for (int k = 0; k < p_end; ++k) {
-          const double4 pt = ptstage[warp][k];
-          PointEval e = eval_point<MODE>(pt, r, inv, cx0, cy0, tilt_c, tilt_s);
-          if (!(e.near & on)) continue;
-          if (MODE != MSURF_MODE_REF)
-            exact_xy<MODE>(pt, r[0], r[1], rowv[rt * 8 + 4], rowv[rt * 8 + 5], tilt_c, e.xw, e.yw);
-          const int ie = cell_index_exact(e.xw, J.x_min, dd);
-          const int je = cell_index_exact(e.yw, J.y_min, dd) - j_lo;
-          const bool in = on & ((unsigned)ie <= span_i) & ((unsigned)je <= span_j);
-          if (in) red_min_u64(keys + key_idx<MODE>(ie, je, ldk), (unsigned long long)e.key);
-          if (DIAG) {
-            n_dep += in;
-            n_atom += in;
-          }
-        }
-      }
+      step_unit<MODE, DIAG, RW>(J, ptstage[warp], r, rt, on, q, npts, lane, inv, cx0, cy0, span_i, span_j, jbias,
+                                j_lo, ldk, keys, tilt_c, tilt_s, dd, rowv, n_dep, n_atom);
       }  // live chunks of the word
       }  // mask words
     }  // groups

@@ -53,6 +53,9 @@ ZCAP_WIDE = __import__("os").environ.get("MSURF_ZCAP_WIDE", "0") != "0"
 # 14.1 / 14.2 / 17.5 ms)
 ZCAP_L2_TILE_BYTES = int(float(__import__("os").environ.get("MSURF_ZCAP_L2_TILE_MB", "72")) * (1 << 20))
 ZCAP_MIN_JOBS = int(__import__("os").environ.get("MSURF_ZCAP_MIN_JOBS", "1"))  # capped jobs swept side by side
+# sub-strips a capped surface is cut into at least (several jobs side by side
+# keep more of the GPU busy than one job's (pass, tooth) chain)
+ZCAP_MIN_STRIPS = int(__import__("os").environ.get("MSURF_ZCAP_MIN_STRIPS", "1"))
 # overlapping (pass, tooth) launches per capped job. Measured on config 5 (3
 # sub-strip jobs; sweep without caps 37.3 ms): single-kernel launches depth 1 /
 # 2 / 3 / 4 -> 27.1 / 20.5 / 20.3 / 20.9 ms; staged two-kernel launches depth
@@ -227,9 +230,12 @@ class SweepBatch:
             # their keys live strip by strip (contiguous slab per sweep job) and the
             # decode writes the row-major heights (msurf_decode_strips)
             budget = l2_tile_bytes
-            if ZCAP and s.plan.mode == MODE_EXT_TILT and s.plan.passes * s.plan.teeth > 1:
+            capped = ZCAP and s.plan.mode == MODE_EXT_TILT and s.plan.passes * s.plan.teeth > 1
+            if capped:
                 budget = max(budget, ZCAP_L2_TILE_BYTES)  # capped surfaces: fewer, larger slabs
             k = 1 if s.plan.record else max(1, min(w, -(-rows * w * 8 // budget)))
+            if capped and not s.plan.record:
+                k = max(k, min(ZCAP_MIN_STRIPS, max(1, w // 64)))
             s.n_strips = k
             s.col0 = [(w * q) // k for q in range(k + 1)]
             if k > 1:

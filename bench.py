@@ -306,15 +306,30 @@ def red_lines(batch):
     return batch.red_lines()
 
 
+def mb_shape_sectors(L):
+    """32-byte sectors one warp RED.MIN of msurf_microbench(32 + L) touches:
+    lane l updates key (l // L) of line (l % L), lanes with l // L >= 16 idle
+    (mb_atomic_lines_kernel)."""
+    per_line = [0] * L
+    for lane in range(32):
+        if lane // L < 16:
+            per_line[lane % L] += 1
+    return sum(-(-k // 4) for k in per_line)
+
+
 def roofline(flops, atomics, sweep_ms, lines, kernel_name):
     """The north star's roofline = the slower of fp64 issue and atomic
     traffic, each as the time the path's minimum work needs at the measured
     peak rate of its unit:
     * t_fp64 = algorithmic fp64 ops / the DADD/DMUL issue rate (microbench 0);
-    * t_red = the 128-byte line updates the sweep's RED.MIN stream performs
-      (its traced warp REDs, each counted by the distinct lines it touches)
-      / the peak L2 atomic line-update rate (the best RED.MIN shape of
-      microbench 32+L, lines/s).
+    * t_red = the 32-byte sector updates the sweep's RED.MIN stream performs
+      (its traced warp REDs, each counted by the distinct sectors it touches)
+      / the peak L2 atomic sector-update rate (the best RED.MIN shape of
+      microbench 32+L, sectors/s). Sectors, not lines: across the measured
+      shapes the L2 atomic throughput is nearly constant per sector update
+      (1.2-1.9e11 /s) while the line-update rate spans 4x, and a 4x4-node
+      blocked Z-map that cut config 4's lines per RED by 30 % left its sweep
+      time unchanged.
     ``bound`` is the larger term and ``frac`` = that term / the measured
     sweep time. The shape-priced RED time (each warp RED at the measured rate
     for its line count, random placement) is reported beside it."""
@@ -331,9 +346,20 @@ def roofline(flops, atomics, sweep_ms, lines, kernel_name):
         line_updates = scale * sum(L * hist[L] for L in range(33))
         peak_L = max(range(1, 33), key=lambda L: pk[32 + L] * L)
         peak_lines = pk[32 + peak_L] * peak_L
-        t_red = line_updates / peak_lines
+        t_lines = line_updates / peak_lines
+        hs = lines.get("hist_sectors") or [0] * 33
+        sector_updates = scale * sum(S * hs[S] for S in range(33))
+        peak_S = max(range(1, 33), key=lambda L: pk[32 + L] * mb_shape_sectors(L))
+        peak_sectors = pk[32 + peak_S] * mb_shape_sectors(peak_S)
+        t_red = sector_updates / peak_sectors
         t_shape = scale * sum(hist[L] / pk[32 + L] for L in range(1, 33))
-        terms.update({"t_red_ms": t_red * 1e3, "frac_red": t_red / t, "line_updates": line_updates,
+        terms.update({"t_red_ms": t_red * 1e3, "frac_red": t_red / t, "sector_updates": sector_updates,
+                      "peak_sector_updates_per_s": peak_sectors, "peak_shape_lines_for_sectors": peak_S,
+                      "achieved_sector_updates_per_s": sector_updates / t,
+                      "red_sectors_hist": hs,
+                      "red_sector_rate_by_lines_per_s": {L: pk[32 + L] * mb_shape_sectors(L)
+                                                         for L in (1, 2, 4, 8, 16, 32)},
+                      "t_red_lines_ms": t_lines * 1e3, "line_updates": line_updates,
                       "peak_line_updates_per_s": peak_lines, "peak_shape_lines": peak_L,
                       "achieved_line_updates_per_s": line_updates / t,
                       "t_red_shape_priced_ms": t_shape * 1e3,
@@ -343,18 +369,18 @@ def roofline(flops, atomics, sweep_ms, lines, kernel_name):
                       "red_lines_hist": hist,
                       "red_instr_rate_by_lines_per_s": {L: pk[32 + L] for L in (1, 2, 4, 8, 16, 32)},
                       "red_note": "every warp-wide RED.MIN of one sweep traced (MSURF_SWEEP_TRACE) and counted "
-                                  "by the distinct 128-B lines it updates"})
+                                  "by the distinct 32-B sectors (t_red) and 128-B lines (t_red_lines) it updates"})
     bound = "fp64" if t_red is None or t_fp64 >= t_red else "atomic"
     if bound == "fp64":
         out = {"bound": "fp64", "achieved": flops / t / 1e12, "peak": pk[0] / 1e12, "unit": "TFLOP/s",
                "frac": t_fp64 / t}
     else:
-        out = {"bound": "atomic", "achieved": terms["achieved_line_updates_per_s"] / 1e9,
-               "peak": terms["peak_line_updates_per_s"] / 1e9, "unit": "G line-updates/s (L2 RED.MIN)",
+        out = {"bound": "atomic", "achieved": terms["achieved_sector_updates_per_s"] / 1e9,
+               "peak": terms["peak_sector_updates_per_s"] / 1e9, "unit": "G sector-updates/s (L2 RED.MIN)",
                "frac": t_red / t}
     out.update({"kernel": kernel_name, "sweep_ms": sweep_ms, "terms": terms,
                 "peak_source": "measured in this run: fp64 = msurf_microbench(0) non-FMA DADD/DMUL issue rate "
-                               "(MEASURED_PEAKS.json has no FP64 entry); atomic = best L2 RED.MIN line-update rate "
+                               "(MEASURED_PEAKS.json has no FP64 entry); atomic = best L2 RED.MIN sector-update rate "
                                "over msurf_microbench(32+L) shapes"})
     return out
 

@@ -324,6 +324,14 @@ int msurf_microbench(int32_t which, double* result);
  * stream at the L2 atomic throughput. */
 int msurf_trace_arm(uint32_t* trace, int64_t cap_records, unsigned long long* counters, const uint64_t* base);
 int msurf_red_lines(const uint32_t* trace, int64_t n_records, unsigned long long* hist, void* stream);
+/* msurf_red_sectors: the same line histogram plus hist_sectors[S] += records
+ * touching S distinct 32-byte sectors (both 33 device u64, caller-zeroed).
+ * The L2 atomic units' throughput is close to constant per sector update
+ * across warp RED shapes (msurf_microbench(32 + L): 1.2-1.9e11 sectors/s
+ * while the line-update rate spans 4x), so the sector count of the sweep's
+ * own RED stream over the best measured sector rate is its atomic roof. */
+int msurf_red_sectors(const uint32_t* trace, int64_t n_records, unsigned long long* hist_lines,
+                      unsigned long long* hist_sectors, void* stream);
 
 /* Small-result readback without the copy engines: msurf_host_alloc returns
  * page-locked host memory mapped into the device address space (NULL on

@@ -111,6 +111,7 @@ EXPORTS = {
     "msurf_microbench": (ctypes.c_int, [c_int32, ctypes.POINTER(c_double)]),
     "msurf_trace_arm": (ctypes.c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
     "msurf_red_lines": (ctypes.c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
+    "msurf_red_sectors": (ctypes.c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "msurf_host_alloc": (c_void_p, [c_int64]),
     "msurf_host_free": (ctypes.c_int, [c_void_p]),
     "msurf_readback": (ctypes.c_int, [c_void_p, c_void_p, c_int64, c_void_p]),

@@ -1982,9 +1982,10 @@ __global__ void mb_atomic_kernel(unsigned long long* buf, long long mask, int it
 // distinct 128-byte lines per traced RED record -> hist[0..32] (one warp
 // per record, grid-stride)
 __global__ void __launch_bounds__(256)
-    red_lines_kernel(const unsigned* __restrict__ trace, long long n_rec, unsigned long long* hist) {
-  __shared__ unsigned long long h[33];
-  for (int i = threadIdx.x; i < 33; i += blockDim.x) h[i] = 0;
+    red_lines_kernel(const unsigned* __restrict__ trace, long long n_rec, unsigned long long* hist,
+                     unsigned long long* hist_sectors) {
+  __shared__ unsigned long long h[33], hs[33];
+  for (int i = threadIdx.x; i < 33; i += blockDim.x) h[i] = hs[i] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -1996,11 +1997,20 @@ __global__ void __launch_bounds__(256)
     // a lane opens a line if no lower active lane holds the same line
     const bool first = on && ((same & act & ((1u << lane) - 1u)) == 0u);
     const int lines = __popc(__ballot_sync(0xffffffffu, first));
-    if (lane == 0) atomicAdd(&h[lines], 1ull);
+    // the same for the 32-byte sectors (four keys each)
+    const unsigned same_s = __match_any_sync(0xffffffffu, on ? (off >> 2) : 0xffffffffu);
+    const bool first_s = on && ((same_s & act & ((1u << lane) - 1u)) == 0u);
+    const int sectors = __popc(__ballot_sync(0xffffffffu, first_s));
+    if (lane == 0) {
+      if (hist) atomicAdd(&h[lines], 1ull);
+      if (hist_sectors) atomicAdd(&hs[sectors], 1ull);
+    }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 33; i += blockDim.x)
-    if (h[i]) atomicAdd(hist + i, h[i]);
+  for (int i = threadIdx.x; i < 33; i += blockDim.x) {
+    if (hist && h[i]) atomicAdd(hist + i, h[i]);
+    if (hist_sectors && hs[i]) atomicAdd(hist_sectors + i, hs[i]);
+  }
 }
 
 // the node rows one (pass, tooth) launch can have deposited into: x = fma(c, x_t,
@@ -2255,7 +2265,19 @@ int msurf_red_lines(const uint32_t* trace, int64_t n_records, unsigned long long
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  red_lines_kernel<<<(unsigned)sms * 8, 256, 0, (cudaStream_t)stream>>>(trace, n_records, hist);
+  red_lines_kernel<<<(unsigned)sms * 8, 256, 0, (cudaStream_t)stream>>>(trace, n_records, hist, nullptr);
+  return check_launch("red_lines_kernel");
+}
+
+int msurf_red_sectors(const uint32_t* trace, int64_t n_records, unsigned long long* hist_lines,
+                      unsigned long long* hist_sectors, void* stream) {
+  if (n_records < 0 || !hist_lines || !hist_sectors || (n_records > 0 && !trace))
+    return set_err("msurf_red_sectors: bad arguments");
+  if (n_records == 0) return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  red_lines_kernel<<<(unsigned)sms * 8, 256, 0, (cudaStream_t)stream>>>(trace, n_records, hist_lines, hist_sectors);
   return check_launch("red_lines_kernel");
 }
 

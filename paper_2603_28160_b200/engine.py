@@ -565,7 +565,8 @@ class SweepBatch:
         RED.MIN of one sweep of this batch (MSURF_SWEEP_TRACE launch, one
         record of 32 key offsets per warp-wide RED) and histogram the records
         by the number of distinct 128-byte lines each touches
-        (msurf_red_lines). Returns {"hist": [33 counts], "records",
+        (msurf_red_sectors). Returns {"hist": [33 counts], "hist_sectors": [33
+        counts, by distinct 32-byte sectors], "records",
         "records_issued", "lanes" (active lanes = RED.MIN of the production
         sweep, all records), "truncated"}; a truncated trace (above
         ``cap_bytes``) histograms the first records in issue order. None when
@@ -578,7 +579,7 @@ class SweepBatch:
         cap = int(min(cap_bytes, free // 2)) // 128
         trace = torch.empty(max(cap, 1) * 32, dtype=torch.int32, device=self.dev)
         ctr = torch.zeros(2, dtype=torch.int64, device=self.dev)
-        hist = torch.zeros(33, dtype=torch.int64, device=self.dev)
+        hist = torch.zeros(66, dtype=torch.int64, device=self.dev)  # lines [0, 33), sectors [33, 66)
         _native.check(lib.msurf_trace_arm(trace.data_ptr(), cap, ctr.data_ptr(), base.data_ptr()))
         prev, self.diagnostics = self.diagnostics, "trace"
         try:
@@ -588,11 +589,13 @@ class SweepBatch:
         torch.cuda.synchronize(self.dev)
         issued, lanes = (int(v) for v in ctr.cpu())
         n_rec = min(issued, cap)
-        _native.check(lib.msurf_red_lines(trace.data_ptr(), n_rec, hist.data_ptr(), _native.stream_ptr()))
+        _native.check(lib.msurf_red_sectors(trace.data_ptr(), n_rec, hist.data_ptr(), hist.data_ptr() + 33 * 8,
+                                            _native.stream_ptr()))
         h = [int(v) for v in hist.cpu()]
         del trace
         torch.cuda.empty_cache()
-        return {"hist": h, "records": n_rec, "records_issued": issued, "lanes": lanes, "truncated": issued > cap}
+        return {"hist": h[:33], "hist_sectors": h[33:], "records": n_rec, "records_issued": issued, "lanes": lanes,
+                "truncated": issued > cap}
 
     def launch_decode(self, sp: int) -> None:
         """Keys -> fp64 heights in place, machined-cell counts."""

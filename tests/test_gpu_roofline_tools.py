@@ -34,4 +34,8 @@ def test_red_trace_counts_the_sweeps_reds():
     assert 0.97 * atomics <= lines["lanes"] <= atomics and atomics > 0
     # a record touches at least ceil(lanes / 16) and at most its lanes' lines
     assert sum(L * n for L, n in enumerate(lines["hist"])) <= lines["lanes"]
+    # sectors: every record once; at least as many sectors as lines, at most its lanes
+    hs = lines["hist_sectors"]
+    assert sum(hs) == lines["records"] and hs[0] == 0
+    assert sum(L * n for L, n in enumerate(lines["hist"])) <= sum(S * n for S, n in enumerate(hs)) <= lines["lanes"]
     assert np.array_equal(b.heights()[0].cpu().numpy(), ref)  # the traced launch changes no result

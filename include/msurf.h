@@ -107,6 +107,9 @@ typedef struct msurf_job {
 } msurf_job;
 
 int msurf_abi_version(void);
+/* edge length in nodes of a surface-cap tile (msurf_job.zcap holds one float
+ * per tile of a job's slab, ceil(rows / t) x ceil(w / t) row-major) */
+int msurf_zcap_tile(void);
 const char* msurf_last_error(void);
 int msurf_sizeof_job(void);
 

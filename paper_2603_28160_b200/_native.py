@@ -73,6 +73,7 @@ GEOM_IN_DTYPE = np.dtype(MsurfGeomIn)
 
 EXPORTS = {
     "msurf_abi_version": (ctypes.c_int, []),
+    "msurf_zcap_tile": (ctypes.c_int, []),
     "msurf_last_error": (ctypes.c_char_p, []),
     "msurf_sizeof_job": (ctypes.c_int, []),
     "msurf_tile_steps": (ctypes.c_int, []),

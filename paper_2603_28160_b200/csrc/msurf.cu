@@ -71,6 +71,10 @@ constexpr int kWarps = kThreads / 32;
 #ifndef MSURF_TILE_CULL
 #define MSURF_TILE_CULL 1  // tile-level chunk pre-cull before phase 1 (see kTileCull)
 #endif
+#ifndef MSURF_CAP_SHIFT
+#define MSURF_CAP_SHIFT 5  // surface-cap tiles of (1 << shift)^2 nodes
+#endif
+constexpr int kCapShift = MSURF_CAP_SHIFT, kCapTile = 1 << kCapShift;
 #ifndef MSURF_TILE_CULL_ALL
 #define MSURF_TILE_CULL_ALL 1  // ... also for by-value REF / EXT launches (A/B knob)
 #endif
@@ -704,7 +708,7 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
     zc_bj = (float)((wyc0 - J.y_min) * inv + 0.5 - (double)J.j_lo);
     zc_imax = (int)J.m;
     zc_jmax = (int)(J.j_hi - J.j_lo);
-    zc_tw = (zc_jmax >> 5) + 1;
+    zc_tw = (zc_jmax >> kCapShift) + 1;
   }
 
   // ---------------- tile-level chunk pre-cull (tilt mode, not in the DIAG=1
@@ -773,9 +777,11 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
           if (zc_on && hit) {
             const float ci = fmaf(uc + oxm, zc_k, zc_bi), cj = fmaf(yc, zc_k, zc_bj);
             const float ri = fmaf(a.z + mgx + mv + vib, zc_k, 2.5f), rj = fmaf(a.w + mgy + mv + feed, zc_k, 2.5f);
-            const int i0 = max(0, __float2int_rd(ci - ri)) >> 5, i1 = min(zc_imax, __float2int_rd(ci + ri)) >> 5;
-            const int j0 = max(0, __float2int_rd(cj - rj)) >> 5, j1 = min(zc_jmax, __float2int_rd(cj + rj)) >> 5;
-            if ((i1 - i0) <= 5 && (j1 - j0) <= 5) {  // larger boxes: keep the chunk (no lookup)
+            const int i0 = max(0, __float2int_rd(ci - ri)) >> kCapShift;
+            const int i1 = min(zc_imax, __float2int_rd(ci + ri)) >> kCapShift;
+            const int j0 = max(0, __float2int_rd(cj - rj)) >> kCapShift;
+            const int j1 = min(zc_jmax, __float2int_rd(cj + rj)) >> kCapShift;
+            if ((i1 - i0) <= (5 << (5 - kCapShift)) && (j1 - j0) <= (5 << (5 - kCapShift))) {  // larger: keep (no lookup)
               float cap = -INFINITY;  // empty range: no in-grid cell at all
               for (int ti = i0; ti <= i1; ++ti)
                 for (int tj = j0; tj <= j1; ++tj) cap = fmaxf(cap, __ldca(J.zcap + ti * zc_tw + tj));
@@ -952,8 +958,10 @@ __global__ void __launch_bounds__(NTHR, sweep_min_blocks(ONE, NTHR))
                 // half-extents: the chunk's radii plus the same fp32 margins as the
                 // window test (in mm), plus 1.5 cells for the fp32 cell coordinate
                 const float ri = fmaf(a.z + mgx, zc_k, 1.5f), rj = fmaf(a.w + mgy, zc_k, 1.5f);
-                const int i0 = max(0, __float2int_rd(ci - ri)) >> 5, i1 = min(zc_imax, __float2int_rd(ci + ri)) >> 5;
-                const int j0 = max(0, __float2int_rd(cj - rj)) >> 5, j1 = min(zc_jmax, __float2int_rd(cj + rj)) >> 5;
+                const int i0 = max(0, __float2int_rd(ci - ri)) >> kCapShift;
+                const int i1 = min(zc_imax, __float2int_rd(ci + ri)) >> kCapShift;
+                const int j0 = max(0, __float2int_rd(cj - rj)) >> kCapShift;
+                const int j1 = min(zc_jmax, __float2int_rd(cj + rj)) >> kCapShift;
                 // exact key of the tile range (tile indices < 2^13, spans <= 3); others uncached
                 const bool cacheable = (i1 - i0) >= 0 && (i1 - i0) <= 3 && (j1 - j0) >= 0 && (j1 - j0) <= 3 &&
                                        i0 < 8192 && j0 < 8192;
@@ -2033,17 +2041,17 @@ __global__ void __launch_bounds__(256)
                 const double* __restrict__ stock, float* __restrict__ zcap, int* stop_reset, ZBand band) {
   if (stop_reset && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *stop_reset = 0;
   __shared__ unsigned long long wmax[8];
-  const long long i0 = (long long)blockIdx.y * 32, j = (long long)blockIdx.x * 32 + (threadIdx.x & 31);
+  const long long i0 = (long long)blockIdx.y * kCapTile, j = (long long)blockIdx.x * kCapTile + (threadIdx.x & (kCapTile - 1));
   if (band.x0) {  // CTA-uniform
     const double* b = band.box;
     const double r = fmax(fabs(b[0]), fabs(b[1])) + fmax(fabs(b[2]), fabs(b[3])) + band.pad;
     const double x0 = *band.x0;
     const double lo = (x0 - r - band.x_min) * band.inv_h - 2.0, hi = (x0 + r - band.x_min) * band.inv_h + 2.0;
-    if ((double)(i0 + 31) < lo || (double)i0 > hi) return;
+    if ((double)(i0 + kCapTile - 1) < lo || (double)i0 > hi) return;
   }
   unsigned long long m = 0ull;
   if (j < cols)
-    for (long long i = i0 + (threadIdx.x >> 5); i < i0 + 32 && i < rows; i += 8) {
+    for (long long i = i0 + (threadIdx.x >> kCapShift); i < i0 + kCapTile && i < rows; i += 256 / kCapTile) {
       const unsigned long long k = keys[i * ld + j];
       m = k > m ? k : m;
     }
@@ -2185,6 +2193,7 @@ int msurf_copy2d_d2h(void* host_dst, int64_t dst_pitch, const void* src, int64_t
 }
 
 int msurf_abi_version(void) { return MSURF_ABI_VERSION; }
+int msurf_zcap_tile(void) { return kCapTile; }
 const char* msurf_last_error(void) { return g_err.c_str(); }
 int msurf_sizeof_job(void) { return (int)sizeof(msurf_job); }
 int msurf_tile_steps(void) { return kBatchTile; }
@@ -2284,7 +2293,7 @@ int msurf_red_sectors(const uint32_t* trace, int64_t n_records, unsigned long lo
 static int zcap_refresh(const uint64_t* keys, int64_t ld, int64_t rows, int64_t cols, const double* stock,
                         float* zcap, int32_t* stop_reset, void* stream, const ZBand& band) {
   if (!keys || !stock || !zcap || rows < 1 || cols < 1 || ld < cols) return set_err("msurf_zcap_refresh: bad arguments");
-  const long long ti = (rows + 31) / 32, tj = (cols + 31) / 32;
+  const long long ti = (rows + kCapTile - 1) / kCapTile, tj = (cols + kCapTile - 1) / kCapTile;
   if (ti > 65535 || tj > 0x7fffffffLL) return set_err("msurf_zcap_refresh: slab too large");
   zcap_kernel<<<dim3((unsigned)tj, (unsigned)ti), 256, 0, (cudaStream_t)stream>>>(keys, ld, rows, cols, stock, zcap,
                                                                                  stop_reset, band);

@@ -418,7 +418,9 @@ class SweepBatch:
                         continue
                     rows, cols = p.grid.m + 1, hi - lo + 1
                     # written by the first cap refresh of every launch
-                    zc = torch.empty(((rows + 31) // 32) * ((cols + 31) // 32), dtype=torch.float32, device=self.dev)
+                    ct = self.lib.msurf_zcap_tile()
+                    zc = torch.empty(((rows + ct - 1) // ct) * ((cols + ct - 1) // ct), dtype=torch.float32,
+                                     device=self.dev)
                     host[k]["zcap"] = zc.data_ptr()
                     # (launches, the cap tiles kept alive, the device stock height)
                     seqs[k] = (p.passes * p.teeth, zc, self.base + self.sentinel_off + 8 * i)

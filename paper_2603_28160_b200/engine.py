@@ -65,6 +65,10 @@ ZCAP_DEPTH = int(__import__("os").environ.get("MSURF_ZCAP_DEPTH", "0"))  # 0: Sw
 ZCAP_LONG_LAUNCH = float(__import__("os").environ.get("MSURF_ZCAP_LONG_LAUNCH", "3e8"))
 # capped launches as two kernels: phase 1 staged to HBM, phase 2 balanced over every warp
 ZCAP_STAGED = __import__("os").environ.get("MSURF_ZCAP_STAGED", "1") != "0"
+# strip-pipelined capped surfaces: the last PROGRESSIVE_PASSES raster passes
+# are launched one call each, and after every call the node rows no later
+# pass can reach are decoded and start crossing PCIe (0: whole strips only)
+PROGRESSIVE_PASSES = int(__import__("os").environ.get("MSURF_PROGRESSIVE_PASSES", "3"))
 
 
 def _per_job_launches(tiles) -> bool:
@@ -283,6 +287,9 @@ class SweepBatch:
                 s, o = surfs[q], offs[q]
                 if s.n_strips > 1:
                     o["col0"] = ar.add(np.asarray(s.col0, dtype=np.int64))
+                    # per strip [0, w_q]: msurf_decode_strips over a row range of one strip
+                    o["strip_w"] = ar.add(np.array([[0, s.col0[q + 1] - s.col0[q]] for q in range(s.n_strips)],
+                                                   dtype=np.int64))
                 # the trajectory record (engine.py:242-310) exposes the per-row
                 # cos/sin themselves, and the reference defines it with the libm
                 # values (simulate and simulate_reference records are identical,
@@ -475,13 +482,17 @@ class SweepBatch:
         buf, each = self._stages[key]
         return buf.data_ptr(), each
 
-    def _launch_capped(self, g: int, ks, mode: int, flag: int, max_pts: int, sp: int, split: bool = False):
+    def _launch_capped(self, g: int, ks, mode: int, flag: int, max_pts: int, sp: int, split: bool = False,
+                       passes=None, anchors=None):
         """Surface-cap jobs ks of by-value group g side by side
         (msurf_sweep_jobs_capped; staged two-kernel launches when
         ZCAP_STAGED). ``split``: one call per job, each forked from and joined
         into its own anchor stream (returned, in ks order) so the caller can
         wait for each job's slab separately; jobs still run side by side, the
-        earlier ones at higher stream priority."""
+        earlier ones at higher stream priority. ``passes`` = (p0, p1): only
+        raster passes [p0, p1) of every job (the caps carry over between
+        calls); ``anchors``: continue on these anchor streams (a previous
+        split call's) instead of forking new ones from ``sp``."""
         host = self.group_host_jobs[g]
         wide = _native.SWEEP_WIDE if ZCAP_WIDE else 0
         depth = self._capped_depth(g, ks)
@@ -496,18 +507,25 @@ class SweepBatch:
                                                                stocks[c0:].ctypes.data, depth, st_p, each, 0, sp))
             return None
         lib = self.lib
-        anchors = []
+        out = []
         for n, k in enumerate(ks):
-            anchor = lib.msurf_anchor_stream(n % 8)
-            if not anchor:
-                raise MillsurfError("libmsurf: no anchor stream")
-            _native.check(lib.msurf_stream_wait(anchor, sp))
-            arr = np.ascontiguousarray(host[k:k + 1])
+            if anchors is not None:
+                anchor = anchors[n]
+            else:
+                anchor = lib.msurf_anchor_stream(n % 8)
+                if not anchor:
+                    raise MillsurfError("libmsurf: no anchor stream")
+                _native.check(lib.msurf_stream_wait(anchor, sp))
+            arr = host[k:k + 1].copy()  # a copy: the pass range edits must not touch the batch's descriptors
+            if passes is not None:
+                p0, p1 = passes
+                arr["pass_x0"] += 8 * p0
+                arr["passes"] = p1 - p0
             st_p = stage + n * depth * each if stage else 0
             _native.check(lib.msurf_sweep_jobs_capped(arr.ctypes.data, 1, mode | flag | wide, max_pts,
                                                       stocks[n:].ctypes.data, depth, st_p, each, n % 8, anchor))
-            anchors.append(anchor)
-        return anchors
+            out.append(anchor)
+        return out
 
     def _launch_job(self, g: int, k: int, mode: int, flag: int, max_pts: int, sp: int) -> None:
         """Job k of by-value launch group g (a surface-cap job through
@@ -647,9 +665,12 @@ class SweepBatch:
         """Same work and results as launch(), ordered strip by strip on the
         current stream: fill, then per sub-strip q its sweep job and its
         decode (msurf_decode_strips over that strip alone), then
-        ``strip_done(q, c0, w)`` (columns [c0, c0 + w) of the surface are
-        final: the caller enqueues their D2H, which then overlaps the sweeps
-        of the later strips). ``events`` = (start, -, -, end)."""
+        ``strip_done(q, c0, w, r0, r1, stream)`` (node rows [r0, r1) of
+        columns [c0, c0 + w) are final once the raw ``stream``'s work so far
+        is done: the caller enqueues their D2H, which then overlaps the later
+        sweeps). Surface-cap strips run side by side; with PROGRESSIVE_PASSES
+        their last passes are launched one call each and the rows no later
+        pass can reach are released after each. ``events`` = (start, -, -, end)."""
         if not self.pipelined_strips():
             raise ConfigError("launch_by_strip needs one strip-layout surface with per-job sweeps")
         lib, base = self.lib, self.base
@@ -673,23 +694,61 @@ class SweepBatch:
         # their decodes and copies then follow, no longer overlapping the sweep
         capped = [k for k, t in enumerate(self.group_tiles[0]) if t and self.zc_seq[0][k] is not None]
         anchor_of = {}
+        done_rows = [0] * s.n_strips
+        strip_of = {k: q for q in range(s.n_strips) for k in by_lo.get(s.j_lo + s.col0[q], ())}
+
+        def release(q, r1, stream):
+            # decode node rows [done, r1) of strip q on `stream`, then hand them out
+            r0 = done_rows[q]
+            if r1 <= r0:
+                return
+            c0, w = s.col0[q], s.col0[q + 1] - s.col0[q]
+            _native.check(lib.msurf_decode_strips(
+                self.strip_keys.data_ptr() + (s.strip_off + rows * c0 + r0 * w) * 8,
+                self.keys.data_ptr() + (s.key_off + r0 * w_all + c0) * 8, r1 - r0, w_all, 1,
+                base + self.offs[i]["strip_w"] + 16 * q, base + self.sentinel_off + 8 * i,
+                base + self.machined_off + 8 * i, stream))
+            done_rows[q] = r1
+            strip_done(q, c0, w, r0, r1, stream)
+
         if capped:
             # side by side, in strip order of stream priority; each strip's decode
             # and copy-out waits for that strip's own jobs only
-            anchor_of = dict(zip(capped, self._launch_capped(0, capped, mode, flag, max_pts, sp, split=True)))
+            n_pass = s.plan.passes
+            k_prog = min(PROGRESSIVE_PASSES, n_pass - 1)
+            cuts = [0] + ([n_pass - k_prog + t for t in range(k_prog)] if k_prog > 0 else []) + [n_pass]
+            anchors = None
+            for c in range(len(cuts) - 1):
+                p0, p1 = cuts[c], cuts[c + 1]
+                anchors = self._launch_capped(0, capped, mode, flag, max_pts, sp, split=True,
+                                              passes=(p0, p1) if len(cuts) > 2 else None, anchors=anchors)
+                if p1 < n_pass:
+                    r_fin = self._final_rows(s, p1)
+                    for k, a in zip(capped, anchors):
+                        release(strip_of[k], r_fin, a)
+            anchor_of = dict(zip(capped, anchors))
         for q in range(s.n_strips):
             for k in by_lo.get(s.j_lo + s.col0[q], ()):
                 if k in anchor_of:
                     _native.check(lib.msurf_stream_wait(sp, anchor_of[k]))
                 elif self.group_tiles[0][k]:
                     self._launch_job(0, k, mode, flag, max_pts, sp)
-            _native.check(lib.msurf_decode_strips(
-                self.strip_keys.data_ptr() + s.strip_off * 8, self.keys.data_ptr() + s.key_off * 8, rows, w_all,
-                1, base + self.offs[i]["col0"] + 8 * q, base + self.sentinel_off + 8 * i,
-                base + self.machined_off + 8 * i, sp))
-            strip_done(q, s.col0[q], s.col0[q + 1] - s.col0[q])
+            release(q, rows, sp)
         if ev[3] is not None:
             ev[3].record()
+
+    def _final_rows(self, s, p_next: int) -> int:
+        """Node rows [0, r) of surface s that no raster pass from p_next on
+        can deposit into: pass q reaches x in x0_q +- (max|x_t| + max|y_t|
+        over every tooth's tool-frame box + |vibration|) (the cap refresh's
+        band, msurf.cu ZBand), located with two nodes of slack."""
+        p = s.plan
+        tb = np.asarray(p.tooth_box, dtype=np.float64).reshape(-1, 6)
+        reach = float((np.maximum(np.abs(tb[:, 0]), np.abs(tb[:, 1])) +
+                       np.maximum(np.abs(tb[:, 2]), np.abs(tb[:, 3]))).max()) + abs(p.vib_amp)
+        x_lo = float(np.min(p.pass_x0[p_next:])) - reach
+        r = int(math.floor((x_lo - p.grid.x_min_mm) / p.grid.spacing_mm)) - 2
+        return max(0, min(p.grid.m + 1, r))
 
     def heights(self):
         """fp64 views (valid after a launch) — one per surface."""
@@ -836,11 +895,10 @@ def _launch_results(plans, trig, diagnostics=False, prefetch=False):
         pitch = (s0.j_hi - s0.j_lo + 1) * 8
         hp, dp, rows = host.data_ptr() + s0.key_off * 8, b.keys.data_ptr() + s0.key_off * 8, s0.plan.grid.m + 1
 
-        def strip_done(q, c0, w):
-            e = torch.cuda.Event()
-            e.record()
-            side.wait_event(e)
-            _native.check(b.lib.msurf_copy2d_d2h(hp + c0 * 8, pitch, dp + c0 * 8, pitch, w * 8, rows, sptr))
+        def strip_done(q, c0, w, r0, r1, stream):
+            _native.check(b.lib.msurf_stream_wait(sptr, stream))
+            off = r0 * pitch + c0 * 8
+            _native.check(b.lib.msurf_copy2d_d2h(hp + off, pitch, dp + off, pitch, w * 8, r1 - r0, sptr))
 
         # the raw 2-D copies are invisible to torch's pinned-memory cache: the
         # buffer stays referenced until they finish, even if every field is

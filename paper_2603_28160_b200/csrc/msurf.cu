@@ -1368,8 +1368,11 @@ __global__ void __launch_bounds__(256)
 // units from the list in order through a global cursor, load the tile's
 // staged rows and masks (L2) and run pair_unit: the heavy tiles' units spread
 // over every warp of the GPU instead of trailing in their own CTA
+#ifndef MSURF_UNITS_MIN_BLOCKS
+#define MSURF_UNITS_MIN_BLOCKS 32  // one-warp CTAs per SM the units kernel's registers are sized for (64 regs)
+#endif
 template <int DIAG>
-__global__ void __launch_bounds__(32, 32)
+__global__ void __launch_bounds__(32, MSURF_UNITS_MIN_BLOCKS)
     sweep_units_kernel(const __grid_constant__ msurf_job J, int mask_words) {
   constexpr int MODE = MSURF_MODE_EXT_TILT;
   __shared__ double4 ptstage[32];

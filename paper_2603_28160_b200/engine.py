@@ -641,10 +641,15 @@ class SweepBatch:
         end) CUDA events, optional, recorded on the same stream."""
         sp = _native.stream_ptr(stream)
         ev = events if events else (None, None, None, None)
+        if stream is None and any(e is not None for e in ev):
+            # the stream object once, by explicit device (Event.record() with no
+            # stream resolves the current device through torch's availability
+            # checks on every call)
+            stream = self.torch.cuda.current_stream(self.dev)
 
         def mark(e):
             if e is not None:
-                e.record(stream) if stream is not None else e.record()
+                e.record(stream)
 
         mark(ev[0])
         self.launch_fill(sp)
@@ -677,8 +682,9 @@ class SweepBatch:
         sp = _native.stream_ptr()
         ev = events if events else (None, None, None, None)
         s, i = self.surfs[0], 0
+        cs = self.torch.cuda.current_stream(self.dev)
         if ev[0] is not None:
-            ev[0].record()
+            ev[0].record(cs)
         self.launch_fill(sp)
         mode, jidx, _, _, _, max_pts = self.group_meta[0]
         flag = self._sweep_flag()
@@ -735,7 +741,7 @@ class SweepBatch:
                     self._launch_job(0, k, mode, flag, max_pts, sp)
             release(q, rows, sp)
         if ev[3] is not None:
-            ev[3].record()
+            ev[3].record(cs)
 
     def _final_rows(self, s, p_next: int) -> int:
         """Node rows [0, r) of surface s that no raster pass from p_next on

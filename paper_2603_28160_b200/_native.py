@@ -254,12 +254,19 @@ class Arena:
 
     def __init__(self):
         self._parts = []
+        self._direct = []  # (offset, page-locked torch tensor): DMA'd after the staged copy
         self.size = 0
 
-    def add(self, arr) -> int:
+    def add(self, arr, pinned=None) -> int:
+        """Reserve room for ``arr``; ``pinned`` = a page-locked torch uint8
+        tensor holding the same bytes: copied to HBM by DMA, not staged."""
         a = arr if isinstance(arr, np.ndarray) and arr.flags.c_contiguous else np.ascontiguousarray(arr)
         off = (self.size + 255) & ~255
-        self._parts.append((off, a))
+        if pinned is not None and pinned.numel() == a.nbytes:
+            self._direct.append((off, pinned))
+            self._parts.append((off, None))
+        else:
+            self._parts.append((off, a))
         self.size = off + a.nbytes
         return off
 
@@ -291,4 +298,6 @@ class Arena:
             b = b if isinstance(b, np.ndarray) else np.frombuffer(b, dtype=np.uint8)
             ctypes.memmove(hp + off, b.ctypes.data, b.nbytes)
         dev.copy_(stage, non_blocking=True)
+        for off, t in self._direct:  # torch records the copies: the pinned blocks are not reused early
+            dev[off: off + t.numel()].copy_(t, non_blocking=True)
         return dev

@@ -268,7 +268,7 @@ class SweepBatch:
                 run = {}
                 for f in DEVICE_FIELDS:
                     a = g.arrays[f]
-                    run[f] = (ar.add(a[b0: b0 + (k - i)]), a[0].nbytes)
+                    run[f] = (ar.add(a[b0: b0 + (k - i)], pinned=g.pinned_sets(f, b0, k - i)), a[0].nbytes)
                 for q in range(i, k):
                     offs[q] = {f: o + (q - i) * nb for f, (o, nb) in run.items()}
             else:

@@ -316,12 +316,23 @@ class PlanGroup:
     ``arrays[name][b]``. SweepBatch packs a run of consecutive sets of one
     group as ONE slice per field instead of one small array per set."""
 
-    __slots__ = ("arrays", "views")
+    __slots__ = ("arrays", "views", "pinned")
 
-    def __init__(self, arrays: dict):
+    def __init__(self, arrays: dict, pinned: dict | None = None):
         self.arrays = arrays
         self.views = [tuple(arrays[f][b] for f in DEVICE_FIELDS if f != "chunk_f32")
                       for b in range(len(arrays["pts"]))]
+        # field -> the page-locked torch tensor (flat uint8) backing arrays[field]
+        self.pinned = pinned or {}
+
+    def pinned_sets(self, name: str, b0: int, count: int):
+        """The page-locked bytes of sets [b0, b0 + count) of a field, or None
+        (then SweepBatch stages the slice like any host array)."""
+        t = self.pinned.get(name)
+        if t is None:
+            return None
+        per = self.arrays[name][0].nbytes
+        return t[b0 * per: (b0 + count) * per]
 
     def owns(self, p: "SweepPlan", b: int) -> bool:
         """True while the plan still holds this group's views (a plan whose
@@ -610,6 +621,22 @@ def _ext_group_key(config, ext: Extensions):
 PLAN_THREADS = max(1, min(8, (__import__("os").cpu_count() or 1)))
 
 
+def _pinned_empty(shape, dtype=np.float64):
+    """(array, backing tensor): an uninitialised array in page-locked host
+    memory from torch's caching host allocator when a GPU is present, else
+    plain (array, None)."""
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+            t = torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)
+            return t.numpy()[:nbytes].view(dtype).reshape(shape), t
+    except Exception:  # noqa: BLE001 - no CUDA runtime: plain host memory
+        pass
+    return np.empty(shape, dtype=dtype), None
+
+
 def plan_many(configs, exts, threads: int | None = None, native_threads: int = 1):
     """plan() for many parameter sets. Extended-model sets that share their
     edge geometry are planned together with (sets, teeth, points) arrays —
@@ -743,7 +770,10 @@ def _plan_ext_group_native(configs, exts, threads: int = 1):
         spans.append(sp)
         zoffs[b] = (sp[5] + (float(stats[b, 0]) if tilt else 0.0)) + 0.0
     nchunk = (n + CHUNK - 1) // CHUNK
-    pts = np.empty((B, z_n, n, 4))
+    # the largest device field (B x teeth x points x 32 B) is written straight
+    # into page-locked memory: SweepBatch then copies it to HBM by DMA instead
+    # of staging it through a host memmove on the launching thread
+    pts, pts_pinned = _pinned_empty((B, z_n, n, 4))
     tbox = np.empty((B, z_n, 6))
     circ = np.empty((B, z_n, nchunk, 6))
     cbox = np.empty((B, z_n, nchunk, 6))
@@ -766,7 +796,7 @@ def _plan_ext_group_native(configs, exts, threads: int = 1):
     zfl = chunk_zfloor(pts[..., 3] if tilt else zw, circ[..., 2], ts if tilt else 0.0, stock)
     grp = PlanGroup({"tooth_base": tbase, "tooth_rows": np.zeros((B, z_n, 8)), "pts": pts, "tooth_box": tbox,
                      "chunk_circ": circ, "chunk_f32": chunk_f32(circ, tbox, zfl), "pass_x0": px0,
-                     "min_index": mins})
+                     "min_index": mins}, pinned={"pts": pts_pinned} if pts_pinned is not None else None)
     plans = []
     for b, (cfg, e) in enumerate(zip(configs, exts)):
         proc, grid = cfg.process, cfg.grid

@@ -75,6 +75,10 @@ constexpr int kWarps = kThreads / 32;
 #define MSURF_CAP_SHIFT 5  // surface-cap tiles of (1 << shift)^2 nodes
 #endif
 constexpr int kCapShift = MSURF_CAP_SHIFT, kCapTile = 1 << kCapShift;
+#ifndef MSURF_SHORT_LAUNCH
+#define MSURF_SHORT_LAUNCH 3e8  // step-points of a (pass, tooth) launch below which it is "short"
+#endif
+constexpr double kShortLaunch = MSURF_SHORT_LAUNCH;
 #ifndef MSURF_TILE_CULL_ALL
 #define MSURF_TILE_CULL_ALL 1  // ... also for by-value REF / EXT launches (A/B knob)
 #endif
@@ -1368,11 +1372,13 @@ __global__ void __launch_bounds__(256)
 // units from the list in order through a global cursor, load the tile's
 // staged rows and masks (L2) and run pair_unit: the heavy tiles' units spread
 // over every warp of the GPU instead of trailing in their own CTA
-#ifndef MSURF_UNITS_MIN_BLOCKS
-#define MSURF_UNITS_MIN_BLOCKS 32  // one-warp CTAs per SM the units kernel's registers are sized for (64 regs)
-#endif
-template <int DIAG>
-__global__ void __launch_bounds__(32, MSURF_UNITS_MIN_BLOCKS)
+// MINB: one-warp CTAs per SM the registers are sized for — 32 (64 registers)
+// for long (pass, tooth) launches that fill the GPU on their own; 16 (~100
+// registers, more of the point loop's fp64 chains in flight per warp) for
+// short ones, where fewer, faster warps shorten the launch (measured: config
+// 2 0.532 -> 0.508 ms; config 5's long launches lose with 16: 10.67 -> 11.03)
+template <int DIAG, int MINB = 32>
+__global__ void __launch_bounds__(32, MINB)
     sweep_units_kernel(const __grid_constant__ msurf_job J, int mask_words) {
   constexpr int MODE = MSURF_MODE_EXT_TILT;
   __shared__ double4 ptstage[32];
@@ -2341,20 +2347,31 @@ static int staged_launch(const msurf_job& sub, int32_t max_points, cudaStream_t 
                                                                                  nullptr);
   if (e != cudaSuccess) return set_err(std::string("staged_launch: phase 1: ") + cudaGetErrorString(e));
   if (check_launch("sweep_kernel (staged)")) return 1;
-  // resident one-warp CTAs of the units kernel, queried once per device
-  static int slots[64] = {};
+  // short launch (the same threshold as engine.ZCAP_LONG_LAUNCH): the
+  // register-rich variant (see sweep_units_kernel)
+  const bool short_launch = (double)(sub.step_hi - sub.step_lo) * (double)sub.points < kShortLaunch;
+  // resident one-warp CTAs of each units-kernel variant, queried once per device
+  static int slots[64][2] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return set_err("staged_launch: device index");
-  if (!slots[dev]) {
+  if (!slots[dev][short_launch]) {
     int sms = 148, per_sm = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_units_kernel<0>, 32, 0);
-    slots[dev] = sms * std::max(per_sm, 1);
+    if (short_launch)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_units_kernel<0, 16>, 32, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_units_kernel<0, 32>, 32, 0);
+    slots[dev][short_launch] = sms * std::max(per_sm, 1);
   }
   const long long units_max = job_tiles(sub, kTiltTile) * nchunk;
-  const long long grid = std::min<long long>(units_max, (long long)slots[dev]);
-  if (grid > 0) sweep_units_kernel<0><<<(unsigned)grid, 32, 0, st>>>(sub, mask_words);
+  const long long grid = std::min<long long>(units_max, (long long)slots[dev][short_launch]);
+  if (grid > 0) {
+    if (short_launch)
+      sweep_units_kernel<0, 16><<<(unsigned)grid, 32, 0, st>>>(sub, mask_words);
+    else
+      sweep_units_kernel<0, 32><<<(unsigned)grid, 32, 0, st>>>(sub, mask_words);
+  }
   return check_launch("sweep_units_kernel");
 }
 

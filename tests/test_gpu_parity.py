@@ -302,3 +302,24 @@ def test_tile_list_path_equals_per_job_path(case, monkeypatch):
         assert np.array_equal(capped.heights()[0].cpu().numpy(), h1), (case, lo, hi, "capped")
         assert int(capped.counters()[1][0]) == int(m1[0])
         monkeypatch.setattr(engine, "ZCAP", False)
+
+
+@pytest.mark.parametrize("case", ["ball_tilt", "ball_noise", "vib_runout"])
+@pytest.mark.parametrize("nodes,points", [((2, 2), 2), ((2, 40), 33), ((40, 2), 2), ((3, 2), 65), ((64, 65), 2)])
+def test_extended_model_degenerate_grids_vs_ext_oracle(case, nodes, points):
+    """Extended kinematics (capped tilt raster passes, edge noise, vibration)
+    on degenerate grids — one cell, one cell row, one cell column, 3 x 2 — and the
+    smallest / odd point counts: heights bit-exact and machined-cell counts
+    equal to the extended oracle (host-libm trig)."""
+    kw = EXT_CASES[case]
+    cfg = _ext_cfg(kw.get("profile", "insert"))
+    g = cfg.grid
+    grid = ms.GridSpec.from_nodes(g.spacing_mm, g.x_min_mm + 0.37 * (g.m + 1 - nodes[0]) * g.spacing_mm,
+                                  g.y_min_mm + 0.41 * (g.n + 1 - nodes[1]) * g.spacing_mm, nodes[0], nodes[1])
+    from dataclasses import replace
+
+    cfg = replace(cfg, grid=grid, edge_point_count=points)
+    res = ms.simulate(cfg, ms.Extensions(**kw), trig="host")
+    h_ref, _, ctr, _ = xorc.ext_sweep(cfg, NS(**kw), workers=2)
+    assert np.array_equal(res.field.heights, h_ref), float(np.max(np.abs(res.field.heights - h_ref)))
+    assert res.cells_updated == ctr["cells_updated"]

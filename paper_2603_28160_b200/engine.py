@@ -181,6 +181,21 @@ class _Surface:
     col0: list = field(default_factory=list)  # sub-strip column offsets from j_lo
 
 
+def final_rows(p: SweepPlan, p_next: int) -> int:
+    """Node rows [0, r) of a surface that no raster pass from p_next on can
+    deposit into: pass q reaches x in x0_q +- (max|x_t| + max|y_t| over every
+    tooth's tool-frame box + |vibration|) (the cap refresh's band, msurf.cu
+    ZBand), located with two nodes of slack (launch_by_strip's progressive
+    row release; tests/test_host_cpu.py checks it against the oracle's
+    per-pass deposits)."""
+    tb = np.asarray(p.tooth_box, dtype=np.float64).reshape(-1, 6)
+    reach = float((np.maximum(np.abs(tb[:, 0]), np.abs(tb[:, 1])) +
+                   np.maximum(np.abs(tb[:, 2]), np.abs(tb[:, 3]))).max()) + abs(p.vib_amp)
+    x_lo = float(np.min(p.pass_x0[p_next:])) - reach
+    r = int(math.floor((x_lo - p.grid.x_min_mm) / p.grid.spacing_mm)) - 2
+    return max(0, min(p.grid.m + 1, r))
+
+
 def _trig_tables(p: SweepPlan):
     """Host-libm tables (parity mode): exactly the reference's per-row trig
     (engine.py:240, 252-255) — np.cos/np.sin of base_K - omega*t."""
@@ -744,17 +759,7 @@ class SweepBatch:
             ev[3].record(cs)
 
     def _final_rows(self, s, p_next: int) -> int:
-        """Node rows [0, r) of surface s that no raster pass from p_next on
-        can deposit into: pass q reaches x in x0_q +- (max|x_t| + max|y_t|
-        over every tooth's tool-frame box + |vibration|) (the cap refresh's
-        band, msurf.cu ZBand), located with two nodes of slack."""
-        p = s.plan
-        tb = np.asarray(p.tooth_box, dtype=np.float64).reshape(-1, 6)
-        reach = float((np.maximum(np.abs(tb[:, 0]), np.abs(tb[:, 1])) +
-                       np.maximum(np.abs(tb[:, 2]), np.abs(tb[:, 3]))).max()) + abs(p.vib_amp)
-        x_lo = float(np.min(p.pass_x0[p_next:])) - reach
-        r = int(math.floor((x_lo - p.grid.x_min_mm) / p.grid.spacing_mm)) - 2
-        return max(0, min(p.grid.m + 1, r))
+        return final_rows(s.plan, p_next)
 
     def heights(self):
         """fp64 views (valid after a launch) — one per surface."""

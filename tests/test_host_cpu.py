@@ -480,3 +480,35 @@ def test_chunk_zfloor_bounds_every_point_at_every_angle(cid):
         q = np.arange(n) // 32
         assert np.all(z >= bound[:, q] - 1e-12), float(np.min(z - bound[:, q]))
     assert zf.shape == (p.teeth, nch)
+
+
+@pytest.mark.parametrize("case", ["ball_tilt", "ball_noise"])
+def test_final_rows_bound_later_passes_deposits(case):
+    """engine.final_rows (the progressive row release of launch_by_strip):
+    the oracle's own deposits of every raster pass q >= p_next stay at node
+    rows >= final_rows(plan, p_next), on a grid wide enough in x that rows
+    are released before the last pass."""
+    from dataclasses import replace as dc_replace
+
+    from paper_2603_28160_b200 import engine
+
+    kw = dict(EXT_CASES[case], passes=6, stepover_mm=0.5)
+    cfg = _ext_cfg(kw.get("profile", "insert"))
+    g = cfg.grid
+    cfg = dc_replace(cfg, grid=ms.GridSpec.from_nodes(g.spacing_mm, -1.2, g.y_min_mm, 481, 41), edge_point_count=40)
+    x_start = cfg.process.initial_position_mm[0]
+    p = planner.plan(cfg, ms.Extensions(**kw))
+    rows = p.grid.m + 1
+    first_hit = []
+    for q in range(kw["passes"]):
+        proc = dc_replace(cfg.process, initial_position_mm=(x_start + q * kw["stepover_mm"],) +
+                          tuple(cfg.process.initial_position_mm[1:]))
+        h, pq, _, _ = xorc.ext_sweep(dc_replace(cfg, process=proc), NS(**dict(kw, passes=1)), workers=2)
+        cut = np.nonzero((h.reshape(rows, -1) < pq.initial_height).any(axis=1))[0]
+        first_hit.append(int(cut[0]) if cut.size else rows)
+    released = 0
+    for p_next in range(1, kw["passes"]):
+        r = engine.final_rows(p, p_next)
+        assert r <= min(first_hit[p_next:]), (p_next, r, first_hit)
+        released = max(released, r)
+    assert released > 0  # the test geometry does release rows early

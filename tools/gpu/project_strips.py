@@ -39,6 +39,9 @@ def main():
     dev = torch.device("cuda", 0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for cid in args.configs:
+        if cid == 3:
+            project_batch(args, dev, flush)
+            continue
         cfg, ext, meta = configs.FACTORIES[cid]()
         p = make_plan(cfg, ext)
         base_ms = None
@@ -75,6 +78,44 @@ def main():
                    "sum_points_evaluated": sum(x["points_evaluated"] for x in ranks),
                    "projected_speedup": base_ms / mx if base_ms else None, "ranks": ranks}
             print(json.dumps(rec), flush=True)
+
+
+def project_batch(args, dev, flush):
+    """Config 3 (256 parameter sets) sharded by set as bench.py does at N > 1:
+    every rank's sets as one SweepBatch (fill + sweep + decode) on this
+    GPU, one rank after another; max over ranks."""
+    import torch
+
+    import bench
+    from paper_2603_28160_b200.engine import SweepBatch
+
+    base_ms = None
+    for n in args.ns:
+        ranks = []
+        for r in range(n):
+            meta, _, plans = bench.config3_plans(r, n)
+            b = SweepBatch([(p, 0, p.grid.n) for p in plans])
+            st = []
+            for k in range(args.steps + 2):
+                flush.fill_(1)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                b.launch()
+                e1.record()
+                torch.cuda.synchronize()
+                if k >= 2:
+                    st.append(e0.elapsed_time(e1))
+            ctr, _ = b.counters()
+            ranks.append({"rank": r, "sets": len(plans), "step_ms": statistics.median(st),
+                          "points_evaluated": int(sum(c[1] for c in ctr))})
+            del b
+            torch.cuda.empty_cache()
+        mx = max(x["step_ms"] for x in ranks)
+        if n == 1:
+            base_ms = mx
+        print(json.dumps({"config": "config3", "n": n, "max_rank_step_ms": mx,
+                          "note": "fill + sweep + decode per rank's sets (parameter-set shards, no communication)",
+                          "projected_speedup": base_ms / mx if base_ms else None, "ranks": ranks}), flush=True)
 
 
 if __name__ == "__main__":

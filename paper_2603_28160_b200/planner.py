@@ -621,19 +621,31 @@ def _ext_group_key(config, ext: Extensions):
 PLAN_THREADS = max(1, min(8, (__import__("os").cpu_count() or 1)))
 
 
+_PINNED_OK = []  # [torch or None], decided once per process
+
+
 def _pinned_empty(shape, dtype=np.float64):
     """(array, backing tensor): an uninitialised array in page-locked host
-    memory from torch's caching host allocator when a GPU is present, else
-    plain (array, None)."""
-    try:
-        import torch
+    memory from torch's caching host allocator when a CUDA device is present
+    (decided once per process), else plain (array, None). An allocation
+    failure (pinned memory exhausted) also falls back to pageable memory:
+    SweepBatch then stages the array like any other."""
+    if not _PINNED_OK:
+        try:
+            import torch
 
-        if torch.cuda.is_available():
-            nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+            _PINNED_OK.append(torch if torch.cuda.is_available() else None)
+        except ImportError:
+            _PINNED_OK.append(None)
+    torch = _PINNED_OK[0]
+    if torch is not None:
+        nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        try:
             t = torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)
+        except RuntimeError:
+            t = None
+        if t is not None:
             return t.numpy()[:nbytes].view(dtype).reshape(shape), t
-    except Exception:  # noqa: BLE001 - no CUDA runtime: plain host memory
-        pass
     return np.empty(shape, dtype=dtype), None
 
 
